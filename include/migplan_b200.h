@@ -1,0 +1,245 @@
+/*
+ * migplan_b200.h — the C-ABI boundary of the B200-native MIG-SERVING optimizer.
+ *
+ * The reference (the headers under /root/reference/proj/include/migplan, header-only C++20) has
+ * no FFI of its own; its public surface is C++ free functions and the
+ * `OptimizerProcedure` plugin class.  Every entry point below is the plain-C
+ * rendering of one of those functions (cited per declaration), with
+ *   - plain pointers and sizes, no C++ or torch types,
+ *   - C++ exceptions mapped onto status codes (util.hpp:12-25, migplan.cpp:414-426),
+ *   - service indices instead of service-id strings (index i == services[i],
+ *     services sorted by id exactly as `validate_services` leaves them,
+ *     core.hpp:151-171).
+ *
+ * Three libraries implement this header:
+ *   libmigplan_b200.so  — the product (CUDA sm_100a kernels + native runtime),
+ *   oracle/liboracle.so — CPU restatement used only by tests/bench as checker,
+ *   oracle/_ref/libmigref.so — the unmodified reference headers behind a shim.
+ */
+#ifndef MIGPLAN_B200_H
+#define MIGPLAN_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes (util.hpp:12-25; CLI exit codes migplan.cpp:414-426) ---- */
+#define MIG_OK 0
+#define MIG_ERR_PLANNING 1 /* migplan::PlanningError  */
+#define MIG_ERR_SCHEMA 2   /* migplan::SchemaError    */
+#define MIG_ERR_DEVICE 3   /* CUDA / NCCL failure     */
+#define MIG_ERR_ARGUMENT 4 /* null pointer, too-small output capacity, limits */
+
+#define MIG_MAX_INSTANCES 7 /* a GPU has 7 compute slots (core.hpp:126)        */
+#define MIG_MAX_RULE_SIZES 8
+#define MIG_MAX_RULE_SLOTS 16
+#define MIG_MAX_EXCLUSIONS 16
+
+/* Thread-local message of the last failing call (the exception's what()). */
+const char* mig_last_error(void);
+int32_t mig_abi_version(void);
+/* "product" / "oracle" / "reference": which implementation this library is. */
+const char* mig_impl_name(void);
+
+/* ---- L1/L2 domain types (core.hpp:57-78,113-118,174-200; mig_rules.hpp:15-34) ---- */
+
+typedef struct mig_profile_entry { /* ProfileEntry, core.hpp:57-61 (+ its size key) */
+    int32_t size;
+    int32_t batch;
+    double throughput_rps;
+    double p90_ms;
+} mig_profile_entry;
+
+typedef struct mig_model_profile { /* ModelProfile, core.hpp:64-76 */
+    const char* model_name;
+    const mig_profile_entry* entries; /* any order; grouped by size, sorted by batch inside */
+    int32_t n_entries;
+} mig_model_profile;
+
+typedef struct mig_service { /* ServiceSpec, core.hpp:113-118 */
+    const char* service_id;
+    const char* model_name;
+    double required_rps;
+    double max_p90_ms;
+} mig_service;
+
+typedef struct mig_rules { /* PartitionRuleSet, mig_rules.hpp:15-34 */
+    int32_t n_sizes;                                    /* slot_positions entries   */
+    int32_t size[MIG_MAX_RULE_SIZES];
+    int32_t n_slots[MIG_MAX_RULE_SIZES];
+    int32_t slots[MIG_MAX_RULE_SIZES][MIG_MAX_RULE_SLOTS];
+    int32_t n_weights;                                  /* memory_weight entries    */
+    int32_t weight_size[MIG_MAX_RULE_SIZES];
+    int32_t weight[MIG_MAX_RULE_SIZES];
+    int32_t n_exclusions;                               /* hard_exclusions pairs    */
+    int32_t exclusion[MIG_MAX_EXCLUSIONS][2];
+    int32_t memory_budget;
+} mig_rules;
+
+typedef struct mig_instance { /* AssignedInstance, core.hpp:174-180 */
+    int32_t slices;
+    int32_t slot;
+    int32_t service; /* index into the context's services */
+    int32_t batch;
+} mig_instance;
+
+typedef struct mig_config { /* GpuConfig (normalized: sorted by (slices, slot)), core.hpp:184-200 */
+    int32_t n_instances;
+    mig_instance inst[MIG_MAX_INSTANCES];
+} mig_config;
+
+typedef struct mig_candidate { /* Candidate, config_enum.hpp:13-18 */
+    mig_config config;
+    int32_t nnz;                          /* util entries, ascending service index */
+    int32_t util_idx[MIG_MAX_INSTANCES];
+    double util_val[MIG_MAX_INSTANCES];
+    double util_sum;
+} mig_candidate;
+
+typedef struct mig_partition { /* LegalPartition, mig_rules.hpp:62-65 */
+    int32_t n;
+    int32_t slices[MIG_MAX_INSTANCES];
+    int32_t slot[MIG_MAX_INSTANCES];
+} mig_partition;
+
+void mig_rules_defaults(mig_rules* out); /* PartitionRuleSet::defaults, mig_rules.hpp:21-33 */
+
+/* is_legal_partition, mig_rules.hpp:38-59 */
+int mig_is_legal_partition(const mig_rules* rules, const int32_t* slices, const int32_t* slots, int32_t n,
+                           int32_t* legal);
+/* enumerate_maximal_partitions, mig_rules.hpp:116-135 (18 under defaults) */
+int mig_enumerate_maximal_partitions(const mig_rules* rules, mig_partition* out, int32_t cap, int32_t* n_out);
+
+/* validate_services, core.hpp:151-171: writes the id-sorted order into perm[n]
+ * (perm[i] = caller index of the i-th service) and throws the reference's errors. */
+int mig_validate_services(const mig_model_profile* models, int32_t n_models, const mig_service* services,
+                          int32_t n_services, int32_t* perm);
+
+/* ---- PlanContext (greedy.hpp:16-31) ---- */
+typedef struct mig_ctx mig_ctx;
+
+/* make_plan_context(services, profiles, rules, max_mix), greedy.hpp:23-31.
+ * `services` must already be sorted by id (as validate_services leaves them).
+ * `device` selects the CUDA device (product only; ignored by CPU libraries). */
+int mig_ctx_create(const mig_rules* rules, const mig_model_profile* models, int32_t n_models,
+                   const mig_service* services, int32_t n_services, int32_t max_mix, int32_t device,
+                   mig_ctx** out);
+void mig_ctx_destroy(mig_ctx* ctx);
+int32_t mig_ctx_n_services(const mig_ctx* ctx);
+
+/* CandidatePool view (config_enum.hpp:20-32).  Pool order is implementation
+ * defined; every optimizer result is a function of the pool as a SET because
+ * the preference order (greedy.hpp:63-67) is total. */
+int mig_pool_size(const mig_ctx* ctx, int64_t* out);
+int mig_pool_candidate(const mig_ctx* ctx, int64_t idx, mig_candidate* out);
+int mig_pool_best_single_util(const mig_ctx* ctx, double* out /* n_services */);
+
+/* score(const Candidate&, const CompletionRates&), greedy.hpp:36-43 */
+int mig_score(const mig_ctx* ctx, int64_t idx, const double* comp, int32_t n, double* out);
+
+/* detail::topk_candidates, mcts.hpp:56-76.  from == NULL (n_from < 0): whole base pool. */
+int mig_topk_candidates(mig_ctx* ctx, const double* comp, int32_t n, int32_t k, const int64_t* from,
+                        int64_t n_from, int64_t* out_idx, int32_t* n_out);
+
+/* ---- fast algorithm (greedy.hpp:95-145) ----
+ * trace(iter, chosen, best_score, comp-after-pick) exactly as greedy.hpp:140.
+ * *n_out is always the plan length; MIG_ERR_ARGUMENT when it exceeds cap. */
+typedef void (*mig_greedy_trace_fn)(void* user, int32_t iter, const mig_candidate* chosen, double score,
+                                    const double* comp, int32_t n);
+int mig_fast_algo(mig_ctx* ctx, const double* comp, int32_t n, mig_config* out, int32_t cap, int32_t* n_out,
+                  mig_greedy_trace_fn trace, void* user);
+
+/* ---- RNG (util.hpp:27-51): std::mt19937_64 streams, splitmix64 seed mixing ---- */
+typedef struct mig_rng mig_rng;
+int mig_rng_create(uint64_t seed, mig_rng** out);
+void mig_rng_destroy(mig_rng* rng);
+uint64_t mig_rng_next(mig_rng* rng);
+uint64_t mig_mix_seed(uint64_t a, uint64_t b);
+uint64_t mig_pick_index(mig_rng* rng, uint64_t n);
+
+/* ---- MCTS slow algorithm (mcts.hpp) ---- */
+typedef struct mig_mcts_params { /* MctsParams, mcts.hpp:13-18 */
+    int32_t budget_iters;
+    int32_t topk;
+    int32_t pick_services;
+    double ucb_c;
+} mig_mcts_params;
+void mig_mcts_params_defaults(mig_mcts_params* out);
+
+/* expand(node, ctx, params, rng), mcts.hpp:89-116: children = top-K pool indices */
+int mig_expand(mig_ctx* ctx, const double* comp, int32_t n, const mig_mcts_params* params, mig_rng* rng,
+               int64_t* children, int32_t cap, int32_t* n_children);
+
+typedef struct mig_rollout_cache mig_rollout_cache; /* RolloutCache, mcts.hpp:47-50 */
+int mig_rollout_cache_create(mig_rollout_cache** out);
+void mig_rollout_cache_destroy(mig_rollout_cache* cache);
+int32_t mig_rollout_cache_builds(const mig_rollout_cache* cache);
+
+/* rollout(comp, ctx, params, cache, rng, max_depth, picked), mcts.hpp:122-143 */
+int mig_rollout(mig_ctx* ctx, const double* comp, int32_t n, const mig_mcts_params* params,
+                mig_rollout_cache* cache, mig_rng* rng, int32_t max_depth, int64_t* picked, int32_t cap,
+                int32_t* steps);
+
+typedef void (*mig_mcts_trace_fn)(void* user, int32_t iter, int32_t depth, int32_t estimate, int32_t best_len);
+/* mcts_solve(comp, ctx, params, seed, trace), mcts.hpp:148-252 */
+int mig_mcts_solve(mig_ctx* ctx, const double* comp, int32_t n, const mig_mcts_params* params, uint64_t seed,
+                   mig_config* out, int32_t cap, int32_t* n_out, mig_mcts_trace_fn trace, void* user);
+
+/* ---- GA (ga.hpp) ---- */
+typedef struct mig_ga_params { /* GaParams, ga.hpp:24-36 */
+    int32_t population;
+    double erase_fraction;
+    int32_t mutation_pairs;
+    int32_t stall_rounds;
+    double time_budget_s;
+    uint64_t seed;
+    int32_t max_rounds;
+    int32_t workers;
+    mig_mcts_params slow;
+} mig_ga_params;
+void mig_ga_params_defaults(mig_ga_params* out);
+
+/* completion_of(configs, services, profiles), core.hpp:291-302 */
+int mig_completion_of(const mig_ctx* ctx, const mig_config* configs, int32_t n_configs, double* comp_out);
+
+/* mutate(parent, params, rng), ga.hpp:83-113 (out may alias nothing; same length as parent) */
+int mig_mutate(const mig_ctx* ctx, const mig_config* parent, int32_t n_gpus, const mig_ga_params* params,
+               mig_rng* rng, mig_config* child);
+
+/* crossover(parent, MctsProcedure(params.slow), ctx, params, rng), ga.hpp:51-77.
+ * slow_kind: 0 = FastProcedure (greedy.hpp:160-164), 1 = MctsProcedure (mcts.hpp:254-260). */
+int mig_crossover(mig_ctx* ctx, const mig_config* parent, int32_t n_gpus, int32_t slow_kind,
+                  const mig_ga_params* params, mig_rng* rng, mig_config* child, int32_t cap, int32_t* n_child);
+
+typedef void (*mig_ga_log_fn)(void* user, int32_t round, int32_t best_gpus, double best_slack, int32_t improved,
+                              double elapsed_s);
+/* two_phase(ctx.services, profiles, rules, params, log), ga.hpp:126-179, on a context
+ * built with max_mix = 2 (as two_phase builds its own, ga.hpp:129).  The output is
+ * make_deployment order (sorted configs, core.hpp:305-312). */
+int mig_two_phase(mig_ctx* ctx, const mig_ga_params* params, mig_config* out, int32_t cap, int32_t* n_out,
+                  mig_ga_log_fn log, void* user);
+
+/* ---- eval bench helpers (bench.hpp) ---- */
+/* lower_bound(services, profiles), bench.hpp:93-108 */
+int mig_lower_bound(const mig_ctx* ctx, int32_t* out);
+
+/* ---- instrumentation (product only; CPU libraries report zeros) ---- */
+typedef struct mig_stats {
+    int64_t rows_scored;      /* Σ working-set rows scored by greedy scans + top-K scans */
+    int64_t greedy_steps;     /* argmax steps executed                                  */
+    int64_t ext_events;       /* extension events (greedy.hpp:107-119)                  */
+    int64_t ext_rows;         /* rows appended by extension enumeration                 */
+    int64_t kernel_launches;  /* CUDA kernels launched by this context                  */
+    double scan_ms;           /* device time of greedy launches (CUDA events)           */
+    double topk_ms;
+} mig_stats;
+int mig_ctx_stats(const mig_ctx* ctx, mig_stats* out);
+void mig_ctx_reset_stats(mig_ctx* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* MIGPLAN_B200_H */

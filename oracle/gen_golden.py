@@ -1,0 +1,172 @@
+"""Generate tests/golden/*.json from the compiled reference (oracle/_ref/libmigref.so).
+
+TEST INFRASTRUCTURE ONLY.  Every vector here is produced by the UNMODIFIED reference
+headers (behind oracle/ref_shim.cpp) on inputs that are either the reference's own
+fixtures (proj/fixtures/*.json, copied to tests/golden/fixtures) or workloads produced
+by the reference's own gen_workload (bench.hpp:125-156).  Floats are stored as
+float.hex() so comparisons are bit-exact.
+
+    python oracle/gen_golden.py [section ...]     # sections: greedy mcts ga topk partitions
+"""
+from __future__ import annotations
+
+import json
+import os
+import sys
+import time
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, os.path.join(os.path.dirname(HERE), "tests"))
+
+import support as S  # noqa: E402
+from support import mp  # noqa: E402
+
+
+def svc_json(services):
+    return [[s.service_id, s.model_name, s.required_rps.hex(), s.max_p90_ms.hex()] for s in services]
+
+
+def store_name(ps):
+    return "two_model" if "cnn-a" in ps else "fixture"
+
+
+def workloads_greedy():
+    ps = S.profiles()
+    out = []
+    for name in ("slos_day", "slos_night", "slos_24"):
+        out.append((name, ps, S.fixture_services(name, ps)))
+    for n, mu in ((24, 6.35), (24, 8.0), (24, 8.7)):
+        p2, sv = S.gen(n, mu)
+        out.append((f"gen{n}_{mu}", p2, sv))
+    for seed in range(1, 51):  # test_greedy.cpp:66-74
+        p2, sv = S.random_workload(2 + seed % 7, seed * 31)
+        out.append((f"rand{seed}", p2, sv))
+    for n, seed in ((12, 7), (16, 11), (20, 13)):  # larger two-model workloads (many extensions)
+        p2, sv = S.random_workload(n, seed)
+        out.append((f"rand_n{n}_s{seed}", p2, sv))
+    return out
+
+
+def greedy_entry(ps, sv, ref):
+    ctx = mp.make_plan_context(sv, ps, mp.PartitionRuleSet.defaults(), backend=ref)
+    trace = []
+    t = time.time()
+    plan = mp.fast_algo(mp.zero_completion(len(sv)), ctx,
+                        trace=lambda i, c, s, comp: trace.append([S.fhex(s), S.comp_digest(comp)]))
+    wall = time.time() - t
+    import ctypes as C
+    rows = C.c_int64()
+    buf, n = ctx._comp(mp.zero_completion(len(sv)))
+    ref.check(ref.lib.mig_ref_count_rows(ctx._p, buf, n, C.byref(rows)))
+    return {"store": store_name(ps), "services": svc_json(sv), "pool_size": len(ctx.pool), "plan": S.plan_key(plan),
+            "trace": trace, "rows_scored": rows.value, "ref_wall_s": round(wall, 4),
+            "final_comp": [S.fhex(c) for c in mp.completion_of(plan, sv, ps)]}
+
+
+def gen_greedy(ref):
+    res = {}
+    for name, ps, sv in workloads_greedy():
+        res[name] = greedy_entry(ps, sv, ref)
+        print(f"greedy {name}: {len(res[name]['plan'])} GPUs, {res[name]['rows_scored']} rows", flush=True)
+    return res
+
+
+def gen_mcts(ref):
+    res = {}
+    ps = S.profiles()
+    cases = [("slos_day", ps, S.fixture_services("slos_day", ps), 200, 1),
+             ("slos_night", ps, S.fixture_services("slos_night", ps), 200, 1)]
+    for seed in range(1, 16):  # test_mcts.cpp:128-140
+        p2, sv = S.random_workload(3 + seed % 5, seed * 17)
+        cases.append((f"rand{seed}", p2, sv, 60, seed))
+    p2, sv = S.random_workload(5, 4242)  # test_mcts.cpp:142-153
+    cases += [("det31", p2, sv, 80, 31), ("det32", p2, sv, 80, 32)]
+    p2, sv = S.gen(24, 6.35)
+    cases.append(("gen24_6.35", p2, sv, 200, 1))
+    for name, p, sv, budget, seed in cases:
+        ctx = mp.make_plan_context(sv, p, mp.PartitionRuleSet.defaults(), backend=ref)
+        tr = []
+        plan = mp.mcts_solve(mp.zero_completion(len(sv)), ctx, mp.MctsParams(budget_iters=budget), seed,
+                             trace=lambda *a: tr.append(list(a)))
+        res[name] = {"store": store_name(p), "services": svc_json(sv), "budget": budget, "seed": seed,
+                     "plan": S.plan_key(plan), "trace": tr}
+        print(f"mcts {name}: {len(plan)} GPUs", flush=True)
+    return res
+
+
+def gen_ga(ref):
+    res = {}
+    ps = S.profiles()
+    cases = [("slos_day", ps, S.fixture_services("slos_day", ps), dict(seed=24, max_rounds=3, time_budget_s=1e9)),
+             ("slos_night", ps, S.fixture_services("slos_night", ps), dict(seed=24, max_rounds=3, time_budget_s=1e9))]
+    p2, sv = S.random_workload(4, 321)  # test_ga.cpp:148-168
+    cases.append(("det77", p2, sv, dict(seed=77, max_rounds=4, time_budget_s=60.0, slow=mp.MctsParams(budget_iters=16))))
+    p2, sv = S.random_workload(5, 901)  # test_ga.cpp:123-146
+    cases.append(("stall9", p2, sv, dict(seed=9, max_rounds=40, time_budget_s=300.0, stall_rounds=10,
+                                         slow=mp.MctsParams(budget_iters=24))))
+    for name, p, sv, kw in cases:
+        params = mp.GaParams(**kw)
+        logs = []
+        dep = mp.two_phase(sv, p, mp.PartitionRuleSet.defaults(), params,
+                           log=lambda r: logs.append([r.round, r.best_gpus, S.fhex(r.best_slack), r.improved]),
+                           backend=ref)
+        kw2 = {k: (v.budget_iters if isinstance(v, mp.MctsParams) else v) for k, v in kw.items()}
+        res[name] = {"store": store_name(p), "services": svc_json(sv), "params": kw2,
+                     "plan": S.plan_key([g.config for g in dep.gpus]), "logs": logs}
+        print(f"ga {name}: {len(dep.gpus)} GPUs, {len(logs)} rounds", flush=True)
+    return res
+
+
+def gen_topk(ref):
+    res = {}
+    import random
+    rnd = random.Random(5)
+    ps = S.profiles()
+    for name, p, sv in (("slos_day", ps, S.fixture_services("slos_day", ps)),
+                        ("slos_24", ps, S.fixture_services("slos_24", ps)),
+                        ("rand_n12", *S.random_workload(12, 7))):
+        ctx = mp.make_plan_context(sv, p, mp.PartitionRuleSet.defaults(), backend=ref)
+        cases = []
+        for trial in range(12):
+            comp = [rnd.choice([0.0, rnd.random(), 1.0 + rnd.random(), 0.999999999]) for _ in sv]
+            k = rnd.choice([1, 3, 10, 25])
+            top = mp.topk_candidates(ctx, comp, k)
+            sub = sorted(rnd.sample(range(len(ctx.pool)), min(len(ctx.pool), 40)))
+            top_sub = mp.topk_candidates(ctx, comp, k, sub)
+            cases.append({"comp": [S.fhex(c) for c in comp], "k": k,
+                          "top": S.plan_key([ctx.pool[i].config for i in top]),
+                          "subset": S.plan_key([ctx.pool[i].config for i in sub]),
+                          "top_subset": S.plan_key([ctx.pool[i].config for i in top_sub])})
+        res[name] = {"store": store_name(p), "services": svc_json(sv), "cases": cases}
+        print(f"topk {name}", flush=True)
+    return res
+
+
+def gen_partitions(ref):
+    out = {}
+    r = mp.PartitionRuleSet.defaults()
+    out["defaults"] = [[[p.slices, p.start_slot] for p in lp.placements] for lp in mp.enumerate_maximal_partitions(r, ref)]
+    r2 = mp.PartitionRuleSet.defaults()
+    r2.hard_exclusions = set()
+    out["no_exclusion"] = [[[p.slices, p.start_slot] for p in lp.placements]
+                           for lp in mp.enumerate_maximal_partitions(r2, ref)]
+    return out
+
+
+SECTIONS = {"greedy": gen_greedy, "mcts": gen_mcts, "ga": gen_ga, "topk": gen_topk, "partitions": gen_partitions}
+
+
+def main(argv):
+    ref = S.ref_backend()
+    if ref is None:
+        sys.exit("oracle/_ref/libmigref.so not built (make -C oracle ref)")
+    for sec in argv or list(SECTIONS):
+        t = time.time()
+        data = SECTIONS[sec](ref)
+        with open(os.path.join(S.GOLDEN, f"{sec}.json"), "w") as f:
+            json.dump(data, f, separators=(",", ":"))
+        print(f"wrote {sec}.json in {time.time() - t:.1f}s", flush=True)
+
+
+if __name__ == "__main__":
+    main(sys.argv[1:])

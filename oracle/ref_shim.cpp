@@ -1,0 +1,536 @@
+// oracle/ref_shim.cpp — TEST INFRASTRUCTURE ONLY (never linked into the product).
+//
+// Puts the UNMODIFIED reference implementation (`/root/reference/proj/include/migplan/*.hpp`,
+// compiled from where it lies via -I, see oracle/Makefile) behind the same C-ABI as the
+// product (`include/migplan_b200.h`).  The result, oracle/_ref/libmigref.so, is
+//   * the checker that pins the CPU restatement (oracle/oracle.cpp),
+//   * the generator of tests/golden/*.json (oracle/gen_golden.py),
+//   * the `cpu_baseline` / `--impl reference` arm of bench.py.
+// Build rule: -O3 -DNDEBUG, no -march=native, -ffp-contract=off.
+#include <atomic>
+#include <chrono>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "migplan/bench.hpp"
+#include "migplan/config_enum.hpp"
+#include "migplan/core.hpp"
+#include "migplan/ga.hpp"
+#include "migplan/greedy.hpp"
+#include "migplan/mcts.hpp"
+#include "migplan/mig_rules.hpp"
+#include "migplan_b200.h"
+
+using namespace migplan;
+
+namespace {
+
+thread_local std::string g_err;
+
+template <class F>
+int guarded(F&& f) {
+    try {
+        f();
+        return MIG_OK;
+    } catch (const PlanningError& e) {
+        g_err = e.what();
+        return MIG_ERR_PLANNING;
+    } catch (const SchemaError& e) {
+        g_err = e.what();
+        return MIG_ERR_SCHEMA;
+    } catch (const std::invalid_argument& e) {
+        g_err = e.what();
+        return MIG_ERR_ARGUMENT;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return MIG_ERR_PLANNING;
+    }
+}
+
+PartitionRuleSet rules_of(const mig_rules* r) {
+    if (!r) return PartitionRuleSet::defaults();
+    PartitionRuleSet out;
+    for (int i = 0; i < r->n_sizes; ++i) {
+        auto& v = out.slot_positions[r->size[i]];
+        for (int k = 0; k < r->n_slots[i]; ++k) v.push_back(r->slots[i][k]);
+        std::sort(v.begin(), v.end());
+    }
+    for (int i = 0; i < r->n_weights; ++i) out.memory_weight[r->weight_size[i]] = r->weight[i];
+    for (int i = 0; i < r->n_exclusions; ++i)
+        out.hard_exclusions.insert(normalized_pair(r->exclusion[i][0], r->exclusion[i][1]));
+    out.memory_budget = r->memory_budget;
+    return out;
+}
+
+ProfileStore store_of(const mig_model_profile* models, int n_models) {
+    ProfileStore ps;
+    for (int m = 0; m < n_models; ++m) {
+        ModelProfile p;
+        p.model_name = models[m].model_name ? models[m].model_name : "";
+        for (int e = 0; e < models[m].n_entries; ++e) {
+            const auto& x = models[m].entries[e];
+            p.entries[x.size].push_back(ProfileEntry{x.batch, x.throughput_rps, x.p90_ms});
+        }
+        for (auto& [size, list] : p.entries)
+            std::sort(list.begin(), list.end(),
+                      [](const ProfileEntry& a, const ProfileEntry& b) { return a.batch < b.batch; });
+        validate_profile(p);
+        if (ps.count(p.model_name)) throw SchemaError("duplicate model '" + p.model_name + "'");
+        ps[p.model_name] = std::move(p);
+    }
+    return ps;
+}
+
+std::vector<ServiceSpec> services_of(const mig_service* s, int n) {
+    std::vector<ServiceSpec> out;
+    for (int i = 0; i < n; ++i)
+        out.push_back(ServiceSpec{s[i].service_id ? s[i].service_id : "", s[i].model_name ? s[i].model_name : "",
+                                  s[i].required_rps, s[i].max_p90_ms});
+    return out;
+}
+
+}  // namespace
+
+struct mig_ctx {
+    ProfileStore profiles;
+    PartitionRuleSet rules;
+    std::vector<ServiceSpec> services;
+    PlanContext plan;
+};
+
+struct mig_rng {
+    Rng rng;
+};
+
+struct mig_rollout_cache {
+    RolloutCache cache;
+};
+
+namespace {
+
+void to_c(const GpuConfig& cfg, const std::vector<ServiceSpec>& services, mig_config* out) {
+    if (cfg.instances.size() > MIG_MAX_INSTANCES) throw std::invalid_argument("config has more than 7 instances");
+    std::memset(out, 0, sizeof *out);
+    out->n_instances = static_cast<int32_t>(cfg.instances.size());
+    for (size_t k = 0; k < cfg.instances.size(); ++k) {
+        const auto& in = cfg.instances[k];
+        out->inst[k] = mig_instance{in.placement.slices, in.placement.start_slot,
+                                    service_index(services, in.service_id), in.batch};
+    }
+}
+
+GpuConfig from_c(const mig_config& c, const std::vector<ServiceSpec>& services) {
+    GpuConfig g;
+    for (int k = 0; k < c.n_instances; ++k) {
+        const auto& in = c.inst[k];
+        if (in.service < 0 || in.service >= static_cast<int>(services.size()))
+            throw PlanningError("unknown service index " + std::to_string(in.service));
+        g.instances.push_back(AssignedInstance{Placement{in.slices, in.slot}, services[in.service].service_id, in.batch});
+    }
+    return g;
+}
+
+void cand_to_c(const Candidate& c, const std::vector<ServiceSpec>& services, mig_candidate* out) {
+    std::memset(out, 0, sizeof *out);
+    to_c(c.config, services, &out->config);
+    out->nnz = static_cast<int32_t>(c.util.size());
+    for (size_t k = 0; k < c.util.size() && k < MIG_MAX_INSTANCES; ++k) {
+        out->util_idx[k] = c.util[k].first;
+        out->util_val[k] = c.util[k].second;
+    }
+    out->util_sum = c.util_sum;
+}
+
+CompletionRates comp_of(const double* comp, int n, const mig_ctx* ctx) {
+    if (n != static_cast<int>(ctx->services.size()))
+        throw PlanningError("completion vector length mismatch");
+    return CompletionRates{std::vector<double>(comp, comp + n)};
+}
+
+int emit_plan(const std::vector<GpuConfig>& plan, const std::vector<ServiceSpec>& services, mig_config* out,
+              int32_t cap, int32_t* n_out) {
+    *n_out = static_cast<int32_t>(plan.size());
+    for (size_t i = 0; i < plan.size() && static_cast<int32_t>(i) < cap; ++i) to_c(plan[i], services, &out[i]);
+    if (static_cast<int32_t>(plan.size()) > cap) {
+        g_err = "output capacity too small";
+        return MIG_ERR_ARGUMENT;
+    }
+    return MIG_OK;
+}
+
+MctsParams mcts_of(const mig_mcts_params* p) {
+    MctsParams m;
+    if (p) {
+        m.budget_iters = p->budget_iters;
+        m.topk = p->topk;
+        m.pick_services = p->pick_services;
+        m.ucb_c = p->ucb_c;
+    }
+    return m;
+}
+
+GaParams ga_of(const mig_ga_params* p) {
+    GaParams g;
+    if (p) {
+        g.population = p->population;
+        g.erase_fraction = p->erase_fraction;
+        g.mutation_pairs = p->mutation_pairs;
+        g.stall_rounds = p->stall_rounds;
+        g.time_budget_s = p->time_budget_s;
+        g.seed = p->seed;
+        g.max_rounds = p->max_rounds;
+        g.workers = p->workers;
+        g.slow = mcts_of(&p->slow);
+    }
+    return g;
+}
+
+// Instrumented replica of fast_algo's working-set growth (greedy.hpp:95-145), used
+// only to count rows scored for bench.py's reference arm; results equal fast_algo.
+int64_t count_rows(const CompletionRates& comp, const PlanContext& ctx) {
+    int64_t rows = 0;
+    CompletionRates cur = comp;
+    if (is_satisfied(cur)) return 0;
+    detail::WorkingSet ws(ctx.pool);
+    std::vector<bool> almost(ctx.services.size(), false);
+    auto maybe_extend = [&] {
+        std::set<int> unsat;
+        for (size_t i = 0; i < cur.values.size(); ++i)
+            if (cur.values[i] < 1.0 - kSatisfyEps) unsat.insert(static_cast<int>(i));
+        for (int i : unsat) {
+            if (almost[i]) continue;
+            if (1.0 - cur.values[i] < ctx.pool.best_single_util[i]) {
+                almost[i] = true;
+                extend_candidate_pool(ws.extra, ctx.services, *ctx.profiles, ctx.rules, i, unsat, 4);
+            }
+        }
+    };
+    maybe_extend();
+    while (!is_satisfied(cur)) {
+        rows += static_cast<int64_t>(ws.size());
+        int best = -1;
+        double best_score = 0.0;
+        for (size_t i = 0; i < ws.size(); ++i) {
+            double s = score(ws.at(i), cur);
+            if (s <= 0.0) continue;
+            if (best < 0 || candidate_preferred(ws.at(i), s, ws.at(best), best_score)) {
+                best = static_cast<int>(i);
+                best_score = s;
+            }
+        }
+        if (best < 0) throw PlanningError("fast_algo: no config with positive score while services remain unsatisfied");
+        for (const auto& [idx, u] : ws.at(best).util) cur.values[idx] += u;
+        maybe_extend();
+    }
+    return rows;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* mig_last_error(void) { return g_err.c_str(); }
+int32_t mig_abi_version(void) { return 1; }
+const char* mig_impl_name(void) { return "reference"; }
+
+void mig_rules_defaults(mig_rules* out) {
+    std::memset(out, 0, sizeof *out);
+    PartitionRuleSet d = PartitionRuleSet::defaults();
+    for (const auto& [size, slots] : d.slot_positions) {
+        int i = out->n_sizes++;
+        out->size[i] = size;
+        out->n_slots[i] = static_cast<int32_t>(slots.size());
+        for (size_t k = 0; k < slots.size(); ++k) out->slots[i][k] = slots[k];
+    }
+    for (const auto& [size, w] : d.memory_weight) {
+        int i = out->n_weights++;
+        out->weight_size[i] = size;
+        out->weight[i] = w;
+    }
+    for (const auto& [a, b] : d.hard_exclusions) {
+        int i = out->n_exclusions++;
+        out->exclusion[i][0] = a;
+        out->exclusion[i][1] = b;
+    }
+    out->memory_budget = d.memory_budget;
+}
+
+int mig_is_legal_partition(const mig_rules* rules, const int32_t* slices, const int32_t* slots, int32_t n,
+                           int32_t* legal) {
+    return guarded([&] {
+        std::vector<Placement> ps;
+        for (int i = 0; i < n; ++i) ps.push_back(Placement{slices[i], slots[i]});
+        *legal = is_legal_partition(ps, rules_of(rules)) ? 1 : 0;
+    });
+}
+
+int mig_enumerate_maximal_partitions(const mig_rules* rules, mig_partition* out, int32_t cap, int32_t* n_out) {
+    return guarded([&] {
+        auto parts = enumerate_maximal_partitions(rules_of(rules));
+        *n_out = static_cast<int32_t>(parts.size());
+        if (*n_out > cap) throw std::invalid_argument("output capacity too small");
+        for (size_t i = 0; i < parts.size(); ++i) {
+            std::memset(&out[i], 0, sizeof out[i]);
+            out[i].n = static_cast<int32_t>(parts[i].placements.size());
+            for (size_t k = 0; k < parts[i].placements.size(); ++k) {
+                out[i].slices[k] = parts[i].placements[k].slices;
+                out[i].slot[k] = parts[i].placements[k].start_slot;
+            }
+        }
+    });
+}
+
+int mig_validate_services(const mig_model_profile* models, int32_t n_models, const mig_service* services,
+                          int32_t n_services, int32_t* perm) {
+    return guarded([&] {
+        ProfileStore ps = store_of(models, n_models);
+        auto svcs = services_of(services, n_services);
+        validate_services(svcs, ps);
+        std::vector<bool> used(n_services, false);
+        for (int i = 0; i < n_services; ++i)
+            for (int j = 0; j < n_services; ++j)
+                if (!used[j] && svcs[i].service_id == (services[j].service_id ? services[j].service_id : "")) {
+                    perm[i] = j;
+                    used[j] = true;
+                    break;
+                }
+    });
+}
+
+int mig_ctx_create(const mig_rules* rules, const mig_model_profile* models, int32_t n_models,
+                   const mig_service* services, int32_t n_services, int32_t max_mix, int32_t, mig_ctx** out) {
+    return guarded([&] {
+        auto ctx = std::make_unique<mig_ctx>();
+        ctx->profiles = store_of(models, n_models);
+        ctx->rules = rules_of(rules);
+        ctx->services = services_of(services, n_services);
+        ctx->plan = make_plan_context(ctx->services, ctx->profiles, ctx->rules, max_mix);
+        *out = ctx.release();
+    });
+}
+
+void mig_ctx_destroy(mig_ctx* ctx) { delete ctx; }
+int32_t mig_ctx_n_services(const mig_ctx* ctx) { return static_cast<int32_t>(ctx->services.size()); }
+
+int mig_pool_size(const mig_ctx* ctx, int64_t* out) {
+    *out = static_cast<int64_t>(ctx->plan.pool.items.size());
+    return MIG_OK;
+}
+
+int mig_pool_candidate(const mig_ctx* ctx, int64_t idx, mig_candidate* out) {
+    return guarded([&] {
+        if (idx < 0 || idx >= static_cast<int64_t>(ctx->plan.pool.items.size()))
+            throw std::invalid_argument("pool index out of range");
+        cand_to_c(ctx->plan.pool.items[idx], ctx->services, out);
+    });
+}
+
+int mig_pool_best_single_util(const mig_ctx* ctx, double* out) {
+    for (size_t i = 0; i < ctx->services.size(); ++i) out[i] = ctx->plan.pool.best_single_util[i];
+    return MIG_OK;
+}
+
+int mig_score(const mig_ctx* ctx, int64_t idx, const double* comp, int32_t n, double* out) {
+    return guarded([&] {
+        if (idx < 0 || idx >= static_cast<int64_t>(ctx->plan.pool.items.size()))
+            throw std::invalid_argument("pool index out of range");
+        *out = score(ctx->plan.pool.items[idx], comp_of(comp, n, ctx));
+    });
+}
+
+int mig_topk_candidates(mig_ctx* ctx, const double* comp, int32_t n, int32_t k, const int64_t* from,
+                        int64_t n_from, int64_t* out_idx, int32_t* n_out) {
+    return guarded([&] {
+        CompletionRates c = comp_of(comp, n, ctx);
+        std::vector<int> f;
+        if (from && n_from >= 0)
+            for (int64_t i = 0; i < n_from; ++i) f.push_back(static_cast<int>(from[i]));
+        auto top = detail::topk_candidates(ctx->plan.pool, c, k, (from && n_from >= 0) ? &f : nullptr);
+        *n_out = static_cast<int32_t>(top.size());
+        for (size_t i = 0; i < top.size(); ++i) out_idx[i] = top[i];
+    });
+}
+
+int mig_fast_algo(mig_ctx* ctx, const double* comp, int32_t n, mig_config* out, int32_t cap, int32_t* n_out,
+                  mig_greedy_trace_fn trace, void* user) {
+    int rc = MIG_OK;
+    int g = guarded([&] {
+        CompletionRates c = comp_of(comp, n, ctx);
+        std::function<void(int, const Candidate&, double, const CompletionRates&)> tr = nullptr;
+        if (trace)
+            tr = [&](int iter, const Candidate& cand, double s, const CompletionRates& cur) {
+                mig_candidate mc;
+                cand_to_c(cand, ctx->services, &mc);
+                trace(user, iter, &mc, s, cur.values.data(), static_cast<int32_t>(cur.values.size()));
+            };
+        auto plan = fast_algo(c, ctx->plan, tr);
+        rc = emit_plan(plan, ctx->services, out, cap, n_out);
+    });
+    return g != MIG_OK ? g : rc;
+}
+
+int mig_rng_create(uint64_t seed, mig_rng** out) {
+    *out = new mig_rng{Rng(seed)};
+    return MIG_OK;
+}
+void mig_rng_destroy(mig_rng* rng) { delete rng; }
+uint64_t mig_rng_next(mig_rng* rng) { return rng->rng(); }
+uint64_t mig_mix_seed(uint64_t a, uint64_t b) { return mix_seed(a, b); }
+uint64_t mig_pick_index(mig_rng* rng, uint64_t n) { return pick_index(rng->rng, n); }
+
+void mig_mcts_params_defaults(mig_mcts_params* out) {
+    MctsParams m;
+    *out = mig_mcts_params{m.budget_iters, m.topk, m.pick_services, m.ucb_c};
+}
+
+int mig_expand(mig_ctx* ctx, const double* comp, int32_t n, const mig_mcts_params* params, mig_rng* rng,
+               int64_t* children, int32_t cap, int32_t* n_children) {
+    return guarded([&] {
+        SearchNode node(comp_of(comp, n, ctx));
+        auto top = expand(node, ctx->plan, mcts_of(params), rng->rng);
+        *n_children = static_cast<int32_t>(top.size());
+        if (*n_children > cap) throw std::invalid_argument("output capacity too small");
+        for (size_t i = 0; i < top.size(); ++i) children[i] = top[i];
+    });
+}
+
+int mig_rollout_cache_create(mig_rollout_cache** out) {
+    *out = new mig_rollout_cache{};
+    return MIG_OK;
+}
+void mig_rollout_cache_destroy(mig_rollout_cache* cache) { delete cache; }
+int32_t mig_rollout_cache_builds(const mig_rollout_cache* cache) { return cache->cache.builds; }
+
+int mig_rollout(mig_ctx* ctx, const double* comp, int32_t n, const mig_mcts_params* params,
+                mig_rollout_cache* cache, mig_rng* rng, int32_t max_depth, int64_t* picked, int32_t cap,
+                int32_t* steps) {
+    return guarded([&] {
+        std::vector<int> p;
+        *steps = rollout(comp_of(comp, n, ctx), ctx->plan, mcts_of(params), cache->cache, rng->rng, max_depth,
+                         picked ? &p : nullptr);
+        if (picked) {
+            if (static_cast<int32_t>(p.size()) > cap) throw std::invalid_argument("output capacity too small");
+            for (size_t i = 0; i < p.size(); ++i) picked[i] = p[i];
+        }
+    });
+}
+
+int mig_mcts_solve(mig_ctx* ctx, const double* comp, int32_t n, const mig_mcts_params* params, uint64_t seed,
+                   mig_config* out, int32_t cap, int32_t* n_out, mig_mcts_trace_fn trace, void* user) {
+    int rc = MIG_OK;
+    int g = guarded([&] {
+        std::function<void(int, int, int, int)> tr = nullptr;
+        if (trace) tr = [&](int a, int b, int c, int d) { trace(user, a, b, c, d); };
+        auto plan = mcts_solve(comp_of(comp, n, ctx), ctx->plan, mcts_of(params), seed, tr);
+        rc = emit_plan(plan, ctx->services, out, cap, n_out);
+    });
+    return g != MIG_OK ? g : rc;
+}
+
+void mig_ga_params_defaults(mig_ga_params* out) {
+    GaParams g;
+    std::memset(out, 0, sizeof *out);
+    out->population = g.population;
+    out->erase_fraction = g.erase_fraction;
+    out->mutation_pairs = g.mutation_pairs;
+    out->stall_rounds = g.stall_rounds;
+    out->time_budget_s = g.time_budget_s;
+    out->seed = g.seed;
+    out->max_rounds = g.max_rounds;
+    out->workers = g.workers;
+    out->slow = mig_mcts_params{g.slow.budget_iters, g.slow.topk, g.slow.pick_services, g.slow.ucb_c};
+}
+
+int mig_completion_of(const mig_ctx* ctx, const mig_config* configs, int32_t n_configs, double* comp_out) {
+    return guarded([&] {
+        std::vector<GpuConfig> cfgs;
+        for (int i = 0; i < n_configs; ++i) cfgs.push_back(from_c(configs[i], ctx->services));
+        auto c = completion_of(cfgs, ctx->services, ctx->profiles);
+        for (size_t i = 0; i < c.values.size(); ++i) comp_out[i] = c.values[i];
+    });
+}
+
+int mig_mutate(const mig_ctx* ctx, const mig_config* parent, int32_t n_gpus, const mig_ga_params* params,
+               mig_rng* rng, mig_config* child) {
+    return guarded([&] {
+        Chromosome p;
+        for (int i = 0; i < n_gpus; ++i) p.gpus.push_back(from_c(parent[i], ctx->services));
+        p.gpu_count = n_gpus;
+        Chromosome c = mutate(p, ga_of(params), rng->rng);
+        for (size_t i = 0; i < c.gpus.size(); ++i) to_c(c.gpus[i], ctx->services, &child[i]);
+    });
+}
+
+int mig_crossover(mig_ctx* ctx, const mig_config* parent, int32_t n_gpus, int32_t slow_kind,
+                  const mig_ga_params* params, mig_rng* rng, mig_config* child, int32_t cap, int32_t* n_child) {
+    int rc = MIG_OK;
+    int g = guarded([&] {
+        std::vector<GpuConfig> gpus;
+        for (int i = 0; i < n_gpus; ++i) gpus.push_back(from_c(parent[i], ctx->services));
+        Chromosome p = gpus.empty() ? Chromosome{} : evaluate_chromosome(gpus, ctx->plan);
+        GaParams gp = ga_of(params);
+        FastProcedure fast;
+        MctsProcedure slow(gp.slow);
+        const OptimizerProcedure& proc = slow_kind == 0 ? static_cast<const OptimizerProcedure&>(fast) : slow;
+        Chromosome c = crossover(p, proc, ctx->plan, gp, rng->rng);
+        rc = emit_plan(c.gpus, ctx->services, child, cap, n_child);
+    });
+    return g != MIG_OK ? g : rc;
+}
+
+int mig_two_phase(mig_ctx* ctx, const mig_ga_params* params, mig_config* out, int32_t cap, int32_t* n_out,
+                  mig_ga_log_fn log, void* user) {
+    int rc = MIG_OK;
+    int g = guarded([&] {
+        std::function<void(const GaRoundLog&)> lg = nullptr;
+        if (log)
+            lg = [&](const GaRoundLog& r) {
+                log(user, r.round, r.best_gpus, r.best_slack, r.improved ? 1 : 0, r.elapsed_s);
+            };
+        Deployment dep = two_phase(ctx->services, ctx->profiles, ctx->rules, ga_of(params), lg);
+        std::vector<GpuConfig> cfgs;
+        for (auto& gpu : dep.gpus) cfgs.push_back(gpu.config);
+        rc = emit_plan(cfgs, ctx->services, out, cap, n_out);
+    });
+    return g != MIG_OK ? g : rc;
+}
+
+int mig_lower_bound(const mig_ctx* ctx, int32_t* out) {
+    return guarded([&] { *out = lower_bound(ctx->services, ctx->profiles); });
+}
+
+int mig_ctx_stats(const mig_ctx*, mig_stats* out) {
+    std::memset(out, 0, sizeof *out);
+    return MIG_OK;
+}
+void mig_ctx_reset_stats(mig_ctx*) {}
+
+// Reference-arm extras (not in the product header): rows a fast_algo scans, and
+// gen_workload (bench.hpp:125-156) so generated workloads come from the reference itself.
+int mig_ref_count_rows(mig_ctx* ctx, const double* comp, int32_t n, int64_t* rows) {
+    return guarded([&] { *rows = count_rows(comp_of(comp, n, ctx), ctx->plan); });
+}
+
+// Writes n services (id/model as indices into caller-owned string tables is awkward in C,
+// so ids follow svc-%03d and models are returned as profile-store indices).
+int mig_ref_gen_workload(const mig_model_profile* models, int32_t n_models, int32_t n, int32_t normal, double mu,
+                         double sigma, double latency_ms, uint64_t seed, int32_t* model_idx, double* required_rps) {
+    return guarded([&] {
+        ProfileStore ps = store_of(models, n_models);
+        WorkloadSpec w = gen_workload(n, normal ? Distribution::Normal : Distribution::Lognormal, mu, sigma,
+                                      latency_ms, seed, ps);
+        std::vector<std::string> names;
+        for (const auto& [name, p] : ps) names.push_back(name);
+        for (int i = 0; i < n; ++i) {
+            const auto& s = w.services[i];
+            model_idx[i] = -1;
+            for (int m = 0; m < n_models; ++m)
+                if (s.model_name == models[m].model_name) model_idx[i] = m;
+            required_rps[i] = s.required_rps;
+        }
+    });
+}
+
+}  // extern "C"

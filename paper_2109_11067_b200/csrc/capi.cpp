@@ -1,0 +1,504 @@
+// capi.cpp — the product's implementation of include/migplan_b200.h.
+// Exceptions are mapped to status codes (util.hpp:12-25, migplan.cpp:414-426).
+#include <cstring>
+#include <string>
+
+#include "engine.hpp"
+#include "migplan_b200.h"
+#include "search.hpp"
+
+using namespace mgb;
+
+namespace {
+
+thread_local std::string g_err;
+
+template <class F>
+int guarded(F&& f) {
+    try {
+        f();
+        return MIG_OK;
+    } catch (const PlanningError& e) {
+        g_err = e.what();
+        return MIG_ERR_PLANNING;
+    } catch (const SchemaError& e) {
+        g_err = e.what();
+        return MIG_ERR_SCHEMA;
+    } catch (const DeviceError& e) {
+        g_err = e.what();
+        return MIG_ERR_DEVICE;
+    } catch (const ArgumentError& e) {
+        g_err = e.what();
+        return MIG_ERR_ARGUMENT;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return MIG_ERR_ARGUMENT;
+    }
+}
+
+Rules rules_of(const mig_rules* r) {
+    if (!r) return Rules::defaults();
+    Rules out;
+    if (r->n_sizes < 0 || r->n_sizes > MIG_MAX_RULE_SIZES || r->n_weights < 0 || r->n_weights > MIG_MAX_RULE_SIZES ||
+        r->n_exclusions < 0 || r->n_exclusions > MIG_MAX_EXCLUSIONS)
+        throw SchemaError("partition rules out of range");
+    for (int i = 0; i < r->n_sizes; ++i) {
+        auto& v = out.slot_positions[r->size[i]];
+        for (int k = 0; k < r->n_slots[i] && k < MIG_MAX_RULE_SLOTS; ++k) v.push_back(r->slots[i][k]);
+        std::sort(v.begin(), v.end());
+    }
+    for (int i = 0; i < r->n_weights; ++i) out.memory_weight[r->weight_size[i]] = r->weight[i];
+    for (int i = 0; i < r->n_exclusions; ++i) {
+        int a = r->exclusion[i][0], b = r->exclusion[i][1];
+        out.hard_exclusions.insert(a <= b ? std::pair{a, b} : std::pair{b, a});
+    }
+    out.memory_budget = r->memory_budget;
+    return out;
+}
+
+std::map<std::string, ModelProfile> profiles_of(const mig_model_profile* models, int n) {
+    std::map<std::string, ModelProfile> ps;
+    for (int m = 0; m < n; ++m) {
+        ModelProfile p;
+        p.name = models[m].model_name ? models[m].model_name : "";
+        for (int e = 0; e < models[m].n_entries; ++e) {
+            const auto& x = models[m].entries[e];
+            if (!valid_slices(x.size)) throw SchemaError("invalid instance size " + std::to_string(x.size));
+            p.entries[x.size].push_back(ProfileEntry{x.batch, x.throughput_rps, x.p90_ms});
+        }
+        for (auto& [size, list] : p.entries)
+            std::sort(list.begin(), list.end(), [](const ProfileEntry& a, const ProfileEntry& b) { return a.batch < b.batch; });
+        validate_profile(p);
+        if (ps.count(p.name)) throw SchemaError("duplicate model '" + p.name + "'");
+        ps[p.name] = std::move(p);
+    }
+    return ps;
+}
+
+std::vector<Service> services_of(const mig_service* s, int n) {
+    std::vector<Service> out;
+    for (int i = 0; i < n; ++i)
+        out.push_back(Service{s[i].service_id ? s[i].service_id : "", s[i].model_name ? s[i].model_name : "",
+                              s[i].required_rps, s[i].max_p90_ms});
+    return out;
+}
+
+void to_c(const Config& c, mig_config* out) {
+    std::memset(out, 0, sizeof *out);
+    out->n_instances = c.n;
+    for (int k = 0; k < c.n; ++k) out->inst[k] = mig_instance{c.inst[k].slices, c.inst[k].slot, c.inst[k].svc, c.inst[k].batch};
+}
+
+Config from_c(const mig_config& c, int n_services) {
+    if (c.n_instances < 0 || c.n_instances > MIG_MAX_INSTANCES) throw ArgumentError("bad instance count");
+    Config g;
+    g.n = c.n_instances;
+    for (int k = 0; k < c.n_instances; ++k) {
+        const auto& in = c.inst[k];
+        if (in.service < 0 || in.service >= n_services)
+            throw PlanningError("unknown service index " + std::to_string(in.service));
+        g.inst[k] = Model::Inst{in.slices, in.slot, in.service, in.batch};
+    }
+    return g;
+}
+
+int emit(const std::vector<Config>& plan, mig_config* out, int32_t cap, int32_t* n_out) {
+    *n_out = static_cast<int32_t>(plan.size());
+    for (size_t i = 0; i < plan.size() && static_cast<int32_t>(i) < cap; ++i) to_c(plan[i], &out[i]);
+    if (static_cast<int32_t>(plan.size()) > cap) {
+        g_err = "output capacity too small";
+        return MIG_ERR_ARGUMENT;
+    }
+    return MIG_OK;
+}
+
+MctsParams mcts_of(const mig_mcts_params* p) {
+    MctsParams m;
+    if (p) m = MctsParams{p->budget_iters, p->topk, p->pick_services, p->ucb_c};
+    return m;
+}
+
+GaParams ga_of(const mig_ga_params* p) {
+    GaParams g;
+    if (p) {
+        g.population = p->population;
+        g.erase_fraction = p->erase_fraction;
+        g.mutation_pairs = p->mutation_pairs;
+        g.stall_rounds = p->stall_rounds;
+        g.time_budget_s = p->time_budget_s;
+        g.seed = p->seed;
+        g.max_rounds = p->max_rounds;
+        g.workers = p->workers;
+        g.slow = mcts_of(&p->slow);
+    }
+    return g;
+}
+
+}  // namespace
+
+struct mig_ctx {
+    std::unique_ptr<Engine> e;
+};
+struct mig_rng {
+    Rng rng;
+};
+struct mig_rollout_cache {
+    RolloutCache cache;
+};
+
+namespace {
+std::vector<double> comp_of(const mig_ctx* ctx, const double* comp, int n) {
+    if (n != ctx->e->n()) throw PlanningError("completion vector length mismatch");
+    return std::vector<double>(comp, comp + n);
+}
+void cand_of(const Engine& e, uint64_t row, mig_candidate* out) {
+    std::memset(out, 0, sizeof *out);
+    to_c(e.config_of(row), &out->config);
+    const Model& m = e.model();
+    int svc[kRowK], pat[kRowK];
+    int k = m.members(row, svc, pat);
+    out->nnz = k;
+    for (int j = 0; j < k; ++j) {
+        out->util_idx[j] = svc[j];
+        out->util_val[j] = m.U[static_cast<size_t>(svc[j]) * m.PP + pat[j]];
+    }
+    out->util_sum = m.util_sum(row);
+}
+}  // namespace
+
+extern "C" {
+
+const char* mig_last_error(void) { return g_err.c_str(); }
+int32_t mig_abi_version(void) { return 1; }
+const char* mig_impl_name(void) { return "product"; }
+
+void mig_rules_defaults(mig_rules* out) {
+    std::memset(out, 0, sizeof *out);
+    Rules d = Rules::defaults();
+    for (const auto& [size, slots] : d.slot_positions) {
+        int i = out->n_sizes++;
+        out->size[i] = size;
+        out->n_slots[i] = static_cast<int32_t>(slots.size());
+        for (size_t k = 0; k < slots.size(); ++k) out->slots[i][k] = slots[k];
+    }
+    for (const auto& [size, w] : d.memory_weight) {
+        int i = out->n_weights++;
+        out->weight_size[i] = size;
+        out->weight[i] = w;
+    }
+    for (const auto& [a, b] : d.hard_exclusions) {
+        int i = out->n_exclusions++;
+        out->exclusion[i][0] = a;
+        out->exclusion[i][1] = b;
+    }
+    out->memory_budget = d.memory_budget;
+}
+
+int mig_is_legal_partition(const mig_rules* rules, const int32_t* slices, const int32_t* slots, int32_t n,
+                           int32_t* legal) {
+    return guarded([&] {
+        std::vector<Place> ps;
+        for (int i = 0; i < n; ++i) ps.push_back(Place{slices[i], slots[i]});
+        *legal = is_legal(ps, rules_of(rules)) ? 1 : 0;
+    });
+}
+
+int mig_enumerate_maximal_partitions(const mig_rules* rules, mig_partition* out, int32_t cap, int32_t* n_out) {
+    return guarded([&] {
+        auto parts = maximal_partitions(rules_of(rules));
+        *n_out = static_cast<int32_t>(parts.size());
+        if (*n_out > cap) throw ArgumentError("output capacity too small");
+        for (size_t i = 0; i < parts.size(); ++i) {
+            std::memset(&out[i], 0, sizeof out[i]);
+            out[i].n = static_cast<int32_t>(parts[i].size());
+            for (size_t k = 0; k < parts[i].size() && k < MIG_MAX_INSTANCES; ++k) {
+                out[i].slices[k] = parts[i][k].slices;
+                out[i].slot[k] = parts[i][k].slot;
+            }
+        }
+    });
+}
+
+int mig_validate_services(const mig_model_profile* models, int32_t n_models, const mig_service* services,
+                          int32_t n_services, int32_t* perm) {
+    return guarded([&] {  // core.hpp:151-171
+        auto ps = profiles_of(models, n_models);
+        auto sv = services_of(services, n_services);
+        std::vector<int> idx(n_services);
+        for (int i = 0; i < n_services; ++i) idx[i] = i;
+        std::sort(idx.begin(), idx.end(), [&](int a, int b) { return sv[a].id < sv[b].id; });
+        for (int i = 0; i + 1 < n_services; ++i)
+            if (sv[idx[i]].id == sv[idx[i + 1]].id) throw SchemaError("duplicate service id '" + sv[idx[i]].id + "'");
+        for (int i : idx) {
+            const auto& s = sv[i];
+            if (s.id.empty()) throw SchemaError("service with empty id");
+            if (s.req <= 0.0) throw PlanningError("service '" + s.id + "': required throughput must be positive");
+            if (s.p90 <= 0.0) throw PlanningError("service '" + s.id + "': latency ceiling must be positive");
+            auto it = ps.find(s.model);
+            if (it == ps.end()) throw PlanningError("no profile for model '" + s.model + "'");
+            bool feasible = false;
+            for (const auto& [size, list] : it->second.entries)
+                for (const auto& e : list)
+                    if (valid_slices(size) && e.p90 <= s.p90) feasible = true;
+            if (!feasible)
+                throw PlanningError("service '" + s.id + "' is unschedulable: no (size, batch) of model '" + s.model +
+                                    "' meets p90 <= " + std::to_string(s.p90) + " ms");
+        }
+        for (int i = 0; i < n_services; ++i) perm[i] = idx[i];
+    });
+}
+
+int mig_ctx_create(const mig_rules* rules, const mig_model_profile* models, int32_t n_models,
+                   const mig_service* services, int32_t n_services, int32_t max_mix, int32_t device, mig_ctx** out) {
+    return guarded([&] {
+        if (!out) throw ArgumentError("null output");
+        auto c = std::make_unique<mig_ctx>();
+        c->e = std::make_unique<Engine>(rules_of(rules), profiles_of(models, n_models), services_of(services, n_services),
+                                        max_mix, device);
+        *out = c.release();
+    });
+}
+
+void mig_ctx_destroy(mig_ctx* ctx) { delete ctx; }
+int32_t mig_ctx_n_services(const mig_ctx* ctx) { return ctx->e->n(); }
+
+int mig_pool_size(const mig_ctx* ctx, int64_t* out) {
+    *out = ctx->e->pool_size();
+    return MIG_OK;
+}
+
+int mig_pool_candidate(const mig_ctx* ctx, int64_t idx, mig_candidate* out) {
+    return guarded([&] {
+        if (idx < 0 || idx >= ctx->e->pool_size()) throw ArgumentError("pool index out of range");
+        cand_of(*ctx->e, ctx->e->base_rows()[idx], out);
+    });
+}
+
+int mig_pool_best_single_util(const mig_ctx* ctx, double* out) {
+    for (int i = 0; i < ctx->e->n(); ++i) out[i] = ctx->e->model().best_single[i];
+    return MIG_OK;
+}
+
+int mig_score(const mig_ctx* ctx, int64_t idx, const double* comp, int32_t n, double* out) {
+    return guarded([&] {
+        if (idx < 0 || idx >= ctx->e->pool_size()) throw ArgumentError("pool index out of range");
+        auto c = comp_of(ctx, comp, n);
+        *out = ctx->e->model().score(ctx->e->base_rows()[idx], c.data());
+    });
+}
+
+int mig_topk_candidates(mig_ctx* ctx, const double* comp, int32_t n, int32_t k, const int64_t* from, int64_t n_from,
+                        int64_t* out_idx, int32_t* n_out) {
+    return guarded([&] {
+        auto c = comp_of(ctx, comp, n);
+        std::vector<long long> idx;
+        if (from && n_from >= 0) {
+            for (int64_t i = 0; i < n_from; ++i) {
+                if (from[i] < 0 || from[i] >= ctx->e->pool_size()) throw ArgumentError("pool index out of range");
+                idx.push_back(from[i]);
+            }
+        }
+        std::vector<long long> top;
+        if (from && n_from == 0) top = {};
+        else top = ctx->e->topk(c, k, (from && n_from >= 0) ? &idx : nullptr, nullptr);
+        *n_out = static_cast<int32_t>(top.size());
+        for (size_t i = 0; i < top.size(); ++i) out_idx[i] = top[i];
+    });
+}
+
+int mig_fast_algo(mig_ctx* ctx, const double* comp, int32_t n, mig_config* out, int32_t cap, int32_t* n_out,
+                  mig_greedy_trace_fn trace, void* user) {
+    int rc = MIG_OK;
+    int g = guarded([&] {
+        auto c = comp_of(ctx, comp, n);
+        std::vector<uint64_t> rows;
+        std::vector<double> scores;
+        ctx->e->fast_algo(c, rows, scores);
+        std::vector<Config> plan;
+        const Model& m = ctx->e->model();
+        for (size_t i = 0; i < rows.size(); ++i) {
+            plan.push_back(ctx->e->config_of(rows[i]));
+            if (trace) {  // replay greedy.hpp:139-140: comp after the pick, then trace
+                int svc[kRowK], pat[kRowK];
+                int k = m.members(rows[i], svc, pat);
+                for (int j = 0; j < k; ++j) c[svc[j]] = c[svc[j]] + m.U[static_cast<size_t>(svc[j]) * m.PP + pat[j]];
+                mig_candidate mc;
+                cand_of(*ctx->e, rows[i], &mc);
+                trace(user, static_cast<int32_t>(i), &mc, scores[i], c.data(), n);
+            }
+        }
+        rc = emit(plan, out, cap, n_out);
+    });
+    return g != MIG_OK ? g : rc;
+}
+
+int mig_rng_create(uint64_t seed, mig_rng** out) {
+    *out = new mig_rng{Rng(seed)};
+    return MIG_OK;
+}
+void mig_rng_destroy(mig_rng* rng) { delete rng; }
+uint64_t mig_rng_next(mig_rng* rng) { return rng->rng(); }
+uint64_t mig_mix_seed(uint64_t a, uint64_t b) { return mix_seed(a, b); }
+uint64_t mig_pick_index(mig_rng* rng, uint64_t n) { return pick_index(rng->rng, n); }
+
+void mig_mcts_params_defaults(mig_mcts_params* out) {
+    MctsParams m;
+    *out = mig_mcts_params{m.budget_iters, m.topk, m.pick_services, m.ucb_c};
+}
+
+int mig_expand(mig_ctx* ctx, const double* comp, int32_t n, const mig_mcts_params* params, mig_rng* rng,
+               int64_t* children, int32_t cap, int32_t* n_children) {
+    return guarded([&] {
+        auto top = expand_children(*ctx->e, comp_of(ctx, comp, n), mcts_of(params), rng->rng);
+        *n_children = static_cast<int32_t>(top.size());
+        if (*n_children > cap) throw ArgumentError("output capacity too small");
+        for (size_t i = 0; i < top.size(); ++i) children[i] = top[i];
+    });
+}
+
+int mig_rollout_cache_create(mig_rollout_cache** out) {
+    *out = new mig_rollout_cache{};
+    return MIG_OK;
+}
+void mig_rollout_cache_destroy(mig_rollout_cache* cache) { delete cache; }
+int32_t mig_rollout_cache_builds(const mig_rollout_cache* cache) { return cache->cache.builds; }
+
+int mig_rollout(mig_ctx* ctx, const double* comp, int32_t n, const mig_mcts_params* params, mig_rollout_cache* cache,
+                mig_rng* rng, int32_t max_depth, int64_t* picked, int32_t cap, int32_t* steps) {
+    return guarded([&] {
+        std::vector<long long> p;
+        *steps = rollout(*ctx->e, comp_of(ctx, comp, n), mcts_of(params), cache->cache, rng->rng, max_depth,
+                         picked ? &p : nullptr);
+        if (picked) {
+            if (static_cast<int32_t>(p.size()) > cap) throw ArgumentError("output capacity too small");
+            for (size_t i = 0; i < p.size(); ++i) picked[i] = p[i];
+        }
+    });
+}
+
+int mig_mcts_solve(mig_ctx* ctx, const double* comp, int32_t n, const mig_mcts_params* params, uint64_t seed,
+                   mig_config* out, int32_t cap, int32_t* n_out, mig_mcts_trace_fn trace, void* user) {
+    int rc = MIG_OK;
+    int g = guarded([&] {
+        std::function<void(int, int, int, int)> tr = nullptr;
+        if (trace) tr = [&](int a, int b, int c, int d) { trace(user, a, b, c, d); };
+        auto plan = mcts_solve(*ctx->e, comp_of(ctx, comp, n), mcts_of(params), seed, tr);
+        rc = emit(plan, out, cap, n_out);
+    });
+    return g != MIG_OK ? g : rc;
+}
+
+void mig_ga_params_defaults(mig_ga_params* out) {
+    GaParams g;
+    std::memset(out, 0, sizeof *out);
+    out->population = g.population;
+    out->erase_fraction = g.erase_fraction;
+    out->mutation_pairs = g.mutation_pairs;
+    out->stall_rounds = g.stall_rounds;
+    out->time_budget_s = g.time_budget_s;
+    out->seed = g.seed;
+    out->max_rounds = g.max_rounds;
+    out->workers = g.workers;
+    out->slow = mig_mcts_params{g.slow.budget_iters, g.slow.topk, g.slow.pick_services, g.slow.ucb_c};
+}
+
+int mig_completion_of(const mig_ctx* ctx, const mig_config* configs, int32_t n_configs, double* comp_out) {
+    return guarded([&] {
+        std::vector<Config> cfgs;
+        for (int i = 0; i < n_configs; ++i) cfgs.push_back(from_c(configs[i], ctx->e->n()));
+        auto c = ctx->e->completion_of(cfgs);
+        for (size_t i = 0; i < c.size(); ++i) comp_out[i] = c[i];
+    });
+}
+
+int mig_mutate(const mig_ctx* ctx, const mig_config* parent, int32_t n_gpus, const mig_ga_params* params, mig_rng* rng,
+               mig_config* child) {
+    return guarded([&] {
+        Chromosome p;
+        for (int i = 0; i < n_gpus; ++i) p.gpus.push_back(from_c(parent[i], ctx->e->n()));
+        p.gpu_count = n_gpus;
+        Chromosome c = mutate(p, ga_of(params), rng->rng);
+        for (size_t i = 0; i < c.gpus.size(); ++i) to_c(c.gpus[i], &child[i]);
+    });
+}
+
+int mig_crossover(mig_ctx* ctx, const mig_config* parent, int32_t n_gpus, int32_t slow_kind,
+                  const mig_ga_params* params, mig_rng* rng, mig_config* child, int32_t cap, int32_t* n_child) {
+    int rc = MIG_OK;
+    int g = guarded([&] {
+        std::vector<Config> gpus;
+        for (int i = 0; i < n_gpus; ++i) gpus.push_back(from_c(parent[i], ctx->e->n()));
+        Chromosome p = gpus.empty() ? Chromosome{} : evaluate_chromosome(gpus, *ctx->e);
+        GaParams gp = ga_of(params);
+        FastProc fast;
+        MctsProc slow(gp.slow);
+        const Procedure& proc = slow_kind == 0 ? static_cast<const Procedure&>(fast) : slow;
+        Chromosome c = crossover(p, proc, *ctx->e, gp, rng->rng);
+        rc = emit(c.gpus, child, cap, n_child);
+    });
+    return g != MIG_OK ? g : rc;
+}
+
+int mig_two_phase(mig_ctx* ctx, const mig_ga_params* params, mig_config* out, int32_t cap, int32_t* n_out,
+                  mig_ga_log_fn log, void* user) {
+    int rc = MIG_OK;
+    int g = guarded([&] {
+        std::function<void(int, int, double, bool, double)> lg = nullptr;
+        if (log) lg = [&](int r, int b, double s, bool imp, double el) { log(user, r, b, s, imp ? 1 : 0, el); };
+        auto plan = two_phase(*ctx->e, ga_of(params), lg);
+        rc = emit(plan, out, cap, n_out);
+    });
+    return g != MIG_OK ? g : rc;
+}
+
+int mig_lower_bound(const mig_ctx* ctx, int32_t* out) {
+    return guarded([&] {  // bench.hpp:93-108 over every constructible size {1,2,3,4,7}
+        const Model& m = ctx->e->model();
+        if (m.n == 0) {
+            *out = 0;
+            return;
+        }
+        double total = 0.0;
+        for (int i = 0; i < m.n; ++i) {
+            const auto& prof = ctx->e->profiles().at(m.services[i].model);
+            double best = 0.0;
+            for (int size : {1, 2, 3, 4, 7}) {
+                auto it = prof.entries.find(size);
+                if (it == prof.entries.end()) continue;
+                const ProfileEntry* sel = nullptr;
+                for (const auto& pe : it->second)
+                    if (pe.p90 <= m.services[i].p90) sel = &pe;
+                if (sel) best = std::max(best, sel->thr / size);
+            }
+            if (best <= 0.0) throw PlanningError("service '" + m.services[i].id + "' has no feasible instance size");
+            total += m.services[i].req / best;
+        }
+        *out = static_cast<int32_t>(std::ceil(total / 7.0 - 1e-9));
+    });
+}
+
+int mig_ctx_stats(const mig_ctx* ctx, mig_stats* out) {
+    std::memset(out, 0, sizeof *out);
+    const Stats& s = ctx->e->stats;
+    out->rows_scored = s.rows_scored.load();
+    out->greedy_steps = s.greedy_steps.load();
+    out->ext_events = s.ext_events.load();
+    out->ext_rows = s.ext_rows.load();
+    out->kernel_launches = s.launches.load();
+    out->scan_ms = s.scan_us.load() / 1000.0;
+    out->topk_ms = s.topk_us.load() / 1000.0;
+    return MIG_OK;
+}
+
+void mig_ctx_reset_stats(mig_ctx* ctx) {
+    Stats& s = ctx->e->stats;
+    s.rows_scored = 0;
+    s.greedy_steps = 0;
+    s.ext_events = 0;
+    s.ext_rows = 0;
+    s.launches = 0;
+    s.scan_us = 0;
+    s.topk_us = 0;
+}
+
+}  // extern "C"

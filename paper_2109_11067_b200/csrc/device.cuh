@@ -1,0 +1,81 @@
+// device.cuh — device-side tables and helpers shared by the sm_100a kernels.
+#pragma once
+
+#include <cstdint>
+
+namespace mgb {
+
+constexpr uint64_t kNoRow = ~0ull;
+
+// Read-only model tables (uploaded once per PlanContext).  See model.hpp for meaning.
+struct DevModel {
+    int n;         // services
+    int PP;        // patterns; row code = svc * PP + pattern, sentinel n * PP
+    int n_sizes;
+    int n_layouts;
+    int max_mix;
+    int n_tmpl[5];           // templates per member count k = 0..4
+    const uint64_t* tmpl[5]; // layout(8) | pat0 << 8 | pat1 << 16 | pat2 << 24 | pat3 << 32
+    const double* U;         // (n+1) * PP utilities, row n zeros
+    const double* best_single;  // n
+    const uint8_t* feas_mask;   // n
+    const uint8_t* pat_mask;    // PP
+    const uint8_t* pat_count;   // PP * 5
+    const uint8_t* layout_count;  // n_layouts * 5
+    const int8_t* layout_slots;   // n_layouts * 5 * 7 (ascending slots per size index)
+    const int* sizes;             // n_sizes (ascending)
+};
+
+// One argmax candidate: score, util_sum, packed row.
+struct Best {
+    double s;
+    double u;
+    uint64_t row;
+};
+
+// Per-call device state of the persistent greedy kernel.
+struct GreedyState {
+    unsigned int bar_count;
+    unsigned int bar_gen;
+    int status;        // 0 ok, 1 no positive score, 2 extension overflow, 3 step overflow
+    int n_steps;
+    unsigned long long ext_count;
+    int n_events;
+    int pad;
+    long long rows_scored;
+};
+
+enum GreedyStatus { kOk = 0, kNoPositive = 1, kExtOverflow = 2, kStepOverflow = 3 };
+
+struct GreedyArgs {
+    DevModel M;
+    const uint64_t* base_rows;
+    long long n_base;
+    uint64_t* ext_rows;
+    long long ext_cap;
+    const double* comp0;
+    GreedyState* st;
+    Best* partials;       // 2 * gridDim.x (double buffered by step parity)
+    uint64_t* pick_row;   // cap_steps
+    double* pick_score;   // cap_steps
+    long long* pick_rows; // rows in the working set at that step
+    int* ev_svc;          // events recorded (service, in order)
+    int cap_steps;
+};
+
+struct TopkArgs {
+    DevModel M;
+    const uint64_t* rows;     // base rows
+    long long n_rows;
+    const long long* index;   // optional: candidate indices to consider (NULL: all rows)
+    long long n_index;
+    const uint64_t* svc_mask; // optional: 4 words; a row qualifies if any member is in the mask
+    const double* comp;
+    int k;
+    unsigned int* bar;        // 2 words
+    Best* partials;           // 2 * gridDim.x
+    uint64_t* out_row;        // k
+    int* n_out;
+};
+
+}  // namespace mgb

@@ -1,0 +1,475 @@
+// engine.cu — device memory, launches and per-call slots for one PlanContext.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstdlib>
+#include <cstring>
+#include <functional>
+
+#include "engine.hpp"
+
+namespace mgb {
+
+size_t greedy_smem_bytes(int n, int PP);
+size_t topk_smem_bytes(int n, int PP);
+const void* greedy_kernel_ptr();
+const void* topk_kernel_ptr();
+const void* enum_base_kernel_ptr();
+int kernel_threads();
+
+namespace {
+
+void ck(cudaError_t e, const char* what) {
+    if (e != cudaSuccess) throw DeviceError(std::string(what) + ": " + cudaGetErrorString(e));
+}
+#define CK(x) ck((x), #x)
+
+template <class T>
+T* dalloc(std::vector<void*>& owned, size_t count) {
+    void* p = nullptr;
+    CK(cudaMalloc(&p, std::max<size_t>(count, 1) * sizeof(T)));
+    owned.push_back(p);
+    return static_cast<T*>(p);
+}
+
+template <class T>
+T* upload(std::vector<void*>& owned, const std::vector<T>& v) {
+    T* p = dalloc<T>(owned, v.size());
+    if (!v.empty()) CK(cudaMemcpy(p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice));
+    return p;
+}
+
+long long binom(long long a, int k) {
+    if (k < 0 || a < k) return 0;
+    long long r = 1;
+    for (int i = 1; i <= k; ++i) r = r * (a - k + i) / i;
+    return r;
+}
+
+}  // namespace
+
+struct Slot {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    uint64_t* ext = nullptr;
+    long long ext_cap = 0;
+    GreedyState* st = nullptr;
+    Best* partials = nullptr;
+    int cap_steps = 0;
+    uint64_t* pick_row = nullptr;
+    double* pick_score = nullptr;
+    long long* pick_rows = nullptr;
+    int* ev_svc = nullptr;
+    double* comp = nullptr;
+    // top-K scratch
+    unsigned* bar = nullptr;
+    uint64_t* out_row = nullptr;
+    int* n_out = nullptr;
+    long long* index = nullptr;
+    long long index_cap = 0;
+    uint64_t* mask = nullptr;
+    // pinned host staging
+    GreedyState* h_st = nullptr;
+
+    ~Slot() {
+        cudaSetDevice(device);
+        if (stream) cudaStreamSynchronize(stream);
+        for (void* p : {(void*)ext, (void*)st, (void*)partials, (void*)pick_row, (void*)pick_score,
+                        (void*)pick_rows, (void*)ev_svc, (void*)comp, (void*)bar, (void*)out_row, (void*)n_out,
+                        (void*)index, (void*)mask})
+            if (p) cudaFree(p);
+        if (h_st) cudaFreeHost(h_st);
+        if (e0) cudaEventDestroy(e0);
+        if (e1) cudaEventDestroy(e1);
+        if (stream) cudaStreamDestroy(stream);
+    }
+};
+
+bool config_less(const Config& a, const Config& b) {  // GpuConfig operator<, core.hpp:199
+    const int m = std::min(a.n, b.n);
+    for (int i = 0; i < m; ++i) {
+        const auto& x = a.inst[i];
+        const auto& y = b.inst[i];
+        if (x.slices != y.slices) return x.slices < y.slices;
+        if (x.slot != y.slot) return x.slot < y.slot;
+        if (x.svc != y.svc) return x.svc < y.svc;
+        if (x.batch != y.batch) return x.batch < y.batch;
+    }
+    return a.n < b.n;
+}
+
+bool config_equal(const Config& a, const Config& b) { return !config_less(a, b) && !config_less(b, a); }
+
+Engine::Engine(const Rules& rules, std::map<std::string, ModelProfile> profiles, std::vector<Service> services,
+               int max_mix, int device)
+    : profiles_(std::move(profiles)), device_(device) {
+    for (const auto& [name, p] : profiles_) validate_profile(p);
+    m_ = build_model(rules, profiles_, services, max_mix);
+
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+        throw DeviceError("no CUDA device available: the B200 planner has no CPU fallback");
+    if (device < 0 || device >= ndev) throw DeviceError("CUDA device index out of range");
+    CK(cudaSetDevice(device));
+    cudaDeviceProp prop{};
+    CK(cudaGetDeviceProperties(&prop, device));
+    if (prop.major < 10) throw DeviceError(std::string("device ") + prop.name + " is not sm_100-class (B200)");
+    num_sms_ = prop.multiProcessorCount;
+
+    const int T = kernel_threads();
+    const size_t gsm = greedy_smem_bytes(m_.n, m_.PP), tsm = topk_smem_bytes(m_.n, m_.PP);
+    CK(cudaFuncSetAttribute(greedy_kernel_ptr(), cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(gsm)));
+    CK(cudaFuncSetAttribute(topk_kernel_ptr(), cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(tsm)));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&greedy_blocks_per_sm_, greedy_kernel_ptr(), T, gsm));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&topk_blocks_per_sm_, topk_kernel_ptr(), T, tsm));
+    if (greedy_blocks_per_sm_ < 1 || topk_blocks_per_sm_ < 1) throw DeviceError("kernel does not fit on an SM");
+
+    // ---- device model tables
+    dm_.n = m_.n;
+    dm_.PP = m_.PP;
+    dm_.n_sizes = static_cast<int>(m_.sizes.size());
+    dm_.n_layouts = static_cast<int>(m_.layouts.size());
+    dm_.max_mix = m_.max_mix;
+    for (int k = 0; k <= kRowK; ++k) {
+        std::vector<uint64_t> t;
+        for (const auto& tp : m_.templates[k]) {
+            uint64_t v = static_cast<uint64_t>(tp.layout);
+            for (int j = 0; j < kRowK; ++j) v |= static_cast<uint64_t>(tp.pat[j]) << (8 * (j + 1));
+            t.push_back(v);
+        }
+        dm_.n_tmpl[k] = static_cast<int>(t.size());
+        dm_.tmpl[k] = upload(dev_allocs_, t);
+    }
+    dm_.U = upload(dev_allocs_, m_.U);
+    dm_.best_single = upload(dev_allocs_, m_.best_single);
+    dm_.feas_mask = upload(dev_allocs_, m_.feas_mask);
+    dm_.pat_mask = upload(dev_allocs_, m_.pat_mask);
+    std::vector<uint8_t> pc(static_cast<size_t>(m_.PP) * 5, 0), lc(m_.layouts.size() * 5, 0);
+    std::vector<int8_t> ls(m_.layouts.size() * 5 * 7, -1);
+    for (int p = 0; p < m_.PP; ++p)
+        for (int s = 0; s < kMaxSizes; ++s) pc[p * 5 + s] = m_.patterns[p][s];
+    for (size_t l = 0; l < m_.layouts.size(); ++l) {
+        for (int s = 0; s < kMaxSizes; ++s) lc[l * 5 + s] = m_.layouts[l].count[s];
+        for (const auto& g : m_.layouts[l].groups)
+            for (size_t t = 0; t < g.slots.size() && t < 7; ++t)
+                ls[(l * 5 + g.size_idx) * 7 + t] = static_cast<int8_t>(g.slots[t]);
+    }
+    dm_.pat_count = upload(dev_allocs_, pc);
+    dm_.layout_count = upload(dev_allocs_, lc);
+    dm_.layout_slots = upload(dev_allocs_, ls);
+    dm_.sizes = upload(dev_allocs_, m_.sizes);
+
+    // ---- K1: base pool (all supports with 1..max_mix members), deterministic order
+    std::vector<uint32_t> supports;
+    std::vector<long long> offsets;
+    long long total = 0;
+    std::vector<int> s(kRowK);
+    for (int k = 1; k <= max_mix; ++k) {
+        std::function<void(int, int)> rec = [&](int from, int d) {
+            if (d == k) {
+                long long c = m_.rows_for_support(s.data(), k);
+                if (c == 0) return;
+                uint32_t packed = 0xFFFFFFFFu;
+                for (int j = 0; j < k; ++j) packed = (packed & ~(0xFFu << (8 * j))) | (uint32_t(s[j]) << (8 * j));
+                supports.push_back(packed);
+                offsets.push_back(total);
+                total += c;
+                return;
+            }
+            for (int v = from; v < m_.n; ++v) {
+                s[d] = v;
+                rec(v + 1, d + 1);
+            }
+        };
+        rec(0, 0);
+    }
+    d_base_ = dalloc<uint64_t>(dev_allocs_, static_cast<size_t>(total) + 2);
+    if (!supports.empty()) {
+        uint32_t* d_sup = dalloc<uint32_t>(dev_allocs_, supports.size());
+        long long* d_off = dalloc<long long>(dev_allocs_, offsets.size());
+        CK(cudaMemcpy(d_sup, supports.data(), supports.size() * 4, cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(d_off, offsets.data(), offsets.size() * 8, cudaMemcpyHostToDevice));
+        int n_sup = static_cast<int>(supports.size());
+        int threads = 256;
+        int blocks = static_cast<int>((static_cast<long long>(n_sup) * 32 + threads - 1) / threads);
+        void* args[] = {&dm_, &d_sup, &d_off, &n_sup, &d_base_};
+        CK(cudaLaunchKernel(enum_base_kernel_ptr(), blocks, threads, args, 0, nullptr));
+        stats.launches++;
+        CK(cudaGetLastError());
+        CK(cudaDeviceSynchronize());
+    }
+    base_rows_.resize(static_cast<size_t>(total));
+    if (total) CK(cudaMemcpy(base_rows_.data(), d_base_, total * 8, cudaMemcpyDeviceToHost));
+    row_index_.reserve(base_rows_.size() * 2);
+    for (size_t i = 0; i < base_rows_.size(); ++i) row_index_.emplace(base_rows_[i], static_cast<long long>(i));
+
+    min_u_.assign(m_.n, 0.0);
+    for (int i = 0; i < m_.n; ++i) {
+        double mu = 0.0;
+        for (int p = 0; p < m_.PP; ++p) {
+            double u = m_.U[static_cast<size_t>(i) * m_.PP + p];
+            if (u > 0.0 && (mu == 0.0 || u < mu)) mu = u;
+        }
+        min_u_[i] = mu;
+    }
+    // extension arena bound: every support with max_mix < |S| <= 4 (all templates).
+    long double eb = 0;
+    for (int k = max_mix + 1; k <= kRowK; ++k) eb += static_cast<long double>(binom(m_.n, k)) * m_.templates[k].size();
+    ext_bound_ = static_cast<long long>(std::min<long double>(eb, 1ll << 31)) + 64;
+}
+
+Engine::~Engine() {
+    cudaSetDevice(device_);
+    slots_.clear();
+    for (void* p : dev_allocs_) cudaFree(p);
+}
+
+long long Engine::index_of(uint64_t row) const {
+    auto it = row_index_.find(row);
+    if (it == row_index_.end()) throw ArgumentError("row not in the base pool");
+    return it->second;
+}
+
+Config Engine::config_of(uint64_t row) const {
+    Config c;
+    c.n = m_.decode(row, c.inst);
+    return c;
+}
+
+Slot* Engine::acquire() {
+    {
+        std::lock_guard<std::mutex> g(mu_);
+        if (!free_.empty()) {
+            Slot* s = free_.back();
+            free_.pop_back();
+            return s;
+        }
+    }
+    CK(cudaSetDevice(device_));
+    auto s = std::make_unique<Slot>();
+    s->device = device_;
+    CK(cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking));
+    CK(cudaEventCreate(&s->e0));
+    CK(cudaEventCreate(&s->e1));
+    CK(cudaMalloc(&s->st, sizeof(GreedyState)));
+    CK(cudaMalloc(&s->partials, sizeof(Best) * 2 * num_sms_ * std::max(greedy_blocks_per_sm_, topk_blocks_per_sm_)));
+    CK(cudaMalloc(&s->ev_svc, sizeof(int) * (m_.n + 1)));
+    CK(cudaMalloc(&s->comp, sizeof(double) * (m_.n + 1)));
+    CK(cudaMalloc(&s->bar, sizeof(unsigned) * 2));
+    CK(cudaMemset(s->bar, 0, sizeof(unsigned) * 2));
+    CK(cudaMalloc(&s->out_row, sizeof(uint64_t) * 1024));
+    CK(cudaMalloc(&s->n_out, sizeof(int)));
+    CK(cudaMalloc(&s->mask, sizeof(uint64_t) * 4));
+    CK(cudaMallocHost(&s->h_st, sizeof(GreedyState)));
+    Slot* raw = s.get();
+    std::lock_guard<std::mutex> g2(mu_);
+    slots_.push_back(std::move(s));
+    return raw;
+}
+
+void Engine::release(Slot* s) {
+    std::lock_guard<std::mutex> g(mu_);
+    free_.push_back(s);
+}
+
+void Engine::ensure_ext(Slot* s, long long rows) {
+    if (s->ext_cap >= rows) return;
+    if (s->ext) CK(cudaFree(s->ext));
+    s->ext = nullptr;
+    CK(cudaMalloc(&s->ext, static_cast<size_t>(rows + 2) * sizeof(uint64_t)));
+    s->ext_cap = rows;
+}
+
+long long Engine::step_bound(const std::vector<double>& comp) const {
+    long long b = 1;
+    for (int i = 0; i < m_.n; ++i) {
+        double need = 1.0 - comp[i];
+        if (need <= 0.0 || min_u_[i] <= 0.0) continue;
+        b += static_cast<long long>(std::ceil(need / min_u_[i])) + 1;
+    }
+    return b;
+}
+
+void Engine::fast_algo(const std::vector<double>& comp, std::vector<uint64_t>& rows, std::vector<double>& scores) {
+    rows.clear();
+    scores.clear();
+    if (static_cast<int>(comp.size()) != m_.n) throw PlanningError("fast_algo: completion vector length mismatch");
+    bool sat = true;
+    for (double c : comp)
+        if (c < 1.0 - kSatisfyEps) sat = false;
+    if (sat) return;  // greedy.hpp:101
+
+    Slot* s = acquire();
+    struct Rel {
+        Engine* e;
+        Slot* s;
+        ~Rel() { e->release(s); }
+    } rel{this, s};
+    CK(cudaSetDevice(device_));
+    long long cap_steps = std::min<long long>(step_bound(comp), 1 << 24);
+    if (s->cap_steps < cap_steps) {
+        for (void* p : {(void*)s->pick_row, (void*)s->pick_score, (void*)s->pick_rows})
+            if (p) CK(cudaFree(p));
+        CK(cudaMalloc(&s->pick_row, sizeof(uint64_t) * cap_steps));
+        CK(cudaMalloc(&s->pick_score, sizeof(double) * cap_steps));
+        CK(cudaMalloc(&s->pick_rows, sizeof(long long) * cap_steps));
+        s->cap_steps = static_cast<int>(cap_steps);
+    }
+    long long want_ext = std::min<long long>(ext_bound_, std::max<long long>(s->ext_cap, 1 << 20));
+    ensure_ext(s, want_ext);
+
+    const int T = kernel_threads();
+    const size_t smem = greedy_smem_bytes(m_.n, m_.PP);
+    int G = num_sms_ * greedy_blocks_per_sm_;
+    if (const char* e = std::getenv("MIGPLAN_GREEDY_CTAS")) G = std::max(1, std::min(G, std::atoi(e)));
+
+    for (int attempt = 0;; ++attempt) {
+        CK(cudaMemcpyAsync(s->comp, comp.data(), sizeof(double) * m_.n, cudaMemcpyHostToDevice, s->stream));
+        CK(cudaMemsetAsync(s->st, 0, sizeof(GreedyState), s->stream));
+        GreedyArgs a{};
+        a.M = dm_;
+        a.base_rows = d_base_;
+        a.n_base = static_cast<long long>(base_rows_.size());
+        a.ext_rows = s->ext;
+        a.ext_cap = s->ext_cap;
+        a.comp0 = s->comp;
+        a.st = s->st;
+        a.partials = s->partials;
+        a.pick_row = s->pick_row;
+        a.pick_score = s->pick_score;
+        a.pick_rows = s->pick_rows;
+        a.ev_svc = s->ev_svc;
+        a.cap_steps = s->cap_steps;
+        void* args[] = {&a};
+        CK(cudaEventRecord(s->e0, s->stream));
+        CK(cudaLaunchCooperativeKernel(greedy_kernel_ptr(), G, T, args, smem, s->stream));
+        stats.launches++;
+        CK(cudaEventRecord(s->e1, s->stream));
+        CK(cudaMemcpyAsync(s->h_st, s->st, sizeof(GreedyState), cudaMemcpyDeviceToHost, s->stream));
+        CK(cudaStreamSynchronize(s->stream));
+        float ms = 0.f;
+        CK(cudaEventElapsedTime(&ms, s->e0, s->e1));
+        stats.scan_us += static_cast<long long>(ms * 1000.0f);
+        const GreedyState h = *s->h_st;
+        if (h.status == kExtOverflow && attempt < 4) {
+            long long need = static_cast<long long>(h.ext_count) * 2 + (1 << 20);
+            ensure_ext(s, std::max(need, s->ext_cap * 2));
+            continue;
+        }
+        if (h.status == kExtOverflow) throw DeviceError("extension arena overflow");
+        if (h.status == kStepOverflow) throw DeviceError("greedy step buffer overflow");
+        rows.resize(h.n_steps);
+        scores.resize(h.n_steps);
+        if (h.n_steps) {
+            CK(cudaMemcpyAsync(rows.data(), s->pick_row, sizeof(uint64_t) * h.n_steps, cudaMemcpyDeviceToHost,
+                               s->stream));
+            CK(cudaMemcpyAsync(scores.data(), s->pick_score, sizeof(double) * h.n_steps, cudaMemcpyDeviceToHost,
+                               s->stream));
+            CK(cudaStreamSynchronize(s->stream));
+        }
+        stats.rows_scored += h.rows_scored;
+        stats.greedy_steps += h.n_steps;
+        stats.ext_events += h.n_events;
+        stats.ext_rows += static_cast<long long>(h.ext_count);
+        if (h.status == kNoPositive)
+            throw PlanningError("fast_algo: no config with positive score while services remain unsatisfied");
+        return;
+    }
+}
+
+std::vector<long long> Engine::topk(const std::vector<double>& comp, int k, const std::vector<long long>* index,
+                                    const std::vector<uint64_t>* svc_mask) {
+    if (static_cast<int>(comp.size()) != m_.n) throw PlanningError("completion vector length mismatch");
+    std::vector<long long> out;
+    if (k <= 0) return out;
+    k = std::min(k, 1024);
+    const long long total = index ? static_cast<long long>(index->size()) : pool_size();
+    if (total == 0) return out;
+    Slot* s = acquire();
+    struct Rel {
+        Engine* e;
+        Slot* s;
+        ~Rel() { e->release(s); }
+    } rel{this, s};
+    CK(cudaSetDevice(device_));
+    CK(cudaMemcpyAsync(s->comp, comp.data(), sizeof(double) * m_.n, cudaMemcpyHostToDevice, s->stream));
+    if (index) {
+        if (s->index_cap < total) {
+            if (s->index) CK(cudaFree(s->index));
+            CK(cudaMalloc(&s->index, sizeof(long long) * total));
+            s->index_cap = total;
+        }
+        CK(cudaMemcpyAsync(s->index, index->data(), sizeof(long long) * total, cudaMemcpyHostToDevice, s->stream));
+    }
+    if (svc_mask) CK(cudaMemcpyAsync(s->mask, svc_mask->data(), sizeof(uint64_t) * 4, cudaMemcpyHostToDevice, s->stream));
+    TopkArgs a{};
+    a.M = dm_;
+    a.rows = d_base_;
+    a.n_rows = pool_size();
+    a.index = index ? s->index : nullptr;
+    a.n_index = index ? total : 0;
+    a.svc_mask = svc_mask ? s->mask : nullptr;
+    a.comp = s->comp;
+    a.k = k;
+    a.bar = s->bar;
+    a.partials = s->partials;
+    a.out_row = s->out_row;
+    a.n_out = s->n_out;
+    const int T = kernel_threads();
+    int G = static_cast<int>(std::min<long long>((total + 4 * T - 1) / (4 * T), num_sms_ * topk_blocks_per_sm_));
+    G = std::max(G, 1);
+    void* args[] = {&a};
+    CK(cudaEventRecord(s->e0, s->stream));
+    CK(cudaLaunchCooperativeKernel(topk_kernel_ptr(), G, T, args, topk_smem_bytes(m_.n, m_.PP), s->stream));
+    stats.launches++;
+    CK(cudaEventRecord(s->e1, s->stream));
+    int got = 0;
+    CK(cudaMemcpyAsync(&got, s->n_out, sizeof(int), cudaMemcpyDeviceToHost, s->stream));
+    CK(cudaStreamSynchronize(s->stream));
+    std::vector<uint64_t> rows(got);
+    if (got) {
+        CK(cudaMemcpyAsync(rows.data(), s->out_row, sizeof(uint64_t) * got, cudaMemcpyDeviceToHost, s->stream));
+        CK(cudaStreamSynchronize(s->stream));
+    }
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, s->e0, s->e1));
+    stats.topk_us += static_cast<long long>(ms * 1000.0f);
+    stats.rows_scored += total * std::max(got, 1);
+    for (uint64_t r : rows) out.push_back(index_of(r));
+    return out;
+}
+
+// completion_of / detail::sum_rates (core.hpp:245-269): counts keyed by (svc, size, batch)
+// in key order, total += count * thr, one division per service.
+std::vector<double> Engine::completion_of(const std::vector<Config>& cfgs) const {
+    std::map<std::tuple<int, int, int>, long long> counts;
+    for (const auto& c : cfgs)
+        for (int k = 0; k < c.n; ++k) {
+            const auto& in = c.inst[k];
+            if (in.svc < 0 || in.svc >= m_.n) throw PlanningError("unknown service index in configuration");
+            counts[{in.svc, in.slices, in.batch}] += 1;
+        }
+    std::vector<double> total(m_.n, 0.0);
+    for (const auto& [key, count] : counts) {
+        auto [idx, size, batch] = key;
+        const auto& prof = profiles_.at(m_.services[idx].model);
+        const ProfileEntry* e = nullptr;
+        auto it = prof.entries.find(size);
+        if (it != prof.entries.end())
+            for (const auto& pe : it->second)
+                if (pe.batch == batch) e = &pe;
+        if (!e)
+            throw PlanningError("profile '" + m_.services[idx].model + "' has no entry for size " +
+                                std::to_string(size) + " batch " + std::to_string(batch));
+        volatile double prod = static_cast<double>(count) * e->thr;
+        total[idx] = total[idx] + prod;
+    }
+    std::vector<double> out(m_.n);
+    for (int i = 0; i < m_.n; ++i) out[i] = total[i] / m_.services[i].req;
+    return out;
+}
+
+}  // namespace mgb

@@ -1,0 +1,90 @@
+// engine.hpp — the native runtime behind the C-ABI: one PlanContext on one B200.
+//
+// Owns the device-resident tables (model + packed base pool), a pool of per-call
+// "slots" (stream, extension arena, step buffers) so that concurrent GA workers can
+// run independent greedy / top-K calls on one context (the reference's functions are
+// reentrant over a const PlanContext, ga.hpp:153-163), and the host-side search
+// drivers (MCTS, GA) that call the kernels.
+#pragma once
+
+#include <atomic>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include "device.cuh"
+#include "model.hpp"
+
+namespace mgb {
+
+struct Config {  // normalized GpuConfig with service indices (mig_config)
+    int n = 0;
+    Model::Inst inst[kMaxInst];
+};
+
+bool config_less(const Config& a, const Config& b);
+bool config_equal(const Config& a, const Config& b);
+
+struct Slot;
+
+struct Stats {
+    std::atomic<long long> rows_scored{0}, greedy_steps{0}, ext_events{0}, ext_rows{0}, launches{0};
+    std::atomic<long long> scan_us{0}, topk_us{0};
+};
+
+class Engine {
+  public:
+    Engine(const Rules& rules, std::map<std::string, ModelProfile> profiles, std::vector<Service> services,
+           int max_mix, int device);
+    ~Engine();
+
+    const Model& model() const { return m_; }
+    int n() const { return m_.n; }
+    const std::vector<uint64_t>& base_rows() const { return base_rows_; }
+    long long pool_size() const { return static_cast<long long>(base_rows_.size()); }
+    long long index_of(uint64_t row) const;
+    Config config_of(uint64_t row) const;
+
+    // fast_algo (greedy.hpp:95-145) on the device.  Returns picked rows and their scores.
+    void fast_algo(const std::vector<double>& comp, std::vector<uint64_t>& rows, std::vector<double>& scores);
+    // topk_candidates (mcts.hpp:56-76) over the base pool; filter by explicit indices or a
+    // service mask (rows touching any masked service).  Returns pool indices, preferred first.
+    std::vector<long long> topk(const std::vector<double>& comp, int k, const std::vector<long long>* index,
+                                const std::vector<uint64_t>* svc_mask);
+
+    // completion_of (core.hpp:291-302), count-based, on the host (control logic, not hot).
+    std::vector<double> completion_of(const std::vector<Config>& cfgs) const;
+    const std::map<std::string, ModelProfile>& profiles() const { return profiles_; }
+
+    Stats stats;
+    int device() const { return device_; }
+
+  private:
+    Slot* acquire();
+    void release(Slot*);
+    void ensure_ext(Slot* s, long long rows);
+    long long step_bound(const std::vector<double>& comp) const;
+
+    Model m_;
+    std::map<std::string, ModelProfile> profiles_;
+    int device_ = 0;
+    int num_sms_ = 0;
+    int greedy_blocks_per_sm_ = 0;
+    int topk_blocks_per_sm_ = 0;
+    DevModel dm_{};
+    std::vector<void*> dev_allocs_;
+    uint64_t* d_base_ = nullptr;
+    std::vector<uint64_t> base_rows_;
+    std::unordered_map<uint64_t, long long> row_index_;
+    std::vector<double> min_u_;  // smallest positive utility per service (step bound)
+    long long ext_bound_ = 0;
+
+    std::mutex mu_;
+    std::vector<std::unique_ptr<Slot>> slots_;
+    std::vector<Slot*> free_;
+};
+
+}  // namespace mgb

@@ -1,0 +1,354 @@
+// search.cpp — MCTS (mcts.hpp) and GA (ga.hpp) drivers; see search.hpp.
+#include "search.hpp"
+
+#include <algorithm>
+#include <chrono>
+#include <exception>
+#include <map>
+#include <thread>
+
+namespace mgb {
+
+std::vector<Config> fast_plan(Engine& e, const std::vector<double>& comp) {
+    std::vector<uint64_t> rows;
+    std::vector<double> scores;
+    e.fast_algo(comp, rows, scores);
+    std::vector<Config> out;
+    out.reserve(rows.size());
+    for (uint64_t r : rows) out.push_back(e.config_of(r));
+    return out;
+}
+
+void add_util(const Engine& e, long long idx, std::vector<double>& comp) {
+    const Model& m = e.model();
+    int svc[kRowK], pat[kRowK];
+    int k = m.members(e.base_rows()[idx], svc, pat);
+    for (int j = 0; j < k; ++j) comp[svc[j]] = comp[svc[j]] + m.U[static_cast<size_t>(svc[j]) * m.PP + pat[j]];
+}
+
+namespace {
+
+std::vector<int> unsatisfied(const std::vector<double>& c) {  // mcts.hpp:78-83
+    std::vector<int> u;
+    for (size_t i = 0; i < c.size(); ++i)
+        if (c[i] < 1.0 - kSatisfyEps) u.push_back(static_cast<int>(i));
+    return u;
+}
+
+std::vector<uint64_t> type_key(const std::vector<double>& c) {  // completion_type_key, mcts.hpp:38-43
+    std::vector<uint64_t> k((c.size() + 63) / 64, 0);
+    for (size_t i = 0; i < c.size(); ++i)
+        if (c[i] < 1.0 - kSatisfyEps) k[i >> 6] |= 1ull << (i & 63);
+    return k;
+}
+
+struct Node {  // SearchNode, mcts.hpp:22-35
+    std::vector<double> comp;
+    bool leaf = false;
+    bool expanded = false;
+    int visits = 0;
+    double value_sum = 0.0;
+    struct Edge {
+        long long cand = -1;
+        std::unique_ptr<Node> node;
+    };
+    std::vector<Edge> children;
+    explicit Node(std::vector<double> c) : comp(std::move(c)) { leaf = satisfied(comp); }
+};
+
+void expand(Engine& e, Node& node, const MctsParams& p, Rng& rng) {
+    std::vector<long long> top = expand_children(e, node.comp, p, rng);
+    node.children.clear();
+    for (long long idx : top) {
+        std::vector<double> child = node.comp;
+        add_util(e, idx, child);
+        node.children.push_back(Node::Edge{idx, std::make_unique<Node>(std::move(child))});
+    }
+    node.expanded = true;
+}
+
+}  // namespace
+
+// expand, mcts.hpp:89-116: partial Fisher-Yates sample of min(5, |unsat|) unsatisfied
+// services; children = top-K over the base rows touching any sampled service.
+std::vector<long long> expand_children(Engine& e, const std::vector<double>& comp, const MctsParams& p, Rng& rng) {
+    if (satisfied(comp)) throw PlanningError("expand: node is already satisfied");
+    std::vector<int> unsat = unsatisfied(comp);
+    size_t take = std::min<size_t>(static_cast<size_t>(std::max(p.pick_services, 0)), unsat.size());
+    for (size_t i = 0; i < take; ++i) {
+        size_t j = i + pick_index(rng, unsat.size() - i);
+        std::swap(unsat[i], unsat[j]);
+    }
+    std::vector<uint64_t> mask(4, 0);
+    for (size_t i = 0; i < take; ++i) mask[unsat[i] >> 6] |= 1ull << (unsat[i] & 63);
+    if (take == 0) return {};
+    return e.topk(comp, p.topk, nullptr, &mask);
+}
+
+// rollout, mcts.hpp:122-143.
+int rollout(Engine& e, const std::vector<double>& comp, const MctsParams& p, RolloutCache& cache, Rng& rng,
+            int max_depth, std::vector<long long>* picked) {
+    std::vector<double> cur = comp;
+    int steps = 0;
+    while (!satisfied(cur)) {
+        if (steps >= max_depth) return max_depth;
+        auto key = type_key(cur);
+        auto it = cache.pools.find(key);
+        if (it == cache.pools.end()) {
+            ++cache.builds;
+            it = cache.pools.emplace(std::move(key), e.topk(cur, p.topk, nullptr, nullptr)).first;
+        }
+        const std::vector<long long>& pool = it->second;
+        if (pool.empty()) throw PlanningError("rollout: no candidate config serves the remaining demand");
+        long long idx = pool[pick_index(rng, pool.size())];
+        add_util(e, idx, cur);
+        if (picked) picked->push_back(idx);
+        ++steps;
+    }
+    return steps;
+}
+
+// mcts_solve, mcts.hpp:148-252.
+std::vector<Config> mcts_solve(Engine& e, const std::vector<double>& comp, const MctsParams& p, uint64_t seed,
+                               const std::function<void(int, int, int, int)>& trace) {
+    if (satisfied(comp)) return {};
+    std::vector<Config> fast_ref = fast_plan(e, comp);
+    if (p.budget_iters <= 0) return fast_ref;
+
+    const int l_ref = static_cast<int>(fast_ref.size());
+    const int max_depth = 2 * l_ref;
+    Rng rng(mix_seed(seed, 0x6d637473));
+    RolloutCache cache;
+    Node root(comp);
+    std::vector<long long> best_path;
+    bool have_best = false;
+
+    auto ucb_pick = [&](Node& node) -> Node::Edge& {
+        double log_n = std::log(std::max(1, node.visits));
+        int pick = -1;
+        double best = -1.0;
+        for (size_t i = 0; i < node.children.size(); ++i) {
+            const Node* c = node.children[i].node.get();
+            if (c->visits == 0) return node.children[i];
+            double mean = c->value_sum / c->visits;
+            double bonus = p.ucb_c * std::sqrt(log_n / c->visits);
+            double v = mean + bonus;
+            if (v > best) {
+                best = v;
+                pick = static_cast<int>(i);
+            }
+        }
+        return node.children[pick];
+    };
+
+    for (int iter = 0; iter < p.budget_iters; ++iter) {
+        std::vector<Node*> path{&root};
+        std::vector<long long> edges;
+        Node* node = &root;
+        while (node->expanded && !node->leaf && !node->children.empty()) {
+            Node::Edge& ed = ucb_pick(*node);
+            edges.push_back(ed.cand);
+            node = ed.node.get();
+            path.push_back(node);
+        }
+        int est;
+        if (node->leaf) {
+            est = 0;
+            if (!have_best || edges.size() < best_path.size()) {
+                best_path = edges;
+                have_best = true;
+            }
+        } else {
+            if (!node->expanded) expand(e, *node, p, rng);
+            if (!node->children.empty()) {
+                size_t pick = pick_index(rng, node->children.size());
+                Node::Edge& ed = node->children[pick];
+                edges.push_back(ed.cand);
+                node = ed.node.get();
+                path.push_back(node);
+            }
+            std::vector<long long> picked;
+            est = rollout(e, node->comp, p, cache, rng, max_depth, &picked);
+            bool complete = node->leaf || static_cast<int>(picked.size()) == est;
+            if (complete && est < max_depth) {
+                std::vector<long long> full = edges;
+                full.insert(full.end(), picked.begin(), picked.end());
+                if (!have_best || full.size() < best_path.size()) {
+                    best_path = std::move(full);
+                    have_best = true;
+                }
+            }
+        }
+        int total_len = static_cast<int>(edges.size()) + est;
+        double reward = total_len > 0 ? std::min(1.0, static_cast<double>(l_ref) / total_len) : 1.0;
+        for (Node* x : path) {
+            x->visits += 1;
+            x->value_sum += reward;
+        }
+        if (trace) trace(iter, static_cast<int>(edges.size()), est, have_best ? static_cast<int>(best_path.size()) : -1);
+    }
+
+    std::vector<long long> descent;
+    Node* node = &root;
+    while (node->expanded && !node->leaf && !node->children.empty()) {
+        int pick = 0;
+        for (size_t i = 1; i < node->children.size(); ++i)
+            if (node->children[i].node->visits > node->children[pick].node->visits) pick = static_cast<int>(i);
+        descent.push_back(node->children[pick].cand);
+        node = node->children[pick].node.get();
+    }
+    std::vector<Config> via_descent;
+    for (long long idx : descent) via_descent.push_back(e.config_of(e.base_rows()[idx]));
+    if (!node->leaf)
+        for (auto& c : fast_plan(e, node->comp)) via_descent.push_back(c);
+
+    std::vector<Config> answer = std::move(fast_ref);
+    if (via_descent.size() < answer.size()) answer = std::move(via_descent);
+    if (have_best && best_path.size() < answer.size()) {
+        answer.clear();
+        for (long long idx : best_path) answer.push_back(e.config_of(e.base_rows()[idx]));
+    }
+    return answer;
+}
+
+namespace {
+double slack_of(const std::vector<double>& c) {  // core.hpp:232-236
+    double s = 0.0;
+    for (double v : c) s += std::max(0.0, v - 1.0);
+    return s;
+}
+bool fitter(const Chromosome& a, const Chromosome& b) {  // ga.hpp:19-22
+    if (a.gpu_count != b.gpu_count) return a.gpu_count < b.gpu_count;
+    return a.slack < b.slack;
+}
+}  // namespace
+
+Chromosome evaluate_chromosome(std::vector<Config> gpus, const Engine& e) {  // ga.hpp:38-46
+    Chromosome c;
+    std::vector<double> comp = e.completion_of(gpus);
+    if (!satisfied(comp)) throw PlanningError("chromosome violates the deployment validity invariant");
+    c.slack = slack_of(comp);
+    c.gpu_count = static_cast<int>(gpus.size());
+    c.gpus = std::move(gpus);
+    return c;
+}
+
+// crossover, ga.hpp:51-77.
+Chromosome crossover(const Chromosome& parent, const Procedure& slow, Engine& e, const GaParams& p, Rng& rng) {
+    size_t n = parent.gpus.size();
+    size_t erase = n == 0 ? 0 : static_cast<size_t>(std::ceil(p.erase_fraction * static_cast<double>(n)));
+    if (erase == 0) return parent;
+    std::vector<size_t> order(n);
+    for (size_t i = 0; i < n; ++i) order[i] = i;
+    for (size_t i = 0; i < erase; ++i) {
+        size_t j = i + pick_index(rng, n - i);
+        std::swap(order[i], order[j]);
+    }
+    std::vector<bool> erased(n, false);
+    for (size_t i = 0; i < erase; ++i) erased[order[i]] = true;
+    std::vector<Config> survivors;
+    survivors.reserve(n);
+    for (size_t i = 0; i < n; ++i)
+        if (!erased[i]) survivors.push_back(parent.gpus[i]);
+    try {
+        std::vector<double> residual = e.completion_of(survivors);
+        std::vector<Config> refill = slow.solve(residual, e, rng);
+        for (auto& c : refill) survivors.push_back(c);
+        return evaluate_chromosome(std::move(survivors), e);
+    } catch (const PlanningError&) {
+        return parent;
+    }
+}
+
+// mutate, ga.hpp:83-113: swap (service, batch) of equal-size instances.
+Chromosome mutate(const Chromosome& parent, const GaParams& p, Rng& rng) {
+    Chromosome child = parent;
+    struct Ref {
+        size_t gpu, inst;
+    };
+    std::map<int, std::vector<Ref>> by_size;
+    for (size_t g = 0; g < child.gpus.size(); ++g)
+        for (int k = 0; k < child.gpus[g].n; ++k) by_size[child.gpus[g].inst[k].slices].push_back(Ref{g, size_t(k)});
+    std::vector<int> sizes;
+    for (const auto& [size, refs] : by_size)
+        if (refs.size() >= 2) sizes.push_back(size);
+    if (sizes.empty()) return child;
+    for (int pair = 0; pair < p.mutation_pairs; ++pair) {
+        for (int attempt = 0; attempt < 64; ++attempt) {
+            int size = sizes[pick_index(rng, sizes.size())];
+            const auto& refs = by_size[size];
+            Ref a = refs[pick_index(rng, refs.size())];
+            Ref b = refs[pick_index(rng, refs.size())];
+            auto& ia = child.gpus[a.gpu].inst[a.inst];
+            auto& ib = child.gpus[b.gpu].inst[b.inst];
+            if (ia.svc == ib.svc) continue;
+            std::swap(ia.svc, ib.svc);
+            std::swap(ia.batch, ib.batch);
+            break;
+        }
+    }
+    return child;
+}
+
+std::vector<Config> sorted_deployment(std::vector<Config> cfgs) {  // make_deployment, core.hpp:305-312
+    std::sort(cfgs.begin(), cfgs.end(), config_less);
+    return cfgs;
+}
+
+// two_phase, ga.hpp:126-179 (on an existing max_mix-2 context).
+std::vector<Config> two_phase(Engine& e, const GaParams& p,
+                              const std::function<void(int, int, double, bool, double)>& log) {
+    auto t0 = std::chrono::steady_clock::now();
+    auto elapsed = [&] { return std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count(); };
+    std::vector<Config> seed_cfg = fast_plan(e, std::vector<double>(e.n(), 0.0));
+    if (p.time_budget_s <= 0.0 || p.max_rounds <= 0) return sorted_deployment(std::move(seed_cfg));
+
+    std::vector<Chromosome> pop;
+    pop.push_back(evaluate_chromosome(std::move(seed_cfg), e));
+    Chromosome best = pop[0];
+    MctsProc slow(p.slow);
+    int stall = 0;
+    for (int round = 1; round <= p.max_rounds; ++round) {
+        if (elapsed() >= p.time_budget_s) break;
+        if (stall >= p.stall_rounds) break;
+        size_t n_parents = std::min(pop.size(), (static_cast<size_t>(p.population) + 1) / 2);
+        std::vector<Chromosome> children(n_parents);
+        std::vector<std::exception_ptr> errs(n_parents);
+        auto work = [&](size_t i) {
+            try {
+                Rng rng(mix_seed(p.seed, (static_cast<uint64_t>(round) << 20) + i));
+                Chromosome c = mutate(pop[i], p, rng);
+                children[i] = crossover(c, slow, e, p, rng);
+            } catch (...) {
+                errs[i] = std::current_exception();
+            }
+        };
+        if (p.workers > 1 && n_parents > 1) {
+            std::vector<std::thread> threads;
+            size_t w = std::min<size_t>(static_cast<size_t>(p.workers), n_parents);
+            for (size_t t = 0; t < w; ++t)
+                threads.emplace_back([&, t] {
+                    for (size_t i = t; i < n_parents; i += w) work(i);
+                });
+            for (auto& th : threads) th.join();
+        } else {
+            for (size_t i = 0; i < n_parents; ++i) work(i);
+        }
+        for (auto& ep : errs)
+            if (ep) std::rethrow_exception(ep);
+        for (auto& c : children) pop.push_back(std::move(c));
+        std::stable_sort(pop.begin(), pop.end(), fitter);
+        if (pop.size() > static_cast<size_t>(p.population)) pop.resize(p.population);
+        bool improved = fitter(pop[0], best);
+        if (improved) {
+            best = pop[0];
+            stall = 0;
+        } else {
+            ++stall;
+        }
+        if (log) log(round, best.gpu_count, best.slack, improved, elapsed());
+    }
+    return sorted_deployment(std::move(best.gpus));
+}
+
+}  // namespace mgb

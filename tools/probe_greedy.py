@@ -1,0 +1,30 @@
+"""Quick timing probe of the product greedy on golden workloads (development aid)."""
+import sys, os, time
+sys.path.insert(0, os.path.join(os.path.dirname(os.path.abspath(__file__)), "..", "tests"))
+import support as S
+from support import mp
+
+def main():
+    gold = S.load_golden("greedy.json")
+    names = sys.argv[1:] or ["slos_day", "slos_24", "gen24_6.35", "gen24_8.0", "gen24_8.7"]
+    for name in names:
+        if name not in gold: continue
+        g = gold[name]
+        sv = [mp.ServiceSpec(i, m, float.fromhex(r), float.fromhex(p)) for i, m, r, p in g["services"]]
+        ps = S.profiles() if g["store"] == "fixture" else S.two_model_store()
+        t0 = time.perf_counter()
+        ctx = mp.make_plan_context(sv, ps, mp.PartitionRuleSet.defaults())
+        t1 = time.perf_counter()
+        for rep in range(3):
+            ctx.reset_stats()
+            t2 = time.perf_counter()
+            plan = mp.fast_algo(mp.zero_completion(len(sv)), ctx)
+            t3 = time.perf_counter()
+        st = ctx.stats()
+        ok = S.plan_key(plan) == g["plan"]
+        print(f"{name}: ctx {1e3*(t1-t0):.1f} ms, plan {1e3*(t3-t2):.2f} ms, GPUs {len(plan)} (ref {len(g['plan'])}), "
+              f"match={ok}, rows {st['rows_scored']} (ref {g['rows_scored']}), kernel {st['scan_ms']:.2f} ms, "
+              f"rate {st['rows_scored']/max(st['scan_ms'],1e-9)/1e6:.2f} Grows/s, ref wall {g['ref_wall_s']} s", flush=True)
+
+if __name__ == "__main__":
+    main()
