@@ -29,3 +29,19 @@ def pytest_collection_modifyitems(config, items):
     for it in items:
         if "gpu" in it.keywords:
             it.add_marker(skip)
+
+
+IMPLS = [pytest.param("product", marks=pytest.mark.gpu), "oracle", "reference"]
+
+
+@pytest.fixture(params=IMPLS)
+def impl(request):
+    """Backend under test: the B200 product, the CPU restatement, or the compiled reference."""
+    import support as S
+
+    if request.param == "product":
+        return S.product_backend()
+    b = S.oracle_backend() if request.param == "oracle" else S.ref_backend()
+    if b is None:
+        pytest.skip(f"{request.param} library not built")
+    return b
