@@ -1,0 +1,334 @@
+"""bench.py — MIG-SERVING optimizer hot path on B200 (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl product|reference] [--workload NAME]
+
+Metric: candidate configs scored per second (BASELINE.json "candidate configs scored/sec
+and end-to-end plan time ... GPUs used").  A STEP is one pass of the optimizer over one
+workload: by default config #2 of BASELINE.json — fixtures/slos_24.json (24 services,
+~100 GPUs), greedy fast_algo seed plan + GA refinement (two_phase, seed 24, max_rounds
+binding, population 16, MCTS slow budget 48 — the reference's own c7 parameters with a
+round cap instead of a wall-clock cap).  "Configs scored" counts, for every
+greedy step, its whole working set and, for every top-K call, its candidate set — the
+same count for every implementation (the oracle counts identical numbers).
+
+value  : rows scored / device time with the context (device tables + base pool) resident,
+         timed per step with CUDA events after torch.cuda.synchronize(), L2 flushed
+         (a 512 MiB write) between steps outside the timed windows, max over ranks.
+e2e    : the same metric through the C-ABI from HOST inputs: each step builds the context
+         from host profiles/services (host->device table upload, base-pool enumeration,
+         base rows copied back) and returns the plan to host memory.
+N > 1  : torchrun, one process per GPU, each rank plans an independent GA island (seed
+         24 + rank) — weak scaling, no data-path collective; ranks barrier + MAX-reduce time.
+--impl reference : the reference's own CPU implementation (oracle/_ref, the unmodified
+         reference headers) on the host cores, rank 0 only, bounded sample (see below).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "tests"))
+
+WORKLOADS = {
+    # name: (description, services source, mode, GA params)
+    "slos24_ga": "fixtures/slos_24.json (24 svc): fast_algo seed + two_phase GA (seed 24, 2 rounds, P=16, MCTS 48)",
+    "slos24_greedy": "fixtures/slos_24.json (24 svc): fast_algo from zero completion",
+    "gen24_8.7_greedy": "gen_workload(24, lognormal mu=8.7, sigma=0.6, seed 4242): fast_algo (~974 GPUs)",
+    "gen48_7.0_greedy": "gen_workload(48, lognormal mu=7.0, sigma=0.6, seed 4242): fast_algo (~372 GPUs)",
+}
+
+
+def load_workload(name, rank=0):
+    import support as S
+
+    ps = S.profiles()
+    if name.startswith("slos24"):
+        sv = S.fixture_services("slos_24", ps)
+    elif name.startswith("gen24_8.7"):
+        ps, sv = S.gen(24, 8.7)
+    elif name.startswith("gen48_7.0"):
+        ps, sv = S.gen(48, 7.0)
+    else:
+        raise SystemExit(f"unknown workload {name}")
+    return ps, sv
+
+
+def ga_params(rank, workers):
+    from paper_2109_11067_b200 import migplan as mp
+
+    return mp.GaParams(seed=24 + rank, max_rounds=2, time_budget_s=1e9, population=16, workers=workers,
+                       slow=mp.MctsParams(budget_iters=48))
+
+
+def run_step(mp, name, ctx, sv, ps, rank, workers):
+    """One optimizer pass; returns the plan (list of GpuConfig)."""
+    if name.endswith("_ga"):
+        dep = mp.two_phase(sv, ps, mp.PartitionRuleSet.defaults(), ga_params(rank, workers), ctx=ctx)
+        return [g.config for g in dep.gpus]
+    return mp.fast_algo(mp.zero_completion(len(sv)), ctx)
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    FIELDS = "index,clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown," \
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown," \
+             "clocks_event_reasons.sw_power_cap"
+
+    def __init__(self, index):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def start(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
+                if out.returncode == 0 and out.stdout.strip():
+                    self.samples.append([x.strip() for x in out.stdout.strip().split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def stop(self):
+        self._stop.set()
+        if self._t:
+            self._t.join(timeout=10)
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        mx = [float(s[2]) for s in self.samples if s[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4) if len(s) > 4 + i and s[4 + i] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+def measured_peak():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def profile_traffic():
+    """dram bytes per greedy-kernel launch from the committed ncu capture, if any."""
+    p = os.path.join(ROOT, "profiles", "greedy_kernel_ncu.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return d.get("dram_bytes_per_launch"), d.get("workload")
+    except Exception:
+        return None, None
+
+
+def cpu_baseline(name, sv, ps, rows_per_step):
+    """The unmodified reference (oracle/_ref) on this host's cores, bounded sample: one step."""
+    import support as S
+    from support import mp
+
+    ref = S.ref_backend()
+    kind = "reference"
+    if ref is None:
+        ref, kind = S.oracle_backend(), "port"
+    if ref is None:
+        return None
+    workers = min(os.cpu_count() or 1, 8) if name.endswith("_ga") else 1
+    ctx = mp.make_plan_context(sv, ps, mp.PartitionRuleSet.defaults(), backend=ref)
+    t0 = time.perf_counter()
+    run_step(mp, name, ctx, sv, ps, 0, workers)
+    dt = time.perf_counter() - t0
+    return {"value": rows_per_step / dt, "unit": "configs/s", "cores": workers, "kind": kind,
+            "sample": f"1 step of {name} ({WORKLOADS[name]}), {dt:.2f} s wall", "step_s": dt}
+
+
+def reference_arm(args):
+    """--impl reference: the reference's CPU implementation, all host threads, bounded sample."""
+    import support as S
+    from support import mp
+
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    ref = S.ref_backend()
+    kind = "reference"
+    if ref is None:
+        ref, kind = S.oracle_backend(), "port"
+    ps, sv = load_workload(args.workload)
+    workers = min(os.cpu_count() or 1, 8)
+    # rows per step: counted by the oracle restatement (identical definition; untimed)
+    orc = S.oracle_backend()
+    octx = mp.make_plan_context(sv, ps, mp.PartitionRuleSet.defaults(), backend=orc)
+    plan = run_step(mp, args.workload, octx, sv, ps, 0, workers)
+    rows = octx.stats()["rows_scored"]
+    ctx = mp.make_plan_context(sv, ps, mp.PartitionRuleSet.defaults(), backend=ref)
+    warm, steps = min(args.warmup, 1), max(1, min(args.steps, 3))  # bounded: a few minutes in total
+    for _ in range(warm):
+        run_step(mp, args.workload, ctx, sv, ps, 0, workers)
+    times = []
+    for _ in range(steps):
+        t0 = time.perf_counter()
+        plan = run_step(mp, args.workload, ctx, sv, ps, 0, workers)
+        times.append(time.perf_counter() - t0)
+    total = sum(times)
+    value = rows * steps / total
+    line = {"impl": "reference", "metric": "candidate configs scored/sec", "value": value, "unit": "configs/s",
+            "n_gpus": args.gpus, "steps": steps, "warmup": warm, "ms_per_step": 1e3 * total / steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": args.workload, "description": WORKLOADS[args.workload], "gpus_used": len(plan),
+                       "rows_per_step": rows},
+            "cpu_baseline": {"value": value, "unit": "configs/s", "cores": workers, "kind": kind,
+                             "sample": f"{steps} step(s) of {args.workload} (warmup {warm})"},
+            "e2e": {"value": value, "unit": "configs/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="product", choices=["product", "reference"])
+    ap.add_argument("--workload", default="slos24_ga", choices=sorted(WORKLOADS))
+    ap.add_argument("--workers", type=int, default=8, help="GA worker threads per rank (product)")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return reference_arm(args)
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2109_11067_b200 import migplan as mp
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl")
+
+    ps, sv = load_workload(args.workload, rank)
+    workers = args.workers
+    ctx = mp.make_plan_context(sv, ps, mp.PartitionRuleSet.defaults(), device=local)
+    flush = torch.empty(512 * 1024 * 1024, dtype=torch.uint8, device="cuda")
+
+    def barrier():
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(max(args.warmup, 0)):
+        plan = run_step(mp, args.workload, ctx, sv, ps, rank, workers)
+
+    # ---- resident (value)
+    clocks = ClockSampler(local)
+    clocks.start()
+    ctx.reset_stats()
+    dev_ms = 0.0
+    barrier()
+    for _ in range(args.steps):
+        flush.zero_()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        plan = run_step(mp, args.workload, ctx, sv, ps, rank, workers)
+        torch.cuda.synchronize()
+        e1.record()
+        torch.cuda.synchronize()
+        dev_ms += e0.elapsed_time(e1)
+    barrier()
+    st = ctx.stats()
+    clock = clocks.stop()
+
+    # ---- end to end through the C-ABI from host buffers (e2e)
+    e2e_ms = 0.0
+    e2e_rows = 0
+    h2d = d2h = 0
+    for _ in range(args.steps):
+        flush.zero_()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        c2 = mp.make_plan_context(sv, ps, mp.PartitionRuleSet.defaults(), device=local)
+        run_step(mp, args.workload, c2, sv, ps, rank, workers)
+        torch.cuda.synchronize()
+        e1.record()
+        torch.cuda.synchronize()
+        e2e_ms += e0.elapsed_time(e1)
+        s2 = c2.stats()
+        e2e_rows += s2["rows_scored"]
+        h2d += s2["h2d_bytes"]
+        d2h += s2["d2h_bytes"]
+        c2.close()
+
+    rows = st["rows_scored"]
+    t = torch.tensor([dev_ms, e2e_ms, float(rows), float(e2e_rows), st["greedy_ms"]], dtype=torch.float64,
+                     device="cuda")
+    if world > 1:
+        tmax = t.clone()
+        dist.all_reduce(tmax[:2], op=dist.ReduceOp.MAX)
+        tsum = t.clone()
+        dist.all_reduce(tsum[2:4], op=dist.ReduceOp.SUM)
+        dev_ms_max, e2e_ms_max = tmax[0].item(), tmax[1].item()
+        rows_all, e2e_rows_all = tsum[2].item(), tsum[3].item()
+    else:
+        dev_ms_max, e2e_ms_max, rows_all, e2e_rows_all = dev_ms, e2e_ms, float(rows), float(e2e_rows)
+
+    if rank == 0:
+        peak, peak_kind = measured_peak()
+        greedy_s = st["greedy_ms"] / 1e3
+        greedy_bytes = 8.0 * st["greedy_rows"] / max(st["greedy_calls"], 1)  # algorithmic bytes per launch
+        launch_s = greedy_s / max(st["greedy_calls"], 1)
+        achieved = greedy_bytes / launch_s / 1e9 if launch_s > 0 else 0.0
+        traffic, traffic_wl = profile_traffic()
+        line = {
+            "metric": "candidate configs scored/sec", "value": rows_all / (dev_ms_max / 1e3), "unit": "configs/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": dev_ms_max / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": args.workload, "description": WORKLOADS[args.workload],
+                       "gpus_used": len(plan), "rows_per_step": rows / args.steps,
+                       "plan_ms": dev_ms_max / args.steps, "l2": "flushed (512 MiB write) between steps",
+                       "parallelism": f"{world} independent GA islands" if world > 1 else "1 GPU",
+                       "ga_workers_per_rank": workers},
+            "e2e": {"value": e2e_rows_all / (e2e_ms_max / 1e3), "unit": "configs/s",
+                    "h2d_bytes_per_step": h2d // args.steps, "d2h_bytes_per_step": d2h // args.steps,
+                    "ms_per_step": e2e_ms_max / args.steps},
+            "gpu_launches": st["kernel_launches"],
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic,
+                         "kernel": "greedy_kernel (persistent fast_algo: scan + argmax + extension)",
+                         "bytes_per_unit": 8, "unit_of_work": "packed candidate row scanned per greedy step",
+                         "peak_kind": peak_kind, "traffic_workload": traffic_wl},
+            "clocks": clock,
+            "breakdown": {"greedy_ms": st["greedy_ms"], "topk_ms": st["topk_ms"], "greedy_calls": st["greedy_calls"],
+                          "topk_calls": st["topk_calls"], "greedy_rows": st["greedy_rows"],
+                          "topk_rows": st["topk_rows"], "greedy_steps": st["greedy_steps"]},
+        }
+        if world == 1 and not args.no_cpu_baseline:
+            line["cpu_baseline"] = cpu_baseline(args.workload, sv, ps, rows / args.steps)
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -226,14 +226,23 @@ int mig_two_phase(mig_ctx* ctx, const mig_ga_params* params, mig_config* out, in
 int mig_lower_bound(const mig_ctx* ctx, int32_t* out);
 
 /* ---- instrumentation (product only; CPU libraries report zeros) ---- */
+/* Work counters.  "Rows scored" is implementation-independent (the oracle counts the same
+ * numbers): every greedy step scores its whole working set (greedy.hpp:126-134) and every
+ * top-K call scores its candidate set once (mcts.hpp:59-67). */
 typedef struct mig_stats {
-    int64_t rows_scored;      /* Σ working-set rows scored by greedy scans + top-K scans */
-    int64_t greedy_steps;     /* argmax steps executed                                  */
-    int64_t ext_events;       /* extension events (greedy.hpp:107-119)                  */
-    int64_t ext_rows;         /* rows appended by extension enumeration                 */
-    int64_t kernel_launches;  /* CUDA kernels launched by this context                  */
-    double scan_ms;           /* device time of greedy launches (CUDA events)           */
-    double topk_ms;
+    int64_t rows_scored;      /* greedy_rows + topk_rows                                 */
+    int64_t greedy_rows;      /* Σ over greedy steps of the working-set size             */
+    int64_t topk_rows;        /* Σ over top-K calls of the candidate-set size            */
+    int64_t greedy_calls;
+    int64_t topk_calls;
+    int64_t greedy_steps;     /* argmax steps executed                                   */
+    int64_t ext_events;       /* extension events (greedy.hpp:107-119)                   */
+    int64_t ext_rows;         /* rows appended by extension enumeration                  */
+    int64_t kernel_launches;  /* CUDA kernels launched by this context (product only)    */
+    int64_t h2d_bytes;        /* host->device bytes copied (product only)                */
+    int64_t d2h_bytes;        /* device->host bytes copied (product only)                */
+    double greedy_ms;         /* device time of greedy launches, CUDA events (product)   */
+    double topk_ms;           /* device time of top-K launches, CUDA events (product)    */
 } mig_stats;
 int mig_ctx_stats(const mig_ctx* ctx, mig_stats* out);
 void mig_ctx_reset_stats(mig_ctx* ctx);

@@ -67,8 +67,10 @@ class GaParamsC(C.Structure):
 
 
 class StatsC(C.Structure):
-    _fields_ = [("rows_scored", C.c_int64), ("greedy_steps", C.c_int64), ("ext_events", C.c_int64),
-                ("ext_rows", C.c_int64), ("kernel_launches", C.c_int64), ("scan_ms", C.c_double),
+    _fields_ = [("rows_scored", C.c_int64), ("greedy_rows", C.c_int64), ("topk_rows", C.c_int64),
+                ("greedy_calls", C.c_int64), ("topk_calls", C.c_int64), ("greedy_steps", C.c_int64),
+                ("ext_events", C.c_int64), ("ext_rows", C.c_int64), ("kernel_launches", C.c_int64),
+                ("h2d_bytes", C.c_int64), ("d2h_bytes", C.c_int64), ("greedy_ms", C.c_double),
                 ("topk_ms", C.c_double)]
 
 

@@ -480,25 +480,22 @@ int mig_lower_bound(const mig_ctx* ctx, int32_t* out) {
 int mig_ctx_stats(const mig_ctx* ctx, mig_stats* out) {
     std::memset(out, 0, sizeof *out);
     const Stats& s = ctx->e->stats;
-    out->rows_scored = s.rows_scored.load();
+    out->greedy_rows = s.greedy_rows.load();
+    out->topk_rows = s.topk_rows.load();
+    out->rows_scored = out->greedy_rows + out->topk_rows;
+    out->greedy_calls = s.greedy_calls.load();
+    out->topk_calls = s.topk_calls.load();
     out->greedy_steps = s.greedy_steps.load();
     out->ext_events = s.ext_events.load();
     out->ext_rows = s.ext_rows.load();
     out->kernel_launches = s.launches.load();
-    out->scan_ms = s.scan_us.load() / 1000.0;
-    out->topk_ms = s.topk_us.load() / 1000.0;
+    out->h2d_bytes = s.h2d.load();
+    out->d2h_bytes = s.d2h.load();
+    out->greedy_ms = s.greedy_ns.load() / 1e6;
+    out->topk_ms = s.topk_ns.load() / 1e6;
     return MIG_OK;
 }
 
-void mig_ctx_reset_stats(mig_ctx* ctx) {
-    Stats& s = ctx->e->stats;
-    s.rows_scored = 0;
-    s.greedy_steps = 0;
-    s.ext_events = 0;
-    s.ext_rows = 0;
-    s.launches = 0;
-    s.scan_us = 0;
-    s.topk_us = 0;
-}
+void mig_ctx_reset_stats(mig_ctx* ctx) { ctx->e->stats.reset(); }
 
 }  // extern "C"

@@ -2,6 +2,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <chrono>
 #include <cmath>
 #include <cstdlib>
@@ -34,10 +35,13 @@ T* dalloc(std::vector<void*>& owned, size_t count) {
     return static_cast<T*>(p);
 }
 
+thread_local std::atomic<long long>* g_h2d = nullptr;  // set while an Engine is being constructed
+
 template <class T>
 T* upload(std::vector<void*>& owned, const std::vector<T>& v) {
     T* p = dalloc<T>(owned, v.size());
     if (!v.empty()) CK(cudaMemcpy(p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice));
+    if (g_h2d) *g_h2d += static_cast<long long>(v.size() * sizeof(T));
     return p;
 }
 
@@ -128,6 +132,7 @@ Engine::Engine(const Rules& rules, std::map<std::string, ModelProfile> profiles,
     if (greedy_blocks_per_sm_ < 1 || topk_blocks_per_sm_ < 1) throw DeviceError("kernel does not fit on an SM");
 
     // ---- device model tables
+    g_h2d = &stats.h2d;
     dm_.n = m_.n;
     dm_.PP = m_.PP;
     dm_.n_sizes = static_cast<int>(m_.sizes.size());
@@ -192,6 +197,7 @@ Engine::Engine(const Rules& rules, std::map<std::string, ModelProfile> profiles,
         long long* d_off = dalloc<long long>(dev_allocs_, offsets.size());
         CK(cudaMemcpy(d_sup, supports.data(), supports.size() * 4, cudaMemcpyHostToDevice));
         CK(cudaMemcpy(d_off, offsets.data(), offsets.size() * 8, cudaMemcpyHostToDevice));
+        stats.h2d += static_cast<long long>(supports.size() * 4 + offsets.size() * 8);
         int n_sup = static_cast<int>(supports.size());
         int threads = 256;
         int blocks = static_cast<int>((static_cast<long long>(n_sup) * 32 + threads - 1) / threads);
@@ -203,6 +209,8 @@ Engine::Engine(const Rules& rules, std::map<std::string, ModelProfile> profiles,
     }
     base_rows_.resize(static_cast<size_t>(total));
     if (total) CK(cudaMemcpy(base_rows_.data(), d_base_, total * 8, cudaMemcpyDeviceToHost));
+    stats.d2h += total * 8;
+    g_h2d = nullptr;
     row_index_.reserve(base_rows_.size() * 2);
     for (size_t i = 0; i < base_rows_.size(); ++i) row_index_.emplace(base_rows_[i], static_cast<long long>(i));
 
@@ -352,7 +360,9 @@ void Engine::fast_algo(const std::vector<double>& comp, std::vector<uint64_t>& r
         CK(cudaStreamSynchronize(s->stream));
         float ms = 0.f;
         CK(cudaEventElapsedTime(&ms, s->e0, s->e1));
-        stats.scan_us += static_cast<long long>(ms * 1000.0f);
+        stats.greedy_ns += static_cast<long long>(ms * 1e6f);
+        stats.h2d += static_cast<long long>(sizeof(double) * m_.n);
+        stats.d2h += static_cast<long long>(sizeof(GreedyState));
         const GreedyState h = *s->h_st;
         if (h.status == kExtOverflow && attempt < 4) {
             long long need = static_cast<long long>(h.ext_count) * 2 + (1 << 20);
@@ -370,7 +380,9 @@ void Engine::fast_algo(const std::vector<double>& comp, std::vector<uint64_t>& r
                                s->stream));
             CK(cudaStreamSynchronize(s->stream));
         }
-        stats.rows_scored += h.rows_scored;
+        stats.d2h += static_cast<long long>((sizeof(uint64_t) + sizeof(double)) * h.n_steps);
+        stats.greedy_rows += h.rows_scored;
+        stats.greedy_calls++;
         stats.greedy_steps += h.n_steps;
         stats.ext_events += h.n_events;
         stats.ext_rows += static_cast<long long>(h.ext_count);
@@ -436,8 +448,12 @@ std::vector<long long> Engine::topk(const std::vector<double>& comp, int k, cons
     }
     float ms = 0.f;
     CK(cudaEventElapsedTime(&ms, s->e0, s->e1));
-    stats.topk_us += static_cast<long long>(ms * 1000.0f);
-    stats.rows_scored += total * std::max(got, 1);
+    stats.topk_ns += static_cast<long long>(ms * 1e6f);
+    stats.topk_rows += total;
+    stats.topk_calls++;
+    stats.h2d += static_cast<long long>(sizeof(double) * m_.n + (index ? sizeof(long long) * total : 0) +
+                                        (svc_mask ? 32 : 0));
+    stats.d2h += static_cast<long long>(sizeof(int) + sizeof(uint64_t) * got);
     for (uint64_t r : rows) out.push_back(index_of(r));
     return out;
 }

@@ -31,8 +31,14 @@ bool config_equal(const Config& a, const Config& b);
 struct Slot;
 
 struct Stats {
-    std::atomic<long long> rows_scored{0}, greedy_steps{0}, ext_events{0}, ext_rows{0}, launches{0};
-    std::atomic<long long> scan_us{0}, topk_us{0};
+    std::atomic<long long> greedy_rows{0}, topk_rows{0}, greedy_calls{0}, topk_calls{0}, greedy_steps{0};
+    std::atomic<long long> ext_events{0}, ext_rows{0}, launches{0}, h2d{0}, d2h{0};
+    std::atomic<long long> greedy_ns{0}, topk_ns{0};
+    void reset() {
+        for (auto* a : {&greedy_rows, &topk_rows, &greedy_calls, &topk_calls, &greedy_steps, &ext_events, &ext_rows,
+                        &launches, &h2d, &d2h, &greedy_ns, &topk_ns})
+            a->store(0);
+    }
 };
 
 class Engine {

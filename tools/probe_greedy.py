@@ -23,8 +23,8 @@ def main():
         st = ctx.stats()
         ok = S.plan_key(plan) == g["plan"]
         print(f"{name}: ctx {1e3*(t1-t0):.1f} ms, plan {1e3*(t3-t2):.2f} ms, GPUs {len(plan)} (ref {len(g['plan'])}), "
-              f"match={ok}, rows {st['rows_scored']} (ref {g['rows_scored']}), kernel {st['scan_ms']:.2f} ms, "
-              f"rate {st['rows_scored']/max(st['scan_ms'],1e-9)/1e6:.2f} Grows/s, ref wall {g['ref_wall_s']} s", flush=True)
+              f"match={ok}, rows {st['greedy_rows']} (ref {g['rows_scored']}), kernel {st['greedy_ms']:.2f} ms, "
+              f"rate {st['greedy_rows']/max(st['greedy_ms'],1e-9)/1e6:.2f} Grows/s, ref wall {g['ref_wall_s']} s", flush=True)
 
 if __name__ == "__main__":
     main()
