@@ -243,6 +243,9 @@ typedef struct mig_stats {
     int64_t d2h_bytes;        /* device->host bytes copied (product only)                */
     double greedy_ms;         /* device time of greedy launches, CUDA events (product)   */
     double topk_ms;           /* device time of top-K launches, CUDA events (product)    */
+    /* greedy-kernel phase split seen by CTA 0 (%globaltimer, product): scan+block argmax,
+     * grid barrier, grid argmax+update, maybe_extend, extension enumeration+barrier     */
+    double phase_ms[5];
 } mig_stats;
 int mig_ctx_stats(const mig_ctx* ctx, mig_stats* out);
 void mig_ctx_reset_stats(mig_ctx* ctx);

@@ -71,7 +71,7 @@ class StatsC(C.Structure):
                 ("greedy_calls", C.c_int64), ("topk_calls", C.c_int64), ("greedy_steps", C.c_int64),
                 ("ext_events", C.c_int64), ("ext_rows", C.c_int64), ("kernel_launches", C.c_int64),
                 ("h2d_bytes", C.c_int64), ("d2h_bytes", C.c_int64), ("greedy_ms", C.c_double),
-                ("topk_ms", C.c_double)]
+                ("topk_ms", C.c_double), ("phase_ms", C.c_double * 5)]
 
 
 GREEDY_TRACE = C.CFUNCTYPE(None, C.c_void_p, C.c_int32, C.POINTER(CandidateC), C.c_double,

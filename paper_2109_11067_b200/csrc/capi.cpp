@@ -493,6 +493,7 @@ int mig_ctx_stats(const mig_ctx* ctx, mig_stats* out) {
     out->d2h_bytes = s.d2h.load();
     out->greedy_ms = s.greedy_ns.load() / 1e6;
     out->topk_ms = s.topk_ns.load() / 1e6;
+    for (int k = 0; k < 5; ++k) out->phase_ms[k] = s.phase_ns[k].load() / 1e6;
     return MIG_OK;
 }
 

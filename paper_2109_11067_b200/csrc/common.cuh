@@ -1,0 +1,137 @@
+// common.cuh — device helpers shared by the sm_100a kernels (kernels.cu, topk.cu).
+#pragma once
+
+#include <cuda/atomic>
+
+#include "device.cuh"
+
+namespace mgb {
+namespace dev {
+
+__device__ __forceinline__ unsigned lane_id() { return threadIdx.x & 31u; }
+__device__ __forceinline__ unsigned lanemask_lt() { return (1u << lane_id()) - 1u; }
+__device__ __forceinline__ unsigned long long globaltimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+
+// 128-bit lexicographic GpuConfig key (core.hpp:174-200): per normalized instance
+// (slices asc, slot asc) a 15-bit field present|slices|slot|svc; shorter sorts first.
+// The row's layout is the sum of its members' count patterns; within a size group the
+// lower service index holds the lower slots (config_enum.hpp:140,159-163).
+static __device__ __noinline__ void row_key(const DevModel& M, uint64_t row, uint64_t& hi, uint64_t& lo) {
+    int svc[4], pat[4], k = 0;
+    const int sentinel = M.n * M.PP;
+    for (int j = 0; j < 4; ++j) {
+        int code = static_cast<int>((row >> (16 * j)) & 0xFFFFull);
+        if (code == sentinel) break;
+        svc[k] = code / M.PP;
+        pat[k] = code % M.PP;
+        ++k;
+    }
+    int tot[5] = {0, 0, 0, 0, 0};
+    for (int j = 0; j < k; ++j)
+        for (int s = 0; s < 5; ++s) tot[s] += M.pat_count[pat[j] * 5 + s];
+    int L = 0;
+    for (int l = 0; l < M.n_layouts; ++l) {
+        bool eq = true;
+        for (int s = 0; s < 5; ++s) eq &= M.layout_count[l * 5 + s] == tot[s];
+        if (eq) {
+            L = l;
+            break;
+        }
+    }
+    unsigned __int128 key = 0;
+    int ninst = 0;
+    for (int si = 0; si < M.n_sizes; ++si) {
+        int j = 0, used = 0;
+        for (int t = 0; t < tot[si]; ++t) {
+            while (used >= M.pat_count[pat[j] * 5 + si]) {
+                ++j;
+                used = 0;
+            }
+            unsigned slot = static_cast<unsigned>(M.layout_slots[(L * 5 + si) * 7 + t]);
+            key = (key << 15) | ((1u << 14) | (static_cast<unsigned>(M.sizes[si]) << 11) | (slot << 8) |
+                                 static_cast<unsigned>(svc[j]));
+            ++used;
+            ++ninst;
+        }
+    }
+    for (; ninst < 7; ++ninst) key <<= 15;
+    hi = static_cast<uint64_t>(key >> 64);
+    lo = static_cast<uint64_t>(key);
+}
+
+// Third key of candidate_preferred; reached only on exact (score, util_sum) ties.
+static __device__ __noinline__ bool row_key_less(const DevModel& M, uint64_t a, uint64_t b) {
+    uint64_t ah, al, bh, bl;
+    row_key(M, a, ah, al);
+    row_key(M, b, bh, bl);
+    return ah != bh ? ah < bh : al < bl;
+}
+
+__device__ __forceinline__ Best none() { return Best{0.0, 0.0, kNoRow}; }
+
+// candidate_preferred (greedy.hpp:63-67) on (score, util_sum, row); none loses to all.
+__device__ __forceinline__ bool better(const DevModel& M, const Best& a, const Best& b) {
+    if (a.s != b.s) return a.s > b.s;
+    if (a.row == kNoRow || b.row == kNoRow || a.row == b.row) return false;
+    if (a.u != b.u) return a.u > b.u;
+    return row_key_less(M, a.row, b.row);
+}
+
+// util_sum (config_enum.hpp:173): ascending members from 0.0; U may be smem or global.
+__device__ __forceinline__ double row_usum(const double* U, uint64_t row) {
+    double s = 0.0;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) s = __dadd_rn(s, U[(row >> (16 * j)) & 0xFFFFull]);
+    return s;
+}
+
+// score (greedy.hpp:36-43) with W = need*U precomputed (0 where need <= 0).  Members are
+// in ascending service order and unused positions hit a zero cell, so the sum order and
+// every rounding step equal the reference's.
+__device__ __forceinline__ double row_score(const double* __restrict__ W, uint64_t row) {
+    double s = __dadd_rn(W[row & 0xFFFFull], W[(row >> 16) & 0xFFFFull]);
+    s = __dadd_rn(s, W[(row >> 32) & 0xFFFFull]);
+    return __dadd_rn(s, W[row >> 48]);
+}
+
+__device__ __forceinline__ Best shfl_xor_best(const Best& b, int off) {
+    return Best{__shfl_xor_sync(0xffffffffu, b.s, off), __shfl_xor_sync(0xffffffffu, b.u, off),
+                __shfl_xor_sync(0xffffffffu, b.row, off)};
+}
+
+__device__ __forceinline__ Best warp_best(const DevModel& M, Best b) {
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+        Best o = shfl_xor_best(b, off);
+        if (better(M, o, b)) b = o;
+    }
+    return b;
+}
+
+// Generation barrier across all co-resident (cooperatively launched) CTAs.  The CTA's
+// writes are ordered before thread 0's arrival by bar.sync + a gpu-scope acq_rel fence
+// (cumulative); the wait is an acquire load.  Data produced by other CTAs is read after the
+// barrier with L2-coherent loads (ld.global.cg), never through the non-coherent path.
+__device__ __forceinline__ void grid_barrier(unsigned* count, unsigned* gen, unsigned nblocks) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        cuda::atomic_ref<unsigned, cuda::thread_scope_device> g(*gen), c(*count);
+        const unsigned my = g.load(cuda::memory_order_relaxed);
+        asm volatile("fence.acq_rel.gpu;" ::: "memory");
+        if (c.fetch_add(1u, cuda::memory_order_acq_rel) == nblocks - 1u) {
+            c.store(0u, cuda::memory_order_relaxed);
+            g.store(my + 1u, cuda::memory_order_release);
+        } else {
+            while (g.load(cuda::memory_order_acquire) == my) {
+            }
+        }
+    }
+    __syncthreads();
+}
+
+}  // namespace dev
+}  // namespace mgb

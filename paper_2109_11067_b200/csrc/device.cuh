@@ -43,22 +43,30 @@ struct GreedyState {
     int n_events;
     int pad;
     long long rows_scored;
+    // CTA-0 %globaltimer phase totals (ns): 0 build W + scan + block reduce, 1 grid barrier,
+    // 2 grid reduce + completion update, 3 maybe_extend, 4 extension enumeration + barrier
+    unsigned long long phase_ns[5];
 };
 
 enum GreedyStatus { kOk = 0, kNoPositive = 1, kExtOverflow = 2, kStepOverflow = 3 };
 
 struct GreedyArgs {
     DevModel M;
-    const uint64_t* base_rows;
+    uint64_t* rows;       // arena: base pool rows [0, n_base), extension rows appended after
     long long n_base;
-    uint64_t* ext_rows;
-    long long ext_cap;
-    const double* comp0;
-    GreedyState* st;
+    long long cap;        // arena capacity (rows)
+    int cache_units;      // 16-byte row units of shared-memory cache per CTA
+    int phase_timers;     // 1: CTA 0 records %globaltimer phase totals (diagnostics)
+    const double* comp0;  // host-mapped pinned
+    GreedyState* st;      // device (barrier + atomics)
+    GreedyState* out;     // host-mapped pinned: final state written by CTA 0
     Best* partials;       // 2 * gridDim.x (double buffered by step parity)
-    uint64_t* pick_row;   // cap_steps
-    double* pick_score;   // cap_steps
-    long long* pick_rows; // rows in the working set at that step
+    uint64_t* pick_row;   // cap_steps (device)
+    double* pick_score;   // cap_steps (device)
+    long long* pick_rows; // rows in the working set at that step (device)
+    uint64_t* host_pick_row;    // host-mapped copies written once at the end
+    double* host_pick_score;
+    long long* host_pick_rows;
     int* ev_svc;          // events recorded (service, in order)
     int cap_steps;
 };
@@ -76,6 +84,22 @@ struct TopkArgs {
     Best* partials;           // 2 * gridDim.x
     uint64_t* out_row;        // k
     int* n_out;
+};
+
+// Single-pass top-K (topk.cu), k <= 16.
+struct Topk1Args {
+    DevModel M;
+    const uint64_t* rows;
+    long long n_rows;
+    const long long* index;
+    long long n_index;
+    const uint64_t* svc_mask;
+    const double* comp;
+    int k;
+    Best* partials;     // gridDim.x * 16 per-CTA lists
+    unsigned* ticket;   // zero before launch; reset by the last CTA
+    uint64_t* out_row;  // k (host-mapped)
+    int* n_out;         // host-mapped
 };
 
 }  // namespace mgb

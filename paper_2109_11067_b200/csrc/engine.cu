@@ -13,12 +13,15 @@
 
 namespace mgb {
 
-size_t greedy_smem_bytes(int n, int PP);
+size_t greedy_smem_bytes(int n, int PP, int cache_units);
 size_t topk_smem_bytes(int n, int PP);
 const void* greedy_kernel_ptr();
 const void* topk_kernel_ptr();
 const void* enum_base_kernel_ptr();
 int kernel_threads();
+size_t topk1_smem_bytes(int n, int PP, int km);
+int topk1_threads();
+const void* topk1_kernel_ptr(int km);
 
 namespace {
 
@@ -54,6 +57,18 @@ long long binom(long long a, int k) {
 
 }  // namespace
 
+// Per-call resources.  Small inputs/outputs live in host-mapped pinned memory that the
+// kernels read/write directly, so a greedy or top-K call costs one launch and one
+// stream synchronisation (no separate H2D/D2H copies on the latency path).
+struct HostIO {
+    GreedyState res;       // final greedy state (written by CTA 0)
+    int top_n;             // top-K result count
+    int pad;
+    double comp[256];      // completion vector input
+    uint64_t mask[4];      // top-K service filter
+    uint64_t top_rows[1024];
+};
+
 struct Slot {
     int device = 0;
     cudaStream_t stream = nullptr;
@@ -63,29 +78,41 @@ struct Slot {
     GreedyState* st = nullptr;
     Best* partials = nullptr;
     int cap_steps = 0;
-    uint64_t* pick_row = nullptr;
-    double* pick_score = nullptr;
-    long long* pick_rows = nullptr;
+    uint64_t* pick_row = nullptr;  // host-mapped
+    double* pick_score = nullptr;  // host-mapped
+    long long* pick_rows = nullptr;  // host-mapped
     int* ev_svc = nullptr;
-    double* comp = nullptr;
-    // top-K scratch
     unsigned* bar = nullptr;
-    uint64_t* out_row = nullptr;
-    int* n_out = nullptr;
+    unsigned* ticket = nullptr;  // single-pass top-K last-CTA ticket
+    Best* tpart = nullptr;       // single-pass top-K per-CTA lists (32 x 16)
     long long* index = nullptr;
     long long index_cap = 0;
-    uint64_t* mask = nullptr;
-    // pinned host staging
-    GreedyState* h_st = nullptr;
+    HostIO* io = nullptr;  // host-mapped
 
+    uint64_t* d_pick_row = nullptr;  // device-side step records
+    double* d_pick_score = nullptr;
+    long long* d_pick_rows = nullptr;
+
+    void free_picks() {
+        for (void* p : {(void*)pick_row, (void*)pick_score, (void*)pick_rows})
+            if (p) cudaFreeHost(p);
+        for (void* p : {(void*)d_pick_row, (void*)d_pick_score, (void*)d_pick_rows})
+            if (p) cudaFree(p);
+        pick_row = nullptr;
+        pick_score = nullptr;
+        pick_rows = nullptr;
+        d_pick_row = nullptr;
+        d_pick_score = nullptr;
+        d_pick_rows = nullptr;
+    }
     ~Slot() {
         cudaSetDevice(device);
         if (stream) cudaStreamSynchronize(stream);
-        for (void* p : {(void*)ext, (void*)st, (void*)partials, (void*)pick_row, (void*)pick_score,
-                        (void*)pick_rows, (void*)ev_svc, (void*)comp, (void*)bar, (void*)out_row, (void*)n_out,
-                        (void*)index, (void*)mask})
+        for (void* p : {(void*)ext, (void*)st, (void*)partials, (void*)ev_svc, (void*)bar, (void*)index,
+                        (void*)ticket, (void*)tpart})
             if (p) cudaFree(p);
-        if (h_st) cudaFreeHost(h_st);
+        free_picks();
+        if (io) cudaFreeHost(io);
         if (e0) cudaEventDestroy(e0);
         if (e1) cudaEventDestroy(e1);
         if (stream) cudaStreamDestroy(stream);
@@ -124,9 +151,21 @@ Engine::Engine(const Rules& rules, std::map<std::string, ModelProfile> profiles,
     num_sms_ = prop.multiProcessorCount;
 
     const int T = kernel_threads();
-    const size_t gsm = greedy_smem_bytes(m_.n, m_.PP), tsm = topk_smem_bytes(m_.n, m_.PP);
+    // greedy: everything but the row cache is fixed; the cache takes the rest of the
+    // opt-in shared memory (one CTA per SM), rounded to whole units per thread.
+    {
+        const long long fixed = static_cast<long long>(greedy_smem_bytes(m_.n, m_.PP, 0));
+        long long room = static_cast<long long>(prop.sharedMemPerBlockOptin) - 2048 - fixed;
+        cache_units_ = static_cast<int>(std::max<long long>(0, room / 16) / T * T);
+        if (const char* e = std::getenv("MIGPLAN_ROW_CACHE_UNITS"))
+            cache_units_ = std::max(0, std::min(cache_units_, std::atoi(e) / T * T));
+    }
+    const size_t gsm = greedy_smem_bytes(m_.n, m_.PP, cache_units_), tsm = topk_smem_bytes(m_.n, m_.PP);
     CK(cudaFuncSetAttribute(greedy_kernel_ptr(), cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(gsm)));
     CK(cudaFuncSetAttribute(topk_kernel_ptr(), cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(tsm)));
+    for (int km : {32})
+        CK(cudaFuncSetAttribute(topk1_kernel_ptr(km), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                static_cast<int>(topk1_smem_bytes(m_.n, m_.PP, km))));
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&greedy_blocks_per_sm_, greedy_kernel_ptr(), T, gsm));
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&topk_blocks_per_sm_, topk_kernel_ptr(), T, tsm));
     if (greedy_blocks_per_sm_ < 1 || topk_blocks_per_sm_ < 1) throw DeviceError("kernel does not fit on an SM");
@@ -265,13 +304,13 @@ Slot* Engine::acquire() {
     CK(cudaMalloc(&s->st, sizeof(GreedyState)));
     CK(cudaMalloc(&s->partials, sizeof(Best) * 2 * num_sms_ * std::max(greedy_blocks_per_sm_, topk_blocks_per_sm_)));
     CK(cudaMalloc(&s->ev_svc, sizeof(int) * (m_.n + 1)));
-    CK(cudaMalloc(&s->comp, sizeof(double) * (m_.n + 1)));
     CK(cudaMalloc(&s->bar, sizeof(unsigned) * 2));
     CK(cudaMemset(s->bar, 0, sizeof(unsigned) * 2));
-    CK(cudaMalloc(&s->out_row, sizeof(uint64_t) * 1024));
-    CK(cudaMalloc(&s->n_out, sizeof(int)));
-    CK(cudaMalloc(&s->mask, sizeof(uint64_t) * 4));
-    CK(cudaMallocHost(&s->h_st, sizeof(GreedyState)));
+    CK(cudaMalloc(&s->ticket, sizeof(unsigned)));
+    CK(cudaMemset(s->ticket, 0, sizeof(unsigned)));
+    CK(cudaMalloc(&s->tpart, sizeof(Best) * 64 * 32));
+    CK(cudaHostAlloc(&s->io, sizeof(HostIO), cudaHostAllocMapped));
+    std::memset(s->io, 0, sizeof(HostIO));
     Slot* raw = s.get();
     std::lock_guard<std::mutex> g2(mu_);
     slots_.push_back(std::move(s));
@@ -319,36 +358,45 @@ void Engine::fast_algo(const std::vector<double>& comp, std::vector<uint64_t>& r
     CK(cudaSetDevice(device_));
     long long cap_steps = std::min<long long>(step_bound(comp), 1 << 24);
     if (s->cap_steps < cap_steps) {
-        for (void* p : {(void*)s->pick_row, (void*)s->pick_score, (void*)s->pick_rows})
-            if (p) CK(cudaFree(p));
-        CK(cudaMalloc(&s->pick_row, sizeof(uint64_t) * cap_steps));
-        CK(cudaMalloc(&s->pick_score, sizeof(double) * cap_steps));
-        CK(cudaMalloc(&s->pick_rows, sizeof(long long) * cap_steps));
+        s->free_picks();
+        CK(cudaHostAlloc(&s->pick_row, sizeof(uint64_t) * cap_steps, cudaHostAllocMapped));
+        CK(cudaHostAlloc(&s->pick_score, sizeof(double) * cap_steps, cudaHostAllocMapped));
+        CK(cudaHostAlloc(&s->pick_rows, sizeof(long long) * cap_steps, cudaHostAllocMapped));
+        CK(cudaMalloc(&s->d_pick_row, sizeof(uint64_t) * cap_steps));
+        CK(cudaMalloc(&s->d_pick_score, sizeof(double) * cap_steps));
+        CK(cudaMalloc(&s->d_pick_rows, sizeof(long long) * cap_steps));
         s->cap_steps = static_cast<int>(cap_steps);
     }
-    long long want_ext = std::min<long long>(ext_bound_, std::max<long long>(s->ext_cap, 1 << 20));
-    ensure_ext(s, want_ext);
+    const long long n_base = static_cast<long long>(base_rows_.size());
+    ensure_ext(s, n_base + std::min<long long>(ext_bound_, std::max<long long>(s->ext_cap - n_base, 1 << 20)));
 
     const int T = kernel_threads();
-    const size_t smem = greedy_smem_bytes(m_.n, m_.PP);
+    const size_t smem = greedy_smem_bytes(m_.n, m_.PP, cache_units_);
     int G = num_sms_ * greedy_blocks_per_sm_;
     if (const char* e = std::getenv("MIGPLAN_GREEDY_CTAS")) G = std::max(1, std::min(G, std::atoi(e)));
 
     for (int attempt = 0;; ++attempt) {
-        CK(cudaMemcpyAsync(s->comp, comp.data(), sizeof(double) * m_.n, cudaMemcpyHostToDevice, s->stream));
+        std::memcpy(s->io->comp, comp.data(), sizeof(double) * m_.n);
         CK(cudaMemsetAsync(s->st, 0, sizeof(GreedyState), s->stream));
+        // the working-set arena starts as a copy of the resident base pool (device to device)
+        if (n_base) CK(cudaMemcpyAsync(s->ext, d_base_, n_base * 8, cudaMemcpyDeviceToDevice, s->stream));
         GreedyArgs a{};
         a.M = dm_;
-        a.base_rows = d_base_;
-        a.n_base = static_cast<long long>(base_rows_.size());
-        a.ext_rows = s->ext;
-        a.ext_cap = s->ext_cap;
-        a.comp0 = s->comp;
+        a.rows = s->ext;
+        a.n_base = n_base;
+        a.cap = s->ext_cap;
+        a.cache_units = cache_units_;
+        a.phase_timers = std::getenv("MIGPLAN_PHASE_TIMERS") ? 1 : 0;
+        a.comp0 = s->io->comp;
         a.st = s->st;
+        a.out = &s->io->res;
         a.partials = s->partials;
-        a.pick_row = s->pick_row;
-        a.pick_score = s->pick_score;
-        a.pick_rows = s->pick_rows;
+        a.pick_row = s->d_pick_row;
+        a.pick_score = s->d_pick_score;
+        a.pick_rows = s->d_pick_rows;
+        a.host_pick_row = s->pick_row;
+        a.host_pick_score = s->pick_score;
+        a.host_pick_rows = s->pick_rows;
         a.ev_svc = s->ev_svc;
         a.cap_steps = s->cap_steps;
         void* args[] = {&a};
@@ -356,36 +404,29 @@ void Engine::fast_algo(const std::vector<double>& comp, std::vector<uint64_t>& r
         CK(cudaLaunchCooperativeKernel(greedy_kernel_ptr(), G, T, args, smem, s->stream));
         stats.launches++;
         CK(cudaEventRecord(s->e1, s->stream));
-        CK(cudaMemcpyAsync(s->h_st, s->st, sizeof(GreedyState), cudaMemcpyDeviceToHost, s->stream));
         CK(cudaStreamSynchronize(s->stream));
         float ms = 0.f;
         CK(cudaEventElapsedTime(&ms, s->e0, s->e1));
-        stats.greedy_ns += static_cast<long long>(ms * 1e6f);
-        stats.h2d += static_cast<long long>(sizeof(double) * m_.n);
-        stats.d2h += static_cast<long long>(sizeof(GreedyState));
-        const GreedyState h = *s->h_st;
+        const GreedyState h = s->io->res;
         if (h.status == kExtOverflow && attempt < 4) {
-            long long need = static_cast<long long>(h.ext_count) * 2 + (1 << 20);
+            long long need = n_base + static_cast<long long>(h.ext_count) * 2 + (1 << 20);
             ensure_ext(s, std::max(need, s->ext_cap * 2));
             continue;
         }
         if (h.status == kExtOverflow) throw DeviceError("extension arena overflow");
         if (h.status == kStepOverflow) throw DeviceError("greedy step buffer overflow");
-        rows.resize(h.n_steps);
-        scores.resize(h.n_steps);
-        if (h.n_steps) {
-            CK(cudaMemcpyAsync(rows.data(), s->pick_row, sizeof(uint64_t) * h.n_steps, cudaMemcpyDeviceToHost,
-                               s->stream));
-            CK(cudaMemcpyAsync(scores.data(), s->pick_score, sizeof(double) * h.n_steps, cudaMemcpyDeviceToHost,
-                               s->stream));
-            CK(cudaStreamSynchronize(s->stream));
-        }
-        stats.d2h += static_cast<long long>((sizeof(uint64_t) + sizeof(double)) * h.n_steps);
+        rows.assign(s->pick_row, s->pick_row + h.n_steps);
+        scores.assign(s->pick_score, s->pick_score + h.n_steps);
+        stats.greedy_ns += static_cast<long long>(ms * 1e6f);
+        stats.h2d += static_cast<long long>(sizeof(double) * m_.n);
+        stats.d2h += static_cast<long long>(sizeof(GreedyState) + (sizeof(uint64_t) + sizeof(double) +
+                                                                    sizeof(long long)) * h.n_steps);
         stats.greedy_rows += h.rows_scored;
         stats.greedy_calls++;
         stats.greedy_steps += h.n_steps;
         stats.ext_events += h.n_events;
         stats.ext_rows += static_cast<long long>(h.ext_count);
+        for (int k = 0; k < 5; ++k) stats.phase_ns[k] += static_cast<long long>(h.phase_ns[k]);
         if (h.status == kNoPositive)
             throw PlanningError("fast_algo: no config with positive score while services remain unsatisfied");
         return;
@@ -407,7 +448,8 @@ std::vector<long long> Engine::topk(const std::vector<double>& comp, int k, cons
         ~Rel() { e->release(s); }
     } rel{this, s};
     CK(cudaSetDevice(device_));
-    CK(cudaMemcpyAsync(s->comp, comp.data(), sizeof(double) * m_.n, cudaMemcpyHostToDevice, s->stream));
+    std::memcpy(s->io->comp, comp.data(), sizeof(double) * m_.n);
+    if (svc_mask) std::memcpy(s->io->mask, svc_mask->data(), sizeof(uint64_t) * 4);
     if (index) {
         if (s->index_cap < total) {
             if (s->index) CK(cudaFree(s->index));
@@ -416,36 +458,50 @@ std::vector<long long> Engine::topk(const std::vector<double>& comp, int k, cons
         }
         CK(cudaMemcpyAsync(s->index, index->data(), sizeof(long long) * total, cudaMemcpyHostToDevice, s->stream));
     }
-    if (svc_mask) CK(cudaMemcpyAsync(s->mask, svc_mask->data(), sizeof(uint64_t) * 4, cudaMemcpyHostToDevice, s->stream));
-    TopkArgs a{};
-    a.M = dm_;
-    a.rows = d_base_;
-    a.n_rows = pool_size();
-    a.index = index ? s->index : nullptr;
-    a.n_index = index ? total : 0;
-    a.svc_mask = svc_mask ? s->mask : nullptr;
-    a.comp = s->comp;
-    a.k = k;
-    a.bar = s->bar;
-    a.partials = s->partials;
-    a.out_row = s->out_row;
-    a.n_out = s->n_out;
-    const int T = kernel_threads();
-    int G = static_cast<int>(std::min<long long>((total + 4 * T - 1) / (4 * T), num_sms_ * topk_blocks_per_sm_));
-    G = std::max(G, 1);
-    void* args[] = {&a};
     CK(cudaEventRecord(s->e0, s->stream));
-    CK(cudaLaunchCooperativeKernel(topk_kernel_ptr(), G, T, args, topk_smem_bytes(m_.n, m_.PP), s->stream));
+    if (k <= 32) {  // single pass, last-CTA merge (topk.cu)
+        Topk1Args a{};
+        a.M = dm_;
+        a.rows = d_base_;
+        a.n_rows = pool_size();
+        a.index = index ? s->index : nullptr;
+        a.n_index = index ? total : 0;
+        a.svc_mask = svc_mask ? s->io->mask : nullptr;
+        a.comp = s->io->comp;
+        a.k = k;
+        a.partials = s->tpart;
+        a.ticket = s->ticket;
+        a.out_row = s->io->top_rows;
+        a.n_out = &s->io->top_n;
+        const int T = topk1_threads(), km = 32;
+        int G = static_cast<int>(std::min<long long>((total + 2047) / 2048, 64));
+        G = std::max(G, 1);
+        void* args[] = {&a};
+        CK(cudaLaunchKernel(topk1_kernel_ptr(km), G, T, args, topk1_smem_bytes(m_.n, m_.PP, km), s->stream));
+    } else {  // k rounds with grid barriers (k > 16: API-only)
+        TopkArgs a{};
+        a.M = dm_;
+        a.rows = d_base_;
+        a.n_rows = pool_size();
+        a.index = index ? s->index : nullptr;
+        a.n_index = index ? total : 0;
+        a.svc_mask = svc_mask ? s->io->mask : nullptr;
+        a.comp = s->io->comp;
+        a.k = k;
+        a.bar = s->bar;
+        a.partials = s->partials;
+        a.out_row = s->io->top_rows;
+        a.n_out = &s->io->top_n;
+        const int T = kernel_threads();
+        int G = static_cast<int>(std::min<long long>((total + 4 * T - 1) / (4 * T), num_sms_ * topk_blocks_per_sm_));
+        G = std::max(G, 1);
+        void* args[] = {&a};
+        CK(cudaLaunchCooperativeKernel(topk_kernel_ptr(), G, T, args, topk_smem_bytes(m_.n, m_.PP), s->stream));
+    }
     stats.launches++;
     CK(cudaEventRecord(s->e1, s->stream));
-    int got = 0;
-    CK(cudaMemcpyAsync(&got, s->n_out, sizeof(int), cudaMemcpyDeviceToHost, s->stream));
     CK(cudaStreamSynchronize(s->stream));
-    std::vector<uint64_t> rows(got);
-    if (got) {
-        CK(cudaMemcpyAsync(rows.data(), s->out_row, sizeof(uint64_t) * got, cudaMemcpyDeviceToHost, s->stream));
-        CK(cudaStreamSynchronize(s->stream));
-    }
+    const int got = s->io->top_n;
     float ms = 0.f;
     CK(cudaEventElapsedTime(&ms, s->e0, s->e1));
     stats.topk_ns += static_cast<long long>(ms * 1e6f);
@@ -454,9 +510,10 @@ std::vector<long long> Engine::topk(const std::vector<double>& comp, int k, cons
     stats.h2d += static_cast<long long>(sizeof(double) * m_.n + (index ? sizeof(long long) * total : 0) +
                                         (svc_mask ? 32 : 0));
     stats.d2h += static_cast<long long>(sizeof(int) + sizeof(uint64_t) * got);
-    for (uint64_t r : rows) out.push_back(index_of(r));
+    for (int i = 0; i < got; ++i) out.push_back(index_of(s->io->top_rows[i]));
     return out;
 }
+
 
 // completion_of / detail::sum_rates (core.hpp:245-269): counts keyed by (svc, size, batch)
 // in key order, total += count * thr, one division per service.

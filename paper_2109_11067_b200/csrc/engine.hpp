@@ -34,10 +34,12 @@ struct Stats {
     std::atomic<long long> greedy_rows{0}, topk_rows{0}, greedy_calls{0}, topk_calls{0}, greedy_steps{0};
     std::atomic<long long> ext_events{0}, ext_rows{0}, launches{0}, h2d{0}, d2h{0};
     std::atomic<long long> greedy_ns{0}, topk_ns{0};
+    std::atomic<long long> phase_ns[5] = {0, 0, 0, 0, 0};
     void reset() {
         for (auto* a : {&greedy_rows, &topk_rows, &greedy_calls, &topk_calls, &greedy_steps, &ext_events, &ext_rows,
                         &launches, &h2d, &d2h, &greedy_ns, &topk_ns})
             a->store(0);
+        for (auto& p : phase_ns) p.store(0);
     }
 };
 
@@ -87,6 +89,7 @@ class Engine {
     std::unordered_map<uint64_t, long long> row_index_;
     std::vector<double> min_u_;  // smallest positive utility per service (step bound)
     long long ext_bound_ = 0;
+    int cache_units_ = 0;  // greedy shared-memory row cache per CTA (16-byte units)
 
     std::mutex mu_;
     std::vector<std::unique_ptr<Slot>> slots_;

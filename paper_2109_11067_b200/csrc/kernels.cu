@@ -2,154 +2,28 @@
 //
 //   K1 enum_base_kernel   build_candidate_pool  (config_enum.hpp:192-202)
 //   K2/K3 greedy_kernel   fast_algo             (greedy.hpp:95-145): persistent cooperative
-//                         kernel; per step a coalesced 128-bit scan of the packed rows with
-//                         a shared-memory need*U table, a warp-shuffle 3-key argmax, a
-//                         grid-wide reduction, the completion update, maybe_extend
+//                         kernel; per step a coalesced 128-bit scan of the packed rows
+//                         (shared-memory resident while they fit, streamed from L2/HBM beyond)
+//                         against a shared-memory need*U table, a warp-shuffle 3-key argmax,
+//                         a grid-wide reduction, the completion update, maybe_extend
 //                         (greedy.hpp:107-119) and the device-side extension enumerator
 //                         (extend_candidate_pool, config_enum.hpp:206-211).
-//   K4 topk_kernel        detail::topk_candidates (mcts.hpp:56-76)
+//   K4 topk_kernel        detail::topk_candidates (mcts.hpp:56-76) for k > 32 (the common
+//                         k <= 32 case is the single-pass kernel in topk.cu).
 //
 // Bit-exactness: every floating add/multiply on the score path is an explicit
 // __dadd_rn/__dmul_rn (and the TU is built with -fmad=false), so no FMA contraction
 // changes the reference's FP64 bits (SURVEY §0 hazard 1).
-#include <cuda/atomic>
-
-#include "device.cuh"
+#include "common.cuh"
 
 namespace mgb {
+
+using namespace dev;
 
 namespace {
 
 constexpr int kThreads = 512;
 constexpr int kWarps = kThreads / 32;
-
-__device__ __forceinline__ unsigned lane_id() { return threadIdx.x & 31u; }
-__device__ __forceinline__ unsigned lanemask_lt() { return (1u << lane_id()) - 1u; }
-
-// Sense-free generation barrier across all (co-resident, cooperatively launched) CTAs.
-__device__ __forceinline__ void grid_barrier(unsigned* count, unsigned* gen, unsigned nblocks) {
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        cuda::atomic_ref<unsigned, cuda::thread_scope_device> g(*gen), c(*count);
-        unsigned my = g.load(cuda::memory_order_relaxed);
-        __threadfence();
-        if (c.fetch_add(1u, cuda::memory_order_acq_rel) == nblocks - 1u) {
-            c.store(0u, cuda::memory_order_relaxed);
-            g.fetch_add(1u, cuda::memory_order_release);
-        } else {
-            while (g.load(cuda::memory_order_acquire) == my) __nanosleep(20);
-        }
-        __threadfence();
-    }
-    __syncthreads();
-}
-
-// 128-bit lexicographic GpuConfig key (core.hpp:174-200): per normalized instance
-// (slices asc, slot asc) a 15-bit field present|slices|slot|svc; shorter sorts first.
-__device__ __noinline__ void row_key(const DevModel& M, uint64_t row, uint64_t& hi, uint64_t& lo) {
-    int svc[4], pat[4], k = 0;
-    const int sentinel = M.n * M.PP;
-    for (int j = 0; j < 4; ++j) {
-        int code = static_cast<int>((row >> (16 * j)) & 0xFFFFull);
-        if (code == sentinel) break;
-        svc[k] = code / M.PP;
-        pat[k] = code % M.PP;
-        ++k;
-    }
-    int tot[5] = {0, 0, 0, 0, 0};
-    for (int j = 0; j < k; ++j)
-        for (int s = 0; s < 5; ++s) tot[s] += M.pat_count[pat[j] * 5 + s];
-    int L = 0;
-    for (int l = 0; l < M.n_layouts; ++l) {
-        bool eq = true;
-        for (int s = 0; s < 5; ++s) eq &= M.layout_count[l * 5 + s] == tot[s];
-        if (eq) {
-            L = l;
-            break;
-        }
-    }
-    unsigned __int128 key = 0;
-    int ninst = 0;
-    for (int si = 0; si < M.n_sizes; ++si) {
-        int j = 0, used = 0;
-        for (int t = 0; t < tot[si]; ++t) {
-            while (used >= M.pat_count[pat[j] * 5 + si]) {
-                ++j;
-                used = 0;
-            }
-            unsigned slot = static_cast<unsigned>(M.layout_slots[(L * 5 + si) * 7 + t]);
-            unsigned f = (1u << 14) | (static_cast<unsigned>(M.sizes[si]) << 11) | (slot << 8) |
-                         static_cast<unsigned>(svc[j]);
-            key = (key << 15) | f;
-            ++used;
-            ++ninst;
-        }
-    }
-    for (; ninst < 7; ++ninst) key <<= 15;
-    hi = static_cast<uint64_t>(key >> 64);
-    lo = static_cast<uint64_t>(key);
-}
-
-__device__ __forceinline__ bool row_key_less(const DevModel& M, uint64_t a, uint64_t b) {
-    uint64_t ah, al, bh, bl;
-    row_key(M, a, ah, al);
-    row_key(M, b, bh, bl);
-    return ah != bh ? ah < bh : al < bl;
-}
-
-// util_sum (config_enum.hpp:173): ascending members, starting from 0.0.
-__device__ __forceinline__ double row_usum(const DevModel& M, uint64_t row) {
-    double s = 0.0;
-#pragma unroll
-    for (int j = 0; j < 4; ++j) s = __dadd_rn(s, __ldg(&M.U[(row >> (16 * j)) & 0xFFFFull]));
-    return s;
-}
-
-// candidate_preferred (greedy.hpp:63-67) on (score, util_sum, config) records.
-__device__ __noinline__ bool better(const DevModel& M, const Best& a, const Best& b) {
-    if (a.s != b.s) return a.s > b.s;
-    if (a.row == kNoRow || b.row == kNoRow || a.row == b.row) return false;
-    if (a.u != b.u) return a.u > b.u;
-    return row_key_less(M, a.row, b.row);
-}
-
-__device__ __noinline__ Best consider_slow(const DevModel& M, uint64_t row, double s, Best best) {
-    double u = row_usum(M, row);
-    Best c{s, u, row};
-    return (best.row == kNoRow || better(M, c, best)) ? c : best;
-}
-
-// score (greedy.hpp:36-43) with W = need*U precomputed per step (0 where need <= 0).
-__device__ __forceinline__ double row_score(const double* __restrict__ W, uint64_t row) {
-    double s = __dadd_rn(W[row & 0xFFFFull], W[(row >> 16) & 0xFFFFull]);
-    s = __dadd_rn(s, W[(row >> 32) & 0xFFFFull]);
-    return __dadd_rn(s, W[row >> 48]);
-}
-
-__device__ __forceinline__ void consider(const DevModel& M, const double* __restrict__ W, uint64_t row,
-                                         Best& best) {
-    double s = row_score(W, row);
-    if (s > 0.0 && s >= best.s) best = consider_slow(M, row, s, best);
-}
-
-__device__ __forceinline__ Best shfl_best(const Best& b, int off) {
-    Best o;
-    o.s = __shfl_xor_sync(0xffffffffu, b.s, off);
-    o.u = __shfl_xor_sync(0xffffffffu, b.u, off);
-    o.row = __shfl_xor_sync(0xffffffffu, b.row, off);
-    return o;
-}
-
-__device__ __forceinline__ Best warp_best(const DevModel& M, Best b) {
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) {
-        Best o = shfl_best(b, off);
-        if (better(M, o, b)) b = o;
-    }
-    return b;
-}
-
-__device__ __forceinline__ Best none() { return Best{0.0, 0.0, kNoRow}; }
 
 // Block-wide argmax; result valid in every thread.
 __device__ Best block_best(const DevModel& M, Best b, Best* red) {
@@ -173,10 +47,8 @@ __device__ Best grid_best(const DevModel& M, const Best* partials, int G, Best* 
     if ((threadIdx.x >> 5) == 0) {
         Best x = none();
         for (int i = lane_id(); i < G; i += 32) {
-            Best p;
-            p.s = __ldcg(&partials[i].s);
-            p.u = __ldcg(&partials[i].u);
-            p.row = __ldcg(reinterpret_cast<const unsigned long long*>(&partials[i].row));
+            Best p{__ldcg(&partials[i].s), __ldcg(&partials[i].u),
+                   __ldcg(reinterpret_cast<const unsigned long long*>(&partials[i].row))};
             if (better(M, p, x)) x = p;
         }
         x = warp_best(M, x);
@@ -188,45 +60,83 @@ __device__ Best grid_best(const DevModel& M, const Best* partials, int G, Best* 
     return r;
 }
 
-// Scan rows[0, nrows) grid-stride with 4 x 128-bit loads in flight per thread.
-__device__ __forceinline__ void scan_rows(const DevModel& M, const double* __restrict__ W,
-                                          const uint64_t* __restrict__ rows, long long nrows, Best& best) {
-    const uint4* v = reinterpret_cast<const uint4*>(rows);
-    const long long nv = nrows >> 1;
-    const long long stride = static_cast<long long>(gridDim.x) * blockDim.x;
-    long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
-    for (; i + 3 * stride < nv; i += 4 * stride) {
-        uint4 a = __ldg(v + i), b = __ldg(v + i + stride), c = __ldg(v + i + 2 * stride),
-              d = __ldg(v + i + 3 * stride);
-        consider(M, W, (static_cast<uint64_t>(a.y) << 32) | a.x, best);
-        consider(M, W, (static_cast<uint64_t>(a.w) << 32) | a.z, best);
-        consider(M, W, (static_cast<uint64_t>(b.y) << 32) | b.x, best);
-        consider(M, W, (static_cast<uint64_t>(b.w) << 32) | b.z, best);
-        consider(M, W, (static_cast<uint64_t>(c.y) << 32) | c.x, best);
-        consider(M, W, (static_cast<uint64_t>(c.w) << 32) | c.z, best);
-        consider(M, W, (static_cast<uint64_t>(d.y) << 32) | d.x, best);
-        consider(M, W, (static_cast<uint64_t>(d.w) << 32) | d.z, best);
+// Grid-wide argmax + barrier in one: every CTA publishes its block winner and takes a
+// ticket; the LAST CTA to arrive reduces the G partials and publishes the single winner
+// record, then releases the generation.  Only one CTA reads the partials (instead of all G
+// CTAs reading all G records — a G^2 hot-line read storm in L2), and waiters read one
+// 24-byte record.  Returns the same winner in every thread of every CTA.
+__device__ Best grid_argmax(const DevModel& M, const Best& mine, Best* partials, Best* winrec, unsigned* count,
+                            unsigned* gen, int G, Best* red) {
+    __shared__ int s_last;
+    __shared__ unsigned s_gen;
+    if (threadIdx.x == 0) {
+        cuda::atomic_ref<unsigned, cuda::thread_scope_device> g(*gen), c(*count);
+        const unsigned my = g.load(cuda::memory_order_relaxed);
+        __stcg(&partials[blockIdx.x].s, mine.s);
+        __stcg(&partials[blockIdx.x].u, mine.u);
+        __stcg(reinterpret_cast<unsigned long long*>(&partials[blockIdx.x].row),
+               static_cast<unsigned long long>(mine.row));
+        const unsigned t = c.fetch_add(1u, cuda::memory_order_acq_rel);
+        s_last = t == static_cast<unsigned>(G) - 1u;
+        s_gen = my;
     }
-    for (; i < nv; i += stride) {
-        uint4 a = __ldg(v + i);
-        consider(M, W, (static_cast<uint64_t>(a.y) << 32) | a.x, best);
-        consider(M, W, (static_cast<uint64_t>(a.w) << 32) | a.z, best);
+    __syncthreads();
+    if (s_last) {
+        if ((threadIdx.x >> 5) == 0) {
+            Best x = none();
+            for (int i = lane_id(); i < G; i += 32) {
+                Best p{__ldcg(&partials[i].s), __ldcg(&partials[i].u),
+                       __ldcg(reinterpret_cast<const unsigned long long*>(&partials[i].row))};
+                if (better(M, p, x)) x = p;
+            }
+            x = warp_best(M, x);
+            if (lane_id() == 0) {
+                red[0] = x;
+                __stcg(&winrec->s, x.s);
+                __stcg(&winrec->u, x.u);
+                __stcg(reinterpret_cast<unsigned long long*>(&winrec->row), static_cast<unsigned long long>(x.row));
+                cuda::atomic_ref<unsigned, cuda::thread_scope_device> g(*gen), c(*count);
+                c.store(0u, cuda::memory_order_relaxed);
+                g.store(s_gen + 1u, cuda::memory_order_release);
+            }
+        }
+    } else if (threadIdx.x == 0) {
+        cuda::atomic_ref<unsigned, cuda::thread_scope_device> g(*gen);
+        while (g.load(cuda::memory_order_acquire) == s_gen) __nanosleep(32);
+        red[0] = Best{__ldcg(&winrec->s), __ldcg(&winrec->u),
+                      __ldcg(reinterpret_cast<const unsigned long long*>(&winrec->row))};
     }
-    if ((nrows & 1) && blockIdx.x == 0 && threadIdx.x == 0) consider(M, W, __ldg(rows + nrows - 1), best);
+    __syncthreads();
+    const Best r = red[0];
+    __syncthreads();
+    return r;
+}
+
+// The thread's running argmax; the slow path runs only when s >= its best score.
+__device__ __forceinline__ void consider(const DevModel& M, const double* __restrict__ W, const double* U,
+                                         uint64_t row, Best& best) {
+    const double s = row_score(W, row);
+    if (s > 0.0 && s >= best.s) {
+        if (s > best.s) {
+            best = Best{s, row_usum(U, row), row};
+            return;
+        }
+        const double u = row_usum(U, row);
+        if (u > best.u || (u == best.u && row != best.row && row_key_less(M, row, best.row))) best = Best{s, u, row};
+    }
+}
+
+__device__ __forceinline__ void consider2(const DevModel& M, const double* __restrict__ W, const double* U,
+                                          const uint4& v, Best& best) {
+    consider(M, W, U, (static_cast<uint64_t>(v.y) << 32) | v.x, best);
+    consider(M, W, U, (static_cast<uint64_t>(v.w) << 32) | v.z, best);
 }
 
 // W[e] = need * U[e] for need = 1 - comp[svc] > 0, else 0 (greedy.hpp:38-41).
-__device__ __forceinline__ void build_W(const DevModel& M, const double* comp, double* W) {
-    const int nW = (M.n + 1) * M.PP;
-    for (int e = threadIdx.x; e < nW; e += blockDim.x) {
-        int svc = e / M.PP;
-        double w = 0.0;
-        if (svc < M.n) {
-            double need = __dadd_rn(1.0, -comp[svc]);
-            if (need > 0.0) w = __dmul_rn(need, __ldg(&M.U[e]));
-        }
-        W[e] = w;
-    }
+__device__ __forceinline__ double w_of(const double* comp, const double* U, int svc, int e, int n) {
+    if (svc >= n) return 0.0;
+    const double need = __dadd_rn(1.0, -comp[svc]);
+    return need > 0.0 ? __dmul_rn(need, U[e]) : 0.0;
 }
 
 __device__ __forceinline__ long long binom(long long a, int q) {
@@ -250,12 +160,44 @@ __device__ __forceinline__ void unrank(long long r, int q, int m, int* out) {
     }
 }
 
+struct GreedySmem {  // byte offsets into dynamic shared memory
+    int W, U, comp, best, evmask, evof, evsvc, xlist, cache, total;
+};
+
+__host__ __device__ inline GreedySmem greedy_layout(int n, int PP, int cache_units) {
+    GreedySmem s;
+    const int nW = (n + 1) * PP;
+    int o = 0;
+    s.W = o;
+    o += nW * 8;
+    s.U = o;
+    o += nW * 8;
+    s.comp = o;
+    o += (n + 1) * 8;
+    s.best = o;
+    o += (n + 1) * 8;
+    s.evmask = o;
+    o += (n + 1) * 4 * 8;
+    s.evof = o;
+    o += (n + 1) * 2;
+    s.evsvc = o;
+    o += (n + 1) * 2;
+    s.xlist = o;
+    o += 256;
+    o = (o + 15) & ~15;
+    s.cache = o;
+    o += cache_units * 16;
+    s.total = o;
+    return s;
+}
+
 }  // namespace
 
 // ---------------------------------------------------------------- K1: base pool rows
 // One warp per support (<= max_mix members, ascending service index); valid templates
 // are written at a host-computed offset in template order (deterministic pool order).
-__global__ void __launch_bounds__(256) enum_base_kernel(const __grid_constant__ DevModel M, const uint32_t* __restrict__ supports,
+__global__ void __launch_bounds__(256) enum_base_kernel(const __grid_constant__ DevModel M,
+                                                        const uint32_t* __restrict__ supports,
                                                         const long long* __restrict__ offsets, int n_supports,
                                                         uint64_t* __restrict__ rows) {
     const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -294,23 +236,34 @@ __global__ void __launch_bounds__(256) enum_base_kernel(const __grid_constant__ 
 }
 
 // ---------------------------------------------------------------- K2+K3: persistent greedy
+// Working set = arena rows [0, n_base + ext_count): the base pool (copied in by the host)
+// followed by extension rows appended on the device.  Rows are processed in 16-byte units
+// (two rows) assigned grid-stride; the first `cache_units / blockDim` units of every
+// thread live in this CTA's shared memory once complete, so a working set of up to
+// ~148 x 200 KB is scanned on-chip every step and only the excess streams from L2/HBM.
 __global__ void __launch_bounds__(kThreads, 1) greedy_kernel(const __grid_constant__ GreedyArgs a) {
     extern __shared__ __align__(16) unsigned char smem[];
     const DevModel& M = a.M;
-    const int n = M.n;
-    const int nW = (n + 1) * M.PP;
+    const int n = M.n, PP = M.PP;
+    const int nW = (n + 1) * PP;
     const int G = gridDim.x;
-    double* W = reinterpret_cast<double*>(smem);
-    double* comp = W + nW;
-    double* best_single = comp + n;
-    uint64_t* ev_mask = reinterpret_cast<uint64_t*>(best_single + n);  // n events x 4 words
-    short* ev_of = reinterpret_cast<short*>(ev_mask + 4 * (n + 1));
-    short* ev_svc = ev_of + n;
-    uint8_t* xlist = reinterpret_cast<uint8_t*>(ev_svc + n + 1);
+    const GreedySmem L = greedy_layout(n, PP, a.cache_units);
+    double* W = reinterpret_cast<double*>(smem + L.W);
+    double* U = reinterpret_cast<double*>(smem + L.U);
+    double* comp = reinterpret_cast<double*>(smem + L.comp);
+    double* best_single = reinterpret_cast<double*>(smem + L.best);
+    uint64_t* ev_mask = reinterpret_cast<uint64_t*>(smem + L.evmask);
+    short* ev_of = reinterpret_cast<short*>(smem + L.evof);
+    short* ev_svc = reinterpret_cast<short*>(smem + L.evsvc);
+    uint8_t* xlist = smem + L.xlist;
+    uint4* cache = reinterpret_cast<uint4*>(smem + L.cache);
     __shared__ Best red[kWarps];
     __shared__ uint64_t unsat[4];
-    __shared__ int s_events, s_first_new, s_done, s_m;
+    __shared__ int s_events, s_first_new, s_done, s_m, s_status;
+    __shared__ long long s_rows;
+    if (threadIdx.x == 0) s_status = kOk;
 
+    for (int e = threadIdx.x; e < nW; e += blockDim.x) U[e] = __ldg(&M.U[e]);
     for (int i = threadIdx.x; i < n; i += blockDim.x) {
         comp[i] = a.comp0[i];
         best_single[i] = M.best_single[i];
@@ -318,6 +271,7 @@ __global__ void __launch_bounds__(kThreads, 1) greedy_kernel(const __grid_consta
     }
     if (threadIdx.x == 0) s_events = 0;
     __syncthreads();
+    for (int e = threadIdx.x; e < nW; e += blockDim.x) W[e] = w_of(comp, U, e / PP, e, n);
 
     // maybe_extend (greedy.hpp:107-119), warp 0, identical in every CTA.
     auto maybe_extend = [&]() {
@@ -359,7 +313,8 @@ __global__ void __launch_bounds__(kThreads, 1) greedy_kernel(const __grid_consta
     // Device-side extend_candidate_pool for the events recorded since `first`
     // (config_enum.hpp:206-211 with must_include = i, allowed = unsat, max_mix = 4):
     // every support S, max_mix < |S| <= 4, i in S subset-of unsat, not covered by an earlier
-    // event e' (i_e' in S subset-of unsat_e'), times every feasible template.
+    // event e' (i_e' in S subset-of unsat_e'), times every feasible template.  One thread
+    // per (support, template) pair; warp-aggregated appends keep the stores coalesced.
     auto extend_new = [&](int first, int last) {
         for (int e = first; e < last; ++e) {
             __syncthreads();
@@ -410,8 +365,7 @@ __global__ void __launch_bounds__(kThreads, 1) greedy_kernel(const __grid_consta
                         S[q++] = v;
                     }
                     if (!placed) S[q++] = ie;
-                    // covered by an earlier extension event?
-                    for (int j = 0; j < k && ok; ++j) {
+                    for (int j = 0; j < k && ok; ++j) {  // covered by an earlier event?
                         int ev = ev_of[S[j]];
                         if (ev >= 0 && ev < e) {
                             const uint64_t* mk = ev_mask + ev * 4;
@@ -426,9 +380,9 @@ __global__ void __launch_bounds__(kThreads, 1) greedy_kernel(const __grid_consta
                         if (j < k) {
                             int p = static_cast<int>((tp >> (8 * (j + 1))) & 0xFF);
                             ok &= (M.pat_mask[p] & ~M.feas_mask[S[j]]) == 0;
-                            code = static_cast<uint64_t>(S[j] * M.PP + p);
+                            code = static_cast<uint64_t>(S[j] * PP + p);
                         } else {
-                            code = static_cast<uint64_t>(n * M.PP);
+                            code = static_cast<uint64_t>(n * PP);
                         }
                         row |= code << (16 * j);
                     }
@@ -438,10 +392,10 @@ __global__ void __launch_bounds__(kThreads, 1) greedy_kernel(const __grid_consta
                     unsigned long long at = 0;
                     if (lane_id() == 0) at = atomicAdd(&a.st->ext_count, static_cast<unsigned long long>(__popc(b)));
                     at = __shfl_sync(0xffffffffu, at, 0);
-                    if (at + __popc(b) > static_cast<unsigned long long>(a.ext_cap)) {
+                    if (a.n_base + static_cast<long long>(at + __popc(b)) > a.cap) {
                         if (lane_id() == 0) atomicExch(&a.st->status, static_cast<int>(kExtOverflow));
                     } else if (ok) {
-                        a.ext_rows[at + __popc(b & lanemask_lt())] = row;
+                        a.rows[a.n_base + static_cast<long long>(at) + __popc(b & lanemask_lt())] = row;
                     }
                 }
             }
@@ -452,69 +406,140 @@ __global__ void __launch_bounds__(kThreads, 1) greedy_kernel(const __grid_consta
     unsigned* bg = &a.st->bar_gen;
     int status = kOk;
 
-    maybe_extend();
-    if (s_events > s_first_new) {
+    // Rows in the working set and the overflow status change only at extension events:
+    // read them once after each extension barrier instead of every step.
+    long long N = a.n_base;
+    auto extend_and_sync = [&]() {
         extend_new(s_first_new, s_events);
         grid_barrier(bc, bg, G);
-    }
+        if (threadIdx.x == 0) {
+            s_status = *reinterpret_cast<volatile int*>(&a.st->status);
+            s_rows = a.n_base + static_cast<long long>(*reinterpret_cast<volatile unsigned long long*>(&a.st->ext_count));
+        }
+        __syncthreads();
+        N = s_rows;
+    };
+    maybe_extend();
+    if (s_events > s_first_new) extend_and_sync();
+
+    const uint4* rows4 = reinterpret_cast<const uint4*>(a.rows);
+    const long long GT = static_cast<long long>(G) * blockDim.x;
+    const long long my0 = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const int J = a.cache_units / static_cast<int>(blockDim.x);  // cached units per thread
+    int cj = 0;                                                  // units of mine cached so far
+
     int step = 0;
     long long rows_total = 0;
+    const bool timer = a.phase_timers && blockIdx.x == 0 && threadIdx.x == 0;
+    unsigned long long ph[5] = {0, 0, 0, 0, 0};
+    unsigned long long tp = timer ? globaltimer() : 0;
+    auto mark = [&](int k) {
+        if (timer) {
+            unsigned long long t = globaltimer();
+            ph[k] += t - tp;
+            tp = t;
+        }
+    };
     while (!s_done) {
-        if (*reinterpret_cast<volatile int*>(&a.st->status) != kOk) {
-            status = *reinterpret_cast<volatile int*>(&a.st->status);
+        if (s_status != kOk) {
+            status = s_status;
             break;
         }
         if (step >= a.cap_steps) {
             status = kStepOverflow;
             break;
         }
-        build_W(M, comp, W);
-        __syncthreads();
-        const long long n_ext =
-            static_cast<long long>(*reinterpret_cast<volatile unsigned long long*>(&a.st->ext_count));
+        mark(4);
+        const long long NU = N >> 1;  // complete 16-byte units
+        while (cj < J && my0 + cj * GT < NU) {  // pull newly complete units of mine on-chip
+            cache[cj * blockDim.x + threadIdx.x] = __ldcg(rows4 + my0 + cj * GT);
+            ++cj;
+        }
         Best best = none();
-        scan_rows(M, W, a.base_rows, a.n_base, best);
-        scan_rows(M, W, a.ext_rows, n_ext, best);
+        {
+            int j = 0;
+            for (; j + 3 < cj; j += 4) {
+                const uint4 v0 = cache[(j + 0) * blockDim.x + threadIdx.x];
+                const uint4 v1 = cache[(j + 1) * blockDim.x + threadIdx.x];
+                const uint4 v2 = cache[(j + 2) * blockDim.x + threadIdx.x];
+                const uint4 v3 = cache[(j + 3) * blockDim.x + threadIdx.x];
+                consider2(M, W, U, v0, best);
+                consider2(M, W, U, v1, best);
+                consider2(M, W, U, v2, best);
+                consider2(M, W, U, v3, best);
+            }
+            for (; j < cj; ++j) consider2(M, W, U, cache[j * blockDim.x + threadIdx.x], best);
+            long long u = my0 + static_cast<long long>(cj) * GT;
+            for (; u + 3 * GT < NU; u += 4 * GT) {
+                // rows appended during this launch: L2-coherent loads (never the non-coherent path)
+                const uint4 v0 = __ldcg(rows4 + u), v1 = __ldcg(rows4 + u + GT), v2 = __ldcg(rows4 + u + 2 * GT),
+                            v3 = __ldcg(rows4 + u + 3 * GT);
+                consider2(M, W, U, v0, best);
+                consider2(M, W, U, v1, best);
+                consider2(M, W, U, v2, best);
+                consider2(M, W, U, v3, best);
+            }
+            for (; u < NU; u += GT) consider2(M, W, U, __ldcg(rows4 + u), best);
+            if ((N & 1) && my0 == 0) consider(M, W, U, __ldcg(a.rows + N - 1), best);
+        }
         best = block_best(M, best, red);
-        Best* part = a.partials + (step & 1) * G;
-        if (threadIdx.x == 0) part[blockIdx.x] = best;
-        grid_barrier(bc, bg, G);
-        const Best win = grid_best(M, part, G, red);
+        mark(0);
+        const Best win = grid_argmax(M, best, a.partials, a.partials + G, bc, bg, G, red);
+        mark(1);
         if (win.row == kNoRow) {
             status = kNoPositive;
             break;
         }
-        rows_total += a.n_base + n_ext;
+        rows_total += N;
         if (threadIdx.x == 0) {
             for (int j = 0; j < 4; ++j) {
                 int code = static_cast<int>((win.row >> (16 * j)) & 0xFFFFull);
-                int svc = code / M.PP;
-                if (svc < n) comp[svc] = __dadd_rn(comp[svc], __ldg(&M.U[code]));
+                int svc = code / PP;
+                if (svc < n) comp[svc] = __dadd_rn(comp[svc], U[code]);
             }
             if (blockIdx.x == 0) {
                 a.pick_row[step] = win.row;
                 a.pick_score[step] = win.s;
-                a.pick_rows[step] = a.n_base + n_ext;
+                a.pick_rows[step] = N;
             }
         }
         __syncthreads();
+        // only the winner's (<= 4) services changed: refresh their W rows
+        for (int e = threadIdx.x; e < 4 * PP; e += blockDim.x) {
+            const int j = e / PP, p = e - j * PP;
+            const int svc = static_cast<int>((win.row >> (16 * j)) & 0xFFFFull) / PP;
+            if (svc < n) W[svc * PP + p] = w_of(comp, U, svc, svc * PP + p, n);
+        }
         ++step;
-        maybe_extend();
-        if (s_events > s_first_new) {
-            extend_new(s_first_new, s_events);
-            grid_barrier(bc, bg, G);
+        mark(2);
+        maybe_extend();  // ends with __syncthreads (also publishes the W refresh)
+        mark(3);
+        if (s_events > s_first_new) extend_and_sync();
+    }
+    mark(4);
+    if (blockIdx.x == 0) {  // one coalesced copy of the plan to host-mapped memory
+        for (int i = threadIdx.x; i < step; i += blockDim.x) {
+            a.host_pick_row[i] = a.pick_row[i];
+            a.host_pick_score[i] = a.pick_score[i];
+            a.host_pick_rows[i] = a.pick_rows[i];
         }
     }
     if (blockIdx.x == 0 && threadIdx.x == 0) {
-        a.st->n_steps = step;
-        a.st->n_events = s_events;
-        a.st->rows_scored = rows_total;
         if (status != kOk) atomicExch(&a.st->status, status);
+        __threadfence();
+        GreedyState* o = a.out;  // host-mapped: the host reads it after one stream sync
+        for (int k = 0; k < 5; ++k) o->phase_ns[k] = ph[k];
+        o->n_steps = step;
+        o->n_events = s_events;
+        o->rows_scored = rows_total;
+        o->ext_count = *reinterpret_cast<volatile unsigned long long*>(&a.st->ext_count);
+        o->status = *reinterpret_cast<volatile int*>(&a.st->status);
+        __threadfence_system();
     }
 }
 
-// ---------------------------------------------------------------- K4: top-K
-// K rounds of "argmax among rows strictly less preferred than the previous pick";
+// ---------------------------------------------------------------- K4 (k > 32): top-K
+// k rounds of "argmax among rows strictly less preferred than the previous pick";
 // because candidate_preferred is a total order this yields the reference's sorted
 // top-K (mcts.hpp:68-71) without materialising or sorting all scores.
 __global__ void __launch_bounds__(kThreads, 1) topk_kernel(const __grid_constant__ TopkArgs a) {
@@ -528,7 +553,7 @@ __global__ void __launch_bounds__(kThreads, 1) topk_kernel(const __grid_constant
     for (int i = threadIdx.x; i < M.n; i += blockDim.x) comp[i] = a.comp[i];
     if (threadIdx.x < 4) mask[threadIdx.x] = a.svc_mask ? a.svc_mask[threadIdx.x] : ~0ull;
     __syncthreads();
-    build_W(M, comp, W);
+    for (int e = threadIdx.x; e < nW; e += blockDim.x) W[e] = w_of(comp, M.U, e / M.PP, e, M.n);
     __syncthreads();
     const int G = gridDim.x;
     const long long total = a.index ? a.n_index : a.n_rows;
@@ -550,12 +575,15 @@ __global__ void __launch_bounds__(kThreads, 1) topk_kernel(const __grid_constant
             const double s = row_score(W, row);
             if (!(s > 0.0)) continue;
             if (r > 0 && s >= last.s) {
-                Best c{s, row_usum(M, row), row};
+                Best c{s, row_usum(M.U, row), row};
                 if (!better(M, last, c)) continue;
                 if (best.row == kNoRow || better(M, c, best)) best = c;
                 continue;
             }
-            if (s >= best.s) best = consider_slow(M, row, s, best);
+            if (s >= best.s) {
+                Best c{s, row_usum(M.U, row), row};
+                if (best.row == kNoRow || better(M, c, best)) best = c;
+            }
         }
         best = block_best(M, best, red);
         Best* part = a.partials + (r & 1) * G;
@@ -571,13 +599,8 @@ __global__ void __launch_bounds__(kThreads, 1) topk_kernel(const __grid_constant
 }
 
 // ---------------------------------------------------------------- launch helpers
-size_t greedy_smem_bytes(int n, int PP) {
-    size_t b = static_cast<size_t>((n + 1) * PP) * 8;  // W
-    b += static_cast<size_t>(n) * 8 * 2;              // comp + best_single
-    b += static_cast<size_t>(n + 1) * 4 * 8;          // event masks
-    b += static_cast<size_t>(n) * 2 + static_cast<size_t>(n + 1) * 2;  // ev_of, ev_svc
-    b += 256 + 16;                                    // xlist
-    return (b + 15) & ~static_cast<size_t>(15);
+size_t greedy_smem_bytes(int n, int PP, int cache_units) {
+    return static_cast<size_t>(greedy_layout(n, PP, cache_units).total);
 }
 
 size_t topk_smem_bytes(int n, int PP) { return static_cast<size_t>((n + 1) * PP + n) * 8 + 16; }
