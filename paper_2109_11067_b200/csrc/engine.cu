@@ -21,6 +21,8 @@ const void* enum_base_kernel_ptr();
 int kernel_threads();
 size_t topk1_smem_bytes(int n, int PP, int km);
 int topk1_threads();
+int topk1_rows_per_cta();
+constexpr int kTopkMaxCtas = 4096;  // 8M candidate rows per top-K call
 const void* topk1_kernel_ptr(int km);
 
 namespace {
@@ -308,7 +310,7 @@ Slot* Engine::acquire() {
     CK(cudaMemset(s->bar, 0, sizeof(unsigned) * 2));
     CK(cudaMalloc(&s->ticket, sizeof(unsigned)));
     CK(cudaMemset(s->ticket, 0, sizeof(unsigned)));
-    CK(cudaMalloc(&s->tpart, sizeof(Best) * 64 * 32));
+    CK(cudaMalloc(&s->tpart, sizeof(Best) * kTopkMaxCtas * 32));
     CK(cudaHostAlloc(&s->io, sizeof(HostIO), cudaHostAllocMapped));
     std::memset(s->io, 0, sizeof(HostIO));
     Slot* raw = s.get();
@@ -474,7 +476,9 @@ std::vector<long long> Engine::topk(const std::vector<double>& comp, int k, cons
         a.out_row = s->io->top_rows;
         a.n_out = &s->io->top_n;
         const int T = topk1_threads(), km = 32;
-        int G = static_cast<int>(std::min<long long>((total + 2047) / 2048, 64));
+        const long long per = topk1_rows_per_cta();
+        if ((total + per - 1) / per > kTopkMaxCtas) throw ArgumentError("top-K candidate set too large");
+        int G = static_cast<int>((total + per - 1) / per);
         G = std::max(G, 1);
         void* args[] = {&a};
         CK(cudaLaunchKernel(topk1_kernel_ptr(km), G, T, args, topk1_smem_bytes(m_.n, m_.PP, km), s->stream));

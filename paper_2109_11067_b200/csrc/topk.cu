@@ -18,6 +18,8 @@ namespace {
 
 constexpr int kTopkThreads = 256;
 constexpr int kTopkWarps = kTopkThreads / 32;
+constexpr int kRowsPerThread = 8;  // the host sizes the grid so every row has a thread slot
+constexpr int kCandCap = 1024;     // per-CTA candidates above the threshold held in smem
 
 __device__ __forceinline__ unsigned lane() { return threadIdx.x & 31u; }
 
@@ -55,13 +57,16 @@ __device__ __forceinline__ void warp_offer(const DevModel& M, Best& wl, const Be
 
 }  // namespace
 
-__global__ void __launch_bounds__(kTopkThreads) topk1_kernel(const __grid_constant__ Topk1Args a) {
+__global__ void __launch_bounds__(kTopkThreads, 1) topk1_kernel(const __grid_constant__ Topk1Args a) {
     extern __shared__ __align__(16) unsigned char smem[];
     const DevModel& M = a.M;
     const int nW = (M.n + 1) * M.PP;
     double* W = reinterpret_cast<double*>(smem);
     double* comp = W + nW;
     Best* wlist = reinterpret_cast<Best*>(comp + M.n + 1);  // [warps][32]
+    Best* cand = wlist + kTopkWarps * 32;                    // [kCandCap]
+    __shared__ double thr[kTopkThreads];
+    __shared__ int n_cand;
     __shared__ uint64_t mask[4];
     __shared__ bool last;
     const int k = a.k;
@@ -79,16 +84,21 @@ __global__ void __launch_bounds__(kTopkThreads) topk1_kernel(const __grid_consta
     }
     __syncthreads();
 
-    Best wl = nil();
+    // Pass 1: every thread scores its (<= kRowsPerThread) rows into registers.
     const int warp = threadIdx.x >> 5;
     const long long total = a.index ? a.n_index : a.n_rows;
-    const long long wstride = static_cast<long long>(gridDim.x) * blockDim.x;
-    for (long long base = static_cast<long long>(blockIdx.x) * blockDim.x + warp * 32; base < total; base += wstride) {
-        const long long i = base + lane();
-        Best c = nil();
-        bool ok = i < total;
-        if (ok) {
+    const long long stride = static_cast<long long>(gridDim.x) * blockDim.x;
+    uint64_t myrow[kRowsPerThread];
+    double mys[kRowsPerThread];
+    double tmax = 0.0;
+#pragma unroll
+    for (int r = 0; r < kRowsPerThread; ++r) {
+        const long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x + r * stride;
+        mys[r] = 0.0;
+        myrow[r] = kNoRow;
+        if (i < total) {
             const uint64_t row = __ldg(a.rows + (a.index ? a.index[i] : i));
+            bool ok = true;
             if (a.svc_mask) {
                 bool hit = false;
 #pragma unroll
@@ -102,30 +112,72 @@ __global__ void __launch_bounds__(kTopkThreads) topk1_kernel(const __grid_consta
                 double s = __dadd_rn(W[row & 0xFFFFull], W[(row >> 16) & 0xFFFFull]);
                 s = __dadd_rn(s, W[(row >> 32) & 0xFFFFull]);
                 s = __dadd_rn(s, W[row >> 48]);
-                ok = s > 0.0;
-                c = Best{s, 0.0, row};
+                if (s > 0.0) {
+                    mys[r] = s;
+                    myrow[r] = row;
+                    tmax = fmax(tmax, s);
+                }
             }
         }
-        const double kth = __shfl_sync(0xffffffffu, wl.s, k - 1);
-        ok = ok && c.s >= kth;
-        if (ok) {
-            double u = 0.0;
-#pragma unroll
-            for (int j = 0; j < 4; ++j) u = __dadd_rn(u, __ldg(&M.U[(c.row >> (16 * j)) & 0xFFFFull]));
-            c.u = u;
-        }
-        warp_offer(M, wl, c, ok, k);
     }
-
-    // block merge by warp 0
-    wlist[warp * 32 + lane()] = wl;
+    // Threshold: T = the k-th largest per-thread maximum in this CTA.  At least k rows of
+    // the CTA score >= T, so the CTA's exact top-k lies among its rows with s >= T.
+    thr[threadIdx.x] = tmax;
+    if (threadIdx.x == 0) n_cand = 0;
+    __syncthreads();
+    for (int k2 = 2; k2 <= kTopkThreads; k2 <<= 1)  // bitonic sort, descending
+        for (int j = k2 >> 1; j > 0; j >>= 1) {
+            const int t = threadIdx.x, p = t ^ j;
+            if (p > t) {
+                const double x = thr[t], y = thr[p];
+                if (((t & k2) == 0) ? (x < y) : (x > y)) {
+                    thr[t] = y;
+                    thr[p] = x;
+                }
+            }
+            __syncthreads();
+        }
+    const double T = thr[k - 1];
+#pragma unroll
+    for (int r = 0; r < kRowsPerThread; ++r)
+        if (myrow[r] != kNoRow && mys[r] >= T) {
+            const int at = atomicAdd(&n_cand, 1);
+            if (at < kCandCap) cand[at] = Best{mys[r], 0.0, myrow[r]};
+        }
+    __syncthreads();
+    const int nc = n_cand;
+    if (warp == 0) {
+        Best bl = nil();
+        if (nc <= kCandCap) {  // exact top-k of the candidates (warp-distributed insertion)
+            for (int b0 = 0; b0 < nc; b0 += 32) {
+                const int i = b0 + static_cast<int>(lane());
+                Best c = i < nc ? cand[i] : nil();
+                if (i < nc) c.u = dev::row_usum(M.U, c.row);
+                warp_offer(M, bl, c, i < nc, k);
+            }
+        }
+        wlist[lane()] = bl;
+    }
+    if (nc > kCandCap) {  // pathological ties at T: every warp offers all its rows (exact)
+        Best wl = nil();
+#pragma unroll
+        for (int r = 0; r < kRowsPerThread; ++r) {
+            Best c{mys[r], 0.0, myrow[r]};
+            const bool ok = myrow[r] != kNoRow;
+            if (ok) c.u = dev::row_usum(M.U, c.row);
+            warp_offer(M, wl, c, ok, k);
+        }
+        __syncthreads();
+        wlist[warp * 32 + lane()] = wl;
+    }
     __syncthreads();
     if (warp == 0) {
-        Best bl = wl;
-        for (int w = 1; w < kTopkWarps; ++w) {
-            const Best c = wlist[w * 32 + lane()];
-            warp_offer(M, bl, c, static_cast<int>(lane()) < k && c.row != kNoRow, k);
-        }
+        Best bl = wlist[lane()];
+        if (nc > kCandCap)
+            for (int w = 1; w < kTopkWarps; ++w) {
+                const Best c = wlist[w * 32 + lane()];
+                warp_offer(M, bl, c, static_cast<int>(lane()) < k && c.row != kNoRow, k);
+            }
         if (gridDim.x == 1) {
             const bool v = static_cast<int>(lane()) < k && bl.row != kNoRow;
             const unsigned valid = __ballot_sync(0xffffffffu, v);
@@ -160,9 +212,11 @@ __global__ void __launch_bounds__(kTopkThreads) topk1_kernel(const __grid_consta
 }
 
 size_t topk1_smem_bytes(int n, int PP, int) {
-    return static_cast<size_t>((n + 1) * PP + n + 1) * 8 + static_cast<size_t>(kTopkWarps) * 32 * sizeof(Best);
+    return static_cast<size_t>((n + 1) * PP + n + 1) * 8 +
+           static_cast<size_t>(kTopkWarps * 32 + kCandCap) * sizeof(Best);
 }
 int topk1_threads() { return kTopkThreads; }
+int topk1_rows_per_cta() { return kTopkThreads * kRowsPerThread; }
 int topk1_max_k() { return 32; }
 const void* topk1_kernel_ptr(int) { return reinterpret_cast<const void*>(&topk1_kernel); }
 
