@@ -43,6 +43,7 @@ WORKLOADS = {
     "slos24_greedy": "fixtures/slos_24.json (24 svc): fast_algo from zero completion",
     "gen24_8.7_greedy": "gen_workload(24, lognormal mu=8.7, sigma=0.6, seed 4242): fast_algo (~974 GPUs)",
     "gen48_7.0_greedy": "gen_workload(48, lognormal mu=7.0, sigma=0.6, seed 4242): fast_algo (~372 GPUs)",
+    "gen128_8.0_greedy": "gen_workload(128, lognormal mu=8.0, sigma=0.6, seed 4242): fast_algo (stress, config #5)",
 }
 
 
@@ -56,6 +57,8 @@ def load_workload(name, rank=0):
         ps, sv = S.gen(24, 8.7)
     elif name.startswith("gen48_7.0"):
         ps, sv = S.gen(48, 7.0)
+    elif name.startswith("gen128_8.0"):
+        ps, sv = S.gen(128, 8.0)
     else:
         raise SystemExit(f"unknown workload {name}")
     return ps, sv
@@ -94,6 +97,22 @@ class ClockSampler:
         self._t.start()
 
     def _run(self):
+        try:  # NVML directly: ~20 ms sampling (nvidia-smi takes ~100 ms per invocation)
+            import pynvml as N
+
+            N.nvmlInit()
+            h = N.nvmlDeviceGetHandleByIndex(self.index)
+            mx = N.nvmlDeviceGetMaxClockInfo(h, N.NVML_CLOCK_SM)
+            bits = [N.nvmlClocksEventReasonHwSlowdown, N.nvmlClocksEventReasonHwThermalSlowdown,
+                    N.nvmlClocksEventReasonSwThermalSlowdown, N.nvmlClocksEventReasonSwPowerCap]
+            while not self._stop.is_set():
+                r = N.nvmlDeviceGetCurrentClocksEventReasons(h)
+                self.samples.append([str(self.index), str(N.nvmlDeviceGetClockInfo(h, N.NVML_CLOCK_SM)), str(mx),
+                                     hex(r)] + ["Active" if r & b else "Not Active" for b in bits])
+                self._stop.wait(0.02)
+            return
+        except Exception:
+            pass
         while not self._stop.is_set():
             try:
                 out = subprocess.run(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",

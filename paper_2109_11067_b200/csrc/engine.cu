@@ -272,7 +272,6 @@ Engine::Engine(const Rules& rules, std::map<std::string, ModelProfile> profiles,
 
 Engine::~Engine() {
     cudaSetDevice(device_);
-    slots_.clear();
     for (void* p : dev_allocs_) cudaFree(p);
 }
 
@@ -288,12 +287,33 @@ Config Engine::config_of(uint64_t row) const {
     return c;
 }
 
+namespace {
+
+// Per-call resources are context-independent (sized for n <= 255 and any grid), so they are
+// pooled per device for the whole process: creating a PlanContext (the e2e path) never
+// pays for stream creation, pinned-mapped host allocations or arena cudaMallocs twice.
+struct SlotPool {
+    std::mutex mu;
+    std::vector<Slot*> free;
+};
+SlotPool& slot_pool(int device) {
+    static std::mutex m;
+    static std::map<int, SlotPool*> pools;  // intentionally leaked: lives until process exit
+    std::lock_guard<std::mutex> g(m);
+    auto& p = pools[device];
+    if (!p) p = new SlotPool;
+    return *p;
+}
+
+}  // namespace
+
 Slot* Engine::acquire() {
+    SlotPool& pool = slot_pool(device_);
     {
-        std::lock_guard<std::mutex> g(mu_);
-        if (!free_.empty()) {
-            Slot* s = free_.back();
-            free_.pop_back();
+        std::lock_guard<std::mutex> g(pool.mu);
+        if (!pool.free.empty()) {
+            Slot* s = pool.free.back();
+            pool.free.pop_back();
             return s;
         }
     }
@@ -304,8 +324,8 @@ Slot* Engine::acquire() {
     CK(cudaEventCreate(&s->e0));
     CK(cudaEventCreate(&s->e1));
     CK(cudaMalloc(&s->st, sizeof(GreedyState)));
-    CK(cudaMalloc(&s->partials, sizeof(Best) * 2 * num_sms_ * std::max(greedy_blocks_per_sm_, topk_blocks_per_sm_)));
-    CK(cudaMalloc(&s->ev_svc, sizeof(int) * (m_.n + 1)));
+    CK(cudaMalloc(&s->partials, sizeof(Best) * 2 * 1024));
+    CK(cudaMalloc(&s->ev_svc, sizeof(int) * (kMaxServices + 1)));
     CK(cudaMalloc(&s->bar, sizeof(unsigned) * 2));
     CK(cudaMemset(s->bar, 0, sizeof(unsigned) * 2));
     CK(cudaMalloc(&s->ticket, sizeof(unsigned)));
@@ -313,15 +333,13 @@ Slot* Engine::acquire() {
     CK(cudaMalloc(&s->tpart, sizeof(Best) * kTopkMaxCtas * 32));
     CK(cudaHostAlloc(&s->io, sizeof(HostIO), cudaHostAllocMapped));
     std::memset(s->io, 0, sizeof(HostIO));
-    Slot* raw = s.get();
-    std::lock_guard<std::mutex> g2(mu_);
-    slots_.push_back(std::move(s));
-    return raw;
+    return s.release();
 }
 
 void Engine::release(Slot* s) {
-    std::lock_guard<std::mutex> g(mu_);
-    free_.push_back(s);
+    SlotPool& pool = slot_pool(device_);
+    std::lock_guard<std::mutex> g(pool.mu);
+    pool.free.push_back(s);
 }
 
 void Engine::ensure_ext(Slot* s, long long rows) {
@@ -370,7 +388,9 @@ void Engine::fast_algo(const std::vector<double>& comp, std::vector<uint64_t>& r
         s->cap_steps = static_cast<int>(cap_steps);
     }
     const long long n_base = static_cast<long long>(base_rows_.size());
-    ensure_ext(s, n_base + std::min<long long>(ext_bound_, std::max<long long>(s->ext_cap - n_base, 1 << 20)));
+    // Arena = base + the all-feasible extension bound (every support with max_mix < |S| <= 4),
+    // capped at 3G rows (24 GB); the kernel reports overflow and the call is retried larger.
+    ensure_ext(s, n_base + std::min<long long>(ext_bound_, 3ll << 30));
 
     const int T = kernel_threads();
     const size_t smem = greedy_smem_bytes(m_.n, m_.PP, cache_units_);
@@ -411,7 +431,7 @@ void Engine::fast_algo(const std::vector<double>& comp, std::vector<uint64_t>& r
         CK(cudaEventElapsedTime(&ms, s->e0, s->e1));
         const GreedyState h = s->io->res;
         if (h.status == kExtOverflow && attempt < 4) {
-            long long need = n_base + static_cast<long long>(h.ext_count) * 2 + (1 << 20);
+            long long need = n_base + static_cast<long long>(h.ext_count) * 4 + (1 << 20);
             ensure_ext(s, std::max(need, s->ext_cap * 2));
             continue;
         }

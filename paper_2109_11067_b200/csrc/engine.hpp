@@ -91,9 +91,6 @@ class Engine {
     long long ext_bound_ = 0;
     int cache_units_ = 0;  // greedy shared-memory row cache per CTA (16-byte units)
 
-    std::mutex mu_;
-    std::vector<std::unique_ptr<Slot>> slots_;
-    std::vector<Slot*> free_;
 };
 
 }  // namespace mgb
