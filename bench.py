@@ -17,8 +17,10 @@ value  : rows scored / device time with the context (device tables + base pool) 
 e2e    : the same metric through the C-ABI from HOST inputs: each step builds the context
          from host profiles/services (host->device table upload, base-pool enumeration,
          base rows copied back) and returns the plan to host memory.
-N > 1  : torchrun, one process per GPU, each rank plans an independent GA island (seed
-         24 + rank) — weak scaling, no data-path collective; ranks barrier + MAX-reduce time.
+N > 1  : torchrun, one process per GPU; the GA runs as islands (paper_2109_11067_b200/dist.py:
+         rank 0 keeps seed 24, rank r uses mix_seed(24, r)); the only exchanges are an NCCL
+         all-gather of (gpus, slack, rank) and one plan broadcast — weak scaling; ranks
+         barrier + MAX-reduce the device time.
 --impl reference : the reference's own CPU implementation (oracle/_ref, the unmodified
          reference headers) on the host cores, rank 0 only, bounded sample (see below).
 """
@@ -71,10 +73,17 @@ def ga_params(rank, workers):
                        slow=mp.MctsParams(budget_iters=48))
 
 
-def run_step(mp, name, ctx, sv, ps, rank, workers):
-    """One optimizer pass; returns the plan (list of GpuConfig)."""
+def run_step(mp, name, ctx, sv, ps, rank, workers, world=1):
+    """One optimizer pass; returns the plan (list of GpuConfig).  With N > 1 ranks the GA
+    runs as islands (one per GPU, dist.island_two_phase): an all-gather of fitness keys and
+    one plan broadcast are the only exchanges."""
     if name.endswith("_ga"):
-        dep = mp.two_phase(sv, ps, mp.PartitionRuleSet.defaults(), ga_params(rank, workers), ctx=ctx)
+        if world > 1:
+            from paper_2109_11067_b200 import dist as D
+
+            _, dep = D.island_two_phase(ctx, ga_params(0, workers))
+        else:
+            dep = mp.two_phase(sv, ps, mp.PartitionRuleSet.defaults(), ga_params(rank, workers), ctx=ctx)
         return [g.config for g in dep.gpus]
     return mp.fast_algo(mp.zero_completion(len(sv)), ctx)
 
@@ -255,7 +264,7 @@ def main():
         torch.cuda.synchronize()
 
     for _ in range(max(args.warmup, 0)):
-        plan = run_step(mp, args.workload, ctx, sv, ps, rank, workers)
+        plan = run_step(mp, args.workload, ctx, sv, ps, rank, workers, world)
 
     # ---- resident (value)
     clocks = ClockSampler(local)
@@ -268,7 +277,7 @@ def main():
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
-        plan = run_step(mp, args.workload, ctx, sv, ps, rank, workers)
+        plan = run_step(mp, args.workload, ctx, sv, ps, rank, workers, world)
         torch.cuda.synchronize()
         e1.record()
         torch.cuda.synchronize()
@@ -287,7 +296,7 @@ def main():
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
         c2 = mp.make_plan_context(sv, ps, mp.PartitionRuleSet.defaults(), device=local)
-        run_step(mp, args.workload, c2, sv, ps, rank, workers)
+        run_step(mp, args.workload, c2, sv, ps, rank, workers, world)
         torch.cuda.synchronize()
         e1.record()
         torch.cuda.synchronize()
@@ -325,7 +334,7 @@ def main():
             "config": {"workload": args.workload, "description": WORKLOADS[args.workload],
                        "gpus_used": len(plan), "rows_per_step": rows / args.steps,
                        "plan_ms": dev_ms_max / args.steps, "l2": "flushed (512 MiB write) between steps",
-                       "parallelism": f"{world} independent GA islands" if world > 1 else "1 GPU",
+                       "parallelism": f"{world} GA islands (NCCL all-gather of fitness + plan broadcast)" if world > 1 else "1 GPU",
                        "ga_workers_per_rank": workers},
             "e2e": {"value": e2e_rows_all / (e2e_ms_max / 1e3), "unit": "configs/s",
                     "h2d_bytes_per_step": h2d // args.steps, "d2h_bytes_per_step": d2h // args.steps,

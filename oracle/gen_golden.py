@@ -153,7 +153,16 @@ def gen_partitions(ref):
     return out
 
 
-SECTIONS = {"greedy": gen_greedy, "mcts": gen_mcts, "ga": gen_ga, "topk": gen_topk, "partitions": gen_partitions}
+def gen_greedy_big(ref):
+    """gen(48, 7.0): ~6 minutes on one core (SURVEY §6); pins the n=48 plan bit-exactly."""
+    p2, sv = S.gen(48, 7.0)
+    e = greedy_entry(p2, sv, ref)
+    print(f"greedy gen48_7.0: {len(e['plan'])} GPUs, {e['rows_scored']} rows", flush=True)
+    return {"gen48_7.0": e}
+
+
+SECTIONS = {"greedy": gen_greedy, "mcts": gen_mcts, "ga": gen_ga, "topk": gen_topk, "partitions": gen_partitions,
+            "greedy_big": gen_greedy_big}
 
 
 def main(argv):
@@ -170,14 +179,3 @@ def main(argv):
 
 if __name__ == "__main__":
     main(sys.argv[1:])
-
-
-def gen_greedy_big(ref):
-    """gen(48, 7.0): ~6 minutes on one core (SURVEY §6); pins the n=48 plan bit-exactly."""
-    p2, sv = S.gen(48, 7.0)
-    e = greedy_entry(p2, sv, ref)
-    print(f"greedy gen48_7.0: {len(e['plan'])} GPUs, {e['rows_scored']} rows", flush=True)
-    return {"gen48_7.0": e}
-
-
-SECTIONS["greedy_big"] = gen_greedy_big
