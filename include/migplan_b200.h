@@ -187,6 +187,52 @@ typedef void (*mig_mcts_trace_fn)(void* user, int32_t iter, int32_t depth, int32
 int mig_mcts_solve(mig_ctx* ctx, const double* comp, int32_t n, const mig_mcts_params* params, uint64_t seed,
                    mig_config* out, int32_t cap, int32_t* n_out, mig_mcts_trace_fn trace, void* user);
 
+/* ---- MCTS throughput mode: root-parallel rollouts (product extension, rollout.cu) ----
+ * The reference runs rollouts one at a time from a sequential mt19937_64 stream
+ * (rollout, mcts.hpp:122-143; memoized per unsatisfied-set key, RolloutCache
+ * mcts.hpp:47-50).  mig_rollouts runs n_rollouts of them from one root concurrently:
+ *   - each step is the reference's rollout step (top-K of the BASE pool under the
+ *     current completion, memoized by the unsatisfied bitmap, uniform pick, add);
+ *   - draw t of rollout r is Philox4x32-10(key = seed, counter = (t, id_offset + r)),
+ *     index = floor(draw * |pool| / 2^64);
+ *   - rollouts advance in lock-step rounds; a key first reached in round d takes its pool
+ *     from the completion vector of the lowest-indexed rollout that reached it in round d;
+ *     the cache persists across the call's batches (rollouts [0,batch), [batch,2 batch)..).
+ * The result is a deterministic function of (comp, params): oracle/oracle.cpp restates
+ * the same schedule on the CPU.  Root-parallel sharding over GPUs gives each rank a
+ * disjoint id range (its own cache), then a MIN-reduction of (best_len, best_id). */
+typedef struct mig_rollout_params {
+    int64_t n_rollouts;
+    int32_t topk;       /* pool size per key, 1..32 (MctsParams.topk, mcts.hpp:15)          */
+    int32_t max_depth;  /* < 0: 2 * |fast_algo(comp)|, as mcts_solve (mcts.hpp:154-155)     */
+    uint64_t seed;      /* Philox key                                                       */
+    int64_t id_offset;  /* global id of rollout 0 (its Philox stream)                       */
+    int64_t batch;      /* rollouts per synchronous batch; <= 0: all in one batch           */
+    int32_t table_log2; /* key-cache capacity 2^table_log2; <= 0: automatic                 */
+} mig_rollout_params;
+
+typedef struct mig_rollout_result {
+    int32_t best_len;  /* steps of the shortest completed rollout; -1 if none completed     */
+    int32_t max_depth; /* the depth cap used                                               */
+    int64_t best_id;   /* its global id (ties: lowest id)                                  */
+    int64_t completed, capped, failed; /* failed: reached a key with an empty pool         */
+    int64_t steps;     /* rollout steps taken (all rollouts)                               */
+    int64_t keys;      /* distinct keys cached (= top-K pool builds)                       */
+    int32_t rounds;
+    int32_t path_len;
+    double device_ms;  /* product: device time of the rollout launches                    */
+} mig_rollout_result;
+
+/* lengths[n_rollouts] (optional): steps per rollout (capped: max_depth; empty pool: -1).
+ * best_path[cap] (optional): the best rollout's picks (pool indices). */
+int mig_rollouts(mig_ctx* ctx, const double* comp, int32_t n, const mig_rollout_params* params, int32_t* lengths,
+                 int64_t* best_path, int32_t cap, mig_rollout_result* out);
+
+/* Throughput-mode mcts_solve: answer = the shorter of fast_algo(comp) and the best
+ * root-parallel rollout (fast_ref wins ties, as mcts.hpp:245-251); max_depth = 2|fast_ref|. */
+int mig_mcts_solve_parallel(mig_ctx* ctx, const double* comp, int32_t n, const mig_rollout_params* params,
+                            mig_config* out, int32_t cap, int32_t* n_out, mig_rollout_result* result);
+
 /* ---- GA (ga.hpp) ---- */
 typedef struct mig_ga_params { /* GaParams, ga.hpp:24-36 */
     int32_t population;
@@ -246,6 +292,9 @@ typedef struct mig_stats {
     /* greedy-kernel phase split seen by CTA 0 (%globaltimer, product): scan+block argmax,
      * grid barrier, grid argmax+update, maybe_extend, extension enumeration+barrier     */
     double phase_ms[5];
+    int64_t rollout_steps;    /* throughput-mode rollout steps (mig_rollouts)            */
+    int64_t rollout_calls;
+    double rollout_ms;        /* device time of rollout launches (product)               */
 } mig_stats;
 int mig_ctx_stats(const mig_ctx* ctx, mig_stats* out);
 void mig_ctx_reset_stats(mig_ctx* ctx);

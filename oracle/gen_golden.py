@@ -153,6 +153,38 @@ def gen_partitions(ref):
     return out
 
 
+def gen_rollouts(ref):
+    """Throughput-mode root-parallel rollouts (mig_rollouts) on the reference's own primitives
+    (completion_type_key, detail::topk_candidates, rollout's util add) under the product's
+    documented schedule: Philox draws, lock-step rounds, lowest-index key claims."""
+    res = {}
+    ps = S.profiles()
+    tw, sv12 = S.random_workload(12, 7)
+    cases = [("slos_day", ps, S.fixture_services("slos_day", ps), dict(n_rollouts=64, seed=7)),
+             ("slos_night", ps, S.fixture_services("slos_night", ps), dict(n_rollouts=48, seed=3, topk=4)),
+             ("slos_day_capped", ps, S.fixture_services("slos_day", ps), dict(n_rollouts=40, seed=9, max_depth=12)),
+             ("rand12", tw, sv12, dict(n_rollouts=200, seed=12, topk=16)),
+             ("slos_24", ps, S.fixture_services("slos_24", ps), dict(n_rollouts=256, seed=11)),
+             ("slos_24_batched", ps, S.fixture_services("slos_24", ps), dict(n_rollouts=256, seed=11, batch=100,
+                                                                              id_offset=1000))]
+    p2, sv = S.gen(24, 6.35)
+    cases.append(("gen24_6.35", p2, sv, dict(n_rollouts=512, seed=5)))
+    for name, p, sv, kw in cases:
+        ctx = mp.make_plan_context(sv, p, mp.PartitionRuleSet.defaults(), backend=ref)
+        prm = mp.RolloutParams(**kw)
+        t = time.time()
+        r = mp.rollouts(mp.zero_completion(len(sv)), ctx, prm, lengths=True)
+        plan, r2 = mp.mcts_solve_parallel(mp.zero_completion(len(sv)), ctx, prm)
+        res[name] = {"store": store_name(p), "services": svc_json(sv), "params": kw, "best_len": r.best_len,
+                     "best_id": r.best_id, "max_depth": r.max_depth, "keys": r.keys, "steps": r.steps,
+                     "rounds": r.rounds, "completed": r.completed, "capped": r.capped, "failed": r.failed,
+                     "lengths": r.lengths, "path": S.plan_key([ctx.pool[i].config for i in r.path]),
+                     "solve_plan": S.plan_key(plan), "ref_wall_s": round(time.time() - t, 3)}
+        print(f"rollouts {name}: best {r.best_len} (id {r.best_id}), keys {r.keys}, solve {len(plan)} GPUs "
+              f"({time.time() - t:.1f}s)", flush=True)
+    return res
+
+
 def gen_greedy_big(ref):
     """gen(48, 7.0): ~6 minutes on one core; pins the n=48 plan bit-exactly."""
     p2, sv = S.gen(48, 7.0)
@@ -162,7 +194,7 @@ def gen_greedy_big(ref):
 
 
 SECTIONS = {"greedy": gen_greedy, "mcts": gen_mcts, "ga": gen_ga, "topk": gen_topk, "partitions": gen_partitions,
-            "greedy_big": gen_greedy_big}
+            "greedy_big": gen_greedy_big, "rollouts": gen_rollouts}
 
 
 def main(argv):

@@ -429,6 +429,154 @@ int mig_mcts_solve(mig_ctx* ctx, const double* comp, int32_t n, const mig_mcts_p
     return g != MIG_OK ? g : rc;
 }
 
+}  // extern "C"
+
+namespace {
+// Throughput-mode rollouts (include/migplan_b200.h, mig_rollouts) assembled from the
+// reference's own primitives: completion_type_key, detail::topk_candidates over ctx.pool,
+// is_satisfied and the util add of rollout (mcts.hpp:38-43,56-76,122-143).  Only the
+// schedule (lock-step rounds, lowest-index claims, Philox draws) is the product's.
+uint64_t philox64_ref(uint64_t seed, uint64_t stream, uint64_t step) {
+    uint32_t c[4] = {(uint32_t)step, (uint32_t)(step >> 32), (uint32_t)stream, (uint32_t)(stream >> 32)};
+    uint32_t k0 = (uint32_t)seed, k1 = (uint32_t)(seed >> 32);
+    for (int r = 0; r < 10; ++r) {
+        uint64_t a = (uint64_t)0xD2511F53u * c[0], b = (uint64_t)0xCD9E8D57u * c[2];
+        c[0] = (uint32_t)(b >> 32) ^ c[1] ^ k0;
+        c[1] = (uint32_t)b;
+        c[2] = (uint32_t)(a >> 32) ^ c[3] ^ k1;
+        c[3] = (uint32_t)a;
+        k0 += 0x9E3779B9u;
+        k1 += 0xBB67AE85u;
+    }
+    return ((uint64_t)c[1] << 32) | c[0];
+}
+struct RefPar {
+    int best_len = -1;
+    long long best_id = -1;
+    std::vector<int> path;
+    long long completed = 0, capped = 0, failed = 0, steps = 0, keys = 0;
+    int rounds = 0;
+};
+RefPar ref_par(const PlanContext& ctx, const CompletionRates& comp, long long R, int K, int depth, uint64_t seed,
+               long long id0, long long batch, int32_t* lengths) {
+    RefPar res;
+    RolloutCache cache;
+    if (batch <= 0 || batch > R) batch = R;
+    for (long long b0 = 0; b0 < R; b0 += batch) {
+        long long nb = std::min(batch, R - b0);
+        std::vector<CompletionRates> cur(nb, comp);
+        std::vector<std::vector<int>> picks(nb);
+        auto finish = [&](long long r) {
+            int L = (int)picks[r].size();
+            if (is_satisfied(cur[r])) {
+                res.completed++;
+                if (lengths) lengths[b0 + r] = L;
+                long long id = id0 + b0 + r;
+                if (res.best_len < 0 || L < res.best_len || (L == res.best_len && id < res.best_id))
+                    res.best_len = L, res.best_id = id, res.path = picks[r];
+                return true;
+            }
+            if (L >= depth) {
+                res.capped++;
+                if (lengths) lengths[b0 + r] = depth;
+                return true;
+            }
+            return false;
+        };
+        std::vector<long long> act;
+        for (long long r = 0; r < nb; ++r)
+            if (!finish(r)) act.push_back(r);
+        int rounds = 0;
+        while (!act.empty()) {
+            ++rounds;
+            for (long long r : act) {  // ascending: the lowest index claims a new key
+                std::string key = completion_type_key(cur[r]);
+                if (!cache.pools.count(key)) {
+                    ++cache.builds;
+                    cache.pools.emplace(key, detail::topk_candidates(ctx.pool, cur[r], K, nullptr));
+                }
+            }
+            std::vector<long long> next;
+            for (long long r : act) {
+                const std::vector<int>& pool = cache.pools.at(completion_type_key(cur[r]));
+                if (pool.empty()) {
+                    res.failed++;
+                    if (lengths) lengths[b0 + r] = -1;
+                    continue;
+                }
+                uint64_t x = philox64_ref(seed, (uint64_t)(id0 + b0 + r), (uint64_t)picks[r].size());
+                int idx = pool[(size_t)(((unsigned __int128)x * pool.size()) >> 64)];
+                for (const auto& [svc, u] : ctx.pool.items[idx].util) cur[r].values[svc] += u;
+                picks[r].push_back(idx);
+                res.steps++;
+                if (!finish(r)) next.push_back(r);
+            }
+            act = std::move(next);
+        }
+        res.rounds = std::max(res.rounds, rounds);
+    }
+    res.keys = cache.builds;
+    return res;
+}
+void ref_par_out(const RefPar& r, int depth, mig_rollout_result* o) {
+    if (!o) return;
+    std::memset(o, 0, sizeof *o);
+    o->best_len = r.best_len;
+    o->max_depth = depth;
+    o->best_id = r.best_id;
+    o->completed = r.completed;
+    o->capped = r.capped;
+    o->failed = r.failed;
+    o->steps = r.steps;
+    o->keys = r.keys;
+    o->rounds = r.rounds;
+    o->path_len = (int32_t)r.path.size();
+}
+}  // namespace
+
+extern "C" {
+
+int mig_rollouts(mig_ctx* ctx, const double* comp, int32_t n, const mig_rollout_params* p, int32_t* lengths,
+                 int64_t* best_path, int32_t cap, mig_rollout_result* out) {
+    return guarded([&] {
+        if (!p) throw std::invalid_argument("null rollout params");
+        if (p->topk < 1 || p->topk > 32) throw std::invalid_argument("rollouts: topk must be in [1, 32]");
+        CompletionRates c = comp_of(comp, n, ctx);
+        int depth = p->max_depth < 0 ? 2 * (int)fast_algo(c, ctx->plan).size() : p->max_depth;
+        RefPar r = ref_par(ctx->plan, c, p->n_rollouts, p->topk, depth, p->seed, p->id_offset, p->batch, lengths);
+        if (best_path) {
+            if ((int)r.path.size() > cap) throw std::invalid_argument("output capacity too small");
+            for (size_t i = 0; i < r.path.size(); ++i) best_path[i] = r.path[i];
+        }
+        ref_par_out(r, depth, out);
+    });
+}
+
+int mig_mcts_solve_parallel(mig_ctx* ctx, const double* comp, int32_t n, const mig_rollout_params* p,
+                            mig_config* out, int32_t cap, int32_t* n_out, mig_rollout_result* res) {
+    int rc = MIG_OK;
+    int g = guarded([&] {
+        if (!p) throw std::invalid_argument("null rollout params");
+        CompletionRates c = comp_of(comp, n, ctx);
+        if (is_satisfied(c)) {
+            ref_par_out(RefPar{}, 0, res);
+            rc = emit_plan({}, ctx->services, out, cap, n_out);
+            return;
+        }
+        std::vector<GpuConfig> fast = fast_algo(c, ctx->plan);
+        int depth = 2 * (int)fast.size();
+        RefPar r = ref_par(ctx->plan, c, p->n_rollouts, p->topk, depth, p->seed, p->id_offset, p->batch, nullptr);
+        ref_par_out(r, depth, res);
+        std::vector<GpuConfig> ans = fast;
+        if (r.best_len >= 0 && (size_t)r.best_len < ans.size()) {
+            ans.clear();
+            for (int i : r.path) ans.push_back(ctx->plan.pool.items[i].config);
+        }
+        rc = emit_plan(ans, ctx->services, out, cap, n_out);
+    });
+    return g != MIG_OK ? g : rc;
+}
+
 void mig_ga_params_defaults(mig_ga_params* out) {
     GaParams g;
     std::memset(out, 0, sizeof *out);

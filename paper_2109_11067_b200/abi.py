@@ -71,7 +71,19 @@ class StatsC(C.Structure):
                 ("greedy_calls", C.c_int64), ("topk_calls", C.c_int64), ("greedy_steps", C.c_int64),
                 ("ext_events", C.c_int64), ("ext_rows", C.c_int64), ("kernel_launches", C.c_int64),
                 ("h2d_bytes", C.c_int64), ("d2h_bytes", C.c_int64), ("greedy_ms", C.c_double),
-                ("topk_ms", C.c_double), ("phase_ms", C.c_double * 5)]
+                ("topk_ms", C.c_double), ("phase_ms", C.c_double * 5), ("rollout_steps", C.c_int64),
+                ("rollout_calls", C.c_int64), ("rollout_ms", C.c_double)]
+
+
+class RolloutParamsC(C.Structure):
+    _fields_ = [("n_rollouts", C.c_int64), ("topk", C.c_int32), ("max_depth", C.c_int32), ("seed", C.c_uint64),
+                ("id_offset", C.c_int64), ("batch", C.c_int64), ("table_log2", C.c_int32)]
+
+
+class RolloutResultC(C.Structure):
+    _fields_ = [("best_len", C.c_int32), ("max_depth", C.c_int32), ("best_id", C.c_int64),
+                ("completed", C.c_int64), ("capped", C.c_int64), ("failed", C.c_int64), ("steps", C.c_int64),
+                ("keys", C.c_int64), ("rounds", C.c_int32), ("path_len", C.c_int32), ("device_ms", C.c_double)]
 
 
 GREEDY_TRACE = C.CFUNCTYPE(None, C.c_void_p, C.c_int32, C.POINTER(CandidateC), C.c_double,
@@ -117,6 +129,10 @@ SIGNATURES = {
     "mig_rollout": (_I, [_P, _DP, C.c_int32, C.POINTER(MctsParamsC), _P, _P, C.c_int32, _I64P, C.c_int32, _I32P]),
     "mig_mcts_solve": (_I, [_P, _DP, C.c_int32, C.POINTER(MctsParamsC), C.c_uint64, C.POINTER(ConfigC),
                             C.c_int32, _I32P, MCTS_TRACE, _P]),
+    "mig_rollouts": (_I, [_P, _DP, C.c_int32, C.POINTER(RolloutParamsC), _I32P, _I64P, C.c_int32,
+                          C.POINTER(RolloutResultC)]),
+    "mig_mcts_solve_parallel": (_I, [_P, _DP, C.c_int32, C.POINTER(RolloutParamsC), C.POINTER(ConfigC), C.c_int32,
+                                     _I32P, C.POINTER(RolloutResultC)]),
     "mig_ga_params_defaults": (None, [C.POINTER(GaParamsC)]),
     "mig_completion_of": (_I, [_P, C.POINTER(ConfigC), C.c_int32, _DP]),
     "mig_mutate": (_I, [_P, C.POINTER(ConfigC), C.c_int32, C.POINTER(GaParamsC), _P, C.POINTER(ConfigC)]),

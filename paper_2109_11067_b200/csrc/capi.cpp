@@ -402,6 +402,85 @@ void mig_ga_params_defaults(mig_ga_params* out) {
     out->slow = mig_mcts_params{g.slow.budget_iters, g.slow.topk, g.slow.pick_services, g.slow.ucb_c};
 }
 
+}  // extern "C"
+
+namespace {
+// mig_rollouts body: resolves max_depth < 0 through the device greedy (mcts.hpp:152-155).
+RolloutResult run_rollouts(mig_ctx* ctx, const std::vector<double>& c, const mig_rollout_params* p, int32_t* lengths,
+                           int* depth_used, int* fast_len) {
+    if (!p) throw ArgumentError("null rollout params");
+    int depth = p->max_depth;
+    *fast_len = -1;
+    if (depth < 0) {
+        std::vector<Config> ref = fast_plan(*ctx->e, c);
+        *fast_len = static_cast<int>(ref.size());
+        depth = 2 * *fast_len;
+    }
+    *depth_used = depth;
+    RolloutResult r = ctx->e->rollouts(c, p->n_rollouts, p->topk, depth, p->seed, p->id_offset, p->batch,
+                                       p->table_log2, lengths);
+    // every pool build is one top-K over the whole base pool (mcts.hpp:129-133)
+    ctx->e->stats.topk_calls += r.keys;
+    ctx->e->stats.topk_rows += r.keys * ctx->e->pool_size();
+    return r;
+}
+void result_of(const RolloutResult& r, int depth, mig_rollout_result* out) {
+    if (!out) return;
+    out->best_len = r.best_len;
+    out->max_depth = depth;
+    out->best_id = r.best_id;
+    out->completed = r.completed;
+    out->capped = r.capped;
+    out->failed = r.failed;
+    out->steps = r.steps;
+    out->keys = r.keys;
+    out->rounds = r.rounds;
+    out->path_len = static_cast<int32_t>(r.path.size());
+    out->device_ms = r.ms;
+}
+}  // namespace
+
+extern "C" {
+
+int mig_rollouts(mig_ctx* ctx, const double* comp, int32_t n, const mig_rollout_params* params, int32_t* lengths,
+                 int64_t* best_path, int32_t cap, mig_rollout_result* out) {
+    return guarded([&] {
+        int depth = 0, fl = 0;
+        RolloutResult r = run_rollouts(ctx, comp_of(ctx, comp, n), params, lengths, &depth, &fl);
+        if (best_path) {
+            if (static_cast<int32_t>(r.path.size()) > cap) throw ArgumentError("output capacity too small");
+            for (size_t i = 0; i < r.path.size(); ++i) best_path[i] = r.path[i];
+        }
+        result_of(r, depth, out);
+    });
+}
+
+int mig_mcts_solve_parallel(mig_ctx* ctx, const double* comp, int32_t n, const mig_rollout_params* params,
+                            mig_config* out, int32_t cap, int32_t* n_out, mig_rollout_result* result) {
+    int rc = MIG_OK;
+    int g = guarded([&] {
+        auto c = comp_of(ctx, comp, n);
+        if (satisfied(c)) {  // mcts.hpp:151
+            result_of(RolloutResult{}, 0, result);
+            rc = emit({}, out, cap, n_out);
+            return;
+        }
+        std::vector<Config> fast_ref = fast_plan(*ctx->e, c);
+        mig_rollout_params p = *params;
+        p.max_depth = 2 * static_cast<int32_t>(fast_ref.size());
+        int depth = 0, fl = 0;
+        RolloutResult r = run_rollouts(ctx, c, &p, nullptr, &depth, &fl);
+        result_of(r, depth, result);
+        std::vector<Config> answer = std::move(fast_ref);
+        if (r.best_len >= 0 && static_cast<size_t>(r.best_len) < answer.size()) {
+            answer.clear();
+            for (long long idx : r.path) answer.push_back(ctx->e->config_of(ctx->e->base_rows()[idx]));
+        }
+        rc = emit(answer, out, cap, n_out);
+    });
+    return g != MIG_OK ? g : rc;
+}
+
 int mig_completion_of(const mig_ctx* ctx, const mig_config* configs, int32_t n_configs, double* comp_out) {
     return guarded([&] {
         std::vector<Config> cfgs;
@@ -494,6 +573,9 @@ int mig_ctx_stats(const mig_ctx* ctx, mig_stats* out) {
     out->greedy_ms = s.greedy_ns.load() / 1e6;
     out->topk_ms = s.topk_ns.load() / 1e6;
     for (int k = 0; k < 5; ++k) out->phase_ms[k] = s.phase_ns[k].load() / 1e6;
+    out->rollout_steps = s.rollout_steps.load();
+    out->rollout_calls = s.rollout_calls.load();
+    out->rollout_ms = s.rollout_ns.load() / 1e6;
     return MIG_OK;
 }
 

@@ -133,5 +133,49 @@ __device__ __forceinline__ void grid_barrier(unsigned* count, unsigned* gen, uns
     __syncthreads();
 }
 
+// ---- exact top-K by parallel ranking (topk.cu, rollout.cu)
+
+struct Cand {
+    double s, u;
+    uint64_t row;
+    long long pos;  // position in the candidate set: orders duplicate rows of an explicit list
+};
+
+// candidate i is preceded by j: preferred (greedy.hpp:63-67), or the same row earlier in
+// the candidate list (duplicates of an explicit `from` list are both kept, mcts.hpp:59-67).
+__device__ __forceinline__ bool precedes(const DevModel& M, const Cand& j, const Cand& i) {
+    if (j.s != i.s) return j.s > i.s;
+    if (j.row == i.row) return j.pos < i.pos;
+    if (j.u != i.u) return j.u > i.u;
+    return row_key_less(M, j.row, i.row);
+}
+
+// Rank the first `nc` entries of `cand` (all threads) and write the K best, in order, to
+// out[0..min(K, nc)).  Ranks are distinct because `precedes` is a strict total order.
+__device__ __forceinline__ void rank_select(const DevModel& M, const Cand* cand, int nc, int k, Cand* out) {
+    for (int i = threadIdx.x; i < nc; i += blockDim.x) {
+        const Cand ci = cand[i];
+        int r = 0;
+        for (int j = 0; j < nc && r < k; ++j) r += precedes(M, cand[j], ci) ? 1 : 0;
+        if (r < k) out[r] = ci;
+    }
+}
+
+// K-th largest (k <= 32) of the warp's lane values: bitonic sort descending over shuffles.
+__device__ __forceinline__ double warp_kth(double v, int k) {
+    const int lane = static_cast<int>(threadIdx.x & 31u);
+#pragma unroll
+    for (int size = 2; size <= 32; size <<= 1) {
+#pragma unroll
+        for (int j = size >> 1; j > 0; j >>= 1) {
+            const double o = __shfl_xor_sync(0xffffffffu, v, j);
+            const bool desc = (lane & size) == 0 || size == 32;
+            const bool low = (lane & j) == 0;
+            v = (low == desc) ? fmax(v, o) : fmin(v, o);
+        }
+    }
+    return __shfl_sync(0xffffffffu, v, k - 1);
+}
+
 }  // namespace dev
 }  // namespace mgb

@@ -102,4 +102,46 @@ struct Topk1Args {
     int* n_out;         // host-mapped
 };
 
+// Throughput-mode root-parallel rollouts (rollout.cu).
+struct RolloutCounters {
+    unsigned long long n_act[2];  // active-list lengths (ping-pong by round parity)
+    unsigned long long n_pend[2]; // key-cache slots created per round (ping-pong)
+    unsigned int bar_count, bar_gen;
+    int status;                   // 0 ok, 1 key cache full
+    int rounds;
+    unsigned long long best;      // min over completed rollouts of (steps << 32 | batch index)
+    unsigned long long steps, completed, capped, failed, keys;
+};
+
+struct RolloutArgs {
+    DevModel M;
+    const uint64_t* base;   // base pool rows (the rollout pool, mcts.hpp:129-133)
+    long long n_base;
+    const double* comp0;    // start completion (host-mapped)
+    long long n_roll;       // rollouts in this batch
+    long long id0;          // global id of the batch's rollout 0 (Philox stream id)
+    uint64_t seed;          // Philox key
+    int k;                  // pool size per key (MctsParams.topk), <= 32
+    int max_depth;
+    double* comp;           // n_roll * n: per-rollout completion vectors
+    int* len;               // n_roll: steps taken
+    uint8_t* status;        // n_roll: 0 active, 1 satisfied, 2 depth cap, 3 empty pool
+    unsigned* rslot;        // n_roll: key-cache slot of the current key
+    long long* act0;        // active lists (ping-pong)
+    long long* act1;
+    // key cache (RolloutCache, mcts.hpp:47-50): open addressing over the unsat bitmap
+    unsigned tab_mask;      // capacity - 1 (power of two)
+    unsigned* tag;          // 0 empty, 1 key being written, 2 key ready
+    uint64_t* key;          // capacity * 4
+    unsigned long long* claimer;  // lowest batch index that probed the slot in its first round
+    int* pool_n;            // -1 until the pool is built
+    unsigned* pool;         // capacity * k base-pool indices, preferred first
+    unsigned* pend0;        // slots created in the round (ping-pong)
+    unsigned* pend1;
+    RolloutCounters* cnt;
+    long long* path;        // host-mapped: winner replay (base-pool indices), max_depth
+    int* path_len;          // host-mapped
+    int* lengths;           // optional, n_roll: steps (capped: max_depth, empty pool: -1)
+};
+
 }  // namespace mgb

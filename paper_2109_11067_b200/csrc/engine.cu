@@ -22,8 +22,12 @@ int kernel_threads();
 size_t topk1_smem_bytes(int n, int PP, int km);
 int topk1_threads();
 int topk1_rows_per_cta();
-constexpr int kTopkMaxCtas = 4096;  // 8M candidate rows per top-K call
+int topk1_max_ctas();
+constexpr int kTopkMaxCtas = 4096;  // partial-list capacity (Best x 32 per CTA)
 const void* topk1_kernel_ptr(int km);
+size_t rollout_smem_bytes(int n, int PP);
+const void* rollout_kernel_ptr();
+int rollout_threads();
 
 namespace {
 
@@ -170,6 +174,13 @@ Engine::Engine(const Rules& rules, std::map<std::string, ModelProfile> profiles,
                                 static_cast<int>(topk1_smem_bytes(m_.n, m_.PP, km))));
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&greedy_blocks_per_sm_, greedy_kernel_ptr(), T, gsm));
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&topk_blocks_per_sm_, topk_kernel_ptr(), T, tsm));
+    {
+        const size_t rsm = rollout_smem_bytes(m_.n, m_.PP);
+        CK(cudaFuncSetAttribute(rollout_kernel_ptr(), cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(rsm)));
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&rollout_blocks_per_sm_, rollout_kernel_ptr(), rollout_threads(),
+                                                         rsm));
+        if (rollout_blocks_per_sm_ < 1) throw DeviceError("rollout kernel does not fit on an SM");
+    }
     if (greedy_blocks_per_sm_ < 1 || topk_blocks_per_sm_ < 1) throw DeviceError("kernel does not fit on an SM");
 
     // ---- device model tables
@@ -481,7 +492,10 @@ std::vector<long long> Engine::topk(const std::vector<double>& comp, int k, cons
         CK(cudaMemcpyAsync(s->index, index->data(), sizeof(long long) * total, cudaMemcpyHostToDevice, s->stream));
     }
     CK(cudaEventRecord(s->e0, s->stream));
-    if (k <= 32) {  // single pass, last-CTA merge (topk.cu)
+    const long long per = topk1_rows_per_cta();
+    const long long g1 = (total + per - 1) / per;
+    bool single = k <= 32 && g1 <= topk1_max_ctas();
+    if (single) {  // one launch: per-CTA threshold + parallel rank, last-CTA merge (topk.cu)
         Topk1Args a{};
         a.M = dm_;
         a.rows = d_base_;
@@ -495,14 +509,18 @@ std::vector<long long> Engine::topk(const std::vector<double>& comp, int k, cons
         a.ticket = s->ticket;
         a.out_row = s->io->top_rows;
         a.n_out = &s->io->top_n;
-        const int T = topk1_threads(), km = 32;
-        const long long per = topk1_rows_per_cta();
-        if ((total + per - 1) / per > kTopkMaxCtas) throw ArgumentError("top-K candidate set too large");
-        int G = static_cast<int>((total + per - 1) / per);
-        G = std::max(G, 1);
+        const int G = static_cast<int>(std::max<long long>(g1, 1));
         void* args[] = {&a};
-        CK(cudaLaunchKernel(topk1_kernel_ptr(km), G, T, args, topk1_smem_bytes(m_.n, m_.PP, km), s->stream));
-    } else {  // k rounds with grid barriers (k > 16: API-only)
+        CK(cudaLaunchKernel(topk1_kernel_ptr(32), G, topk1_threads(), args, topk1_smem_bytes(m_.n, m_.PP, 32),
+                            s->stream));
+        stats.launches++;
+        CK(cudaStreamSynchronize(s->stream));
+        // *n_out == -1: a CTA's rows tied at its threshold beyond the candidate capacity;
+        // the exact k-round kernel below answers instead.
+        single = s->io->top_n >= 0;
+        if (!single) CK(cudaMemsetAsync(s->ticket, 0, sizeof(unsigned), s->stream));
+    }
+    if (!single) {  // k rounds with grid barriers (k > 32, huge lists, or tie overflow)
         TopkArgs a{};
         a.M = dm_;
         a.rows = d_base_;
@@ -521,8 +539,8 @@ std::vector<long long> Engine::topk(const std::vector<double>& comp, int k, cons
         G = std::max(G, 1);
         void* args[] = {&a};
         CK(cudaLaunchCooperativeKernel(topk_kernel_ptr(), G, T, args, topk_smem_bytes(m_.n, m_.PP), s->stream));
+        stats.launches++;
     }
-    stats.launches++;
     CK(cudaEventRecord(s->e1, s->stream));
     CK(cudaStreamSynchronize(s->stream));
     const int got = s->io->top_n;
@@ -538,6 +556,177 @@ std::vector<long long> Engine::topk(const std::vector<double>& comp, int k, cons
     return out;
 }
 
+// Root-parallel rollouts (rollout.cu).  Device buffers live for the call; the key cache
+// persists across the call's batches (the reference's RolloutCache lives for one
+// mcts_solve call, mcts.hpp:158).  A full key cache restarts the call with 4x capacity.
+RolloutResult Engine::rollouts(const std::vector<double>& comp, long long n_roll, int k, int max_depth, uint64_t seed,
+                               long long id_offset, long long batch, int table_log2, int* lengths) {
+    if (static_cast<int>(comp.size()) != m_.n) throw PlanningError("completion vector length mismatch");
+    if (k < 1 || k > 32) throw ArgumentError("rollouts: topk must be in [1, 32]");
+    if (n_roll < 0 || max_depth < 0) throw ArgumentError("rollouts: negative count or depth");
+    if (batch <= 0 || batch > n_roll) batch = n_roll;
+    batch = std::min<long long>(batch, 1ll << 31);
+    RolloutResult res;
+    if (n_roll == 0) return res;
+    CK(cudaSetDevice(device_));
+    int L2 = table_log2;
+    if (L2 <= 0) {
+        long long want = std::max<long long>(1 << 16, std::min<long long>(1ll << 24, 4 * n_roll));
+        L2 = 0;
+        while ((1ll << L2) < want) ++L2;
+    }
+    L2 = std::min(std::max(L2, 4), 30);
+    const int n = m_.n;
+    std::vector<void*> owned;
+    struct Free {
+        std::vector<void*>& v;
+        ~Free() {
+            for (void* p : v) cudaFree(p);
+        }
+    } fr{owned};
+    auto alloc = [&](size_t bytes) {
+        void* p = nullptr;
+        CK(cudaMalloc(&p, std::max<size_t>(bytes, 16)));
+        owned.push_back(p);
+        return p;
+    };
+    struct HostOut {
+        int path_len;
+        int pad;
+        double comp[256];
+    };
+    HostOut* ho = nullptr;
+    long long* hpath = nullptr;
+    CK(cudaHostAlloc(&ho, sizeof(HostOut), cudaHostAllocMapped));
+    CK(cudaHostAlloc(&hpath, sizeof(long long) * (max_depth + 1), cudaHostAllocMapped));
+    struct FreeHost {
+        void* a;
+        void* b;
+        ~FreeHost() {
+            cudaFreeHost(a);
+            cudaFreeHost(b);
+        }
+    } fh{ho, hpath};
+    std::memcpy(ho->comp, comp.data(), sizeof(double) * n);
+
+    RolloutArgs a{};
+    a.M = dm_;
+    a.base = d_base_;
+    a.n_base = pool_size();
+    a.comp0 = ho->comp;
+    a.seed = seed;
+    a.k = k;
+    a.max_depth = max_depth;
+    a.comp = static_cast<double*>(alloc(sizeof(double) * n * batch));
+    a.len = static_cast<int*>(alloc(sizeof(int) * batch));
+    a.status = static_cast<uint8_t*>(alloc(batch));
+    a.rslot = static_cast<unsigned*>(alloc(sizeof(unsigned) * batch));
+    a.act0 = static_cast<long long*>(alloc(sizeof(long long) * batch));
+    a.act1 = static_cast<long long*>(alloc(sizeof(long long) * batch));
+    a.cnt = static_cast<RolloutCounters*>(alloc(sizeof(RolloutCounters)));
+    a.path = hpath;
+    a.path_len = &ho->path_len;
+    int* d_len = lengths ? static_cast<int*>(alloc(sizeof(int) * batch)) : nullptr;
+    a.lengths = d_len;
+    cudaStream_t st = nullptr;
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    CK(cudaEventCreate(&e0));
+    CK(cudaEventCreate(&e1));
+    struct FreeStream {
+        cudaStream_t s;
+        cudaEvent_t a, b;
+        ~FreeStream() {
+            cudaEventDestroy(a);
+            cudaEventDestroy(b);
+            cudaStreamDestroy(s);
+        }
+    } fs{st, e0, e1};
+    const int G = num_sms_ * rollout_blocks_per_sm_;
+    const size_t smem = rollout_smem_bytes(n, m_.PP);
+
+    for (int attempt = 0;; ++attempt) {
+        const size_t cap = size_t{1} << L2;
+        std::vector<void*> table;
+        auto talloc = [&](size_t bytes) {
+            void* p = alloc(bytes);
+            table.push_back(p);
+            return p;
+        };
+        a.tab_mask = static_cast<unsigned>(cap - 1);
+        a.tag = static_cast<unsigned*>(talloc(sizeof(unsigned) * cap));
+        a.key = static_cast<uint64_t*>(talloc(sizeof(uint64_t) * 4 * cap));
+        a.claimer = static_cast<unsigned long long*>(talloc(sizeof(unsigned long long) * cap));
+        a.pool_n = static_cast<int*>(talloc(sizeof(int) * cap));
+        a.pool = static_cast<unsigned*>(talloc(sizeof(unsigned) * k * cap));
+        a.pend0 = static_cast<unsigned*>(talloc(sizeof(unsigned) * cap));
+        a.pend1 = static_cast<unsigned*>(talloc(sizeof(unsigned) * cap));
+        CK(cudaMemsetAsync(a.tag, 0, sizeof(unsigned) * cap, st));
+        CK(cudaMemsetAsync(a.claimer, 0xFF, sizeof(unsigned long long) * cap, st));
+        CK(cudaMemsetAsync(a.pool_n, 0xFF, sizeof(int) * cap, st));
+        RolloutResult r;
+        bool full = false;
+        unsigned long long best_key = ~0ull;
+        for (long long done = 0; done < n_roll; done += batch) {
+            a.n_roll = std::min(batch, n_roll - done);
+            a.id0 = id_offset + done;
+            CK(cudaMemsetAsync(a.cnt, 0, sizeof(RolloutCounters), st));
+            CK(cudaMemsetAsync(&a.cnt->best, 0xFF, sizeof(unsigned long long), st));
+            void* args[] = {&a};
+            CK(cudaEventRecord(e0, st));
+            CK(cudaLaunchCooperativeKernel(rollout_kernel_ptr(), G, rollout_threads(), args, smem, st));
+            CK(cudaEventRecord(e1, st));
+            stats.launches++;
+            r.launches++;
+            RolloutCounters c{};
+            CK(cudaMemcpyAsync(&c, a.cnt, sizeof c, cudaMemcpyDeviceToHost, st));
+            if (lengths)
+                CK(cudaMemcpyAsync(lengths + done, d_len, sizeof(int) * a.n_roll, cudaMemcpyDeviceToHost, st));
+            CK(cudaStreamSynchronize(st));
+            float ms = 0.f;
+            CK(cudaEventElapsedTime(&ms, e0, e1));
+            r.ms += ms;
+            if (c.status != 0) {
+                full = true;
+                break;
+            }
+            r.completed += static_cast<long long>(c.completed);
+            r.capped += static_cast<long long>(c.capped);
+            r.failed += static_cast<long long>(c.failed);
+            r.steps += static_cast<long long>(c.steps);
+            r.keys += static_cast<long long>(c.keys);
+            r.rounds = std::max(r.rounds, c.rounds);
+            if (c.best != ~0ull) {  // (steps, global id): batches are in id order
+                const unsigned long long len = c.best >> 32;
+                const unsigned long long key = (len << 40) | static_cast<unsigned long long>(done + (c.best & 0xFFFFFFFFull));
+                if (key < best_key) {
+                    best_key = key;
+                    r.best_len = static_cast<int>(len);
+                    r.best_id = id_offset + done + static_cast<long long>(c.best & 0xFFFFFFFFull);
+                    r.path.assign(hpath, hpath + ho->path_len);
+                }
+            }
+        }
+        if (full && attempt < 3 && L2 < 30) {
+            for (void* p : table) {
+                cudaFree(p);
+                owned.erase(std::find(owned.begin(), owned.end(), p));
+            }
+            L2 = std::min(L2 + 2, 30);
+            continue;
+        }
+        if (full) throw DeviceError("rollouts: key cache full");
+        res = std::move(r);
+        break;
+    }
+    stats.rollout_ns += static_cast<long long>(res.ms * 1e6);
+    stats.rollout_steps += res.steps;
+    stats.rollout_calls++;
+    stats.h2d += static_cast<long long>(sizeof(double) * n);
+    stats.d2h += static_cast<long long>(sizeof(RolloutCounters) + sizeof(long long) * res.path.size() +
+                                        (lengths ? sizeof(int) * n_roll : 0));
+    return res;
+}
 
 // completion_of / detail::sum_rates (core.hpp:245-269): counts keyed by (svc, size, batch)
 // in key order, total += count * thr, one division per service.

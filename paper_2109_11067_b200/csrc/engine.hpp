@@ -33,14 +33,24 @@ struct Slot;
 struct Stats {
     std::atomic<long long> greedy_rows{0}, topk_rows{0}, greedy_calls{0}, topk_calls{0}, greedy_steps{0};
     std::atomic<long long> ext_events{0}, ext_rows{0}, launches{0}, h2d{0}, d2h{0};
-    std::atomic<long long> greedy_ns{0}, topk_ns{0};
+    std::atomic<long long> greedy_ns{0}, topk_ns{0}, rollout_ns{0}, rollout_steps{0}, rollout_calls{0};
     std::atomic<long long> phase_ns[5] = {0, 0, 0, 0, 0};
     void reset() {
         for (auto* a : {&greedy_rows, &topk_rows, &greedy_calls, &topk_calls, &greedy_steps, &ext_events, &ext_rows,
-                        &launches, &h2d, &d2h, &greedy_ns, &topk_ns})
+                        &launches, &h2d, &d2h, &greedy_ns, &topk_ns, &rollout_ns, &rollout_steps, &rollout_calls})
             a->store(0);
         for (auto& p : phase_ns) p.store(0);
     }
+};
+
+// Throughput-mode root-parallel rollouts (rollout.cu): the result of one mig_rollouts call.
+struct RolloutResult {
+    int best_len = -1;        // shortest completed rollout (steps); -1: none completed
+    long long best_id = -1;   // its global id (ties: lowest id)
+    std::vector<long long> path;  // its picks (base-pool indices)
+    long long completed = 0, capped = 0, failed = 0, steps = 0, keys = 0;
+    int rounds = 0, launches = 0;
+    double ms = 0.0;          // device time (CUDA events)
 };
 
 class Engine {
@@ -63,6 +73,11 @@ class Engine {
     std::vector<long long> topk(const std::vector<double>& comp, int k, const std::vector<long long>* index,
                                 const std::vector<uint64_t>* svc_mask);
 
+    // n_roll root-parallel rollouts from comp (rollout.cu), processed in synchronous batches
+    // of `batch` rollouts sharing one key cache; rollout r has global id id_offset + r.
+    RolloutResult rollouts(const std::vector<double>& comp, long long n_roll, int k, int max_depth, uint64_t seed,
+                           long long id_offset, long long batch, int table_log2, int* lengths);
+
     // completion_of (core.hpp:291-302), count-based, on the host (control logic, not hot).
     std::vector<double> completion_of(const std::vector<Config>& cfgs) const;
     const std::map<std::string, ModelProfile>& profiles() const { return profiles_; }
@@ -82,6 +97,7 @@ class Engine {
     int num_sms_ = 0;
     int greedy_blocks_per_sm_ = 0;
     int topk_blocks_per_sm_ = 0;
+    int rollout_blocks_per_sm_ = 0;
     DevModel dm_{};
     std::vector<void*> dev_allocs_;
     uint64_t* d_base_ = nullptr;

@@ -1,0 +1,386 @@
+// rollout.cu — K5: throughput-mode root-parallel MCTS rollouts, one rollout per warp.
+//
+// The reference's rollout (mcts.hpp:122-143) completes a partial deployment by repeatedly
+// picking a uniformly random candidate among the top-K of the BASE pool under the current
+// completion vector, memoized by the unsatisfied-service bitmap (completion_type_key,
+// mcts.hpp:38-43; RolloutCache mcts.hpp:47-50).  Here N rollouts from one root run
+// concurrently in one persistent cooperative kernel:
+//   - one warp owns one rollout at a time; lane l keeps comp[l + 32 j] in registers, the
+//     type key is a handful of ballots, a pick adds <= 4 utilities in the owning lanes;
+//   - draws are Philox4x32-10 (philox.cuh): draw t of rollout r is philox(seed, (t, id0+r)),
+//     so the result does not depend on which warp runs which rollout, or when;
+//   - the key cache is a device-wide open-addressing table shared by all rollouts;
+//   - rollouts advance in LOCK-STEP ROUNDS so the memoized pools are deterministic: the pool
+//     of a key first seen in round d is the top-K under the completion vector of the
+//     LOWEST-indexed rollout that reached the key in round d (atomicMin claim), built by one
+//     CTA after a grid barrier (the same threshold + parallel-rank top-K as topk.cu);
+//   - the shortest completed rollout (ties: lowest index) is replayed at the end from the
+//     (immutable) cache to emit its path.
+// Per round: [pick + add + satisfied check + key probe, warp per rollout] -> grid barrier ->
+// [build the round's new pools, CTA per key] -> grid barrier.
+// oracle/oracle.cpp (`rollouts_restated`) restates exactly this schedule on the CPU.
+#include <cuda/atomic>
+
+#include "common.cuh"
+#include "philox.cuh"
+
+namespace mgb {
+
+using namespace dev;
+
+namespace {
+
+constexpr int kRThreads = 512;
+constexpr int kRWarps = kRThreads / 32;
+constexpr int kRCandCap = 2048;
+constexpr int kRMaxK = 32;
+constexpr int kMaxJ = 8;  // comp registers per lane: n <= 256
+
+__device__ __forceinline__ uint64_t mix64(uint64_t z) {
+    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+    z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+    return z ^ (z >> 31);
+}
+
+// Find (or, with `insert`, create) the slot of key kw[0..nk).  Lane-0 code.
+// Returns the slot, -1 (absent, !insert) or -2 (table full).
+__device__ long long probe(const RolloutArgs& a, const uint64_t* kw, int nk, bool insert, bool& created) {
+    uint64_t h = 0x9e3779b97f4a7c15ull;
+    for (int w = 0; w < nk; ++w) h = mix64(h ^ kw[w]);
+    unsigned s = static_cast<unsigned>(h) & a.tab_mask;
+    created = false;
+    for (unsigned t = 0; t <= a.tab_mask; ++t, s = (s + 1) & a.tab_mask) {
+        cuda::atomic_ref<unsigned, cuda::thread_scope_device> tag(a.tag[s]);
+        unsigned tg = tag.load(cuda::memory_order_acquire);
+        if (tg == 0) {
+            if (!insert) return -1;
+            unsigned expect = 0;
+            if (tag.compare_exchange_strong(expect, 1u, cuda::memory_order_acq_rel)) {
+                for (int w = 0; w < 4; ++w) __stcg(&a.key[4ull * s + w], w < nk ? kw[w] : 0ull);
+                tag.store(2u, cuda::memory_order_release);
+                created = true;
+                return s;
+            }
+            tg = expect;
+        }
+        while (tg == 1) {
+            __nanosleep(20);
+            tg = tag.load(cuda::memory_order_acquire);
+        }
+        bool eq = true;
+        for (int w = 0; w < nk; ++w) eq &= __ldcg(&a.key[4ull * s + w]) == kw[w];
+        if (eq) return s;
+    }
+    return -2;
+}
+
+// Unsatisfied-service bitmap (completion_type_key, mcts.hpp:38-43): bit i set when
+// comp[i] < 1 - 1e-9 (core.hpp:18,217-221).  Warp-uniform result.
+__device__ __forceinline__ bool type_key(const double (&c)[kMaxJ], int n, uint64_t (&kw)[4]) {
+    const int lane = static_cast<int>(threadIdx.x & 31u);
+    bool any = false;
+    for (int w = 0; w < 4; ++w) kw[w] = 0;
+#pragma unroll
+    for (int j = 0; j < kMaxJ; ++j) {
+        if (32 * j >= n) break;
+        const bool un = lane + 32 * j < n && c[j] < 1.0 - 1e-9;
+        const unsigned b = __ballot_sync(0xffffffffu, un);
+        kw[j >> 1] |= static_cast<uint64_t>(b) << (32 * (j & 1));
+        any |= b != 0;
+    }
+    return any;
+}
+
+// Add the chosen candidate's utilities (add_util; mcts.hpp:139) in the owning lanes.
+__device__ __forceinline__ void add_row(const DevModel& M, uint64_t row, double (&c)[kMaxJ]) {
+    const int lane = static_cast<int>(threadIdx.x & 31u);
+#pragma unroll
+    for (int m = 0; m < 4; ++m) {
+        const int code = static_cast<int>((row >> (16 * m)) & 0xFFFFull);
+        const int svc = code / M.PP;
+        if (svc < M.n && (svc & 31) == lane) {
+            const double u = __ldg(&M.U[code]);
+#pragma unroll
+            for (int j = 0; j < kMaxJ; ++j)
+                if ((svc >> 5) == j) c[j] = __dadd_rn(c[j], u);
+        }
+    }
+}
+
+// Top-K of the base pool under `comp` (smem) by one CTA: W = need*U, threshold from the
+// per-warp K-th lane maxima, parallel rank of the rows >= T (topk.cu), exact k-round
+// fallback when ties at T overflow the candidate buffer.  Writes pool[0..got), returns got.
+__device__ int block_topk(const RolloutArgs& a, const double* comp, double* W, Cand* cand, Cand* win,
+                          unsigned* pool_out) {
+    const DevModel& M = a.M;
+    __shared__ unsigned long long t_bits;
+    __shared__ int n_cand;
+    __shared__ Cand red[kRWarps];
+    const int nW = (M.n + 1) * M.PP;
+    const int k = a.k;
+    for (int e = threadIdx.x; e < nW; e += blockDim.x) {
+        const int svc = e / M.PP;
+        double w = 0.0;
+        if (svc < M.n) {
+            const double need = __dadd_rn(1.0, -comp[svc]);
+            if (need > 0.0) w = __dmul_rn(need, __ldg(&M.U[e]));
+        }
+        W[e] = w;
+    }
+    if (threadIdx.x == 0) {
+        t_bits = 0ull;
+        n_cand = 0;
+    }
+    __syncthreads();
+    double tmax = 0.0;
+    for (long long i = threadIdx.x; i < a.n_base; i += blockDim.x) tmax = fmax(tmax, row_score(W, __ldg(a.base + i)));
+    const double tw = warp_kth(tmax, k);
+    if ((threadIdx.x & 31u) == 0) atomicMax(&t_bits, static_cast<unsigned long long>(__double_as_longlong(tw)));
+    __syncthreads();
+    const double T = __longlong_as_double(static_cast<long long>(t_bits));
+    for (long long i0 = 0; i0 < a.n_base; i0 += blockDim.x) {
+        const long long i = i0 + threadIdx.x;
+        uint64_t row = 0;
+        double s = 0.0;
+        if (i < a.n_base) {
+            row = __ldg(a.base + i);
+            s = row_score(W, row);
+        }
+        const bool take = i < a.n_base && s > 0.0 && s >= T;
+        const unsigned b = __ballot_sync(0xffffffffu, take);
+        if (b) {
+            int at = 0;
+            if ((threadIdx.x & 31u) == 0) at = atomicAdd(&n_cand, __popc(b));
+            at = __shfl_sync(0xffffffffu, at, 0) + __popc(b & lanemask_lt());
+            if (take && at < kRCandCap) cand[at] = Cand{s, row_usum(M.U, row), row, i};
+        }
+    }
+    __syncthreads();
+    const int nc = n_cand;
+    int got;
+    if (nc <= kRCandCap) {
+        got = min(nc, k);
+        rank_select(M, cand, nc, k, win);
+    } else {  // exact: k rounds of "best row strictly after the previous pick"
+        got = 0;
+        Cand last{0.0, 0.0, kNoRow, -1};
+        for (int r = 0; r < k; ++r) {
+            Cand b{0.0, 0.0, kNoRow, -1};
+            for (long long i = threadIdx.x; i < a.n_base; i += blockDim.x) {
+                const uint64_t row = __ldg(a.base + i);
+                const double s = row_score(W, row);
+                if (!(s > 0.0)) continue;
+                const Cand c{s, row_usum(M.U, row), row, i};
+                if (r > 0 && !precedes(M, last, c)) continue;
+                if (b.row == kNoRow || precedes(M, c, b)) b = c;
+            }
+            for (int off = 16; off > 0; off >>= 1) {
+                const Cand o{__shfl_xor_sync(0xffffffffu, b.s, off), __shfl_xor_sync(0xffffffffu, b.u, off),
+                             __shfl_xor_sync(0xffffffffu, b.row, off), __shfl_xor_sync(0xffffffffu, b.pos, off)};
+                if (o.row != kNoRow && (b.row == kNoRow || precedes(M, o, b))) b = o;
+            }
+            if ((threadIdx.x & 31u) == 0) red[threadIdx.x >> 5] = b;
+            __syncthreads();
+            Cand x = red[0];
+            for (int w = 1; w < kRWarps; ++w)
+                if (red[w].row != kNoRow && (x.row == kNoRow || precedes(M, red[w], x))) x = red[w];
+            __syncthreads();
+            if (x.row == kNoRow) break;
+            if (threadIdx.x == 0) win[r] = x;
+            last = x;
+            ++got;
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x < got) pool_out[threadIdx.x] = static_cast<unsigned>(win[threadIdx.x].pos);
+    return got;
+}
+
+}  // namespace
+
+__global__ void __launch_bounds__(kRThreads, 1) rollout_kernel(const __grid_constant__ RolloutArgs a) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const DevModel& M = a.M;
+    const int n = M.n;
+    const int nk = (n + 63) / 64;
+    double* W = reinterpret_cast<double*>(smem);
+    double* comp_s = W + (n + 1) * M.PP;
+    Cand* cand = reinterpret_cast<Cand*>(comp_s + n + 1);
+    Cand* win = cand + kRCandCap;
+    __shared__ long long wbuf[kRWarps][32];  // per-warp survivor buffer (one atomic per 32 pushes)
+    __shared__ unsigned long long c_steps, c_done, c_cap, c_fail;
+    const int lane = static_cast<int>(threadIdx.x & 31u);
+    const int warp = static_cast<int>(threadIdx.x >> 5);
+    const long long gw = static_cast<long long>(blockIdx.x) * kRWarps + warp;
+    const long long nwarps = static_cast<long long>(gridDim.x) * kRWarps;
+    RolloutCounters* C = a.cnt;
+    unsigned* bc = &C->bar_count;
+    unsigned* bg = &C->bar_gen;
+    if (threadIdx.x == 0) c_steps = c_done = c_cap = c_fail = 0;
+    __syncthreads();
+
+    // One warp-step of rollout r (see the file comment).  first: the start state (no pick).
+    auto advance = [&](long long r, bool first, int nxt, int& nbuf) {
+        double c[kMaxJ];
+        const double* src = first ? a.comp0 : a.comp + r * n;
+#pragma unroll
+        for (int j = 0; j < kMaxJ; ++j) c[j] = (lane + 32 * j < n) ? src[lane + 32 * j] : 2.0;
+        int L = first ? 0 : a.len[r];
+        if (!first) {
+            const unsigned slot = a.rslot[r];
+            const int pn = __ldcg(&a.pool_n[slot]);
+            if (pn <= 0) {  // rollout: "no candidate config serves the remaining demand" (mcts.hpp:135-136)
+                if (lane == 0) {
+                    a.status[r] = 3;
+                    if (a.lengths) a.lengths[r] = -1;
+                    atomicAdd(&c_fail, 1ull);
+                }
+                return;
+            }
+            const uint64_t x = philox_u64(a.seed, static_cast<uint64_t>(a.id0 + r), static_cast<uint64_t>(L));
+            const unsigned pick = __ldcg(&a.pool[static_cast<size_t>(slot) * a.k + philox_below(x, pn)]);
+            add_row(M, __ldg(a.base + pick), c);
+            ++L;
+            if (lane == 0) {
+                a.len[r] = L;
+                atomicAdd(&c_steps, 1ull);
+            }
+        }
+        uint64_t kw[4];
+        if (!type_key(c, n, kw)) {  // satisfied
+            if (lane == 0) {
+                a.status[r] = 1;
+                if (a.lengths) a.lengths[r] = L;
+                atomicMin(&C->best, (static_cast<unsigned long long>(L) << 32) | static_cast<unsigned long long>(r));
+                atomicAdd(&c_done, 1ull);
+            }
+            return;
+        }
+        if (L >= a.max_depth) {  // rollout returns max_depth (mcts.hpp:127)
+            if (lane == 0) {
+                a.status[r] = 2;
+                if (a.lengths) a.lengths[r] = a.max_depth;
+                atomicAdd(&c_cap, 1ull);
+            }
+            return;
+        }
+#pragma unroll
+        for (int j = 0; j < kMaxJ; ++j)
+            if (lane + 32 * j < n) a.comp[r * n + lane + 32 * j] = c[j];
+        long long slot = 0;
+        if (lane == 0) {
+            bool created = false;
+            slot = probe(a, kw, nk, true, created);
+            if (slot < 0) {
+                atomicExch(&C->status, 1);
+                slot = 0;
+            } else {
+                if (created) {
+                    const unsigned long long at = atomicAdd(&C->n_pend[nxt], 1ull);
+                    (nxt ? a.pend1 : a.pend0)[at] = static_cast<unsigned>(slot);
+                }
+                if (__ldcg(&a.pool_n[slot]) < 0 && __ldcg(&a.claimer[slot]) > static_cast<unsigned long long>(r))
+                    atomicMin(&a.claimer[slot], static_cast<unsigned long long>(r));
+            }
+            a.rslot[r] = static_cast<unsigned>(slot);
+            wbuf[warp][nbuf] = r;
+        }
+        if (++nbuf == 32) {
+            if (lane == 0) {
+                const unsigned long long at = atomicAdd(&C->n_act[nxt], 32ull);
+                for (int i = 0; i < 32; ++i) (nxt ? a.act1 : a.act0)[at + i] = wbuf[warp][i];
+            }
+            __syncwarp();
+            nbuf = 0;
+        }
+    };
+    auto flush = [&](int nxt, int nbuf) {
+        if (nbuf && lane == 0) {
+            const unsigned long long at = atomicAdd(&C->n_act[nxt], static_cast<unsigned long long>(nbuf));
+            for (int i = 0; i < nbuf; ++i) (nxt ? a.act1 : a.act0)[at + i] = wbuf[warp][i];
+        }
+        __syncwarp();
+    };
+
+    // round 0: every rollout starts at the root
+    {
+        int nbuf = 0;
+        for (long long r = gw; r < a.n_roll; r += nwarps) advance(r, true, 0, nbuf);
+        flush(0, nbuf);
+    }
+    grid_barrier(bc, bg, gridDim.x);
+    int round = 0;
+    for (;; ++round) {
+        const int cur = round & 1, nxt = cur ^ 1;
+        const unsigned long long n_act = __ldcg(&C->n_act[cur]);
+        const unsigned long long n_pend = __ldcg(&C->n_pend[cur]);
+        if (n_act == 0 || __ldcg(&C->status) != 0) break;
+        if (blockIdx.x == 0 && threadIdx.x == 0) {  // last read in round - 1, next written after the barrier below
+            C->n_act[nxt] = 0;
+            C->n_pend[nxt] = 0;
+            C->keys += n_pend;
+        }
+        // build the pools of the keys first reached in this round (CTA per key)
+        for (unsigned long long p = blockIdx.x; p < n_pend; p += gridDim.x) {
+            const unsigned slot = __ldcg(&(cur ? a.pend1 : a.pend0)[p]);
+            const long long r = static_cast<long long>(__ldcg(&a.claimer[slot]));
+            for (int i = threadIdx.x; i < n; i += blockDim.x) comp_s[i] = __ldcg(&a.comp[r * n + i]);
+            __syncthreads();
+            const int got = block_topk(a, comp_s, W, cand, win, a.pool + static_cast<size_t>(slot) * a.k);
+            if (threadIdx.x == 0) a.pool_n[slot] = got;
+            __syncthreads();
+        }
+        grid_barrier(bc, bg, gridDim.x);
+        int nbuf = 0;
+        const long long* act = cur ? a.act1 : a.act0;
+        for (long long i = gw; i < static_cast<long long>(n_act); i += nwarps) advance(__ldcg(&act[i]), false, nxt, nbuf);
+        flush(nxt, nbuf);
+        grid_barrier(bc, bg, gridDim.x);
+    }
+    if (threadIdx.x == 0) {
+        atomicAdd(&C->steps, c_steps);
+        atomicAdd(&C->completed, c_done);
+        atomicAdd(&C->capped, c_cap);
+        atomicAdd(&C->failed, c_fail);
+    }
+    // replay the winner from the immutable cache: its path, pick by pick
+    if (blockIdx.x == 0 && warp == 0) {
+        const unsigned long long best = __ldcg(&C->best);
+        int plen = 0;
+        if (best != ~0ull && __ldcg(&C->status) == 0) {
+            const long long r = static_cast<long long>(best & 0xFFFFFFFFull);
+            const int L = static_cast<int>(best >> 32);
+            double c[kMaxJ];
+#pragma unroll
+            for (int j = 0; j < kMaxJ; ++j) c[j] = (lane + 32 * j < n) ? a.comp0[lane + 32 * j] : 2.0;
+            for (int t = 0; t < L; ++t) {
+                uint64_t kw[4];
+                type_key(c, n, kw);
+                long long slot = 0;
+                if (lane == 0) {
+                    bool created;
+                    slot = probe(a, kw, nk, false, created);
+                }
+                slot = __shfl_sync(0xffffffffu, slot, 0);
+                const int pn = __ldcg(&a.pool_n[slot]);
+                const uint64_t x = philox_u64(a.seed, static_cast<uint64_t>(a.id0 + r), static_cast<uint64_t>(t));
+                const unsigned pick = __ldcg(&a.pool[static_cast<size_t>(slot) * a.k + philox_below(x, pn)]);
+                if (lane == 0) a.path[t] = pick;
+                add_row(M, __ldg(a.base + pick), c);
+            }
+            plen = L;
+        }
+        if (lane == 0) {
+            *a.path_len = plen;
+            C->rounds = round;
+        }
+    }
+}
+
+size_t rollout_smem_bytes(int n, int PP) {
+    return static_cast<size_t>((n + 1) * PP + n + 1) * 8 + static_cast<size_t>(kRCandCap + kRMaxK) * sizeof(Cand);
+}
+const void* rollout_kernel_ptr() { return reinterpret_cast<const void*>(&rollout_kernel); }
+int rollout_threads() { return kRThreads; }
+
+}  // namespace mgb

@@ -1,59 +1,35 @@
-// topk.cu — K4: single-pass top-K (detail::topk_candidates, mcts.hpp:56-76) for k <= 32.
+// topk.cu — K4: single-launch top-K (detail::topk_candidates, mcts.hpp:56-76) for k <= 32.
 //
 // The reference scores every candidate, keeps s > 0, sorts by candidate_preferred
-// (greedy.hpp:63-67) and truncates to K.  That order is total, so the top-K is built
-// here in one pass with a WARP-DISTRIBUTED sorted list: lane r of a warp holds the r-th
-// best candidate seen so far.  Each batch of 32 rows (one per lane) is scored, filtered
-// against the current K-th best with one ballot, and the few survivors are inserted by
-// rank (ballot+popc) and a shfl_up shift — O(1) warp instructions per insertion and no
-// per-thread serial insertion sort.  Warp lists are merged by warp 0 of each CTA through
-// shared memory, CTA lists by the last CTA to finish (atomic ticket): one launch, no grid
-// barrier, no cooperative launch.  MCTS calls this on every rollout-cache miss and every
-// expansion, so latency is the figure of merit.
+// (greedy.hpp:63-67) and truncates to K.  That order is total, so only the few rows that
+// can reach the top K need to be ordered at all:
+//   1. every thread scores its <= 16 rows of the CTA's chunk into registers;
+//   2. every warp sorts its 32 per-lane maxima (bitonic, shuffles only) and takes the K-th
+//      largest; the CTA threshold T is the largest such value over the warps — at least K
+//      rows of the CTA score >= T, so the CTA's exact top-K lies among its rows >= T;
+//   3. those few rows go to shared memory and are ranked IN PARALLEL (thread i counts the
+//      candidates preferred to candidate i): no serial insertion, no block-wide sort;
+//   4. with more than one CTA, the last CTA to finish (atomic ticket) ranks the G x K
+//      per-CTA winners the same way.
+// One launch, no grid barrier, no cooperative launch.  MCTS calls this on every
+// rollout-cache miss and every expansion, so latency is the figure of merit.
+// A CTA whose rows tie at T beyond the candidate capacity reports overflow (*n_out = -1)
+// and the host re-runs the exact k-round kernel (kernels.cu) — a pathological case.
 #include "common.cuh"
 
 namespace mgb {
 
 namespace {
 
-constexpr int kTopkThreads = 256;
+constexpr int kTopkThreads = 512;
 constexpr int kTopkWarps = kTopkThreads / 32;
-constexpr int kRowsPerThread = 8;  // the host sizes the grid so every row has a thread slot
-constexpr int kCandCap = 1024;     // per-CTA candidates above the threshold held in smem
+constexpr int kRowsPerThread = 16;  // the host sizes the grid so every row has a register slot
+constexpr int kCandCap = 2048;      // per-CTA candidates (and merged per-CTA winners) in smem
+constexpr int kTopkMaxK = 32;
 
-__device__ __forceinline__ unsigned lane() { return threadIdx.x & 31u; }
-
-// candidate_preferred on (score, util_sum, row); "none" (row == kNoRow, s == 0) loses to all.
-__device__ __forceinline__ bool pref(const DevModel& M, const Best& a, const Best& b) { return dev::better(M, a, b); }
-__device__ __forceinline__ Best nil() { return dev::none(); }
-
-__device__ __forceinline__ Best shfl(const Best& b, int src) {
-    return Best{__shfl_sync(0xffffffffu, b.s, src), __shfl_sync(0xffffffffu, b.u, src),
-                __shfl_sync(0xffffffffu, b.row, src)};
-}
-
-__device__ __forceinline__ Best shfl_up1(const Best& b) {
-    return Best{__shfl_up_sync(0xffffffffu, b.s, 1), __shfl_up_sync(0xffffffffu, b.u, 1),
-                __shfl_up_sync(0xffffffffu, b.row, 1)};
-}
-
-// Offer one candidate per lane (valid lanes only) to the warp list `wl` (lane r = rank r,
-// r < k).  Candidates must be distinct rows.
-__device__ __forceinline__ void warp_offer(const DevModel& M, Best& wl, const Best& c, bool valid, int k) {
-    const Best kth = shfl(wl, k - 1);
-    unsigned todo = __ballot_sync(0xffffffffu, valid && pref(M, c, kth));
-    while (todo) {
-        const int src = __ffs(todo) - 1;
-        todo &= todo - 1;
-        const Best x = shfl(c, src);
-        const bool ahead = static_cast<int>(lane()) < k && pref(M, wl, x);
-        const int rank = __popc(__ballot_sync(0xffffffffu, ahead));
-        if (rank >= k) continue;
-        const Best up = shfl_up1(wl);
-        if (static_cast<int>(lane()) > rank && static_cast<int>(lane()) < k) wl = up;
-        if (static_cast<int>(lane()) == rank) wl = x;
-    }
-}
+using dev::Cand;
+using dev::rank_select;
+using dev::warp_kth;
 
 }  // namespace
 
@@ -63,15 +39,19 @@ __global__ void __launch_bounds__(kTopkThreads, 1) topk1_kernel(const __grid_con
     const int nW = (M.n + 1) * M.PP;
     double* W = reinterpret_cast<double*>(smem);
     double* comp = W + nW;
-    Best* wlist = reinterpret_cast<Best*>(comp + M.n + 1);  // [warps][32]
-    Best* cand = wlist + kTopkWarps * 32;                    // [kCandCap]
-    __shared__ double thr[kTopkThreads];
+    Cand* cand = reinterpret_cast<Cand*>(comp + M.n + 1);  // [kCandCap]
+    Cand* win = cand + kCandCap;                           // [kTopkMaxK]
+    __shared__ unsigned long long t_bits;
     __shared__ int n_cand;
     __shared__ uint64_t mask[4];
     __shared__ bool last;
     const int k = a.k;
     for (int i = threadIdx.x; i < M.n; i += blockDim.x) comp[i] = a.comp[i];
     if (threadIdx.x < 4) mask[threadIdx.x] = a.svc_mask ? a.svc_mask[threadIdx.x] : ~0ull;
+    if (threadIdx.x == 0) {
+        t_bits = 0ull;
+        n_cand = 0;
+    }
     __syncthreads();
     for (int e = threadIdx.x; e < nW; e += blockDim.x) {  // W = need * U (greedy.hpp:38-41)
         const int svc = e / M.PP;
@@ -84,20 +64,21 @@ __global__ void __launch_bounds__(kTopkThreads, 1) topk1_kernel(const __grid_con
     }
     __syncthreads();
 
-    // Pass 1: every thread scores its (<= kRowsPerThread) rows into registers.
-    const int warp = threadIdx.x >> 5;
+    // 1. score this CTA's chunk into registers (coalesced: consecutive threads, consecutive rows)
     const long long total = a.index ? a.n_index : a.n_rows;
-    const long long stride = static_cast<long long>(gridDim.x) * blockDim.x;
+    const long long chunk = (total + gridDim.x - 1) / gridDim.x;
+    const long long lo = static_cast<long long>(blockIdx.x) * chunk;
+    const long long hi = min(total, lo + chunk);
     uint64_t myrow[kRowsPerThread];
     double mys[kRowsPerThread];
     double tmax = 0.0;
 #pragma unroll
     for (int r = 0; r < kRowsPerThread; ++r) {
-        const long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x + r * stride;
+        const long long i = lo + threadIdx.x + static_cast<long long>(r) * blockDim.x;
         mys[r] = 0.0;
         myrow[r] = kNoRow;
-        if (i < total) {
-            const uint64_t row = __ldg(a.rows + (a.index ? a.index[i] : i));
+        if (i < hi) {
+            const uint64_t row = __ldg(a.rows + (a.index ? __ldg(a.index + i) : i));
             bool ok = true;
             if (a.svc_mask) {
                 bool hit = false;
@@ -109,9 +90,7 @@ __global__ void __launch_bounds__(kTopkThreads, 1) topk1_kernel(const __grid_con
                 ok = hit;
             }
             if (ok) {  // score, greedy.hpp:36-43 (ascending members, no FMA)
-                double s = __dadd_rn(W[row & 0xFFFFull], W[(row >> 16) & 0xFFFFull]);
-                s = __dadd_rn(s, W[(row >> 32) & 0xFFFFull]);
-                s = __dadd_rn(s, W[row >> 48]);
+                const double s = dev::row_score(W, row);
                 if (s > 0.0) {
                     mys[r] = s;
                     myrow[r] = row;
@@ -120,104 +99,84 @@ __global__ void __launch_bounds__(kTopkThreads, 1) topk1_kernel(const __grid_con
             }
         }
     }
-    // Threshold: T = the k-th largest per-thread maximum in this CTA.  At least k rows of
-    // the CTA score >= T, so the CTA's exact top-k lies among its rows with s >= T.
-    thr[threadIdx.x] = tmax;
-    if (threadIdx.x == 0) n_cand = 0;
+    // 2. threshold: the largest per-warp K-th lane maximum (non-negative doubles order as
+    //    their bit patterns, so an integer atomicMax on the bits is a max on the values)
+    const double tw = warp_kth(tmax, k);
+    if ((threadIdx.x & 31u) == 0) atomicMax(&t_bits, static_cast<unsigned long long>(__double_as_longlong(tw)));
     __syncthreads();
-    for (int k2 = 2; k2 <= kTopkThreads; k2 <<= 1)  // bitonic sort, descending
-        for (int j = k2 >> 1; j > 0; j >>= 1) {
-            const int t = threadIdx.x, p = t ^ j;
-            if (p > t) {
-                const double x = thr[t], y = thr[p];
-                if (((t & k2) == 0) ? (x < y) : (x > y)) {
-                    thr[t] = y;
-                    thr[p] = x;
-                }
-            }
-            __syncthreads();
-        }
-    const double T = thr[k - 1];
+    const double T = __longlong_as_double(static_cast<long long>(t_bits));
+    // 3. collect rows >= T (warp-aggregated appends), then rank them in parallel
 #pragma unroll
-    for (int r = 0; r < kRowsPerThread; ++r)
-        if (myrow[r] != kNoRow && mys[r] >= T) {
-            const int at = atomicAdd(&n_cand, 1);
-            if (at < kCandCap) cand[at] = Best{mys[r], 0.0, myrow[r]};
+    for (int r = 0; r < kRowsPerThread; ++r) {
+        const bool take = myrow[r] != kNoRow && mys[r] >= T;
+        const unsigned b = __ballot_sync(0xffffffffu, take);
+        if (b) {
+            int at = 0;
+            if ((threadIdx.x & 31u) == 0) at = atomicAdd(&n_cand, __popc(b));
+            at = __shfl_sync(0xffffffffu, at, 0) + __popc(b & dev::lanemask_lt());
+            if (take && at < kCandCap)
+                cand[at] = Cand{mys[r], 0.0, myrow[r], lo + threadIdx.x + static_cast<long long>(r) * blockDim.x};
         }
+    }
     __syncthreads();
     const int nc = n_cand;
-    if (warp == 0) {
-        Best bl = nil();
-        if (nc <= kCandCap) {  // exact top-k of the candidates (warp-distributed insertion)
-            for (int b0 = 0; b0 < nc; b0 += 32) {
-                const int i = b0 + static_cast<int>(lane());
-                Best c = i < nc ? cand[i] : nil();
-                if (i < nc) c.u = dev::row_usum(M.U, c.row);
-                warp_offer(M, bl, c, i < nc, k);
-            }
-        }
-        wlist[lane()] = bl;
+    if (nc > kCandCap) {  // pathological ties at T: the host re-runs the exact k-round kernel
+        if (threadIdx.x == 0) *a.n_out = -1;
+        return;
     }
-    if (nc > kCandCap) {  // pathological ties at T: every warp offers all its rows (exact)
-        Best wl = nil();
-#pragma unroll
-        for (int r = 0; r < kRowsPerThread; ++r) {
-            Best c{mys[r], 0.0, myrow[r]};
-            const bool ok = myrow[r] != kNoRow;
-            if (ok) c.u = dev::row_usum(M.U, c.row);
-            warp_offer(M, wl, c, ok, k);
-        }
-        __syncthreads();
-        wlist[warp * 32 + lane()] = wl;
-    }
+    for (int i = threadIdx.x; i < nc; i += blockDim.x) cand[i].u = dev::row_usum(M.U, cand[i].row);
     __syncthreads();
-    if (warp == 0) {
-        Best bl = wlist[lane()];
-        if (nc > kCandCap)
-            for (int w = 1; w < kTopkWarps; ++w) {
-                const Best c = wlist[w * 32 + lane()];
-                warp_offer(M, bl, c, static_cast<int>(lane()) < k && c.row != kNoRow, k);
-            }
-        if (gridDim.x == 1) {
-            const bool v = static_cast<int>(lane()) < k && bl.row != kNoRow;
-            const unsigned valid = __ballot_sync(0xffffffffu, v);
-            if (v) a.out_row[lane()] = bl.row;
-            if (lane() == 0) *a.n_out = __popc(valid);
-        } else {
-            a.partials[blockIdx.x * 32 + lane()] = bl;
-            __threadfence();
-            unsigned t = 0;
-            if (lane() == 0) t = atomicAdd(a.ticket, 1u);
-            t = __shfl_sync(0xffffffffu, t, 0);
-            if (lane() == 0) last = (t == gridDim.x - 1);
-        }
-    }
-    if (gridDim.x == 1) return;
+    const int got = min(nc, k);
+    rank_select(M, cand, nc, k, win);
     __syncthreads();
-    if (!last || warp != 0) return;
+    if (gridDim.x == 1) {
+        if (threadIdx.x < got) a.out_row[threadIdx.x] = win[threadIdx.x].row;
+        if (threadIdx.x == 0) *a.n_out = got;
+        return;
+    }
+    // 4. publish this CTA's winners; the last CTA ranks the G x K of them
+    Best* part = a.partials + static_cast<long long>(blockIdx.x) * kTopkMaxK;
+    if (threadIdx.x < kTopkMaxK) {
+        const Cand c = threadIdx.x < got ? win[threadIdx.x] : Cand{0.0, 0.0, kNoRow, 0};
+        __stcg(&part[threadIdx.x].s, c.s);
+        __stcg(&part[threadIdx.x].u, c.u);
+        __stcg(reinterpret_cast<unsigned long long*>(&part[threadIdx.x].row), static_cast<unsigned long long>(c.row));
+    }
     __threadfence();
-    Best gl = nil();
-    for (unsigned b = 0; b < gridDim.x; ++b) {  // last CTA merges the per-CTA lists
-        const Best* p = &a.partials[b * 32 + lane()];
-        const Best c{__ldcg(&p->s), __ldcg(&p->u), __ldcg(reinterpret_cast<const unsigned long long*>(&p->row))};
-        warp_offer(M, gl, c, static_cast<int>(lane()) < k && c.row != kNoRow, k);
+    __syncthreads();
+    if (threadIdx.x == 0) last = atomicAdd(a.ticket, 1u) == gridDim.x - 1;
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    if (threadIdx.x == 0) n_cand = 0;
+    __syncthreads();
+    for (int i = threadIdx.x; i < static_cast<int>(gridDim.x) * k; i += blockDim.x) {
+        const Best* p = a.partials + static_cast<long long>(i / k) * kTopkMaxK + (i % k);
+        const uint64_t row = __ldcg(reinterpret_cast<const unsigned long long*>(&p->row));
+        if (row == kNoRow) continue;
+        const int at = atomicAdd(&n_cand, 1);
+        // CTA chunks are disjoint and ascending, so (CTA, rank) orders duplicates by position
+        cand[at] = Cand{__ldcg(&p->s), __ldcg(&p->u), row, static_cast<long long>(i)};
     }
-    const bool v = static_cast<int>(lane()) < k && gl.row != kNoRow;
-    const unsigned valid = __ballot_sync(0xffffffffu, v);
-    if (v) a.out_row[lane()] = gl.row;
-    if (lane() == 0) {
-        *a.n_out = __popc(valid);
+    __syncthreads();
+    const int mc = n_cand;
+    const int mgot = min(mc, k);
+    rank_select(M, cand, mc, k, win);
+    __syncthreads();
+    if (threadIdx.x < mgot) a.out_row[threadIdx.x] = win[threadIdx.x].row;
+    if (threadIdx.x == 0) {
+        *a.n_out = mgot;
         *a.ticket = 0;
     }
 }
 
 size_t topk1_smem_bytes(int n, int PP, int) {
-    return static_cast<size_t>((n + 1) * PP + n + 1) * 8 +
-           static_cast<size_t>(kTopkWarps * 32 + kCandCap) * sizeof(Best);
+    return static_cast<size_t>((n + 1) * PP + n + 1) * 8 + static_cast<size_t>(kCandCap + kTopkMaxK) * sizeof(Cand);
 }
 int topk1_threads() { return kTopkThreads; }
 int topk1_rows_per_cta() { return kTopkThreads * kRowsPerThread; }
-int topk1_max_k() { return 32; }
+int topk1_max_k() { return kTopkMaxK; }
+int topk1_max_ctas() { return kCandCap / kTopkMaxK; }
 const void* topk1_kernel_ptr(int) { return reinterpret_cast<const void*>(&topk1_kernel); }
 
 }  // namespace mgb

@@ -827,6 +827,71 @@ class MctsProcedure(OptimizerProcedure):  # mcts.hpp:254-260
         return mcts_solve(comp, ctx, self.params, rng())
 
 
+# ---------------------------------------------------------------- MCTS throughput mode (rollout.cu)
+
+
+@dataclass
+class RolloutParams:
+    """Root-parallel rollouts (include/migplan_b200.h, mig_rollouts): Philox draws, lock-step
+    rounds, one shared key cache per call.  max_depth < 0: 2 * |fast_algo(comp)|."""
+    n_rollouts: int = 1 << 16
+    topk: int = 10
+    max_depth: int = -1
+    seed: int = 0
+    id_offset: int = 0
+    batch: int = 0
+    table_log2: int = 0
+
+    def to_c(self) -> abi.RolloutParamsC:
+        return abi.RolloutParamsC(self.n_rollouts, self.topk, self.max_depth, self.seed & (2**64 - 1),
+                                  self.id_offset, self.batch, self.table_log2)
+
+
+@dataclass
+class RolloutResult:
+    best_len: int
+    max_depth: int
+    best_id: int
+    completed: int
+    capped: int
+    failed: int
+    steps: int
+    keys: int
+    rounds: int
+    device_ms: float
+    path: list = field(default_factory=list)  # pool indices of the best rollout
+    lengths: list | None = None
+
+
+def _rollout_result(r: abi.RolloutResultC, path, lengths) -> RolloutResult:
+    return RolloutResult(r.best_len, r.max_depth, r.best_id, r.completed, r.capped, r.failed, r.steps, r.keys,
+                         r.rounds, r.device_ms, path, lengths)
+
+
+def rollouts(comp, ctx: PlanContext, params: RolloutParams, lengths: bool = False) -> RolloutResult:
+    """params.n_rollouts root-parallel rollouts from `comp` (rollout, mcts.hpp:122-143, run
+    concurrently with Philox draws); returns the shortest completed one."""
+    buf, n = ctx._comp(comp)
+    pc = params.to_c()
+    res = abi.RolloutResultC()
+    lbuf = (C.c_int32 * max(params.n_rollouts, 1))() if lengths else None
+    cap = 1 << 16
+    path = (C.c_int64 * cap)()
+    ctx.backend.check(ctx.backend.lib.mig_rollouts(ctx._p, buf, n, C.byref(pc), lbuf, path, cap, C.byref(res)))
+    return _rollout_result(res, list(path[:res.path_len]), list(lbuf[:params.n_rollouts]) if lengths else None)
+
+
+def mcts_solve_parallel(comp, ctx: PlanContext, params: RolloutParams) -> tuple[list[GpuConfig], RolloutResult]:
+    """Throughput-mode mcts_solve: the shorter of fast_algo(comp) and the best root-parallel
+    rollout (fast_ref wins ties, mcts.hpp:245-251)."""
+    buf, n = ctx._comp(comp)
+    pc = params.to_c()
+    res = abi.RolloutResultC()
+    plan = _run_plan(ctx, lambda out, cap, nout: ctx.backend.lib.mig_mcts_solve_parallel(
+        ctx._p, buf, n, C.byref(pc), out, cap, C.byref(nout), C.byref(res)))
+    return plan, _rollout_result(res, [], None)
+
+
 # ---------------------------------------------------------------- GA (ga.hpp)
 
 
