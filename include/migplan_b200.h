@@ -233,6 +233,25 @@ int mig_rollouts(mig_ctx* ctx, const double* comp, int32_t n, const mig_rollout_
 int mig_mcts_solve_parallel(mig_ctx* ctx, const double* comp, int32_t n, const mig_rollout_params* params,
                             mig_config* out, int32_t cap, int32_t* n_out, mig_rollout_result* result);
 
+/* ---- sharded greedy across ranks (product) ----
+ * The reference's fast_algo scans one working set on one core.  Sharded, every rank's
+ * context keeps 1/n_ranks of every working set (base supports by index mod n_ranks,
+ * extension supports by a fixed hash) and the persistent greedy kernel exchanges its
+ * per-step winner with the other ranks through EXCHANGE BOARDS: small device buffers, one
+ * per rank, written by every rank with peer stores (CUDA IPC over NVLink/NVSwitch, or
+ * plain device pointers for ranks sharing a GPU).  Every rank applies the same global
+ * winner, so plans are bit-identical to the unsharded fast_algo at any rank count.
+ * Protocol: each rank allocates its board (mig_board_alloc), the ranks exchange the IPC
+ * handles, open the peers' boards (mig_board_open), call mig_ctx_set_shard with all
+ * n_ranks board pointers (boards[rank] = own), BARRIER, then call mig_fast_algo SPMD.
+ * A missing peer fails the call with MIG_ERR_DEVICE after a watchdog (no hang). */
+int mig_board_bytes(int32_t n_ranks, int64_t* bytes);
+int mig_board_alloc(int32_t device, int32_t n_ranks, void** board, uint8_t* ipc_handle /* 64 bytes, or NULL */);
+int mig_board_open(int32_t device, const uint8_t* ipc_handle /* 64 bytes */, void** board);
+int mig_board_free(void* board, int32_t opened /* 1: from mig_board_open */);
+/* max_ctas > 0 caps the greedy grid of this context (ranks sharing one GPU). */
+int mig_ctx_set_shard(mig_ctx* ctx, int32_t rank, int32_t n_ranks, void* const* boards, int32_t max_ctas);
+
 /* ---- GA (ga.hpp) ---- */
 typedef struct mig_ga_params { /* GaParams, ga.hpp:24-36 */
     int32_t population;

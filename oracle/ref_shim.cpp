@@ -577,6 +577,23 @@ int mig_mcts_solve_parallel(mig_ctx* ctx, const double* comp, int32_t n, const m
     return g != MIG_OK ? g : rc;
 }
 
+// Sharding is a device feature of the product (include/migplan_b200.h); the CPU checkers
+// plan unsharded, so only the trivial single-rank shard is accepted.
+int mig_board_bytes(int32_t n_ranks, int64_t* bytes) {
+    return guarded([&] { *bytes = (int64_t)(32 * 2 * (n_ranks > 0 ? n_ranks : 1)); });
+}
+int mig_board_alloc(int32_t, int32_t, void**, uint8_t*) {
+    return guarded([&] { throw std::invalid_argument("exchange boards are device memory (product only)"); });
+}
+int mig_board_open(int32_t, const uint8_t*, void**) {
+    return guarded([&] { throw std::invalid_argument("exchange boards are device memory (product only)"); });
+}
+int mig_board_free(void*, int32_t) { return MIG_OK; }
+int mig_ctx_set_shard(mig_ctx*, int32_t rank, int32_t n_ranks, void* const*, int32_t) {
+    return guarded([&] {
+        if (n_ranks != 1 || rank != 0) throw std::invalid_argument("sharded greedy is a device feature (product only)");
+    });
+}
 void mig_ga_params_defaults(mig_ga_params* out) {
     GaParams g;
     std::memset(out, 0, sizeof *out);

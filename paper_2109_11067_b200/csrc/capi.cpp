@@ -481,6 +481,29 @@ int mig_mcts_solve_parallel(mig_ctx* ctx, const double* comp, int32_t n, const m
     return g != MIG_OK ? g : rc;
 }
 
+int mig_board_bytes(int32_t n_ranks, int64_t* bytes) {
+    return guarded([&] { *bytes = static_cast<int64_t>(board_bytes(n_ranks)); });
+}
+int mig_board_alloc(int32_t device, int32_t n_ranks, void** board, uint8_t* ipc_handle) {
+    return guarded([&] { *board = board_alloc(device, n_ranks, ipc_handle); });
+}
+int mig_board_open(int32_t device, const uint8_t* ipc_handle, void** board) {
+    return guarded([&] { *board = board_open(device, ipc_handle); });
+}
+int mig_board_free(void* board, int32_t opened) {
+    return guarded([&] { board_close(board, opened != 0); });
+}
+int mig_ctx_set_shard(mig_ctx* ctx, int32_t rank, int32_t n_ranks, void* const* boards, int32_t max_ctas) {
+    return guarded([&] {
+        std::vector<void*> b;
+        if (n_ranks > 1) {
+            if (!boards) throw ArgumentError("set_shard: null boards");
+            b.assign(boards, boards + n_ranks);
+        }
+        ctx->e->set_shard(rank, n_ranks, b, max_ctas);
+    });
+}
+
 int mig_completion_of(const mig_ctx* ctx, const mig_config* configs, int32_t n_configs, double* comp_out) {
     return guarded([&] {
         std::vector<Config> cfgs;

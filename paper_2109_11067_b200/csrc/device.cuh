@@ -46,9 +46,20 @@ struct GreedyState {
     // CTA-0 %globaltimer phase totals (ns): 0 build W + scan + block reduce, 1 grid barrier,
     // 2 grid reduce + completion update, 3 maybe_extend, 4 extension enumeration + barrier
     unsigned long long phase_ns[5];
+    unsigned long long last_seq;  // sharded greedy: exchange sequence number of the last step
 };
 
-enum GreedyStatus { kOk = 0, kNoPositive = 1, kExtOverflow = 2, kStepOverflow = 3 };
+enum GreedyStatus { kOk = 0, kNoPositive = 1, kExtOverflow = 2, kStepOverflow = 3, kExchTimeout = 4 };
+
+// One record of the sharded greedy's per-step exchange board (kernels.cu exchange_best).
+// A board is [2 parities][n_ranks] slots; seq = global step counter + 1 (monotonic).
+struct ExchSlot {
+    double s;
+    double u;
+    unsigned long long row;
+    unsigned long long seq;
+};
+constexpr int kMaxRanks = 8;
 
 struct GreedyArgs {
     DevModel M;
@@ -57,6 +68,8 @@ struct GreedyArgs {
     long long cap;        // arena capacity (rows)
     int cache_units;      // 16-byte row units of shared-memory cache per CTA
     int phase_timers;     // 1: CTA 0 records %globaltimer phase totals (diagnostics)
+    int prefetch;         // bulk L2 prefetch distance of the streaming scan (iterations; 0 off)
+    int load_mode;        // streaming row load flavour (kernels.cu ld_row4)
     const double* comp0;  // host-mapped pinned
     GreedyState* st;      // device (barrier + atomics)
     GreedyState* out;     // host-mapped pinned: final state written by CTA 0
@@ -69,6 +82,12 @@ struct GreedyArgs {
     long long* host_pick_rows;
     int* ev_svc;          // events recorded (service, in order)
     int cap_steps;
+    // sharded greedy: this rank scans 1/n_ranks of every working set
+    int n_ranks;          // 1: unsharded
+    int rank;
+    ExchSlot* boards[kMaxRanks];  // every rank's exchange board (peer or local device memory)
+    unsigned long long exch_seq0; // step counter base of this call (monotonic across calls)
+    long long exch_timeout_ns;
 };
 
 struct TopkArgs {
@@ -86,20 +105,23 @@ struct TopkArgs {
     int* n_out;
 };
 
-// Single-pass top-K (topk.cu), k <= 16.
+// Single-launch top-K (topk.cu), k <= 32.  The completion vector and the service mask
+// travel inside the launch parameters: no host-mapped reads on the latency path.
 struct Topk1Args {
     DevModel M;
     const uint64_t* rows;
     long long n_rows;
     const long long* index;
     long long n_index;
-    const uint64_t* svc_mask;
-    const double* comp;
+    int use_mask;
     int k;
-    Best* partials;     // gridDim.x * 16 per-CTA lists
+    long long rows_per_cta;
+    Best* partials;     // gridDim.x * 32 per-CTA lists
     unsigned* ticket;   // zero before launch; reset by the last CTA
     uint64_t* out_row;  // k (host-mapped)
     int* n_out;         // host-mapped
+    uint64_t svc_mask[4];
+    double comp[256];
 };
 
 // Throughput-mode root-parallel rollouts (rollout.cu).
@@ -117,7 +139,6 @@ struct RolloutArgs {
     DevModel M;
     const uint64_t* base;   // base pool rows (the rollout pool, mcts.hpp:129-133)
     long long n_base;
-    const double* comp0;    // start completion (host-mapped)
     long long n_roll;       // rollouts in this batch
     long long id0;          // global id of the batch's rollout 0 (Philox stream id)
     uint64_t seed;          // Philox key
@@ -142,6 +163,7 @@ struct RolloutArgs {
     long long* path;        // host-mapped: winner replay (base-pool indices), max_depth
     int* path_len;          // host-mapped
     int* lengths;           // optional, n_roll: steps (capped: max_depth, empty pool: -1)
+    double comp0[256];      // start completion (travels with the launch)
 };
 
 }  // namespace mgb

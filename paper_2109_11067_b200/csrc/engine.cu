@@ -7,6 +7,7 @@
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
+#include <cstdio>
 #include <functional>
 
 #include "engine.hpp"
@@ -143,53 +144,77 @@ bool config_equal(const Config& a, const Config& b) { return !config_less(a, b) 
 Engine::Engine(const Rules& rules, std::map<std::string, ModelProfile> profiles, std::vector<Service> services,
                int max_mix, int device)
     : profiles_(std::move(profiles)), device_(device) {
+    const auto tb = std::chrono::steady_clock::now();
     for (const auto& [name, p] : profiles_) validate_profile(p);
     m_ = build_model(rules, profiles_, services, max_mix);
 
-    int ndev = 0;
-    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
-        throw DeviceError("no CUDA device available: the B200 planner has no CPU fallback");
-    if (device < 0 || device >= ndev) throw DeviceError("CUDA device index out of range");
-    CK(cudaSetDevice(device));
-    cudaDeviceProp prop{};
-    CK(cudaGetDeviceProperties(&prop, device));
-    if (prop.major < 10) throw DeviceError(std::string("device ") + prop.name + " is not sm_100-class (B200)");
-    num_sms_ = prop.multiProcessorCount;
+    using clk = std::chrono::steady_clock;
+    const auto t0 = clk::now();
+    const DeviceInfo& info = device_info(device);  // process-wide: properties + kernel attributes, once
+    num_sms_ = info.num_sms;
+    const auto t1 = clk::now();
 
     const int T = kernel_threads();
     // greedy: everything but the row cache is fixed; the cache takes the rest of the
     // opt-in shared memory (one CTA per SM), rounded to whole units per thread.
     {
         const long long fixed = static_cast<long long>(greedy_smem_bytes(m_.n, m_.PP, 0));
-        long long room = static_cast<long long>(prop.sharedMemPerBlockOptin) - 2048 - fixed;
+        long long room = static_cast<long long>(info.smem_optin) - 2048 - fixed;
         cache_units_ = static_cast<int>(std::max<long long>(0, room / 16) / T * T);
         if (const char* e = std::getenv("MIGPLAN_ROW_CACHE_UNITS"))
             cache_units_ = std::max(0, std::min(cache_units_, std::atoi(e) / T * T));
     }
     const size_t gsm = greedy_smem_bytes(m_.n, m_.PP, cache_units_), tsm = topk_smem_bytes(m_.n, m_.PP);
-    CK(cudaFuncSetAttribute(greedy_kernel_ptr(), cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(gsm)));
-    CK(cudaFuncSetAttribute(topk_kernel_ptr(), cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(tsm)));
-    for (int km : {32})
-        CK(cudaFuncSetAttribute(topk1_kernel_ptr(km), cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                static_cast<int>(topk1_smem_bytes(m_.n, m_.PP, km))));
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&greedy_blocks_per_sm_, greedy_kernel_ptr(), T, gsm));
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&topk_blocks_per_sm_, topk_kernel_ptr(), T, tsm));
-    {
-        const size_t rsm = rollout_smem_bytes(m_.n, m_.PP);
-        CK(cudaFuncSetAttribute(rollout_kernel_ptr(), cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(rsm)));
-        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&rollout_blocks_per_sm_, rollout_kernel_ptr(), rollout_threads(),
-                                                         rsm));
-        if (rollout_blocks_per_sm_ < 1) throw DeviceError("rollout kernel does not fit on an SM");
-    }
-    if (greedy_blocks_per_sm_ < 1 || topk_blocks_per_sm_ < 1) throw DeviceError("kernel does not fit on an SM");
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&rollout_blocks_per_sm_, rollout_kernel_ptr(), rollout_threads(),
+                                                     rollout_smem_bytes(m_.n, m_.PP)));
+    if (greedy_blocks_per_sm_ < 1 || topk_blocks_per_sm_ < 1 || rollout_blocks_per_sm_ < 1)
+        throw DeviceError("kernel does not fit on an SM");
 
-    // ---- device model tables
-    g_h2d = &stats.h2d;
+    // ---- K1 input: every support with 1..max_mix members and its row offset (pool order)
+    std::vector<uint32_t> supports;
+    std::vector<long long> offsets;
+    long long total = 0;
+    {
+        std::vector<int> sv(kRowK);
+        for (int k = 1; k <= max_mix; ++k) {
+            std::function<void(int, int)> rec = [&](int from, int d) {
+                if (d == k) {
+                    long long c = m_.rows_for_support(sv.data(), k);
+                    if (c == 0) return;
+                    uint32_t packed = 0xFFFFFFFFu;
+                    for (int j = 0; j < k; ++j) packed = (packed & ~(0xFFu << (8 * j))) | (uint32_t(sv[j]) << (8 * j));
+                    supports.push_back(packed);
+                    offsets.push_back(total);
+                    total += c;
+                    return;
+                }
+                for (int v = from; v < m_.n; ++v) {
+                    sv[d] = v;
+                    rec(v + 1, d + 1);
+                }
+            };
+            rec(0, 0);
+        }
+    }
+    support_off_ = offsets;
+    support_off_.push_back(total);
+
+    // ---- device model tables + K1 inputs: one host blob, one allocation, one copy
+    std::vector<unsigned char> blob;
+    auto put = [&](const void* p, size_t bytes) {
+        size_t at = (blob.size() + 15) & ~size_t{15};
+        blob.resize(at + std::max<size_t>(bytes, 1));
+        if (bytes) std::memcpy(blob.data() + at, p, bytes);
+        return at;
+    };
     dm_.n = m_.n;
     dm_.PP = m_.PP;
     dm_.n_sizes = static_cast<int>(m_.sizes.size());
     dm_.n_layouts = static_cast<int>(m_.layouts.size());
     dm_.max_mix = m_.max_mix;
+    size_t o_tmpl[kRowK + 1];
     for (int k = 0; k <= kRowK; ++k) {
         std::vector<uint64_t> t;
         for (const auto& tp : m_.templates[k]) {
@@ -198,58 +223,43 @@ Engine::Engine(const Rules& rules, std::map<std::string, ModelProfile> profiles,
             t.push_back(v);
         }
         dm_.n_tmpl[k] = static_cast<int>(t.size());
-        dm_.tmpl[k] = upload(dev_allocs_, t);
+        o_tmpl[k] = put(t.data(), t.size() * 8);
     }
-    dm_.U = upload(dev_allocs_, m_.U);
-    dm_.best_single = upload(dev_allocs_, m_.best_single);
-    dm_.feas_mask = upload(dev_allocs_, m_.feas_mask);
-    dm_.pat_mask = upload(dev_allocs_, m_.pat_mask);
     std::vector<uint8_t> pc(static_cast<size_t>(m_.PP) * 5, 0), lc(m_.layouts.size() * 5, 0);
     std::vector<int8_t> ls(m_.layouts.size() * 5 * 7, -1);
     for (int p = 0; p < m_.PP; ++p)
-        for (int s = 0; s < kMaxSizes; ++s) pc[p * 5 + s] = m_.patterns[p][s];
+        for (int q = 0; q < kMaxSizes; ++q) pc[p * 5 + q] = m_.patterns[p][q];
     for (size_t l = 0; l < m_.layouts.size(); ++l) {
-        for (int s = 0; s < kMaxSizes; ++s) lc[l * 5 + s] = m_.layouts[l].count[s];
+        for (int q = 0; q < kMaxSizes; ++q) lc[l * 5 + q] = m_.layouts[l].count[q];
         for (const auto& g : m_.layouts[l].groups)
             for (size_t t = 0; t < g.slots.size() && t < 7; ++t)
                 ls[(l * 5 + g.size_idx) * 7 + t] = static_cast<int8_t>(g.slots[t]);
     }
-    dm_.pat_count = upload(dev_allocs_, pc);
-    dm_.layout_count = upload(dev_allocs_, lc);
-    dm_.layout_slots = upload(dev_allocs_, ls);
-    dm_.sizes = upload(dev_allocs_, m_.sizes);
+    const size_t o_U = put(m_.U.data(), m_.U.size() * 8), o_best = put(m_.best_single.data(), m_.best_single.size() * 8),
+                 o_feas = put(m_.feas_mask.data(), m_.feas_mask.size()), o_pm = put(m_.pat_mask.data(), m_.pat_mask.size()),
+                 o_pc = put(pc.data(), pc.size()), o_lc = put(lc.data(), lc.size()), o_ls = put(ls.data(), ls.size()),
+                 o_sz = put(m_.sizes.data(), m_.sizes.size() * 4), o_sup = put(supports.data(), supports.size() * 4),
+                 o_off = put(offsets.data(), offsets.size() * 8);
+    const size_t o_base = (blob.size() + 15) & ~size_t{15};
+    unsigned char* d = dalloc<unsigned char>(dev_allocs_, o_base + (static_cast<size_t>(total) + 2) * 8);
+    CK(cudaMemcpy(d, blob.data(), blob.size(), cudaMemcpyHostToDevice));
+    stats.h2d += static_cast<long long>(blob.size());
+    for (int k = 0; k <= kRowK; ++k) dm_.tmpl[k] = reinterpret_cast<const uint64_t*>(d + o_tmpl[k]);
+    dm_.U = reinterpret_cast<const double*>(d + o_U);
+    dm_.best_single = reinterpret_cast<const double*>(d + o_best);
+    dm_.feas_mask = d + o_feas;
+    dm_.pat_mask = d + o_pm;
+    dm_.pat_count = d + o_pc;
+    dm_.layout_count = d + o_lc;
+    dm_.layout_slots = reinterpret_cast<const int8_t*>(d + o_ls);
+    dm_.sizes = reinterpret_cast<const int*>(d + o_sz);
+    d_base_ = reinterpret_cast<uint64_t*>(d + o_base);
+    const auto t2 = clk::now();
 
-    // ---- K1: base pool (all supports with 1..max_mix members), deterministic order
-    std::vector<uint32_t> supports;
-    std::vector<long long> offsets;
-    long long total = 0;
-    std::vector<int> s(kRowK);
-    for (int k = 1; k <= max_mix; ++k) {
-        std::function<void(int, int)> rec = [&](int from, int d) {
-            if (d == k) {
-                long long c = m_.rows_for_support(s.data(), k);
-                if (c == 0) return;
-                uint32_t packed = 0xFFFFFFFFu;
-                for (int j = 0; j < k; ++j) packed = (packed & ~(0xFFu << (8 * j))) | (uint32_t(s[j]) << (8 * j));
-                supports.push_back(packed);
-                offsets.push_back(total);
-                total += c;
-                return;
-            }
-            for (int v = from; v < m_.n; ++v) {
-                s[d] = v;
-                rec(v + 1, d + 1);
-            }
-        };
-        rec(0, 0);
-    }
-    d_base_ = dalloc<uint64_t>(dev_allocs_, static_cast<size_t>(total) + 2);
+    // ---- K1: base pool rows, deterministic (support, template) order
     if (!supports.empty()) {
-        uint32_t* d_sup = dalloc<uint32_t>(dev_allocs_, supports.size());
-        long long* d_off = dalloc<long long>(dev_allocs_, offsets.size());
-        CK(cudaMemcpy(d_sup, supports.data(), supports.size() * 4, cudaMemcpyHostToDevice));
-        CK(cudaMemcpy(d_off, offsets.data(), offsets.size() * 8, cudaMemcpyHostToDevice));
-        stats.h2d += static_cast<long long>(supports.size() * 4 + offsets.size() * 8);
+        const uint32_t* d_sup = reinterpret_cast<const uint32_t*>(d + o_sup);
+        const long long* d_off = reinterpret_cast<const long long*>(d + o_off);
         int n_sup = static_cast<int>(supports.size());
         int threads = 256;
         int blocks = static_cast<int>((static_cast<long long>(n_sup) * 32 + threads - 1) / threads);
@@ -257,14 +267,16 @@ Engine::Engine(const Rules& rules, std::map<std::string, ModelProfile> profiles,
         CK(cudaLaunchKernel(enum_base_kernel_ptr(), blocks, threads, args, 0, nullptr));
         stats.launches++;
         CK(cudaGetLastError());
-        CK(cudaDeviceSynchronize());
     }
     base_rows_.resize(static_cast<size_t>(total));
     if (total) CK(cudaMemcpy(base_rows_.data(), d_base_, total * 8, cudaMemcpyDeviceToHost));
     stats.d2h += total * 8;
-    g_h2d = nullptr;
-    row_index_.reserve(base_rows_.size() * 2);
-    for (size_t i = 0; i < base_rows_.size(); ++i) row_index_.emplace(base_rows_[i], static_cast<long long>(i));
+    const auto t3 = clk::now();
+    if (std::getenv("MIGPLAN_CTX_TIMERS")) {
+        auto us = [](auto a, auto b) { return std::chrono::duration<double, std::micro>(b - a).count(); };
+        std::fprintf(stderr, "[migplan ctx] n=%d model %.0f us, device info %.0f us, tables %.0f us, K1+base %.0f us\n",
+                     m_.n, us(tb, t0), us(t0, t1), us(t1, t2), us(t2, t3));
+    }
 
     min_u_.assign(m_.n, 0.0);
     for (int i = 0; i < m_.n; ++i) {
@@ -283,10 +295,15 @@ Engine::Engine(const Rules& rules, std::map<std::string, ModelProfile> profiles,
 
 Engine::~Engine() {
     cudaSetDevice(device_);
+    if (d_shard_) cudaFree(d_shard_);
     for (void* p : dev_allocs_) cudaFree(p);
 }
 
 long long Engine::index_of(uint64_t row) const {
+    std::call_once(row_index_once_, [this] {  // built on first use: not on the context-creation path
+        row_index_.reserve(base_rows_.size() * 2);
+        for (size_t i = 0; i < base_rows_.size(); ++i) row_index_.emplace(base_rows_[i], static_cast<long long>(i));
+    });
     auto it = row_index_.find(row);
     if (it == row_index_.end()) throw ArgumentError("row not in the base pool");
     return it->second;
@@ -296,6 +313,36 @@ Config Engine::config_of(uint64_t row) const {
     Config c;
     c.n = m_.decode(row, c.inst);
     return c;
+}
+
+const DeviceInfo& device_info(int device) {
+    static std::mutex mu;
+    static std::map<int, DeviceInfo> cache;  // one entry per device for the process lifetime
+    std::lock_guard<std::mutex> g(mu);
+    auto it = cache.find(device);
+    if (it != cache.end()) {
+        CK(cudaSetDevice(device));
+        return it->second;
+    }
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+        throw DeviceError("no CUDA device available: the B200 planner has no CPU fallback");
+    if (device < 0 || device >= ndev) throw DeviceError("CUDA device index out of range");
+    CK(cudaSetDevice(device));
+    cudaDeviceProp prop{};
+    CK(cudaGetDeviceProperties(&prop, device));
+    if (prop.major < 10) throw DeviceError(std::string("device ") + prop.name + " is not sm_100-class (B200)");
+    DeviceInfo info;
+    info.num_sms = prop.multiProcessorCount;
+    info.smem_optin = static_cast<long long>(prop.sharedMemPerBlockOptin);
+    // every kernel may use all the opt-in shared memory its static allocation leaves
+    for (const void* k : {greedy_kernel_ptr(), topk_kernel_ptr(), topk1_kernel_ptr(32), rollout_kernel_ptr()}) {
+        cudaFuncAttributes fa{};
+        CK(cudaFuncGetAttributes(&fa, k));
+        CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                static_cast<int>(prop.sharedMemPerBlockOptin - fa.sharedSizeBytes)));
+    }
+    return cache.emplace(device, info).first->second;
 }
 
 namespace {
@@ -398,7 +445,8 @@ void Engine::fast_algo(const std::vector<double>& comp, std::vector<uint64_t>& r
         CK(cudaMalloc(&s->d_pick_rows, sizeof(long long) * cap_steps));
         s->cap_steps = static_cast<int>(cap_steps);
     }
-    const long long n_base = static_cast<long long>(base_rows_.size());
+    const long long n_base = n_ranks_ > 1 ? n_shard_ : static_cast<long long>(base_rows_.size());
+    const uint64_t* base_src = n_ranks_ > 1 ? d_shard_ : d_base_;
     // Arena = base + the all-feasible extension bound (every support with max_mix < |S| <= 4),
     // capped at 3G rows (24 GB); the kernel reports overflow and the call is retried larger.
     ensure_ext(s, n_base + std::min<long long>(ext_bound_, 3ll << 30));
@@ -406,13 +454,14 @@ void Engine::fast_algo(const std::vector<double>& comp, std::vector<uint64_t>& r
     const int T = kernel_threads();
     const size_t smem = greedy_smem_bytes(m_.n, m_.PP, cache_units_);
     int G = num_sms_ * greedy_blocks_per_sm_;
+    if (max_ctas_ > 0) G = std::min(G, max_ctas_);
     if (const char* e = std::getenv("MIGPLAN_GREEDY_CTAS")) G = std::max(1, std::min(G, std::atoi(e)));
 
     for (int attempt = 0;; ++attempt) {
         std::memcpy(s->io->comp, comp.data(), sizeof(double) * m_.n);
         CK(cudaMemsetAsync(s->st, 0, sizeof(GreedyState), s->stream));
         // the working-set arena starts as a copy of the resident base pool (device to device)
-        if (n_base) CK(cudaMemcpyAsync(s->ext, d_base_, n_base * 8, cudaMemcpyDeviceToDevice, s->stream));
+        if (n_base) CK(cudaMemcpyAsync(s->ext, base_src, n_base * 8, cudaMemcpyDeviceToDevice, s->stream));
         GreedyArgs a{};
         a.M = dm_;
         a.rows = s->ext;
@@ -420,6 +469,10 @@ void Engine::fast_algo(const std::vector<double>& comp, std::vector<uint64_t>& r
         a.cap = s->ext_cap;
         a.cache_units = cache_units_;
         a.phase_timers = std::getenv("MIGPLAN_PHASE_TIMERS") ? 1 : 0;
+        a.prefetch = 4;
+        if (const char* e = std::getenv("MIGPLAN_PREFETCH")) a.prefetch = std::atoi(e);
+        a.load_mode = 0;
+        if (const char* e = std::getenv("MIGPLAN_LOAD_MODE")) a.load_mode = std::atoi(e);
         a.comp0 = s->io->comp;
         a.st = s->st;
         a.out = &s->io->res;
@@ -432,6 +485,12 @@ void Engine::fast_algo(const std::vector<double>& comp, std::vector<uint64_t>& r
         a.host_pick_rows = s->pick_rows;
         a.ev_svc = s->ev_svc;
         a.cap_steps = s->cap_steps;
+        a.n_ranks = n_ranks_;
+        a.rank = rank_;
+        for (int q = 0; q < n_ranks_ && n_ranks_ > 1; ++q) a.boards[q] = static_cast<ExchSlot*>(boards_[q]);
+        a.exch_seq0 = exch_seq_;
+        a.exch_timeout_ns = 10'000'000'000ll;
+        if (const char* e = std::getenv("MIGPLAN_EXCH_TIMEOUT_MS")) a.exch_timeout_ns = std::atoll(e) * 1'000'000ll;
         void* args[] = {&a};
         CK(cudaEventRecord(s->e0, s->stream));
         CK(cudaLaunchCooperativeKernel(greedy_kernel_ptr(), G, T, args, smem, s->stream));
@@ -441,6 +500,14 @@ void Engine::fast_algo(const std::vector<double>& comp, std::vector<uint64_t>& r
         float ms = 0.f;
         CK(cudaEventElapsedTime(&ms, s->e0, s->e1));
         const GreedyState h = s->io->res;
+        if (n_ranks_ > 1) {
+            if (h.status == kExtOverflow || h.status == kExchTimeout) {
+                n_ranks_ = 1;  // the ranks' exchange sequences diverged: the shard must be set again
+                throw DeviceError(h.status == kExchTimeout ? "sharded greedy: exchange with a peer rank timed out"
+                                                           : "sharded greedy: extension arena overflow");
+            }
+            exch_seq_ = h.last_seq;
+        }
         if (h.status == kExtOverflow && attempt < 4) {
             long long need = n_base + static_cast<long long>(h.ext_count) * 4 + (1 << 20);
             ensure_ext(s, std::max(need, s->ext_cap * 2));
@@ -492,7 +559,8 @@ std::vector<long long> Engine::topk(const std::vector<double>& comp, int k, cons
         CK(cudaMemcpyAsync(s->index, index->data(), sizeof(long long) * total, cudaMemcpyHostToDevice, s->stream));
     }
     CK(cudaEventRecord(s->e0, s->stream));
-    const long long per = topk1_rows_per_cta();
+    long long per = topk1_rows_per_cta();
+    if (const char* e = std::getenv("MIGPLAN_TOPK_ROWS_PER_CTA")) per = std::max(1024ll, std::atoll(e));
     const long long g1 = (total + per - 1) / per;
     bool single = k <= 32 && g1 <= topk1_max_ctas();
     if (single) {  // one launch: per-CTA threshold + parallel rank, last-CTA merge (topk.cu)
@@ -502,9 +570,11 @@ std::vector<long long> Engine::topk(const std::vector<double>& comp, int k, cons
         a.n_rows = pool_size();
         a.index = index ? s->index : nullptr;
         a.n_index = index ? total : 0;
-        a.svc_mask = svc_mask ? s->io->mask : nullptr;
-        a.comp = s->io->comp;
+        a.use_mask = svc_mask ? 1 : 0;
+        if (svc_mask) std::memcpy(a.svc_mask, svc_mask->data(), sizeof(uint64_t) * 4);
+        std::memcpy(a.comp, comp.data(), sizeof(double) * m_.n);
         a.k = k;
+        a.rows_per_cta = per;
         a.partials = s->tpart;
         a.ticket = s->ticket;
         a.out_row = s->io->top_rows;
@@ -514,6 +584,7 @@ std::vector<long long> Engine::topk(const std::vector<double>& comp, int k, cons
         CK(cudaLaunchKernel(topk1_kernel_ptr(32), G, topk1_threads(), args, topk1_smem_bytes(m_.n, m_.PP, 32),
                             s->stream));
         stats.launches++;
+        CK(cudaEventRecord(s->e1, s->stream));
         CK(cudaStreamSynchronize(s->stream));
         // *n_out == -1: a CTA's rows tied at its threshold beyond the candidate capacity;
         // the exact k-round kernel below answers instead.
@@ -540,9 +611,9 @@ std::vector<long long> Engine::topk(const std::vector<double>& comp, int k, cons
         void* args[] = {&a};
         CK(cudaLaunchCooperativeKernel(topk_kernel_ptr(), G, T, args, topk_smem_bytes(m_.n, m_.PP), s->stream));
         stats.launches++;
+        CK(cudaEventRecord(s->e1, s->stream));
+        CK(cudaStreamSynchronize(s->stream));
     }
-    CK(cudaEventRecord(s->e1, s->stream));
-    CK(cudaStreamSynchronize(s->stream));
     const int got = s->io->top_n;
     float ms = 0.f;
     CK(cudaEventElapsedTime(&ms, s->e0, s->e1));
@@ -613,7 +684,7 @@ RolloutResult Engine::rollouts(const std::vector<double>& comp, long long n_roll
     a.M = dm_;
     a.base = d_base_;
     a.n_base = pool_size();
-    a.comp0 = ho->comp;
+    std::memcpy(a.comp0, comp.data(), sizeof(double) * n);
     a.seed = seed;
     a.k = k;
     a.max_depth = max_depth;
@@ -726,6 +797,69 @@ RolloutResult Engine::rollouts(const std::vector<double>& comp, long long n_roll
     stats.d2h += static_cast<long long>(sizeof(RolloutCounters) + sizeof(long long) * res.path.size() +
                                         (lengths ? sizeof(int) * n_roll : 0));
     return res;
+}
+
+void Engine::set_shard(int rank, int n_ranks, const std::vector<void*>& boards, int max_ctas) {
+    if (n_ranks < 1 || n_ranks > kMaxRanks || rank < 0 || rank >= n_ranks)
+        throw ArgumentError("set_shard: rank/n_ranks out of range (1..8 ranks)");
+    if (n_ranks > 1 && static_cast<int>(boards.size()) != n_ranks) throw ArgumentError("set_shard: one board per rank");
+    CK(cudaSetDevice(device_));
+    if (d_shard_) {
+        CK(cudaFree(d_shard_));
+        d_shard_ = nullptr;
+    }
+    n_shard_ = 0;
+    max_ctas_ = max_ctas;
+    rank_ = rank;
+    n_ranks_ = 1;
+    boards_.clear();
+    if (n_ranks == 1) return;
+    // base rows of the supports with index == rank (mod n_ranks), in pool order
+    std::vector<uint64_t> mine;
+    for (size_t i = 0; i + 1 < support_off_.size(); ++i)
+        if (static_cast<int>(i % n_ranks) == rank)
+            mine.insert(mine.end(), base_rows_.begin() + support_off_[i], base_rows_.begin() + support_off_[i + 1]);
+    CK(cudaMalloc(&d_shard_, std::max<size_t>(mine.size(), 1) * 8 + 16));
+    if (!mine.empty()) CK(cudaMemcpy(d_shard_, mine.data(), mine.size() * 8, cudaMemcpyHostToDevice));
+    stats.h2d += static_cast<long long>(mine.size() * 8);
+    n_shard_ = static_cast<long long>(mine.size());
+    // the own board starts empty (every rank zeroes its own before the group's first call)
+    CK(cudaMemset(boards[rank], 0, board_bytes(n_ranks)));
+    CK(cudaDeviceSynchronize());
+    boards_ = boards;
+    n_ranks_ = n_ranks;
+    exch_seq_ = 0;
+}
+
+size_t board_bytes(int n_ranks) { return sizeof(ExchSlot) * 2 * static_cast<size_t>(std::max(n_ranks, 1)); }
+
+void* board_alloc(int device, int n_ranks, unsigned char ipc_handle[64]) {
+    CK(cudaSetDevice(device));
+    void* p = nullptr;
+    CK(cudaMalloc(&p, std::max<size_t>(board_bytes(n_ranks), 256)));
+    CK(cudaMemset(p, 0, board_bytes(n_ranks)));
+    if (ipc_handle) {
+        cudaIpcMemHandle_t h;
+        static_assert(sizeof(h) == 64, "cudaIpcMemHandle_t is 64 bytes");
+        CK(cudaIpcGetMemHandle(&h, p));
+        std::memcpy(ipc_handle, &h, 64);
+    }
+    return p;
+}
+
+void* board_open(int device, const unsigned char ipc_handle[64]) {
+    CK(cudaSetDevice(device));
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, ipc_handle, 64);
+    void* p = nullptr;
+    CK(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
+    return p;
+}
+
+void board_close(void* board, bool opened) {
+    if (!board) return;
+    if (opened) cudaIpcCloseMemHandle(board);
+    else cudaFree(board);
 }
 
 // completion_of / detail::sum_rates (core.hpp:245-269): counts keyed by (svc, size, batch)

@@ -26,9 +26,21 @@ struct Config {  // normalized GpuConfig with service indices (mig_config)
 };
 
 bool config_less(const Config& a, const Config& b);
+
+// Exchange boards of the sharded greedy (device memory, IPC-shareable across processes).
+size_t board_bytes(int n_ranks);
+void* board_alloc(int device, int n_ranks, unsigned char ipc_handle[64]);
+void* board_open(int device, const unsigned char ipc_handle[64]);
+void board_close(void* board, bool opened);
 bool config_equal(const Config& a, const Config& b);
 
 struct Slot;
+
+struct DeviceInfo {
+    int num_sms = 0;
+    long long smem_optin = 0;
+};
+const DeviceInfo& device_info(int device);
 
 struct Stats {
     std::atomic<long long> greedy_rows{0}, topk_rows{0}, greedy_calls{0}, topk_calls{0}, greedy_steps{0};
@@ -78,6 +90,14 @@ class Engine {
     RolloutResult rollouts(const std::vector<double>& comp, long long n_roll, int k, int max_depth, uint64_t seed,
                            long long id_offset, long long batch, int table_log2, int* lengths);
 
+    // Sharded greedy: from now on fast_algo scans only this rank's 1/n_ranks of
+    // every working set and exchanges per-step winners through the boards (every rank's
+    // board, device pointers valid on this device: peer memory or local).  All ranks must
+    // call fast_algo with identical inputs (SPMD); their plans are identical.
+    // max_ctas > 0 caps this context's greedy grid (ranks sharing one GPU).
+    void set_shard(int rank, int n_ranks, const std::vector<void*>& boards, int max_ctas);
+    int n_ranks() const { return n_ranks_; }
+
     // completion_of (core.hpp:291-302), count-based, on the host (control logic, not hot).
     std::vector<double> completion_of(const std::vector<Config>& cfgs) const;
     const std::map<std::string, ModelProfile>& profiles() const { return profiles_; }
@@ -102,10 +122,17 @@ class Engine {
     std::vector<void*> dev_allocs_;
     uint64_t* d_base_ = nullptr;
     std::vector<uint64_t> base_rows_;
-    std::unordered_map<uint64_t, long long> row_index_;
+    mutable std::unordered_map<uint64_t, long long> row_index_;
+    mutable std::once_flag row_index_once_;
     std::vector<double> min_u_;  // smallest positive utility per service (step bound)
     long long ext_bound_ = 0;
     int cache_units_ = 0;  // greedy shared-memory row cache per CTA (16-byte units)
+    std::vector<long long> support_off_;  // base pool: row offset of every support (K1 order) + total
+    int rank_ = 0, n_ranks_ = 1, max_ctas_ = 0;
+    std::vector<void*> boards_;
+    uint64_t* d_shard_ = nullptr;  // this rank's base rows (sharded greedy)
+    long long n_shard_ = 0;
+    unsigned long long exch_seq_ = 0;
 
 };
 

@@ -24,6 +24,22 @@ namespace {
 
 constexpr int kThreads = 512;
 constexpr int kWarps = kThreads / 32;
+// Streaming-row loads.  Rows are append-only and every row a step reads was completed
+// before a grid barrier, so any load that bypasses L1 (L2 is the coherence point) is exact.
+//   0: ld.global.cg (L2 only)   1: ld.global.nc.L1::no_allocate   2: ld.global.cs (evict-first)
+__device__ __forceinline__ uint4 ld_row4(const uint4* p, int mode) {
+    uint4 v;
+    if (mode == 1) {
+        asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+                     : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                     : "l"(p));
+    } else if (mode == 2) {
+        asm volatile("ld.global.cs.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p));
+    } else {
+        v = __ldcg(p);
+    }
+    return v;
+}
 
 // Block-wide argmax; result valid in every thread.
 __device__ Best block_best(const DevModel& M, Best b, Best* red) {
@@ -65,8 +81,45 @@ __device__ Best grid_best(const DevModel& M, const Best* partials, int G, Best* 
 // record, then releases the generation.  Only one CTA reads the partials (instead of all G
 // CTAs reading all G records — a G^2 hot-line read storm in L2), and waiters read one
 // 24-byte record.  Returns the same winner in every thread of every CTA.
+// Cross-rank step of the sharded greedy, run by one thread of the last CTA:
+// post this rank's winner into slot [parity][rank] of EVERY rank's exchange board (peer
+// memory over NVLink, or plain device memory for ranks sharing a GPU), then wait until all
+// n_ranks records of this step are in the own board and reduce them in the same total
+// order.  Every rank computes the same global winner.  Double-buffering by step parity is
+// enough: a rank posts step t+1 only after it read all records of step t.  A watchdog turns
+// a missing peer into kExchTimeout instead of a hang.
+__device__ Best exchange_best(const DevModel& M, const GreedyArgs& a, Best x, unsigned long long seq, int& status) {
+    const int P = a.n_ranks;
+    const int par = static_cast<int>(seq & 1ull);
+    for (int q = 0; q < P; ++q) {
+        ExchSlot* d = a.boards[q] + par * P + a.rank;
+        d->s = x.s;
+        d->u = x.u;
+        d->row = x.row;
+        cuda::atomic_ref<unsigned long long, cuda::thread_scope_system> f(d->seq);
+        f.store(seq, cuda::memory_order_release);
+    }
+    ExchSlot* mine = a.boards[a.rank] + par * P;
+    const unsigned long long t0 = globaltimer();
+    Best g = none();
+    for (int q = 0; q < P; ++q) {
+        cuda::atomic_ref<unsigned long long, cuda::thread_scope_system> f(mine[q].seq);
+        while (f.load(cuda::memory_order_acquire) < seq) {
+            if (globaltimer() - t0 > static_cast<unsigned long long>(a.exch_timeout_ns)) {
+                status = kExchTimeout;
+                return none();
+            }
+        }
+        const Best p{*reinterpret_cast<volatile double*>(&mine[q].s), *reinterpret_cast<volatile double*>(&mine[q].u),
+                     *reinterpret_cast<volatile unsigned long long*>(&mine[q].row)};
+        if (better(M, p, g)) g = p;
+    }
+    return g;
+}
+
 __device__ Best grid_argmax(const DevModel& M, const Best& mine, Best* partials, Best* winrec, unsigned* count,
-                            unsigned* gen, int G, Best* red) {
+                            unsigned* gen, int G, Best* red, const GreedyArgs& a, unsigned long long seq,
+                            int* xstatus) {
     __shared__ int s_last;
     __shared__ unsigned s_gen;
     if (threadIdx.x == 0) {
@@ -91,6 +144,11 @@ __device__ Best grid_argmax(const DevModel& M, const Best& mine, Best* partials,
             }
             x = warp_best(M, x);
             if (lane_id() == 0) {
+                if (a.n_ranks > 1) {
+                    int st = kOk;
+                    x = exchange_best(M, a, x, seq, st);
+                    if (st != kOk) atomicExch(xstatus, st);
+                }
                 red[0] = x;
                 __stcg(&winrec->s, x.s);
                 __stcg(&winrec->u, x.u);
@@ -112,10 +170,9 @@ __device__ Best grid_argmax(const DevModel& M, const Best& mine, Best* partials,
     return r;
 }
 
-// The thread's running argmax; the slow path runs only when s >= its best score.
-__device__ __forceinline__ void consider(const DevModel& M, const double* __restrict__ W, const double* U,
-                                         uint64_t row, Best& best) {
-    const double s = row_score(W, row);
+// The thread's running argmax over one scored row (s = row_score): the 3-key order of
+// candidate_preferred (greedy.hpp:63-67); util_sum and the config key only on ties.
+__device__ __forceinline__ void take(const DevModel& M, const double* U, uint64_t row, double s, Best& best) {
     if (s > 0.0 && s >= best.s) {
         if (s > best.s) {
             best = Best{s, row_usum(U, row), row};
@@ -123,6 +180,36 @@ __device__ __forceinline__ void consider(const DevModel& M, const double* __rest
         }
         const double u = row_usum(U, row);
         if (u > best.u || (u == best.u && row != best.row && row_key_less(M, row, best.row))) best = Best{s, u, row};
+    }
+}
+
+__device__ __forceinline__ void consider(const DevModel& M, const double* __restrict__ W, const double* U,
+                                         uint64_t row, Best& best) {
+    take(M, U, row, row_score(W, row), best);
+}
+
+// Eight rows (four 16-byte units) at once: all 32 table gathers and 24 adds are issued
+// without a branch in between (instruction-level parallelism across rows); the per-row
+// preference logic runs only if some row reaches the thread's best score — rare once the
+// running best is established.  `floor` = the thread's best score, or the smallest
+// positive double while it has none (rows must score > 0, greedy.hpp:130).
+__device__ __forceinline__ void consider8(const DevModel& M, const double* __restrict__ W, const double* U,
+                                          const uint4& v0, const uint4& v1, const uint4& v2, const uint4& v3,
+                                          Best& best) {
+    const uint64_t r[8] = {(static_cast<uint64_t>(v0.y) << 32) | v0.x, (static_cast<uint64_t>(v0.w) << 32) | v0.z,
+                           (static_cast<uint64_t>(v1.y) << 32) | v1.x, (static_cast<uint64_t>(v1.w) << 32) | v1.z,
+                           (static_cast<uint64_t>(v2.y) << 32) | v2.x, (static_cast<uint64_t>(v2.w) << 32) | v2.z,
+                           (static_cast<uint64_t>(v3.y) << 32) | v3.x, (static_cast<uint64_t>(v3.w) << 32) | v3.z};
+    double sc[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) sc[j] = row_score(W, r[j]);
+    const double floor = best.s > 0.0 ? best.s : 4.9406564584124654e-324;
+    bool hit = false;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) hit |= sc[j] >= floor;
+    if (hit) {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) take(M, U, r[j], sc[j], best);
     }
 }
 
@@ -352,6 +439,8 @@ __global__ void __launch_bounds__(kThreads, 1) greedy_kernel(const __grid_consta
                     const int nt = M.n_tmpl[k];
                     const long long r = rem / nt;
                     const int t = static_cast<int>(rem - r * nt);
+                    // sharded greedy: support (event e, size k, rank r) lives on one rank only
+                    if (a.n_ranks > 1 && (r * 4 + k + e) % a.n_ranks != a.rank) ok = false;
                     int idx[3];
                     unrank(r, k - 1, m, idx);
                     int S[4];
@@ -429,6 +518,7 @@ __global__ void __launch_bounds__(kThreads, 1) greedy_kernel(const __grid_consta
     int cj = 0;                                                  // units of mine cached so far
 
     int step = 0;
+    unsigned long long last_seq = a.exch_seq0;
     long long rows_total = 0;
     const bool timer = a.phase_timers && blockIdx.x == 0 && threadIdx.x == 0;
     unsigned long long ph[5] = {0, 0, 0, 0, 0};
@@ -463,31 +553,37 @@ __global__ void __launch_bounds__(kThreads, 1) greedy_kernel(const __grid_consta
                 const uint4 v1 = cache[(j + 1) * blockDim.x + threadIdx.x];
                 const uint4 v2 = cache[(j + 2) * blockDim.x + threadIdx.x];
                 const uint4 v3 = cache[(j + 3) * blockDim.x + threadIdx.x];
-                consider2(M, W, U, v0, best);
-                consider2(M, W, U, v1, best);
-                consider2(M, W, U, v2, best);
-                consider2(M, W, U, v3, best);
+                consider8(M, W, U, v0, v1, v2, v3, best);
             }
             for (; j < cj; ++j) consider2(M, W, U, cache[j * blockDim.x + threadIdx.x], best);
             long long u = my0 + static_cast<long long>(cj) * GT;
             for (; u + 3 * GT < NU; u += 4 * GT) {
+                // Bulk L2 prefetch, a.prefetch iterations ahead: one thread per CTA pulls the
+                // CTA's next 8 KB stripes (contiguous: unit index = cta * blockDim + thread) into
+                // L2, so the loads below hit L2 instead of waiting on HBM latency.
+                if (threadIdx.x < 4 && a.prefetch > 0) {
+                    const long long pu = u - threadIdx.x + (a.prefetch * 4 + threadIdx.x) * GT;
+                    if (pu + static_cast<long long>(blockDim.x) <= NU)
+                        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(rows4 + pu),
+                                     "r"(static_cast<unsigned>(blockDim.x * 16))
+                                     : "memory");
+                }
                 // rows appended during this launch: L2-coherent loads (never the non-coherent path)
-                const uint4 v0 = __ldcg(rows4 + u), v1 = __ldcg(rows4 + u + GT), v2 = __ldcg(rows4 + u + 2 * GT),
-                            v3 = __ldcg(rows4 + u + 3 * GT);
-                consider2(M, W, U, v0, best);
-                consider2(M, W, U, v1, best);
-                consider2(M, W, U, v2, best);
-                consider2(M, W, U, v3, best);
+                const uint4 v0 = ld_row4(rows4 + u, a.load_mode), v1 = ld_row4(rows4 + u + GT, a.load_mode),
+                            v2 = ld_row4(rows4 + u + 2 * GT, a.load_mode), v3 = ld_row4(rows4 + u + 3 * GT, a.load_mode);
+                consider8(M, W, U, v0, v1, v2, v3, best);
             }
             for (; u < NU; u += GT) consider2(M, W, U, __ldcg(rows4 + u), best);
             if ((N & 1) && my0 == 0) consider(M, W, U, __ldcg(a.rows + N - 1), best);
         }
         best = block_best(M, best, red);
         mark(0);
-        const Best win = grid_argmax(M, best, a.partials, a.partials + G, bc, bg, G, red);
+        last_seq = a.exch_seq0 + static_cast<unsigned long long>(step) + 1ull;
+        const Best win = grid_argmax(M, best, a.partials, a.partials + G, bc, bg, G, red, a, last_seq, &a.st->status);
         mark(1);
         if (win.row == kNoRow) {
-            status = kNoPositive;
+            const int xs = *reinterpret_cast<volatile int*>(&a.st->status);
+            status = xs != kOk ? xs : kNoPositive;
             break;
         }
         rows_total += N;
@@ -530,6 +626,7 @@ __global__ void __launch_bounds__(kThreads, 1) greedy_kernel(const __grid_consta
         GreedyState* o = a.out;  // host-mapped: the host reads it after one stream sync
         for (int k = 0; k < 5; ++k) o->phase_ns[k] = ph[k];
         o->n_steps = step;
+        o->last_seq = last_seq;
         o->n_events = s_events;
         o->rows_scored = rows_total;
         o->ext_count = *reinterpret_cast<volatile unsigned long long*>(&a.st->ext_count);

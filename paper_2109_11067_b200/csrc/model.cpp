@@ -240,6 +240,14 @@ Model build_model(const Rules& rules, const std::map<std::string, ModelProfile>&
             for (int j = 0; j < k; ++j) t.pat[j] = static_cast<uint8_t>(pat_id.at(pats[j]));
             m.templates[k].push_back(t);
         }
+    // Template order fixes the arena order inside a support block (K1/K2 emit rows
+    // template-major).  Sorting by (p0, p1, p2, p3) makes the rows a warp scans together share
+    // their leading members' patterns, so the W-table gathers of those members mostly hit
+    // one shared-memory address (broadcast) instead of conflicting banks.  The optimizer's
+    // results do not depend on row order (the preference order is total, greedy.hpp:63-67).
+    for (int k = 1; k <= kRowK; ++k)
+        std::stable_sort(m.templates[k].begin(), m.templates[k].end(),
+                         [](const Template& a, const Template& b) { return a.pat < b.pat; });
 
     // feasibility_table (config_enum.hpp:73-84) via select_entry (core.hpp:122-138).
     m.feas.assign(m.n, std::vector<Feasible>(m.sizes.size()));

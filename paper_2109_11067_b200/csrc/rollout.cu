@@ -226,6 +226,7 @@ __global__ void __launch_bounds__(kRThreads, 1) rollout_kernel(const __grid_cons
 #pragma unroll
         for (int j = 0; j < kMaxJ; ++j) c[j] = (lane + 32 * j < n) ? src[lane + 32 * j] : 2.0;
         int L = first ? 0 : a.len[r];
+        if (first && lane == 0) a.len[r] = 0;
         if (!first) {
             const unsigned slot = a.rslot[r];
             const int pn = __ldcg(&a.pool_n[slot]);

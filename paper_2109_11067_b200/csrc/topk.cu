@@ -3,11 +3,12 @@
 // The reference scores every candidate, keeps s > 0, sorts by candidate_preferred
 // (greedy.hpp:63-67) and truncates to K.  That order is total, so only the few rows that
 // can reach the top K need to be ordered at all:
-//   1. every thread scores its <= 16 rows of the CTA's chunk into registers;
+//   1. every thread scores its rows of the CTA's chunk and keeps its maximum;
 //   2. every warp sorts its 32 per-lane maxima (bitonic, shuffles only) and takes the K-th
 //      largest; the CTA threshold T is the largest such value over the warps — at least K
 //      rows of the CTA score >= T, so the CTA's exact top-K lies among its rows >= T;
-//   3. those few rows go to shared memory and are ranked IN PARALLEL (thread i counts the
+//   3. a second pass over the (cache-hot) chunk sends those few rows to shared memory,
+//      where they are ranked IN PARALLEL (thread i counts the
 //      candidates preferred to candidate i): no serial insertion, no block-wide sort;
 //   4. with more than one CTA, the last CTA to finish (atomic ticket) ranks the G x K
 //      per-CTA winners the same way.
@@ -23,7 +24,6 @@ namespace {
 
 constexpr int kTopkThreads = 512;
 constexpr int kTopkWarps = kTopkThreads / 32;
-constexpr int kRowsPerThread = 16;  // the host sizes the grid so every row has a register slot
 constexpr int kCandCap = 2048;      // per-CTA candidates (and merged per-CTA winners) in smem
 constexpr int kTopkMaxK = 32;
 
@@ -38,66 +38,50 @@ __global__ void __launch_bounds__(kTopkThreads, 1) topk1_kernel(const __grid_con
     const DevModel& M = a.M;
     const int nW = (M.n + 1) * M.PP;
     double* W = reinterpret_cast<double*>(smem);
-    double* comp = W + nW;
-    Cand* cand = reinterpret_cast<Cand*>(comp + M.n + 1);  // [kCandCap]
-    Cand* win = cand + kCandCap;                           // [kTopkMaxK]
+    Cand* cand = reinterpret_cast<Cand*>(W + nW + 1);  // [kCandCap]
+    Cand* win = cand + kCandCap;                        // [kTopkMaxK]
     __shared__ unsigned long long t_bits;
     __shared__ int n_cand;
-    __shared__ uint64_t mask[4];
     __shared__ bool last;
     const int k = a.k;
-    for (int i = threadIdx.x; i < M.n; i += blockDim.x) comp[i] = a.comp[i];
-    if (threadIdx.x < 4) mask[threadIdx.x] = a.svc_mask ? a.svc_mask[threadIdx.x] : ~0ull;
     if (threadIdx.x == 0) {
         t_bits = 0ull;
         n_cand = 0;
     }
-    __syncthreads();
     for (int e = threadIdx.x; e < nW; e += blockDim.x) {  // W = need * U (greedy.hpp:38-41)
         const int svc = e / M.PP;
         double w = 0.0;
         if (svc < M.n) {
-            const double need = __dadd_rn(1.0, -comp[svc]);
+            const double need = __dadd_rn(1.0, -a.comp[svc]);
             if (need > 0.0) w = __dmul_rn(need, __ldg(&M.U[e]));
         }
         W[e] = w;
     }
     __syncthreads();
 
-    // 1. score this CTA's chunk into registers (coalesced: consecutive threads, consecutive rows)
+    // 1. this CTA's chunk (coalesced: consecutive threads, consecutive rows); a compact loop,
+    //    so the launch does not stream a large unrolled body through the instruction cache
     const long long total = a.index ? a.n_index : a.n_rows;
-    const long long chunk = (total + gridDim.x - 1) / gridDim.x;
-    const long long lo = static_cast<long long>(blockIdx.x) * chunk;
-    const long long hi = min(total, lo + chunk);
-    uint64_t myrow[kRowsPerThread];
-    double mys[kRowsPerThread];
-    double tmax = 0.0;
+    const long long lo = static_cast<long long>(blockIdx.x) * a.rows_per_cta;
+    const long long hi = min(total, lo + a.rows_per_cta);
+    auto score_at = [&](long long i, uint64_t& row) -> double {
+        row = __ldg(a.rows + (a.index ? __ldg(a.index + i) : i));
+        if (a.use_mask) {
+            bool hit = false;
 #pragma unroll
-    for (int r = 0; r < kRowsPerThread; ++r) {
-        const long long i = lo + threadIdx.x + static_cast<long long>(r) * blockDim.x;
-        mys[r] = 0.0;
-        myrow[r] = kNoRow;
-        if (i < hi) {
-            const uint64_t row = __ldg(a.rows + (a.index ? __ldg(a.index + i) : i));
-            bool ok = true;
-            if (a.svc_mask) {
-                bool hit = false;
-#pragma unroll
-                for (int j = 0; j < 4; ++j) {
-                    const int svc = static_cast<int>(((row >> (16 * j)) & 0xFFFFull) / M.PP);
-                    if (svc < M.n) hit |= ((mask[svc >> 6] >> (svc & 63)) & 1ull) != 0;
-                }
-                ok = hit;
+            for (int j = 0; j < 4; ++j) {
+                const int svc = static_cast<int>(((row >> (16 * j)) & 0xFFFFull) / M.PP);
+                if (svc < M.n) hit |= ((a.svc_mask[svc >> 6] >> (svc & 63)) & 1ull) != 0;
             }
-            if (ok) {  // score, greedy.hpp:36-43 (ascending members, no FMA)
-                const double s = dev::row_score(W, row);
-                if (s > 0.0) {
-                    mys[r] = s;
-                    myrow[r] = row;
-                    tmax = fmax(tmax, s);
-                }
-            }
+            if (!hit) return 0.0;
         }
+        return dev::row_score(W, row);  // score, greedy.hpp:36-43 (ascending members, no FMA)
+    };
+    double tmax = 0.0;
+#pragma unroll 4
+    for (long long i = lo + threadIdx.x; i < hi; i += blockDim.x) {
+        uint64_t row;
+        tmax = fmax(tmax, score_at(i, row));
     }
     // 2. threshold: the largest per-warp K-th lane maximum (non-negative doubles order as
     //    their bit patterns, so an integer atomicMax on the bits is a max on the values)
@@ -105,17 +89,18 @@ __global__ void __launch_bounds__(kTopkThreads, 1) topk1_kernel(const __grid_con
     if ((threadIdx.x & 31u) == 0) atomicMax(&t_bits, static_cast<unsigned long long>(__double_as_longlong(tw)));
     __syncthreads();
     const double T = __longlong_as_double(static_cast<long long>(t_bits));
-    // 3. collect rows >= T (warp-aggregated appends), then rank them in parallel
-#pragma unroll
-    for (int r = 0; r < kRowsPerThread; ++r) {
-        const bool take = myrow[r] != kNoRow && mys[r] >= T;
+    // 3. collect rows >= T (warp-aggregated appends; L1/L2-hot second read), then rank them
+    for (long long i0 = lo; i0 < hi; i0 += blockDim.x) {
+        const long long i = i0 + threadIdx.x;
+        uint64_t row = 0;
+        const double sc = i < hi ? score_at(i, row) : 0.0;
+        const bool take = sc > 0.0 && sc >= T;
         const unsigned b = __ballot_sync(0xffffffffu, take);
         if (b) {
             int at = 0;
             if ((threadIdx.x & 31u) == 0) at = atomicAdd(&n_cand, __popc(b));
             at = __shfl_sync(0xffffffffu, at, 0) + __popc(b & dev::lanemask_lt());
-            if (take && at < kCandCap)
-                cand[at] = Cand{mys[r], 0.0, myrow[r], lo + threadIdx.x + static_cast<long long>(r) * blockDim.x};
+            if (take && at < kCandCap) cand[at] = Cand{sc, 0.0, row, i};
         }
     }
     __syncthreads();
@@ -171,10 +156,10 @@ __global__ void __launch_bounds__(kTopkThreads, 1) topk1_kernel(const __grid_con
 }
 
 size_t topk1_smem_bytes(int n, int PP, int) {
-    return static_cast<size_t>((n + 1) * PP + n + 1) * 8 + static_cast<size_t>(kCandCap + kTopkMaxK) * sizeof(Cand);
+    return static_cast<size_t>((n + 1) * PP + 1) * 8 + static_cast<size_t>(kCandCap + kTopkMaxK) * sizeof(Cand);
 }
 int topk1_threads() { return kTopkThreads; }
-int topk1_rows_per_cta() { return kTopkThreads * kRowsPerThread; }
+int topk1_rows_per_cta() { return 24576; }
 int topk1_max_k() { return kTopkMaxK; }
 int topk1_max_ctas() { return kCandCap / kTopkMaxK; }
 const void* topk1_kernel_ptr(int) { return reinterpret_cast<const void*>(&topk1_kernel); }

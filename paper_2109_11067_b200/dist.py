@@ -93,3 +93,84 @@ def root_parallel_mcts(comp, ctx: mp.PlanContext, params: mp.MctsParams, seed: i
     s = mp.mix_seed(seed, rank) if rank > 0 else seed  # rank 0 == mcts_solve(seed)
     plan = mp.mcts_solve(comp, ctx, params, s)
     return _pick_and_broadcast((len(plan), rank), plan, ctx, group)
+
+
+# ---------------------------------------------------------------- sharded greedy
+
+def _board_alloc(ctx: mp.PlanContext, n_ranks: int, device: int, ipc: bool):
+    import ctypes as C
+
+    lib = ctx.backend.lib
+    ptr = C.c_void_p()
+    handle = (C.c_uint8 * 64)()
+    ctx.backend.check(lib.mig_board_alloc(device, n_ranks, C.byref(ptr), handle if ipc else None))
+    return ptr, bytes(handle)
+
+
+def shard_local(ctxs: list, max_ctas: int | None = None):
+    """Ranks sharing ONE GPU (tests, development): context r scans shard r of every working
+    set on max_ctas CTAs (default: SMs / ranks) and the exchange boards are plain device
+    buffers.  Call fast_algo on all contexts concurrently (one host thread each)."""
+    import ctypes as C
+
+    P = len(ctxs)
+    boards = [_board_alloc(c, P, 0, False)[0] for c in ctxs]
+    arr = (C.c_void_p * P)(*[b.value for b in boards])
+    if max_ctas is None:
+        import torch
+
+        max_ctas = torch.cuda.get_device_properties(0).multi_processor_count // P
+    for r, c in enumerate(ctxs):
+        c.backend.check(c.backend.lib.mig_ctx_set_shard(c._p, r, P, arr, max_ctas))
+    return boards
+
+
+def shard_context(ctx: mp.PlanContext, device: int, group=None):
+    """One rank per GPU (torch.distributed): allocate this rank's exchange board, all-gather
+    the CUDA IPC handles, open the peers' boards (NVLink peer memory) and shard the context.
+    Afterwards every rank calls mp.fast_algo SPMD and receives the identical plan."""
+    import ctypes as C
+
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    own, handle = _board_alloc(ctx, world, device, True)
+    handles = [None] * world
+    dist.all_gather_object(handles, handle, group=group)
+    ptrs = []
+    for q in range(world):
+        if q == rank:
+            ptrs.append(own.value)
+            continue
+        p = C.c_void_p()
+        h = (C.c_uint8 * 64).from_buffer_copy(handles[q])
+        ctx.backend.check(ctx.backend.lib.mig_board_open(device, h, C.byref(p)))
+        ptrs.append(p.value)
+    arr = (C.c_void_p * world)(*ptrs)
+    ctx.backend.check(ctx.backend.lib.mig_ctx_set_shard(ctx._p, rank, world, arr, 0))
+    dist.barrier(group=group)  # every board is zeroed before any rank posts into it
+    return ptrs
+
+
+def sharded_rows(ctx: mp.PlanContext, group=None) -> int:
+    """Greedy rows scored by all ranks together (each rank counts its shard)."""
+    dev = _device(group)
+    t = torch.tensor([ctx.stats()["greedy_rows"]], dtype=torch.int64, device=dev)
+    dist.all_reduce(t, group=group)
+    return int(t.item())
+
+
+# ---------------------------------------------------------------- root-parallel rollouts (throughput mode)
+
+def root_parallel_rollouts(comp, ctx: mp.PlanContext, params: mp.RolloutParams, group=None):
+    """params.n_rollouts rollouts sharded over the ranks by global id (rank r runs ids
+    [r*R/P, (r+1)*R/P) with its own key cache); MIN-reduction of (best_len, best_id) and a
+    broadcast of the winner's path.  Deterministic for a given rank count."""
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    R = params.n_rollouts
+    lo, hi = R * rank // world, R * (rank + 1) // world
+    p = mp.RolloutParams(**{**params.__dict__, "n_rollouts": hi - lo, "id_offset": params.id_offset + lo})
+    res = mp.rollouts(comp, ctx, p)
+    plan = [ctx.pool[i].config for i in res.path]
+    big = 1 << 62
+    key = (res.best_len if res.best_len >= 0 else big, res.best_id if res.best_id >= 0 else big, rank)
+    winner, best = _pick_and_broadcast(key, plan, ctx, group)
+    return winner, best, res

@@ -1,0 +1,146 @@
+"""Sharded greedy and root-parallel rollouts across ranks.
+
+GPU: P virtual ranks share one B200 — each context scans 1/P of every working set on
+SMs/P CTAs and the per-step winners are exchanged through device-memory boards by the
+persistent kernel itself (the same code path as NVLink peer boards between GPUs).  The plan,
+every best-score bit and the total rows scored must equal the unsharded reference run.
+CPU: world size 2 over gloo for the rank-sharded rollouts (id ranges, MIN-reduction,
+winner broadcast) with the CPU checker backend.
+"""
+import os
+import socket
+import threading
+
+import pytest
+import torch.distributed as dist
+import torch.multiprocessing as tmp
+
+import support as S
+from support import mp
+
+GREEDY = S.load_golden("greedy.json")
+
+
+def services_of(entry):
+    return [mp.ServiceSpec(i, m, float.fromhex(r), float.fromhex(p)) for i, m, r, p in entry["services"]]
+
+
+def store_of(entry):
+    return S.profiles() if entry["store"] == "fixture" else S.two_model_store()
+
+
+def run_sharded(ctxs, comp):
+    out = [None] * len(ctxs)
+
+    def work(r):
+        tr = []
+        try:
+            plan = mp.fast_algo(comp, ctxs[r], trace=lambda i, c, s, cp: tr.append(S.fhex(s)))
+            out[r] = (S.plan_key(plan), tr, ctxs[r].stats()["greedy_rows"])
+        except Exception as e:  # surfaced below
+            out[r] = e
+
+    th = [threading.Thread(target=work, args=(r,)) for r in range(len(ctxs))]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(timeout=120)
+    for o in out:
+        if isinstance(o, Exception) or o is None:
+            raise AssertionError(f"sharded rank failed: {o!r}")
+    return out
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("P", [2, 3, 4])
+@pytest.mark.parametrize("name", ["slos_24", "gen24_8.7", "rand_n20_s13", "slos_day"])
+def test_sharded_greedy_bit_exact(P, name):
+    from paper_2109_11067_b200 import dist as D
+
+    g = GREEDY[name]
+    sv, ps = services_of(g), store_of(g)
+    ctxs = [mp.make_plan_context(sv, ps, mp.PartitionRuleSet.defaults()) for _ in range(P)]
+    D.shard_local(ctxs)
+    for rep in range(2):  # the exchange sequence continues across calls
+        for c in ctxs:
+            c.reset_stats()
+        out = run_sharded(ctxs, mp.zero_completion(len(sv)))
+        for plan, tr, _ in out:
+            assert plan == g["plan"]
+            assert tr == [t[0] for t in g["trace"]]
+        assert sum(o[2] for o in out) == g["rows_scored"]
+        assert min(o[2] for o in out) > 0 or len(g["plan"]) == 0
+
+
+@pytest.mark.gpu
+def test_shard_reset_to_single():
+    from paper_2109_11067_b200 import dist as D
+
+    g = GREEDY["slos_night"]
+    sv, ps = services_of(g), store_of(g)
+    ctxs = [mp.make_plan_context(sv, ps, mp.PartitionRuleSet.defaults()) for _ in range(2)]
+    D.shard_local(ctxs)
+    run_sharded(ctxs, mp.zero_completion(len(sv)))
+    c = ctxs[0]
+    c.backend.check(c.backend.lib.mig_ctx_set_shard(c._p, 0, 1, None, 0))
+    assert S.plan_key(mp.fast_algo(mp.zero_completion(len(sv)), c)) == g["plan"]
+
+
+def test_checkers_reject_sharding(impl):
+    if impl.name == "product":
+        pytest.skip("product shards")
+    ps = S.profiles()
+    sv = S.fixture_services("slos_day", ps)
+    c = mp.make_plan_context(sv, ps, mp.PartitionRuleSet.defaults(), backend=impl)
+    assert c.backend.lib.mig_ctx_set_shard(c._p, 0, 1, None, 0) == 0
+    assert c.backend.lib.mig_ctx_set_shard(c._p, 0, 2, None, 0) != 0
+
+
+# ---------------------------------------------------------------- rank-sharded rollouts (gloo)
+
+def free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def roll_worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2109_11067_b200 import dist as D
+
+        ps = S.profiles()
+        sv = S.fixture_services("slos_day", ps)
+        ctx = mp.make_plan_context(sv, ps, mp.PartitionRuleSet.defaults(), backend=S.checker_backend())
+        prm = mp.RolloutParams(n_rollouts=50, seed=21, max_depth=36)
+        win, plan, res = D.root_parallel_rollouts(mp.zero_completion(len(sv)), ctx, prm)
+        q.put((rank, win, S.plan_key(plan), res.best_len, res.best_id))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.skipif(S.checker_backend() is None, reason="no CPU checker library")
+def test_root_parallel_rollouts_world2():
+    ctx = tmp.get_context("spawn")
+    q = ctx.Queue()
+    port = free_port()
+    procs = [ctx.Process(target=roll_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=300) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    (_, w0, p0, l0, i0), (_, w1, p1, l1, i1) = res
+    assert w0 == w1 and p0 == p1
+    # the same shards computed in one process: ids [0,25) and [25,50), each with its own cache
+    ps = S.profiles()
+    sv = S.fixture_services("slos_day", ps)
+    c = mp.make_plan_context(sv, ps, mp.PartitionRuleSet.defaults(), backend=S.checker_backend())
+    shards = [mp.rollouts(mp.zero_completion(len(sv)), c, mp.RolloutParams(n_rollouts=25, seed=21, max_depth=36,
+                                                                          id_offset=o)) for o in (0, 25)]
+    best = min(range(2), key=lambda r: (shards[r].best_len if shards[r].best_len >= 0 else 1 << 62, r))
+    assert w0 == best
+    assert p0 == S.plan_key([c.pool[i].config for i in shards[best].path])
+    assert (l0, i0) == (shards[0].best_len, shards[0].best_id) and (l1, i1) == (shards[1].best_len, shards[1].best_id)
