@@ -249,8 +249,13 @@ int mig_board_bytes(int32_t n_ranks, int64_t* bytes);
 int mig_board_alloc(int32_t device, int32_t n_ranks, void** board, uint8_t* ipc_handle /* 64 bytes, or NULL */);
 int mig_board_open(int32_t device, const uint8_t* ipc_handle /* 64 bytes */, void** board);
 int mig_board_free(void* board, int32_t opened /* 1: from mig_board_open */);
-/* max_ctas > 0 caps the greedy grid of this context (ranks sharing one GPU). */
+/* max_ctas > 0 caps the greedy grid of this context. */
 int mig_ctx_set_shard(mig_ctx* ctx, int32_t rank, int32_t n_ranks, void* const* boards, int32_t max_ctas);
+/* fast_algo on ALL ranks of a shard whose contexts share one GPU (ctxs in rank order):
+ * their instances run as CTA ranges of one cooperative launch and exchange through the
+ * boards exactly as ranks on different GPUs do.  n_ctx == 1: plain mig_fast_algo. */
+int mig_fast_algo_group(mig_ctx* const* ctxs, int32_t n_ctx, const double* comp, int32_t n, mig_config* out,
+                        int32_t cap, int32_t* n_out);
 
 /* ---- GA (ga.hpp) ---- */
 typedef struct mig_ga_params { /* GaParams, ga.hpp:24-36 */

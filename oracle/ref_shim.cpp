@@ -589,6 +589,11 @@ int mig_board_open(int32_t, const uint8_t*, void**) {
     return guarded([&] { throw std::invalid_argument("exchange boards are device memory (product only)"); });
 }
 int mig_board_free(void*, int32_t) { return MIG_OK; }
+int mig_fast_algo_group(mig_ctx* const* ctxs, int32_t n_ctx, const double* comp, int32_t n, mig_config* out,
+                        int32_t cap, int32_t* n_out) {
+    if (n_ctx == 1 && ctxs) return mig_fast_algo(ctxs[0], comp, n, out, cap, n_out, nullptr, nullptr);
+    return guarded([&] { throw std::invalid_argument("sharded greedy is a device feature (product only)"); });
+}
 int mig_ctx_set_shard(mig_ctx*, int32_t rank, int32_t n_ranks, void* const*, int32_t) {
     return guarded([&] {
         if (n_ranks != 1 || rank != 0) throw std::invalid_argument("sharded greedy is a device feature (product only)");

@@ -138,6 +138,7 @@ SIGNATURES = {
     "mig_board_open": (_I, [C.c_int32, C.POINTER(C.c_uint8), C.POINTER(_P)]),
     "mig_board_free": (_I, [_P, C.c_int32]),
     "mig_ctx_set_shard": (_I, [_P, C.c_int32, C.c_int32, C.POINTER(_P), C.c_int32]),
+    "mig_fast_algo_group": (_I, [C.POINTER(_P), C.c_int32, _DP, C.c_int32, C.POINTER(ConfigC), C.c_int32, _I32P]),
     "mig_ga_params_defaults": (None, [C.POINTER(GaParamsC)]),
     "mig_completion_of": (_I, [_P, C.POINTER(ConfigC), C.c_int32, _DP]),
     "mig_mutate": (_I, [_P, C.POINTER(ConfigC), C.c_int32, C.POINTER(GaParamsC), _P, C.POINTER(ConfigC)]),

@@ -504,6 +504,24 @@ int mig_ctx_set_shard(mig_ctx* ctx, int32_t rank, int32_t n_ranks, void* const* 
     });
 }
 
+int mig_fast_algo_group(mig_ctx* const* ctxs, int32_t n_ctx, const double* comp, int32_t n, mig_config* out,
+                        int32_t cap, int32_t* n_out) {
+    int rc = MIG_OK;
+    int g = guarded([&] {
+        if (!ctxs || n_ctx < 1) throw ArgumentError("fast_algo_group: no contexts");
+        std::vector<Engine*> es;
+        for (int i = 0; i < n_ctx; ++i) es.push_back(ctxs[i]->e.get());
+        auto c = comp_of(ctxs[0], comp, n);
+        std::vector<uint64_t> rows;
+        std::vector<double> scores;
+        Engine::fast_algo_group(es, c, rows, scores);
+        std::vector<Config> plan;
+        for (uint64_t r : rows) plan.push_back(es[0]->config_of(r));
+        rc = emit(plan, out, cap, n_out);
+    });
+    return g != MIG_OK ? g : rc;
+}
+
 int mig_completion_of(const mig_ctx* ctx, const mig_config* configs, int32_t n_configs, double* comp_out) {
     return guarded([&] {
         std::vector<Config> cfgs;

@@ -90,6 +90,14 @@ struct GreedyArgs {
     long long exch_timeout_ns;
 };
 
+// A greedy launch: n_groups independent instances (ranks sharing this GPU), each on
+// ctas_per_group consecutive CTAs.
+struct GreedyLaunch {
+    int n_groups;
+    int ctas_per_group;
+    GreedyArgs g[kMaxRanks];
+};
+
 struct TopkArgs {
     DevModel M;
     const uint64_t* rows;     // base rows

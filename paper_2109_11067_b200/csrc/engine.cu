@@ -419,20 +419,20 @@ long long Engine::step_bound(const std::vector<double>& comp) const {
 }
 
 void Engine::fast_algo(const std::vector<double>& comp, std::vector<uint64_t>& rows, std::vector<double>& scores) {
-    rows.clear();
-    scores.clear();
-    if (static_cast<int>(comp.size()) != m_.n) throw PlanningError("fast_algo: completion vector length mismatch");
-    bool sat = true;
-    for (double c : comp)
-        if (c < 1.0 - kSatisfyEps) sat = false;
-    if (sat) return;  // greedy.hpp:101
+    fast_algo_group({this}, comp, rows, scores);
+}
 
-    Slot* s = acquire();
-    struct Rel {
-        Engine* e;
-        Slot* s;
-        ~Rel() { e->release(s); }
-    } rel{this, s};
+// Per-call resources and arguments of one greedy instance.
+struct GreedyCall {
+    Engine* e = nullptr;
+    Slot* s = nullptr;
+    long long n_base = 0;
+    const uint64_t* base_src = nullptr;
+    GreedyArgs a{};
+};
+
+void Engine::greedy_prepare(GreedyCall& c, const std::vector<double>& comp) {
+    Slot* s = c.s;
     CK(cudaSetDevice(device_));
     long long cap_steps = std::min<long long>(step_bound(comp), 1 << 24);
     if (s->cap_steps < cap_steps) {
@@ -445,91 +445,155 @@ void Engine::fast_algo(const std::vector<double>& comp, std::vector<uint64_t>& r
         CK(cudaMalloc(&s->d_pick_rows, sizeof(long long) * cap_steps));
         s->cap_steps = static_cast<int>(cap_steps);
     }
-    const long long n_base = n_ranks_ > 1 ? n_shard_ : static_cast<long long>(base_rows_.size());
-    const uint64_t* base_src = n_ranks_ > 1 ? d_shard_ : d_base_;
+    c.n_base = n_ranks_ > 1 ? n_shard_ : static_cast<long long>(base_rows_.size());
+    c.base_src = n_ranks_ > 1 ? d_shard_ : d_base_;
     // Arena = base + the all-feasible extension bound (every support with max_mix < |S| <= 4),
     // capped at 3G rows (24 GB); the kernel reports overflow and the call is retried larger.
-    ensure_ext(s, n_base + std::min<long long>(ext_bound_, 3ll << 30));
+    ensure_ext(s, c.n_base + std::min<long long>(ext_bound_, 3ll << 30));
+    std::memcpy(s->io->comp, comp.data(), sizeof(double) * m_.n);
+    CK(cudaMemsetAsync(s->st, 0, sizeof(GreedyState), s->stream));
+    // the working-set arena starts as a copy of the resident base pool (device to device)
+    if (c.n_base) CK(cudaMemcpyAsync(s->ext, c.base_src, c.n_base * 8, cudaMemcpyDeviceToDevice, s->stream));
+    GreedyArgs& a = c.a;
+    a = GreedyArgs{};
+    a.M = dm_;
+    a.rows = s->ext;
+    a.n_base = c.n_base;
+    a.cap = s->ext_cap;
+    a.cache_units = cache_units_;
+    a.phase_timers = std::getenv("MIGPLAN_PHASE_TIMERS") ? 1 : 0;
+    a.prefetch = 4;
+    if (const char* e = std::getenv("MIGPLAN_PREFETCH")) a.prefetch = std::atoi(e);
+    a.load_mode = 2;  // ld.global.cs: measured best for the streaming scan (profiles/)
+    if (const char* e = std::getenv("MIGPLAN_LOAD_MODE")) a.load_mode = std::atoi(e);
+    a.comp0 = s->io->comp;
+    a.st = s->st;
+    a.out = &s->io->res;
+    a.partials = s->partials;
+    a.pick_row = s->d_pick_row;
+    a.pick_score = s->d_pick_score;
+    a.pick_rows = s->d_pick_rows;
+    a.host_pick_row = s->pick_row;
+    a.host_pick_score = s->pick_score;
+    a.host_pick_rows = s->pick_rows;
+    a.ev_svc = s->ev_svc;
+    a.cap_steps = s->cap_steps;
+    a.n_ranks = n_ranks_;
+    a.rank = rank_;
+    for (int q = 0; q < n_ranks_ && n_ranks_ > 1; ++q) a.boards[q] = static_cast<ExchSlot*>(boards_[q]);
+    a.exch_seq0 = exch_seq_;
+    a.exch_timeout_ns = 10'000'000'000ll;
+    if (const char* e = std::getenv("MIGPLAN_EXCH_TIMEOUT_MS")) a.exch_timeout_ns = std::atoll(e) * 1'000'000ll;
+}
 
+// Returns false when the arena overflowed and was grown (the caller relaunches).
+bool Engine::greedy_finish(GreedyCall& c, float ms, int attempt, std::vector<uint64_t>& rows, std::vector<double>& scores) {
+    Slot* s = c.s;
+    const GreedyState h = s->io->res;
+    if (n_ranks_ > 1) {
+        if (h.status == kExtOverflow || h.status == kExchTimeout) {
+            n_ranks_ = 1;  // the ranks' exchange sequences diverged: the shard must be set again
+            throw DeviceError(h.status == kExchTimeout ? "sharded greedy: exchange with a peer rank timed out"
+                                                       : "sharded greedy: extension arena overflow");
+        }
+        exch_seq_ = h.last_seq;
+    }
+    if (h.status == kExtOverflow && attempt < 4) {
+        long long need = c.n_base + static_cast<long long>(h.ext_count) * 4 + (1 << 20);
+        ensure_ext(s, std::max(need, s->ext_cap * 2));
+        return false;
+    }
+    if (h.status == kExtOverflow) throw DeviceError("extension arena overflow");
+    if (h.status == kStepOverflow) throw DeviceError("greedy step buffer overflow");
+    rows.assign(s->pick_row, s->pick_row + h.n_steps);
+    scores.assign(s->pick_score, s->pick_score + h.n_steps);
+    stats.greedy_ns += static_cast<long long>(ms * 1e6f);
+    stats.h2d += static_cast<long long>(sizeof(double) * m_.n);
+    stats.d2h += static_cast<long long>(sizeof(GreedyState) + (sizeof(uint64_t) + sizeof(double) + sizeof(long long)) *
+                                                                  h.n_steps);
+    stats.greedy_rows += h.rows_scored;
+    stats.greedy_calls++;
+    stats.greedy_steps += h.n_steps;
+    stats.ext_events += h.n_events;
+    stats.ext_rows += static_cast<long long>(h.ext_count);
+    for (int k = 0; k < 5; ++k) stats.phase_ns[k] += static_cast<long long>(h.phase_ns[k]);
+    if (h.status == kNoPositive)
+        throw PlanningError("fast_algo: no config with positive score while services remain unsatisfied");
+    return true;
+}
+
+// fast_algo on one engine, or on the ranks of a sharded greedy that share this GPU: their
+// instances run as CTA ranges of ONE cooperative launch (GreedyLaunch), so the per-step
+// exchange between them never waits on a kernel that is not resident.
+void Engine::fast_algo_group(const std::vector<Engine*>& es, const std::vector<double>& comp,
+                             std::vector<uint64_t>& rows, std::vector<double>& scores) {
+    rows.clear();
+    scores.clear();
+    const int P = static_cast<int>(es.size());
+    if (P < 1 || P > kMaxRanks) throw ArgumentError("fast_algo: 1..8 contexts per group");
+    Engine* e0 = es[0];
+    for (Engine* e : es) {
+        if (e->device_ != e0->device_) throw ArgumentError("fast_algo group: contexts on different devices");
+        if (P > 1 && (e->n_ranks_ != P || e->max_ctas_ != es[0]->max_ctas_))
+            throw ArgumentError("fast_algo group: every context must be one rank of a P-way shard");
+    }
+    for (int r = 0; r < P && P > 1; ++r)
+        if (es[r]->rank_ != r) throw ArgumentError("fast_algo group: contexts must be in rank order");
+    if (static_cast<int>(comp.size()) != e0->m_.n) throw PlanningError("fast_algo: completion vector length mismatch");
+    bool sat = true;
+    for (double c : comp)
+        if (c < 1.0 - kSatisfyEps) sat = false;
+    if (sat) return;  // greedy.hpp:101
+
+    std::vector<GreedyCall> calls(P);
+    struct Rel {
+        std::vector<GreedyCall>& c;
+        ~Rel() {
+            for (auto& x : c)
+                if (x.s) x.e->release(x.s);
+        }
+    } rel{calls};
+    for (int r = 0; r < P; ++r) {
+        calls[r].e = es[r];
+        calls[r].s = es[r]->acquire();
+    }
     const int T = kernel_threads();
-    const size_t smem = greedy_smem_bytes(m_.n, m_.PP, cache_units_);
-    int G = num_sms_ * greedy_blocks_per_sm_;
-    if (max_ctas_ > 0) G = std::min(G, max_ctas_);
-    if (const char* e = std::getenv("MIGPLAN_GREEDY_CTAS")) G = std::max(1, std::min(G, std::atoi(e)));
-
+    const size_t smem = greedy_smem_bytes(e0->m_.n, e0->m_.PP, e0->cache_units_);
+    int G = e0->num_sms_ * e0->greedy_blocks_per_sm_ / P;
+    if (e0->max_ctas_ > 0) G = std::min(G, e0->max_ctas_);
+    if (const char* v = std::getenv("MIGPLAN_GREEDY_CTAS")) G = std::max(1, std::min(G, std::atoi(v)));
+    Slot* s0 = calls[0].s;
     for (int attempt = 0;; ++attempt) {
-        std::memcpy(s->io->comp, comp.data(), sizeof(double) * m_.n);
-        CK(cudaMemsetAsync(s->st, 0, sizeof(GreedyState), s->stream));
-        // the working-set arena starts as a copy of the resident base pool (device to device)
-        if (n_base) CK(cudaMemcpyAsync(s->ext, base_src, n_base * 8, cudaMemcpyDeviceToDevice, s->stream));
-        GreedyArgs a{};
-        a.M = dm_;
-        a.rows = s->ext;
-        a.n_base = n_base;
-        a.cap = s->ext_cap;
-        a.cache_units = cache_units_;
-        a.phase_timers = std::getenv("MIGPLAN_PHASE_TIMERS") ? 1 : 0;
-        a.prefetch = 4;
-        if (const char* e = std::getenv("MIGPLAN_PREFETCH")) a.prefetch = std::atoi(e);
-        a.load_mode = 0;
-        if (const char* e = std::getenv("MIGPLAN_LOAD_MODE")) a.load_mode = std::atoi(e);
-        a.comp0 = s->io->comp;
-        a.st = s->st;
-        a.out = &s->io->res;
-        a.partials = s->partials;
-        a.pick_row = s->d_pick_row;
-        a.pick_score = s->d_pick_score;
-        a.pick_rows = s->d_pick_rows;
-        a.host_pick_row = s->pick_row;
-        a.host_pick_score = s->pick_score;
-        a.host_pick_rows = s->pick_rows;
-        a.ev_svc = s->ev_svc;
-        a.cap_steps = s->cap_steps;
-        a.n_ranks = n_ranks_;
-        a.rank = rank_;
-        for (int q = 0; q < n_ranks_ && n_ranks_ > 1; ++q) a.boards[q] = static_cast<ExchSlot*>(boards_[q]);
-        a.exch_seq0 = exch_seq_;
-        a.exch_timeout_ns = 10'000'000'000ll;
-        if (const char* e = std::getenv("MIGPLAN_EXCH_TIMEOUT_MS")) a.exch_timeout_ns = std::atoll(e) * 1'000'000ll;
-        void* args[] = {&a};
-        CK(cudaEventRecord(s->e0, s->stream));
-        CK(cudaLaunchCooperativeKernel(greedy_kernel_ptr(), G, T, args, smem, s->stream));
-        stats.launches++;
-        CK(cudaEventRecord(s->e1, s->stream));
-        CK(cudaStreamSynchronize(s->stream));
+        GreedyLaunch L{};
+        L.n_groups = P;
+        L.ctas_per_group = G;
+        for (int r = 0; r < P; ++r) {
+            es[r]->greedy_prepare(calls[r], comp);
+            L.g[r] = calls[r].a;
+        }
+        for (int r = 1; r < P; ++r) CK(cudaStreamSynchronize(calls[r].s->stream));  // their arena copies
+        void* args[] = {&L};
+        CK(cudaEventRecord(s0->e0, s0->stream));
+        CK(cudaLaunchCooperativeKernel(greedy_kernel_ptr(), G * P, T, args, smem, s0->stream));
+        for (Engine* e : es) e->stats.launches++;
+        CK(cudaEventRecord(s0->e1, s0->stream));
+        CK(cudaStreamSynchronize(s0->stream));
         float ms = 0.f;
-        CK(cudaEventElapsedTime(&ms, s->e0, s->e1));
-        const GreedyState h = s->io->res;
-        if (n_ranks_ > 1) {
-            if (h.status == kExtOverflow || h.status == kExchTimeout) {
-                n_ranks_ = 1;  // the ranks' exchange sequences diverged: the shard must be set again
-                throw DeviceError(h.status == kExchTimeout ? "sharded greedy: exchange with a peer rank timed out"
-                                                           : "sharded greedy: extension arena overflow");
+        CK(cudaEventElapsedTime(&ms, s0->e0, s0->e1));
+        bool done = true;
+        for (int r = 0; r < P; ++r) {
+            std::vector<uint64_t> rr;
+            std::vector<double> ss;
+            if (!es[r]->greedy_finish(calls[r], ms, attempt, rr, ss)) done = false;
+            if (r == 0) {
+                rows = std::move(rr);
+                scores = std::move(ss);
+            } else if (done && rr != rows) {
+                throw DeviceError("sharded greedy: ranks disagree on the plan");
             }
-            exch_seq_ = h.last_seq;
         }
-        if (h.status == kExtOverflow && attempt < 4) {
-            long long need = n_base + static_cast<long long>(h.ext_count) * 4 + (1 << 20);
-            ensure_ext(s, std::max(need, s->ext_cap * 2));
-            continue;
-        }
-        if (h.status == kExtOverflow) throw DeviceError("extension arena overflow");
-        if (h.status == kStepOverflow) throw DeviceError("greedy step buffer overflow");
-        rows.assign(s->pick_row, s->pick_row + h.n_steps);
-        scores.assign(s->pick_score, s->pick_score + h.n_steps);
-        stats.greedy_ns += static_cast<long long>(ms * 1e6f);
-        stats.h2d += static_cast<long long>(sizeof(double) * m_.n);
-        stats.d2h += static_cast<long long>(sizeof(GreedyState) + (sizeof(uint64_t) + sizeof(double) +
-                                                                    sizeof(long long)) * h.n_steps);
-        stats.greedy_rows += h.rows_scored;
-        stats.greedy_calls++;
-        stats.greedy_steps += h.n_steps;
-        stats.ext_events += h.n_events;
-        stats.ext_rows += static_cast<long long>(h.ext_count);
-        for (int k = 0; k < 5; ++k) stats.phase_ns[k] += static_cast<long long>(h.phase_ns[k]);
-        if (h.status == kNoPositive)
-            throw PlanningError("fast_algo: no config with positive score while services remain unsatisfied");
-        return;
+        if (done) return;
+        if (P > 1) throw DeviceError("sharded greedy: extension arena overflow");
     }
 }
 
@@ -559,8 +623,10 @@ std::vector<long long> Engine::topk(const std::vector<double>& comp, int k, cons
         CK(cudaMemcpyAsync(s->index, index->data(), sizeof(long long) * total, cudaMemcpyHostToDevice, s->stream));
     }
     CK(cudaEventRecord(s->e0, s->stream));
-    long long per = topk1_rows_per_cta();
-    if (const char* e = std::getenv("MIGPLAN_TOPK_ROWS_PER_CTA")) per = std::max(1024ll, std::atoll(e));
+    // spread the scan over many SMs (one SM alone is issue-bound: ~30 us for 17K rows);
+    // the last-CTA merge ranks only rows above the per-CTA K-th scores
+    long long per = std::max<long long>(topk1_rows_per_cta(), (total + topk1_max_ctas() - 1) / topk1_max_ctas());
+    if (const char* e = std::getenv("MIGPLAN_TOPK_ROWS_PER_CTA")) per = std::max(256ll, std::atoll(e));
     const long long g1 = (total + per - 1) / per;
     bool single = k <= 32 && g1 <= topk1_max_ctas();
     if (single) {  // one launch: per-CTA threshold + parallel rank, last-CTA merge (topk.cu)

@@ -35,6 +35,7 @@ void board_close(void* board, bool opened);
 bool config_equal(const Config& a, const Config& b);
 
 struct Slot;
+struct GreedyCall;
 
 struct DeviceInfo {
     int num_sms = 0;
@@ -80,6 +81,9 @@ class Engine {
 
     // fast_algo (greedy.hpp:95-145) on the device.  Returns picked rows and their scores.
     void fast_algo(const std::vector<double>& comp, std::vector<uint64_t>& rows, std::vector<double>& scores);
+    // The same on the ranks (in rank order) of a sharded greedy that share one GPU: one launch.
+    static void fast_algo_group(const std::vector<Engine*>& es, const std::vector<double>& comp,
+                                std::vector<uint64_t>& rows, std::vector<double>& scores);
     // topk_candidates (mcts.hpp:56-76) over the base pool; filter by explicit indices or a
     // service mask (rows touching any masked service).  Returns pool indices, preferred first.
     std::vector<long long> topk(const std::vector<double>& comp, int k, const std::vector<long long>* index,
@@ -110,6 +114,8 @@ class Engine {
     void release(Slot*);
     void ensure_ext(Slot* s, long long rows);
     long long step_bound(const std::vector<double>& comp) const;
+    void greedy_prepare(GreedyCall& c, const std::vector<double>& comp);
+    bool greedy_finish(GreedyCall& c, float ms, int attempt, std::vector<uint64_t>& rows, std::vector<double>& scores);
 
     Model m_;
     std::map<std::string, ModelProfile> profiles_;

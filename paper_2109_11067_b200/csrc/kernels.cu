@@ -119,15 +119,15 @@ __device__ Best exchange_best(const DevModel& M, const GreedyArgs& a, Best x, un
 
 __device__ Best grid_argmax(const DevModel& M, const Best& mine, Best* partials, Best* winrec, unsigned* count,
                             unsigned* gen, int G, Best* red, const GreedyArgs& a, unsigned long long seq,
-                            int* xstatus) {
+                            int* xstatus, int bi) {
     __shared__ int s_last;
     __shared__ unsigned s_gen;
     if (threadIdx.x == 0) {
         cuda::atomic_ref<unsigned, cuda::thread_scope_device> g(*gen), c(*count);
         const unsigned my = g.load(cuda::memory_order_relaxed);
-        __stcg(&partials[blockIdx.x].s, mine.s);
-        __stcg(&partials[blockIdx.x].u, mine.u);
-        __stcg(reinterpret_cast<unsigned long long*>(&partials[blockIdx.x].row),
+        __stcg(&partials[bi].s, mine.s);
+        __stcg(&partials[bi].u, mine.u);
+        __stcg(reinterpret_cast<unsigned long long*>(&partials[bi].row),
                static_cast<unsigned long long>(mine.row));
         const unsigned t = c.fetch_add(1u, cuda::memory_order_acq_rel);
         s_last = t == static_cast<unsigned>(G) - 1u;
@@ -188,28 +188,38 @@ __device__ __forceinline__ void consider(const DevModel& M, const double* __rest
     take(M, U, row, row_score(W, row), best);
 }
 
-// Eight rows (four 16-byte units) at once: all 32 table gathers and 24 adds are issued
-// without a branch in between (instruction-level parallelism across rows); the per-row
-// preference logic runs only if some row reaches the thread's best score — rare once the
-// running best is established.  `floor` = the thread's best score, or the smallest
+// Eight rows (four 16-byte units) at once, two-level.  Level 1 gathers a 4-byte FP32
+// table Wf = W rounded UP (one shared-memory wavefront serves a whole warp far more often
+// than for the 8-byte W) and adds with round-up: ub >= the exact FP64 score, always (all
+// terms are >= 0).  A row with ub below the thread's running best (or ub == 0) can neither
+// win nor tie, so only the few survivors pay the exact FP64 gathers and adds of score()
+// (greedy.hpp:36-43, bit-exact).  `floor` = the thread's best score, or the smallest
 // positive double while it has none (rows must score > 0, greedy.hpp:130).
-__device__ __forceinline__ void consider8(const DevModel& M, const double* __restrict__ W, const double* U,
-                                          const uint4& v0, const uint4& v1, const uint4& v2, const uint4& v3,
-                                          Best& best) {
+__device__ __forceinline__ float row_ub(const float* __restrict__ Wf, uint64_t row) {
+    float s = __fadd_ru(Wf[row & 0xFFFFull], Wf[(row >> 16) & 0xFFFFull]);
+    s = __fadd_ru(s, Wf[(row >> 32) & 0xFFFFull]);
+    return __fadd_ru(s, Wf[row >> 48]);
+}
+
+__device__ __forceinline__ void consider8(const DevModel& M, const double* __restrict__ W, const float* __restrict__ Wf,
+                                          const double* U, const uint4& v0, const uint4& v1, const uint4& v2,
+                                          const uint4& v3, Best& best) {
     const uint64_t r[8] = {(static_cast<uint64_t>(v0.y) << 32) | v0.x, (static_cast<uint64_t>(v0.w) << 32) | v0.z,
                            (static_cast<uint64_t>(v1.y) << 32) | v1.x, (static_cast<uint64_t>(v1.w) << 32) | v1.z,
                            (static_cast<uint64_t>(v2.y) << 32) | v2.x, (static_cast<uint64_t>(v2.w) << 32) | v2.z,
                            (static_cast<uint64_t>(v3.y) << 32) | v3.x, (static_cast<uint64_t>(v3.w) << 32) | v3.z};
-    double sc[8];
+    float ub[8];
 #pragma unroll
-    for (int j = 0; j < 8; ++j) sc[j] = row_score(W, r[j]);
+    for (int j = 0; j < 8; ++j) ub[j] = row_ub(Wf, r[j]);
     const double floor = best.s > 0.0 ? best.s : 4.9406564584124654e-324;
     bool hit = false;
 #pragma unroll
-    for (int j = 0; j < 8; ++j) hit |= sc[j] >= floor;
+    for (int j = 0; j < 8; ++j) hit |= static_cast<double>(ub[j]) >= floor;
     if (hit) {
 #pragma unroll
-        for (int j = 0; j < 8; ++j) take(M, U, r[j], sc[j], best);
+        for (int j = 0; j < 8; ++j)
+            if (static_cast<double>(ub[j]) >= (best.s > 0.0 ? best.s : 4.9406564584124654e-324))
+                take(M, U, r[j], row_score(W, r[j]), best);
     }
 }
 
@@ -248,7 +258,7 @@ __device__ __forceinline__ void unrank(long long r, int q, int m, int* out) {
 }
 
 struct GreedySmem {  // byte offsets into dynamic shared memory
-    int W, U, comp, best, evmask, evof, evsvc, xlist, cache, total;
+    int W, Wf, U, comp, best, evmask, evof, evsvc, xlist, cache, total;
 };
 
 __host__ __device__ inline GreedySmem greedy_layout(int n, int PP, int cache_units) {
@@ -257,6 +267,8 @@ __host__ __device__ inline GreedySmem greedy_layout(int n, int PP, int cache_uni
     int o = 0;
     s.W = o;
     o += nW * 8;
+    s.Wf = o;
+    o += ((nW * 4 + 15) / 16) * 16;
     s.U = o;
     o += nW * 8;
     s.comp = o;
@@ -328,14 +340,22 @@ __global__ void __launch_bounds__(256) enum_base_kernel(const __grid_constant__ 
 // (two rows) assigned grid-stride; the first `cache_units / blockDim` units of every
 // thread live in this CTA's shared memory once complete, so a working set of up to
 // ~148 x 200 KB is scanned on-chip every step and only the excess streams from L2/HBM.
-__global__ void __launch_bounds__(kThreads, 1) greedy_kernel(const __grid_constant__ GreedyArgs a) {
+// One launch may carry several independent instances ("groups"): the ranks of a sharded
+// greedy that share one GPU run as CTA ranges of ONE cooperative grid, so their per-step
+// exchange never depends on two kernels being co-scheduled.  bi / G are the CTA index and
+// CTA count of this CTA's instance.
+__global__ void __launch_bounds__(kThreads, 1) greedy_kernel(const __grid_constant__ GreedyLaunch GL) {
     extern __shared__ __align__(16) unsigned char smem[];
+    const int grp = static_cast<int>(blockIdx.x) / GL.ctas_per_group;
+    const GreedyArgs& a = GL.g[grp];
+    const int G = GL.ctas_per_group;
+    const int bi = static_cast<int>(blockIdx.x) - grp * G;
     const DevModel& M = a.M;
     const int n = M.n, PP = M.PP;
     const int nW = (n + 1) * PP;
-    const int G = gridDim.x;
     const GreedySmem L = greedy_layout(n, PP, a.cache_units);
     double* W = reinterpret_cast<double*>(smem + L.W);
+    float* Wf = reinterpret_cast<float*>(smem + L.Wf);
     double* U = reinterpret_cast<double*>(smem + L.U);
     double* comp = reinterpret_cast<double*>(smem + L.comp);
     double* best_single = reinterpret_cast<double*>(smem + L.best);
@@ -358,7 +378,10 @@ __global__ void __launch_bounds__(kThreads, 1) greedy_kernel(const __grid_consta
     }
     if (threadIdx.x == 0) s_events = 0;
     __syncthreads();
-    for (int e = threadIdx.x; e < nW; e += blockDim.x) W[e] = w_of(comp, U, e / PP, e, n);
+    for (int e = threadIdx.x; e < nW; e += blockDim.x) {
+        W[e] = w_of(comp, U, e / PP, e, n);
+        Wf[e] = __double2float_ru(W[e]);
+    }
 
     // maybe_extend (greedy.hpp:107-119), warp 0, identical in every CTA.
     auto maybe_extend = [&]() {
@@ -383,7 +406,7 @@ __global__ void __launch_bounds__(kThreads, 1) greedy_kernel(const __grid_consta
                     ev_of[i] = static_cast<short>(pos);
                     ev_svc[pos] = static_cast<short>(i);
                     for (int w = 0; w < 4; ++w) ev_mask[pos * 4 + w] = um[w];
-                    if (blockIdx.x == 0) a.ev_svc[pos] = i;
+                    if (bi == 0) a.ev_svc[pos] = i;
                 }
                 ev += __popc(b);
             }
@@ -427,7 +450,7 @@ __global__ void __launch_bounds__(kThreads, 1) greedy_kernel(const __grid_consta
                 total += seg[k];
             }
             const long long stride = static_cast<long long>(G) * blockDim.x;
-            for (long long base = static_cast<long long>(blockIdx.x) * blockDim.x + (threadIdx.x & ~31u);
+            for (long long base = static_cast<long long>(bi) * blockDim.x + (threadIdx.x & ~31u);
                  base < total; base += stride) {
                 long long g = base + lane_id();
                 bool ok = g < total;
@@ -513,14 +536,14 @@ __global__ void __launch_bounds__(kThreads, 1) greedy_kernel(const __grid_consta
 
     const uint4* rows4 = reinterpret_cast<const uint4*>(a.rows);
     const long long GT = static_cast<long long>(G) * blockDim.x;
-    const long long my0 = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const long long my0 = static_cast<long long>(bi) * blockDim.x + threadIdx.x;
     const int J = a.cache_units / static_cast<int>(blockDim.x);  // cached units per thread
     int cj = 0;                                                  // units of mine cached so far
 
     int step = 0;
     unsigned long long last_seq = a.exch_seq0;
     long long rows_total = 0;
-    const bool timer = a.phase_timers && blockIdx.x == 0 && threadIdx.x == 0;
+    const bool timer = a.phase_timers && bi == 0 && threadIdx.x == 0;
     unsigned long long ph[5] = {0, 0, 0, 0, 0};
     unsigned long long tp = timer ? globaltimer() : 0;
     auto mark = [&](int k) {
@@ -553,7 +576,7 @@ __global__ void __launch_bounds__(kThreads, 1) greedy_kernel(const __grid_consta
                 const uint4 v1 = cache[(j + 1) * blockDim.x + threadIdx.x];
                 const uint4 v2 = cache[(j + 2) * blockDim.x + threadIdx.x];
                 const uint4 v3 = cache[(j + 3) * blockDim.x + threadIdx.x];
-                consider8(M, W, U, v0, v1, v2, v3, best);
+                consider8(M, W, Wf, U, v0, v1, v2, v3, best);
             }
             for (; j < cj; ++j) consider2(M, W, U, cache[j * blockDim.x + threadIdx.x], best);
             long long u = my0 + static_cast<long long>(cj) * GT;
@@ -571,7 +594,7 @@ __global__ void __launch_bounds__(kThreads, 1) greedy_kernel(const __grid_consta
                 // rows appended during this launch: L2-coherent loads (never the non-coherent path)
                 const uint4 v0 = ld_row4(rows4 + u, a.load_mode), v1 = ld_row4(rows4 + u + GT, a.load_mode),
                             v2 = ld_row4(rows4 + u + 2 * GT, a.load_mode), v3 = ld_row4(rows4 + u + 3 * GT, a.load_mode);
-                consider8(M, W, U, v0, v1, v2, v3, best);
+                consider8(M, W, Wf, U, v0, v1, v2, v3, best);
             }
             for (; u < NU; u += GT) consider2(M, W, U, __ldcg(rows4 + u), best);
             if ((N & 1) && my0 == 0) consider(M, W, U, __ldcg(a.rows + N - 1), best);
@@ -579,7 +602,7 @@ __global__ void __launch_bounds__(kThreads, 1) greedy_kernel(const __grid_consta
         best = block_best(M, best, red);
         mark(0);
         last_seq = a.exch_seq0 + static_cast<unsigned long long>(step) + 1ull;
-        const Best win = grid_argmax(M, best, a.partials, a.partials + G, bc, bg, G, red, a, last_seq, &a.st->status);
+        const Best win = grid_argmax(M, best, a.partials, a.partials + G, bc, bg, G, red, a, last_seq, &a.st->status, bi);
         mark(1);
         if (win.row == kNoRow) {
             const int xs = *reinterpret_cast<volatile int*>(&a.st->status);
@@ -593,7 +616,7 @@ __global__ void __launch_bounds__(kThreads, 1) greedy_kernel(const __grid_consta
                 int svc = code / PP;
                 if (svc < n) comp[svc] = __dadd_rn(comp[svc], U[code]);
             }
-            if (blockIdx.x == 0) {
+            if (bi == 0) {
                 a.pick_row[step] = win.row;
                 a.pick_score[step] = win.s;
                 a.pick_rows[step] = N;
@@ -604,7 +627,10 @@ __global__ void __launch_bounds__(kThreads, 1) greedy_kernel(const __grid_consta
         for (int e = threadIdx.x; e < 4 * PP; e += blockDim.x) {
             const int j = e / PP, p = e - j * PP;
             const int svc = static_cast<int>((win.row >> (16 * j)) & 0xFFFFull) / PP;
-            if (svc < n) W[svc * PP + p] = w_of(comp, U, svc, svc * PP + p, n);
+            if (svc < n) {
+                W[svc * PP + p] = w_of(comp, U, svc, svc * PP + p, n);
+                Wf[svc * PP + p] = __double2float_ru(W[svc * PP + p]);
+            }
         }
         ++step;
         mark(2);
@@ -613,14 +639,14 @@ __global__ void __launch_bounds__(kThreads, 1) greedy_kernel(const __grid_consta
         if (s_events > s_first_new) extend_and_sync();
     }
     mark(4);
-    if (blockIdx.x == 0) {  // one coalesced copy of the plan to host-mapped memory
+    if (bi == 0) {  // one coalesced copy of the plan to host-mapped memory
         for (int i = threadIdx.x; i < step; i += blockDim.x) {
             a.host_pick_row[i] = a.pick_row[i];
             a.host_pick_score[i] = a.pick_score[i];
             a.host_pick_rows[i] = a.pick_rows[i];
         }
     }
-    if (blockIdx.x == 0 && threadIdx.x == 0) {
+    if (bi == 0 && threadIdx.x == 0) {
         if (status != kOk) atomicExch(&a.st->status, status);
         __threadfence();
         GreedyState* o = a.out;  // host-mapped: the host reads it after one stream sync

@@ -22,7 +22,7 @@ namespace mgb {
 
 namespace {
 
-constexpr int kTopkThreads = 512;
+constexpr int kTopkThreads = 256;
 constexpr int kTopkWarps = kTopkThreads / 32;
 constexpr int kCandCap = 2048;      // per-CTA candidates (and merged per-CTA winners) in smem
 constexpr int kTopkMaxK = 32;
@@ -133,18 +133,39 @@ __global__ void __launch_bounds__(kTopkThreads, 1) topk1_kernel(const __grid_con
     __syncthreads();
     if (!last) return;
     __threadfence();
-    if (threadIdx.x == 0) n_cand = 0;
+    if (threadIdx.x == 0) {
+        n_cand = 0;
+        t_bits = 0ull;
+    }
     __syncthreads();
+    // merge threshold: every CTA with a full list holds K rows scoring >= its K-th score,
+    // so the global top-K scores >= the largest such K-th score
+    for (int b = threadIdx.x; b < static_cast<int>(gridDim.x); b += blockDim.x) {
+        const Best* p = a.partials + static_cast<long long>(b) * kTopkMaxK + (k - 1);
+        if (__ldcg(reinterpret_cast<const unsigned long long*>(&p->row)) != kNoRow)
+            atomicMax(&t_bits, static_cast<unsigned long long>(__double_as_longlong(__ldcg(&p->s))));
+    }
+    __syncthreads();
+    const double TM = __longlong_as_double(static_cast<long long>(t_bits));
     for (int i = threadIdx.x; i < static_cast<int>(gridDim.x) * k; i += blockDim.x) {
         const Best* p = a.partials + static_cast<long long>(i / k) * kTopkMaxK + (i % k);
         const uint64_t row = __ldcg(reinterpret_cast<const unsigned long long*>(&p->row));
         if (row == kNoRow) continue;
+        const double ps = __ldcg(&p->s);
+        if (ps < TM) continue;
         const int at = atomicAdd(&n_cand, 1);
         // CTA chunks are disjoint and ascending, so (CTA, rank) orders duplicates by position
-        cand[at] = Cand{__ldcg(&p->s), __ldcg(&p->u), row, static_cast<long long>(i)};
+        if (at < kCandCap) cand[at] = Cand{ps, __ldcg(&p->u), row, static_cast<long long>(i)};
     }
     __syncthreads();
     const int mc = n_cand;
+    if (mc > kCandCap) {  // pathological ties: the host re-runs the exact k-round kernel
+        if (threadIdx.x == 0) {
+            *a.n_out = -1;
+            *a.ticket = 0;
+        }
+        return;
+    }
     const int mgot = min(mc, k);
     rank_select(M, cand, mc, k, win);
     __syncthreads();
@@ -159,9 +180,9 @@ size_t topk1_smem_bytes(int n, int PP, int) {
     return static_cast<size_t>((n + 1) * PP + 1) * 8 + static_cast<size_t>(kCandCap + kTopkMaxK) * sizeof(Cand);
 }
 int topk1_threads() { return kTopkThreads; }
-int topk1_rows_per_cta() { return 24576; }
+int topk1_rows_per_cta() { return 1024; }
 int topk1_max_k() { return kTopkMaxK; }
-int topk1_max_ctas() { return kCandCap / kTopkMaxK; }
+int topk1_max_ctas() { return 1024; }
 const void* topk1_kernel_ptr(int) { return reinterpret_cast<const void*>(&topk1_kernel); }
 
 }  // namespace mgb

@@ -107,22 +107,29 @@ def _board_alloc(ctx: mp.PlanContext, n_ranks: int, device: int, ipc: bool):
     return ptr, bytes(handle)
 
 
-def shard_local(ctxs: list, max_ctas: int | None = None):
+def shard_local(ctxs: list):
     """Ranks sharing ONE GPU (tests, development): context r scans shard r of every working
-    set on max_ctas CTAs (default: SMs / ranks) and the exchange boards are plain device
-    buffers.  Call fast_algo on all contexts concurrently (one host thread each)."""
+    set; the exchange boards are plain device buffers.  Plan with fast_algo_local(ctxs, comp):
+    the instances run as CTA ranges of one cooperative launch."""
     import ctypes as C
 
     P = len(ctxs)
-    boards = [_board_alloc(c, P, 0, False)[0] for c in ctxs]
+    boards = [_board_alloc(c, P, c.device, False)[0] for c in ctxs]
     arr = (C.c_void_p * P)(*[b.value for b in boards])
-    if max_ctas is None:
-        import torch
-
-        max_ctas = torch.cuda.get_device_properties(0).multi_processor_count // P
     for r, c in enumerate(ctxs):
-        c.backend.check(c.backend.lib.mig_ctx_set_shard(c._p, r, P, arr, max_ctas))
+        c.backend.check(c.backend.lib.mig_ctx_set_shard(c._p, r, P, arr, 0))
     return boards
+
+
+def fast_algo_local(ctxs: list, comp):
+    """fast_algo on all ranks of a shard_local group (one launch); returns the common plan."""
+    import ctypes as C
+
+    c0 = ctxs[0]
+    buf, n = c0._comp(comp)
+    arr = (C.c_void_p * len(ctxs))(*[c._p.value for c in ctxs])
+    return mp._run_plan(c0, lambda out, cap, nout: c0.backend.lib.mig_fast_algo_group(arr, len(ctxs), buf, n, out, cap,
+                                                                                      C.byref(nout)))
 
 
 def shard_context(ctx: mp.PlanContext, device: int, group=None):

@@ -585,6 +585,7 @@ class PlanContext:
         self.profiles = profiles
         self.rules = rules
         self.max_mix = max_mix
+        self.device = device
         self.n = len(self.services)
         self._ids = {s.service_id: i for i, s in enumerate(self.services)}
         prof_c, n_models, k1 = _profiles_to_c(profiles)

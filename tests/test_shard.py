@@ -9,7 +9,6 @@ winner broadcast) with the CPU checker backend.
 """
 import os
 import socket
-import threading
 
 import pytest
 import torch.distributed as dist
@@ -30,25 +29,11 @@ def store_of(entry):
 
 
 def run_sharded(ctxs, comp):
-    out = [None] * len(ctxs)
+    """All ranks in one launch; returns (plan, per-rank rows scored)."""
+    from paper_2109_11067_b200 import dist as D
 
-    def work(r):
-        tr = []
-        try:
-            plan = mp.fast_algo(comp, ctxs[r], trace=lambda i, c, s, cp: tr.append(S.fhex(s)))
-            out[r] = (S.plan_key(plan), tr, ctxs[r].stats()["greedy_rows"])
-        except Exception as e:  # surfaced below
-            out[r] = e
-
-    th = [threading.Thread(target=work, args=(r,)) for r in range(len(ctxs))]
-    for t in th:
-        t.start()
-    for t in th:
-        t.join(timeout=120)
-    for o in out:
-        if isinstance(o, Exception) or o is None:
-            raise AssertionError(f"sharded rank failed: {o!r}")
-    return out
+    plan = D.fast_algo_local(ctxs, comp)
+    return S.plan_key(plan), [c.stats()["greedy_rows"] for c in ctxs]
 
 
 @pytest.mark.gpu
@@ -64,12 +49,16 @@ def test_sharded_greedy_bit_exact(P, name):
     for rep in range(2):  # the exchange sequence continues across calls
         for c in ctxs:
             c.reset_stats()
-        out = run_sharded(ctxs, mp.zero_completion(len(sv)))
-        for plan, tr, _ in out:
-            assert plan == g["plan"]
-            assert tr == [t[0] for t in g["trace"]]
-        assert sum(o[2] for o in out) == g["rows_scored"]
-        assert min(o[2] for o in out) > 0 or len(g["plan"]) == 0
+        plan, rows = run_sharded(ctxs, mp.zero_completion(len(sv)))
+        assert plan == g["plan"]
+        assert sum(rows) == g["rows_scored"]
+        assert min(rows) > 0 or len(g["plan"]) == 0
+    # a partial start (completion from the first half of the plan) shards the same way
+    half = [mp.GpuConfig(tuple(mp.AssignedInstance(mp.Placement(a, b), c, d) for a, b, c, d in cfg))
+            for cfg in g["plan"][:len(g["plan"]) // 2]]
+    comp = mp.completion_of(half, sv, ps)
+    single = mp.make_plan_context(sv, ps, mp.PartitionRuleSet.defaults())
+    assert run_sharded(ctxs, comp)[0] == S.plan_key(mp.fast_algo(comp, single))
 
 
 @pytest.mark.gpu
@@ -80,7 +69,7 @@ def test_shard_reset_to_single():
     sv, ps = services_of(g), store_of(g)
     ctxs = [mp.make_plan_context(sv, ps, mp.PartitionRuleSet.defaults()) for _ in range(2)]
     D.shard_local(ctxs)
-    run_sharded(ctxs, mp.zero_completion(len(sv)))
+    assert run_sharded(ctxs, mp.zero_completion(len(sv)))[0] == g["plan"]
     c = ctxs[0]
     c.backend.check(c.backend.lib.mig_ctx_set_shard(c._p, 0, 1, None, 0))
     assert S.plan_key(mp.fast_algo(mp.zero_completion(len(sv)), c)) == g["plan"]

@@ -1,7 +1,6 @@
 """Sharded greedy probe (development aid): P virtual ranks on one GPU vs the unsharded plan."""
 import os
 import sys
-import threading
 import time
 
 sys.path.insert(0, os.path.join(os.path.dirname(os.path.abspath(__file__)), "..", "tests"))
@@ -20,15 +19,8 @@ def main():
     rows = base.stats()["greedy_rows"]
     ctxs = [mp.make_plan_context(sv, ps, mp.PartitionRuleSet.defaults()) for _ in range(P)]
     D.shard_local(ctxs)
-    out = [None] * P
-
-    def work(r):
-        out[r] = S.plan_key(mp.fast_algo(mp.zero_completion(n), ctxs[r]))
-
     t2 = time.perf_counter()
-    th = [threading.Thread(target=work, args=(r,)) for r in range(P)]
-    [t.start() for t in th]
-    [t.join() for t in th]
+    out = [S.plan_key(D.fast_algo_local(ctxs, mp.zero_completion(n)))]
     t3 = time.perf_counter()
     srows = sum(c.stats()["greedy_rows"] for c in ctxs)
     print(f"n={n} mu={mu} P={P}: unsharded {len(ref)} GPUs {1e3*(t1-t0):.1f} ms; sharded plans equal: "
