@@ -291,6 +291,16 @@ typedef void (*mig_ga_log_fn)(void* user, int32_t round, int32_t best_gpus, doub
 int mig_two_phase(mig_ctx* ctx, const mig_ga_params* params, mig_config* out, int32_t cap, int32_t* n_out,
                   mig_ga_log_fn log, void* user);
 
+/* Throughput-mode two_phase (product extension, ga.cu): the same rounds, elitism and stop
+ * rules as two_phase, with crossover's slow procedure = FastProcedure (greedy.hpp:160-164)
+ * and Philox draws — draw t of child i in round r is Philox4x32-10(key = seed, counter =
+ * (t, (r << 20) + i)), index = floor(draw * n / 2^64).  Every generation's mutation,
+ * crossover and fitness run on the device over the whole population; children longer than
+ * 2 * |seed plan| + 64 GPUs count as failed crossovers.  params->workers and ->slow are
+ * ignored.  oracle/ and the reference shim restate the same rule on the CPU. */
+int mig_two_phase_parallel(mig_ctx* ctx, const mig_ga_params* params, mig_config* out, int32_t cap, int32_t* n_out,
+                           mig_ga_log_fn log, void* user);
+
 /* ---- eval bench helpers (bench.hpp) ---- */
 /* lower_bound(services, profiles), bench.hpp:93-108 */
 int mig_lower_bound(const mig_ctx* ctx, int32_t* out);

@@ -185,6 +185,29 @@ def gen_rollouts(ref):
     return res
 
 
+def gen_ga_parallel(ref):
+    """Throughput-mode two_phase (mig_two_phase_parallel): the reference's operators and
+    fast_algo refill under the product's Philox draw rule."""
+    res = {}
+    ps = S.profiles()
+    tw, sv6 = S.random_workload(6, 77)
+    cases = [("slos_day", ps, S.fixture_services("slos_day", ps), dict(seed=24, max_rounds=4)),
+             ("slos_night", ps, S.fixture_services("slos_night", ps), dict(seed=5, max_rounds=4, population=8)),
+             ("rand6", tw, sv6, dict(seed=9, max_rounds=5, mutation_pairs=3, erase_fraction=0.25)),
+             ("slos_24", ps, S.fixture_services("slos_24", ps), dict(seed=24, max_rounds=3))]
+    for name, p, sv, kw in cases:
+        t = time.time()
+        logs = []
+        dep = mp.two_phase_parallel(sv, p, mp.PartitionRuleSet.defaults(), mp.GaParams(time_budget_s=1e9, **kw),
+                                    log=lambda l: logs.append([l.round, l.best_gpus, l.best_slack.hex(), l.improved]),
+                                    backend=ref)
+        res[name] = {"store": store_name(p), "services": svc_json(sv), "params": kw,
+                     "plan": S.plan_key([g.config for g in dep.gpus]), "log": logs,
+                     "ref_wall_s": round(time.time() - t, 3)}
+        print(f"ga_parallel {name}: {len(dep.gpus)} GPUs ({time.time() - t:.1f}s)", flush=True)
+    return res
+
+
 def gen_greedy_big(ref):
     """gen(48, 7.0): ~6 minutes on one core; pins the n=48 plan bit-exactly."""
     p2, sv = S.gen(48, 7.0)
@@ -194,7 +217,7 @@ def gen_greedy_big(ref):
 
 
 SECTIONS = {"greedy": gen_greedy, "mcts": gen_mcts, "ga": gen_ga, "topk": gen_topk, "partitions": gen_partitions,
-            "greedy_big": gen_greedy_big, "rollouts": gen_rollouts}
+            "greedy_big": gen_greedy_big, "rollouts": gen_rollouts, "ga_parallel": gen_ga_parallel}
 
 
 def main(argv):

@@ -10,6 +10,8 @@
 #include <atomic>
 #include <chrono>
 #include <cstring>
+#include <map>
+#include <functional>
 #include <memory>
 #include <string>
 #include <vector>
@@ -518,6 +520,105 @@ RefPar ref_par(const PlanContext& ctx, const CompletionRates& comp, long long R,
     res.keys = cache.builds;
     return res;
 }
+// Throughput-mode two_phase (mig_two_phase_parallel) on the reference's own operators'
+// building blocks (GpuConfig, fast_algo, completion_of, evaluate_chromosome, fitter,
+// make_deployment; ga.hpp, greedy.hpp, core.hpp).  The draws are the product's Philox
+// stream instead of mt19937_64, so mutate/crossover are restated around them.
+Chromosome mutate_philox(const Chromosome& parent, const GaParams& params, const std::function<size_t(size_t)>& dr) {
+    Chromosome child = parent;  // ga.hpp:83-113
+    struct Ref {
+        size_t gpu, inst;
+    };
+    std::map<int, std::vector<Ref>> by_size;
+    for (size_t g = 0; g < child.gpus.size(); ++g)
+        for (size_t k = 0; k < child.gpus[g].instances.size(); ++k)
+            by_size[child.gpus[g].instances[k].placement.slices].push_back(Ref{g, k});
+    std::vector<int> sizes;
+    for (const auto& [size, refs] : by_size)
+        if (refs.size() >= 2) sizes.push_back(size);
+    if (sizes.empty()) return child;
+    for (int pair = 0; pair < params.mutation_pairs; ++pair)
+        for (int attempt = 0; attempt < 64; ++attempt) {
+            int size = sizes[dr(sizes.size())];
+            const auto& refs = by_size[size];
+            Ref a = refs[dr(refs.size())];
+            Ref b = refs[dr(refs.size())];
+            AssignedInstance& ia = child.gpus[a.gpu].instances[a.inst];
+            AssignedInstance& ib = child.gpus[b.gpu].instances[b.inst];
+            if (ia.service_id == ib.service_id) continue;
+            std::swap(ia.service_id, ib.service_id);
+            std::swap(ia.batch, ib.batch);
+            break;
+        }
+    return child;
+}
+
+Chromosome crossover_philox(const Chromosome& parent, const PlanContext& ctx, const GaParams& params,
+                            const std::function<size_t(size_t)>& dr, size_t lcap) {  // ga.hpp:51-77, FastProcedure
+    size_t n = parent.gpus.size();
+    size_t erase = n == 0 ? 0 : static_cast<size_t>(std::ceil(params.erase_fraction * static_cast<double>(n)));
+    if (erase == 0) return parent;
+    std::vector<size_t> order(n);
+    for (size_t i = 0; i < n; ++i) order[i] = i;
+    for (size_t i = 0; i < erase; ++i) std::swap(order[i], order[i + dr(n - i)]);
+    std::vector<bool> erased(n, false);
+    for (size_t i = 0; i < erase; ++i) erased[order[i]] = true;
+    std::vector<GpuConfig> survivors;
+    for (size_t i = 0; i < n; ++i)
+        if (!erased[i]) survivors.push_back(parent.gpus[i]);
+    try {
+        CompletionRates residual = completion_of(survivors, ctx.services, *ctx.profiles);
+        for (auto& cfg : fast_algo(residual, ctx)) survivors.push_back(std::move(cfg));
+        if (survivors.size() > lcap) return parent;
+        return evaluate_chromosome(std::move(survivors), ctx);
+    } catch (const PlanningError&) {
+        return parent;
+    }
+}
+
+std::vector<GpuConfig> two_phase_philox(const PlanContext& ctx, const GaParams& params,
+                                        const std::function<void(const GaRoundLog&)>& log) {
+    auto t0 = std::chrono::steady_clock::now();
+    auto elapsed = [&] { return std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count(); };
+    std::vector<GpuConfig> seed_cfg = fast_algo(zero_completion(ctx.services.size()), ctx);
+    if (params.time_budget_s <= 0.0 || params.max_rounds <= 0) {
+        std::sort(seed_cfg.begin(), seed_cfg.end());
+        return seed_cfg;
+    }
+    const size_t lcap = 2 * seed_cfg.size() + 64;
+    std::vector<Chromosome> pop;
+    pop.push_back(evaluate_chromosome(std::move(seed_cfg), ctx));
+    Chromosome best = pop[0];
+    int stall = 0;
+    for (int round = 1; round <= params.max_rounds; ++round) {
+        if (elapsed() >= params.time_budget_s) break;
+        if (stall >= params.stall_rounds) break;
+        size_t n_parents = std::min(pop.size(), (static_cast<size_t>(params.population) + 1) / 2);
+        std::vector<Chromosome> children(n_parents);
+        for (size_t i = 0; i < n_parents; ++i) {
+            uint64_t t = 0;
+            const uint64_t stream = (static_cast<uint64_t>(round) << 20) + i;
+            std::function<size_t(size_t)> dr = [&](size_t m) {
+                return static_cast<size_t>(((unsigned __int128)philox64_ref(params.seed, stream, t++) * m) >> 64);
+            };
+            children[i] = crossover_philox(mutate_philox(pop[i], params, dr), ctx, params, dr, lcap);
+        }
+        for (auto& c : children) pop.push_back(std::move(c));
+        std::stable_sort(pop.begin(), pop.end(), fitter);
+        if (pop.size() > static_cast<size_t>(params.population)) pop.resize(params.population);
+        bool improved = fitter(pop[0], best);
+        if (improved) {
+            best = pop[0];
+            stall = 0;
+        } else {
+            ++stall;
+        }
+        if (log) log(GaRoundLog{round, best.gpu_count, best.slack, improved, elapsed()});
+    }
+    std::sort(best.gpus.begin(), best.gpus.end());
+    return best.gpus;
+}
+
 void ref_par_out(const RefPar& r, int depth, mig_rollout_result* o) {
     if (!o) return;
     std::memset(o, 0, sizeof *o);
@@ -663,6 +764,20 @@ int mig_two_phase(mig_ctx* ctx, const mig_ga_params* params, mig_config* out, in
         std::vector<GpuConfig> cfgs;
         for (auto& gpu : dep.gpus) cfgs.push_back(gpu.config);
         rc = emit_plan(cfgs, ctx->services, out, cap, n_out);
+    });
+    return g != MIG_OK ? g : rc;
+}
+
+int mig_two_phase_parallel(mig_ctx* ctx, const mig_ga_params* params, mig_config* out, int32_t cap, int32_t* n_out,
+                           mig_ga_log_fn log, void* user) {
+    int rc = MIG_OK;
+    int g = guarded([&] {
+        std::function<void(const GaRoundLog&)> lg = nullptr;
+        if (log)
+            lg = [&](const GaRoundLog& r) {
+                log(user, r.round, r.best_gpus, r.best_slack, r.improved ? 1 : 0, r.elapsed_s);
+            };
+        rc = emit_plan(two_phase_philox(ctx->plan, ga_of(params), lg), ctx->services, out, cap, n_out);
     });
     return g != MIG_OK ? g : rc;
 }

@@ -24,6 +24,8 @@ struct DevModel {
     const uint8_t* layout_count;  // n_layouts * 5
     const int8_t* layout_slots;   // n_layouts * 5 * 7 (ascending slots per size index)
     const int* sizes;             // n_sizes (ascending)
+    const double* thr;            // n * 5: selected throughput per (service, size index), 0 if infeasible
+    const double* req;            // n: required rps
 };
 
 // One argmax candidate: score, util_sum, packed row.
@@ -70,6 +72,7 @@ struct GreedyArgs {
     int phase_timers;     // 1: CTA 0 records %globaltimer phase totals (diagnostics)
     int prefetch;         // bulk L2 prefetch distance of the streaming scan (iterations; 0 off)
     int load_mode;        // streaming row load flavour (kernels.cu ld_row4)
+    int ring_stages;      // TMA ring stages (32 KB each) for rows beyond the cache; 0: direct loads
     const double* comp0;  // host-mapped pinned
     GreedyState* st;      // device (barrier + atomics)
     GreedyState* out;     // host-mapped pinned: final state written by CTA 0
@@ -92,10 +95,11 @@ struct GreedyArgs {
 
 // A greedy launch: n_groups independent instances (ranks sharing this GPU), each on
 // ctas_per_group consecutive CTAs.
+constexpr int kMaxGroups = 8;  // instances per launch (param space: 8 x 368 B)
 struct GreedyLaunch {
     int n_groups;
     int ctas_per_group;
-    GreedyArgs g[kMaxRanks];
+    GreedyArgs g[kMaxGroups];
 };
 
 struct TopkArgs {
@@ -130,6 +134,38 @@ struct Topk1Args {
     int* n_out;         // host-mapped
     uint64_t svc_mask[4];
     double comp[256];
+};
+
+// Throughput-mode GA (ga.cu).  A chromosome is a list of GPU GENOMES (8 bytes each):
+// byte 0 = canonical layout id, byte 1 + k = service of the layout's k-th instance in
+// normalized order (size ascending, slot ascending; core.hpp:187-190), 0xFF = none.
+// Batch is a function of (service, size), so swaps of equal-size instances keep it exact.
+struct GaBreedArgs {
+    DevModel M;
+    const uint64_t* pop;   // parents: [n_children][L_cap] genomes
+    const int* pop_len;
+    uint64_t* work;        // [n_children][L_cap] mutated parents (crossover's fallback)
+    uint64_t* child;       // [n_children][L_cap] survivors, then refill
+    int* n_surv;
+    double* residual;      // [n_children][n] completion of the survivors
+    unsigned* scratch;     // [n_children][8 * L_cap] erase order / size refs
+    int L_cap;
+    int round;
+    int mutation_pairs;
+    double erase_fraction;
+    uint64_t seed;
+};
+
+struct GaFinishArgs {
+    DevModel M;
+    const uint64_t* work;
+    uint64_t* child;
+    const int* n_surv;
+    const uint64_t* const* refill;  // [n_children] device pointers to picked rows
+    const int* refill_n;            // [n_children] picks, -1: the refill failed
+    int* child_len;
+    double* child_slack;
+    int L_cap;
 };
 
 // Throughput-mode root-parallel rollouts (rollout.cu).

@@ -11,10 +11,11 @@
 #include <functional>
 
 #include "engine.hpp"
+#include "search.hpp"
 
 namespace mgb {
 
-size_t greedy_smem_bytes(int n, int PP, int cache_units);
+size_t greedy_smem_bytes(int n, int PP, int cache_units, int stages);
 size_t topk_smem_bytes(int n, int PP);
 const void* greedy_kernel_ptr();
 const void* topk_kernel_ptr();
@@ -157,14 +158,18 @@ Engine::Engine(const Rules& rules, std::map<std::string, ModelProfile> profiles,
     const int T = kernel_threads();
     // greedy: everything but the row cache is fixed; the cache takes the rest of the
     // opt-in shared memory (one CTA per SM), rounded to whole units per thread.
+    // TMA ring for rows beyond the on-chip cache: measured slower than direct L2-prefetched
+    // loads at n = 128 (profiles/), so off by default; MIGPLAN_RING=k enables k stages.
+    ring_stages_ = 0;
+    if (const char* e = std::getenv("MIGPLAN_RING")) ring_stages_ = std::max(0, std::min(8, std::atoi(e)));
     {
-        const long long fixed = static_cast<long long>(greedy_smem_bytes(m_.n, m_.PP, 0));
+        const long long fixed = static_cast<long long>(greedy_smem_bytes(m_.n, m_.PP, 0, ring_stages_)) + 128;
         long long room = static_cast<long long>(info.smem_optin) - 2048 - fixed;
         cache_units_ = static_cast<int>(std::max<long long>(0, room / 16) / T * T);
         if (const char* e = std::getenv("MIGPLAN_ROW_CACHE_UNITS"))
             cache_units_ = std::max(0, std::min(cache_units_, std::atoi(e) / T * T));
     }
-    const size_t gsm = greedy_smem_bytes(m_.n, m_.PP, cache_units_), tsm = topk_smem_bytes(m_.n, m_.PP);
+    const size_t gsm = greedy_smem_bytes(m_.n, m_.PP, cache_units_, ring_stages_), tsm = topk_smem_bytes(m_.n, m_.PP);
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&greedy_blocks_per_sm_, greedy_kernel_ptr(), T, gsm));
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&topk_blocks_per_sm_, topk_kernel_ptr(), T, tsm));
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&rollout_blocks_per_sm_, rollout_kernel_ptr(), rollout_threads(),
@@ -240,6 +245,13 @@ Engine::Engine(const Rules& rules, std::map<std::string, ModelProfile> profiles,
                  o_pc = put(pc.data(), pc.size()), o_lc = put(lc.data(), lc.size()), o_ls = put(ls.data(), ls.size()),
                  o_sz = put(m_.sizes.data(), m_.sizes.size() * 4), o_sup = put(supports.data(), supports.size() * 4),
                  o_off = put(offsets.data(), offsets.size() * 8);
+    std::vector<double> thr(static_cast<size_t>(m_.n) * kMaxSizes, 0.0), req(m_.n, 0.0);
+    for (int i = 0; i < m_.n; ++i) {
+        req[i] = m_.services[i].req;
+        for (size_t si = 0; si < m_.sizes.size(); ++si)
+            if (m_.feas[i][si].ok) thr[static_cast<size_t>(i) * kMaxSizes + si] = m_.feas[i][si].thr;
+    }
+    const size_t o_thr = put(thr.data(), thr.size() * 8), o_req = put(req.data(), req.size() * 8);
     const size_t o_base = (blob.size() + 15) & ~size_t{15};
     unsigned char* d = dalloc<unsigned char>(dev_allocs_, o_base + (static_cast<size_t>(total) + 2) * 8);
     CK(cudaMemcpy(d, blob.data(), blob.size(), cudaMemcpyHostToDevice));
@@ -253,6 +265,8 @@ Engine::Engine(const Rules& rules, std::map<std::string, ModelProfile> profiles,
     dm_.layout_count = d + o_lc;
     dm_.layout_slots = reinterpret_cast<const int8_t*>(d + o_ls);
     dm_.sizes = reinterpret_cast<const int*>(d + o_sz);
+    dm_.thr = reinterpret_cast<const double*>(d + o_thr);
+    dm_.req = reinterpret_cast<const double*>(d + o_req);
     d_base_ = reinterpret_cast<uint64_t*>(d + o_base);
     const auto t2 = clk::now();
 
@@ -336,6 +350,7 @@ const DeviceInfo& device_info(int device) {
     info.num_sms = prop.multiProcessorCount;
     info.smem_optin = static_cast<long long>(prop.sharedMemPerBlockOptin);
     // every kernel may use all the opt-in shared memory its static allocation leaves
+    CK(cudaFuncSetAttribute(topk1_kernel_ptr(32), cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     for (const void* k : {greedy_kernel_ptr(), topk_kernel_ptr(), topk1_kernel_ptr(32), rollout_kernel_ptr()}) {
         cudaFuncAttributes fa{};
         CK(cudaFuncGetAttributes(&fa, k));
@@ -431,10 +446,9 @@ struct GreedyCall {
     GreedyArgs a{};
 };
 
-void Engine::greedy_prepare(GreedyCall& c, const std::vector<double>& comp) {
+void Engine::greedy_prepare(GreedyCall& c, const double* comp_host, const double* comp_dev, long long cap_steps) {
     Slot* s = c.s;
     CK(cudaSetDevice(device_));
-    long long cap_steps = std::min<long long>(step_bound(comp), 1 << 24);
     if (s->cap_steps < cap_steps) {
         s->free_picks();
         CK(cudaHostAlloc(&s->pick_row, sizeof(uint64_t) * cap_steps, cudaHostAllocMapped));
@@ -450,7 +464,7 @@ void Engine::greedy_prepare(GreedyCall& c, const std::vector<double>& comp) {
     // Arena = base + the all-feasible extension bound (every support with max_mix < |S| <= 4),
     // capped at 3G rows (24 GB); the kernel reports overflow and the call is retried larger.
     ensure_ext(s, c.n_base + std::min<long long>(ext_bound_, 3ll << 30));
-    std::memcpy(s->io->comp, comp.data(), sizeof(double) * m_.n);
+    if (comp_host) std::memcpy(s->io->comp, comp_host, sizeof(double) * m_.n);
     CK(cudaMemsetAsync(s->st, 0, sizeof(GreedyState), s->stream));
     // the working-set arena starts as a copy of the resident base pool (device to device)
     if (c.n_base) CK(cudaMemcpyAsync(s->ext, c.base_src, c.n_base * 8, cudaMemcpyDeviceToDevice, s->stream));
@@ -461,12 +475,13 @@ void Engine::greedy_prepare(GreedyCall& c, const std::vector<double>& comp) {
     a.n_base = c.n_base;
     a.cap = s->ext_cap;
     a.cache_units = cache_units_;
+    a.ring_stages = ring_stages_;
     a.phase_timers = std::getenv("MIGPLAN_PHASE_TIMERS") ? 1 : 0;
     a.prefetch = 4;
     if (const char* e = std::getenv("MIGPLAN_PREFETCH")) a.prefetch = std::atoi(e);
     a.load_mode = 2;  // ld.global.cs: measured best for the streaming scan (profiles/)
     if (const char* e = std::getenv("MIGPLAN_LOAD_MODE")) a.load_mode = std::atoi(e);
-    a.comp0 = s->io->comp;
+    a.comp0 = comp_host ? s->io->comp : comp_dev;
     a.st = s->st;
     a.out = &s->io->res;
     a.partials = s->partials;
@@ -558,7 +573,7 @@ void Engine::fast_algo_group(const std::vector<Engine*>& es, const std::vector<d
         calls[r].s = es[r]->acquire();
     }
     const int T = kernel_threads();
-    const size_t smem = greedy_smem_bytes(e0->m_.n, e0->m_.PP, e0->cache_units_);
+    const size_t smem = greedy_smem_bytes(e0->m_.n, e0->m_.PP, e0->cache_units_, e0->ring_stages_);
     int G = e0->num_sms_ * e0->greedy_blocks_per_sm_ / P;
     if (e0->max_ctas_ > 0) G = std::min(G, e0->max_ctas_);
     if (const char* v = std::getenv("MIGPLAN_GREEDY_CTAS")) G = std::max(1, std::min(G, std::atoi(v)));
@@ -567,8 +582,9 @@ void Engine::fast_algo_group(const std::vector<Engine*>& es, const std::vector<d
         GreedyLaunch L{};
         L.n_groups = P;
         L.ctas_per_group = G;
+        const long long cap_steps = std::min<long long>(e0->step_bound(comp), 1 << 24);
         for (int r = 0; r < P; ++r) {
-            es[r]->greedy_prepare(calls[r], comp);
+            es[r]->greedy_prepare(calls[r], comp.data(), nullptr, cap_steps);
             L.g[r] = calls[r].a;
         }
         for (int r = 1; r < P; ++r) CK(cudaStreamSynchronize(calls[r].s->stream));  // their arena copies
@@ -626,6 +642,7 @@ std::vector<long long> Engine::topk(const std::vector<double>& comp, int k, cons
     // spread the scan over many SMs (one SM alone is issue-bound: ~30 us for 17K rows);
     // the last-CTA merge ranks only rows above the per-CTA K-th scores
     long long per = std::max<long long>(topk1_rows_per_cta(), (total + topk1_max_ctas() - 1) / topk1_max_ctas());
+    if (total > (1ll << 22)) per = total + 1;  // huge explicit lists: the exact k-round kernel below
     if (const char* e = std::getenv("MIGPLAN_TOPK_ROWS_PER_CTA")) per = std::max(256ll, std::atoll(e));
     const long long g1 = (total + per - 1) / per;
     bool single = k <= 32 && g1 <= topk1_max_ctas();
@@ -646,9 +663,22 @@ std::vector<long long> Engine::topk(const std::vector<double>& comp, int k, cons
         a.out_row = s->io->top_rows;
         a.n_out = &s->io->top_n;
         const int G = static_cast<int>(std::max<long long>(g1, 1));
+        a.rows_per_cta = (total + G - 1) / G;
         void* args[] = {&a};
-        CK(cudaLaunchKernel(topk1_kernel_ptr(32), G, topk1_threads(), args, topk1_smem_bytes(m_.n, m_.PP, 32),
-                            s->stream));
+        // the grid is one thread-block cluster: the CTAs merge their winners over DSMEM
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3(G);
+        cfg.blockDim = dim3(topk1_threads());
+        cfg.dynamicSmemBytes = topk1_smem_bytes(m_.n, m_.PP, 32);
+        cfg.stream = s->stream;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = G;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        CK(cudaLaunchKernelExC(&cfg, topk1_kernel_ptr(32), args));
         stats.launches++;
         CK(cudaEventRecord(s->e1, s->stream));
         CK(cudaStreamSynchronize(s->stream));
@@ -863,6 +893,218 @@ RolloutResult Engine::rollouts(const std::vector<double>& comp, long long n_roll
     stats.d2h += static_cast<long long>(sizeof(RolloutCounters) + sizeof(long long) * res.path.size() +
                                         (lengths ? sizeof(int) * n_roll : 0));
     return res;
+}
+
+// Independent greedy instances, one CTA each, in one launch: the GA's refills
+// (FastProcedure, greedy.hpp:160-164) from `count` device-resident completion vectors.
+// n_steps[i] = plan length, or -1 when fast_algo raised PlanningError (no positive score)
+// or the plan would exceed cap_steps.  rows[i] = device pointer to the picked rows.
+void Engine::greedy_batch(const double* d_comps, int count, long long cap_steps, std::vector<const uint64_t*>& rows,
+                          std::vector<int>& n_steps) {
+    rows.assign(count, nullptr);
+    n_steps.assign(count, -1);
+    if (count <= 0) return;
+    if (n_ranks_ > 1) throw ArgumentError("greedy_batch on a sharded context");
+    const int T = kernel_threads();
+    const size_t smem = greedy_smem_bytes(m_.n, m_.PP, cache_units_, ring_stages_);
+    for (int b0 = 0; b0 < count; b0 += kMaxGroups) {
+        const int nb = std::min(kMaxGroups, count - b0);
+        std::vector<GreedyCall> calls(nb);
+        struct Rel {
+            std::vector<GreedyCall>& c;
+            ~Rel() {
+                for (auto& x : c)
+                    if (x.s) x.e->release(x.s);
+            }
+        } rel{calls};
+        // the SMs are split between the instances (each a complete fast_algo on its CTAs)
+        const int gpc = std::max(1, num_sms_ * greedy_blocks_per_sm_ / nb);
+        std::unique_ptr<GreedyLaunch> L(new GreedyLaunch{});
+        L->n_groups = nb;
+        L->ctas_per_group = gpc;
+        for (int i = 0; i < nb; ++i) {
+            calls[i].e = this;
+            calls[i].s = acquire();
+            greedy_prepare(calls[i], nullptr, d_comps + static_cast<size_t>(b0 + i) * m_.n, cap_steps);
+            L->g[i] = calls[i].a;
+        }
+        for (int i = 1; i < nb; ++i) CK(cudaStreamSynchronize(calls[i].s->stream));
+        Slot* s0 = calls[0].s;
+        void* args[] = {L.get()};
+        CK(cudaEventRecord(s0->e0, s0->stream));
+        CK(cudaLaunchCooperativeKernel(greedy_kernel_ptr(), nb * gpc, T, args, smem, s0->stream));
+        stats.launches++;
+        CK(cudaEventRecord(s0->e1, s0->stream));
+        CK(cudaStreamSynchronize(s0->stream));
+        float ms = 0.f;
+        CK(cudaEventElapsedTime(&ms, s0->e0, s0->e1));
+        stats.greedy_ns += static_cast<long long>(ms * 1e6f);
+        for (int i = 0; i < nb; ++i) {
+            const GreedyState h = calls[i].s->io->res;
+            if (h.status == kExtOverflow) throw DeviceError("greedy_batch: extension arena overflow");
+            stats.greedy_rows += h.rows_scored;
+            stats.greedy_calls++;
+            stats.greedy_steps += h.n_steps;
+            stats.ext_events += h.n_events;
+            stats.ext_rows += static_cast<long long>(h.ext_count);
+            if (h.status == kOk) {
+                n_steps[b0 + i] = h.n_steps;
+                rows[b0 + i] = calls[i].s->d_pick_row;
+            }
+        }
+        // the picked rows stay valid until these slots are reused: the caller consumes them
+        // (ga_finish) before the next greedy call, on this thread
+        for (auto& x : calls) {
+            x.e->release(x.s);
+            x.s = nullptr;
+        }
+    }
+}
+
+// ---- throughput-mode GA device state (ga.cu)
+size_t ga_breed_smem_bytes(int n);
+size_t ga_finish_smem_bytes(int n);
+const void* ga_breed_kernel_ptr();
+const void* ga_finish_kernel_ptr();
+int ga_threads();
+
+struct GaRun {
+    int P = 0, nch = 0, L_cap = 0;
+    uint64_t* pop[2] = {nullptr, nullptr};
+    int* pop_len = nullptr;
+    uint64_t* work = nullptr;
+    uint64_t* child = nullptr;
+    int* n_surv = nullptr;
+    double* residual = nullptr;
+    unsigned* scratch = nullptr;
+    const uint64_t** refill = nullptr;
+    int* refill_n = nullptr;
+    int* child_len = nullptr;
+    double* child_slack = nullptr;
+    std::vector<void*> owned;
+    ~GaRun() {
+        for (void* p : owned) cudaFree(p);
+    }
+};
+
+GaRun* Engine::ga_begin(int P, int L_cap) {
+    CK(cudaSetDevice(device_));
+    auto r = std::make_unique<GaRun>();
+    r->P = P;
+    r->nch = (P + 1) / 2;
+    r->L_cap = L_cap;
+    auto al = [&](size_t bytes) {
+        void* p = nullptr;
+        CK(cudaMalloc(&p, std::max<size_t>(bytes, 16)));
+        r->owned.push_back(p);
+        return p;
+    };
+    const size_t rowb = sizeof(uint64_t) * L_cap;
+    for (auto& p : r->pop) p = static_cast<uint64_t*>(al(rowb * std::max(P, 1)));
+    r->pop_len = static_cast<int*>(al(sizeof(int) * r->nch));
+    r->work = static_cast<uint64_t*>(al(rowb * r->nch));
+    r->child = static_cast<uint64_t*>(al(rowb * r->nch));
+    r->n_surv = static_cast<int*>(al(sizeof(int) * r->nch));
+    r->residual = static_cast<double*>(al(sizeof(double) * m_.n * r->nch));
+    r->scratch = static_cast<unsigned*>(al(sizeof(unsigned) * 8 * L_cap * r->nch));
+    r->refill = static_cast<const uint64_t**>(al(sizeof(void*) * r->nch));
+    r->refill_n = static_cast<int*>(al(sizeof(int) * r->nch));
+    r->child_len = static_cast<int*>(al(sizeof(int) * r->nch));
+    r->child_slack = static_cast<double*>(al(sizeof(double) * r->nch));
+    static std::once_flag attrs;
+    std::call_once(attrs, [] {
+        for (const void* k : {ga_breed_kernel_ptr(), ga_finish_kernel_ptr()})
+            CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024));
+    });
+    return r.release();
+}
+
+void Engine::ga_end(GaRun* r) { delete r; }
+
+void Engine::ga_put(GaRun* r, int buf, int idx, const std::vector<uint64_t>& genomes) {
+    if (static_cast<int>(genomes.size()) > r->L_cap) throw ArgumentError("GA: chromosome longer than L_cap");
+    CK(cudaMemcpy(r->pop[buf] + static_cast<size_t>(idx) * r->L_cap, genomes.data(), genomes.size() * 8,
+                  cudaMemcpyHostToDevice));
+}
+
+std::vector<uint64_t> Engine::ga_get(GaRun* r, int buf, int idx, int len, bool from_child) {
+    std::vector<uint64_t> g(len);
+    const uint64_t* src = (from_child ? r->child : r->pop[buf]) + static_cast<size_t>(idx) * r->L_cap;
+    if (len) CK(cudaMemcpy(g.data(), src, len * 8ull, cudaMemcpyDeviceToHost));
+    return g;
+}
+
+// One generation: children of pop[buf][0..npar) (parents in fitness order, ga.hpp:146-151).
+void Engine::ga_generation(GaRun* r, int buf, const std::vector<int>& parent_len, int round, const GaParams& p,
+                           std::vector<int>& child_len, std::vector<double>& child_slack) {
+    const int npar = static_cast<int>(parent_len.size());
+    CK(cudaSetDevice(device_));
+    CK(cudaMemcpy(r->pop_len, parent_len.data(), sizeof(int) * npar, cudaMemcpyHostToDevice));
+    GaBreedArgs b{};
+    b.M = dm_;
+    b.pop = r->pop[buf];
+    b.pop_len = r->pop_len;
+    b.work = r->work;
+    b.child = r->child;
+    b.n_surv = r->n_surv;
+    b.residual = r->residual;
+    b.scratch = r->scratch;
+    b.L_cap = r->L_cap;
+    b.round = round;
+    b.mutation_pairs = p.mutation_pairs;
+    b.erase_fraction = p.erase_fraction;
+    b.seed = p.seed;
+    {
+        void* args[] = {&b};
+        CK(cudaLaunchKernel(ga_breed_kernel_ptr(), npar, ga_threads(), args, ga_breed_smem_bytes(m_.n), nullptr));
+        stats.launches++;
+        CK(cudaDeviceSynchronize());
+    }
+    // refill every child's residual with the device greedy, all children in one launch
+    std::vector<const uint64_t*> rows;
+    std::vector<int> steps;
+    greedy_batch(r->residual, npar, r->L_cap, rows, steps);
+    std::vector<int> ns(npar);
+    CK(cudaMemcpy(ns.data(), r->n_surv, sizeof(int) * npar, cudaMemcpyDeviceToHost));
+    for (int i = 0; i < npar; ++i)
+        if (ns[i] < 0) steps[i] = -1;  // no crossover: the child is the mutated parent
+    CK(cudaMemcpy(r->refill, rows.data(), sizeof(void*) * npar, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(r->refill_n, steps.data(), sizeof(int) * npar, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(r->child_len, parent_len.data(), sizeof(int) * npar, cudaMemcpyHostToDevice));
+    GaFinishArgs f{};
+    f.M = dm_;
+    f.work = r->work;
+    f.child = r->child;
+    f.n_surv = r->n_surv;
+    f.refill = r->refill;
+    f.refill_n = r->refill_n;
+    f.child_len = r->child_len;
+    f.child_slack = r->child_slack;
+    f.L_cap = r->L_cap;
+    {
+        void* args[] = {&f};
+        CK(cudaLaunchKernel(ga_finish_kernel_ptr(), npar, ga_threads(), args, ga_finish_smem_bytes(m_.n), nullptr));
+        stats.launches++;
+        CK(cudaDeviceSynchronize());
+    }
+    child_len.resize(npar);
+    child_slack.resize(npar);
+    CK(cudaMemcpy(child_len.data(), r->child_len, sizeof(int) * npar, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(child_slack.data(), r->child_slack, sizeof(double) * npar, cudaMemcpyDeviceToHost));
+    stats.h2d += static_cast<long long>(sizeof(int) * 3 * npar + sizeof(void*) * npar);
+    stats.d2h += static_cast<long long>((sizeof(int) * 2 + sizeof(double)) * npar);
+}
+
+// Next population buffer: entry j is (from_child ? child[idx] : pop[buf][idx]) of length len.
+void Engine::ga_select(GaRun* r, int buf, const std::vector<std::tuple<bool, int, int>>& order) {
+    const int nxt = buf ^ 1;
+    for (size_t j = 0; j < order.size(); ++j) {
+        const auto& [from_child, idx, len] = order[j];
+        const uint64_t* src = (from_child ? r->child : r->pop[buf]) + static_cast<size_t>(idx) * r->L_cap;
+        if (len) CK(cudaMemcpyAsync(r->pop[nxt] + j * static_cast<size_t>(r->L_cap), src, len * 8ull,
+                                    cudaMemcpyDeviceToDevice, nullptr));
+    }
+    CK(cudaDeviceSynchronize());
 }
 
 void Engine::set_shard(int rank, int n_ranks, const std::vector<void*>& boards, int max_ctas) {

@@ -12,6 +12,7 @@
 #include <memory>
 #include <mutex>
 #include <string>
+#include <tuple>
 #include <unordered_map>
 #include <vector>
 
@@ -36,6 +37,8 @@ bool config_equal(const Config& a, const Config& b);
 
 struct Slot;
 struct GreedyCall;
+struct GaRun;
+struct GaParams;
 
 struct DeviceInfo {
     int num_sms = 0;
@@ -102,6 +105,18 @@ class Engine {
     void set_shard(int rank, int n_ranks, const std::vector<void*>& boards, int max_ctas);
     int n_ranks() const { return n_ranks_; }
 
+    // Independent single-CTA greedy instances in one launch (the GA's refills).
+    void greedy_batch(const double* d_comps, int count, long long cap_steps, std::vector<const uint64_t*>& rows,
+                      std::vector<int>& n_steps);
+    // Throughput-mode GA device state and one generation (ga.cu; driver in search.cpp).
+    GaRun* ga_begin(int population, int L_cap);
+    void ga_end(GaRun* r);
+    void ga_put(GaRun* r, int buf, int idx, const std::vector<uint64_t>& genomes);
+    std::vector<uint64_t> ga_get(GaRun* r, int buf, int idx, int len, bool from_child);
+    void ga_generation(GaRun* r, int buf, const std::vector<int>& parent_len, int round, const GaParams& p,
+                       std::vector<int>& child_len, std::vector<double>& child_slack);
+    void ga_select(GaRun* r, int buf, const std::vector<std::tuple<bool, int, int>>& order);
+
     // completion_of (core.hpp:291-302), count-based, on the host (control logic, not hot).
     std::vector<double> completion_of(const std::vector<Config>& cfgs) const;
     const std::map<std::string, ModelProfile>& profiles() const { return profiles_; }
@@ -114,7 +129,7 @@ class Engine {
     void release(Slot*);
     void ensure_ext(Slot* s, long long rows);
     long long step_bound(const std::vector<double>& comp) const;
-    void greedy_prepare(GreedyCall& c, const std::vector<double>& comp);
+    void greedy_prepare(GreedyCall& c, const double* comp_host, const double* comp_dev, long long cap_steps);
     bool greedy_finish(GreedyCall& c, float ms, int attempt, std::vector<uint64_t>& rows, std::vector<double>& scores);
 
     Model m_;
@@ -133,6 +148,7 @@ class Engine {
     std::vector<double> min_u_;  // smallest positive utility per service (step bound)
     long long ext_bound_ = 0;
     int cache_units_ = 0;  // greedy shared-memory row cache per CTA (16-byte units)
+    int ring_stages_ = 0;  // greedy TMA ring stages
     std::vector<long long> support_off_;  // base pool: row offset of every support (K1 order) + total
     int rank_ = 0, n_ranks_ = 1, max_ctas_ = 0;
     std::vector<void*> boards_;

@@ -257,11 +257,42 @@ __device__ __forceinline__ void unrank(long long r, int q, int m, int* out) {
     }
 }
 
+// ---- TMA ring (cp.async.bulk + mbarrier) for the streaming part of the scan
+constexpr int kChunkUnits = 2048;  // 32 KB of rows per stage (4 units per thread)
+constexpr int kMaxStages = 8;
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+    return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(unsigned long long* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "MBAR_WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra MBAR_WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+// One elected thread: expect `bytes` on `bar`, then bulk-copy them global -> shared (TMA).
+__device__ __forceinline__ void tma_load(void* dst, const void* src, unsigned bytes, unsigned long long* bar) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+
 struct GreedySmem {  // byte offsets into dynamic shared memory
-    int W, Wf, U, comp, best, evmask, evof, evsvc, xlist, cache, total;
+    int W, Wf, U, comp, best, evmask, evof, evsvc, xlist, cache, ring, total;
 };
 
-__host__ __device__ inline GreedySmem greedy_layout(int n, int PP, int cache_units) {
+__host__ __device__ inline GreedySmem greedy_layout(int n, int PP, int cache_units, int stages) {
     GreedySmem s;
     const int nW = (n + 1) * PP;
     int o = 0;
@@ -286,6 +317,9 @@ __host__ __device__ inline GreedySmem greedy_layout(int n, int PP, int cache_uni
     o = (o + 15) & ~15;
     s.cache = o;
     o += cache_units * 16;
+    o = (o + 127) & ~127;
+    s.ring = o;
+    o += stages * kChunkUnits * 16;
     s.total = o;
     return s;
 }
@@ -353,7 +387,7 @@ __global__ void __launch_bounds__(kThreads, 1) greedy_kernel(const __grid_consta
     const DevModel& M = a.M;
     const int n = M.n, PP = M.PP;
     const int nW = (n + 1) * PP;
-    const GreedySmem L = greedy_layout(n, PP, a.cache_units);
+    const GreedySmem L = greedy_layout(n, PP, a.cache_units, a.ring_stages);
     double* W = reinterpret_cast<double*>(smem + L.W);
     float* Wf = reinterpret_cast<float*>(smem + L.Wf);
     double* U = reinterpret_cast<double*>(smem + L.U);
@@ -364,6 +398,16 @@ __global__ void __launch_bounds__(kThreads, 1) greedy_kernel(const __grid_consta
     short* ev_svc = reinterpret_cast<short*>(smem + L.evsvc);
     uint8_t* xlist = smem + L.xlist;
     uint4* cache = reinterpret_cast<uint4*>(smem + L.cache);
+    uint4* ring = reinterpret_cast<uint4*>(smem + L.ring);
+    __shared__ __align__(8) unsigned long long full_bar[kMaxStages], empty_bar[kMaxStages];
+    const int S = a.ring_stages;
+    if (threadIdx.x == 0) {
+        for (int q = 0; q < S; ++q) {
+            mbar_init(&full_bar[q], 1);
+            mbar_init(&empty_bar[q], kWarps);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
     __shared__ Best red[kWarps];
     __shared__ uint64_t unsat[4];
     __shared__ int s_events, s_first_new, s_done, s_m, s_status;
@@ -541,6 +585,7 @@ __global__ void __launch_bounds__(kThreads, 1) greedy_kernel(const __grid_consta
     int cj = 0;                                                  // units of mine cached so far
 
     int step = 0;
+    unsigned long long kchunk = 0;  // TMA ring chunks consumed by this CTA (all steps)
     unsigned long long last_seq = a.exch_seq0;
     long long rows_total = 0;
     const bool timer = a.phase_timers && bi == 0 && threadIdx.x == 0;
@@ -580,6 +625,51 @@ __global__ void __launch_bounds__(kThreads, 1) greedy_kernel(const __grid_consta
             }
             for (; j < cj; ++j) consider2(M, W, U, cache[j * blockDim.x + threadIdx.x], best);
             long long u = my0 + static_cast<long long>(cj) * GT;
+            if (S > 0) {
+                // Rows beyond the on-chip cache, TMA-staged: the CTA streams contiguous 32 KB
+                // chunks (chunk c = bi, bi + G, ...) through an S-stage shared-memory ring; one
+                // elected thread issues cp.async.bulk, mbarriers signal full / empty stages, so
+                // up to S x 32 KB per SM are in flight while the warps score the previous stage.
+                const long long base_u = static_cast<long long>(J) * GT;
+                const long long n_ch = NU > base_u ? (NU - base_u + kChunkUnits - 1) / kChunkUnits : 0;
+                const long long my_n = n_ch > bi ? (n_ch - bi + G - 1) / G : 0;
+                auto issue = [&](long long i) {
+                    const unsigned long long kk = kchunk + static_cast<unsigned long long>(i);
+                    const int slot = static_cast<int>(kk % S);
+                    if (kk >= static_cast<unsigned long long>(S))
+                        mbar_wait(&empty_bar[slot], static_cast<unsigned>((kk / S - 1) & 1ull));
+                    const long long u0 = base_u + (bi + i * G) * kChunkUnits;
+                    const long long cnt = min(static_cast<long long>(kChunkUnits), NU - u0);
+                    tma_load(ring + static_cast<long long>(slot) * kChunkUnits, rows4 + u0, static_cast<unsigned>(cnt * 16),
+                             &full_bar[slot]);
+                };
+                if (threadIdx.x == 0 && my_n > 0) {
+                    asm volatile("fence.proxy.async.global;" ::: "memory");  // rows appended this launch
+                    for (long long i = 0; i < my_n && i < S; ++i) issue(i);
+                }
+                const uint64_t pad = static_cast<uint64_t>(n * PP) * 0x0001000100010001ull;  // 4 sentinel codes
+                const uint4 padv = make_uint4(static_cast<unsigned>(pad), static_cast<unsigned>(pad >> 32),
+                                              static_cast<unsigned>(pad), static_cast<unsigned>(pad >> 32));
+                for (long long i = 0; i < my_n; ++i) {
+                    const unsigned long long kk = kchunk + static_cast<unsigned long long>(i);
+                    const int slot = static_cast<int>(kk % S);
+                    mbar_wait(&full_bar[slot], static_cast<unsigned>((kk / S) & 1ull));
+                    const long long u0 = base_u + (bi + i * G) * kChunkUnits;
+                    const int cnt = static_cast<int>(min(static_cast<long long>(kChunkUnits), NU - u0));
+                    const uint4* st = ring + static_cast<long long>(slot) * kChunkUnits;
+                    const int t = threadIdx.x;
+                    const uint4 v0 = t < cnt ? st[t] : padv;
+                    const uint4 v1 = t + 512 < cnt ? st[t + 512] : padv;
+                    const uint4 v2 = t + 1024 < cnt ? st[t + 1024] : padv;
+                    const uint4 v3 = t + 1536 < cnt ? st[t + 1536] : padv;
+                    __syncwarp();
+                    if (lane_id() == 0) mbar_arrive(&empty_bar[slot]);
+                    consider8(M, W, Wf, U, v0, v1, v2, v3, best);
+                    if (threadIdx.x == 0 && i + S < my_n) issue(i + S);
+                }
+                kchunk += static_cast<unsigned long long>(my_n);
+                u = NU;  // everything beyond the cache was streamed
+            }
             for (; u + 3 * GT < NU; u += 4 * GT) {
                 // Bulk L2 prefetch, a.prefetch iterations ahead: one thread per CTA pulls the
                 // CTA's next 8 KB stripes (contiguous: unit index = cta * blockDim + thread) into
@@ -722,9 +812,10 @@ __global__ void __launch_bounds__(kThreads, 1) topk_kernel(const __grid_constant
 }
 
 // ---------------------------------------------------------------- launch helpers
-size_t greedy_smem_bytes(int n, int PP, int cache_units) {
-    return static_cast<size_t>(greedy_layout(n, PP, cache_units).total);
+size_t greedy_smem_bytes(int n, int PP, int cache_units, int stages) {
+    return static_cast<size_t>(greedy_layout(n, PP, cache_units, stages).total);
 }
+int greedy_chunk_bytes() { return kChunkUnits * 16; }
 
 size_t topk_smem_bytes(int n, int PP) { return static_cast<size_t>((n + 1) * PP + n) * 8 + 16; }
 

@@ -365,6 +365,51 @@ double Model::score(uint64_t row, const double* comp) const {  // greedy.hpp:36-
     return s;
 }
 
+namespace {
+// normalized (slices, slot) placements of a layout: size ascending, slot ascending
+std::vector<std::pair<int, int>> layout_places(const Layout& L) {
+    std::vector<std::pair<int, int>> v;
+    for (const auto& g : L.groups)
+        for (int slot : g.slots) v.emplace_back(g.size, slot);
+    std::sort(v.begin(), v.end());
+    return v;
+}
+}  // namespace
+
+uint64_t Model::genome_of(const Inst* inst, int n) const {
+    std::vector<std::pair<int, int>> want;
+    for (int i = 0; i < n; ++i) want.emplace_back(inst[i].slices, inst[i].slot);
+    std::vector<int> order(n);
+    for (int i = 0; i < n; ++i) order[i] = i;
+    std::sort(order.begin(), order.end(), [&](int a, int b) { return want[a] < want[b]; });
+    std::vector<std::pair<int, int>> sorted;
+    for (int i : order) sorted.push_back(want[i]);
+    for (size_t l = 0; l < layouts.size(); ++l) {
+        if (layout_places(layouts[l]) != sorted) continue;
+        uint64_t g = static_cast<uint64_t>(l);
+        int pos = 0;
+        for (int i : order) g |= static_cast<uint64_t>(inst[i].svc) << (8 * (1 + pos++));
+        for (; pos < kMaxInst; ++pos) g |= 0xFFull << (8 * (1 + pos));
+        return g;
+    }
+    throw ArgumentError("configuration is not a canonical layout");
+}
+
+int Model::decode_genome(uint64_t g, Inst* out) const {
+    const int l = static_cast<int>(g & 0xFF);
+    if (l >= static_cast<int>(layouts.size())) throw ArgumentError("genome: bad layout");
+    auto places = layout_places(layouts[l]);
+    int n = 0;
+    for (const auto& [size, slot] : places) {
+        const int svc = static_cast<int>((g >> (8 * (1 + n))) & 0xFF);
+        int si = 0;
+        while (sizes[si] != size) ++si;
+        out[n] = Inst{size, slot, svc, feas[svc][si].batch};
+        ++n;
+    }
+    return n;
+}
+
 int64_t Model::rows_for_support(const int* s, int k) const {
     int64_t c = 0;
     for (const auto& t : templates[k]) {

@@ -139,6 +139,11 @@ struct Model {
     double util_sum(uint64_t row) const;
     double score(uint64_t row, const double* comp) const;
     int64_t rows_for_support(const int* s, int k) const;
+    // GPU genome of the throughput-mode GA (device.cuh GaBreedArgs): layout id + the service
+    // of each instance in normalized order.  genome_of throws if no canonical layout has
+    // exactly these placements.
+    uint64_t genome_of(const Inst* inst, int n) const;
+    int decode_genome(uint64_t g, Inst* out) const;
     void emit_support(const int* s, int k, std::vector<uint64_t>& out) const;
 };
 

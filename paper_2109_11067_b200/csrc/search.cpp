@@ -6,6 +6,8 @@
 #include <exception>
 #include <map>
 #include <thread>
+#include <cstdio>
+#include <cstdlib>
 
 namespace mgb {
 
@@ -288,6 +290,90 @@ Chromosome mutate(const Chromosome& parent, const GaParams& p, Rng& rng) {
         }
     }
     return child;
+}
+
+std::vector<Config> sorted_deployment(std::vector<Config> cfgs);
+
+// Throughput-mode two_phase (ga.cu): every generation's mutation, crossover (erase +
+// FastProcedure refill, all children in one greedy launch) and fitness run on the device
+// over the whole population, with Philox draws (child i of round r: stream (r << 20) + i).
+// Host: elitist stable selection over (gpu count, slack) as ga.hpp:165-175.
+std::vector<Config> two_phase_parallel(Engine& e, const GaParams& p,
+                                       const std::function<void(int, int, double, bool, double)>& log) {
+    auto t0 = std::chrono::steady_clock::now();
+    auto elapsed = [&] { return std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count(); };
+    std::vector<Config> seed_cfg = fast_plan(e, std::vector<double>(e.n(), 0.0));
+    if (p.time_budget_s <= 0.0 || p.max_rounds <= 0) return sorted_deployment(std::move(seed_cfg));
+    if (p.population < 1) throw ArgumentError("two_phase_parallel: population must be >= 1");
+    Chromosome seed = evaluate_chromosome(seed_cfg, e);
+    const int L_cap = 2 * seed.gpu_count + 64;
+    std::vector<uint64_t> g0;
+    for (const auto& c : seed_cfg) g0.push_back(e.model().genome_of(c.inst, c.n));
+    const double tb0 = elapsed();
+    GaRun* run = e.ga_begin(p.population, L_cap);
+    if (std::getenv("MIGPLAN_GA_TIMERS"))
+        std::fprintf(stderr, "[ga] seed %.2f ms, setup %.2f ms\n", 1e3 * tb0, 1e3 * (elapsed() - tb0));
+    struct End {
+        Engine& e;
+        GaRun* r;
+        ~End() { e.ga_end(r); }
+    } end{e, run};
+    e.ga_put(run, 0, 0, g0);
+    struct Ent {
+        int len;
+        double slack;
+    };
+    std::vector<Ent> pop{{seed.gpu_count, seed.slack}};
+    Ent best = pop[0];
+    std::vector<uint64_t> best_g = g0;
+    int buf = 0, stall = 0;
+    auto fitter = [](const Ent& a, const Ent& b) { return a.len != b.len ? a.len < b.len : a.slack < b.slack; };
+    for (int round = 1; round <= p.max_rounds; ++round) {
+        if (elapsed() >= p.time_budget_s) break;
+        if (stall >= p.stall_rounds) break;
+        const size_t npar = std::min(pop.size(), (static_cast<size_t>(p.population) + 1) / 2);
+        std::vector<int> plen(npar), clen;
+        std::vector<double> cslack;
+        for (size_t i = 0; i < npar; ++i) plen[i] = pop[i].len;
+        const double tg0 = elapsed();
+        e.ga_generation(run, buf, plen, round, p, clen, cslack);
+        if (std::getenv("MIGPLAN_GA_TIMERS"))
+            std::fprintf(stderr, "[ga] round %d: generation %.2f ms\n", round, 1e3 * (elapsed() - tg0));
+        struct Cand {
+            bool child;
+            int idx;
+            Ent f;
+        };
+        std::vector<Cand> all;
+        for (size_t i = 0; i < pop.size(); ++i) all.push_back({false, static_cast<int>(i), pop[i]});
+        for (size_t c = 0; c < npar; ++c) all.push_back({true, static_cast<int>(c), {clen[c], cslack[c]}});
+        std::stable_sort(all.begin(), all.end(), [&](const Cand& a, const Cand& b) { return fitter(a.f, b.f); });
+        if (all.size() > static_cast<size_t>(p.population)) all.resize(p.population);
+        std::vector<std::tuple<bool, int, int>> order;
+        pop.clear();
+        for (const auto& c : all) {
+            order.emplace_back(c.child, c.idx, c.f.len);
+            pop.push_back(c.f);
+        }
+        e.ga_select(run, buf, order);
+        buf ^= 1;
+        const bool improved = fitter(pop[0], best);
+        if (improved) {
+            best = pop[0];
+            best_g = e.ga_get(run, buf, 0, best.len, false);
+            stall = 0;
+        } else {
+            ++stall;
+        }
+        if (log) log(round, best.len, best.slack, improved, elapsed());
+    }
+    std::vector<Config> out;
+    for (uint64_t g : best_g) {
+        Config c;
+        c.n = e.model().decode_genome(g, c.inst);
+        out.push_back(c);
+    }
+    return sorted_deployment(std::move(out));
 }
 
 std::vector<Config> sorted_deployment(std::vector<Config> cfgs) {  // make_deployment, core.hpp:305-312

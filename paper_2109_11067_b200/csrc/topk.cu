@@ -16,7 +16,11 @@
 // rollout-cache miss and every expansion, so latency is the figure of merit.
 // A CTA whose rows tie at T beyond the candidate capacity reports overflow (*n_out = -1)
 // and the host re-runs the exact k-round kernel (kernels.cu) — a pathological case.
+#include <cooperative_groups.h>
+
 #include "common.cuh"
+
+namespace cg = cooperative_groups;
 
 namespace mgb {
 
@@ -41,8 +45,7 @@ __global__ void __launch_bounds__(kTopkThreads, 1) topk1_kernel(const __grid_con
     Cand* cand = reinterpret_cast<Cand*>(W + nW + 1);  // [kCandCap]
     Cand* win = cand + kCandCap;                        // [kTopkMaxK]
     __shared__ unsigned long long t_bits;
-    __shared__ int n_cand;
-    __shared__ bool last;
+    __shared__ int n_cand, n_got;
     const int k = a.k;
     if (threadIdx.x == 0) {
         t_bits = 0ull;
@@ -104,85 +107,77 @@ __global__ void __launch_bounds__(kTopkThreads, 1) topk1_kernel(const __grid_con
         }
     }
     __syncthreads();
-    const int nc = n_cand;
-    if (nc > kCandCap) {  // pathological ties at T: the host re-runs the exact k-round kernel
+    const int nc_raw = n_cand;
+    if (nc_raw > kCandCap && gridDim.x == 1) {  // pathological ties at T: the host re-runs the exact k-round kernel
         if (threadIdx.x == 0) *a.n_out = -1;
         return;
     }
+    const int nc = min(nc_raw, kCandCap);
     for (int i = threadIdx.x; i < nc; i += blockDim.x) cand[i].u = dev::row_usum(M.U, cand[i].row);
     __syncthreads();
-    const int got = min(nc, k);
-    rank_select(M, cand, nc, k, win);
+    const int got = nc_raw > kCandCap ? 0 : min(nc, k);
+    if (nc_raw <= kCandCap) rank_select(M, cand, nc, k, win);
     __syncthreads();
     if (gridDim.x == 1) {
         if (threadIdx.x < got) a.out_row[threadIdx.x] = win[threadIdx.x].row;
         if (threadIdx.x == 0) *a.n_out = got;
         return;
     }
-    // 4. publish this CTA's winners; the last CTA ranks the G x K of them
-    Best* part = a.partials + static_cast<long long>(blockIdx.x) * kTopkMaxK;
-    if (threadIdx.x < kTopkMaxK) {
-        const Cand c = threadIdx.x < got ? win[threadIdx.x] : Cand{0.0, 0.0, kNoRow, 0};
-        __stcg(&part[threadIdx.x].s, c.s);
-        __stcg(&part[threadIdx.x].u, c.u);
-        __stcg(reinterpret_cast<unsigned long long*>(&part[threadIdx.x].row), static_cast<unsigned long long>(c.row));
-    }
-    __threadfence();
-    __syncthreads();
-    if (threadIdx.x == 0) last = atomicAdd(a.ticket, 1u) == gridDim.x - 1;
-    __syncthreads();
-    if (!last) return;
-    __threadfence();
-    if (threadIdx.x == 0) {
-        n_cand = 0;
-        t_bits = 0ull;
-    }
-    __syncthreads();
-    // merge threshold: every CTA with a full list holds K rows scoring >= its K-th score,
-    // so the global top-K scores >= the largest such K-th score
-    for (int b = threadIdx.x; b < static_cast<int>(gridDim.x); b += blockDim.x) {
-        const Best* p = a.partials + static_cast<long long>(b) * kTopkMaxK + (k - 1);
-        if (__ldcg(reinterpret_cast<const unsigned long long*>(&p->row)) != kNoRow)
-            atomicMax(&t_bits, static_cast<unsigned long long>(__double_as_longlong(__ldcg(&p->s))));
-    }
-    __syncthreads();
-    const double TM = __longlong_as_double(static_cast<long long>(t_bits));
-    for (int i = threadIdx.x; i < static_cast<int>(gridDim.x) * k; i += blockDim.x) {
-        const Best* p = a.partials + static_cast<long long>(i / k) * kTopkMaxK + (i % k);
-        const uint64_t row = __ldcg(reinterpret_cast<const unsigned long long*>(&p->row));
-        if (row == kNoRow) continue;
-        const double ps = __ldcg(&p->s);
-        if (ps < TM) continue;
-        const int at = atomicAdd(&n_cand, 1);
-        // CTA chunks are disjoint and ascending, so (CTA, rank) orders duplicates by position
-        if (at < kCandCap) cand[at] = Cand{ps, __ldcg(&p->u), row, static_cast<long long>(i)};
-    }
-    __syncthreads();
-    const int mc = n_cand;
-    if (mc > kCandCap) {  // pathological ties: the host re-runs the exact k-round kernel
+    // 4. cluster merge over distributed shared memory: the grid is ONE thread-block cluster;
+    //    CTA 0 reads every CTA's K winners straight from their shared memory (no global
+    //    round trip, no atomics), ranks those above the merge threshold and writes the answer.
+    if (threadIdx.x == 0) n_got = nc_raw > kCandCap ? -1 : got;  // -1: this CTA overflowed
+    cg::cluster_group cluster = cg::this_cluster();
+    cluster.sync();
+    if (cluster.block_rank() == 0) {
+        const int nb = static_cast<int>(cluster.num_blocks());
+        __shared__ int overflow;
         if (threadIdx.x == 0) {
-            *a.n_out = -1;
-            *a.ticket = 0;
+            n_cand = 0;
+            t_bits = 0ull;
+            overflow = 0;
         }
-        return;
+        __syncthreads();
+        // merge threshold: every CTA with a full list holds K rows scoring >= its K-th score
+        for (int r = threadIdx.x; r < nb; r += blockDim.x) {
+            const int rg = *cluster.map_shared_rank(&n_got, r);
+            if (rg < 0) overflow = 1;
+            if (rg == k) {
+                const Cand* rw = cluster.map_shared_rank(win, r);
+                atomicMax(&t_bits, static_cast<unsigned long long>(__double_as_longlong(rw[k - 1].s)));
+            }
+        }
+        __syncthreads();
+        const double TM = __longlong_as_double(static_cast<long long>(t_bits));
+        Cand* mc_list = cand;  // own candidates are no longer needed
+        for (int i = threadIdx.x; i < nb * k; i += blockDim.x) {
+            const int r = i / k, q = i % k;
+            if (q >= *cluster.map_shared_rank(&n_got, r)) continue;
+            const Cand c = cluster.map_shared_rank(win, r)[q];
+            if (c.s < TM) continue;
+            const int at = atomicAdd(&n_cand, 1);
+            // CTA chunks are disjoint and ascending, so (CTA, rank) orders duplicates by position
+            if (at < kCandCap) mc_list[at] = Cand{c.s, c.u, c.row, static_cast<long long>(i)};
+        }
+        __syncthreads();
+        const int mc = min(n_cand, kCandCap);
+        Cand* out = win + kTopkMaxK;  // spare list after this CTA's own winners
+        rank_select(M, mc_list, mc, k, out);
+        __syncthreads();
+        const int mgot = min(mc, k);
+        if (threadIdx.x < mgot) a.out_row[threadIdx.x] = out[threadIdx.x].row;
+        if (threadIdx.x == 0) *a.n_out = (overflow || n_cand > kCandCap) ? -1 : mgot;
     }
-    const int mgot = min(mc, k);
-    rank_select(M, cand, mc, k, win);
-    __syncthreads();
-    if (threadIdx.x < mgot) a.out_row[threadIdx.x] = win[threadIdx.x].row;
-    if (threadIdx.x == 0) {
-        *a.n_out = mgot;
-        *a.ticket = 0;
-    }
+    cluster.sync();  // peers' shared memory stays alive until rank 0 has read it
 }
 
 size_t topk1_smem_bytes(int n, int PP, int) {
-    return static_cast<size_t>((n + 1) * PP + 1) * 8 + static_cast<size_t>(kCandCap + kTopkMaxK) * sizeof(Cand);
+    return static_cast<size_t>((n + 1) * PP + 1) * 8 + static_cast<size_t>(kCandCap + 2 * kTopkMaxK) * sizeof(Cand);
 }
 int topk1_threads() { return kTopkThreads; }
 int topk1_rows_per_cta() { return 1024; }
 int topk1_max_k() { return kTopkMaxK; }
-int topk1_max_ctas() { return 1024; }
+int topk1_max_ctas() { return 16; }  // one thread-block cluster (non-portable size 16)
 const void* topk1_kernel_ptr(int) { return reinterpret_cast<const void*>(&topk1_kernel); }
 
 }  // namespace mgb

@@ -1009,6 +1009,23 @@ def two_phase(services, profiles, rules, params: GaParams, log: Callable | None 
     return make_deployment(cfgs)
 
 
+def two_phase_parallel(services, profiles, rules, params: GaParams, log: Callable | None = None, backend=None,
+                       ctx: PlanContext | None = None) -> Deployment:
+    """Throughput-mode two_phase (include/migplan_b200.h): device-resident population, every
+    generation's mutation / crossover (FastProcedure refill) / fitness on the B200, Philox
+    draws.  Same rounds, elitism and stop rules as two_phase."""
+    own = ctx is None
+    if own:
+        ctx = make_plan_context(services, profiles, rules, 2, backend)
+    gp = params.to_c()
+    cb = abi.GA_LOG()
+    if log is not None:
+        cb = abi.GA_LOG(lambda _u, r, g, s, imp, el: log(GaRoundLog(r, g, s, bool(imp), el)))
+    cfgs = _run_plan(ctx, lambda out, cap, nout: ctx.backend.lib.mig_two_phase_parallel(
+        ctx._p, C.byref(gp), out, cap, C.byref(nout), cb, None))
+    return make_deployment(cfgs)
+
+
 # ---------------------------------------------------------------- bench helpers (bench.hpp)
 
 

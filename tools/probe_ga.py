@@ -1,0 +1,35 @@
+"""Throughput-mode GA probe (development aid): device two_phase_parallel vs parity two_phase."""
+import os
+import sys
+import time
+
+sys.path.insert(0, os.path.join(os.path.dirname(os.path.abspath(__file__)), "..", "tests"))
+import support as S  # noqa: E402
+from support import mp  # noqa: E402
+
+
+def main():
+    wl = sys.argv[1] if len(sys.argv) > 1 else "slos_24"
+    rounds = int(sys.argv[2]) if len(sys.argv) > 2 else 10
+    if wl.startswith("gen"):
+        n, mu = wl[3:].split("_")
+        ps, sv = S.gen(int(n), float(mu))
+    else:
+        ps = S.profiles()
+        sv = S.fixture_services(wl, ps)
+    ctx = mp.make_plan_context(sv, ps, mp.PartitionRuleSet.defaults())
+    for rep in range(2):
+        for fn in (mp.two_phase_parallel, mp.two_phase):
+            ctx.reset_stats()
+            t0 = time.perf_counter()
+            dep = fn(sv, ps, mp.PartitionRuleSet.defaults(), mp.GaParams(seed=24, max_rounds=rounds, time_budget_s=1e9,
+                                                                          workers=8), ctx=ctx)
+            dt = time.perf_counter() - t0
+            st = ctx.stats()
+            print(f"{wl} {fn.__name__}: {rounds} rounds {len(dep.gpus)} GPUs in {1e3*dt:.1f} ms, rows {st['rows_scored']:.3e}"
+                  f", greedy {st['greedy_ms']:.1f} ms / {st['greedy_calls']} calls, topk {st['topk_ms']:.1f} ms / "
+                  f"{st['topk_calls']} calls, launches {st['kernel_launches']}", flush=True)
+
+
+if __name__ == "__main__":
+    main()
