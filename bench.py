@@ -165,6 +165,70 @@ def profile_traffic():
         return None, None
 
 
+def extra_measurements(mp, local, peak):
+    """Device-timed evidence for the other BASELINE configs (not the headline line): the
+    n=128 stress greedy against the HBM roofline (config #5), 1e6 root-parallel rollouts at
+    n=48 (config #4) and the device GA (throughput mode) on config #2.  Each is one warm-up
+    plus one timed run; inputs resident, CUDA-event device time from the C-ABI stats."""
+    import support as S
+
+    out = {}
+    try:  # config #5: greedy sweep, HBM-bound
+        ps, sv = S.gen(128, 8.0)
+        ctx = mp.make_plan_context(sv, ps, mp.PartitionRuleSet.defaults(), device=local)
+        z = mp.zero_completion(len(sv))
+        mp.fast_algo(z, ctx)
+        ctx.reset_stats()
+        plan = mp.fast_algo(z, ctx)
+        st = ctx.stats()
+        sec = st["greedy_ms"] / 1e3
+        ach = 8.0 * st["greedy_rows"] / sec / 1e9
+        out["stress_greedy"] = {
+            "workload": "gen128_8.0_greedy (BASELINE config #5: 128 services, gen_workload mu=8.0)",
+            "gpus_used": len(plan), "rows_scored": st["greedy_rows"], "steps": st["greedy_steps"],
+            "ext_rows": st["ext_rows"], "kernel_ms": st["greedy_ms"], "configs_per_s": st["greedy_rows"] / sec,
+            "roofline": {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
+                         "bytes_per_unit": 8, "kernel": "greedy_kernel"}}
+        ctx.close()
+    except Exception as e:  # pragma: no cover - reported, not fatal
+        out["stress_greedy"] = {"error": repr(e)}
+    try:  # config #4: 1e6 root-parallel rollouts
+        ps, sv = S.gen(48, 7.0)
+        ctx = mp.make_plan_context(sv, ps, mp.PartitionRuleSet.defaults(), device=local)
+        z = mp.zero_completion(len(sv))
+        greedy = mp.fast_algo(z, ctx)
+        prm = mp.RolloutParams(n_rollouts=1_000_000, seed=1, max_depth=2 * len(greedy))
+        mp.rollouts(z, ctx, prm)
+        r = mp.rollouts(z, ctx, prm)
+        out["rollouts"] = {
+            "workload": "gen48_7.0, 1e6 root-parallel rollouts (BASELINE config #4), Philox seed 1",
+            "device_ms": r.device_ms, "rollouts_per_s": 1e6 / (r.device_ms / 1e3),
+            "rollout_steps_per_s": r.steps / (r.device_ms / 1e3), "steps": r.steps, "keys": r.keys,
+            "best_rollout_gpus": r.best_len, "greedy_gpus": len(greedy)}
+        ctx.close()
+    except Exception as e:  # pragma: no cover
+        out["rollouts"] = {"error": repr(e)}
+    try:  # config #2 throughput mode: the device GA
+        ps = S.profiles()
+        sv = S.fixture_services("slos_24", ps)
+        ctx = mp.make_plan_context(sv, ps, mp.PartitionRuleSet.defaults(), device=local)
+        prm = mp.GaParams(seed=24, max_rounds=10, time_budget_s=1e9)
+        mp.two_phase_parallel(sv, ps, mp.PartitionRuleSet.defaults(), prm, ctx=ctx)
+        ctx.reset_stats()
+        t0 = time.perf_counter()
+        dep = mp.two_phase_parallel(sv, ps, mp.PartitionRuleSet.defaults(), prm, ctx=ctx)
+        wall = time.perf_counter() - t0
+        st = ctx.stats()
+        out["ga_parallel"] = {
+            "workload": "slos24 two_phase_parallel: 10 rounds, P=16, Philox seed 24, FastProcedure refill",
+            "wall_ms": 1e3 * wall, "gpus_used": len(dep.gpus), "rows_scored": st["rows_scored"],
+            "kernel_launches": st["kernel_launches"], "configs_per_s": st["rows_scored"] / wall}
+        ctx.close()
+    except Exception as e:  # pragma: no cover
+        out["ga_parallel"] = {"error": repr(e)}
+    return out
+
+
 def cpu_baseline(name, sv, ps, rows_per_step):
     """The unmodified reference (oracle/_ref) on this host's cores, bounded sample: one step."""
     import support as S
@@ -236,6 +300,7 @@ def main():
     ap.add_argument("--workload", default="slos24_ga", choices=sorted(WORKLOADS))
     ap.add_argument("--workers", type=int, default=8, help="GA worker threads per rank (product)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-extras", action="store_true", help="skip the stress/rollout/GA evidence objects")
     args = ap.parse_args()
     if args.impl == "reference":
         return reference_arm(args)
@@ -322,10 +387,15 @@ def main():
 
     if rank == 0:
         peak, peak_kind = measured_peak()
-        greedy_s = st["greedy_ms"] / 1e3
-        greedy_bytes = 8.0 * st["greedy_rows"] / max(st["greedy_calls"], 1)  # algorithmic bytes per launch
-        launch_s = greedy_s / max(st["greedy_calls"], 1)
-        achieved = greedy_bytes / launch_s / 1e9 if launch_s > 0 else 0.0
+        # roofline of the DOMINANT kernel of this workload by device time: algorithmic bytes =
+        # 8 B per packed row scanned (greedy: rows x steps; top-K: its candidate set)
+        kern = {"greedy_kernel": (st["greedy_ms"], st["greedy_rows"], st["greedy_calls"]),
+                "topk1_kernel": (st["topk_ms"], st["topk_rows"], st["topk_calls"])}
+        dom = max(kern, key=lambda k: kern[k][0])
+        k_ms, k_rows, k_calls = kern[dom]
+        launch_s = k_ms / 1e3 / max(k_calls, 1)
+        k_bytes = 8.0 * k_rows / max(k_calls, 1)  # algorithmic bytes per launch
+        achieved = k_bytes / launch_s / 1e9 if launch_s > 0 else 0.0
         traffic, traffic_wl = profile_traffic()
         line = {
             "metric": "candidate configs scored/sec", "value": rows_all / (dev_ms_max / 1e3), "unit": "configs/s",
@@ -341,9 +411,11 @@ def main():
                     "ms_per_step": e2e_ms_max / args.steps},
             "gpu_launches": st["kernel_launches"],
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": traffic,
-                         "kernel": "greedy_kernel (persistent fast_algo: scan + argmax + extension)",
-                         "bytes_per_unit": 8, "unit_of_work": "packed candidate row scanned per greedy step",
+                         "frac": achieved / peak, "traffic": traffic, "kernel": dom,
+                         "launch_us": 1e6 * launch_s, "bytes_per_launch": k_bytes,
+                         "bytes_per_unit": 8, "unit_of_work": "packed candidate row scored (8 B)",
+                         "note": "this workload's kernels are latency-bound (<= 1.3M-row working sets, L2/smem "
+                                 "resident); the HBM-bound regime is extras.stress_greedy",
                          "peak_kind": peak_kind, "traffic_workload": traffic_wl},
             "clocks": clock,
             "breakdown": {"greedy_ms": st["greedy_ms"], "topk_ms": st["topk_ms"], "greedy_calls": st["greedy_calls"],
@@ -352,6 +424,8 @@ def main():
         }
         if world == 1 and not args.no_cpu_baseline:
             line["cpu_baseline"] = cpu_baseline(args.workload, sv, ps, rows / args.steps)
+        if world == 1 and not args.no_extras:
+            line["extras"] = extra_measurements(mp, local, peak)
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()

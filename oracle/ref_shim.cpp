@@ -24,6 +24,9 @@
 #include "migplan/mcts.hpp"
 #include "migplan/mig_rules.hpp"
 #include "migplan_b200.h"
+#ifdef MIGREF_WITH_IO
+#include "migplan/io.hpp"
+#endif
 
 using namespace migplan;
 
@@ -794,6 +797,24 @@ void mig_ctx_reset_stats(mig_ctx*) {}
 
 // Reference-arm extras (not in the product header): rows a fast_algo scans, and
 // gen_workload (bench.hpp:125-156) so generated workloads come from the reference itself.
+/* deployment_to_json(make_deployment(configs)).dump(2) + "\n" — the reference's own output
+ * file bytes (io.hpp:44-48,196-208; core.hpp:305-312).  *len = bytes (NUL excluded). */
+int mig_ref_deployment_json(mig_ctx* ctx, const mig_config* cfgs, int32_t n, char* buf, int32_t cap, int32_t* len) {
+    return guarded([&] {
+#ifdef MIGREF_WITH_IO
+        std::vector<GpuConfig> v;
+        for (int i = 0; i < n; ++i) v.push_back(from_c(cfgs[i], ctx->services));
+        std::string out = deployment_to_json(make_deployment(std::move(v))).dump(2) + "\n";
+        *len = static_cast<int32_t>(out.size());
+        if (static_cast<int32_t>(out.size()) + 1 > cap) throw std::invalid_argument("output capacity too small");
+        std::memcpy(buf, out.c_str(), out.size() + 1);
+#else
+        (void)ctx, (void)cfgs, (void)n, (void)buf, (void)cap, (void)len;
+        throw std::invalid_argument("built without nlohmann/json (io.hpp)");
+#endif
+    });
+}
+
 int mig_ref_count_rows(mig_ctx* ctx, const double* comp, int32_t n, int64_t* rows) {
     return guarded([&] { *rows = count_rows(comp_of(comp, n, ctx), ctx->plan); });
 }

@@ -27,6 +27,8 @@ constexpr int kWarps = kThreads / 32;
 // Streaming-row loads.  Rows are append-only and every row a step reads was completed
 // before a grid barrier, so any load that bypasses L1 (L2 is the coherence point) is exact.
 //   0: ld.global.cg (L2 only)   1: ld.global.nc.L1::no_allocate   2: ld.global.cs (evict-first)
+// (ld.global.cs measured best for the n = 128 stress scan, profiles/: the hot loop uses it)
+#define LOADM 2
 __device__ __forceinline__ uint4 ld_row4(const uint4* p, int mode) {
     uint4 v;
     if (mode == 1) {
@@ -201,21 +203,30 @@ __device__ __forceinline__ float row_ub(const float* __restrict__ Wf, uint64_t r
     return __fadd_ru(s, Wf[row >> 48]);
 }
 
+// Upper bound of one row from its two 32-bit halves (codes 0,1 in lo; 2,3 in hi): 32-bit
+// field extraction only, no 64-bit shifts on the hot path.
+__device__ __forceinline__ float ub2(const float* __restrict__ Wf, unsigned lo, unsigned hi) {
+    float s = __fadd_ru(Wf[lo & 0xFFFFu], Wf[lo >> 16]);
+    s = __fadd_ru(s, Wf[hi & 0xFFFFu]);
+    return __fadd_ru(s, Wf[hi >> 16]);
+}
+
 __device__ __forceinline__ void consider8(const DevModel& M, const double* __restrict__ W, const float* __restrict__ Wf,
                                           const double* U, const uint4& v0, const uint4& v1, const uint4& v2,
                                           const uint4& v3, Best& best) {
-    const uint64_t r[8] = {(static_cast<uint64_t>(v0.y) << 32) | v0.x, (static_cast<uint64_t>(v0.w) << 32) | v0.z,
-                           (static_cast<uint64_t>(v1.y) << 32) | v1.x, (static_cast<uint64_t>(v1.w) << 32) | v1.z,
-                           (static_cast<uint64_t>(v2.y) << 32) | v2.x, (static_cast<uint64_t>(v2.w) << 32) | v2.z,
-                           (static_cast<uint64_t>(v3.y) << 32) | v3.x, (static_cast<uint64_t>(v3.w) << 32) | v3.z};
-    float ub[8];
-#pragma unroll
-    for (int j = 0; j < 8; ++j) ub[j] = row_ub(Wf, r[j]);
-    const double floor = best.s > 0.0 ? best.s : 4.9406564584124654e-324;
+    const float ub[8] = {ub2(Wf, v0.x, v0.y), ub2(Wf, v0.z, v0.w), ub2(Wf, v1.x, v1.y), ub2(Wf, v1.z, v1.w),
+                         ub2(Wf, v2.x, v2.y), ub2(Wf, v2.z, v2.w), ub2(Wf, v3.x, v3.y), ub2(Wf, v3.z, v3.w)};
+    // FP32 floor rounded DOWN: ub >= best.s implies ub >= ff, so no row that can win or tie
+    // is skipped; with no best yet, ff = the smallest positive float (rows must score > 0)
+    const float ff = best.s > 0.0 ? __double2float_rd(best.s) : 1.40129846e-45f;
     bool hit = false;
 #pragma unroll
-    for (int j = 0; j < 8; ++j) hit |= static_cast<double>(ub[j]) >= floor;
+    for (int j = 0; j < 8; ++j) hit |= ub[j] >= ff;
     if (hit) {
+        const uint64_t r[8] = {(static_cast<uint64_t>(v0.y) << 32) | v0.x, (static_cast<uint64_t>(v0.w) << 32) | v0.z,
+                               (static_cast<uint64_t>(v1.y) << 32) | v1.x, (static_cast<uint64_t>(v1.w) << 32) | v1.z,
+                               (static_cast<uint64_t>(v2.y) << 32) | v2.x, (static_cast<uint64_t>(v2.w) << 32) | v2.z,
+                               (static_cast<uint64_t>(v3.y) << 32) | v3.x, (static_cast<uint64_t>(v3.w) << 32) | v3.z};
 #pragma unroll
         for (int j = 0; j < 8; ++j)
             if (static_cast<double>(ub[j]) >= (best.s > 0.0 ? best.s : 4.9406564584124654e-324))
@@ -682,8 +693,8 @@ __global__ void __launch_bounds__(kThreads, 1) greedy_kernel(const __grid_consta
                                      : "memory");
                 }
                 // rows appended during this launch: L2-coherent loads (never the non-coherent path)
-                const uint4 v0 = ld_row4(rows4 + u, a.load_mode), v1 = ld_row4(rows4 + u + GT, a.load_mode),
-                            v2 = ld_row4(rows4 + u + 2 * GT, a.load_mode), v3 = ld_row4(rows4 + u + 3 * GT, a.load_mode);
+                const uint4 v0 = ld_row4(rows4 + u, LOADM), v1 = ld_row4(rows4 + u + GT, LOADM),
+                            v2 = ld_row4(rows4 + u + 2 * GT, LOADM), v3 = ld_row4(rows4 + u + 3 * GT, LOADM);
                 consider8(M, W, Wf, U, v0, v1, v2, v3, best);
             }
             for (; u < NU; u += GT) consider2(M, W, U, __ldcg(rows4 + u), best);
