@@ -132,6 +132,7 @@ struct Topk1Args {
     unsigned* ticket;   // zero before launch; reset by the last CTA
     uint64_t* out_row;  // k (host-mapped)
     int* n_out;         // host-mapped
+    unsigned long long* n_scored;  // host-mapped: rows passing the service mask (zeroed by the host)
     uint64_t svc_mask[4];
     double comp[256];
 };

@@ -75,6 +75,7 @@ struct HostIO {
     double comp[256];      // completion vector input
     uint64_t mask[4];      // top-K service filter
     uint64_t top_rows[1024];
+    unsigned long long n_scored;  // top-K: rows passing the service mask
 };
 
 struct Slot {
@@ -662,6 +663,8 @@ std::vector<long long> Engine::topk(const std::vector<double>& comp, int k, cons
         a.ticket = s->ticket;
         a.out_row = s->io->top_rows;
         a.n_out = &s->io->top_n;
+        a.n_scored = &s->io->n_scored;
+        s->io->n_scored = 0;
         const int G = static_cast<int>(std::max<long long>(g1, 1));
         a.rows_per_cta = (total + G - 1) / G;
         void* args[] = {&a};
@@ -714,7 +717,22 @@ std::vector<long long> Engine::topk(const std::vector<double>& comp, int k, cons
     float ms = 0.f;
     CK(cudaEventElapsedTime(&ms, s->e0, s->e1));
     stats.topk_ns += static_cast<long long>(ms * 1e6f);
-    stats.topk_rows += total;
+    // rows scored (mcts.hpp:59-67): the candidate list, or for expand's service filter the
+    // rows touching a sampled service (the union of by_service lists, mcts.hpp:98-107)
+    long long scored = total;
+    if (svc_mask && single) {
+        scored = static_cast<long long>(s->io->n_scored);
+    } else if (svc_mask) {  // exact k-round fallback: count the filtered set on the host
+        scored = 0;
+        for (uint64_t row : base_rows_) {
+            int svc[kRowK], pat[kRowK];
+            const int k2 = m_.members(row, svc, pat);
+            bool hit = false;
+            for (int j = 0; j < k2; ++j) hit |= (((*svc_mask)[svc[j] >> 6] >> (svc[j] & 63)) & 1ull) != 0;
+            scored += hit;
+        }
+    }
+    stats.topk_rows += scored;
     stats.topk_calls++;
     stats.h2d += static_cast<long long>(sizeof(double) * m_.n + (index ? sizeof(long long) * total : 0) +
                                         (svc_mask ? 32 : 0));

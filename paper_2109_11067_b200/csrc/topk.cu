@@ -67,6 +67,7 @@ __global__ void __launch_bounds__(kTopkThreads, 1) topk1_kernel(const __grid_con
     const long long total = a.index ? a.n_index : a.n_rows;
     const long long lo = static_cast<long long>(blockIdx.x) * a.rows_per_cta;
     const long long hi = min(total, lo + a.rows_per_cta);
+    int scored = 0;  // candidates actually scored (a service-mask filter defines the set)
     auto score_at = [&](long long i, uint64_t& row) -> double {
         row = __ldg(a.rows + (a.index ? __ldg(a.index + i) : i));
         if (a.use_mask) {
@@ -85,6 +86,19 @@ __global__ void __launch_bounds__(kTopkThreads, 1) topk1_kernel(const __grid_con
     for (long long i = lo + threadIdx.x; i < hi; i += blockDim.x) {
         uint64_t row;
         tmax = fmax(tmax, score_at(i, row));
+        if (a.use_mask) {
+            bool hit = false;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const int svc = static_cast<int>(((row >> (16 * j)) & 0xFFFFull) / M.PP);
+                if (svc < M.n) hit |= ((a.svc_mask[svc >> 6] >> (svc & 63)) & 1ull) != 0;
+            }
+            scored += hit;
+        }
+    }
+    if (a.use_mask) {  // expand's candidate set = rows touching a sampled service (mcts.hpp:98-107)
+        for (int off = 16; off > 0; off >>= 1) scored += __shfl_xor_sync(0xffffffffu, scored, off);
+        if ((threadIdx.x & 31u) == 0 && scored) atomicAdd(a.n_scored, static_cast<unsigned long long>(scored));
     }
     // 2. threshold: the largest per-warp K-th lane maximum (non-negative doubles order as
     //    their bit patterns, so an integer atomicMax on the bits is a max on the values)

@@ -231,3 +231,27 @@ def test_mutation_cases(impl):  # test_ga.cpp:57-108
         for _ in range(50):
             par = mp.mutate(par, mp.GaParams(), rng, ctx2)
             assert mp.completion_of(par.gpus, sv2, ps2) == before  # bitwise
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("kind", ["mcts", "ga"])
+def test_rows_scored_counts_match_checker(kind):
+    """The BASELINE metric's work count ("configs scored") is implementation-independent:
+    the product and the CPU checker count identical rows for the same MCTS / GA call."""
+    chk = S.oracle_backend()
+    if chk is None:
+        pytest.skip("oracle not built")
+    ps = S.profiles()
+    sv = S.fixture_services("slos_day", ps)
+    counts = []
+    for b in (S.product_backend(), chk):
+        ctx = mp.make_plan_context(sv, ps, mp.PartitionRuleSet.defaults(), backend=b)
+        ctx.reset_stats()
+        if kind == "mcts":
+            mp.mcts_solve(mp.zero_completion(len(sv)), ctx, mp.MctsParams(budget_iters=200), 1)
+        else:
+            mp.two_phase(sv, ps, mp.PartitionRuleSet.defaults(),
+                         mp.GaParams(seed=24, max_rounds=2, time_budget_s=1e9), ctx=ctx)
+        st = ctx.stats()
+        counts.append((st["greedy_rows"], st["topk_rows"], st["topk_calls"], st["greedy_steps"]))
+    assert counts[0] == counts[1]
