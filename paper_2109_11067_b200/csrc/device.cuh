@@ -169,6 +169,45 @@ struct GaFinishArgs {
     int L_cap;
 };
 
+// Device-resident parity mcts_solve (mcts.cu): one CTA per search.
+struct MctsSolveArgs {
+    const double* comp0;     // start completion (n, device)
+    uint64_t seed;           // mt19937_64 seed = mix_seed(seed, 0x6d637473) (mcts.hpp:157)
+    int l_ref;               // |fast_algo(comp0)|
+    int max_nodes;
+    double* node_comp;       // max_nodes * n
+    int* node_visits;
+    double* node_value;
+    int* node_first;
+    int* node_nch;
+    int* node_cand;          // base-pool index of the edge into the node
+    unsigned char* node_flags;
+    int* pathnodes;          // selection path (node ids)
+    int* edges;              // candidate ids along the path
+    int* picked;             // rollout picks
+    int* unsat;              // n
+    unsigned tab_mask;       // rollout cache (open addressing over the unsat bitmap)
+    unsigned* tag;
+    uint64_t* key;
+    int* pool_n;
+    unsigned* pool;          // (tab_mask + 1) * topk
+    int* trace;              // budget * 4: iter, depth, estimate, best_len (mcts.hpp:226)
+    int* best_out;           // best complete path (candidate ids)
+    int* descent_out;        // visit-count descent (candidate ids)
+    double* descent_comp;    // n: completion at the end of the descent
+    int* out;                // status, best_len, descent_len, descent_leaf, builds, nodes, iterations
+};
+
+struct MctsLaunch {
+    DevModel M;
+    const uint64_t* base;
+    long long n_base;
+    const double* logtab;    // std::log(v) for v = 0..budget (host-computed, bit-exact)
+    int budget, topk, pick_services;
+    double ucb_c;
+    MctsSolveArgs s[kMaxGroups];
+};
+
 // Throughput-mode root-parallel rollouts (rollout.cu).
 struct RolloutCounters {
     unsigned long long n_act[2];  // active-list lengths (ping-pong by round parity)

@@ -28,10 +28,20 @@ int topk1_max_ctas();
 constexpr int kTopkMaxCtas = 4096;  // partial-list capacity (Best x 32 per CTA)
 const void* topk1_kernel_ptr(int km);
 size_t rollout_smem_bytes(int n, int PP);
+size_t mcts_smem_bytes(int n, int PP);
+const void* mcts_kernel_ptr();
+int mcts_threads();
 const void* rollout_kernel_ptr();
 int rollout_threads();
 
 namespace {
+
+uint64_t mix_seed_u64(uint64_t a, uint64_t b) {  // util.hpp:30-35
+    uint64_t z = a + 0x9e3779b97f4a7c15ULL * (b + 1);
+    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+    z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+    return z ^ (z >> 31);
+}
 
 void ck(cudaError_t e, const char* what) {
     if (e != cudaSuccess) throw DeviceError(std::string(what) + ": " + cudaGetErrorString(e));
@@ -98,6 +108,12 @@ struct Slot {
     long long index_cap = 0;
     HostIO* io = nullptr;  // host-mapped
 
+    // device MCTS scratch (mcts.cu), grown on demand
+    void* mcts_mem = nullptr;
+    size_t mcts_bytes = 0;
+    double* logtab = nullptr;
+    int logtab_n = 0;
+
     uint64_t* d_pick_row = nullptr;  // device-side step records
     double* d_pick_score = nullptr;
     long long* d_pick_rows = nullptr;
@@ -118,7 +134,7 @@ struct Slot {
         cudaSetDevice(device);
         if (stream) cudaStreamSynchronize(stream);
         for (void* p : {(void*)ext, (void*)st, (void*)partials, (void*)ev_svc, (void*)bar, (void*)index,
-                        (void*)ticket, (void*)tpart})
+                        (void*)ticket, (void*)tpart, mcts_mem, (void*)logtab})
             if (p) cudaFree(p);
         free_picks();
         if (io) cudaFreeHost(io);
@@ -352,7 +368,8 @@ const DeviceInfo& device_info(int device) {
     info.smem_optin = static_cast<long long>(prop.sharedMemPerBlockOptin);
     // every kernel may use all the opt-in shared memory its static allocation leaves
     CK(cudaFuncSetAttribute(topk1_kernel_ptr(32), cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-    for (const void* k : {greedy_kernel_ptr(), topk_kernel_ptr(), topk1_kernel_ptr(32), rollout_kernel_ptr()}) {
+    for (const void* k : {greedy_kernel_ptr(), topk_kernel_ptr(), topk1_kernel_ptr(32), rollout_kernel_ptr(),
+                          mcts_kernel_ptr()}) {
         cudaFuncAttributes fa{};
         CK(cudaFuncGetAttributes(&fa, k));
         CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -977,6 +994,133 @@ void Engine::greedy_batch(const double* d_comps, int count, long long cap_steps,
             x.s = nullptr;
         }
     }
+}
+
+// ---- device-resident parity mcts_solve (mcts.cu)
+MctsDeviceResult Engine::mcts_device(const std::vector<double>& comp, int budget, int topk, int pick_services,
+                                     double ucb_c, uint64_t seed, int l_ref) {
+    if (topk < 1 || topk > 32) throw ArgumentError("mcts: topk must be in [1, 32] on the device path");
+    if (n_ranks_ > 1) throw ArgumentError("mcts on a sharded context");
+    const int n = m_.n;
+    const int max_depth = 2 * l_ref;
+    const long long max_nodes = 1 + static_cast<long long>(budget) * topk;
+    const long long path_cap = max_nodes + max_depth + 8;
+    long long want = std::max<long long>(1024, 2ll * budget * (max_depth + 1));
+    long long cap = 1;
+    while (cap < want) cap <<= 1;
+    Slot* s = acquire();
+    struct Rel {
+        Engine* e;
+        Slot* s;
+        ~Rel() { e->release(s); }
+    } rel{this, s};
+    CK(cudaSetDevice(device_));
+    // carve one buffer
+    size_t off = 0;
+    auto take = [&](size_t bytes) {
+        size_t at = (off + 15) & ~size_t{15};
+        off = at + bytes;
+        return at;
+    };
+    const size_t o_comp0 = take(sizeof(double) * n), o_ncomp = take(sizeof(double) * max_nodes * n),
+                 o_vis = take(sizeof(int) * max_nodes), o_val = take(sizeof(double) * max_nodes),
+                 o_first = take(sizeof(int) * max_nodes), o_nch = take(sizeof(int) * max_nodes),
+                 o_cand = take(sizeof(int) * max_nodes), o_flags = take(max_nodes),
+                 o_path = take(sizeof(int) * path_cap), o_edges = take(sizeof(int) * path_cap),
+                 o_picked = take(sizeof(int) * (max_depth + 8)), o_unsat = take(sizeof(int) * (n + 1)),
+                 o_tag = take(sizeof(unsigned) * cap), o_key = take(sizeof(uint64_t) * 4 * cap),
+                 o_pn = take(sizeof(int) * cap), o_pool = take(sizeof(unsigned) * topk * cap),
+                 o_trace = take(sizeof(int) * 4 * std::max(budget, 1)), o_best = take(sizeof(int) * path_cap),
+                 o_desc = take(sizeof(int) * path_cap), o_dcomp = take(sizeof(double) * n), o_out = take(sizeof(int) * 16);
+    if (s->mcts_bytes < off) {
+        if (s->mcts_mem) CK(cudaFree(s->mcts_mem));
+        s->mcts_mem = nullptr;
+        CK(cudaMalloc(&s->mcts_mem, off));
+        s->mcts_bytes = off;
+    }
+    if (s->logtab_n < budget + 2) {  // std::log(v), v = 0..budget+1 (the reference's own libm values)
+        if (s->logtab) CK(cudaFree(s->logtab));
+        std::vector<double> lt(budget + 2);
+        for (int v = 0; v < budget + 2; ++v) lt[v] = std::log(static_cast<double>(std::max(1, v)));
+        CK(cudaMalloc(&s->logtab, sizeof(double) * lt.size()));
+        CK(cudaMemcpy(s->logtab, lt.data(), sizeof(double) * lt.size(), cudaMemcpyHostToDevice));
+        s->logtab_n = static_cast<int>(lt.size());
+    }
+    unsigned char* b = static_cast<unsigned char*>(s->mcts_mem);
+    CK(cudaMemcpyAsync(b + o_comp0, comp.data(), sizeof(double) * n, cudaMemcpyHostToDevice, s->stream));
+    CK(cudaMemsetAsync(b + o_tag, 0, sizeof(unsigned) * cap, s->stream));
+    std::unique_ptr<MctsLaunch> L(new MctsLaunch{});
+    L->M = dm_;
+    L->base = d_base_;
+    L->n_base = pool_size();
+    L->logtab = s->logtab;
+    L->budget = budget;
+    L->topk = topk;
+    L->pick_services = pick_services;
+    L->ucb_c = ucb_c;
+    MctsSolveArgs& a = L->s[0];
+    a.comp0 = reinterpret_cast<const double*>(b + o_comp0);
+    a.seed = mix_seed_u64(seed, 0x6d637473);
+    a.l_ref = l_ref;
+    a.max_nodes = static_cast<int>(max_nodes);
+    a.node_comp = reinterpret_cast<double*>(b + o_ncomp);
+    a.node_visits = reinterpret_cast<int*>(b + o_vis);
+    a.node_value = reinterpret_cast<double*>(b + o_val);
+    a.node_first = reinterpret_cast<int*>(b + o_first);
+    a.node_nch = reinterpret_cast<int*>(b + o_nch);
+    a.node_cand = reinterpret_cast<int*>(b + o_cand);
+    a.node_flags = b + o_flags;
+    a.pathnodes = reinterpret_cast<int*>(b + o_path);
+    a.edges = reinterpret_cast<int*>(b + o_edges);
+    a.picked = reinterpret_cast<int*>(b + o_picked);
+    a.unsat = reinterpret_cast<int*>(b + o_unsat);
+    a.tab_mask = static_cast<unsigned>(cap - 1);
+    a.tag = reinterpret_cast<unsigned*>(b + o_tag);
+    a.key = reinterpret_cast<uint64_t*>(b + o_key);
+    a.pool_n = reinterpret_cast<int*>(b + o_pn);
+    a.pool = reinterpret_cast<unsigned*>(b + o_pool);
+    a.trace = reinterpret_cast<int*>(b + o_trace);
+    a.best_out = reinterpret_cast<int*>(b + o_best);
+    a.descent_out = reinterpret_cast<int*>(b + o_desc);
+    a.descent_comp = reinterpret_cast<double*>(b + o_dcomp);
+    a.out = reinterpret_cast<int*>(b + o_out);
+    void* args[] = {L.get()};
+    CK(cudaEventRecord(s->e0, s->stream));
+    CK(cudaLaunchKernel(mcts_kernel_ptr(), 1, mcts_threads(), args, mcts_smem_bytes(n, m_.PP), s->stream));
+    stats.launches++;
+    CK(cudaEventRecord(s->e1, s->stream));
+    int out[16];
+    CK(cudaMemcpyAsync(out, b + o_out, sizeof(out), cudaMemcpyDeviceToHost, s->stream));
+    CK(cudaStreamSynchronize(s->stream));
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, s->e0, s->e1));
+    MctsDeviceResult r;
+    r.status = out[0];
+    r.best_len = out[1];
+    r.descent_leaf = out[3] != 0;
+    r.builds = out[4];
+    r.iterations = out[6];
+    r.expands = out[7];
+    std::memcpy(&r.expand_rows, &out[8], sizeof(long long));
+    r.trace.resize(4 * static_cast<size_t>(r.iterations));
+    std::vector<int> best(std::max(r.best_len, 0)), desc(out[2]);
+    if (!r.trace.empty())
+        CK(cudaMemcpy(r.trace.data(), b + o_trace, sizeof(int) * r.trace.size(), cudaMemcpyDeviceToHost));
+    if (!best.empty()) CK(cudaMemcpy(best.data(), b + o_best, sizeof(int) * best.size(), cudaMemcpyDeviceToHost));
+    if (!desc.empty()) CK(cudaMemcpy(desc.data(), b + o_desc, sizeof(int) * desc.size(), cudaMemcpyDeviceToHost));
+    r.descent_comp.resize(n);
+    CK(cudaMemcpy(r.descent_comp.data(), b + o_dcomp, sizeof(double) * n, cudaMemcpyDeviceToHost));
+    r.best.assign(best.begin(), best.end());
+    r.descent.assign(desc.begin(), desc.end());
+    // work counters with the reference's definitions (mcts.hpp:59-67): every expansion
+    // scores its filtered set, every rollout-cache miss the whole base pool
+    stats.topk_calls += r.expands + r.builds;
+    stats.topk_rows += r.expand_rows + static_cast<long long>(r.builds) * pool_size();
+    stats.topk_ns += static_cast<long long>(ms * 1e6);
+    stats.h2d += static_cast<long long>(sizeof(double) * n);
+    stats.d2h += static_cast<long long>(sizeof(out) + sizeof(int) * (r.trace.size() + best.size() + desc.size()) +
+                                        sizeof(double) * n);
+    return r;
 }
 
 // ---- throughput-mode GA device state (ga.cu)

@@ -59,6 +59,20 @@ struct Stats {
     }
 };
 
+// Device-resident parity mcts_solve (mcts.cu): what the kernel returns to the host driver.
+struct MctsDeviceResult {
+    int status = 0;                  // 0 ok, 1 rollout found an empty pool (PlanningError), 2/3 capacity
+    int iterations = 0;
+    std::vector<int> trace;          // 4 per iteration: iter, depth, estimate, best_len
+    std::vector<long long> best;     // best complete path (base-pool indices); empty + best_len -1: none
+    int best_len = -1;
+    std::vector<long long> descent;  // visit-count descent
+    std::vector<double> descent_comp;
+    bool descent_leaf = false;
+    int builds = 0, expands = 0;
+    long long expand_rows = 0;
+};
+
 // Throughput-mode root-parallel rollouts (rollout.cu): the result of one mig_rollouts call.
 struct RolloutResult {
     int best_len = -1;        // shortest completed rollout (steps); -1: none completed
@@ -104,6 +118,10 @@ class Engine {
     // max_ctas > 0 caps this context's greedy grid (ranks sharing one GPU).
     void set_shard(int rank, int n_ranks, const std::vector<void*>& boards, int max_ctas);
     int n_ranks() const { return n_ranks_; }
+
+    // mcts_solve's search loop on the device (one CTA); l_ref = |fast_algo(comp)|.
+    MctsDeviceResult mcts_device(const std::vector<double>& comp, int budget, int topk, int pick_services, double ucb_c,
+                                 uint64_t seed, int l_ref);
 
     // Independent single-CTA greedy instances in one launch (the GA's refills).
     void greedy_batch(const double* d_comps, int count, long long cap_steps, std::vector<const uint64_t*>& rows,

@@ -1,0 +1,494 @@
+// mcts.cu — K7: device-resident parity-mode mcts_solve (mcts.hpp:148-252).
+//
+// One CTA runs one whole search: UCB1 selection (strict >, first unvisited child), expansion
+// (partial Fisher-Yates over the unsatisfied services, top-K of the base rows touching a
+// sampled service), the random child, the memoized rollout (RolloutCache keyed by the
+// unsatisfied bitmap, top-K of the whole base pool on a miss), backpropagation, and the final
+// visit-count descent — with the reference's std::mt19937_64 stream reproduced on the device
+// (thread 0), so under a matched seed the tree, every trace line and the answer are the
+// reference's.  The host runs the two fast_algo calls around it (fast_ref before, the
+// descent completion after) on the greedy kernel, and replays the trace.
+// Every top-K is one block-wide pass: FP32 round-up bounds (Wf) filter the rows, exact FP64
+// scores only where a bound reaches the thread's running best, threshold from the per-warp
+// K-th best exact maxima, parallel rank of the survivors (common.cuh).
+// log(visits) comes from a host table (std::log), so the UCB arithmetic is bit-exact; the
+// divisions, sqrt and adds are correctly rounded on both sides (no FMA).
+#include "common.cuh"
+
+namespace mgb {
+
+using namespace dev;
+
+namespace {
+
+constexpr int kMThreads = 512;
+constexpr int kMWarps = kMThreads / 32;
+constexpr int kMCandCap = 2048;
+constexpr int kMMaxK = 32;
+constexpr unsigned char kExpanded = 1, kLeaf = 2;
+
+struct Mt64 {  // std::mt19937_64 (w 64, n 312, m 156, r 31)
+    uint64_t mt[312];
+    int idx;
+};
+
+__device__ void mt_seed(Mt64& g, uint64_t s) {
+    g.mt[0] = s;
+    for (int i = 1; i < 312; ++i) g.mt[i] = 6364136223846793005ull * (g.mt[i - 1] ^ (g.mt[i - 1] >> 62)) + static_cast<uint64_t>(i);
+    g.idx = 312;
+}
+
+__device__ uint64_t mt_next(Mt64& g) {
+    if (g.idx >= 312) {
+        for (int i = 0; i < 312; ++i) {
+            const uint64_t x = (g.mt[i] & 0xFFFFFFFF80000000ull) | (g.mt[(i + 1) % 312] & 0x7FFFFFFFull);
+            uint64_t xa = x >> 1;
+            if (x & 1ull) xa ^= 0xB5026F5AA96619E9ull;
+            g.mt[i] = g.mt[(i + 156) % 312] ^ xa;
+        }
+        g.idx = 0;
+    }
+    uint64_t y = g.mt[g.idx++];
+    y ^= (y >> 29) & 0x5555555555555555ull;
+    y ^= (y << 17) & 0x71D67FFFEDA60000ull;
+    y ^= (y << 37) & 0xFFF7EEE000000000ull;
+    y ^= y >> 43;
+    return y;
+}
+
+__device__ uint64_t mt_pick(Mt64& g, uint64_t n) {  // pick_index, util.hpp:39-47
+    if (n <= 1) return 0;
+    const uint64_t limit = ~0ull - (~0ull % n);
+    uint64_t r;
+    do {
+        r = mt_next(g);
+    } while (r >= limit);
+    return r % n;
+}
+
+// row touches a masked service: per-code flags built with the W table (4 byte lookups)
+__device__ __forceinline__ bool row_hits(const unsigned char* hitc, uint64_t row) {
+    return (hitc[row & 0xFFFFull] | hitc[(row >> 16) & 0xFFFFull] | hitc[(row >> 32) & 0xFFFFull] |
+            hitc[row >> 48]) != 0;
+}
+
+__device__ __forceinline__ float ub_row(const float* Wf, uint64_t row) {
+    float s = __fadd_ru(Wf[row & 0xFFFFull], Wf[(row >> 16) & 0xFFFFull]);
+    s = __fadd_ru(s, Wf[(row >> 32) & 0xFFFFull]);
+    return __fadd_ru(s, Wf[row >> 48]);
+}
+
+// detail::topk_candidates (mcts.hpp:56-76) over the base rows (mask: rows touching a masked
+// service, else all), block-wide.  Writes base-pool indices in preference order to out[],
+// returns their count.  Ends with a barrier.
+__device__ int block_topk_exact(const DevModel& M, const uint64_t* base, long long nb, const double* comp,
+                                const uint64_t* mask, int k, double* W, float* Wf, unsigned char* hitc, Cand* cand,
+                                Cand* win, int* out, int* scored) {
+    __shared__ unsigned long long t_bits;
+    __shared__ int n_cand, n_hit;
+    __shared__ Cand red[kMWarps];
+    const int nW = (M.n + 1) * M.PP;
+    for (int e = threadIdx.x; e < nW; e += blockDim.x) {
+        const int svc = e / M.PP;
+        double w = 0.0;
+        if (svc < M.n) {
+            const double need = __dadd_rn(1.0, -comp[svc]);
+            if (need > 0.0) w = __dmul_rn(need, __ldg(&M.U[e]));
+        }
+        W[e] = w;
+        Wf[e] = __double2float_ru(w);
+        if (mask) hitc[e] = svc < M.n && ((mask[svc >> 6] >> (svc & 63)) & 1ull) != 0;
+    }
+    if (threadIdx.x == 0) {
+        t_bits = 0ull;
+        n_cand = 0;
+        n_hit = 0;
+    }
+    __syncthreads();
+    // pass 1: the thread's exact maximum; exact scores only where the FP32 bound reaches it.
+    // With a mask, the candidate set is the rows touching a sampled service (its size is the
+    // work count of the call, mcts.hpp:98-107).
+    double tmax = 0.0;
+    int hits = 0;
+    for (long long i = threadIdx.x; i < nb; i += blockDim.x) {
+        const uint64_t row = __ldg(base + i);
+        if (mask) {
+            if (!row_hits(hitc, row)) continue;
+            ++hits;
+        }
+        const float ub = ub_row(Wf, row);
+        if (!(ub > 0.0f) || static_cast<double>(ub) < tmax) continue;
+        tmax = fmax(tmax, row_score(W, row));
+    }
+    if (mask) {
+        for (int off = 16; off > 0; off >>= 1) hits += __shfl_xor_sync(0xffffffffu, hits, off);
+        if ((threadIdx.x & 31u) == 0) atomicAdd(&n_hit, hits);
+    }
+    const double tw = warp_kth(tmax, k);
+    if ((threadIdx.x & 31u) == 0) atomicMax(&t_bits, static_cast<unsigned long long>(__double_as_longlong(tw)));
+    __syncthreads();
+    const double T = __longlong_as_double(static_cast<long long>(t_bits));
+    // pass 2: rows whose exact score reaches T (at least k of them exist)
+    for (long long i0 = 0; i0 < nb; i0 += blockDim.x) {
+        const long long i = i0 + threadIdx.x;
+        bool take = false;
+        double s = 0.0;
+        uint64_t row = 0;
+        if (i < nb) {
+            row = __ldg(base + i);
+            const float ub = ub_row(Wf, row);
+            if (ub > 0.0f && static_cast<double>(ub) >= T && (!mask || row_hits(hitc, row))) {
+                s = row_score(W, row);
+                take = s > 0.0 && s >= T;
+            }
+        }
+        const unsigned b = __ballot_sync(0xffffffffu, take);
+        if (b) {
+            int at = 0;
+            if ((threadIdx.x & 31u) == 0) at = atomicAdd(&n_cand, __popc(b));
+            at = __shfl_sync(0xffffffffu, at, 0) + __popc(b & lanemask_lt());
+            if (take && at < kMCandCap) cand[at] = Cand{s, row_usum(M.U, row), row, i};
+        }
+    }
+    __syncthreads();
+    const int nc = n_cand;
+    int got;
+    if (nc <= kMCandCap) {
+        got = min(nc, k);
+        rank_select(M, cand, nc, k, win);
+    } else {  // pathological ties at T: exact k rounds of "best row strictly after the previous"
+        got = 0;
+        Cand last{0.0, 0.0, kNoRow, -1};
+        for (int r = 0; r < k; ++r) {
+            Cand b{0.0, 0.0, kNoRow, -1};
+            for (long long i = threadIdx.x; i < nb; i += blockDim.x) {
+                const uint64_t row = __ldg(base + i);
+                if (mask && !row_hits(hitc, row)) continue;
+                const double s = row_score(W, row);
+                if (!(s > 0.0)) continue;
+                const Cand c{s, row_usum(M.U, row), row, i};
+                if (r > 0 && !precedes(M, last, c)) continue;
+                if (b.row == kNoRow || precedes(M, c, b)) b = c;
+            }
+            for (int off = 16; off > 0; off >>= 1) {
+                const Cand o{__shfl_xor_sync(0xffffffffu, b.s, off), __shfl_xor_sync(0xffffffffu, b.u, off),
+                             __shfl_xor_sync(0xffffffffu, b.row, off), __shfl_xor_sync(0xffffffffu, b.pos, off)};
+                if (o.row != kNoRow && (b.row == kNoRow || precedes(M, o, b))) b = o;
+            }
+            if ((threadIdx.x & 31u) == 0) red[threadIdx.x >> 5] = b;
+            __syncthreads();
+            Cand x = red[0];
+            for (int w = 1; w < kMWarps; ++w)
+                if (red[w].row != kNoRow && (x.row == kNoRow || precedes(M, red[w], x))) x = red[w];
+            __syncthreads();
+            if (x.row == kNoRow) break;
+            if (threadIdx.x == 0) win[r] = x;
+            last = x;
+            ++got;
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x < got) out[threadIdx.x] = static_cast<int>(win[threadIdx.x].pos);
+    if (threadIdx.x == 0) *scored = mask ? n_hit : static_cast<int>(nb);
+    __syncthreads();
+    return got;
+}
+
+__device__ __forceinline__ bool comp_satisfied(const double* c, int n) {  // core.hpp:217-221
+    for (int i = 0; i < n; ++i)
+        if (c[i] < 1.0 - 1e-9) return false;
+    return true;
+}
+
+__device__ __forceinline__ void add_row_util(const DevModel& M, uint64_t row, double* c) {  // rollout / expand add
+    for (int j = 0; j < 4; ++j) {
+        const int code = static_cast<int>((row >> (16 * j)) & 0xFFFFull);
+        const int svc = code / M.PP;
+        if (svc < M.n) c[svc] = __dadd_rn(c[svc], __ldg(&M.U[code]));
+    }
+}
+
+}  // namespace
+
+__global__ void __launch_bounds__(kMThreads, 1) mcts_kernel(const __grid_constant__ MctsLaunch L) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const MctsSolveArgs& a = L.s[blockIdx.x];
+    const DevModel& M = L.M;
+    const int n = M.n, K = L.topk;
+    const int nW = (n + 1) * M.PP;
+    double* W = reinterpret_cast<double*>(smem);
+    double* cur = W + nW;                                     // n (+1)
+    Cand* cand = reinterpret_cast<Cand*>(cur + n + 1);        // kMCandCap
+    Cand* win = cand + kMCandCap;                             // kMMaxK
+    float* Wf = reinterpret_cast<float*>(win + kMMaxK);       // nW
+    unsigned char* hitc = reinterpret_cast<unsigned char*>(Wf + nW);  // nW
+    __shared__ Mt64 g;
+    __shared__ int s_node, s_leaf, s_expand, s_take, s_nch, s_done, s_est, s_miss, s_slot, s_abort, s_steps;
+    __shared__ int s_edges, s_path, s_best, s_have, s_nodes, s_builds, s_iters, s_scored, s_expands;
+    __shared__ long long s_expand_rows;
+    __shared__ uint64_t s_mask[4];
+    __shared__ int s_out[kMMaxK];
+    const int max_depth = 2 * a.l_ref;
+    const int tid = threadIdx.x;
+
+    // root (mcts.hpp:157-160)
+    if (tid == 0) {
+        mt_seed(g, a.seed);
+        s_nodes = 1;
+        s_have = 0;
+        s_best = 0;
+        s_abort = 0;
+        s_builds = 0;
+        s_iters = 0;
+        s_expands = 0;
+        s_expand_rows = 0;
+        a.node_visits[0] = 0;
+        a.node_value[0] = 0.0;
+        a.node_nch[0] = 0;
+        a.node_first[0] = 0;
+        a.node_cand[0] = -1;
+    }
+    for (int i = tid; i < n; i += blockDim.x) a.node_comp[i] = a.comp0[i];
+    __syncthreads();
+    if (tid == 0) a.node_flags[0] = comp_satisfied(a.node_comp, n) ? kLeaf : 0;
+    __syncthreads();
+
+    for (int iter = 0; iter < L.budget && !s_abort; ++iter) {
+        // ---- selection (mcts.hpp:183-191): UCB1, first unvisited child, strict >
+        if (tid == 0) {
+            int node = 0;
+            s_edges = 0;
+            a.pathnodes[0] = 0;
+            s_path = 1;
+            while ((a.node_flags[node] & kExpanded) && !(a.node_flags[node] & kLeaf) && a.node_nch[node] > 0) {
+                const double log_n = L.logtab[max(1, a.node_visits[node])];
+                int pick = -1;
+                double best = -1.0;
+                for (int q = 0; q < a.node_nch[node]; ++q) {
+                    const int c = a.node_first[node] + q;
+                    const int v = a.node_visits[c];
+                    if (v == 0) {
+                        pick = q;
+                        break;
+                    }
+                    const double dv = static_cast<double>(v);
+                    const double val = __dadd_rn(__ddiv_rn(a.node_value[c], dv),
+                                                 __dmul_rn(L.ucb_c, __dsqrt_rn(__ddiv_rn(log_n, dv))));
+                    if (val > best) {
+                        best = val;
+                        pick = q;
+                    }
+                }
+                node = a.node_first[node] + pick;
+                a.edges[s_edges++] = a.node_cand[node];
+                a.pathnodes[s_path++] = node;
+            }
+            s_node = node;
+            s_leaf = (a.node_flags[node] & kLeaf) != 0;
+            s_expand = !s_leaf && !(a.node_flags[node] & kExpanded);
+            s_est = 0;
+        }
+        __syncthreads();
+        if (s_leaf) {  // mcts.hpp:193-198
+            if (tid == 0 && (!s_have || s_edges < s_best)) {
+                for (int q = 0; q < s_edges; ++q) a.best_out[q] = a.edges[q];
+                s_best = s_edges;
+                s_have = 1;
+            }
+        } else {
+            if (s_expand) {  // expand (mcts.hpp:89-116)
+                if (tid == 0) {
+                    const double* nc = a.node_comp + static_cast<long long>(s_node) * n;
+                    int m = 0;
+                    for (int i = 0; i < n; ++i)
+                        if (nc[i] < 1.0 - 1e-9) a.unsat[m++] = i;
+                    const int take = min(L.pick_services, m);
+                    for (int i = 0; i < take; ++i) {
+                        const int j = i + static_cast<int>(mt_pick(g, static_cast<uint64_t>(m - i)));
+                        const int t = a.unsat[i];
+                        a.unsat[i] = a.unsat[j];
+                        a.unsat[j] = t;
+                    }
+                    for (int w = 0; w < 4; ++w) s_mask[w] = 0;
+                    for (int i = 0; i < take; ++i) s_mask[a.unsat[i] >> 6] |= 1ull << (a.unsat[i] & 63);
+                    s_take = take;
+                }
+                for (int i = tid; i < n; i += blockDim.x) cur[i] = a.node_comp[static_cast<long long>(s_node) * n + i];
+                __syncthreads();
+                const int got = s_take > 0 ? block_topk_exact(M, L.base, L.n_base, cur, s_mask, K, W, Wf, hitc, cand,
+                                                              win, s_out, &s_scored)
+                                           : 0;
+                if (tid == 0 && s_take > 0) {
+                    ++s_expands;
+                    s_expand_rows += s_scored;
+                }
+                if (tid == 0) {
+                    if (s_nodes + got > a.max_nodes) {
+                        s_abort = 3;  // node storage exhausted (host sizes it from the budget)
+                    } else {
+                        const int first = s_nodes;
+                        for (int q = 0; q < got; ++q) {
+                            const int c = first + q;
+                            double* cc = a.node_comp + static_cast<long long>(c) * n;
+                            for (int i = 0; i < n; ++i) cc[i] = cur[i];
+                            add_row_util(M, __ldg(L.base + s_out[q]), cc);
+                            a.node_cand[c] = s_out[q];
+                            a.node_visits[c] = 0;
+                            a.node_value[c] = 0.0;
+                            a.node_nch[c] = 0;
+                            a.node_first[c] = 0;
+                            a.node_flags[c] = comp_satisfied(cc, n) ? kLeaf : 0;
+                        }
+                        a.node_first[s_node] = first;
+                        a.node_nch[s_node] = got;
+                        a.node_flags[s_node] |= kExpanded;
+                        s_nodes += got;
+                    }
+                }
+                __syncthreads();
+                if (s_abort) break;
+            }
+            // random child (mcts.hpp:202-207)
+            if (tid == 0) {
+                const int nch = a.node_nch[s_node];
+                if (nch > 0) {
+                    const int c = a.node_first[s_node] + static_cast<int>(mt_pick(g, static_cast<uint64_t>(nch)));
+                    a.edges[s_edges++] = a.node_cand[c];
+                    a.pathnodes[s_path++] = c;
+                    s_node = c;
+                }
+                s_steps = 0;
+            }
+            __syncthreads();
+            for (int i = tid; i < n; i += blockDim.x) cur[i] = a.node_comp[static_cast<long long>(s_node) * n + i];
+            __syncthreads();
+            // rollout (mcts.hpp:122-143) with the RolloutCache keyed by the unsatisfied bitmap
+            for (;;) {
+                if (tid == 0) {
+                    s_done = 0;
+                    s_miss = 0;
+                    if (comp_satisfied(cur, n)) {
+                        s_done = 1;
+                        s_est = s_steps;
+                    } else if (s_steps >= max_depth) {
+                        s_done = 1;
+                        s_est = max_depth;
+                    } else {
+                        uint64_t kw[4] = {0, 0, 0, 0};
+                        for (int i = 0; i < n; ++i)
+                            if (cur[i] < 1.0 - 1e-9) kw[i >> 6] |= 1ull << (i & 63);
+                        uint64_t h = 0x9e3779b97f4a7c15ull;
+                        for (int w = 0; w < 4; ++w) {
+                            h ^= kw[w];
+                            h *= 0xbf58476d1ce4e5b9ull;
+                            h ^= h >> 31;
+                        }
+                        unsigned sl = static_cast<unsigned>(h) & a.tab_mask;
+                        for (unsigned t = 0;; ++t, sl = (sl + 1) & a.tab_mask) {
+                            if (t > a.tab_mask) {
+                                s_abort = 2;  // cache full
+                                break;
+                            }
+                            if (!a.tag[sl]) {  // miss: insert, pool built below
+                                a.tag[sl] = 1;
+                                for (int w = 0; w < 4; ++w) a.key[4ull * sl + w] = kw[w];
+                                s_miss = 1;
+                                break;
+                            }
+                            if (a.key[4ull * sl] == kw[0] && a.key[4ull * sl + 1] == kw[1] &&
+                                a.key[4ull * sl + 2] == kw[2] && a.key[4ull * sl + 3] == kw[3])
+                                break;
+                        }
+                        s_slot = static_cast<int>(sl);
+                    }
+                }
+                __syncthreads();
+                if (s_done || s_abort) break;
+                if (s_miss) {  // cache miss: top-K of the whole base pool (mcts.hpp:129-133)
+                    const int got = block_topk_exact(M, L.base, L.n_base, cur, nullptr, K, W, Wf, hitc, cand, win, s_out,
+                                                     &s_scored);
+                    if (tid < got) a.pool[static_cast<long long>(s_slot) * K + tid] = static_cast<unsigned>(s_out[tid]);
+                    if (tid == 0) {
+                        a.pool_n[s_slot] = got;
+                        ++s_builds;
+                    }
+                    __syncthreads();
+                }
+                if (tid == 0) {
+                    const int pn = a.pool_n[s_slot];
+                    if (pn <= 0) {
+                        s_abort = 1;  // "rollout: no candidate config serves the remaining demand"
+                    } else {
+                        const int idx = static_cast<int>(a.pool[static_cast<long long>(s_slot) * K +
+                                                                mt_pick(g, static_cast<uint64_t>(pn))]);
+                        add_row_util(M, __ldg(L.base + idx), cur);
+                        a.picked[s_steps++] = idx;
+                    }
+                }
+                __syncthreads();
+                if (s_abort) break;
+            }
+            if (s_abort) break;
+            if (tid == 0) {  // mcts.hpp:210-218
+                const bool complete = (a.node_flags[s_node] & kLeaf) || s_steps == s_est;
+                if (complete && s_est < max_depth) {
+                    const int len = s_edges + s_steps;
+                    if (!s_have || len < s_best) {
+                        for (int q = 0; q < s_edges; ++q) a.best_out[q] = a.edges[q];
+                        for (int q = 0; q < s_steps; ++q) a.best_out[s_edges + q] = a.picked[q];
+                        s_best = len;
+                        s_have = 1;
+                    }
+                }
+            }
+        }
+        if (tid == 0) {  // backpropagation + trace (mcts.hpp:220-226)
+            const int total = s_edges + s_est;
+            const double reward = total > 0 ? fmin(1.0, __ddiv_rn(static_cast<double>(a.l_ref), static_cast<double>(total)))
+                                            : 1.0;
+            for (int q = 0; q < s_path; ++q) {
+                const int nd = a.pathnodes[q];
+                a.node_visits[nd] += 1;
+                a.node_value[nd] = __dadd_rn(a.node_value[nd], reward);
+            }
+            a.trace[4 * iter + 0] = iter;
+            a.trace[4 * iter + 1] = s_edges;
+            a.trace[4 * iter + 2] = s_est;
+            a.trace[4 * iter + 3] = s_have ? s_best : -1;
+            s_iters = iter + 1;
+        }
+        __syncthreads();
+    }
+    // visit-count descent (mcts.hpp:230-238); the host completes it with fast_algo
+    if (tid == 0) {
+        int node = 0, dl = 0;
+        if (!s_abort)
+            while ((a.node_flags[node] & kExpanded) && !(a.node_flags[node] & kLeaf) && a.node_nch[node] > 0) {
+                int pick = 0;
+                for (int q = 1; q < a.node_nch[node]; ++q)
+                    if (a.node_visits[a.node_first[node] + q] > a.node_visits[a.node_first[node] + pick]) pick = q;
+                node = a.node_first[node] + pick;
+                a.descent_out[dl++] = a.node_cand[node];
+            }
+        for (int i = 0; i < n; ++i) a.descent_comp[i] = a.node_comp[static_cast<long long>(node) * n + i];
+        a.out[0] = s_abort;
+        a.out[1] = s_have ? s_best : -1;
+        a.out[2] = dl;
+        a.out[3] = (a.node_flags[node] & kLeaf) ? 1 : 0;
+        a.out[4] = s_builds;
+        a.out[5] = s_nodes;
+        a.out[6] = s_iters;
+        a.out[7] = s_expands;
+        reinterpret_cast<long long*>(a.out)[4] = s_expand_rows;  // out[8..9]
+    }
+}
+
+size_t mcts_smem_bytes(int n, int PP) {
+    const size_t nW = static_cast<size_t>(n + 1) * PP;
+    return nW * 8 + static_cast<size_t>(n + 1) * 8 + static_cast<size_t>(kMCandCap + kMMaxK) * sizeof(Cand) + nW * 4 +
+           nW + 16;
+}
+const void* mcts_kernel_ptr() { return reinterpret_cast<const void*>(&mcts_kernel); }
+int mcts_threads() { return kMThreads; }
+
+}  // namespace mgb

@@ -110,12 +110,43 @@ int rollout(Engine& e, const std::vector<double>& comp, const MctsParams& p, Rol
     return steps;
 }
 
-// mcts_solve, mcts.hpp:148-252.
+// mcts_solve, mcts.hpp:148-252: fast_ref and the descent completion on the greedy kernel, the
+// search loop itself device-resident (mcts.cu: one CTA, the reference's mt19937_64 stream on
+// the device).  MIGPLAN_HOST_MCTS=1 selects the host-driven loop below (every top-K a launch).
+std::vector<Config> mcts_solve_host(Engine& e, const std::vector<double>& comp, const MctsParams& p, uint64_t seed,
+                                    const std::function<void(int, int, int, int)>& trace,
+                                    std::vector<Config> fast_ref);
+
 std::vector<Config> mcts_solve(Engine& e, const std::vector<double>& comp, const MctsParams& p, uint64_t seed,
                                const std::function<void(int, int, int, int)>& trace) {
     if (satisfied(comp)) return {};
     std::vector<Config> fast_ref = fast_plan(e, comp);
     if (p.budget_iters <= 0) return fast_ref;
+    static const bool host_loop = std::getenv("MIGPLAN_HOST_MCTS") != nullptr;
+    if (host_loop || p.topk < 1 || p.topk > 32) return mcts_solve_host(e, comp, p, seed, trace, std::move(fast_ref));
+    const int l_ref = static_cast<int>(fast_ref.size());
+    MctsDeviceResult r = e.mcts_device(comp, p.budget_iters, p.topk, p.pick_services, p.ucb_c, seed, l_ref);
+    if (trace)
+        for (int i = 0; i < r.iterations; ++i)
+            trace(r.trace[4 * i], r.trace[4 * i + 1], r.trace[4 * i + 2], r.trace[4 * i + 3]);
+    if (r.status == 1) throw PlanningError("rollout: no candidate config serves the remaining demand");
+    if (r.status != 0) throw DeviceError("mcts: device search storage exhausted");
+    std::vector<Config> via_descent;
+    for (long long idx : r.descent) via_descent.push_back(e.config_of(e.base_rows()[idx]));
+    if (!r.descent_leaf)
+        for (auto& c : fast_plan(e, r.descent_comp)) via_descent.push_back(c);
+    std::vector<Config> answer = std::move(fast_ref);
+    if (via_descent.size() < answer.size()) answer = std::move(via_descent);
+    if (r.best_len >= 0 && static_cast<size_t>(r.best_len) < answer.size()) {
+        answer.clear();
+        for (long long idx : r.best) answer.push_back(e.config_of(e.base_rows()[idx]));
+    }
+    return answer;
+}
+
+std::vector<Config> mcts_solve_host(Engine& e, const std::vector<double>& comp, const MctsParams& p, uint64_t seed,
+                                    const std::function<void(int, int, int, int)>& trace,
+                                    std::vector<Config> fast_ref) {
 
     const int l_ref = static_cast<int>(fast_ref.size());
     const int max_depth = 2 * l_ref;

@@ -45,11 +45,12 @@ __global__ void __launch_bounds__(kTopkThreads, 1) topk1_kernel(const __grid_con
     Cand* cand = reinterpret_cast<Cand*>(W + nW + 1);  // [kCandCap]
     Cand* win = cand + kCandCap;                        // [kTopkMaxK]
     __shared__ unsigned long long t_bits;
-    __shared__ int n_cand, n_got;
+    __shared__ int n_cand, n_got, cta_scored;
     const int k = a.k;
     if (threadIdx.x == 0) {
         t_bits = 0ull;
         n_cand = 0;
+        cta_scored = 0;
     }
     for (int e = threadIdx.x; e < nW; e += blockDim.x) {  // W = need * U (greedy.hpp:38-41)
         const int svc = e / M.PP;
@@ -98,7 +99,7 @@ __global__ void __launch_bounds__(kTopkThreads, 1) topk1_kernel(const __grid_con
     }
     if (a.use_mask) {  // expand's candidate set = rows touching a sampled service (mcts.hpp:98-107)
         for (int off = 16; off > 0; off >>= 1) scored += __shfl_xor_sync(0xffffffffu, scored, off);
-        if ((threadIdx.x & 31u) == 0 && scored) atomicAdd(a.n_scored, static_cast<unsigned long long>(scored));
+        if ((threadIdx.x & 31u) == 0 && scored) atomicAdd(&cta_scored, scored);  // shared: summed by rank 0
     }
     // 2. threshold: the largest per-warp K-th lane maximum (non-negative doubles order as
     //    their bit patterns, so an integer atomicMax on the bits is a max on the values)
@@ -134,7 +135,10 @@ __global__ void __launch_bounds__(kTopkThreads, 1) topk1_kernel(const __grid_con
     __syncthreads();
     if (gridDim.x == 1) {
         if (threadIdx.x < got) a.out_row[threadIdx.x] = win[threadIdx.x].row;
-        if (threadIdx.x == 0) *a.n_out = got;
+        if (threadIdx.x == 0) {
+            *a.n_out = got;
+            if (a.use_mask) *a.n_scored = static_cast<unsigned long long>(cta_scored);  // one host write
+        }
         return;
     }
     // 4. cluster merge over distributed shared memory: the grid is ONE thread-block cluster;
@@ -180,7 +184,14 @@ __global__ void __launch_bounds__(kTopkThreads, 1) topk1_kernel(const __grid_con
         __syncthreads();
         const int mgot = min(mc, k);
         if (threadIdx.x < mgot) a.out_row[threadIdx.x] = out[threadIdx.x].row;
-        if (threadIdx.x == 0) *a.n_out = (overflow || n_cand > kCandCap) ? -1 : mgot;
+        if (threadIdx.x == 0) {
+            *a.n_out = (overflow || n_cand > kCandCap) ? -1 : mgot;
+            if (a.use_mask) {  // one host write for the whole cluster
+                unsigned long long tot = 0;
+                for (int r = 0; r < nb; ++r) tot += static_cast<unsigned long long>(*cluster.map_shared_rank(&cta_scored, r));
+                *a.n_scored = tot;
+            }
+        }
     }
     cluster.sync();  // peers' shared memory stays alive until rank 0 has read it
 }
