@@ -935,7 +935,7 @@ RolloutResult Engine::rollouts(const std::vector<double>& comp, long long n_roll
 // n_steps[i] = plan length, or -1 when fast_algo raised PlanningError (no positive score)
 // or the plan would exceed cap_steps.  rows[i] = device pointer to the picked rows.
 void Engine::greedy_batch(const double* d_comps, int count, long long cap_steps, std::vector<const uint64_t*>& rows,
-                          std::vector<int>& n_steps) {
+                          std::vector<int>& n_steps, std::vector<std::vector<uint64_t>>* host_rows) {
     rows.assign(count, nullptr);
     n_steps.assign(count, -1);
     if (count <= 0) return;
@@ -985,7 +985,9 @@ void Engine::greedy_batch(const double* d_comps, int count, long long cap_steps,
             if (h.status == kOk) {
                 n_steps[b0 + i] = h.n_steps;
                 rows[b0 + i] = calls[i].s->d_pick_row;
+                if (host_rows) (*host_rows)[b0 + i].assign(calls[i].s->pick_row, calls[i].s->pick_row + h.n_steps);
             }
+            stats.d2h += static_cast<long long>(sizeof(GreedyState) + sizeof(uint64_t) * std::max(h.n_steps, 0));
         }
         // the picked rows stay valid until these slots are reused: the caller consumes them
         // (ga_finish) before the next greedy call, on this thread
@@ -999,128 +1001,206 @@ void Engine::greedy_batch(const double* d_comps, int count, long long cap_steps,
 // ---- device-resident parity mcts_solve (mcts.cu)
 MctsDeviceResult Engine::mcts_device(const std::vector<double>& comp, int budget, int topk, int pick_services,
                                      double ucb_c, uint64_t seed, int l_ref) {
+    return mcts_device_group({comp}, budget, topk, pick_services, ucb_c, {seed}, {l_ref})[0];
+}
+
+// Several independent searches (the GA's children) as CTAs of one launch; each search has
+// its own slot (scratch + rollout cache).
+std::vector<MctsDeviceResult> Engine::mcts_device_group(const std::vector<std::vector<double>>& comps, int budget,
+                                                        int topk, int pick_services, double ucb_c,
+                                                        const std::vector<uint64_t>& seeds,
+                                                        const std::vector<int>& l_refs) {
     if (topk < 1 || topk > 32) throw ArgumentError("mcts: topk must be in [1, 32] on the device path");
     if (n_ranks_ > 1) throw ArgumentError("mcts on a sharded context");
     const int n = m_.n;
-    const int max_depth = 2 * l_ref;
-    const long long max_nodes = 1 + static_cast<long long>(budget) * topk;
-    const long long path_cap = max_nodes + max_depth + 8;
-    long long want = std::max<long long>(1024, 2ll * budget * (max_depth + 1));
-    long long cap = 1;
-    while (cap < want) cap <<= 1;
-    Slot* s = acquire();
-    struct Rel {
-        Engine* e;
-        Slot* s;
-        ~Rel() { e->release(s); }
-    } rel{this, s};
+    const int count = static_cast<int>(comps.size());
+    std::vector<MctsDeviceResult> results(count);
     CK(cudaSetDevice(device_));
-    // carve one buffer
-    size_t off = 0;
-    auto take = [&](size_t bytes) {
-        size_t at = (off + 15) & ~size_t{15};
-        off = at + bytes;
-        return at;
-    };
-    const size_t o_comp0 = take(sizeof(double) * n), o_ncomp = take(sizeof(double) * max_nodes * n),
-                 o_vis = take(sizeof(int) * max_nodes), o_val = take(sizeof(double) * max_nodes),
-                 o_first = take(sizeof(int) * max_nodes), o_nch = take(sizeof(int) * max_nodes),
-                 o_cand = take(sizeof(int) * max_nodes), o_flags = take(max_nodes),
-                 o_path = take(sizeof(int) * path_cap), o_edges = take(sizeof(int) * path_cap),
-                 o_picked = take(sizeof(int) * (max_depth + 8)), o_unsat = take(sizeof(int) * (n + 1)),
-                 o_tag = take(sizeof(unsigned) * cap), o_key = take(sizeof(uint64_t) * 4 * cap),
-                 o_pn = take(sizeof(int) * cap), o_pool = take(sizeof(unsigned) * topk * cap),
-                 o_trace = take(sizeof(int) * 4 * std::max(budget, 1)), o_best = take(sizeof(int) * path_cap),
-                 o_desc = take(sizeof(int) * path_cap), o_dcomp = take(sizeof(double) * n), o_out = take(sizeof(int) * 16);
-    if (s->mcts_bytes < off) {
-        if (s->mcts_mem) CK(cudaFree(s->mcts_mem));
-        s->mcts_mem = nullptr;
-        CK(cudaMalloc(&s->mcts_mem, off));
-        s->mcts_bytes = off;
+    for (int b0 = 0; b0 < count; b0 += kMaxGroups) {
+        const int nb = std::min(kMaxGroups, count - b0);
+        std::vector<Slot*> slots;
+        struct Rel {
+            Engine* e;
+            std::vector<Slot*>& v;
+            ~Rel() {
+                for (Slot* s : v) e->release(s);
+            }
+        } rel{this, slots};
+        std::unique_ptr<MctsLaunch> L(new MctsLaunch{});
+        L->M = dm_;
+        L->base = d_base_;
+        L->n_base = pool_size();
+        L->budget = budget;
+        L->topk = topk;
+        L->pick_services = pick_services;
+        L->ucb_c = ucb_c;
+        struct Off {
+            size_t comp0, ncomp, vis, val, first, nch, cand, flags, path, edges, picked, unsat, tag, key, pn, pool,
+                trace, best, desc, dcomp, out;
+            long long cap, max_nodes;
+        };
+        std::vector<Off> offs(nb);
+        for (int q = 0; q < nb; ++q) {
+            const int l_ref = l_refs[b0 + q];
+            const int max_depth = 2 * l_ref;
+            const long long max_nodes = 1 + static_cast<long long>(budget) * topk;
+            const long long path_cap = max_nodes + max_depth + 8;
+            long long want = std::max<long long>(1024, 2ll * budget * (max_depth + 1));
+            long long cap = 1;
+            while (cap < want) cap <<= 1;
+            Slot* s = acquire();
+            slots.push_back(s);
+            size_t off = 0;
+            auto take = [&](size_t bytes) {
+                size_t at = (off + 15) & ~size_t{15};
+                off = at + bytes;
+                return at;
+            };
+            Off& o = offs[q];
+            o.cap = cap;
+            o.max_nodes = max_nodes;
+            o.comp0 = take(sizeof(double) * n);
+            o.ncomp = take(sizeof(double) * max_nodes * n);
+            o.vis = take(sizeof(int) * max_nodes);
+            o.val = take(sizeof(double) * max_nodes);
+            o.first = take(sizeof(int) * max_nodes);
+            o.nch = take(sizeof(int) * max_nodes);
+            o.cand = take(sizeof(int) * max_nodes);
+            o.flags = take(max_nodes);
+            o.path = take(sizeof(int) * path_cap);
+            o.edges = take(sizeof(int) * path_cap);
+            o.picked = take(sizeof(int) * (max_depth + 8));
+            o.unsat = take(sizeof(int) * (n + 1));
+            o.tag = take(sizeof(unsigned) * cap);
+            o.key = take(sizeof(uint64_t) * 4 * cap);
+            o.pn = take(sizeof(int) * cap);
+            o.pool = take(sizeof(unsigned) * topk * cap);
+            o.trace = take(sizeof(int) * 4 * std::max(budget, 1));
+            o.best = take(sizeof(int) * path_cap);
+            o.desc = take(sizeof(int) * path_cap);
+            o.dcomp = take(sizeof(double) * n);
+            o.out = take(sizeof(int) * 16);
+            if (s->mcts_bytes < off) {
+                if (s->mcts_mem) CK(cudaFree(s->mcts_mem));
+                s->mcts_mem = nullptr;
+                CK(cudaMalloc(&s->mcts_mem, off));
+                s->mcts_bytes = off;
+            }
+            if (s->logtab_n < budget + 2) {  // std::log(v), v = 0..budget+1 (the reference's own libm values)
+                if (s->logtab) CK(cudaFree(s->logtab));
+                std::vector<double> lt(budget + 2);
+                for (int v = 0; v < budget + 2; ++v) lt[v] = std::log(static_cast<double>(std::max(1, v)));
+                CK(cudaMalloc(&s->logtab, sizeof(double) * lt.size()));
+                CK(cudaMemcpy(s->logtab, lt.data(), sizeof(double) * lt.size(), cudaMemcpyHostToDevice));
+                s->logtab_n = static_cast<int>(lt.size());
+            }
+            unsigned char* b = static_cast<unsigned char*>(s->mcts_mem);
+            CK(cudaMemcpyAsync(b + o.comp0, comps[b0 + q].data(), sizeof(double) * n, cudaMemcpyHostToDevice,
+                               s->stream));
+            CK(cudaMemsetAsync(b + o.tag, 0, sizeof(unsigned) * cap, s->stream));
+            MctsSolveArgs& a = L->s[q];
+            a.comp0 = reinterpret_cast<const double*>(b + o.comp0);
+            a.seed = mix_seed_u64(seeds[b0 + q], 0x6d637473);
+            a.l_ref = l_ref;
+            a.max_nodes = static_cast<int>(max_nodes);
+            a.node_comp = reinterpret_cast<double*>(b + o.ncomp);
+            a.node_visits = reinterpret_cast<int*>(b + o.vis);
+            a.node_value = reinterpret_cast<double*>(b + o.val);
+            a.node_first = reinterpret_cast<int*>(b + o.first);
+            a.node_nch = reinterpret_cast<int*>(b + o.nch);
+            a.node_cand = reinterpret_cast<int*>(b + o.cand);
+            a.node_flags = b + o.flags;
+            a.pathnodes = reinterpret_cast<int*>(b + o.path);
+            a.edges = reinterpret_cast<int*>(b + o.edges);
+            a.picked = reinterpret_cast<int*>(b + o.picked);
+            a.unsat = reinterpret_cast<int*>(b + o.unsat);
+            a.tab_mask = static_cast<unsigned>(cap - 1);
+            a.tag = reinterpret_cast<unsigned*>(b + o.tag);
+            a.key = reinterpret_cast<uint64_t*>(b + o.key);
+            a.pool_n = reinterpret_cast<int*>(b + o.pn);
+            a.pool = reinterpret_cast<unsigned*>(b + o.pool);
+            a.trace = reinterpret_cast<int*>(b + o.trace);
+            a.best_out = reinterpret_cast<int*>(b + o.best);
+            a.descent_out = reinterpret_cast<int*>(b + o.desc);
+            a.descent_comp = reinterpret_cast<double*>(b + o.dcomp);
+            a.out = reinterpret_cast<int*>(b + o.out);
+        }
+        L->logtab = slots[0]->logtab;  // identical tables; slot 0's is >= budget + 2 long
+        for (int q = 1; q < nb; ++q) CK(cudaStreamSynchronize(slots[q]->stream));
+        Slot* s0 = slots[0];
+        void* args[] = {L.get()};
+        CK(cudaEventRecord(s0->e0, s0->stream));
+        CK(cudaLaunchKernel(mcts_kernel_ptr(), nb, mcts_threads(), args, mcts_smem_bytes(n, m_.PP), s0->stream));
+        stats.launches++;
+        CK(cudaEventRecord(s0->e1, s0->stream));
+        CK(cudaStreamSynchronize(s0->stream));
+        float ms = 0.f;
+        CK(cudaEventElapsedTime(&ms, s0->e0, s0->e1));
+        stats.topk_ns += static_cast<long long>(ms * 1e6);
+        for (int q = 0; q < nb; ++q) {
+            const Off& o = offs[q];
+            unsigned char* b = static_cast<unsigned char*>(slots[q]->mcts_mem);
+            int out[16];
+            CK(cudaMemcpy(out, b + o.out, sizeof(out), cudaMemcpyDeviceToHost));
+            MctsDeviceResult& r = results[b0 + q];
+            r.status = out[0];
+            r.best_len = out[1];
+            r.descent_leaf = out[3] != 0;
+            r.builds = out[4];
+            r.iterations = out[6];
+            r.expands = out[7];
+            std::memcpy(&r.expand_rows, &out[8], sizeof(long long));
+            r.trace.resize(4 * static_cast<size_t>(r.iterations));
+            std::vector<int> best(std::max(r.best_len, 0)), desc(out[2]);
+            if (!r.trace.empty())
+                CK(cudaMemcpy(r.trace.data(), b + o.trace, sizeof(int) * r.trace.size(), cudaMemcpyDeviceToHost));
+            if (!best.empty()) CK(cudaMemcpy(best.data(), b + o.best, sizeof(int) * best.size(), cudaMemcpyDeviceToHost));
+            if (!desc.empty()) CK(cudaMemcpy(desc.data(), b + o.desc, sizeof(int) * desc.size(), cudaMemcpyDeviceToHost));
+            r.descent_comp.resize(n);
+            CK(cudaMemcpy(r.descent_comp.data(), b + o.dcomp, sizeof(double) * n, cudaMemcpyDeviceToHost));
+            r.best.assign(best.begin(), best.end());
+            r.descent.assign(desc.begin(), desc.end());
+            // work counters with the reference's definitions (mcts.hpp:59-67): every expansion
+            // scores its filtered set, every rollout-cache miss the whole base pool
+            stats.topk_calls += r.expands + r.builds;
+            stats.topk_rows += r.expand_rows + static_cast<long long>(r.builds) * pool_size();
+            stats.h2d += static_cast<long long>(sizeof(double) * n);
+            stats.d2h += static_cast<long long>(sizeof(out) + sizeof(int) * (r.trace.size() + best.size() + desc.size()) +
+                                                sizeof(double) * n);
+        }
     }
-    if (s->logtab_n < budget + 2) {  // std::log(v), v = 0..budget+1 (the reference's own libm values)
-        if (s->logtab) CK(cudaFree(s->logtab));
-        std::vector<double> lt(budget + 2);
-        for (int v = 0; v < budget + 2; ++v) lt[v] = std::log(static_cast<double>(std::max(1, v)));
-        CK(cudaMalloc(&s->logtab, sizeof(double) * lt.size()));
-        CK(cudaMemcpy(s->logtab, lt.data(), sizeof(double) * lt.size(), cudaMemcpyHostToDevice));
-        s->logtab_n = static_cast<int>(lt.size());
+    return results;
+}
+
+// fast_algo on several host completion vectors, all in one grouped launch (CTA groups).
+// status[i] = 0 ok, 1 PlanningError (no positive score).
+void Engine::fast_algo_batch(const std::vector<std::vector<double>>& comps, std::vector<std::vector<uint64_t>>& rows,
+                             std::vector<int>& status) {
+    const int count = static_cast<int>(comps.size());
+    rows.assign(count, {});
+    status.assign(count, 0);
+    if (count == 0) return;
+    CK(cudaSetDevice(device_));
+    long long cap_steps = 1;
+    for (const auto& c : comps) {
+        if (static_cast<int>(c.size()) != m_.n) throw PlanningError("fast_algo: completion vector length mismatch");
+        cap_steps = std::max(cap_steps, std::min<long long>(step_bound(c), 1 << 24));
     }
-    unsigned char* b = static_cast<unsigned char*>(s->mcts_mem);
-    CK(cudaMemcpyAsync(b + o_comp0, comp.data(), sizeof(double) * n, cudaMemcpyHostToDevice, s->stream));
-    CK(cudaMemsetAsync(b + o_tag, 0, sizeof(unsigned) * cap, s->stream));
-    std::unique_ptr<MctsLaunch> L(new MctsLaunch{});
-    L->M = dm_;
-    L->base = d_base_;
-    L->n_base = pool_size();
-    L->logtab = s->logtab;
-    L->budget = budget;
-    L->topk = topk;
-    L->pick_services = pick_services;
-    L->ucb_c = ucb_c;
-    MctsSolveArgs& a = L->s[0];
-    a.comp0 = reinterpret_cast<const double*>(b + o_comp0);
-    a.seed = mix_seed_u64(seed, 0x6d637473);
-    a.l_ref = l_ref;
-    a.max_nodes = static_cast<int>(max_nodes);
-    a.node_comp = reinterpret_cast<double*>(b + o_ncomp);
-    a.node_visits = reinterpret_cast<int*>(b + o_vis);
-    a.node_value = reinterpret_cast<double*>(b + o_val);
-    a.node_first = reinterpret_cast<int*>(b + o_first);
-    a.node_nch = reinterpret_cast<int*>(b + o_nch);
-    a.node_cand = reinterpret_cast<int*>(b + o_cand);
-    a.node_flags = b + o_flags;
-    a.pathnodes = reinterpret_cast<int*>(b + o_path);
-    a.edges = reinterpret_cast<int*>(b + o_edges);
-    a.picked = reinterpret_cast<int*>(b + o_picked);
-    a.unsat = reinterpret_cast<int*>(b + o_unsat);
-    a.tab_mask = static_cast<unsigned>(cap - 1);
-    a.tag = reinterpret_cast<unsigned*>(b + o_tag);
-    a.key = reinterpret_cast<uint64_t*>(b + o_key);
-    a.pool_n = reinterpret_cast<int*>(b + o_pn);
-    a.pool = reinterpret_cast<unsigned*>(b + o_pool);
-    a.trace = reinterpret_cast<int*>(b + o_trace);
-    a.best_out = reinterpret_cast<int*>(b + o_best);
-    a.descent_out = reinterpret_cast<int*>(b + o_desc);
-    a.descent_comp = reinterpret_cast<double*>(b + o_dcomp);
-    a.out = reinterpret_cast<int*>(b + o_out);
-    void* args[] = {L.get()};
-    CK(cudaEventRecord(s->e0, s->stream));
-    CK(cudaLaunchKernel(mcts_kernel_ptr(), 1, mcts_threads(), args, mcts_smem_bytes(n, m_.PP), s->stream));
-    stats.launches++;
-    CK(cudaEventRecord(s->e1, s->stream));
-    int out[16];
-    CK(cudaMemcpyAsync(out, b + o_out, sizeof(out), cudaMemcpyDeviceToHost, s->stream));
-    CK(cudaStreamSynchronize(s->stream));
-    float ms = 0.f;
-    CK(cudaEventElapsedTime(&ms, s->e0, s->e1));
-    MctsDeviceResult r;
-    r.status = out[0];
-    r.best_len = out[1];
-    r.descent_leaf = out[3] != 0;
-    r.builds = out[4];
-    r.iterations = out[6];
-    r.expands = out[7];
-    std::memcpy(&r.expand_rows, &out[8], sizeof(long long));
-    r.trace.resize(4 * static_cast<size_t>(r.iterations));
-    std::vector<int> best(std::max(r.best_len, 0)), desc(out[2]);
-    if (!r.trace.empty())
-        CK(cudaMemcpy(r.trace.data(), b + o_trace, sizeof(int) * r.trace.size(), cudaMemcpyDeviceToHost));
-    if (!best.empty()) CK(cudaMemcpy(best.data(), b + o_best, sizeof(int) * best.size(), cudaMemcpyDeviceToHost));
-    if (!desc.empty()) CK(cudaMemcpy(desc.data(), b + o_desc, sizeof(int) * desc.size(), cudaMemcpyDeviceToHost));
-    r.descent_comp.resize(n);
-    CK(cudaMemcpy(r.descent_comp.data(), b + o_dcomp, sizeof(double) * n, cudaMemcpyDeviceToHost));
-    r.best.assign(best.begin(), best.end());
-    r.descent.assign(desc.begin(), desc.end());
-    // work counters with the reference's definitions (mcts.hpp:59-67): every expansion
-    // scores its filtered set, every rollout-cache miss the whole base pool
-    stats.topk_calls += r.expands + r.builds;
-    stats.topk_rows += r.expand_rows + static_cast<long long>(r.builds) * pool_size();
-    stats.topk_ns += static_cast<long long>(ms * 1e6);
-    stats.h2d += static_cast<long long>(sizeof(double) * n);
-    stats.d2h += static_cast<long long>(sizeof(out) + sizeof(int) * (r.trace.size() + best.size() + desc.size()) +
-                                        sizeof(double) * n);
-    return r;
+    std::vector<double> flat;
+    for (const auto& c : comps) flat.insert(flat.end(), c.begin(), c.end());
+    double* d = nullptr;
+    CK(cudaMalloc(&d, sizeof(double) * flat.size()));
+    struct Free {
+        double* p;
+        ~Free() { cudaFree(p); }
+    } fr{d};
+    CK(cudaMemcpy(d, flat.data(), sizeof(double) * flat.size(), cudaMemcpyHostToDevice));
+    stats.h2d += static_cast<long long>(sizeof(double) * flat.size());
+    std::vector<const uint64_t*> drows;
+    std::vector<int> steps;
+    greedy_batch(d, count, cap_steps, drows, steps, &rows);
+    for (int i = 0; i < count; ++i)
+        if (steps[i] < 0) status[i] = 1;
 }
 
 // ---- throughput-mode GA device state (ga.cu)

@@ -125,7 +125,12 @@ class Engine {
 
     // Independent single-CTA greedy instances in one launch (the GA's refills).
     void greedy_batch(const double* d_comps, int count, long long cap_steps, std::vector<const uint64_t*>& rows,
-                      std::vector<int>& n_steps);
+                      std::vector<int>& n_steps, std::vector<std::vector<uint64_t>>* host_rows = nullptr);
+    void fast_algo_batch(const std::vector<std::vector<double>>& comps, std::vector<std::vector<uint64_t>>& rows,
+                         std::vector<int>& status);
+    std::vector<MctsDeviceResult> mcts_device_group(const std::vector<std::vector<double>>& comps, int budget, int topk,
+                                                    int pick_services, double ucb_c, const std::vector<uint64_t>& seeds,
+                                                    const std::vector<int>& l_refs);
     // Throughput-mode GA device state and one generation (ga.cu; driver in search.cpp).
     GaRun* ga_begin(int population, int L_cap);
     void ga_end(GaRun* r);

@@ -412,6 +412,156 @@ std::vector<Config> sorted_deployment(std::vector<Config> cfgs) {  // make_deplo
     return cfgs;
 }
 
+namespace {
+
+// One GA round's children (ga.hpp:147-151: child i = crossover(mutate(pop[i]), MctsProcedure)),
+// computed PHASE BY PHASE across the children so that each device stage is one grouped launch
+// over all of them: every child keeps its own mt19937_64 stream and its own sequence of steps,
+// so the children are exactly the reference's.
+//   host    mutate; crossover's erase draws, survivors, residual; MctsProcedure's seed = rng()
+//   device  fast_ref = fast_algo(residual) for all children       (grouped greedy)
+//   device  the mcts_solve search loops                            (grouped mcts_kernel)
+//   device  fast_algo completions of the visit-count descents      (grouped greedy)
+//   host    answer precedence (mcts.hpp:245-251), evaluate_chromosome; PlanningError -> parent
+std::vector<Chromosome> breed_round(Engine& e, const std::vector<Chromosome>& pop, size_t n_parents, int round,
+                                    const GaParams& p) {
+    struct Child {
+        Chromosome c;  // the mutated parent (crossover's fallback)
+        std::vector<Config> survivors, fast_ref, refill;
+        std::vector<double> residual;
+        uint64_t seed = 0;
+        bool done = false;       // crossover fell back to the parent (result)
+        bool no_refill = false;  // the survivors already satisfy every service
+        Chromosome result;
+        MctsDeviceResult mr;
+    };
+    std::vector<Child> ch(n_parents);
+    auto fail = [&](Child& x) {  // crossover: catch (PlanningError) { return parent; }
+        x.result = x.c;
+        x.done = true;
+    };
+    for (size_t i = 0; i < n_parents; ++i) {
+        Child& x = ch[i];
+        Rng rng(mix_seed(p.seed, (static_cast<uint64_t>(round) << 20) + i));
+        x.c = mutate(pop[i], p, rng);
+        const size_t n = x.c.gpus.size();
+        const size_t erase = n == 0 ? 0 : static_cast<size_t>(std::ceil(p.erase_fraction * static_cast<double>(n)));
+        if (erase == 0) {
+            fail(x);  // crossover returns its parent unchanged (ga.hpp:55)
+            continue;
+        }
+        std::vector<size_t> order(n);
+        for (size_t k = 0; k < n; ++k) order[k] = k;
+        for (size_t k = 0; k < erase; ++k) std::swap(order[k], order[k + pick_index(rng, n - k)]);
+        std::vector<bool> erased(n, false);
+        for (size_t k = 0; k < erase; ++k) erased[order[k]] = true;
+        for (size_t k = 0; k < n; ++k)
+            if (!erased[k]) x.survivors.push_back(x.c.gpus[k]);
+        try {
+            x.residual = e.completion_of(x.survivors);
+        } catch (const PlanningError&) {
+            fail(x);
+            continue;
+        }
+        x.seed = rng();  // MctsProcedure::solve: mcts_solve(comp, ctx, params, rng()) (mcts.hpp:258)
+        if (satisfied(x.residual)) x.no_refill = true;  // mcts_solve returns {} (mcts.hpp:151)
+    }
+    // fast_ref for every child still searching
+    std::vector<size_t> live;
+    std::vector<std::vector<double>> comps;
+    for (size_t i = 0; i < n_parents; ++i)
+        if (!ch[i].done && !ch[i].no_refill) {
+            live.push_back(i);
+            comps.push_back(ch[i].residual);
+        }
+    std::vector<std::vector<uint64_t>> rows;
+    std::vector<int> st;
+    e.fast_algo_batch(comps, rows, st);
+    std::vector<size_t> search;
+    for (size_t q = 0; q < live.size(); ++q) {
+        Child& x = ch[live[q]];
+        if (st[q]) {
+            fail(x);
+            continue;
+        }
+        for (uint64_t r : rows[q]) x.fast_ref.push_back(e.config_of(r));
+        if (p.slow.budget_iters <= 0 || p.slow.topk < 1) x.refill = x.fast_ref;
+        else search.push_back(live[q]);
+    }
+    // the searches, one CTA each, one launch
+    {
+        std::vector<std::vector<double>> sc;
+        std::vector<uint64_t> seeds;
+        std::vector<int> lrefs;
+        for (size_t i : search) {
+            sc.push_back(ch[i].residual);
+            seeds.push_back(ch[i].seed);
+            lrefs.push_back(static_cast<int>(ch[i].fast_ref.size()));
+        }
+        auto res = e.mcts_device_group(sc, p.slow.budget_iters, p.slow.topk, p.slow.pick_services, p.slow.ucb_c, seeds,
+                                       lrefs);
+        for (size_t q = 0; q < search.size(); ++q) {
+            if (res[q].status == 1) {
+                fail(ch[search[q]]);  // rollout: empty pool -> PlanningError
+                continue;
+            }
+            if (res[q].status != 0) throw DeviceError("mcts: device search storage exhausted");
+            ch[search[q]].mr = std::move(res[q]);
+        }
+    }
+    // descent completions
+    std::vector<size_t> desc;
+    std::vector<std::vector<double>> dc;
+    for (size_t i : search)
+        if (!ch[i].done && !ch[i].mr.descent_leaf) {
+            desc.push_back(i);
+            dc.push_back(ch[i].mr.descent_comp);
+        }
+    std::vector<std::vector<uint64_t>> drows;
+    std::vector<int> dst;
+    e.fast_algo_batch(dc, drows, dst);
+    std::vector<std::vector<Config>> tail(n_parents);
+    for (size_t q = 0; q < desc.size(); ++q) {
+        if (dst[q]) {
+            fail(ch[desc[q]]);
+            continue;
+        }
+        for (uint64_t r : drows[q]) tail[desc[q]].push_back(e.config_of(r));
+    }
+    for (size_t i : search) {
+        Child& x = ch[i];
+        if (x.done) continue;
+        std::vector<Config> via;
+        for (long long idx : x.mr.descent) via.push_back(e.config_of(e.base_rows()[idx]));
+        for (auto& c : tail[i]) via.push_back(c);
+        std::vector<Config> answer = x.fast_ref;
+        if (via.size() < answer.size()) answer = std::move(via);
+        if (x.mr.best_len >= 0 && static_cast<size_t>(x.mr.best_len) < answer.size()) {
+            answer.clear();
+            for (long long idx : x.mr.best) answer.push_back(e.config_of(e.base_rows()[idx]));
+        }
+        x.refill = std::move(answer);
+    }
+    std::vector<Chromosome> out(n_parents);
+    for (size_t i = 0; i < n_parents; ++i) {
+        Child& x = ch[i];
+        if (x.done) {
+            out[i] = x.result;
+            continue;
+        }
+        std::vector<Config> full = x.survivors;
+        for (auto& c : x.refill) full.push_back(c);
+        try {
+            out[i] = evaluate_chromosome(std::move(full), e);
+        } catch (const PlanningError&) {
+            out[i] = x.c;
+        }
+    }
+    return out;
+}
+
+}  // namespace
+
 // two_phase, ga.hpp:126-179 (on an existing max_mix-2 context).
 std::vector<Config> two_phase(Engine& e, const GaParams& p,
                               const std::function<void(int, int, double, bool, double)>& log) {
@@ -429,6 +579,22 @@ std::vector<Config> two_phase(Engine& e, const GaParams& p,
         if (elapsed() >= p.time_budget_s) break;
         if (stall >= p.stall_rounds) break;
         size_t n_parents = std::min(pop.size(), (static_cast<size_t>(p.population) + 1) / 2);
+        static const bool host_loop = std::getenv("MIGPLAN_HOST_MCTS") != nullptr;
+        if (!host_loop && p.slow.topk >= 1 && p.slow.topk <= 32) {  // phased, device-batched children
+            std::vector<Chromosome> children = breed_round(e, pop, n_parents, round, p);
+            for (auto& c : children) pop.push_back(std::move(c));
+            std::stable_sort(pop.begin(), pop.end(), fitter);
+            if (pop.size() > static_cast<size_t>(p.population)) pop.resize(p.population);
+            bool improved = fitter(pop[0], best);
+            if (improved) {
+                best = pop[0];
+                stall = 0;
+            } else {
+                ++stall;
+            }
+            if (log) log(round, best.gpu_count, best.slack, improved, elapsed());
+            continue;
+        }
         std::vector<Chromosome> children(n_parents);
         std::vector<std::exception_ptr> errs(n_parents);
         auto work = [&](size_t i) {
