@@ -205,6 +205,8 @@ struct MctsLaunch {
     const double* logtab;    // std::log(v) for v = 0..budget (host-computed, bit-exact)
     int budget, topk, pick_services;
     double ucb_c;
+    int node_smem;           // node metadata in shared memory (all solves: same max_nodes)
+    int rows_smem;           // the base pool copied into shared memory
     MctsSolveArgs s[kMaxGroups];
 };
 

@@ -28,7 +28,7 @@ int topk1_max_ctas();
 constexpr int kTopkMaxCtas = 4096;  // partial-list capacity (Best x 32 per CTA)
 const void* topk1_kernel_ptr(int km);
 size_t rollout_smem_bytes(int n, int PP);
-size_t mcts_smem_bytes(int n, int PP);
+size_t mcts_smem_bytes(int n, int PP, int max_nodes, long long n_base, bool node_smem, bool rows_smem);
 const void* mcts_kernel_ptr();
 int mcts_threads();
 const void* rollout_kernel_ptr();
@@ -1079,7 +1079,7 @@ std::vector<MctsDeviceResult> Engine::mcts_device_group(const std::vector<std::v
             o.best = take(sizeof(int) * path_cap);
             o.desc = take(sizeof(int) * path_cap);
             o.dcomp = take(sizeof(double) * n);
-            o.out = take(sizeof(int) * 16);
+            o.out = take(sizeof(int) * 24);
             if (s->mcts_bytes < off) {
                 if (s->mcts_mem) CK(cudaFree(s->mcts_mem));
                 s->mcts_mem = nullptr;
@@ -1126,11 +1126,21 @@ std::vector<MctsDeviceResult> Engine::mcts_device_group(const std::vector<std::v
             a.out = reinterpret_cast<int*>(b + o.out);
         }
         L->logtab = slots[0]->logtab;  // identical tables; slot 0's is >= budget + 2 long
+        // on-chip placement: the base pool first (every top-K scans it twice), then the nodes
+        {
+            const long long room = device_info(device_).smem_optin - 8 * 1024;
+            const int mn = static_cast<int>(offs[0].max_nodes);
+            L->rows_smem = static_cast<long long>(mcts_smem_bytes(n, m_.PP, mn, pool_size(), false, true)) <= room;
+            L->node_smem =
+                static_cast<long long>(mcts_smem_bytes(n, m_.PP, mn, pool_size(), true, L->rows_smem != 0)) <= room;
+        }
+        const size_t msm = mcts_smem_bytes(n, m_.PP, static_cast<int>(offs[0].max_nodes), pool_size(), L->node_smem != 0,
+                                           L->rows_smem != 0);
         for (int q = 1; q < nb; ++q) CK(cudaStreamSynchronize(slots[q]->stream));
         Slot* s0 = slots[0];
         void* args[] = {L.get()};
         CK(cudaEventRecord(s0->e0, s0->stream));
-        CK(cudaLaunchKernel(mcts_kernel_ptr(), nb, mcts_threads(), args, mcts_smem_bytes(n, m_.PP), s0->stream));
+        CK(cudaLaunchKernel(mcts_kernel_ptr(), nb, mcts_threads(), args, msm, s0->stream));
         stats.launches++;
         CK(cudaEventRecord(s0->e1, s0->stream));
         CK(cudaStreamSynchronize(s0->stream));
@@ -1140,7 +1150,7 @@ std::vector<MctsDeviceResult> Engine::mcts_device_group(const std::vector<std::v
         for (int q = 0; q < nb; ++q) {
             const Off& o = offs[q];
             unsigned char* b = static_cast<unsigned char*>(slots[q]->mcts_mem);
-            int out[16];
+            int out[24];
             CK(cudaMemcpy(out, b + o.out, sizeof(out), cudaMemcpyDeviceToHost));
             MctsDeviceResult& r = results[b0 + q];
             r.status = out[0];
@@ -1150,6 +1160,13 @@ std::vector<MctsDeviceResult> Engine::mcts_device_group(const std::vector<std::v
             r.iterations = out[6];
             r.expands = out[7];
             std::memcpy(&r.expand_rows, &out[8], sizeof(long long));
+            if (std::getenv("MIGPLAN_MCTS_TIMERS")) {
+                long long t[5];
+                std::memcpy(t, &out[10], sizeof t);
+                std::fprintf(stderr, "[mcts] solve %d: %.1f ms device, cycles sel %lld expand-host %lld miss-host %lld topk %lld "
+                             "rollout-ctl %lld, builds %d expands %d iters %d\n",
+                             b0 + q, ms, t[0], t[1], t[2], t[3], t[4], out[4], out[7], out[6]);
+            }
             r.trace.resize(4 * static_cast<size_t>(r.iterations));
             std::vector<int> best(std::max(r.best_len, 0)), desc(out[2]);
             if (!r.trace.empty())

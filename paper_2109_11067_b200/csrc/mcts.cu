@@ -23,7 +23,7 @@ namespace {
 
 constexpr int kMThreads = 512;
 constexpr int kMWarps = kMThreads / 32;
-constexpr int kMCandCap = 2048;
+constexpr int kMCandCap = 512;  // above-threshold rows per top-K (ties beyond: exact k-round path)
 constexpr int kMMaxK = 32;
 constexpr unsigned char kExpanded = 1, kLeaf = 2;
 
@@ -81,9 +81,18 @@ __device__ __forceinline__ float ub_row(const float* Wf, uint64_t row) {
 // detail::topk_candidates (mcts.hpp:56-76) over the base rows (mask: rows touching a masked
 // service, else all), block-wide.  Writes base-pool indices in preference order to out[],
 // returns their count.  Ends with a barrier.
+__device__ __forceinline__ float ub_half(const float* Wf, unsigned lo, unsigned hi) {
+    float s = __fadd_ru(Wf[lo & 0xFFFFu], Wf[lo >> 16]);
+    s = __fadd_ru(s, Wf[hi & 0xFFFFu]);
+    return __fadd_ru(s, Wf[hi >> 16]);
+}
+__device__ __forceinline__ bool hit_half(const unsigned char* hitc, unsigned lo, unsigned hi) {
+    return (hitc[lo & 0xFFFFu] | hitc[lo >> 16] | hitc[hi & 0xFFFFu] | hitc[hi >> 16]) != 0;
+}
+
 __device__ int block_topk_exact(const DevModel& M, const uint64_t* base, long long nb, const double* comp,
-                                const uint64_t* mask, int k, double* W, float* Wf, unsigned char* hitc, Cand* cand,
-                                Cand* win, int* out, int* scored) {
+                                const uint64_t* mask, int k, const double* U, double* W, float* Wf,
+                                unsigned char* hitc, Cand* cand, Cand* win, int* out, int* scored) {
     __shared__ unsigned long long t_bits;
     __shared__ int n_cand, n_hit;
     __shared__ Cand red[kMWarps];
@@ -93,7 +102,7 @@ __device__ int block_topk_exact(const DevModel& M, const uint64_t* base, long lo
         double w = 0.0;
         if (svc < M.n) {
             const double need = __dadd_rn(1.0, -comp[svc]);
-            if (need > 0.0) w = __dmul_rn(need, __ldg(&M.U[e]));
+            if (need > 0.0) w = __dmul_rn(need, U[e]);
         }
         W[e] = w;
         Wf[e] = __double2float_ru(w);
@@ -105,20 +114,36 @@ __device__ int block_topk_exact(const DevModel& M, const uint64_t* base, long lo
         n_hit = 0;
     }
     __syncthreads();
+    // Rows are read two at a time (16 bytes) and split into 32-bit halves: no 64-bit shifts.
+    const uint4* base2 = reinterpret_cast<const uint4*>(base);
+    const long long np = nb >> 1;
     // pass 1: the thread's exact maximum; exact scores only where the FP32 bound reaches it.
     // With a mask, the candidate set is the rows touching a sampled service (its size is the
     // work count of the call, mcts.hpp:98-107).
     double tmax = 0.0;
+    float tmax_f = 0.0f;  // tmax rounded down: ub < tmax_f  =>  ub < tmax
     int hits = 0;
-    for (long long i = threadIdx.x; i < nb; i += blockDim.x) {
-        const uint64_t row = __ldg(base + i);
+    auto visit1 = [&](unsigned lo, unsigned hi) {
         if (mask) {
-            if (!row_hits(hitc, row)) continue;
+            if (!hit_half(hitc, lo, hi)) return;
             ++hits;
         }
-        const float ub = ub_row(Wf, row);
-        if (!(ub > 0.0f) || static_cast<double>(ub) < tmax) continue;
-        tmax = fmax(tmax, row_score(W, row));
+        const float ub = ub_half(Wf, lo, hi);
+        if (!(ub > 0.0f) || ub < tmax_f) return;
+        const double sc = row_score(W, (static_cast<uint64_t>(hi) << 32) | lo);
+        if (sc > tmax) {
+            tmax = sc;
+            tmax_f = __double2float_rd(sc);
+        }
+    };
+    for (long long p = threadIdx.x; p < np; p += blockDim.x) {
+        const uint4 v = base2[p];
+        visit1(v.x, v.y);
+        visit1(v.z, v.w);
+    }
+    if ((nb & 1) && threadIdx.x == 0) {
+        const uint64_t r = base[nb - 1];
+        visit1(static_cast<unsigned>(r), static_cast<unsigned>(r >> 32));
     }
     if (mask) {
         for (int off = 16; off > 0; off >>= 1) hits += __shfl_xor_sync(0xffffffffu, hits, off);
@@ -128,26 +153,42 @@ __device__ int block_topk_exact(const DevModel& M, const uint64_t* base, long lo
     if ((threadIdx.x & 31u) == 0) atomicMax(&t_bits, static_cast<unsigned long long>(__double_as_longlong(tw)));
     __syncthreads();
     const double T = __longlong_as_double(static_cast<long long>(t_bits));
+    const float T_f = __double2float_rd(T);
     // pass 2: rows whose exact score reaches T (at least k of them exist)
-    for (long long i0 = 0; i0 < nb; i0 += blockDim.x) {
-        const long long i = i0 + threadIdx.x;
+    auto visit2 = [&](unsigned lo, unsigned hi, long long pos) {
         bool take = false;
-        double s = 0.0;
-        uint64_t row = 0;
-        if (i < nb) {
-            row = __ldg(base + i);
-            const float ub = ub_row(Wf, row);
-            if (ub > 0.0f && static_cast<double>(ub) >= T && (!mask || row_hits(hitc, row))) {
-                s = row_score(W, row);
-                take = s > 0.0 && s >= T;
-            }
+        double sc = 0.0;
+        const uint64_t row = (static_cast<uint64_t>(hi) << 32) | lo;
+        const float ub = ub_half(Wf, lo, hi);
+        if (ub > 0.0f && ub >= T_f && (!mask || hit_half(hitc, lo, hi))) {
+            sc = row_score(W, row);
+            take = sc > 0.0 && sc >= T;
         }
         const unsigned b = __ballot_sync(0xffffffffu, take);
         if (b) {
             int at = 0;
             if ((threadIdx.x & 31u) == 0) at = atomicAdd(&n_cand, __popc(b));
             at = __shfl_sync(0xffffffffu, at, 0) + __popc(b & lanemask_lt());
-            if (take && at < kMCandCap) cand[at] = Cand{s, row_usum(M.U, row), row, i};
+            if (take && at < kMCandCap) cand[at] = Cand{sc, row_usum(U, row), row, pos};
+        }
+    };
+    const long long np_pad = (np + blockDim.x - 1) / blockDim.x * blockDim.x;  // warp-uniform trip count
+    for (long long p = threadIdx.x; p < np_pad; p += blockDim.x) {
+        uint4 v = make_uint4(0u, 0u, 0u, 0u);
+        const bool in = p < np;
+        if (in) v = base2[p];
+        else {  // padding lanes: sentinel rows (score 0)
+            const unsigned sent = static_cast<unsigned>(M.n * M.PP) * 0x00010001u;
+            v = make_uint4(sent, sent, sent, sent);
+        }
+        visit2(v.x, v.y, 2 * p);
+        visit2(v.z, v.w, 2 * p + 1);
+    }
+    if (nb & 1) {  // last odd row, warp 0 (ballot needs the whole warp)
+        if ((threadIdx.x >> 5) == 0) {
+            const uint64_t r = threadIdx.x == 0 ? base[nb - 1]
+                                                : static_cast<uint64_t>(M.n * M.PP) * 0x0001000100010001ull;
+            visit2(static_cast<unsigned>(r), static_cast<unsigned>(r >> 32), nb - 1);
         }
     }
     __syncthreads();
@@ -162,11 +203,11 @@ __device__ int block_topk_exact(const DevModel& M, const uint64_t* base, long lo
         for (int r = 0; r < k; ++r) {
             Cand b{0.0, 0.0, kNoRow, -1};
             for (long long i = threadIdx.x; i < nb; i += blockDim.x) {
-                const uint64_t row = __ldg(base + i);
+                const uint64_t row = base[i];
                 if (mask && !row_hits(hitc, row)) continue;
                 const double s = row_score(W, row);
                 if (!(s > 0.0)) continue;
-                const Cand c{s, row_usum(M.U, row), row, i};
+                const Cand c{s, row_usum(U, row), row, i};
                 if (r > 0 && !precedes(M, last, c)) continue;
                 if (b.row == kNoRow || precedes(M, c, b)) b = c;
             }
@@ -200,11 +241,11 @@ __device__ __forceinline__ bool comp_satisfied(const double* c, int n) {  // cor
     return true;
 }
 
-__device__ __forceinline__ void add_row_util(const DevModel& M, uint64_t row, double* c) {  // rollout / expand add
-    for (int j = 0; j < 4; ++j) {
+__device__ __forceinline__ void add_row_util(const DevModel& M, const double* U, uint64_t row, double* c) {
+    for (int j = 0; j < 4; ++j) {  // rollout / expand add (mcts.hpp:112,139)
         const int code = static_cast<int>((row >> (16 * j)) & 0xFFFFull);
         const int svc = code / M.PP;
-        if (svc < M.n) c[svc] = __dadd_rn(c[svc], __ldg(&M.U[code]));
+        if (svc < M.n) c[svc] = __dadd_rn(c[svc], U[code]);
     }
 }
 
@@ -216,12 +257,39 @@ __global__ void __launch_bounds__(kMThreads, 1) mcts_kernel(const __grid_constan
     const DevModel& M = L.M;
     const int n = M.n, K = L.topk;
     const int nW = (n + 1) * M.PP;
-    double* W = reinterpret_cast<double*>(smem);
-    double* cur = W + nW;                                     // n (+1)
-    Cand* cand = reinterpret_cast<Cand*>(cur + n + 1);        // kMCandCap
-    Cand* win = cand + kMCandCap;                             // kMMaxK
-    float* Wf = reinterpret_cast<float*>(win + kMMaxK);       // nW
-    unsigned char* hitc = reinterpret_cast<unsigned char*>(Wf + nW);  // nW
+    // dynamic shared memory: tables, then (when they fit) the node metadata and the base pool
+    size_t off = 0;
+    auto carve = [&](size_t bytes) {
+        unsigned char* p = smem + off;
+        off = (off + bytes + 15) & ~size_t{15};
+        return p;
+    };
+    double* W = reinterpret_cast<double*>(carve(sizeof(double) * nW));
+    double* Us = reinterpret_cast<double*>(carve(sizeof(double) * nW));
+    double* cur = reinterpret_cast<double*>(carve(sizeof(double) * (n + 1)));
+    Cand* cand = reinterpret_cast<Cand*>(carve(sizeof(Cand) * kMCandCap));
+    Cand* win = reinterpret_cast<Cand*>(carve(sizeof(Cand) * kMMaxK));
+    float* Wf = reinterpret_cast<float*>(carve(sizeof(float) * nW));
+    unsigned char* hitc = carve(nW);
+    const int MN = a.max_nodes;
+    double* nval = a.node_value;
+    int *nvis = a.node_visits, *nfirst = a.node_first, *nnch = a.node_nch, *ncand = a.node_cand;
+    unsigned char* nflags = a.node_flags;
+    if (L.node_smem) {  // selection walks these every iteration: keep them on chip
+        nval = reinterpret_cast<double*>(carve(sizeof(double) * MN));
+        nvis = reinterpret_cast<int*>(carve(sizeof(int) * MN));
+        nfirst = reinterpret_cast<int*>(carve(sizeof(int) * MN));
+        nnch = reinterpret_cast<int*>(carve(sizeof(int) * MN));
+        ncand = reinterpret_cast<int*>(carve(sizeof(int) * MN));
+        nflags = carve(MN);
+    }
+    const uint64_t* rows = L.base;
+    if (L.rows_smem) {  // every top-K streams the base pool twice: keep it on chip
+        uint64_t* r = reinterpret_cast<uint64_t*>(carve(sizeof(uint64_t) * L.n_base));
+        for (long long i = threadIdx.x; i < L.n_base; i += blockDim.x) r[i] = __ldg(L.base + i);
+        rows = r;
+    }
+    for (int e = threadIdx.x; e < nW; e += blockDim.x) Us[e] = __ldg(&M.U[e]);
     __shared__ Mt64 g;
     __shared__ int s_node, s_leaf, s_expand, s_take, s_nch, s_done, s_est, s_miss, s_slot, s_abort, s_steps;
     __shared__ int s_edges, s_path, s_best, s_have, s_nodes, s_builds, s_iters, s_scored, s_expands;
@@ -230,6 +298,15 @@ __global__ void __launch_bounds__(kMThreads, 1) mcts_kernel(const __grid_constan
     __shared__ int s_out[kMMaxK];
     const int max_depth = 2 * a.l_ref;
     const int tid = threadIdx.x;
+    long long t_sel = 0, t_exp = 0, t_miss = 0, t_roll = 0, t_topk = 0, tc = 0;  // thread-0 clock64 phase split
+    auto tick = [&](long long& acc) {
+        if (tid == 0) {
+            const long long t = clock64();
+            acc += t - tc;
+            tc = t;
+        }
+    };
+    if (tid == 0) tc = clock64();
 
     // root (mcts.hpp:157-160)
     if (tid == 0) {
@@ -242,15 +319,15 @@ __global__ void __launch_bounds__(kMThreads, 1) mcts_kernel(const __grid_constan
         s_iters = 0;
         s_expands = 0;
         s_expand_rows = 0;
-        a.node_visits[0] = 0;
-        a.node_value[0] = 0.0;
-        a.node_nch[0] = 0;
-        a.node_first[0] = 0;
-        a.node_cand[0] = -1;
+        nvis[0] = 0;
+        nval[0] = 0.0;
+        nnch[0] = 0;
+        nfirst[0] = 0;
+        ncand[0] = -1;
     }
     for (int i = tid; i < n; i += blockDim.x) a.node_comp[i] = a.comp0[i];
     __syncthreads();
-    if (tid == 0) a.node_flags[0] = comp_satisfied(a.node_comp, n) ? kLeaf : 0;
+    if (tid == 0) nflags[0] = comp_satisfied(a.node_comp, n) ? kLeaf : 0;
     __syncthreads();
 
     for (int iter = 0; iter < L.budget && !s_abort; ++iter) {
@@ -260,35 +337,36 @@ __global__ void __launch_bounds__(kMThreads, 1) mcts_kernel(const __grid_constan
             s_edges = 0;
             a.pathnodes[0] = 0;
             s_path = 1;
-            while ((a.node_flags[node] & kExpanded) && !(a.node_flags[node] & kLeaf) && a.node_nch[node] > 0) {
-                const double log_n = L.logtab[max(1, a.node_visits[node])];
+            while ((nflags[node] & kExpanded) && !(nflags[node] & kLeaf) && nnch[node] > 0) {
+                const double log_n = L.logtab[max(1, nvis[node])];
                 int pick = -1;
                 double best = -1.0;
-                for (int q = 0; q < a.node_nch[node]; ++q) {
-                    const int c = a.node_first[node] + q;
-                    const int v = a.node_visits[c];
+                for (int q = 0; q < nnch[node]; ++q) {
+                    const int c = nfirst[node] + q;
+                    const int v = nvis[c];
                     if (v == 0) {
                         pick = q;
                         break;
                     }
                     const double dv = static_cast<double>(v);
-                    const double val = __dadd_rn(__ddiv_rn(a.node_value[c], dv),
+                    const double val = __dadd_rn(__ddiv_rn(nval[c], dv),
                                                  __dmul_rn(L.ucb_c, __dsqrt_rn(__ddiv_rn(log_n, dv))));
                     if (val > best) {
                         best = val;
                         pick = q;
                     }
                 }
-                node = a.node_first[node] + pick;
-                a.edges[s_edges++] = a.node_cand[node];
+                node = nfirst[node] + pick;
+                a.edges[s_edges++] = ncand[node];
                 a.pathnodes[s_path++] = node;
             }
             s_node = node;
-            s_leaf = (a.node_flags[node] & kLeaf) != 0;
-            s_expand = !s_leaf && !(a.node_flags[node] & kExpanded);
+            s_leaf = (nflags[node] & kLeaf) != 0;
+            s_expand = !s_leaf && !(nflags[node] & kExpanded);
             s_est = 0;
         }
         __syncthreads();
+        tick(t_sel);
         if (s_leaf) {  // mcts.hpp:193-198
             if (tid == 0 && (!s_have || s_edges < s_best)) {
                 for (int q = 0; q < s_edges; ++q) a.best_out[q] = a.edges[q];
@@ -315,9 +393,11 @@ __global__ void __launch_bounds__(kMThreads, 1) mcts_kernel(const __grid_constan
                 }
                 for (int i = tid; i < n; i += blockDim.x) cur[i] = a.node_comp[static_cast<long long>(s_node) * n + i];
                 __syncthreads();
-                const int got = s_take > 0 ? block_topk_exact(M, L.base, L.n_base, cur, s_mask, K, W, Wf, hitc, cand,
-                                                              win, s_out, &s_scored)
+                tick(t_exp);
+                const int got = s_take > 0 ? block_topk_exact(M, rows, L.n_base, cur, s_mask, K, Us, W, Wf, hitc,
+                                                              cand, win, s_out, &s_scored)
                                            : 0;
+                tick(t_topk);
                 if (tid == 0 && s_take > 0) {
                     ++s_expands;
                     s_expand_rows += s_scored;
@@ -331,29 +411,30 @@ __global__ void __launch_bounds__(kMThreads, 1) mcts_kernel(const __grid_constan
                             const int c = first + q;
                             double* cc = a.node_comp + static_cast<long long>(c) * n;
                             for (int i = 0; i < n; ++i) cc[i] = cur[i];
-                            add_row_util(M, __ldg(L.base + s_out[q]), cc);
-                            a.node_cand[c] = s_out[q];
-                            a.node_visits[c] = 0;
-                            a.node_value[c] = 0.0;
-                            a.node_nch[c] = 0;
-                            a.node_first[c] = 0;
-                            a.node_flags[c] = comp_satisfied(cc, n) ? kLeaf : 0;
+                            add_row_util(M, Us, rows[s_out[q]], cc);
+                            ncand[c] = s_out[q];
+                            nvis[c] = 0;
+                            nval[c] = 0.0;
+                            nnch[c] = 0;
+                            nfirst[c] = 0;
+                            nflags[c] = comp_satisfied(cc, n) ? kLeaf : 0;
                         }
-                        a.node_first[s_node] = first;
-                        a.node_nch[s_node] = got;
-                        a.node_flags[s_node] |= kExpanded;
+                        nfirst[s_node] = first;
+                        nnch[s_node] = got;
+                        nflags[s_node] |= kExpanded;
                         s_nodes += got;
                     }
                 }
                 __syncthreads();
+                tick(t_exp);
                 if (s_abort) break;
             }
             // random child (mcts.hpp:202-207)
             if (tid == 0) {
-                const int nch = a.node_nch[s_node];
+                const int nch = nnch[s_node];
                 if (nch > 0) {
-                    const int c = a.node_first[s_node] + static_cast<int>(mt_pick(g, static_cast<uint64_t>(nch)));
-                    a.edges[s_edges++] = a.node_cand[c];
+                    const int c = nfirst[s_node] + static_cast<int>(mt_pick(g, static_cast<uint64_t>(nch)));
+                    a.edges[s_edges++] = ncand[c];
                     a.pathnodes[s_path++] = c;
                     s_node = c;
                 }
@@ -404,15 +485,19 @@ __global__ void __launch_bounds__(kMThreads, 1) mcts_kernel(const __grid_constan
                 }
                 __syncthreads();
                 if (s_done || s_abort) break;
+                tick(t_roll);
                 if (s_miss) {  // cache miss: top-K of the whole base pool (mcts.hpp:129-133)
-                    const int got = block_topk_exact(M, L.base, L.n_base, cur, nullptr, K, W, Wf, hitc, cand, win, s_out,
-                                                     &s_scored);
+                    tick(t_miss);
+                    const int got = block_topk_exact(M, rows, L.n_base, cur, nullptr, K, Us, W, Wf, hitc, cand, win,
+                                                     s_out, &s_scored);
+                    tick(t_topk);
                     if (tid < got) a.pool[static_cast<long long>(s_slot) * K + tid] = static_cast<unsigned>(s_out[tid]);
                     if (tid == 0) {
                         a.pool_n[s_slot] = got;
                         ++s_builds;
                     }
                     __syncthreads();
+                    tick(t_miss);
                 }
                 if (tid == 0) {
                     const int pn = a.pool_n[s_slot];
@@ -421,7 +506,7 @@ __global__ void __launch_bounds__(kMThreads, 1) mcts_kernel(const __grid_constan
                     } else {
                         const int idx = static_cast<int>(a.pool[static_cast<long long>(s_slot) * K +
                                                                 mt_pick(g, static_cast<uint64_t>(pn))]);
-                        add_row_util(M, __ldg(L.base + idx), cur);
+                        add_row_util(M, Us, rows[idx], cur);
                         a.picked[s_steps++] = idx;
                     }
                 }
@@ -430,7 +515,7 @@ __global__ void __launch_bounds__(kMThreads, 1) mcts_kernel(const __grid_constan
             }
             if (s_abort) break;
             if (tid == 0) {  // mcts.hpp:210-218
-                const bool complete = (a.node_flags[s_node] & kLeaf) || s_steps == s_est;
+                const bool complete = (nflags[s_node] & kLeaf) || s_steps == s_est;
                 if (complete && s_est < max_depth) {
                     const int len = s_edges + s_steps;
                     if (!s_have || len < s_best) {
@@ -448,8 +533,8 @@ __global__ void __launch_bounds__(kMThreads, 1) mcts_kernel(const __grid_constan
                                             : 1.0;
             for (int q = 0; q < s_path; ++q) {
                 const int nd = a.pathnodes[q];
-                a.node_visits[nd] += 1;
-                a.node_value[nd] = __dadd_rn(a.node_value[nd], reward);
+                nvis[nd] += 1;
+                nval[nd] = __dadd_rn(nval[nd], reward);
             }
             a.trace[4 * iter + 0] = iter;
             a.trace[4 * iter + 1] = s_edges;
@@ -463,30 +548,50 @@ __global__ void __launch_bounds__(kMThreads, 1) mcts_kernel(const __grid_constan
     if (tid == 0) {
         int node = 0, dl = 0;
         if (!s_abort)
-            while ((a.node_flags[node] & kExpanded) && !(a.node_flags[node] & kLeaf) && a.node_nch[node] > 0) {
+            while ((nflags[node] & kExpanded) && !(nflags[node] & kLeaf) && nnch[node] > 0) {
                 int pick = 0;
-                for (int q = 1; q < a.node_nch[node]; ++q)
-                    if (a.node_visits[a.node_first[node] + q] > a.node_visits[a.node_first[node] + pick]) pick = q;
-                node = a.node_first[node] + pick;
-                a.descent_out[dl++] = a.node_cand[node];
+                for (int q = 1; q < nnch[node]; ++q)
+                    if (nvis[nfirst[node] + q] > nvis[nfirst[node] + pick]) pick = q;
+                node = nfirst[node] + pick;
+                a.descent_out[dl++] = ncand[node];
             }
         for (int i = 0; i < n; ++i) a.descent_comp[i] = a.node_comp[static_cast<long long>(node) * n + i];
         a.out[0] = s_abort;
         a.out[1] = s_have ? s_best : -1;
         a.out[2] = dl;
-        a.out[3] = (a.node_flags[node] & kLeaf) ? 1 : 0;
+        a.out[3] = (nflags[node] & kLeaf) ? 1 : 0;
         a.out[4] = s_builds;
         a.out[5] = s_nodes;
         a.out[6] = s_iters;
         a.out[7] = s_expands;
+        reinterpret_cast<long long*>(a.out)[5] = t_sel;   // out[10..11]
+        reinterpret_cast<long long*>(a.out)[6] = t_exp;   // out[12..13]
+        reinterpret_cast<long long*>(a.out)[7] = t_miss;  // out[14..15]
+        reinterpret_cast<long long*>(a.out)[8] = t_topk;  // out[16..17]
+        reinterpret_cast<long long*>(a.out)[9] = t_roll;  // out[18..19]
         reinterpret_cast<long long*>(a.out)[4] = s_expand_rows;  // out[8..9]
     }
 }
 
-size_t mcts_smem_bytes(int n, int PP) {
+// Dynamic shared memory of mcts_kernel (must mirror its carve order).
+size_t mcts_smem_bytes(int n, int PP, int max_nodes, long long n_base, bool node_smem, bool rows_smem) {
     const size_t nW = static_cast<size_t>(n + 1) * PP;
-    return nW * 8 + static_cast<size_t>(n + 1) * 8 + static_cast<size_t>(kMCandCap + kMMaxK) * sizeof(Cand) + nW * 4 +
-           nW + 16;
+    size_t off = 0;
+    auto carve = [&](size_t bytes) { off = (off + bytes + 15) & ~size_t{15}; };
+    carve(8 * nW);
+    carve(8 * nW);
+    carve(8 * static_cast<size_t>(n + 1));
+    carve(sizeof(Cand) * kMCandCap);
+    carve(sizeof(Cand) * kMMaxK);
+    carve(4 * nW);
+    carve(nW);
+    if (node_smem) {
+        carve(8 * static_cast<size_t>(max_nodes));
+        for (int i = 0; i < 4; ++i) carve(4 * static_cast<size_t>(max_nodes));
+        carve(static_cast<size_t>(max_nodes));
+    }
+    if (rows_smem) carve(8 * static_cast<size_t>(n_base));
+    return off;
 }
 const void* mcts_kernel_ptr() { return reinterpret_cast<const void*>(&mcts_kernel); }
 int mcts_threads() { return kMThreads; }
