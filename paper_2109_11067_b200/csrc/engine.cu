@@ -368,6 +368,7 @@ const DeviceInfo& device_info(int device) {
     info.smem_optin = static_cast<long long>(prop.sharedMemPerBlockOptin);
     // every kernel may use all the opt-in shared memory its static allocation leaves
     CK(cudaFuncSetAttribute(topk1_kernel_ptr(32), cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    CK(cudaFuncSetAttribute(mcts_kernel_ptr(), cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     for (const void* k : {greedy_kernel_ptr(), topk_kernel_ptr(), topk1_kernel_ptr(32), rollout_kernel_ptr(),
                           mcts_kernel_ptr()}) {
         cudaFuncAttributes fa{};
@@ -1126,21 +1127,40 @@ std::vector<MctsDeviceResult> Engine::mcts_device_group(const std::vector<std::v
             a.out = reinterpret_cast<int*>(b + o.out);
         }
         L->logtab = slots[0]->logtab;  // identical tables; slot 0's is >= budget + 2 long
-        // on-chip placement: the base pool first (every top-K scans it twice), then the nodes
+        // one thread-block cluster per search: C ranks each scan 1/C of the base pool per top-K
+        // (measured: the per-top-K fixed costs — cluster barriers, DSMEM merge — outweigh the
+        // 1/C scan at the pool sizes of the GA workloads, so one CTA per search by default)
+        int C = 1;
+        if (const char* v = std::getenv("MIGPLAN_MCTS_CLUSTER")) C = std::max(1, std::min(16, std::atoi(v)));
+        const long long slice = ((pool_size() + C - 1) / C + 1) & ~1ll;
+        // on-chip placement: the slice first (every top-K scans it twice), then the nodes
         {
             const long long room = device_info(device_).smem_optin - 8 * 1024;
             const int mn = static_cast<int>(offs[0].max_nodes);
-            L->rows_smem = static_cast<long long>(mcts_smem_bytes(n, m_.PP, mn, pool_size(), false, true)) <= room;
-            L->node_smem =
-                static_cast<long long>(mcts_smem_bytes(n, m_.PP, mn, pool_size(), true, L->rows_smem != 0)) <= room;
+            L->rows_smem = static_cast<long long>(mcts_smem_bytes(n, m_.PP, mn, slice, false, true)) <= room;
+            L->node_smem = static_cast<long long>(mcts_smem_bytes(n, m_.PP, mn, slice, true, L->rows_smem != 0)) <= room;
         }
-        const size_t msm = mcts_smem_bytes(n, m_.PP, static_cast<int>(offs[0].max_nodes), pool_size(), L->node_smem != 0,
+        const size_t msm = mcts_smem_bytes(n, m_.PP, static_cast<int>(offs[0].max_nodes), slice, L->node_smem != 0,
                                            L->rows_smem != 0);
         for (int q = 1; q < nb; ++q) CK(cudaStreamSynchronize(slots[q]->stream));
         Slot* s0 = slots[0];
         void* args[] = {L.get()};
         CK(cudaEventRecord(s0->e0, s0->stream));
-        CK(cudaLaunchKernel(mcts_kernel_ptr(), nb, mcts_threads(), args, msm, s0->stream));
+        {
+            cudaLaunchConfig_t cfg{};
+            cfg.gridDim = dim3(nb * C);
+            cfg.blockDim = dim3(mcts_threads());
+            cfg.dynamicSmemBytes = msm;
+            cfg.stream = s0->stream;
+            cudaLaunchAttribute attr[1];
+            attr[0].id = cudaLaunchAttributeClusterDimension;
+            attr[0].val.clusterDim.x = C;
+            attr[0].val.clusterDim.y = 1;
+            attr[0].val.clusterDim.z = 1;
+            cfg.attrs = attr;
+            cfg.numAttrs = 1;
+            CK(cudaLaunchKernelExC(&cfg, mcts_kernel_ptr(), args));
+        }
         stats.launches++;
         CK(cudaEventRecord(s0->e1, s0->stream));
         CK(cudaStreamSynchronize(s0->stream));

@@ -13,7 +13,11 @@
 // K-th best exact maxima, parallel rank of the survivors (common.cuh).
 // log(visits) comes from a host table (std::log), so the UCB arithmetic is bit-exact; the
 // divisions, sqrt and adds are correctly rounded on both sides (no FMA).
+#include <cooperative_groups.h>
+
 #include "common.cuh"
+
+namespace cg = cooperative_groups;
 
 namespace mgb {
 
@@ -90,8 +94,8 @@ __device__ __forceinline__ bool hit_half(const unsigned char* hitc, unsigned lo,
     return (hitc[lo & 0xFFFFu] | hitc[lo >> 16] | hitc[hi & 0xFFFFu] | hitc[hi >> 16]) != 0;
 }
 
-__device__ int block_topk_exact(const DevModel& M, const uint64_t* base, long long nb, const double* comp,
-                                const uint64_t* mask, int k, const double* U, double* W, float* Wf,
+__device__ int block_topk_exact(const DevModel& M, const uint64_t* base, long long nb, long long pos0,
+                                const double* comp, const uint64_t* mask, int k, const double* U, double* W, float* Wf,
                                 unsigned char* hitc, Cand* cand, Cand* win, int* out, int* scored) {
     __shared__ unsigned long long t_bits;
     __shared__ int n_cand, n_hit;
@@ -181,14 +185,14 @@ __device__ int block_topk_exact(const DevModel& M, const uint64_t* base, long lo
             const unsigned sent = static_cast<unsigned>(M.n * M.PP) * 0x00010001u;
             v = make_uint4(sent, sent, sent, sent);
         }
-        visit2(v.x, v.y, 2 * p);
-        visit2(v.z, v.w, 2 * p + 1);
+        visit2(v.x, v.y, pos0 + 2 * p);
+        visit2(v.z, v.w, pos0 + 2 * p + 1);
     }
     if (nb & 1) {  // last odd row, warp 0 (ballot needs the whole warp)
         if ((threadIdx.x >> 5) == 0) {
             const uint64_t r = threadIdx.x == 0 ? base[nb - 1]
                                                 : static_cast<uint64_t>(M.n * M.PP) * 0x0001000100010001ull;
-            visit2(static_cast<unsigned>(r), static_cast<unsigned>(r >> 32), nb - 1);
+            visit2(static_cast<unsigned>(r), static_cast<unsigned>(r >> 32), pos0 + nb - 1);
         }
     }
     __syncthreads();
@@ -207,7 +211,7 @@ __device__ int block_topk_exact(const DevModel& M, const uint64_t* base, long lo
                 if (mask && !row_hits(hitc, row)) continue;
                 const double s = row_score(W, row);
                 if (!(s > 0.0)) continue;
-                const Cand c{s, row_usum(U, row), row, i};
+                const Cand c{s, row_usum(U, row), row, pos0 + i};
                 if (r > 0 && !precedes(M, last, c)) continue;
                 if (b.row == kNoRow || precedes(M, c, b)) b = c;
             }
@@ -229,7 +233,7 @@ __device__ int block_topk_exact(const DevModel& M, const uint64_t* base, long lo
         }
     }
     __syncthreads();
-    if (threadIdx.x < got) out[threadIdx.x] = static_cast<int>(win[threadIdx.x].pos);
+    if (out && threadIdx.x < got) out[threadIdx.x] = static_cast<int>(win[threadIdx.x].pos);
     if (threadIdx.x == 0) *scored = mask ? n_hit : static_cast<int>(nb);
     __syncthreads();
     return got;
@@ -253,11 +257,20 @@ __device__ __forceinline__ void add_row_util(const DevModel& M, const double* U,
 
 __global__ void __launch_bounds__(kMThreads, 1) mcts_kernel(const __grid_constant__ MctsLaunch L) {
     extern __shared__ __align__(16) unsigned char smem[];
-    const MctsSolveArgs& a = L.s[blockIdx.x];
+    // One search per thread-block CLUSTER: rank 0 runs the search; every rank scans its slice
+    // of the base pool for each top-K and rank 0 merges the slices' winners over DSMEM.
+    cg::cluster_group cl = cg::this_cluster();
+    const int C = static_cast<int>(cl.num_blocks());
+    const int rank = static_cast<int>(cl.block_rank());
+    const MctsSolveArgs& a = L.s[blockIdx.x / C];
     const DevModel& M = L.M;
     const int n = M.n, K = L.topk;
     const int nW = (n + 1) * M.PP;
-    // dynamic shared memory: tables, then (when they fit) the node metadata and the base pool
+    const long long chunk = ((L.n_base + C - 1) / C + 1) & ~1ll;  // even: 16-byte row pairs stay aligned
+    const long long lo = min(L.n_base, static_cast<long long>(rank) * chunk);
+    const long long hi = min(L.n_base, lo + chunk);
+    // dynamic shared memory: tables (same offsets in every rank: peers read `cur`, `win` and
+    // the request over DSMEM), then rank 0's node metadata, then this rank's slice of the pool
     size_t off = 0;
     auto carve = [&](size_t bytes) {
         unsigned char* p = smem + off;
@@ -268,7 +281,7 @@ __global__ void __launch_bounds__(kMThreads, 1) mcts_kernel(const __grid_constan
     double* Us = reinterpret_cast<double*>(carve(sizeof(double) * nW));
     double* cur = reinterpret_cast<double*>(carve(sizeof(double) * (n + 1)));
     Cand* cand = reinterpret_cast<Cand*>(carve(sizeof(Cand) * kMCandCap));
-    Cand* win = reinterpret_cast<Cand*>(carve(sizeof(Cand) * kMMaxK));
+    Cand* win = reinterpret_cast<Cand*>(carve(sizeof(Cand) * 2 * kMMaxK));  // [0,K) local, [K,2K) merged
     float* Wf = reinterpret_cast<float*>(carve(sizeof(float) * nW));
     unsigned char* hitc = carve(nW);
     const int MN = a.max_nodes;
@@ -283,18 +296,93 @@ __global__ void __launch_bounds__(kMThreads, 1) mcts_kernel(const __grid_constan
         ncand = reinterpret_cast<int*>(carve(sizeof(int) * MN));
         nflags = carve(MN);
     }
-    const uint64_t* rows = L.base;
-    if (L.rows_smem) {  // every top-K streams the base pool twice: keep it on chip
-        uint64_t* r = reinterpret_cast<uint64_t*>(carve(sizeof(uint64_t) * L.n_base));
-        for (long long i = threadIdx.x; i < L.n_base; i += blockDim.x) r[i] = __ldg(L.base + i);
-        rows = r;
+    const uint64_t* rows = L.base;  // whole pool (rank 0's adds); slice for the top-K scans
+    const uint64_t* slice = L.base + lo;
+    if (L.rows_smem) {
+        uint64_t* r = reinterpret_cast<uint64_t*>(carve(sizeof(uint64_t) * chunk));
+        for (long long i = threadIdx.x; i < hi - lo; i += blockDim.x) r[i] = __ldg(L.base + lo + i);
+        slice = r;
     }
     for (int e = threadIdx.x; e < nW; e += blockDim.x) Us[e] = __ldg(&M.U[e]);
+    __shared__ int s_exit, s_usemask, n_got, s_hits;
+    __shared__ uint64_t s_mask[4];
+    if (threadIdx.x == 0) {
+        s_exit = 0;
+        s_usemask = 0;
+    }
+    __syncthreads();
+    if (rank != 0) {  // helper: serve rank 0's top-K requests until it posts exit
+        for (;;) {
+            cl.sync();  // request posted
+            if (*cl.map_shared_rank(&s_exit, 0)) {
+                cl.sync();  // rank 0 stays resident until every helper has read the flag
+                break;
+            }
+            const double* rc = cl.map_shared_rank(cur, 0);
+            for (int i = threadIdx.x; i < n; i += blockDim.x) cur[i] = rc[i];
+            if (threadIdx.x < 4) s_mask[threadIdx.x] = cl.map_shared_rank(s_mask, 0)[threadIdx.x];
+            if (threadIdx.x == 0) s_usemask = *cl.map_shared_rank(&s_usemask, 0);
+            __syncthreads();
+            int sc = 0;
+            const int got = block_topk_exact(M, slice, hi - lo, lo, cur, s_usemask ? s_mask : nullptr, K, Us, W, Wf,
+                                             hitc, cand, win, nullptr, &sc);
+            if (threadIdx.x == 0) {
+                n_got = got;
+                s_hits = sc;
+            }
+            cl.sync();  // winners published
+        }
+        return;
+    }
+    // rank 0: the top-K of the whole pool under `cur` (mask: rows touching a sampled service)
+    auto cluster_topk = [&](bool usemask, int* out, int* scored) -> int {
+        if (threadIdx.x == 0) s_usemask = usemask ? 1 : 0;
+        __syncthreads();
+        cl.sync();
+        int sc = 0;
+        const int got0 = block_topk_exact(M, slice, hi - lo, lo, cur, usemask ? s_mask : nullptr, K, Us, W, Wf, hitc,
+                                          cand, win, nullptr, &sc);
+        if (threadIdx.x == 0) {
+            n_got = got0;
+            s_hits = sc;
+        }
+        cl.sync();
+        __shared__ unsigned long long m_bits;
+        __shared__ int m_n, m_scored;
+        if (threadIdx.x == 0) {
+            m_bits = 0ull;
+            m_n = 0;
+            m_scored = 0;
+        }
+        __syncthreads();
+        for (int r = threadIdx.x; r < C; r += blockDim.x) {  // merge threshold: full lists' K-th scores
+            const int g = *cl.map_shared_rank(&n_got, r);
+            atomicAdd(&m_scored, *cl.map_shared_rank(&s_hits, r));
+            if (g == K) atomicMax(&m_bits, static_cast<unsigned long long>(__double_as_longlong(cl.map_shared_rank(win, r)[K - 1].s)));
+        }
+        __syncthreads();
+        const double TM = __longlong_as_double(static_cast<long long>(m_bits));
+        for (int i = threadIdx.x; i < C * K; i += blockDim.x) {
+            const int r = i / K, q = i % K;
+            if (q >= *cl.map_shared_rank(&n_got, r)) continue;
+            const Cand c = cl.map_shared_rank(win, r)[q];
+            if (c.s < TM) continue;
+            cand[atomicAdd(&m_n, 1)] = c;  // <= C * K <= kMCandCap
+        }
+        __syncthreads();
+        const int mc = m_n;
+        rank_select(M, cand, mc, K, win + kMMaxK);
+        __syncthreads();
+        const int got = min(mc, K);
+        if (threadIdx.x < got) out[threadIdx.x] = static_cast<int>(win[kMMaxK + threadIdx.x].pos);
+        if (threadIdx.x == 0) *scored = m_scored;
+        __syncthreads();
+        return got;
+    };
     __shared__ Mt64 g;
     __shared__ int s_node, s_leaf, s_expand, s_take, s_nch, s_done, s_est, s_miss, s_slot, s_abort, s_steps;
     __shared__ int s_edges, s_path, s_best, s_have, s_nodes, s_builds, s_iters, s_scored, s_expands;
     __shared__ long long s_expand_rows;
-    __shared__ uint64_t s_mask[4];
     __shared__ int s_out[kMMaxK];
     const int max_depth = 2 * a.l_ref;
     const int tid = threadIdx.x;
@@ -394,9 +482,7 @@ __global__ void __launch_bounds__(kMThreads, 1) mcts_kernel(const __grid_constan
                 for (int i = tid; i < n; i += blockDim.x) cur[i] = a.node_comp[static_cast<long long>(s_node) * n + i];
                 __syncthreads();
                 tick(t_exp);
-                const int got = s_take > 0 ? block_topk_exact(M, rows, L.n_base, cur, s_mask, K, Us, W, Wf, hitc,
-                                                              cand, win, s_out, &s_scored)
-                                           : 0;
+                const int got = s_take > 0 ? cluster_topk(true, s_out, &s_scored) : 0;
                 tick(t_topk);
                 if (tid == 0 && s_take > 0) {
                     ++s_expands;
@@ -488,8 +574,7 @@ __global__ void __launch_bounds__(kMThreads, 1) mcts_kernel(const __grid_constan
                 tick(t_roll);
                 if (s_miss) {  // cache miss: top-K of the whole base pool (mcts.hpp:129-133)
                     tick(t_miss);
-                    const int got = block_topk_exact(M, rows, L.n_base, cur, nullptr, K, Us, W, Wf, hitc, cand, win,
-                                                     s_out, &s_scored);
+                    const int got = cluster_topk(false, s_out, &s_scored);
                     tick(t_topk);
                     if (tid < got) a.pool[static_cast<long long>(s_slot) * K + tid] = static_cast<unsigned>(s_out[tid]);
                     if (tid == 0) {
@@ -571,10 +656,15 @@ __global__ void __launch_bounds__(kMThreads, 1) mcts_kernel(const __grid_constan
         reinterpret_cast<long long*>(a.out)[9] = t_roll;  // out[18..19]
         reinterpret_cast<long long*>(a.out)[4] = s_expand_rows;  // out[8..9]
     }
+    if (threadIdx.x == 0) s_exit = 1;  // release the helper ranks
+    __syncthreads();
+    cl.sync();
+    cl.sync();  // ... and keep this shared memory alive until they have read the flag
 }
 
 // Dynamic shared memory of mcts_kernel (must mirror its carve order).
 size_t mcts_smem_bytes(int n, int PP, int max_nodes, long long n_base, bool node_smem, bool rows_smem) {
+    // n_base: rows of ONE rank's slice
     const size_t nW = static_cast<size_t>(n + 1) * PP;
     size_t off = 0;
     auto carve = [&](size_t bytes) { off = (off + bytes + 15) & ~size_t{15}; };
@@ -582,7 +672,7 @@ size_t mcts_smem_bytes(int n, int PP, int max_nodes, long long n_base, bool node
     carve(8 * nW);
     carve(8 * static_cast<size_t>(n + 1));
     carve(sizeof(Cand) * kMCandCap);
-    carve(sizeof(Cand) * kMMaxK);
+    carve(sizeof(Cand) * 2 * kMMaxK);
     carve(4 * nW);
     carve(nW);
     if (node_smem) {
