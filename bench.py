@@ -390,7 +390,9 @@ def main():
         # roofline of the DOMINANT kernel of this workload by device time: algorithmic bytes =
         # 8 B per packed row scanned (greedy: rows x steps; top-K: its candidate set)
         kern = {"greedy_kernel": (st["greedy_ms"], st["greedy_rows"], st["greedy_calls"]),
-                "topk1_kernel": (st["topk_ms"], st["topk_rows"], st["topk_calls"])}
+                "topk1_kernel": (st["topk_ms"], st["topk_rows"] - st["mcts_rows"],
+                                 st["topk_calls"] - st["mcts_topk_calls"]),
+                "mcts_kernel": (st["mcts_ms"], st["mcts_rows"], st["mcts_launches"])}
         dom = max(kern, key=lambda k: kern[k][0])
         k_ms, k_rows, k_calls = kern[dom]
         launch_s = k_ms / 1e3 / max(k_calls, 1)
@@ -418,7 +420,8 @@ def main():
                                  "resident); the HBM-bound regime is extras.stress_greedy",
                          "peak_kind": peak_kind, "traffic_workload": traffic_wl},
             "clocks": clock,
-            "breakdown": {"greedy_ms": st["greedy_ms"], "topk_ms": st["topk_ms"], "greedy_calls": st["greedy_calls"],
+            "breakdown": {"greedy_ms": st["greedy_ms"], "topk_ms": st["topk_ms"], "mcts_ms": st["mcts_ms"],
+                          "mcts_launches": st["mcts_launches"], "greedy_calls": st["greedy_calls"],
                           "topk_calls": st["topk_calls"], "greedy_rows": st["greedy_rows"],
                           "topk_rows": st["topk_rows"], "greedy_steps": st["greedy_steps"]},
         }

@@ -329,6 +329,10 @@ typedef struct mig_stats {
     int64_t rollout_steps;    /* throughput-mode rollout steps (mig_rollouts)            */
     int64_t rollout_calls;
     double rollout_ms;        /* device time of rollout launches (product)               */
+    double mcts_ms;           /* device time of the device-resident MCTS searches        */
+    int64_t mcts_launches;
+    int64_t mcts_rows;        /* rows scored by those searches' top-Ks (part of topk_rows) */
+    int64_t mcts_topk_calls;  /* their top-K calls (part of topk_calls)                   */
 } mig_stats;
 int mig_ctx_stats(const mig_ctx* ctx, mig_stats* out);
 void mig_ctx_reset_stats(mig_ctx* ctx);

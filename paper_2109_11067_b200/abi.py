@@ -72,7 +72,8 @@ class StatsC(C.Structure):
                 ("ext_events", C.c_int64), ("ext_rows", C.c_int64), ("kernel_launches", C.c_int64),
                 ("h2d_bytes", C.c_int64), ("d2h_bytes", C.c_int64), ("greedy_ms", C.c_double),
                 ("topk_ms", C.c_double), ("phase_ms", C.c_double * 5), ("rollout_steps", C.c_int64),
-                ("rollout_calls", C.c_int64), ("rollout_ms", C.c_double)]
+                ("rollout_calls", C.c_int64), ("rollout_ms", C.c_double), ("mcts_ms", C.c_double),
+                ("mcts_launches", C.c_int64), ("mcts_rows", C.c_int64), ("mcts_topk_calls", C.c_int64)]
 
 
 class RolloutParamsC(C.Structure):

@@ -629,6 +629,10 @@ int mig_ctx_stats(const mig_ctx* ctx, mig_stats* out) {
     out->rollout_steps = s.rollout_steps.load();
     out->rollout_calls = s.rollout_calls.load();
     out->rollout_ms = s.rollout_ns.load() / 1e6;
+    out->mcts_ms = s.mcts_ns.load() / 1e6;
+    out->mcts_launches = s.mcts_launches.load();
+    out->mcts_rows = s.mcts_rows.load();
+    out->mcts_topk_calls = s.mcts_topk_calls.load();
     return MIG_OK;
 }
 

@@ -1166,7 +1166,8 @@ std::vector<MctsDeviceResult> Engine::mcts_device_group(const std::vector<std::v
         CK(cudaStreamSynchronize(s0->stream));
         float ms = 0.f;
         CK(cudaEventElapsedTime(&ms, s0->e0, s0->e1));
-        stats.topk_ns += static_cast<long long>(ms * 1e6);
+        stats.mcts_ns += static_cast<long long>(ms * 1e6);
+        stats.mcts_launches++;
         for (int q = 0; q < nb; ++q) {
             const Off& o = offs[q];
             unsigned char* b = static_cast<unsigned char*>(slots[q]->mcts_mem);
@@ -1201,6 +1202,8 @@ std::vector<MctsDeviceResult> Engine::mcts_device_group(const std::vector<std::v
             // scores its filtered set, every rollout-cache miss the whole base pool
             stats.topk_calls += r.expands + r.builds;
             stats.topk_rows += r.expand_rows + static_cast<long long>(r.builds) * pool_size();
+            stats.mcts_topk_calls += r.expands + r.builds;
+            stats.mcts_rows += r.expand_rows + static_cast<long long>(r.builds) * pool_size();
             stats.h2d += static_cast<long long>(sizeof(double) * n);
             stats.d2h += static_cast<long long>(sizeof(out) + sizeof(int) * (r.trace.size() + best.size() + desc.size()) +
                                                 sizeof(double) * n);

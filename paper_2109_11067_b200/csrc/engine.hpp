@@ -50,10 +50,12 @@ struct Stats {
     std::atomic<long long> greedy_rows{0}, topk_rows{0}, greedy_calls{0}, topk_calls{0}, greedy_steps{0};
     std::atomic<long long> ext_events{0}, ext_rows{0}, launches{0}, h2d{0}, d2h{0};
     std::atomic<long long> greedy_ns{0}, topk_ns{0}, rollout_ns{0}, rollout_steps{0}, rollout_calls{0};
+    std::atomic<long long> mcts_ns{0}, mcts_launches{0}, mcts_rows{0}, mcts_topk_calls{0};
     std::atomic<long long> phase_ns[5] = {0, 0, 0, 0, 0};
     void reset() {
         for (auto* a : {&greedy_rows, &topk_rows, &greedy_calls, &topk_calls, &greedy_steps, &ext_events, &ext_rows,
-                        &launches, &h2d, &d2h, &greedy_ns, &topk_ns, &rollout_ns, &rollout_steps, &rollout_calls})
+                        &launches, &h2d, &d2h, &greedy_ns, &topk_ns, &rollout_ns, &rollout_steps, &rollout_calls,
+                        &mcts_ns, &mcts_launches, &mcts_rows, &mcts_topk_calls})
             a->store(0);
         for (auto& p : phase_ns) p.store(0);
     }
