@@ -375,6 +375,7 @@ const DeviceInfo& device_info(int device) {
         CK(cudaFuncGetAttributes(&fa, k));
         CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 static_cast<int>(prop.sharedMemPerBlockOptin - fa.sharedSizeBytes)));
+        if (k == mcts_kernel_ptr()) info.mcts_static_smem = static_cast<long long>(fa.sharedSizeBytes);
     }
     return cache.emplace(device, info).first->second;
 }
@@ -1135,7 +1136,8 @@ std::vector<MctsDeviceResult> Engine::mcts_device_group(const std::vector<std::v
         const long long slice = ((pool_size() + C - 1) / C + 1) & ~1ll;
         // on-chip placement: the slice first (every top-K scans it twice), then the nodes
         {
-            const long long room = device_info(device_).smem_optin - 8 * 1024;
+            const DeviceInfo& di = device_info(device_);
+            const long long room = di.smem_optin - di.mcts_static_smem - 1024;
             const int mn = static_cast<int>(offs[0].max_nodes);
             L->rows_smem = static_cast<long long>(mcts_smem_bytes(n, m_.PP, mn, slice, false, true)) <= room;
             L->node_smem = static_cast<long long>(mcts_smem_bytes(n, m_.PP, mn, slice, true, L->rows_smem != 0)) <= room;
@@ -1185,8 +1187,8 @@ std::vector<MctsDeviceResult> Engine::mcts_device_group(const std::vector<std::v
                 long long t[5];
                 std::memcpy(t, &out[10], sizeof t);
                 std::fprintf(stderr, "[mcts] solve %d: %.1f ms device, cycles sel %lld expand-host %lld miss-host %lld topk %lld "
-                             "rollout-ctl %lld, builds %d expands %d iters %d\n",
-                             b0 + q, ms, t[0], t[1], t[2], t[3], t[4], out[4], out[7], out[6]);
+                             "rollout-ctl %lld, builds %d expands %d iters %d, exact-path top-Ks (cumulative) %d\n",
+                             b0 + q, ms, t[0], t[1], t[2], t[3], t[4], out[4], out[7], out[6], out[20]);
             }
             r.trace.resize(4 * static_cast<size_t>(r.iterations));
             std::vector<int> best(std::max(r.best_len, 0)), desc(out[2]);

@@ -43,6 +43,7 @@ struct GaParams;
 struct DeviceInfo {
     int num_sms = 0;
     long long smem_optin = 0;
+    long long mcts_static_smem = 0;  // static shared memory of mcts_kernel
 };
 const DeviceInfo& device_info(int device);
 

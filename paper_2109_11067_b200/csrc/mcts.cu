@@ -30,6 +30,7 @@ constexpr int kMWarps = kMThreads / 32;
 constexpr int kMCandCap = 512;  // above-threshold rows per top-K (ties beyond: exact k-round path)
 constexpr int kMMaxK = 32;
 constexpr unsigned char kExpanded = 1, kLeaf = 2;
+constexpr int kL1Slots = 256, kL1MaxK = 16, kL1Empty = -2, kL1Pending = -3;
 
 struct Mt64 {  // std::mt19937_64 (w 64, n 312, m 156, r 31)
     uint64_t mt[312];
@@ -85,6 +86,8 @@ __device__ __forceinline__ float ub_row(const float* Wf, uint64_t row) {
 // detail::topk_candidates (mcts.hpp:56-76) over the base rows (mask: rows touching a masked
 // service, else all), block-wide.  Writes base-pool indices in preference order to out[],
 // returns their count.  Ends with a barrier.
+__device__ unsigned g_mcts_fallbacks = 0;  // diagnostics: exact-path top-Ks (MIGPLAN_MCTS_TIMERS)
+
 __device__ __forceinline__ float ub_half(const float* Wf, unsigned lo, unsigned hi) {
     float s = __fadd_ru(Wf[lo & 0xFFFFu], Wf[lo >> 16]);
     s = __fadd_ru(s, Wf[hi & 0xFFFFu]);
@@ -140,7 +143,44 @@ __device__ int block_topk_exact(const DevModel& M, const uint64_t* base, long lo
             tmax_f = __double2float_rd(sc);
         }
     };
-    for (long long p = threadIdx.x; p < np; p += blockDim.x) {
+    const long long B = blockDim.x;
+    const unsigned sent = static_cast<unsigned>(M.n * M.PP) * 0x00010001u;  // two sentinel codes
+    const uint4 padv = make_uint4(sent, sent, sent, sent);
+    // main body: 8 rows per thread per iteration, bounds and hit flags computed branch-free,
+    // the exact path entered only when one of them reaches the thread's running maximum
+    long long p = threadIdx.x;
+    for (; p + 3 * B < np; p += 4 * B) {
+        const uint4 v[4] = {base2[p], base2[p + B], base2[p + 2 * B], base2[p + 3 * B]};
+        float ub[8];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            ub[2 * q] = ub_half(Wf, v[q].x, v[q].y);
+            ub[2 * q + 1] = ub_half(Wf, v[q].z, v[q].w);
+            if (mask) {
+                const bool h0 = hit_half(hitc, v[q].x, v[q].y), h1 = hit_half(hitc, v[q].z, v[q].w);
+                hits += h0 + h1;
+                if (!h0) ub[2 * q] = 0.0f;
+                if (!h1) ub[2 * q + 1] = 0.0f;
+            }
+        }
+        float mx = ub[0];
+#pragma unroll
+        for (int j = 1; j < 8; ++j) mx = fmaxf(mx, ub[j]);
+        if (mx > 0.0f && mx >= tmax_f) {
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                if (!(ub[j] > 0.0f) || ub[j] < tmax_f) continue;
+                const uint4& w = v[j >> 1];
+                const unsigned lo = (j & 1) ? w.z : w.x, hi = (j & 1) ? w.w : w.y;
+                const double sc = row_score(W, (static_cast<uint64_t>(hi) << 32) | lo);
+                if (sc > tmax) {
+                    tmax = sc;
+                    tmax_f = __double2float_rd(sc);
+                }
+            }
+        }
+    }
+    for (; p < np; p += B) {
         const uint4 v = base2[p];
         visit1(v.x, v.y);
         visit1(v.z, v.w);
@@ -176,17 +216,28 @@ __device__ int block_topk_exact(const DevModel& M, const uint64_t* base, long lo
             if (take && at < kMCandCap) cand[at] = Cand{sc, row_usum(U, row), row, pos};
         }
     };
-    const long long np_pad = (np + blockDim.x - 1) / blockDim.x * blockDim.x;  // warp-uniform trip count
-    for (long long p = threadIdx.x; p < np_pad; p += blockDim.x) {
-        uint4 v = make_uint4(0u, 0u, 0u, 0u);
-        const bool in = p < np;
-        if (in) v = base2[p];
-        else {  // padding lanes: sentinel rows (score 0)
-            const unsigned sent = static_cast<unsigned>(M.n * M.PP) * 0x00010001u;
-            v = make_uint4(sent, sent, sent, sent);
+    // warp-uniform trip count: 4 row pairs per thread per iteration, padding = sentinel rows;
+    // a warp skips a group at once when no lane's bound reaches T (one vote)
+    const long long np4 = (np + 4 * B - 1) / (4 * B) * (4 * B);
+    for (long long p0 = threadIdx.x; p0 < np4; p0 += 4 * B) {
+        uint4 v[4];
+        float ub[8];
+        float mx = 0.0f;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const long long pp = p0 + q * B;
+            v[q] = pp < np ? base2[pp] : padv;
+            ub[2 * q] = ub_half(Wf, v[q].x, v[q].y);
+            ub[2 * q + 1] = ub_half(Wf, v[q].z, v[q].w);
+            mx = fmaxf(mx, fmaxf(ub[2 * q], ub[2 * q + 1]));
         }
-        visit2(v.x, v.y, pos0 + 2 * p);
-        visit2(v.z, v.w, pos0 + 2 * p + 1);
+        if (!__any_sync(0xffffffffu, mx > 0.0f && mx >= T_f)) continue;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const long long pp = p0 + q * B;
+            visit2(v[q].x, v[q].y, pos0 + 2 * pp);
+            visit2(v[q].z, v[q].w, pos0 + 2 * pp + 1);
+        }
     }
     if (nb & 1) {  // last odd row, warp 0 (ballot needs the whole warp)
         if ((threadIdx.x >> 5) == 0) {
@@ -202,6 +253,7 @@ __device__ int block_topk_exact(const DevModel& M, const uint64_t* base, long lo
         got = min(nc, k);
         rank_select(M, cand, nc, k, win);
     } else {  // pathological ties at T: exact k rounds of "best row strictly after the previous"
+        if (threadIdx.x == 0) atomicAdd(&g_mcts_fallbacks, 1u);
         got = 0;
         Cand last{0.0, 0.0, kNoRow, -1};
         for (int r = 0; r < k; ++r) {
@@ -384,6 +436,16 @@ __global__ void __launch_bounds__(kMThreads, 1) mcts_kernel(const __grid_constan
     __shared__ int s_edges, s_path, s_best, s_have, s_nodes, s_builds, s_iters, s_scored, s_expands;
     __shared__ long long s_expand_rows;
     __shared__ int s_out[kMMaxK];
+    // on-chip level of the rollout cache: kL1Slots keys (filled to 3/4) with their pools
+    __shared__ uint64_t l1_key[kL1Slots][4];
+    __shared__ int l1_n[kL1Slots];
+    __shared__ unsigned l1_pool[kL1Slots][kL1MaxK];
+    __shared__ int l1_used, s_l1, s_l1new;
+    const bool use_l1 = K <= kL1MaxK;
+    for (int q = threadIdx.x; q < kL1Slots; q += blockDim.x) l1_n[q] = kL1Empty;
+    if (threadIdx.x == 0) l1_used = 0;
+    // rows by pool index for the utility adds: the on-chip copy when it holds the whole pool
+    const uint64_t* prow = (C == 1 && L.rows_smem) ? slice : rows;
     const int max_depth = 2 * a.l_ref;
     const int tid = threadIdx.x;
     long long t_sel = 0, t_exp = 0, t_miss = 0, t_roll = 0, t_topk = 0, tc = 0;  // thread-0 clock64 phase split
@@ -497,7 +559,7 @@ __global__ void __launch_bounds__(kMThreads, 1) mcts_kernel(const __grid_constan
                             const int c = first + q;
                             double* cc = a.node_comp + static_cast<long long>(c) * n;
                             for (int i = 0; i < n; ++i) cc[i] = cur[i];
-                            add_row_util(M, Us, rows[s_out[q]], cc);
+                            add_row_util(M, Us, prow[s_out[q]], cc);
                             ncand[c] = s_out[q];
                             nvis[c] = 0;
                             nval[c] = 0.0;
@@ -550,23 +612,47 @@ __global__ void __launch_bounds__(kMThreads, 1) mcts_kernel(const __grid_constan
                             h *= 0xbf58476d1ce4e5b9ull;
                             h ^= h >> 31;
                         }
-                        unsigned sl = static_cast<unsigned>(h) & a.tab_mask;
-                        for (unsigned t = 0;; ++t, sl = (sl + 1) & a.tab_mask) {
-                            if (t > a.tab_mask) {
-                                s_abort = 2;  // cache full
-                                break;
+                        // level 1: the on-chip copy of the cache (keys + pools in shared memory)
+                        s_l1 = -1;
+                        s_l1new = -1;
+                        if (use_l1) {
+                            unsigned q = static_cast<unsigned>(h >> 32) & (kL1Slots - 1);
+                            for (int t = 0; t < kL1Slots; ++t, q = (q + 1) & (kL1Slots - 1)) {
+                                if (l1_n[q] == kL1Empty) break;
+                                if (l1_key[q][0] == kw[0] && l1_key[q][1] == kw[1] && l1_key[q][2] == kw[2] &&
+                                    l1_key[q][3] == kw[3]) {
+                                    s_l1 = static_cast<int>(q);
+                                    break;
+                                }
                             }
-                            if (!a.tag[sl]) {  // miss: insert, pool built below
-                                a.tag[sl] = 1;
-                                for (int w = 0; w < 4; ++w) a.key[4ull * sl + w] = kw[w];
-                                s_miss = 1;
-                                break;
-                            }
-                            if (a.key[4ull * sl] == kw[0] && a.key[4ull * sl + 1] == kw[1] &&
-                                a.key[4ull * sl + 2] == kw[2] && a.key[4ull * sl + 3] == kw[3])
-                                break;
                         }
-                        s_slot = static_cast<int>(sl);
+                        if (s_l1 < 0) {  // level 2: the global table (source of truth)
+                            unsigned sl = static_cast<unsigned>(h) & a.tab_mask;
+                            for (unsigned t = 0;; ++t, sl = (sl + 1) & a.tab_mask) {
+                                if (t > a.tab_mask) {
+                                    s_abort = 2;  // cache full
+                                    break;
+                                }
+                                if (!a.tag[sl]) {  // miss: insert, pool built below
+                                    a.tag[sl] = 1;
+                                    for (int w = 0; w < 4; ++w) a.key[4ull * sl + w] = kw[w];
+                                    s_miss = 1;
+                                    break;
+                                }
+                                if (a.key[4ull * sl] == kw[0] && a.key[4ull * sl + 1] == kw[1] &&
+                                    a.key[4ull * sl + 2] == kw[2] && a.key[4ull * sl + 3] == kw[3])
+                                    break;
+                            }
+                            s_slot = static_cast<int>(sl);
+                            if (s_miss && use_l1 && l1_used < kL1Slots * 3 / 4) {  // mirror the new key on chip
+                                unsigned q = static_cast<unsigned>(h >> 32) & (kL1Slots - 1);
+                                while (l1_n[q] != kL1Empty) q = (q + 1) & (kL1Slots - 1);
+                                for (int w = 0; w < 4; ++w) l1_key[q][w] = kw[w];
+                                l1_n[q] = kL1Pending;
+                                ++l1_used;
+                                s_l1new = static_cast<int>(q);
+                            }
+                        }
                     }
                 }
                 __syncthreads();
@@ -577,21 +663,27 @@ __global__ void __launch_bounds__(kMThreads, 1) mcts_kernel(const __grid_constan
                     const int got = cluster_topk(false, s_out, &s_scored);
                     tick(t_topk);
                     if (tid < got) a.pool[static_cast<long long>(s_slot) * K + tid] = static_cast<unsigned>(s_out[tid]);
+                    if (s_l1new >= 0 && tid < got) l1_pool[s_l1new][tid] = static_cast<unsigned>(s_out[tid]);
                     if (tid == 0) {
                         a.pool_n[s_slot] = got;
+                        if (s_l1new >= 0) {
+                            l1_n[s_l1new] = got;
+                            s_l1 = s_l1new;
+                        }
                         ++s_builds;
                     }
                     __syncthreads();
                     tick(t_miss);
                 }
                 if (tid == 0) {
-                    const int pn = a.pool_n[s_slot];
+                    const int pn = s_l1 >= 0 ? l1_n[s_l1] : a.pool_n[s_slot];
                     if (pn <= 0) {
                         s_abort = 1;  // "rollout: no candidate config serves the remaining demand"
                     } else {
-                        const int idx = static_cast<int>(a.pool[static_cast<long long>(s_slot) * K +
-                                                                mt_pick(g, static_cast<uint64_t>(pn))]);
-                        add_row_util(M, Us, rows[idx], cur);
+                        const unsigned pk = static_cast<unsigned>(mt_pick(g, static_cast<uint64_t>(pn)));
+                        const int idx = static_cast<int>(s_l1 >= 0 ? l1_pool[s_l1][pk]
+                                                                   : a.pool[static_cast<long long>(s_slot) * K + pk]);
+                        add_row_util(M, Us, prow[idx], cur);
                         a.picked[s_steps++] = idx;
                     }
                 }
@@ -654,6 +746,7 @@ __global__ void __launch_bounds__(kMThreads, 1) mcts_kernel(const __grid_constan
         reinterpret_cast<long long*>(a.out)[7] = t_miss;  // out[14..15]
         reinterpret_cast<long long*>(a.out)[8] = t_topk;  // out[16..17]
         reinterpret_cast<long long*>(a.out)[9] = t_roll;  // out[18..19]
+        a.out[20] = static_cast<int>(g_mcts_fallbacks);
         reinterpret_cast<long long*>(a.out)[4] = s_expand_rows;  // out[8..9]
     }
     if (threadIdx.x == 0) s_exit = 1;  // release the helper ranks
