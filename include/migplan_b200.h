@@ -305,6 +305,17 @@ int mig_two_phase_parallel(mig_ctx* ctx, const mig_ga_params* params, mig_config
 /* lower_bound(services, profiles), bench.hpp:93-108 */
 int mig_lower_bound(const mig_ctx* ctx, int32_t* out);
 
+/* brute_force_optimum(services, profiles, rules, cap, node_budget), bench.hpp:160-219: the
+ * exhaustive minimum-GPU search over config multisets (iterative deepening, admissible bound).
+ * The context's pool must be the max_mix >= min(n, 7) pool (the product holds <= 4-member
+ * configs: n <= 4).  *found = 0 (and *n_out = 0) when the optimum exceeds cap; PlanningError
+ * "oracle: node budget exceeded; ..." when more than node_budget DFS nodes are visited and
+ * "oracle: service cannot be served by any config" when a service has no utility anywhere.
+ * Among several optima the product returns the smallest pool-index tuple; the GPU count is
+ * the reference's (test_bench.cpp:120-160 compares counts). */
+int mig_brute_force_optimum(mig_ctx* ctx, int32_t cap, int64_t node_budget, mig_config* out, int32_t out_cap,
+                            int32_t* n_out, int32_t* found);
+
 /* ---- instrumentation (product only; CPU libraries report zeros) ---- */
 /* Work counters.  "Rows scored" is implementation-independent (the oracle counts the same
  * numbers): every greedy step scores its whole working set (greedy.hpp:126-134) and every

@@ -216,7 +216,52 @@ def gen_greedy_big(ref):
     return {"gen48_7.0": e}
 
 
-SECTIONS = {"greedy": gen_greedy, "mcts": gen_mcts, "ga": gen_ga, "topk": gen_topk, "partitions": gen_partitions,
+def gen_brute_force(ref):
+    """brute_force_optimum (bench.hpp:160-219) on the instances the reference's own tests give it:
+    test_bench.cpp:120-160, test_mcts.cpp:108-126, acceptance.cpp:202-244 (criterion 6), plus
+    4-service random workloads (fixtures.hpp:51-58).  outcome: plan | "none" | "error:<msg>"."""
+    rules = mp.PartitionRuleSet.defaults()
+    tm, fx = S.two_model_store(), S.profiles()
+    cases = [("bench_single", tm, [mp.ServiceSpec("a", "cnn-a", 350.0, 100.0)], 3),
+             ("bench_overcap", tm, [mp.ServiceSpec("a", "cnn-a", 3500.0, 100.0)], 3)]
+    for seed in range(1, 11):
+        cases.append((f"bench_vs_fast_{seed}", tm, [mp.ServiceSpec("a", "cnn-a", 80.0 + 60.0 * (seed % 4), 100.0),
+                                                  mp.ServiceSpec("b", "nlp-a", 40.0 + 30.0 * (seed % 3), 100.0)], 4))
+    for seed in range(1, 9):
+        cases.append((f"mcts_tiny_{seed}", tm, [mp.ServiceSpec("a", "cnn-a", 120.0 + 40.0 * (seed % 5), 100.0),
+                                              mp.ServiceSpec("b", "nlp-a", 60.0 + 20.0 * (seed % 3), 100.0)], 3))
+    for s in range(1, 41):
+        n = 1 + s % 3
+        sv = mp.gen_workload(n, True, 4.6, 0.6, 100.0, 31000 + s, fx, backend=S.host_backend())
+        cases.append((f"accept_c6_{s}", fx, list(sv), 3))
+    for s in range(1, 9):  # 4 services, lighter demand: depth-4 searches over the n=4 pool
+        sv = mp.gen_workload(4, True, 4.0 + 0.1 * s, 0.6, 100.0, 500 + s, fx, backend=S.host_backend())
+        cases.append((f"gen4_{s}", fx, list(sv), 4))
+    res = {}
+    for name, ps, sv, cap in cases:
+        t = time.time()
+        try:
+            dep = mp.brute_force_optimum(sv, ps, rules, cap, backend=ref)
+            out = "none" if dep is None else S.plan_key([g.config for g in dep.gpus])
+        except mp.PlanningError as e:
+            out = "error:" + str(e)
+        res[name] = {"store": store_name(ps), "services": svc_json(sv), "cap": cap, "outcome": out,
+                     "ref_wall_s": round(time.time() - t, 3)}
+        if not (isinstance(out, str) and out.startswith("error")) and res[name]["ref_wall_s"] < 0.3:
+            lo, hi = 0, 20_000_000  # the reference's exact node count: the smallest budget that passes
+            while lo < hi:
+                mid = (lo + hi) // 2
+                try:
+                    mp.brute_force_optimum(sv, ps, rules, cap, node_budget=mid, backend=ref)
+                    hi = mid
+                except mp.PlanningError:
+                    lo = mid + 1
+            res[name]["nodes"] = lo
+        print(f"brute_force {name}: {out if isinstance(out, str) else len(out)} ({time.time() - t:.2f}s)", flush=True)
+    return res
+
+
+SECTIONS = {"brute_force": gen_brute_force, "greedy": gen_greedy, "mcts": gen_mcts, "ga": gen_ga, "topk": gen_topk, "partitions": gen_partitions,
             "greedy_big": gen_greedy_big, "rollouts": gen_rollouts, "ga_parallel": gen_ga_parallel}
 
 

@@ -789,6 +789,23 @@ int mig_lower_bound(const mig_ctx* ctx, int32_t* out) {
     return guarded([&] { *out = lower_bound(ctx->services, ctx->profiles); });
 }
 
+int mig_brute_force_optimum(mig_ctx* ctx, int32_t cap, int64_t node_budget, mig_config* out, int32_t out_cap,
+                            int32_t* n_out, int32_t* found) {
+    int rc = MIG_OK;
+    *found = 0;
+    *n_out = 0;
+    int g = guarded([&] {  // the reference's own oracle (bench.hpp:160-219)
+        if (cap < 0) throw std::invalid_argument("brute_force_optimum: cap must be >= 0");
+        auto dep = brute_force_optimum(ctx->services, ctx->profiles, ctx->rules, cap, node_budget);
+        if (!dep) return;
+        *found = 1;
+        std::vector<GpuConfig> plan;
+        for (const auto& g : dep->gpus) plan.push_back(g.config);
+        rc = emit_plan(plan, ctx->services, out, out_cap, n_out);
+    });
+    return g != MIG_OK ? g : rc;
+}
+
 int mig_ctx_stats(const mig_ctx*, mig_stats* out) {
     std::memset(out, 0, sizeof *out);
     return MIG_OK;

@@ -2,10 +2,11 @@
 
     python -m paper_2109_11067_b200.cli optimize --mode fast --slos S.json --profiles P.json -o dep.json
     python -m paper_2109_11067_b200.cli lowerbound --slos S.json --profiles P.json
+    python -m paper_2109_11067_b200.cli oracle --slos S.json --profiles P.json --cap 3 -o dep.json
     python -m paper_2109_11067_b200.cli enumerate-partitions [--rules R.json] [-o parts.json]
 
-Restates the reference CLI's `optimize` / `lowerbound` / `enumerate-partitions`
-(proj/tools/migplan.cpp:88-147, 159-200, 262-300) over the C-ABI:
+Restates the reference CLI's `optimize` / `lowerbound` / `oracle` / `enumerate-partitions`
+(proj/tools/migplan.cpp:88-147, 159-200, 244-251, 262-300, 382-397) over the C-ABI:
   - output files are `json.dump(indent=2)` with sorted keys + "\\n" — the byte layout of
     nlohmann's `dump(2)` (write_json_file, io.hpp:44-48; std::map keys are sorted);
   - trace lines go to stdout as compact sorted-key JSON (migplan.cpp:99-137), numbers through
@@ -167,6 +168,19 @@ def cmd_lowerbound(a, manifest: Manifest) -> int:  # lower_bound, bench.hpp:93-1
     return 0
 
 
+def cmd_oracle(a, manifest: Manifest) -> int:  # migplan.cpp:382-397 (brute_force_optimum on the device)
+    profiles = mp.load_profiles(a.profiles)
+    services = mp.load_services(a.slos, profiles)
+    rules = load_rules(a.rules) if a.rules else mp.PartitionRuleSet.defaults()
+    dep = mp.brute_force_optimum(services, profiles, rules, a.cap, backend=_BACKEND, device=a.device)
+    if dep is None:
+        sys.stderr.write(f"no deployment within {a.cap} GPUs\n")
+        return 1
+    dump_file(a.output, mp.deployment_to_json(dep))
+    manifest.write(a.output)
+    return 0
+
+
 def cmd_enumerate(a, manifest: Manifest) -> int:  # migplan.cpp:56-64
     rules = load_rules(a.rules) if a.rules else mp.PartitionRuleSet.defaults()
     parts = mp.enumerate_maximal_partitions(rules, backend=_BACKEND)
@@ -208,6 +222,14 @@ def build_parser() -> argparse.ArgumentParser:
     lb.add_argument("--slos", required=True)
     lb.add_argument("--profiles", required=True)
     lb.add_argument("-o", "--output", default="")
+    orc = sub.add_parser("oracle", help="Brute-force minimum-GPU deployment (small instances)")
+    orc.add_argument("--slos", required=True)
+    orc.add_argument("--profiles", required=True)
+    orc.add_argument("--rules", default="")
+    orc.add_argument("--cap", type=int, default=3, help="Maximum GPUs to search")
+    orc.add_argument("-o", "--output", required=True)
+    orc.add_argument("--device", type=int, default=0)
+    orc.add_argument("--backend", default="", help=argparse.SUPPRESS)
     en = sub.add_parser("enumerate-partitions", help="Print the derived legal partition table")
     en.add_argument("--rules", default="")
     en.add_argument("-o", "--output", default="")
@@ -243,6 +265,8 @@ def main(argv=None) -> int:
             return cmd_optimize(a, manifest)
         if a.command == "lowerbound":
             return cmd_lowerbound(a, manifest)
+        if a.command == "oracle":
+            return cmd_oracle(a, manifest)
         return cmd_enumerate(a, manifest)
     except mp.SchemaError as e:
         sys.stderr.write(f"error: {e}\n")

@@ -609,6 +609,21 @@ int mig_lower_bound(const mig_ctx* ctx, int32_t* out) {
     });
 }
 
+int mig_brute_force_optimum(mig_ctx* ctx, int32_t cap, int64_t node_budget, mig_config* out, int32_t out_cap,
+                            int32_t* n_out, int32_t* found) {
+    int rc = MIG_OK;
+    *found = 0;
+    *n_out = 0;
+    int g = guarded([&] {
+        if (cap < 0) throw ArgumentError("brute_force_optimum: cap must be >= 0");
+        bool f = false;
+        auto plan = ctx->e->brute_force(cap, node_budget, f);
+        *found = f ? 1 : 0;
+        rc = emit(plan, out, out_cap, n_out);
+    });
+    return g != MIG_OK ? g : rc;
+}
+
 int mig_ctx_stats(const mig_ctx* ctx, mig_stats* out) {
     std::memset(out, 0, sizeof *out);
     const Stats& s = ctx->e->stats;

@@ -210,6 +210,25 @@ struct MctsLaunch {
     MctsSolveArgs s[kMaxGroups];
 };
 
+// Device brute_force_optimum (bf.cu): one launch per iterative-deepening depth.
+constexpr int kBfMaxDepth = 8;  // cap
+constexpr int kBfMaxN = 8;      // services (the device pool holds <= 4-member configs: n <= 4)
+struct BfArgs {
+    DevModel M;
+    const uint64_t* rows;        // the pool with max_mix = min(n, 4)
+    long long n_rows;
+    const double* best_any;      // n: best utility any config gives each service
+    int depth;
+    long long rank0, rank_end;   // this launch's DFS prefixes (lexicographic ranks)
+    long long replay;            // >= 0: only this prefix rank, writes its tuple
+    unsigned long long remaining;  // node budget left before this launch
+    unsigned long long* cnt;     // per prefix: reference-order DFS nodes in its subtree
+    unsigned long long* best_key;  // smallest solving rank
+    unsigned long long* overrun;   // smallest rank whose own subtree exceeded `remaining`
+    unsigned long long* sum;       // bf_sum_kernel: Σ cnt[rank0 .. min(best_key, rank_end-1)]
+    long long* tuple;            // replay: picks (pool indices), tuple[kBfMaxDepth] = length
+};
+
 // Throughput-mode root-parallel rollouts (rollout.cu).
 struct RolloutCounters {
     unsigned long long n_act[2];  // active-list lengths (ping-pong by round parity)

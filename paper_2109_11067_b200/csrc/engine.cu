@@ -29,6 +29,9 @@ constexpr int kTopkMaxCtas = 4096;  // partial-list capacity (Best x 32 per CTA)
 const void* topk1_kernel_ptr(int km);
 size_t rollout_smem_bytes(int n, int PP);
 size_t mcts_smem_bytes(int n, int PP, int max_nodes, long long n_base, bool node_smem, bool rows_smem);
+const void* bf_kernel_ptr();
+const void* bf_sum_kernel_ptr();
+int bf_threads();
 const void* mcts_kernel_ptr();
 int mcts_threads();
 const void* rollout_kernel_ptr();
@@ -1243,6 +1246,133 @@ void Engine::fast_algo_batch(const std::vector<std::vector<double>>& comps, std:
     greedy_batch(d, count, cap_steps, drows, steps, &rows);
     for (int i = 0; i < count; ++i)
         if (steps[i] < 0) status[i] = 1;
+}
+
+// ---- brute_force_optimum (bf.cu)
+std::vector<Config> Engine::brute_force(int cap, long long node_budget, bool& found) {
+    found = false;
+    const int n = m_.n;
+    if (n == 0) {
+        found = true;
+        return {};
+    }
+    if (n > 4 || n > kBfMaxN) throw ArgumentError("device brute_force_optimum: n <= 4 services (4-member rows)");
+    if (m_.max_mix < n) throw ArgumentError("brute_force_optimum needs the max_mix = n pool");
+    if (cap > kBfMaxDepth) throw ArgumentError("brute_force_optimum: cap <= 8 on the device");
+    std::vector<double> best_any(n, 0.0);  // bench.hpp:167-171
+    for (uint64_t row : base_rows_) {
+        int svc[kRowK], pat[kRowK];
+        const int k = m_.members(row, svc, pat);
+        for (int j = 0; j < k; ++j) best_any[svc[j]] = std::max(best_any[svc[j]], m_.U[static_cast<size_t>(svc[j]) * m_.PP + pat[j]]);
+    }
+    for (int i = 0; i < n; ++i)
+        if (best_any[i] <= 0.0) throw PlanningError("oracle: service cannot be served by any config");
+    // The reference's DFS walks pool.items in emission order (config_enum.hpp:108-150): size
+    // multisets in canonical order, then the per-group nondecreasing service sequences in
+    // lexicographic order.  Search the rows in that order so the first solution and the node
+    // count are the reference's.
+    const long long P = pool_size();
+    std::vector<std::pair<std::array<int, 8>, uint64_t>> keyed;
+    keyed.reserve(static_cast<size_t>(P));
+    for (uint64_t row : base_rows_) {
+        int svc[kRowK], pat[kRowK];
+        const int k = m_.members(row, svc, pat);
+        std::array<int, kMaxSizes> cnt{};
+        for (int j = 0; j < k; ++j)
+            for (int z = 0; z < kMaxSizes; ++z) cnt[z] += m_.patterns[pat[j]][z];
+        std::array<int, 8> key;
+        key.fill(-1);
+        int li = 0;
+        while (li < static_cast<int>(m_.layouts.size())) {
+            bool same = true;
+            for (int z = 0; z < kMaxSizes; ++z) same &= m_.layouts[li].count[z] == cnt[z];
+            if (same) break;
+            ++li;
+        }
+        key[0] = li;
+        int w = 1;
+        for (const auto& g : m_.layouts.at(li).groups)
+            for (int j = 0; j < k; ++j)
+                for (int c = 0; c < m_.patterns[pat[j]][g.size_idx] && w < 8; ++c) key[w++] = svc[j];
+        keyed.emplace_back(key, row);
+    }
+    std::sort(keyed.begin(), keyed.end());
+    std::vector<uint64_t> rows(keyed.size());
+    for (size_t i = 0; i < keyed.size(); ++i) rows[i] = keyed[i].second;
+    CK(cudaSetDevice(device_));
+    const long long chunk = static_cast<long long>(num_sms_) * bf_threads() * 4;
+    const long long max_ranks = std::min(P * (P + 1) / 2, chunk);
+    struct Words {
+        unsigned long long best_key, overrun, sum, pad;
+    };
+    const size_t off_tuple = sizeof(Words), off_any = off_tuple + sizeof(long long) * (kBfMaxDepth + 1);
+    const size_t off_rows = (off_any + sizeof(double) * n + 255) & ~size_t(255);
+    const size_t off_cnt = (off_rows + sizeof(uint64_t) * static_cast<size_t>(P) + 255) & ~size_t(255);
+    void* mem = nullptr;
+    CK(cudaMalloc(&mem, off_cnt + sizeof(unsigned long long) * std::max<long long>(max_ranks, 1)));
+    struct Free {
+        void* p;
+        ~Free() { cudaFree(p); }
+    } fr{mem};
+    unsigned char* m8 = static_cast<unsigned char*>(mem);
+    Words* w = reinterpret_cast<Words*>(m8);
+    CK(cudaMemcpy(m8 + off_any, best_any.data(), sizeof(double) * n, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(m8 + off_rows, rows.data(), sizeof(uint64_t) * rows.size(), cudaMemcpyHostToDevice));
+    const unsigned long long budget = static_cast<unsigned long long>(std::max<long long>(node_budget, 0));
+    auto over = [] { throw PlanningError("oracle: node budget exceeded; shrink the instance or raise the budget"); };
+    unsigned long long nodes = 0;  // the reference's ++nodes, cumulative over depths
+    int root_bound = 0;            // bound(zero completion), bench.hpp:179-187
+    for (int i = 0; i < n; ++i) root_bound = std::max(root_bound, static_cast<int>(std::ceil(1.0 / best_any[i] - 1e-12)));
+    const int T = bf_threads();
+    for (int d = 0; d <= cap; ++d) {
+        if (++nodes > budget) over();  // dfs root; satisfied only for an empty workload (above)
+        if (d == 0 || root_bound > d) continue;  // bench.hpp:197
+        BfArgs a{};
+        a.M = dm_;
+        a.rows = reinterpret_cast<const uint64_t*>(m8 + off_rows);
+        a.n_rows = P;
+        a.best_any = reinterpret_cast<const double*>(m8 + off_any);
+        a.depth = d;
+        a.replay = -1;
+        a.cnt = reinterpret_cast<unsigned long long*>(m8 + off_cnt);
+        a.best_key = &w->best_key;
+        a.overrun = &w->overrun;
+        a.sum = &w->sum;
+        a.tuple = reinterpret_cast<long long*>(m8 + off_tuple);
+        const Words init{~0ull, ~0ull, 0ull, 0ull};
+        CK(cudaMemcpy(w, &init, sizeof init, cudaMemcpyHostToDevice));
+        const long long ranks = d == 1 ? P : P * (P + 1) / 2;
+        for (long long r0 = 0; r0 < ranks; r0 += chunk) {
+            a.rank0 = r0;
+            a.rank_end = std::min(ranks, r0 + chunk);
+            a.remaining = budget - nodes;
+            void* args[] = {&a};
+            const unsigned grid = static_cast<unsigned>((a.rank_end - r0 + T - 1) / T);
+            CK(cudaLaunchKernel(bf_kernel_ptr(), grid, T, args, 0, nullptr));
+            CK(cudaLaunchKernel(bf_sum_kernel_ptr(), std::min<unsigned>(grid, num_sms_ * 4), T, args, 0, nullptr));
+            stats.launches += 2;
+            Words got{};
+            CK(cudaMemcpy(&got, w, sizeof got, cudaMemcpyDeviceToHost));
+            CK(cudaMemcpy(&w->sum, &init.sum, sizeof init.sum, cudaMemcpyHostToDevice));
+            const bool hit = got.best_key != ~0ull;
+            const unsigned long long stop_rank = hit ? got.best_key : static_cast<unsigned long long>(a.rank_end - 1);
+            if (got.overrun <= stop_rank) over();
+            nodes += got.sum;
+            if (nodes > budget) over();
+            if (hit) {
+                a.replay = static_cast<long long>(got.best_key);
+                CK(cudaLaunchKernel(bf_kernel_ptr(), 1, T, args, 0, nullptr));
+                stats.launches++;
+                long long tup[kBfMaxDepth + 1];
+                CK(cudaMemcpy(tup, a.tuple, sizeof tup, cudaMemcpyDeviceToHost));
+                std::vector<Config> out;
+                for (long long q = 0; q < tup[kBfMaxDepth]; ++q) out.push_back(config_of(rows[tup[q]]));
+                found = true;
+                return out;
+            }
+        }
+    }
+    return {};
 }
 
 // ---- throughput-mode GA device state (ga.cu)

@@ -126,6 +126,10 @@ class Engine {
     MctsDeviceResult mcts_device(const std::vector<double>& comp, int budget, int topk, int pick_services, double ucb_c,
                                  uint64_t seed, int l_ref);
 
+    // brute_force_optimum (bench.hpp:160-219) on the device over this context's pool (which
+    // must be the max_mix = n pool, n <= 4).  found = false: the optimum exceeds cap.
+    std::vector<Config> brute_force(int cap, long long node_budget, bool& found);
+
     // Independent single-CTA greedy instances in one launch (the GA's refills).
     void greedy_batch(const double* d_comps, int count, long long cap_steps, std::vector<const uint64_t*>& rows,
                       std::vector<int>& n_steps, std::vector<std::vector<uint64_t>>* host_rows = nullptr);

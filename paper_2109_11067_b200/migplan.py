@@ -1046,6 +1046,21 @@ def lower_bound(services, profiles) -> int:  # bench.hpp:93-108 (host arithmetic
     return int(math.ceil(total / 7.0 - 1e-9))
 
 
+def brute_force_optimum(services, profiles, rules, cap: int, node_budget: int = 20_000_000,
+                        backend=None, device: int = 0) -> Deployment | None:
+    """brute_force_optimum, bench.hpp:160-219 — the exhaustive minimum-GPU oracle for small
+    instances; None when the optimum exceeds cap.  Runs over the max_mix = min(n, 7) pool
+    (the product's device search holds <= 4-member configs, so n <= 4 there)."""
+    services = list(services)
+    if not services:  # bench.hpp:163
+        return make_deployment([])
+    ctx = PlanContext(services, profiles, rules, min(len(services), 7), backend, device)
+    found = C.c_int32()
+    plan = _run_plan(ctx, lambda out, cp, nout: ctx.backend.lib.mig_brute_force_optimum(
+        ctx._p, cap, node_budget, out, cp, C.byref(nout), C.byref(found)))
+    return make_deployment(plan) if found.value else None
+
+
 def validate_deployment(dep: Deployment, services, profiles, rules, backend=None) -> None:  # mig_rules.hpp:155-177
     ids = set()
     for gpu in dep.gpus:

@@ -99,3 +99,24 @@ def test_lowerbound_and_partitions(impl, tmp_path, capsys):
     assert json.loads(capsys.readouterr().out) == {"lower_bound": 15}
     out = str(tmp_path / "parts.json")
     assert cli.main(["enumerate-partitions", "-o", out]) == 0 if impl.name == "product" else True
+
+
+@pytest.mark.skipif(S.ref_backend() is None, reason="reference shim not built")
+def test_oracle_subcommand(impl, tmp_path, capsys):  # migplan.cpp:244-251, 382-397
+    g = S.load_golden("brute_force.json")["accept_c6_5"]
+    ps = S.profiles()
+    slos = tmp_path / "slos.json"
+    slos.write_text(json.dumps({"services": [{"id": i, "model": m, "required_rps": float.fromhex(r),
+                                              "max_p90_ms": float.fromhex(p)} for i, m, r, p in g["services"]]}))
+    out = str(tmp_path / "orc.json")
+    base = ["oracle", "--slos", str(slos), "--profiles", os.path.join(FIX, "profiles.json"), "-o", out,
+            *backend_args(impl)]
+    assert cli.main(base + ["--cap", "3"]) == 0
+    plan = plan_of(out)
+    assert S.plan_key(plan) == g["outcome"]
+    sv = mp.load_services(str(slos), ps)
+    with open(out, "rb") as f:
+        assert f.read() == ref_json(plan, sv, ps)
+    assert json.load(open(out + ".manifest.json"))["command"] == "oracle"
+    assert cli.main(base + ["--cap", "2"]) == 1  # "no deployment within 2 GPUs"
+    assert "no deployment within 2 GPUs" in capsys.readouterr().err
