@@ -31,6 +31,7 @@ size_t rollout_smem_bytes(int n, int PP);
 size_t mcts_smem_bytes(int n, int PP, int max_nodes, long long n_base, bool node_smem, bool rows_smem);
 const void* bf_kernel_ptr();
 const void* bf_sum_kernel_ptr();
+const void* bf_warp_kernel_ptr();
 int bf_threads();
 const void* mcts_kernel_ptr();
 int mcts_threads();
@@ -1300,8 +1301,10 @@ std::vector<Config> Engine::brute_force(int cap, long long node_budget, bool& fo
     std::vector<uint64_t> rows(keyed.size());
     for (size_t i = 0; i < keyed.size(); ++i) rows[i] = keyed[i].second;
     CK(cudaSetDevice(device_));
-    const long long chunk = static_cast<long long>(num_sms_) * bf_threads() * 4;
-    const long long max_ranks = std::min(P * (P + 1) / 2, chunk);
+    // depth 1-2: a thread per prefix; depth >= 3: a warp per two-pick prefix (bf.cu)
+    const long long chunk_t = static_cast<long long>(num_sms_) * bf_threads() * 4;
+    const long long chunk_w = static_cast<long long>(num_sms_) * 64 * 8;
+    const long long max_ranks = std::min(P * (P + 1) / 2, std::max(chunk_t, chunk_w));
     struct Words {
         unsigned long long best_key, overrun, sum, pad;
     };
@@ -1342,13 +1345,17 @@ std::vector<Config> Engine::brute_force(int cap, long long node_budget, bool& fo
         const Words init{~0ull, ~0ull, 0ull, 0ull};
         CK(cudaMemcpy(w, &init, sizeof init, cudaMemcpyHostToDevice));
         const long long ranks = d == 1 ? P : P * (P + 1) / 2;
+        const bool warp = d >= 3;
+        const long long chunk = warp ? chunk_w : chunk_t;
+        const void* kern = warp ? bf_warp_kernel_ptr() : bf_kernel_ptr();
         for (long long r0 = 0; r0 < ranks; r0 += chunk) {
             a.rank0 = r0;
             a.rank_end = std::min(ranks, r0 + chunk);
             a.remaining = budget - nodes;
             void* args[] = {&a};
-            const unsigned grid = static_cast<unsigned>((a.rank_end - r0 + T - 1) / T);
-            CK(cudaLaunchKernel(bf_kernel_ptr(), grid, T, args, 0, nullptr));
+            const long long lanes = (a.rank_end - r0) * (warp ? 32 : 1);
+            const unsigned grid = static_cast<unsigned>((lanes + T - 1) / T);
+            CK(cudaLaunchKernel(kern, grid, T, args, 0, nullptr));
             CK(cudaLaunchKernel(bf_sum_kernel_ptr(), std::min<unsigned>(grid, num_sms_ * 4), T, args, 0, nullptr));
             stats.launches += 2;
             Words got{};
@@ -1361,7 +1368,7 @@ std::vector<Config> Engine::brute_force(int cap, long long node_budget, bool& fo
             if (nodes > budget) over();
             if (hit) {
                 a.replay = static_cast<long long>(got.best_key);
-                CK(cudaLaunchKernel(bf_kernel_ptr(), 1, T, args, 0, nullptr));
+                CK(cudaLaunchKernel(kern, 1, T, args, 0, nullptr));
                 stats.launches++;
                 long long tup[kBfMaxDepth + 1];
                 CK(cudaMemcpy(tup, a.tuple, sizeof tup, cudaMemcpyDeviceToHost));
