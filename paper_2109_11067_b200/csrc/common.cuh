@@ -161,6 +161,22 @@ __device__ __forceinline__ void rank_select(const DevModel& M, const Cand* cand,
     }
 }
 
+// rank_select with a warp per candidate: the lanes compare it against 32 others at a time
+// and count with a ballot (a block-wide call; same output as rank_select).
+__device__ __forceinline__ void rank_select_warp(const DevModel& M, const Cand* cand, int nc, int k, Cand* out) {
+    const int lane = static_cast<int>(threadIdx.x & 31u);
+    const int nw = static_cast<int>(blockDim.x >> 5);
+    for (int i = static_cast<int>(threadIdx.x >> 5); i < nc; i += nw) {
+        const Cand ci = cand[i];
+        int r = 0;
+        for (int j0 = 0; j0 < nc && r < k; j0 += 32) {
+            const int j = j0 + lane;
+            r += __popc(__ballot_sync(0xffffffffu, j < nc && precedes(M, cand[j], ci)));
+        }
+        if (lane == 0 && r < k) out[r] = ci;
+    }
+}
+
 // K-th largest (k <= 32) of the warp's lane values: bitonic sort descending over shuffles.
 __device__ __forceinline__ double warp_kth(double v, int k) {
     const int lane = static_cast<int>(threadIdx.x & 31u);

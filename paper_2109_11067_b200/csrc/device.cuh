@@ -202,11 +202,13 @@ struct MctsLaunch {
     DevModel M;
     const uint64_t* base;
     long long n_base;
+    const unsigned* keyrank; // rank of each base row in the config order (tie-break)
     const double* logtab;    // std::log(v) for v = 0..budget (host-computed, bit-exact)
     int budget, topk, pick_services;
     double ucb_c;
     int node_smem;           // node metadata in shared memory (all solves: same max_nodes)
     int rows_smem;           // the base pool copied into shared memory
+    int timers;              // accumulate top-K phase cycles (MIGPLAN_MCTS_TIMERS)
     MctsSolveArgs s[kMaxGroups];
 };
 

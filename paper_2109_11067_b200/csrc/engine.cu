@@ -34,6 +34,7 @@ const void* bf_sum_kernel_ptr();
 const void* bf_warp_kernel_ptr();
 int bf_threads();
 const void* mcts_kernel_ptr();
+void mcts_read_topk_timers(unsigned long long* h);
 int mcts_threads();
 const void* rollout_kernel_ptr();
 int rollout_threads();
@@ -326,6 +327,22 @@ Engine::Engine(const Rules& rules, std::map<std::string, ModelProfile> profiles,
     long double eb = 0;
     for (int k = max_mix + 1; k <= kRowK; ++k) eb += static_cast<long double>(binom(m_.n, k)) * m_.templates[k].size();
     ext_bound_ = static_cast<long long>(std::min<long double>(eb, 1ll << 31)) + 64;
+}
+
+const unsigned* Engine::keyrank() {
+    std::call_once(keyrank_once_, [&] {
+        const size_t P = base_rows_.size();
+        std::vector<std::pair<std::array<uint64_t, 2>, unsigned>> k(P);
+        for (size_t i = 0; i < P; ++i) k[i] = {m_.key(base_rows_[i]), static_cast<unsigned>(i)};
+        std::sort(k.begin(), k.end());
+        std::vector<unsigned> rank(P);
+        for (size_t r = 0; r < P; ++r) rank[k[r].second] = static_cast<unsigned>(r);
+        CK(cudaSetDevice(device_));
+        CK(cudaMalloc(&d_keyrank_, sizeof(unsigned) * std::max<size_t>(P, 1)));
+        dev_allocs_.push_back(d_keyrank_);
+        if (P) CK(cudaMemcpy(d_keyrank_, rank.data(), sizeof(unsigned) * P, cudaMemcpyHostToDevice));
+    });
+    return d_keyrank_;
 }
 
 Engine::~Engine() {
@@ -1036,6 +1053,7 @@ std::vector<MctsDeviceResult> Engine::mcts_device_group(const std::vector<std::v
         L->M = dm_;
         L->base = d_base_;
         L->n_base = pool_size();
+        L->keyrank = keyrank();
         L->budget = budget;
         L->topk = topk;
         L->pick_services = pick_services;
@@ -1144,6 +1162,7 @@ std::vector<MctsDeviceResult> Engine::mcts_device_group(const std::vector<std::v
             const long long room = di.smem_optin - di.mcts_static_smem - 1024;
             const int mn = static_cast<int>(offs[0].max_nodes);
             L->rows_smem = static_cast<long long>(mcts_smem_bytes(n, m_.PP, mn, slice, false, true)) <= room;
+            L->timers = std::getenv("MIGPLAN_MCTS_TIMERS") ? 1 : 0;
             L->node_smem = static_cast<long long>(mcts_smem_bytes(n, m_.PP, mn, slice, true, L->rows_smem != 0)) <= room;
         }
         const size_t msm = mcts_smem_bytes(n, m_.PP, static_cast<int>(offs[0].max_nodes), slice, L->node_smem != 0,
@@ -1190,6 +1209,12 @@ std::vector<MctsDeviceResult> Engine::mcts_device_group(const std::vector<std::v
             if (std::getenv("MIGPLAN_MCTS_TIMERS")) {
                 long long t[5];
                 std::memcpy(t, &out[10], sizeof t);
+                unsigned long long tk[6];
+                mcts_read_topk_timers(tk);
+                if (tk[5])
+                    std::fprintf(stderr, "[mcts] top-K (cumulative) calls %llu, cycles/call: tables %.0f pass1 %.0f pass2 %.0f "
+                                 "rank %.0f, candidates/call %.1f\n", tk[5], double(tk[0]) / tk[5], double(tk[1]) / tk[5],
+                                 double(tk[2]) / tk[5], double(tk[3]) / tk[5], double(tk[4]) / tk[5]);
                 std::fprintf(stderr, "[mcts] solve %d: %.1f ms device, cycles sel %lld expand-host %lld miss-host %lld topk %lld "
                              "rollout-ctl %lld, builds %d expands %d iters %d, exact-path top-Ks (cumulative) %d\n",
                              b0 + q, ms, t[0], t[1], t[2], t[3], t[4], out[4], out[7], out[6], out[20]);

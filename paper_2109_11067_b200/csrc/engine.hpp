@@ -175,6 +175,11 @@ class Engine {
     std::vector<uint64_t> base_rows_;
     mutable std::unordered_map<uint64_t, long long> row_index_;
     mutable std::once_flag row_index_once_;
+    // rank of every base row in the config order (core.hpp:174-200), for the device
+    // top-Ks' last tie-break (built on first use)
+    unsigned* d_keyrank_ = nullptr;
+    std::once_flag keyrank_once_;
+    const unsigned* keyrank();
     std::vector<double> min_u_;  // smallest positive utility per service (step bound)
     long long ext_bound_ = 0;
     int cache_units_ = 0;  // greedy shared-memory row cache per CTA (16-byte units)

@@ -87,6 +87,9 @@ __device__ __forceinline__ float ub_row(const float* Wf, uint64_t row) {
 // service, else all), block-wide.  Writes base-pool indices in preference order to out[],
 // returns their count.  Ends with a barrier.
 __device__ unsigned g_mcts_fallbacks = 0;  // diagnostics: exact-path top-Ks (MIGPLAN_MCTS_TIMERS)
+// diagnostics (MctsLaunch::timers): top-K phase cycles seen by thread 0 — tables, pass 1 +
+// threshold, pass 2, rank + output — then Σ candidates and calls
+__device__ unsigned long long g_tk[6];
 
 __device__ __forceinline__ float ub_half(const float* Wf, unsigned lo, unsigned hi) {
     float s = __fadd_ru(Wf[lo & 0xFFFFu], Wf[lo >> 16]);
@@ -97,10 +100,47 @@ __device__ __forceinline__ bool hit_half(const unsigned char* hitc, unsigned lo,
     return (hitc[lo & 0xFFFFu] | hitc[lo >> 16] | hitc[hi & 0xFFFFu] | hitc[hi >> 16]) != 0;
 }
 
-__device__ int block_topk_exact(const DevModel& M, const uint64_t* base, long long nb, long long pos0,
+// Candidates here carry pos | keyrank[pos] << 32: the config-order tie-break (core.hpp:174-200)
+// becomes one integer compare instead of decoding both rows.
+__device__ __forceinline__ bool precedes_kr(const Cand& j, const Cand& i) {
+    if (j.s != i.s) return j.s > i.s;
+    if (j.row == i.row) return static_cast<unsigned>(j.pos) < static_cast<unsigned>(i.pos);
+    if (j.u != i.u) return j.u > i.u;
+    return (j.pos >> 32) < (i.pos >> 32);
+}
+__device__ __forceinline__ long long pack_pos(const unsigned* keyrank, long long pos) {
+    return pos | (static_cast<long long>(keyrank[pos]) << 32);
+}
+__device__ __forceinline__ int pos_of(const Cand& c) { return static_cast<int>(c.pos & 0xffffffffll); }
+
+// rank_select (common.cuh) with a warp per candidate and the packed key rank.
+__device__ __forceinline__ void rank_select_kr(const Cand* cand, int nc, int k, Cand* out) {
+    const int lane = static_cast<int>(threadIdx.x & 31u);
+    const int nw = static_cast<int>(blockDim.x >> 5);
+    for (int i = static_cast<int>(threadIdx.x >> 5); i < nc; i += nw) {
+        const Cand ci = cand[i];
+        int r = 0;
+        for (int j0 = 0; j0 < nc && r < k; j0 += 32) {
+            const int j = j0 + lane;
+            r += __popc(__ballot_sync(0xffffffffu, j < nc && precedes_kr(cand[j], ci)));
+        }
+        if (lane == 0 && r < k) out[r] = ci;
+    }
+}
+
+__device__ int block_topk_exact(const DevModel& M, const unsigned* keyrank, const uint64_t* base, long long nb, long long pos0,
                                 const double* comp, const uint64_t* mask, int k, const double* U, double* W, float* Wf,
-                                unsigned char* hitc, Cand* cand, Cand* win, int* out, int* scored) {
+                                unsigned char* hitc, Cand* cand, Cand* win, int* out, int* scored, bool tm) {
     __shared__ unsigned long long t_bits;
+    long long c0 = 0, c1 = 0;
+    auto mark = [&](int slot) {
+        if (tm && threadIdx.x == 0) {
+            c1 = clock64();
+            if (slot >= 0) atomicAdd(&g_tk[slot], static_cast<unsigned long long>(c1 - c0));
+            c0 = c1;
+        }
+    };
+    mark(-1);
     __shared__ int n_cand, n_hit;
     __shared__ Cand red[kMWarps];
     const int nW = (M.n + 1) * M.PP;
@@ -121,6 +161,7 @@ __device__ int block_topk_exact(const DevModel& M, const uint64_t* base, long lo
         n_hit = 0;
     }
     __syncthreads();
+    mark(0);
     // Rows are read two at a time (16 bytes) and split into 32-bit halves: no 64-bit shifts.
     const uint4* base2 = reinterpret_cast<const uint4*>(base);
     const long long np = nb >> 1;
@@ -196,6 +237,7 @@ __device__ int block_topk_exact(const DevModel& M, const uint64_t* base, long lo
     const double tw = warp_kth(tmax, k);
     if ((threadIdx.x & 31u) == 0) atomicMax(&t_bits, static_cast<unsigned long long>(__double_as_longlong(tw)));
     __syncthreads();
+    mark(1);
     const double T = __longlong_as_double(static_cast<long long>(t_bits));
     const float T_f = __double2float_rd(T);
     // pass 2: rows whose exact score reaches T (at least k of them exist)
@@ -213,7 +255,7 @@ __device__ int block_topk_exact(const DevModel& M, const uint64_t* base, long lo
             int at = 0;
             if ((threadIdx.x & 31u) == 0) at = atomicAdd(&n_cand, __popc(b));
             at = __shfl_sync(0xffffffffu, at, 0) + __popc(b & lanemask_lt());
-            if (take && at < kMCandCap) cand[at] = Cand{sc, row_usum(U, row), row, pos};
+            if (take && at < kMCandCap) cand[at] = Cand{sc, row_usum(U, row), row, pack_pos(keyrank, pos)};
         }
     };
     // warp-uniform trip count: 4 row pairs per thread per iteration, padding = sentinel rows;
@@ -247,11 +289,12 @@ __device__ int block_topk_exact(const DevModel& M, const uint64_t* base, long lo
         }
     }
     __syncthreads();
+    mark(2);
     const int nc = n_cand;
     int got;
     if (nc <= kMCandCap) {
         got = min(nc, k);
-        rank_select(M, cand, nc, k, win);
+        rank_select_kr(cand, nc, k, win);
     } else {  // pathological ties at T: exact k rounds of "best row strictly after the previous"
         if (threadIdx.x == 0) atomicAdd(&g_mcts_fallbacks, 1u);
         got = 0;
@@ -263,20 +306,20 @@ __device__ int block_topk_exact(const DevModel& M, const uint64_t* base, long lo
                 if (mask && !row_hits(hitc, row)) continue;
                 const double s = row_score(W, row);
                 if (!(s > 0.0)) continue;
-                const Cand c{s, row_usum(U, row), row, pos0 + i};
-                if (r > 0 && !precedes(M, last, c)) continue;
-                if (b.row == kNoRow || precedes(M, c, b)) b = c;
+                const Cand c{s, row_usum(U, row), row, pack_pos(keyrank, pos0 + i)};
+                if (r > 0 && !precedes_kr(last, c)) continue;
+                if (b.row == kNoRow || precedes_kr(c, b)) b = c;
             }
             for (int off = 16; off > 0; off >>= 1) {
                 const Cand o{__shfl_xor_sync(0xffffffffu, b.s, off), __shfl_xor_sync(0xffffffffu, b.u, off),
                              __shfl_xor_sync(0xffffffffu, b.row, off), __shfl_xor_sync(0xffffffffu, b.pos, off)};
-                if (o.row != kNoRow && (b.row == kNoRow || precedes(M, o, b))) b = o;
+                if (o.row != kNoRow && (b.row == kNoRow || precedes_kr(o, b))) b = o;
             }
             if ((threadIdx.x & 31u) == 0) red[threadIdx.x >> 5] = b;
             __syncthreads();
             Cand x = red[0];
             for (int w = 1; w < kMWarps; ++w)
-                if (red[w].row != kNoRow && (x.row == kNoRow || precedes(M, red[w], x))) x = red[w];
+                if (red[w].row != kNoRow && (x.row == kNoRow || precedes_kr(red[w], x))) x = red[w];
             __syncthreads();
             if (x.row == kNoRow) break;
             if (threadIdx.x == 0) win[r] = x;
@@ -285,9 +328,14 @@ __device__ int block_topk_exact(const DevModel& M, const uint64_t* base, long lo
         }
     }
     __syncthreads();
-    if (out && threadIdx.x < got) out[threadIdx.x] = static_cast<int>(win[threadIdx.x].pos);
+    if (out && threadIdx.x < got) out[threadIdx.x] = pos_of(win[threadIdx.x]);
     if (threadIdx.x == 0) *scored = mask ? n_hit : static_cast<int>(nb);
     __syncthreads();
+    mark(3);
+    if (tm && threadIdx.x == 0) {
+        atomicAdd(&g_tk[4], static_cast<unsigned long long>(nc));
+        atomicAdd(&g_tk[5], 1ull);
+    }
     return got;
 }
 
@@ -376,8 +424,8 @@ __global__ void __launch_bounds__(kMThreads, 1) mcts_kernel(const __grid_constan
             if (threadIdx.x == 0) s_usemask = *cl.map_shared_rank(&s_usemask, 0);
             __syncthreads();
             int sc = 0;
-            const int got = block_topk_exact(M, slice, hi - lo, lo, cur, s_usemask ? s_mask : nullptr, K, Us, W, Wf,
-                                             hitc, cand, win, nullptr, &sc);
+            const int got = block_topk_exact(M, L.keyrank, slice, hi - lo, lo, cur, s_usemask ? s_mask : nullptr, K, Us, W, Wf,
+                                             hitc, cand, win, nullptr, &sc, L.timers != 0);
             if (threadIdx.x == 0) {
                 n_got = got;
                 s_hits = sc;
@@ -392,8 +440,8 @@ __global__ void __launch_bounds__(kMThreads, 1) mcts_kernel(const __grid_constan
         __syncthreads();
         cl.sync();
         int sc = 0;
-        const int got0 = block_topk_exact(M, slice, hi - lo, lo, cur, usemask ? s_mask : nullptr, K, Us, W, Wf, hitc,
-                                          cand, win, nullptr, &sc);
+        const int got0 = block_topk_exact(M, L.keyrank, slice, hi - lo, lo, cur, usemask ? s_mask : nullptr, K, Us, W, Wf, hitc,
+                                          cand, win, nullptr, &sc, L.timers != 0);
         if (threadIdx.x == 0) {
             n_got = got0;
             s_hits = sc;
@@ -423,10 +471,10 @@ __global__ void __launch_bounds__(kMThreads, 1) mcts_kernel(const __grid_constan
         }
         __syncthreads();
         const int mc = m_n;
-        rank_select(M, cand, mc, K, win + kMMaxK);
+        rank_select_kr(cand, mc, K, win + kMMaxK);
         __syncthreads();
         const int got = min(mc, K);
-        if (threadIdx.x < got) out[threadIdx.x] = static_cast<int>(win[kMMaxK + threadIdx.x].pos);
+        if (threadIdx.x < got) out[threadIdx.x] = pos_of(win[kMMaxK + threadIdx.x]);
         if (threadIdx.x == 0) *scored = m_scored;
         __syncthreads();
         return got;
@@ -776,6 +824,7 @@ size_t mcts_smem_bytes(int n, int PP, int max_nodes, long long n_base, bool node
     if (rows_smem) carve(8 * static_cast<size_t>(n_base));
     return off;
 }
+void mcts_read_topk_timers(unsigned long long* h) { cudaMemcpyFromSymbol(h, g_tk, sizeof g_tk); }
 const void* mcts_kernel_ptr() { return reinterpret_cast<const void*>(&mcts_kernel); }
 int mcts_threads() { return kMThreads; }
 
