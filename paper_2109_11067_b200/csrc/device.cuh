@@ -209,6 +209,7 @@ struct MctsLaunch {
     int node_smem;           // node metadata in shared memory (all solves: same max_nodes)
     int rows_smem;           // the base pool copied into shared memory
     int timers;              // accumulate top-K phase cycles (MIGPLAN_MCTS_TIMERS)
+    int pair;                // every base row has <= 2 members: on-chip copy as 32-bit rows
     MctsSolveArgs s[kMaxGroups];
 };
 

@@ -28,7 +28,7 @@ int topk1_max_ctas();
 constexpr int kTopkMaxCtas = 4096;  // partial-list capacity (Best x 32 per CTA)
 const void* topk1_kernel_ptr(int km);
 size_t rollout_smem_bytes(int n, int PP);
-size_t mcts_smem_bytes(int n, int PP, int max_nodes, long long n_base, bool node_smem, bool rows_smem);
+size_t mcts_smem_bytes(int n, int PP, int max_nodes, long long n_base, bool node_smem, bool rows_smem, bool pair);
 const void* bf_kernel_ptr();
 const void* bf_sum_kernel_ptr();
 const void* bf_warp_kernel_ptr();
@@ -1155,18 +1155,20 @@ std::vector<MctsDeviceResult> Engine::mcts_device_group(const std::vector<std::v
         // 1/C scan at the pool sizes of the GA workloads, so one CTA per search by default)
         int C = 1;
         if (const char* v = std::getenv("MIGPLAN_MCTS_CLUSTER")) C = std::max(1, std::min(16, std::atoi(v)));
-        const long long slice = ((pool_size() + C - 1) / C + 1) & ~1ll;
+        const bool pair = m_.max_mix <= 2 && !(std::getenv("MIGPLAN_MCTS_PAIR") && std::atoi(std::getenv("MIGPLAN_MCTS_PAIR")) == 0);
+        L->pair = pair ? 1 : 0;
+        const long long slice = pair ? (((pool_size() + C - 1) / C + 3) & ~3ll) : (((pool_size() + C - 1) / C + 1) & ~1ll);
         // on-chip placement: the slice first (every top-K scans it twice), then the nodes
         {
             const DeviceInfo& di = device_info(device_);
             const long long room = di.smem_optin - di.mcts_static_smem - 1024;
             const int mn = static_cast<int>(offs[0].max_nodes);
-            L->rows_smem = static_cast<long long>(mcts_smem_bytes(n, m_.PP, mn, slice, false, true)) <= room;
+            L->rows_smem = static_cast<long long>(mcts_smem_bytes(n, m_.PP, mn, slice, false, true, pair)) <= room;
             L->timers = std::getenv("MIGPLAN_MCTS_TIMERS") ? 1 : 0;
-            L->node_smem = static_cast<long long>(mcts_smem_bytes(n, m_.PP, mn, slice, true, L->rows_smem != 0)) <= room;
+            L->node_smem = static_cast<long long>(mcts_smem_bytes(n, m_.PP, mn, slice, true, L->rows_smem != 0, pair)) <= room;
         }
         const size_t msm = mcts_smem_bytes(n, m_.PP, static_cast<int>(offs[0].max_nodes), slice, L->node_smem != 0,
-                                           L->rows_smem != 0);
+                                           L->rows_smem != 0, pair);
         for (int q = 1; q < nb; ++q) CK(cudaStreamSynchronize(slots[q]->stream));
         Slot* s0 = slots[0];
         void* args[] = {L.get()};
@@ -1209,12 +1211,12 @@ std::vector<MctsDeviceResult> Engine::mcts_device_group(const std::vector<std::v
             if (std::getenv("MIGPLAN_MCTS_TIMERS")) {
                 long long t[5];
                 std::memcpy(t, &out[10], sizeof t);
-                unsigned long long tk[6];
+                unsigned long long tk[8];
                 mcts_read_topk_timers(tk);
                 if (tk[5])
                     std::fprintf(stderr, "[mcts] top-K (cumulative) calls %llu, cycles/call: tables %.0f pass1 %.0f pass2 %.0f "
-                                 "rank %.0f, candidates/call %.1f\n", tk[5], double(tk[0]) / tk[5], double(tk[1]) / tk[5],
-                                 double(tk[2]) / tk[5], double(tk[3]) / tk[5], double(tk[4]) / tk[5]);
+                                 "rank %.0f, candidates/call %.1f, rescans %llu\n", tk[5], double(tk[0]) / tk[5], double(tk[1]) / tk[5],
+                                 double(tk[2]) / tk[5], double(tk[3]) / tk[5], double(tk[4]) / tk[5], tk[6]);
                 std::fprintf(stderr, "[mcts] solve %d: %.1f ms device, cycles sel %lld expand-host %lld miss-host %lld topk %lld "
                              "rollout-ctl %lld, builds %d expands %d iters %d, exact-path top-Ks (cumulative) %d\n",
                              b0 + q, ms, t[0], t[1], t[2], t[3], t[4], out[4], out[7], out[6], out[20]);

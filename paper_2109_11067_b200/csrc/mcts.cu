@@ -89,7 +89,7 @@ __device__ __forceinline__ float ub_row(const float* Wf, uint64_t row) {
 __device__ unsigned g_mcts_fallbacks = 0;  // diagnostics: exact-path top-Ks (MIGPLAN_MCTS_TIMERS)
 // diagnostics (MctsLaunch::timers): top-K phase cycles seen by thread 0 — tables, pass 1 +
 // threshold, pass 2, rank + output — then Σ candidates and calls
-__device__ unsigned long long g_tk[6];
+__device__ unsigned long long g_tk[8];  // [6]: pass-2 rescans
 
 __device__ __forceinline__ float ub_half(const float* Wf, unsigned lo, unsigned hi) {
     float s = __fadd_ru(Wf[lo & 0xFFFFu], Wf[lo >> 16]);
@@ -122,16 +122,52 @@ __device__ __forceinline__ void rank_select_kr(const Cand* cand, int nc, int k, 
         int r = 0;
         for (int j0 = 0; j0 < nc && r < k; j0 += 32) {
             const int j = j0 + lane;
-            r += __popc(__ballot_sync(0xffffffffu, j < nc && precedes_kr(cand[j], ci)));
+            bool p = false;
+            if (j < nc) {  // the score decides unless it ties: load the rest only then
+                const double sj = cand[j].s;
+                p = sj != ci.s ? sj > ci.s : precedes_kr(cand[j], ci);
+            }
+            r += __popc(__ballot_sync(0xffffffffu, p));
         }
         if (lane == 0 && r < k) out[r] = ci;
     }
 }
 
-__device__ int block_topk_exact(const DevModel& M, const unsigned* keyrank, const uint64_t* base, long long nb, long long pos0,
-                                const double* comp, const uint64_t* mask, int k, const double* U, double* W, float* Wf,
-                                unsigned char* hitc, Cand* cand, Cand* win, int* out, int* scored, bool tm) {
-    __shared__ unsigned long long t_bits;
+// warp_kth (common.cuh) on floats: half the shuffles of the double version.
+__device__ __forceinline__ float warp_kth_f(float v, int k) {
+    const int lane = static_cast<int>(threadIdx.x & 31u);
+#pragma unroll
+    for (int size = 2; size <= 32; size <<= 1) {
+#pragma unroll
+        for (int j = size >> 1; j > 0; j >>= 1) {
+            const float o = __shfl_xor_sync(0xffffffffu, v, j);
+            const bool desc = (lane & size) == 0 || size == 32;
+            const bool low = (lane & j) == 0;
+            v = (low == desc) ? fmaxf(v, o) : fminf(v, o);
+        }
+    }
+    return __shfl_sync(0xffffffffu, v, k - 1);
+}
+
+// The candidates' key ranks (pos | keyrank[pos] << 32), fetched in one parallel round trip
+// after compaction instead of one dependent global load per push.
+__device__ __forceinline__ void fill_keyrank(const unsigned* keyrank, Cand* cand, int nc) {
+    for (int i = threadIdx.x; i < nc; i += blockDim.x) cand[i].pos = pack_pos(keyrank, cand[i].pos);
+}
+
+// The same top-K with an FP32-only first pass: every thread's largest bound ub, the K-th
+// largest of a warp's lane maxima (max over warps) U_K, then LB = U_K (1 - 2^-20) is a lower
+// bound of the K-th exact score: K rows have ub >= U_K, and ub over-estimates an exact score
+// by < 4.01 * 2^-23 relative (4 round-up conversions/adds of non-negative terms), so those K
+// rows score >= LB.  Pass 2 scores exactly only rows whose bound reaches LB; the candidates
+// (exact score >= LB) contain every row of the top-K.
+__device__ __noinline__ int block_topk_bound(const DevModel& M, const unsigned* keyrank, const uint64_t* base, long long nb,
+                                long long pos0, const double* comp, const uint64_t* mask, int k, const double* U,
+                                double* W, float* Wf, unsigned char* hitc, Cand* cand, Cand* win, int* out, int* scored,
+                                bool tm) {
+    __shared__ unsigned t_fbits;
+    __shared__ int n_cand, n_hit;
+    __shared__ Cand red[kMWarps];
     long long c0 = 0, c1 = 0;
     auto mark = [&](int slot) {
         if (tm && threadIdx.x == 0) {
@@ -141,8 +177,6 @@ __device__ int block_topk_exact(const DevModel& M, const unsigned* keyrank, cons
         }
     };
     mark(-1);
-    __shared__ int n_cand, n_hit;
-    __shared__ Cand red[kMWarps];
     const int nW = (M.n + 1) * M.PP;
     for (int e = threadIdx.x; e < nW; e += blockDim.x) {
         const int svc = e / M.PP;
@@ -156,99 +190,71 @@ __device__ int block_topk_exact(const DevModel& M, const unsigned* keyrank, cons
         if (mask) hitc[e] = svc < M.n && ((mask[svc >> 6] >> (svc & 63)) & 1ull) != 0;
     }
     if (threadIdx.x == 0) {
-        t_bits = 0ull;
+        t_fbits = 0u;
         n_cand = 0;
         n_hit = 0;
     }
     __syncthreads();
     mark(0);
-    // Rows are read two at a time (16 bytes) and split into 32-bit halves: no 64-bit shifts.
     const uint4* base2 = reinterpret_cast<const uint4*>(base);
     const long long np = nb >> 1;
-    // pass 1: the thread's exact maximum; exact scores only where the FP32 bound reaches it.
-    // With a mask, the candidate set is the rows touching a sampled service (its size is the
-    // work count of the call, mcts.hpp:98-107).
-    double tmax = 0.0;
-    float tmax_f = 0.0f;  // tmax rounded down: ub < tmax_f  =>  ub < tmax
-    int hits = 0;
-    auto visit1 = [&](unsigned lo, unsigned hi) {
-        if (mask) {
-            if (!hit_half(hitc, lo, hi)) return;
-            ++hits;
-        }
-        const float ub = ub_half(Wf, lo, hi);
-        if (!(ub > 0.0f) || ub < tmax_f) return;
-        const double sc = row_score(W, (static_cast<uint64_t>(hi) << 32) | lo);
-        if (sc > tmax) {
-            tmax = sc;
-            tmax_f = __double2float_rd(sc);
-        }
-    };
     const long long B = blockDim.x;
-    const unsigned sent = static_cast<unsigned>(M.n * M.PP) * 0x00010001u;  // two sentinel codes
-    const uint4 padv = make_uint4(sent, sent, sent, sent);
-    // main body: 8 rows per thread per iteration, bounds and hit flags computed branch-free,
-    // the exact path entered only when one of them reaches the thread's running maximum
+    // pass 1: FP32 bounds only (no exact scores, no divergence)
+    float umax = 0.0f;
+    int hits = 0;
     long long p = threadIdx.x;
     for (; p + 3 * B < np; p += 4 * B) {
         const uint4 v[4] = {base2[p], base2[p + B], base2[p + 2 * B], base2[p + 3 * B]};
-        float ub[8];
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
-            ub[2 * q] = ub_half(Wf, v[q].x, v[q].y);
-            ub[2 * q + 1] = ub_half(Wf, v[q].z, v[q].w);
+            float u0 = ub_half(Wf, v[q].x, v[q].y), u1 = ub_half(Wf, v[q].z, v[q].w);
             if (mask) {
                 const bool h0 = hit_half(hitc, v[q].x, v[q].y), h1 = hit_half(hitc, v[q].z, v[q].w);
                 hits += h0 + h1;
-                if (!h0) ub[2 * q] = 0.0f;
-                if (!h1) ub[2 * q + 1] = 0.0f;
+                if (!h0) u0 = 0.0f;
+                if (!h1) u1 = 0.0f;
             }
-        }
-        float mx = ub[0];
-#pragma unroll
-        for (int j = 1; j < 8; ++j) mx = fmaxf(mx, ub[j]);
-        if (mx > 0.0f && mx >= tmax_f) {
-#pragma unroll
-            for (int j = 0; j < 8; ++j) {
-                if (!(ub[j] > 0.0f) || ub[j] < tmax_f) continue;
-                const uint4& w = v[j >> 1];
-                const unsigned lo = (j & 1) ? w.z : w.x, hi = (j & 1) ? w.w : w.y;
-                const double sc = row_score(W, (static_cast<uint64_t>(hi) << 32) | lo);
-                if (sc > tmax) {
-                    tmax = sc;
-                    tmax_f = __double2float_rd(sc);
-                }
-            }
+            umax = fmaxf(umax, fmaxf(u0, u1));
         }
     }
     for (; p < np; p += B) {
         const uint4 v = base2[p];
-        visit1(v.x, v.y);
-        visit1(v.z, v.w);
+        float u0 = ub_half(Wf, v.x, v.y), u1 = ub_half(Wf, v.z, v.w);
+        if (mask) {
+            const bool h0 = hit_half(hitc, v.x, v.y), h1 = hit_half(hitc, v.z, v.w);
+            hits += h0 + h1;
+            if (!h0) u0 = 0.0f;
+            if (!h1) u1 = 0.0f;
+        }
+        umax = fmaxf(umax, fmaxf(u0, u1));
     }
     if ((nb & 1) && threadIdx.x == 0) {
         const uint64_t r = base[nb - 1];
-        visit1(static_cast<unsigned>(r), static_cast<unsigned>(r >> 32));
+        const unsigned lo = static_cast<unsigned>(r), hi = static_cast<unsigned>(r >> 32);
+        if (!mask || hit_half(hitc, lo, hi)) {
+            hits += mask ? 1 : 0;
+            umax = fmaxf(umax, ub_half(Wf, lo, hi));
+        }
     }
     if (mask) {
         for (int off = 16; off > 0; off >>= 1) hits += __shfl_xor_sync(0xffffffffu, hits, off);
         if ((threadIdx.x & 31u) == 0) atomicAdd(&n_hit, hits);
     }
-    const double tw = warp_kth(tmax, k);
-    if ((threadIdx.x & 31u) == 0) atomicMax(&t_bits, static_cast<unsigned long long>(__double_as_longlong(tw)));
+    const float uk = warp_kth_f(umax, k);
+    if ((threadIdx.x & 31u) == 0) atomicMax(&t_fbits, __float_as_uint(uk));  // non-negative floats
     __syncthreads();
     mark(1);
-    const double T = __longlong_as_double(static_cast<long long>(t_bits));
-    const float T_f = __double2float_rd(T);
-    // pass 2: rows whose exact score reaches T (at least k of them exist)
+    const double LB = __dmul_rd(static_cast<double>(__uint_as_float(t_fbits)), 1.0 - 0x1p-20);
+    const float LB_f = __double2float_rd(LB);
+    // pass 2: exact scores where the bound reaches LB; candidates score >= LB (> 0)
     auto visit2 = [&](unsigned lo, unsigned hi, long long pos) {
         bool take = false;
         double sc = 0.0;
         const uint64_t row = (static_cast<uint64_t>(hi) << 32) | lo;
         const float ub = ub_half(Wf, lo, hi);
-        if (ub > 0.0f && ub >= T_f && (!mask || hit_half(hitc, lo, hi))) {
+        if (ub > 0.0f && ub >= LB_f && (!mask || hit_half(hitc, lo, hi))) {
             sc = row_score(W, row);
-            take = sc > 0.0 && sc >= T;
+            take = sc > 0.0 && sc >= LB;
         }
         const unsigned b = __ballot_sync(0xffffffffu, take);
         if (b) {
@@ -258,22 +264,19 @@ __device__ int block_topk_exact(const DevModel& M, const unsigned* keyrank, cons
             if (take && at < kMCandCap) cand[at] = Cand{sc, row_usum(U, row), row, pack_pos(keyrank, pos)};
         }
     };
-    // warp-uniform trip count: 4 row pairs per thread per iteration, padding = sentinel rows;
-    // a warp skips a group at once when no lane's bound reaches T (one vote)
+    const unsigned sent = static_cast<unsigned>(M.n * M.PP) * 0x00010001u;
+    const uint4 padv = make_uint4(sent, sent, sent, sent);
     const long long np4 = (np + 4 * B - 1) / (4 * B) * (4 * B);
     for (long long p0 = threadIdx.x; p0 < np4; p0 += 4 * B) {
         uint4 v[4];
-        float ub[8];
         float mx = 0.0f;
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
             const long long pp = p0 + q * B;
             v[q] = pp < np ? base2[pp] : padv;
-            ub[2 * q] = ub_half(Wf, v[q].x, v[q].y);
-            ub[2 * q + 1] = ub_half(Wf, v[q].z, v[q].w);
-            mx = fmaxf(mx, fmaxf(ub[2 * q], ub[2 * q + 1]));
+            mx = fmaxf(mx, fmaxf(ub_half(Wf, v[q].x, v[q].y), ub_half(Wf, v[q].z, v[q].w)));
         }
-        if (!__any_sync(0xffffffffu, mx > 0.0f && mx >= T_f)) continue;
+        if (!__any_sync(0xffffffffu, mx > 0.0f && mx >= LB_f)) continue;
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
             const long long pp = p0 + q * B;
@@ -281,7 +284,7 @@ __device__ int block_topk_exact(const DevModel& M, const unsigned* keyrank, cons
             visit2(v[q].z, v[q].w, pos0 + 2 * pp + 1);
         }
     }
-    if (nb & 1) {  // last odd row, warp 0 (ballot needs the whole warp)
+    if (nb & 1) {
         if ((threadIdx.x >> 5) == 0) {
             const uint64_t r = threadIdx.x == 0 ? base[nb - 1]
                                                 : static_cast<uint64_t>(M.n * M.PP) * 0x0001000100010001ull;
@@ -295,7 +298,7 @@ __device__ int block_topk_exact(const DevModel& M, const unsigned* keyrank, cons
     if (nc <= kMCandCap) {
         got = min(nc, k);
         rank_select_kr(cand, nc, k, win);
-    } else {  // pathological ties at T: exact k rounds of "best row strictly after the previous"
+    } else {  // pathological ties: exact k rounds of "best row strictly after the previous"
         if (threadIdx.x == 0) atomicAdd(&g_mcts_fallbacks, 1u);
         got = 0;
         Cand last{0.0, 0.0, kNoRow, -1};
@@ -307,6 +310,180 @@ __device__ int block_topk_exact(const DevModel& M, const unsigned* keyrank, cons
                 const double s = row_score(W, row);
                 if (!(s > 0.0)) continue;
                 const Cand c{s, row_usum(U, row), row, pack_pos(keyrank, pos0 + i)};
+                if (r > 0 && !precedes_kr(last, c)) continue;
+                if (b.row == kNoRow || precedes_kr(c, b)) b = c;
+            }
+            for (int off = 16; off > 0; off >>= 1) {
+                const Cand o{__shfl_xor_sync(0xffffffffu, b.s, off), __shfl_xor_sync(0xffffffffu, b.u, off),
+                             __shfl_xor_sync(0xffffffffu, b.row, off), __shfl_xor_sync(0xffffffffu, b.pos, off)};
+                if (o.row != kNoRow && (b.row == kNoRow || precedes_kr(o, b))) b = o;
+            }
+            if ((threadIdx.x & 31u) == 0) red[threadIdx.x >> 5] = b;
+            __syncthreads();
+            Cand x = red[0];
+            for (int w = 1; w < kMWarps; ++w)
+                if (red[w].row != kNoRow && (x.row == kNoRow || precedes_kr(red[w], x))) x = red[w];
+            __syncthreads();
+            if (x.row == kNoRow) break;
+            if (threadIdx.x == 0) win[r] = x;
+            last = x;
+            ++got;
+        }
+    }
+    __syncthreads();
+    if (out && threadIdx.x < got) out[threadIdx.x] = pos_of(win[threadIdx.x]);
+    if (threadIdx.x == 0) *scored = mask ? n_hit : static_cast<int>(nb);
+    __syncthreads();
+    mark(3);
+    if (tm && threadIdx.x == 0) {
+        atomicAdd(&g_tk[4], static_cast<unsigned long long>(nc));
+        atomicAdd(&g_tk[5], 1ull);
+    }
+    return got;
+}
+
+// block_topk_bound over rows of at most two members (max_mix <= 2), stored as their low 32
+// bits: two bound gathers and 4 bytes per row instead of four gathers and 8 bytes.  The
+// omitted members are sentinels (W = 0, U = 0), so every exact score and util_sum is the
+// 64-bit row's bit for bit.
+__device__ __forceinline__ float ub_pair(const float* Wf, unsigned x) { return __fadd_ru(Wf[x & 0xFFFFu], Wf[x >> 16]); }
+__device__ __forceinline__ bool hit_pair(const unsigned char* hitc, unsigned x) {
+    return (hitc[x & 0xFFFFu] | hitc[x >> 16]) != 0;
+}
+__device__ __noinline__ int block_topk_pair(const DevModel& M, const unsigned* keyrank, const unsigned* base, long long nb,
+                               long long pos0, const double* comp, const uint64_t* mask, int k, const double* U,
+                               double* W, float* Wf, unsigned char* hitc, Cand* cand, Cand* win, int* out, int* scored,
+                               bool tm) {
+    __shared__ unsigned t_fbits;
+    __shared__ int n_cand, n_hit;
+    __shared__ Cand red[kMWarps];
+    long long c0 = 0, c1 = 0;
+    auto mark = [&](int slot) {
+        if (tm && threadIdx.x == 0) {
+            c1 = clock64();
+            if (slot >= 0) atomicAdd(&g_tk[slot], static_cast<unsigned long long>(c1 - c0));
+            c0 = c1;
+        }
+    };
+    mark(-1);
+    const int nW = (M.n + 1) * M.PP;
+    const unsigned sent = static_cast<unsigned>(M.n * M.PP);
+    const uint64_t hiS = static_cast<uint64_t>(sent | (sent << 16)) << 32;
+    for (int e = threadIdx.x; e < nW; e += blockDim.x) {
+        const int svc = e / M.PP;
+        double w = 0.0;
+        if (svc < M.n) {
+            const double need = __dadd_rn(1.0, -comp[svc]);
+            if (need > 0.0) w = __dmul_rn(need, U[e]);
+        }
+        W[e] = w;
+        Wf[e] = __double2float_ru(w);
+        if (mask) hitc[e] = svc < M.n && ((mask[svc >> 6] >> (svc & 63)) & 1ull) != 0;
+    }
+    if (threadIdx.x == 0) {
+        t_fbits = 0u;
+        n_cand = 0;
+        n_hit = 0;
+    }
+    __syncthreads();
+    mark(0);
+    const uint4* base4 = reinterpret_cast<const uint4*>(base);  // 4 rows per 16 bytes
+    const long long nq = nb >> 2;
+    const long long B = blockDim.x;
+    float umax = 0.0f;
+    int hits = 0;
+    auto bound1 = [&](unsigned x) {
+        float u = ub_pair(Wf, x);
+        if (mask) {
+            const bool h = hit_pair(hitc, x);
+            hits += h;
+            if (!h) u = 0.0f;
+        }
+        umax = fmaxf(umax, u);
+    };
+    long long p = threadIdx.x;
+    for (; p + B < nq; p += 2 * B) {
+        const uint4 v0 = base4[p], v1 = base4[p + B];
+        bound1(v0.x), bound1(v0.y), bound1(v0.z), bound1(v0.w);
+        bound1(v1.x), bound1(v1.y), bound1(v1.z), bound1(v1.w);
+    }
+    for (; p < nq; p += B) {
+        const uint4 v = base4[p];
+        bound1(v.x), bound1(v.y), bound1(v.z), bound1(v.w);
+    }
+    if (threadIdx.x < (nb & 3)) bound1(base[4 * nq + threadIdx.x]);
+    if (mask) {
+        for (int off = 16; off > 0; off >>= 1) hits += __shfl_xor_sync(0xffffffffu, hits, off);
+        if ((threadIdx.x & 31u) == 0) atomicAdd(&n_hit, hits);
+    }
+    const float uk = warp_kth_f(umax, k);
+    if ((threadIdx.x & 31u) == 0) atomicMax(&t_fbits, __float_as_uint(uk));
+    __syncthreads();
+    mark(1);
+    const double LB = __dmul_rd(static_cast<double>(__uint_as_float(t_fbits)), 1.0 - 0x1p-20);
+    const float LB_f = __double2float_rd(LB);
+    auto visit2 = [&](unsigned x, long long pos) {
+        bool take = false;
+        double sc = 0.0;
+        const float ub = ub_pair(Wf, x);
+        if (ub > 0.0f && ub >= LB_f && (!mask || hit_pair(hitc, x))) {
+            sc = __dadd_rn(W[x & 0xFFFFu], W[x >> 16]);
+            take = sc > 0.0 && sc >= LB;
+        }
+        const unsigned b = __ballot_sync(0xffffffffu, take);
+        if (b) {
+            int at = 0;
+            if ((threadIdx.x & 31u) == 0) at = atomicAdd(&n_cand, __popc(b));
+            at = __shfl_sync(0xffffffffu, at, 0) + __popc(b & lanemask_lt());
+            if (take && at < kMCandCap) {
+                const uint64_t row = x | hiS;
+                cand[at] = Cand{sc, row_usum(U, row), row, pos};
+            }
+        }
+    };
+    const unsigned sp = sent | (sent << 16);
+    const uint4 padv = make_uint4(sp, sp, sp, sp);
+    const long long nq2 = (nq + 2 * B - 1) / (2 * B) * (2 * B);
+    for (long long p0 = threadIdx.x; p0 < nq2; p0 += 2 * B) {
+        const uint4 v0 = p0 < nq ? base4[p0] : padv;
+        const uint4 v1 = p0 + B < nq ? base4[p0 + B] : padv;
+        const float mx = fmaxf(fmaxf(fmaxf(ub_pair(Wf, v0.x), ub_pair(Wf, v0.y)), fmaxf(ub_pair(Wf, v0.z), ub_pair(Wf, v0.w))),
+                               fmaxf(fmaxf(ub_pair(Wf, v1.x), ub_pair(Wf, v1.y)), fmaxf(ub_pair(Wf, v1.z), ub_pair(Wf, v1.w))));
+        if (!__any_sync(0xffffffffu, mx > 0.0f && mx >= LB_f)) continue;
+        const long long r0 = pos0 + 4 * p0, r1 = pos0 + 4 * (p0 + B);
+        visit2(v0.x, r0), visit2(v0.y, r0 + 1), visit2(v0.z, r0 + 2), visit2(v0.w, r0 + 3);
+        visit2(v1.x, r1), visit2(v1.y, r1 + 1), visit2(v1.z, r1 + 2), visit2(v1.w, r1 + 3);
+    }
+    if (nb & 3) {  // the last rows, warp 0 (ballot needs the whole warp)
+        if ((threadIdx.x >> 5) == 0) {
+            const int t = static_cast<int>(threadIdx.x);
+            visit2(t < (nb & 3) ? base[4 * nq + t] : sp, pos0 + 4 * nq + t);
+        }
+    }
+    __syncthreads();
+    const int nc = n_cand;
+    if (nc <= kMCandCap) {
+        fill_keyrank(keyrank, cand, nc);
+        __syncthreads();
+    }
+    mark(2);
+    int got;
+    if (nc <= kMCandCap) {
+        got = min(nc, k);
+        rank_select_kr(cand, nc, k, win);
+    } else {  // pathological ties: exact k rounds of "best row strictly after the previous"
+        if (threadIdx.x == 0) atomicAdd(&g_mcts_fallbacks, 1u);
+        got = 0;
+        Cand last{0.0, 0.0, kNoRow, -1};
+        for (int r = 0; r < k; ++r) {
+            Cand b{0.0, 0.0, kNoRow, -1};
+            for (long long i = threadIdx.x; i < nb; i += blockDim.x) {
+                const unsigned x = base[i];
+                if (mask && !hit_pair(hitc, x)) continue;
+                const double sc = __dadd_rn(W[x & 0xFFFFu], W[x >> 16]);
+                if (!(sc > 0.0)) continue;
+                const uint64_t row = x | hiS;
+                const Cand c{sc, row_usum(U, row), row, pack_pos(keyrank, pos0 + i)};
                 if (r > 0 && !precedes_kr(last, c)) continue;
                 if (b.row == kNoRow || precedes_kr(c, b)) b = c;
             }
@@ -366,7 +543,8 @@ __global__ void __launch_bounds__(kMThreads, 1) mcts_kernel(const __grid_constan
     const DevModel& M = L.M;
     const int n = M.n, K = L.topk;
     const int nW = (n + 1) * M.PP;
-    const long long chunk = ((L.n_base + C - 1) / C + 1) & ~1ll;  // even: 16-byte row pairs stay aligned
+    // a multiple of 2 rows (4 with 32-bit pair rows): 16-byte vectors stay aligned
+    const long long chunk = L.pair ? (((L.n_base + C - 1) / C + 3) & ~3ll) : (((L.n_base + C - 1) / C + 1) & ~1ll);
     const long long lo = min(L.n_base, static_cast<long long>(rank) * chunk);
     const long long hi = min(L.n_base, lo + chunk);
     // dynamic shared memory: tables (same offsets in every rank: peers read `cur`, `win` and
@@ -398,11 +576,19 @@ __global__ void __launch_bounds__(kMThreads, 1) mcts_kernel(const __grid_constan
     }
     const uint64_t* rows = L.base;  // whole pool (rank 0's adds); slice for the top-K scans
     const uint64_t* slice = L.base + lo;
-    if (L.rows_smem) {
+    const unsigned* slice32 = nullptr;  // pair rows: low halves only (L.pair)
+    const bool pair = L.rows_smem && L.pair;
+    if (pair) {
+        unsigned* r = reinterpret_cast<unsigned*>(carve(sizeof(unsigned) * chunk));
+        for (long long i = threadIdx.x; i < hi - lo; i += blockDim.x) r[i] = static_cast<unsigned>(__ldg(L.base + lo + i));
+        slice32 = r;
+    } else if (L.rows_smem) {
         uint64_t* r = reinterpret_cast<uint64_t*>(carve(sizeof(uint64_t) * chunk));
         for (long long i = threadIdx.x; i < hi - lo; i += blockDim.x) r[i] = __ldg(L.base + lo + i);
         slice = r;
     }
+    const unsigned sent16 = static_cast<unsigned>(n * M.PP);
+    const uint64_t hiS = static_cast<uint64_t>(sent16 | (sent16 << 16)) << 32;
     for (int e = threadIdx.x; e < nW; e += blockDim.x) Us[e] = __ldg(&M.U[e]);
     __shared__ int s_exit, s_usemask, n_got, s_hits;
     __shared__ uint64_t s_mask[4];
@@ -424,7 +610,9 @@ __global__ void __launch_bounds__(kMThreads, 1) mcts_kernel(const __grid_constan
             if (threadIdx.x == 0) s_usemask = *cl.map_shared_rank(&s_usemask, 0);
             __syncthreads();
             int sc = 0;
-            const int got = block_topk_exact(M, L.keyrank, slice, hi - lo, lo, cur, s_usemask ? s_mask : nullptr, K, Us, W, Wf,
+            const int got = pair ? block_topk_pair(M, L.keyrank, slice32, hi - lo, lo, cur, s_usemask ? s_mask : nullptr, K, Us, W, Wf,
+                                                   hitc, cand, win, nullptr, &sc, L.timers != 0)
+                                 : block_topk_bound(M, L.keyrank, slice, hi - lo, lo, cur, s_usemask ? s_mask : nullptr, K, Us, W, Wf,
                                              hitc, cand, win, nullptr, &sc, L.timers != 0);
             if (threadIdx.x == 0) {
                 n_got = got;
@@ -436,11 +624,20 @@ __global__ void __launch_bounds__(kMThreads, 1) mcts_kernel(const __grid_constan
     }
     // rank 0: the top-K of the whole pool under `cur` (mask: rows touching a sampled service)
     auto cluster_topk = [&](bool usemask, int* out, int* scored) -> int {
+        if (C == 1) {  // one CTA: its own top-K is the answer (no merge, no cluster barriers)
+            __syncthreads();
+            return pair ? block_topk_pair(M, L.keyrank, slice32, hi - lo, lo, cur, usemask ? s_mask : nullptr, K, Us, W,
+                                          Wf, hitc, cand, win, out, scored, L.timers != 0)
+                        : block_topk_bound(M, L.keyrank, slice, hi - lo, lo, cur, usemask ? s_mask : nullptr, K, Us,
+                                        W, Wf, hitc, cand, win, out, scored, L.timers != 0);
+        }
         if (threadIdx.x == 0) s_usemask = usemask ? 1 : 0;
         __syncthreads();
         cl.sync();
         int sc = 0;
-        const int got0 = block_topk_exact(M, L.keyrank, slice, hi - lo, lo, cur, usemask ? s_mask : nullptr, K, Us, W, Wf, hitc,
+        const int got0 = pair ? block_topk_pair(M, L.keyrank, slice32, hi - lo, lo, cur, usemask ? s_mask : nullptr, K, Us, W, Wf,
+                                                hitc, cand, win, nullptr, &sc, L.timers != 0)
+                               : block_topk_bound(M, L.keyrank, slice, hi - lo, lo, cur, usemask ? s_mask : nullptr, K, Us, W, Wf, hitc,
                                           cand, win, nullptr, &sc, L.timers != 0);
         if (threadIdx.x == 0) {
             n_got = got0;
@@ -493,7 +690,9 @@ __global__ void __launch_bounds__(kMThreads, 1) mcts_kernel(const __grid_constan
     for (int q = threadIdx.x; q < kL1Slots; q += blockDim.x) l1_n[q] = kL1Empty;
     if (threadIdx.x == 0) l1_used = 0;
     // rows by pool index for the utility adds: the on-chip copy when it holds the whole pool
-    const uint64_t* prow = (C == 1 && L.rows_smem) ? slice : rows;
+    const uint64_t* prow = (C == 1 && L.rows_smem && !pair) ? slice : rows;
+    const unsigned* prow32 = (C == 1 && pair) ? slice32 : nullptr;
+    auto rowat = [&](int idx) -> uint64_t { return prow32 ? (prow32[idx] | hiS) : prow[idx]; };
     const int max_depth = 2 * a.l_ref;
     const int tid = threadIdx.x;
     long long t_sel = 0, t_exp = 0, t_miss = 0, t_roll = 0, t_topk = 0, tc = 0;  // thread-0 clock64 phase split
@@ -528,40 +727,61 @@ __global__ void __launch_bounds__(kMThreads, 1) mcts_kernel(const __grid_constan
     if (tid == 0) nflags[0] = comp_satisfied(a.node_comp, n) ? kLeaf : 0;
     __syncthreads();
 
+    const int lane = tid & 31, warp = tid >> 5;
     for (int iter = 0; iter < L.budget && !s_abort; ++iter) {
-        // ---- selection (mcts.hpp:183-191): UCB1, first unvisited child, strict >
-        if (tid == 0) {
-            int node = 0;
-            s_edges = 0;
-            a.pathnodes[0] = 0;
-            s_path = 1;
+        // ---- selection (mcts.hpp:183-191): UCB1, first unvisited child, strict >.  Warp 0, a
+        // lane per child: the first unvisited child, else the first maximum.
+        if (warp == 0) {
+            int node = 0, edges = 0, path = 1;
+            if (lane == 0) a.pathnodes[0] = 0;
             while ((nflags[node] & kExpanded) && !(nflags[node] & kLeaf) && nnch[node] > 0) {
+                const int nch = nnch[node], f0 = nfirst[node];
                 const double log_n = L.logtab[max(1, nvis[node])];
-                int pick = -1;
-                double best = -1.0;
-                for (int q = 0; q < nnch[node]; ++q) {
-                    const int c = nfirst[node] + q;
-                    const int v = nvis[c];
-                    if (v == 0) {
-                        pick = q;
+                int pick = -1, bq = -1;
+                double bv = -1.0;
+                for (int q0 = 0; q0 < nch; q0 += 32) {
+                    const int q = q0 + lane;
+                    double val = -1.0;
+                    bool unvisited = false;
+                    if (q < nch) {
+                        const int v = nvis[f0 + q];
+                        unvisited = v == 0;
+                        if (!unvisited) {
+                            const double dv = static_cast<double>(v);
+                            val = __dadd_rn(__ddiv_rn(nval[f0 + q], dv),
+                                            __dmul_rn(L.ucb_c, __dsqrt_rn(__ddiv_rn(log_n, dv))));
+                        }
+                    }
+                    const unsigned um = __ballot_sync(0xffffffffu, unvisited);
+                    if (um) {
+                        pick = q0 + __ffs(um) - 1;
                         break;
                     }
-                    const double dv = static_cast<double>(v);
-                    const double val = __dadd_rn(__ddiv_rn(nval[c], dv),
-                                                 __dmul_rn(L.ucb_c, __dsqrt_rn(__ddiv_rn(log_n, dv))));
-                    if (val > best) {
-                        best = val;
-                        pick = q;
+                    int qq = q < nch ? q : 0x7fffffff;
+                    for (int off = 16; off > 0; off >>= 1) {
+                        const double ov = __shfl_xor_sync(0xffffffffu, val, off);
+                        const int oq = __shfl_xor_sync(0xffffffffu, qq, off);
+                        if (ov > val || (ov == val && oq < qq)) val = ov, qq = oq;
                     }
+                    if (val > bv) bv = val, bq = qq;  // strict: an earlier round wins ties
                 }
-                node = nfirst[node] + pick;
-                a.edges[s_edges++] = ncand[node];
-                a.pathnodes[s_path++] = node;
+                if (pick < 0) pick = bq;
+                node = f0 + pick;
+                if (lane == 0) {
+                    a.edges[edges] = ncand[node];
+                    a.pathnodes[path] = node;
+                }
+                ++edges;
+                ++path;
             }
-            s_node = node;
-            s_leaf = (nflags[node] & kLeaf) != 0;
-            s_expand = !s_leaf && !(nflags[node] & kExpanded);
-            s_est = 0;
+            if (lane == 0) {
+                s_edges = edges;
+                s_path = path;
+                s_node = node;
+                s_leaf = (nflags[node] & kLeaf) != 0;
+                s_expand = !s_leaf && !(nflags[node] & kExpanded);
+                s_est = 0;
+            }
         }
         __syncthreads();
         tick(t_sel);
@@ -573,21 +793,29 @@ __global__ void __launch_bounds__(kMThreads, 1) mcts_kernel(const __grid_constan
             }
         } else {
             if (s_expand) {  // expand (mcts.hpp:89-116)
-                if (tid == 0) {
+                if (warp == 0) {  // unsatisfied services in order (ballot compaction), then lane 0's shuffle
                     const double* nc = a.node_comp + static_cast<long long>(s_node) * n;
                     int m = 0;
-                    for (int i = 0; i < n; ++i)
-                        if (nc[i] < 1.0 - 1e-9) a.unsat[m++] = i;
-                    const int take = min(L.pick_services, m);
-                    for (int i = 0; i < take; ++i) {
-                        const int j = i + static_cast<int>(mt_pick(g, static_cast<uint64_t>(m - i)));
-                        const int t = a.unsat[i];
-                        a.unsat[i] = a.unsat[j];
-                        a.unsat[j] = t;
+                    for (int i0 = 0; i0 < n; i0 += 32) {
+                        const int i = i0 + lane;
+                        const bool u = i < n && nc[i] < 1.0 - 1e-9;
+                        const unsigned bm = __ballot_sync(0xffffffffu, u);
+                        if (u) a.unsat[m + __popc(bm & lanemask_lt())] = i;
+                        m += __popc(bm);
                     }
-                    for (int w = 0; w < 4; ++w) s_mask[w] = 0;
-                    for (int i = 0; i < take; ++i) s_mask[a.unsat[i] >> 6] |= 1ull << (a.unsat[i] & 63);
-                    s_take = take;
+                    __syncwarp();
+                    if (lane == 0) {
+                        const int take = min(L.pick_services, m);
+                        for (int i = 0; i < take; ++i) {
+                            const int j = i + static_cast<int>(mt_pick(g, static_cast<uint64_t>(m - i)));
+                            const int t = a.unsat[i];
+                            a.unsat[i] = a.unsat[j];
+                            a.unsat[j] = t;
+                        }
+                        for (int w = 0; w < 4; ++w) s_mask[w] = 0;
+                        for (int i = 0; i < take; ++i) s_mask[a.unsat[i] >> 6] |= 1ull << (a.unsat[i] & 63);
+                        s_take = take;
+                    }
                 }
                 for (int i = tid; i < n; i += blockDim.x) cur[i] = a.node_comp[static_cast<long long>(s_node) * n + i];
                 __syncthreads();
@@ -598,23 +826,39 @@ __global__ void __launch_bounds__(kMThreads, 1) mcts_kernel(const __grid_constan
                     ++s_expands;
                     s_expand_rows += s_scored;
                 }
-                if (tid == 0) {
-                    if (s_nodes + got > a.max_nodes) {
-                        s_abort = 3;  // node storage exhausted (host sizes it from the budget)
-                    } else {
-                        const int first = s_nodes;
-                        for (int q = 0; q < got; ++q) {
-                            const int c = first + q;
-                            double* cc = a.node_comp + static_cast<long long>(c) * n;
-                            for (int i = 0; i < n; ++i) cc[i] = cur[i];
-                            add_row_util(M, Us, prow[s_out[q]], cc);
+                // the children: a warp each (copy, add the config's utility, satisfied flag)
+                const int first = s_nodes;
+                const bool fits = first + got <= a.max_nodes;
+                if (fits) {
+                    for (int q = warp; q < got; q += kMWarps) {
+                        const int c = first + q;
+                        double* cc = a.node_comp + static_cast<long long>(c) * n;
+                        for (int i = lane; i < n; i += 32) cc[i] = cur[i];
+                        __syncwarp();
+                        if (lane < 4) {  // members have distinct services: the adds commute
+                            const int code = static_cast<int>((rowat(s_out[q]) >> (16 * lane)) & 0xFFFFull);
+                            const int svc = code / M.PP;
+                            if (svc < n) cc[svc] = __dadd_rn(cc[svc], Us[code]);
+                        }
+                        __syncwarp();
+                        bool uns = false;
+                        for (int i = lane; i < n; i += 32) uns |= cc[i] < 1.0 - 1e-9;
+                        const bool sat = !__any_sync(0xffffffffu, uns);
+                        if (lane == 0) {
                             ncand[c] = s_out[q];
                             nvis[c] = 0;
                             nval[c] = 0.0;
                             nnch[c] = 0;
                             nfirst[c] = 0;
-                            nflags[c] = comp_satisfied(cc, n) ? kLeaf : 0;
+                            nflags[c] = sat ? kLeaf : 0;
                         }
+                    }
+                }
+                __syncthreads();
+                if (tid == 0) {
+                    if (!fits) {
+                        s_abort = 3;  // node storage exhausted (host sizes it from the budget)
+                    } else {
                         nfirst[s_node] = first;
                         nnch[s_node] = got;
                         nflags[s_node] |= kExpanded;
@@ -635,108 +879,124 @@ __global__ void __launch_bounds__(kMThreads, 1) mcts_kernel(const __grid_constan
                     s_node = c;
                 }
                 s_steps = 0;
+                s_done = 0;
             }
             __syncthreads();
             for (int i = tid; i < n; i += blockDim.x) cur[i] = a.node_comp[static_cast<long long>(s_node) * n + i];
             __syncthreads();
-            // rollout (mcts.hpp:122-143) with the RolloutCache keyed by the unsatisfied bitmap
+            // rollout (mcts.hpp:122-143) with the RolloutCache keyed by the unsatisfied bitmap:
+            // warp 0 steps alone through cache hits; the block joins for a miss's top-K
             for (;;) {
-                if (tid == 0) {
-                    s_done = 0;
-                    s_miss = 0;
-                    if (comp_satisfied(cur, n)) {
-                        s_done = 1;
-                        s_est = s_steps;
-                    } else if (s_steps >= max_depth) {
-                        s_done = 1;
-                        s_est = max_depth;
-                    } else {
+                if (warp == 0) {
+                    for (;;) {
                         uint64_t kw[4] = {0, 0, 0, 0};
-                        for (int i = 0; i < n; ++i)
-                            if (cur[i] < 1.0 - 1e-9) kw[i >> 6] |= 1ull << (i & 63);
-                        uint64_t h = 0x9e3779b97f4a7c15ull;
-                        for (int w = 0; w < 4; ++w) {
-                            h ^= kw[w];
-                            h *= 0xbf58476d1ce4e5b9ull;
-                            h ^= h >> 31;
+                        for (int i0 = 0; i0 < n; i0 += 32) {
+                            const int i = i0 + lane;
+                            const unsigned bm = __ballot_sync(0xffffffffu, i < n && cur[i] < 1.0 - 1e-9);
+                            kw[i0 >> 6] |= static_cast<uint64_t>(bm) << (i0 & 63);
                         }
-                        // level 1: the on-chip copy of the cache (keys + pools in shared memory)
-                        s_l1 = -1;
-                        s_l1new = -1;
-                        if (use_l1) {
-                            unsigned q = static_cast<unsigned>(h >> 32) & (kL1Slots - 1);
-                            for (int t = 0; t < kL1Slots; ++t, q = (q + 1) & (kL1Slots - 1)) {
-                                if (l1_n[q] == kL1Empty) break;
-                                if (l1_key[q][0] == kw[0] && l1_key[q][1] == kw[1] && l1_key[q][2] == kw[2] &&
-                                    l1_key[q][3] == kw[3]) {
-                                    s_l1 = static_cast<int>(q);
-                                    break;
+                        int st = 0, idx = 0;  // st: 1 done, 2 miss, 3 abort
+                        if (lane == 0) {
+                            s_miss = 0;
+                            if (!(kw[0] | kw[1] | kw[2] | kw[3])) {  // satisfied
+                                s_done = 1;
+                                s_est = s_steps;
+                                st = 1;
+                            } else if (s_steps >= max_depth) {
+                                s_done = 1;
+                                s_est = max_depth;
+                                st = 1;
+                            } else {
+                                uint64_t h = 0x9e3779b97f4a7c15ull;
+                                for (int w = 0; w < 4; ++w) {
+                                    h ^= kw[w];
+                                    h *= 0xbf58476d1ce4e5b9ull;
+                                    h ^= h >> 31;
+                                }
+                                // level 1: the on-chip copy of the cache (keys + pools in shared memory)
+                                s_l1 = -1;
+                                s_l1new = -1;
+                                if (use_l1) {
+                                    unsigned q = static_cast<unsigned>(h >> 32) & (kL1Slots - 1);
+                                    for (int t = 0; t < kL1Slots; ++t, q = (q + 1) & (kL1Slots - 1)) {
+                                        if (l1_n[q] == kL1Empty) break;
+                                        if (l1_key[q][0] == kw[0] && l1_key[q][1] == kw[1] && l1_key[q][2] == kw[2] &&
+                                            l1_key[q][3] == kw[3]) {
+                                            s_l1 = static_cast<int>(q);
+                                            break;
+                                        }
+                                    }
+                                }
+                                if (s_l1 < 0) {  // level 2: the global table (source of truth)
+                                    unsigned sl = static_cast<unsigned>(h) & a.tab_mask;
+                                    for (unsigned t = 0;; ++t, sl = (sl + 1) & a.tab_mask) {
+                                        if (t > a.tab_mask) {
+                                            s_abort = 2;  // cache full
+                                            st = 3;
+                                            break;
+                                        }
+                                        if (!a.tag[sl]) {  // miss: insert, pool built by the block
+                                            a.tag[sl] = 1;
+                                            for (int w = 0; w < 4; ++w) a.key[4ull * sl + w] = kw[w];
+                                            s_miss = 1;
+                                            st = 2;
+                                            break;
+                                        }
+                                        if (a.key[4ull * sl] == kw[0] && a.key[4ull * sl + 1] == kw[1] &&
+                                            a.key[4ull * sl + 2] == kw[2] && a.key[4ull * sl + 3] == kw[3])
+                                            break;
+                                    }
+                                    s_slot = static_cast<int>(sl);
+                                    if (s_miss && use_l1 && l1_used < kL1Slots * 3 / 4) {  // mirror the new key on chip
+                                        unsigned q = static_cast<unsigned>(h >> 32) & (kL1Slots - 1);
+                                        while (l1_n[q] != kL1Empty) q = (q + 1) & (kL1Slots - 1);
+                                        for (int w = 0; w < 4; ++w) l1_key[q][w] = kw[w];
+                                        l1_n[q] = kL1Pending;
+                                        ++l1_used;
+                                        s_l1new = static_cast<int>(q);
+                                    }
+                                }
+                                if (st == 0) {  // hit: a uniform pick from the cached pool
+                                    const int pn = s_l1 >= 0 ? l1_n[s_l1] : a.pool_n[s_slot];
+                                    if (pn <= 0) {
+                                        s_abort = 1;  // "rollout: no candidate config serves the remaining demand"
+                                        st = 3;
+                                    } else {
+                                        const unsigned pk = static_cast<unsigned>(mt_pick(g, static_cast<uint64_t>(pn)));
+                                        idx = static_cast<int>(s_l1 >= 0 ? l1_pool[s_l1][pk]
+                                                                         : a.pool[static_cast<long long>(s_slot) * K + pk]);
+                                        a.picked[s_steps++] = idx;
+                                    }
                                 }
                             }
                         }
-                        if (s_l1 < 0) {  // level 2: the global table (source of truth)
-                            unsigned sl = static_cast<unsigned>(h) & a.tab_mask;
-                            for (unsigned t = 0;; ++t, sl = (sl + 1) & a.tab_mask) {
-                                if (t > a.tab_mask) {
-                                    s_abort = 2;  // cache full
-                                    break;
-                                }
-                                if (!a.tag[sl]) {  // miss: insert, pool built below
-                                    a.tag[sl] = 1;
-                                    for (int w = 0; w < 4; ++w) a.key[4ull * sl + w] = kw[w];
-                                    s_miss = 1;
-                                    break;
-                                }
-                                if (a.key[4ull * sl] == kw[0] && a.key[4ull * sl + 1] == kw[1] &&
-                                    a.key[4ull * sl + 2] == kw[2] && a.key[4ull * sl + 3] == kw[3])
-                                    break;
-                            }
-                            s_slot = static_cast<int>(sl);
-                            if (s_miss && use_l1 && l1_used < kL1Slots * 3 / 4) {  // mirror the new key on chip
-                                unsigned q = static_cast<unsigned>(h >> 32) & (kL1Slots - 1);
-                                while (l1_n[q] != kL1Empty) q = (q + 1) & (kL1Slots - 1);
-                                for (int w = 0; w < 4; ++w) l1_key[q][w] = kw[w];
-                                l1_n[q] = kL1Pending;
-                                ++l1_used;
-                                s_l1new = static_cast<int>(q);
-                            }
+                        st = __shfl_sync(0xffffffffu, st, 0);
+                        if (st) break;
+                        idx = __shfl_sync(0xffffffffu, idx, 0);
+                        if (lane < 4) {  // rollout add (mcts.hpp:139): distinct services, the adds commute
+                            const int code = static_cast<int>((rowat(idx) >> (16 * lane)) & 0xFFFFull);
+                            const int svc = code / M.PP;
+                            if (svc < n) cur[svc] = __dadd_rn(cur[svc], Us[code]);
                         }
+                        __syncwarp();
                     }
                 }
                 __syncthreads();
-                if (s_done || s_abort) break;
                 tick(t_roll);
-                if (s_miss) {  // cache miss: top-K of the whole base pool (mcts.hpp:129-133)
-                    tick(t_miss);
-                    const int got = cluster_topk(false, s_out, &s_scored);
-                    tick(t_topk);
-                    if (tid < got) a.pool[static_cast<long long>(s_slot) * K + tid] = static_cast<unsigned>(s_out[tid]);
-                    if (s_l1new >= 0 && tid < got) l1_pool[s_l1new][tid] = static_cast<unsigned>(s_out[tid]);
-                    if (tid == 0) {
-                        a.pool_n[s_slot] = got;
-                        if (s_l1new >= 0) {
-                            l1_n[s_l1new] = got;
-                            s_l1 = s_l1new;
-                        }
-                        ++s_builds;
-                    }
-                    __syncthreads();
-                    tick(t_miss);
-                }
+                if (s_done || s_abort) break;
+                // cache miss: top-K of the whole base pool (mcts.hpp:129-133); warp 0 then
+                // finds the key again and picks from the new pool
+                const int got = cluster_topk(false, s_out, &s_scored);
+                tick(t_topk);
+                if (tid < got) a.pool[static_cast<long long>(s_slot) * K + tid] = static_cast<unsigned>(s_out[tid]);
+                if (s_l1new >= 0 && tid < got) l1_pool[s_l1new][tid] = static_cast<unsigned>(s_out[tid]);
                 if (tid == 0) {
-                    const int pn = s_l1 >= 0 ? l1_n[s_l1] : a.pool_n[s_slot];
-                    if (pn <= 0) {
-                        s_abort = 1;  // "rollout: no candidate config serves the remaining demand"
-                    } else {
-                        const unsigned pk = static_cast<unsigned>(mt_pick(g, static_cast<uint64_t>(pn)));
-                        const int idx = static_cast<int>(s_l1 >= 0 ? l1_pool[s_l1][pk]
-                                                                   : a.pool[static_cast<long long>(s_slot) * K + pk]);
-                        add_row_util(M, Us, prow[idx], cur);
-                        a.picked[s_steps++] = idx;
-                    }
+                    a.pool_n[s_slot] = got;
+                    if (s_l1new >= 0) l1_n[s_l1new] = got;
+                    ++s_builds;
                 }
                 __syncthreads();
-                if (s_abort) break;
+                tick(t_miss);
             }
             if (s_abort) break;
             if (tid == 0) {  // mcts.hpp:210-218
@@ -804,7 +1064,7 @@ __global__ void __launch_bounds__(kMThreads, 1) mcts_kernel(const __grid_constan
 }
 
 // Dynamic shared memory of mcts_kernel (must mirror its carve order).
-size_t mcts_smem_bytes(int n, int PP, int max_nodes, long long n_base, bool node_smem, bool rows_smem) {
+size_t mcts_smem_bytes(int n, int PP, int max_nodes, long long n_base, bool node_smem, bool rows_smem, bool pair) {
     // n_base: rows of ONE rank's slice
     const size_t nW = static_cast<size_t>(n + 1) * PP;
     size_t off = 0;
@@ -821,7 +1081,7 @@ size_t mcts_smem_bytes(int n, int PP, int max_nodes, long long n_base, bool node
         for (int i = 0; i < 4; ++i) carve(4 * static_cast<size_t>(max_nodes));
         carve(static_cast<size_t>(max_nodes));
     }
-    if (rows_smem) carve(8 * static_cast<size_t>(n_base));
+    if (rows_smem) carve((pair ? 4 : 8) * static_cast<size_t>(n_base));
     return off;
 }
 void mcts_read_topk_timers(unsigned long long* h) { cudaMemcpyFromSymbol(h, g_tk, sizeof g_tk); }
