@@ -1215,8 +1215,8 @@ std::vector<MctsDeviceResult> Engine::mcts_device_group(const std::vector<std::v
                 mcts_read_topk_timers(tk);
                 if (tk[5])
                     std::fprintf(stderr, "[mcts] top-K (cumulative) calls %llu, cycles/call: tables %.0f pass1 %.0f pass2 %.0f "
-                                 "rank %.0f, candidates/call %.1f, rescans %llu\n", tk[5], double(tk[0]) / tk[5], double(tk[1]) / tk[5],
-                                 double(tk[2]) / tk[5], double(tk[3]) / tk[5], double(tk[4]) / tk[5], tk[6]);
+                                 "keyrank %.0f rank %.0f, candidates/call %.1f\n", tk[5], double(tk[0]) / tk[5], double(tk[1]) / tk[5],
+                                 double(tk[2]) / tk[5], double(tk[7]) / tk[5], double(tk[3]) / tk[5], double(tk[4]) / tk[5]);
                 std::fprintf(stderr, "[mcts] solve %d: %.1f ms device, cycles sel %lld expand-host %lld miss-host %lld topk %lld "
                              "rollout-ctl %lld, builds %d expands %d iters %d, exact-path top-Ks (cumulative) %d\n",
                              b0 + q, ms, t[0], t[1], t[2], t[3], t[4], out[4], out[7], out[6], out[20]);

@@ -133,6 +133,22 @@ __device__ __forceinline__ void rank_select_kr(const Cand* cand, int nc, int k, 
     }
 }
 
+// Bitonic sort of the warp's lane values, descending (lane q ends with the q-th largest).
+__device__ __forceinline__ float warp_sort_desc_f(float v) {
+    const int lane = static_cast<int>(threadIdx.x & 31u);
+#pragma unroll
+    for (int size = 2; size <= 32; size <<= 1) {
+#pragma unroll
+        for (int j = size >> 1; j > 0; j >>= 1) {
+            const float o = __shfl_xor_sync(0xffffffffu, v, j);
+            const bool desc = (lane & size) == 0 || size == 32;
+            const bool low = (lane & j) == 0;
+            v = (low == desc) ? fmaxf(v, o) : fminf(v, o);
+        }
+    }
+    return v;
+}
+
 // warp_kth (common.cuh) on floats: half the shuffles of the double version.
 __device__ __forceinline__ float warp_kth_f(float v, int k) {
     const int lane = static_cast<int>(threadIdx.x & 31u);
@@ -416,28 +432,56 @@ __device__ __noinline__ int block_topk_pair(const DevModel& M, const unsigned* k
         for (int off = 16; off > 0; off >>= 1) hits += __shfl_xor_sync(0xffffffffu, hits, off);
         if ((threadIdx.x & 31u) == 0) atomicAdd(&n_hit, hits);
     }
-    const float uk = warp_kth_f(umax, k);
-    if ((threadIdx.x & 31u) == 0) atomicMax(&t_fbits, __float_as_uint(uk));
+    // U_K = the K-th largest of ALL lane maxima: every warp sorts its lane maxima, then a
+    // tree of bitonic merges (top 32 of two sorted lists: elementwise max against the partner
+    // reversed, then 5 merge stages) leaves the block's top 32 in warp 0.
+    __shared__ float ws[2][kMWarps / 2][32];
+    {
+        const int w = static_cast<int>(threadIdx.x >> 5), lane = static_cast<int>(threadIdx.x & 31u);
+        float srt = warp_sort_desc_f(umax);
+        int buf = 0;
+        for (int half = static_cast<int>(blockDim.x >> 6); half >= 1; half >>= 1, buf ^= 1) {
+            if (w >= half && w < 2 * half) ws[buf][w - half][lane] = srt;
+            __syncthreads();
+            if (w < half) {
+                float v = fmaxf(srt, ws[buf][w][31 - lane]);
+#pragma unroll
+                for (int j = 16; j > 0; j >>= 1) {
+                    const float o = __shfl_xor_sync(0xffffffffu, v, j);
+                    v = (lane & j) == 0 ? fmaxf(v, o) : fminf(v, o);
+                }
+                srt = v;
+            }
+        }
+        if (w == 0 && lane == k - 1) t_fbits = __float_as_uint(srt);
+    }
     __syncthreads();
     mark(1);
     const double LB = __dmul_rd(static_cast<double>(__uint_as_float(t_fbits)), 1.0 - 0x1p-20);
     const float LB_f = __double2float_rd(LB);
-    auto visit2 = [&](unsigned x, long long pos) {
-        bool take = false;
-        double sc = 0.0;
-        const float ub = ub_pair(Wf, x);
-        if (ub > 0.0f && ub >= LB_f && (!mask || hit_pair(hitc, x))) {
-            sc = __dadd_rn(W[x & 0xFFFFu], W[x >> 16]);
-            take = sc > 0.0 && sc >= LB;
+    // one compaction per 8 rows: the lane's taken rows, a warp scan, one atomic per warp
+    auto emit = [&](const unsigned (&x)[8], const double (&sc)[8], unsigned tk, long long r0, long long r1) {
+        const int lane = static_cast<int>(threadIdx.x & 31u);
+        const int cnt = __popc(tk);
+        int incl = cnt;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int t = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += t;
         }
-        const unsigned b = __ballot_sync(0xffffffffu, take);
-        if (b) {
-            int at = 0;
-            if ((threadIdx.x & 31u) == 0) at = atomicAdd(&n_cand, __popc(b));
-            at = __shfl_sync(0xffffffffu, at, 0) + __popc(b & lanemask_lt());
-            if (take && at < kMCandCap) {
-                const uint64_t row = x | hiS;
-                cand[at] = Cand{sc, row_usum(U, row), row, pos};
+        const int total = __shfl_sync(0xffffffffu, incl, 31);
+        if (total == 0) return;
+        int at = 0;
+        if (lane == 31) at = atomicAdd(&n_cand, total);
+        at = __shfl_sync(0xffffffffu, at, 31) + incl - cnt;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            if ((tk >> j) & 1u) {
+                if (at < kMCandCap) {
+                    const uint64_t row = x[j] | hiS;
+                    cand[at] = Cand{sc[j], row_usum(U, row), row, (j < 4 ? r0 + j : r1 + j - 4)};
+                }
+                ++at;
             }
         }
     };
@@ -447,26 +491,50 @@ __device__ __noinline__ int block_topk_pair(const DevModel& M, const unsigned* k
     for (long long p0 = threadIdx.x; p0 < nq2; p0 += 2 * B) {
         const uint4 v0 = p0 < nq ? base4[p0] : padv;
         const uint4 v1 = p0 + B < nq ? base4[p0 + B] : padv;
-        const float mx = fmaxf(fmaxf(fmaxf(ub_pair(Wf, v0.x), ub_pair(Wf, v0.y)), fmaxf(ub_pair(Wf, v0.z), ub_pair(Wf, v0.w))),
-                               fmaxf(fmaxf(ub_pair(Wf, v1.x), ub_pair(Wf, v1.y)), fmaxf(ub_pair(Wf, v1.z), ub_pair(Wf, v1.w))));
+        const unsigned x[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
+        float ub[8];
+        float mx = 0.0f;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            ub[j] = ub_pair(Wf, x[j]);
+            if (mask && !hit_pair(hitc, x[j])) ub[j] = 0.0f;
+            mx = fmaxf(mx, ub[j]);
+        }
         if (!__any_sync(0xffffffffu, mx > 0.0f && mx >= LB_f)) continue;
-        const long long r0 = pos0 + 4 * p0, r1 = pos0 + 4 * (p0 + B);
-        visit2(v0.x, r0), visit2(v0.y, r0 + 1), visit2(v0.z, r0 + 2), visit2(v0.w, r0 + 3);
-        visit2(v1.x, r1), visit2(v1.y, r1 + 1), visit2(v1.z, r1 + 2), visit2(v1.w, r1 + 3);
+        double sc[8];
+        unsigned tk = 0;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            sc[j] = 0.0;
+            if (ub[j] > 0.0f && ub[j] >= LB_f) {
+                sc[j] = __dadd_rn(W[x[j] & 0xFFFFu], W[x[j] >> 16]);
+                if (sc[j] > 0.0 && sc[j] >= LB) tk |= 1u << j;
+            }
+        }
+        emit(x, sc, tk, pos0 + 4 * p0, pos0 + 4 * (p0 + B));
     }
-    if (nb & 3) {  // the last rows, warp 0 (ballot needs the whole warp)
+    if (nb & 3) {  // the last rows, warp 0 (the scan needs the whole warp)
         if ((threadIdx.x >> 5) == 0) {
             const int t = static_cast<int>(threadIdx.x);
-            visit2(t < (nb & 3) ? base[4 * nq + t] : sp, pos0 + 4 * nq + t);
+            unsigned x[8] = {t < (nb & 3) ? base[4 * nq + t] : sp, sp, sp, sp, sp, sp, sp, sp};
+            double sc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+            unsigned tk = 0;
+            const float ub = ub_pair(Wf, x[0]);
+            if (ub > 0.0f && ub >= LB_f && (!mask || hit_pair(hitc, x[0]))) {
+                sc[0] = __dadd_rn(W[x[0] & 0xFFFFu], W[x[0] >> 16]);
+                if (sc[0] > 0.0 && sc[0] >= LB) tk = 1u;
+            }
+            emit(x, sc, tk, pos0 + 4 * nq + t, 0);
         }
     }
     __syncthreads();
+    mark(2);
     const int nc = n_cand;
     if (nc <= kMCandCap) {
         fill_keyrank(keyrank, cand, nc);
         __syncthreads();
     }
-    mark(2);
+    mark(7);
     int got;
     if (nc <= kMCandCap) {
         got = min(nc, k);
