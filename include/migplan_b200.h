@@ -305,6 +305,13 @@ int mig_two_phase_parallel(mig_ctx* ctx, const mig_ga_params* params, mig_config
 /* lower_bound(services, profiles), bench.hpp:93-108 */
 int mig_lower_bound(const mig_ctx* ctx, int32_t* out);
 
+/* baseline(kind, services, profiles), bench.hpp:42-90: the static-partition deployments.
+ * kind: 0 = A100-7/7 (whole GPUs), 1 = A100-7x1/7 (1/7 instances packed seven to a GPU),
+ * 2 = A100-MIX (4/7 + 2/7 + 1/7 per GPU).  Configs in construction order (make_deployment
+ * sorts them); PlanningError "service '<id>' is infeasible on a <s>/7 instance under its
+ * latency ceiling" when a needed size has no feasible batch. */
+int mig_baseline(const mig_ctx* ctx, int32_t kind, mig_config* out, int32_t cap, int32_t* n_out);
+
 /* brute_force_optimum(services, profiles, rules, cap, node_budget), bench.hpp:160-219: the
  * exhaustive minimum-GPU search over config multisets (iterative deepening, admissible bound).
  * The context's pool must be the max_mix >= min(n, 7) pool (the product holds <= 4-member

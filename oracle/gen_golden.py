@@ -261,7 +261,36 @@ def gen_brute_force(ref):
     return res
 
 
-SECTIONS = {"brute_force": gen_brute_force, "greedy": gen_greedy, "mcts": gen_mcts, "ga": gen_ga, "topk": gen_topk, "partitions": gen_partitions,
+def gen_baseline(ref):
+    """baseline(kind, services, profiles) (bench.hpp:42-90) for the three static partitions on
+    fixture workloads (with and without the 1/7- and 2/7-infeasible gpt2-medium services),
+    generated workloads and two-model random workloads.  outcome: plan | "error:<msg>"."""
+    fx, tm = S.profiles(), S.two_model_store()
+    cases = []
+    for name in ("slos_day", "slos_night", "slos_24"):
+        sv = S.fixture_services(name, fx)
+        cases.append((name, fx, sv))
+        cases.append((name + "_no_gpt2", fx, [x for x in sv if x.model_name != "gpt2-medium"]))
+    for s in (1, 2, 3):
+        sv = mp.gen_workload(12, True, 6.0 + s, 0.6, 100.0, 900 + s, fx, backend=S.host_backend())
+        cases.append((f"gen12_{s}_no_gpt2", fx, [x for x in sv if x.model_name != "gpt2-medium"]))
+    for seed in (3, 4, 7, 8):
+        ps, sv = S.random_workload(6, seed)
+        cases.append((f"rand6_{seed}", ps, list(sv)))
+    res = {}
+    for name, ps, sv in cases:
+        for kind in (0, 1, 2):
+            try:
+                dep = mp.baseline(kind, sv, ps, backend=ref)
+                out = S.plan_key([g.config for g in dep.gpus])
+            except mp.PlanningError as e:
+                out = "error:" + str(e)
+            res[f"{name}/{kind}"] = {"store": store_name(ps), "services": svc_json(sv), "kind": kind, "outcome": out}
+            print(f"baseline {name}/{kind}: {out if isinstance(out, str) else len(out)}", flush=True)
+    return res
+
+
+SECTIONS = {"baseline": gen_baseline, "brute_force": gen_brute_force, "greedy": gen_greedy, "mcts": gen_mcts, "ga": gen_ga, "topk": gen_topk, "partitions": gen_partitions,
             "greedy_big": gen_greedy_big, "rollouts": gen_rollouts, "ga_parallel": gen_ga_parallel}
 
 

@@ -789,6 +789,21 @@ int mig_lower_bound(const mig_ctx* ctx, int32_t* out) {
     return guarded([&] { *out = lower_bound(ctx->services, ctx->profiles); });
 }
 
+int mig_baseline(const mig_ctx* ctx, int32_t kind, mig_config* out, int32_t cap, int32_t* n_out) {
+    int rc = MIG_OK;
+    *n_out = 0;
+    int g = guarded([&] {  // the reference's baseline (bench.hpp:42-90), in construction order
+        if (kind < 0 || kind > 2) throw std::invalid_argument("baseline kind must be 0, 1 or 2");
+        const BaselineKind k = kind == 0 ? BaselineKind::WholeGpu : kind == 1 ? BaselineKind::SevenSlices
+                                                                              : BaselineKind::Mix421;
+        Deployment dep = baseline(k, ctx->services, ctx->profiles);
+        std::vector<GpuConfig> plan;
+        for (const auto& d : dep.gpus) plan.push_back(d.config);
+        rc = emit_plan(plan, ctx->services, out, cap, n_out);
+    });
+    return g != MIG_OK ? g : rc;
+}
+
 int mig_brute_force_optimum(mig_ctx* ctx, int32_t cap, int64_t node_budget, mig_config* out, int32_t out_cap,
                             int32_t* n_out, int32_t* found) {
     int rc = MIG_OK;

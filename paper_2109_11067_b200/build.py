@@ -16,7 +16,7 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 OUT_DIR = os.path.join(HERE, "_native")
 LIB = os.path.join(OUT_DIR, "libmigplan_b200.so")
-SOURCES = ["model.cpp", "kernels.cu", "topk.cu", "rollout.cu", "ga.cu", "mcts.cu", "bf.cu", "engine.cu", "search.cpp", "capi.cpp"]
+SOURCES = ["model.cpp", "kernels.cu", "topk.cu", "rollout.cu", "ga.cu", "mcts.cu", "keyrank.cu", "bf.cu", "engine.cu", "search.cpp", "capi.cpp"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-std=c++20", "-O3", "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo", "-fmad=false",
          "-Xcompiler", "-fPIC,-ffp-contract=off,-O3,-Wall", f"-I{os.path.join(ROOT, 'include')}", f"-I{CSRC}",

@@ -3,10 +3,13 @@
     python -m paper_2109_11067_b200.cli optimize --mode fast --slos S.json --profiles P.json -o dep.json
     python -m paper_2109_11067_b200.cli lowerbound --slos S.json --profiles P.json
     python -m paper_2109_11067_b200.cli oracle --slos S.json --profiles P.json --cap 3 -o dep.json
+    python -m paper_2109_11067_b200.cli baseline --kind 7of7|7x1|mix --slos S.json --profiles P.json -o dep.json
+    python -m paper_2109_11067_b200.cli gen-workload --n 24 --seed 7 --profiles P.json -o slos.json
     python -m paper_2109_11067_b200.cli enumerate-partitions [--rules R.json] [-o parts.json]
 
-Restates the reference CLI's `optimize` / `lowerbound` / `oracle` / `enumerate-partitions`
-(proj/tools/migplan.cpp:88-147, 159-200, 244-251, 262-300, 382-397) over the C-ABI:
+Restates the reference CLI's `optimize` / `lowerbound` / `oracle` / `baseline` /
+`gen-workload` / `enumerate-partitions` (proj/tools/migplan.cpp:88-147, 159-215, 244-251,
+262-345, 382-397) over the C-ABI:
   - output files are `json.dump(indent=2)` with sorted keys + "\\n" — the byte layout of
     nlohmann's `dump(2)` (write_json_file, io.hpp:44-48; std::map keys are sorted);
   - trace lines go to stdout as compact sorted-key JSON (migplan.cpp:99-137), numbers through
@@ -181,6 +184,34 @@ def cmd_oracle(a, manifest: Manifest) -> int:  # migplan.cpp:382-397 (brute_forc
     return 0
 
 
+def cmd_baseline(a, manifest: Manifest) -> int:  # migplan.cpp:294-309
+    profiles = mp.load_profiles(a.profiles)
+    services = mp.load_services(a.slos, profiles)
+    if a.kind not in mp.BASELINE_KINDS:
+        raise mp.SchemaError(f"unknown baseline kind '{a.kind}' (expected 7of7, 7x1, or mix)")
+    dep = mp.baseline(a.kind, services, profiles, backend=_BACKEND)
+    dump_file(a.output, mp.deployment_to_json(dep))
+    manifest.write(a.output)
+    return 0
+
+
+def cmd_gen_workload(a, manifest: Manifest) -> int:  # migplan.cpp:324-345 (services_to_json, io.hpp:153-161)
+    if a.seed is None:
+        raise mp.SchemaError("--seed is required for gen-workload")
+    if a.dist not in ("normal", "lognormal"):
+        raise mp.SchemaError(f"unknown distribution '{a.dist}'")
+    normal = a.dist == "normal"
+    mu = a.mu if a.mu >= 0.0 else (5000.0 if normal else 8.0)
+    sigma = a.sigma if a.sigma >= 0.0 else (2000.0 if normal else 0.6)
+    profiles = mp.load_profiles(a.profiles)
+    sv = mp.gen_workload(a.n, not normal, mu, sigma, a.latency_ms, a.seed, profiles, backend=_BACKEND)
+    dump_file(a.output, {"services": [{"id": s.service_id, "model": s.model_name,
+                                       "required_rps": out_num(s.required_rps),
+                                       "max_p90_ms": out_num(s.max_p90_ms)} for s in sv]})
+    manifest.write(a.output)
+    return 0
+
+
 def cmd_enumerate(a, manifest: Manifest) -> int:  # migplan.cpp:56-64
     rules = load_rules(a.rules) if a.rules else mp.PartitionRuleSet.defaults()
     parts = mp.enumerate_maximal_partitions(rules, backend=_BACKEND)
@@ -222,6 +253,22 @@ def build_parser() -> argparse.ArgumentParser:
     lb.add_argument("--slos", required=True)
     lb.add_argument("--profiles", required=True)
     lb.add_argument("-o", "--output", default="")
+    bl = sub.add_parser("baseline", help="Static-partition baseline deployments")
+    bl.add_argument("--kind", required=True, help="7of7 | 7x1 | mix")
+    bl.add_argument("--slos", required=True)
+    bl.add_argument("--profiles", required=True)
+    bl.add_argument("-o", "--output", required=True)
+    bl.add_argument("--backend", default="", help=argparse.SUPPRESS)
+    gw = sub.add_parser("gen-workload", help="Generate a random workload SLO file")
+    gw.add_argument("--dist", default="lognormal", help="normal | lognormal")
+    gw.add_argument("--n", type=int, default=24)
+    gw.add_argument("--mu", type=float, default=-1.0)
+    gw.add_argument("--sigma", type=float, default=-1.0)
+    gw.add_argument("--latency-ms", type=float, default=100.0)
+    gw.add_argument("--seed", type=int, default=None)
+    gw.add_argument("--profiles", required=True)
+    gw.add_argument("-o", "--output", required=True)
+    gw.add_argument("--backend", default="", help=argparse.SUPPRESS)
     orc = sub.add_parser("oracle", help="Brute-force minimum-GPU deployment (small instances)")
     orc.add_argument("--slos", required=True)
     orc.add_argument("--profiles", required=True)
@@ -267,6 +314,10 @@ def main(argv=None) -> int:
             return cmd_lowerbound(a, manifest)
         if a.command == "oracle":
             return cmd_oracle(a, manifest)
+        if a.command == "baseline":
+            return cmd_baseline(a, manifest)
+        if a.command == "gen-workload":
+            return cmd_gen_workload(a, manifest)
         return cmd_enumerate(a, manifest)
     except mp.SchemaError as e:
         sys.stderr.write(f"error: {e}\n")

@@ -609,6 +609,65 @@ int mig_lower_bound(const mig_ctx* ctx, int32_t* out) {
     });
 }
 
+int mig_baseline(const mig_ctx* ctx, int32_t kind, mig_config* out, int32_t cap, int32_t* n_out) {
+    int rc = MIG_OK;
+    *n_out = 0;
+    int g = guarded([&] {  // bench.hpp:42-90
+        if (kind < 0 || kind > 2) throw ArgumentError("baseline kind must be 0 (7/7), 1 (7x1/7) or 2 (mix)");
+        const Model& m = ctx->e->model();
+        auto entry = [&](int i, int size) -> std::pair<int, double> {  // entry_or_throw, bench.hpp:26-31
+            const auto& prof = ctx->e->profiles().at(m.services[i].model);
+            const ProfileEntry* sel = nullptr;
+            auto it = prof.entries.find(size);
+            if (it != prof.entries.end())
+                for (const auto& pe : it->second)
+                    if (pe.p90 <= m.services[i].p90) sel = &pe;  // select_entry: largest feasible batch
+            if (!sel)
+                throw PlanningError("service '" + m.services[i].id + "' is infeasible on a " + std::to_string(size) +
+                                    "/7 instance under its latency ceiling");
+            return {sel->batch, sel->thr};
+        };
+        auto count = [](double need, double per) { return static_cast<int>(std::ceil(need / per - 1e-9)); };
+        std::vector<Config> plan;
+        auto one = [](std::initializer_list<Model::Inst> in) {
+            Config c;
+            c.n = 0;
+            for (const auto& x : in) c.inst[c.n++] = x;
+            return c;
+        };
+        if (kind == 0) {
+            for (int i = 0; i < m.n; ++i) {
+                auto [b, t] = entry(i, 7);
+                for (int k = count(m.services[i].req, t); k > 0; --k) plan.push_back(one({{7, 0, i, b}}));
+            }
+        } else if (kind == 1) {
+            Config cur;
+            cur.n = 0;
+            for (int i = 0; i < m.n; ++i) {
+                auto [b, t] = entry(i, 1);
+                for (int k = count(m.services[i].req, t); k > 0; --k) {
+                    cur.inst[cur.n] = Model::Inst{1, cur.n, i, b};
+                    if (++cur.n == 7) {
+                        plan.push_back(cur);
+                        cur.n = 0;
+                    }
+                }
+            }
+            if (cur.n) plan.push_back(cur);
+        } else {
+            for (int i = 0; i < m.n; ++i) {
+                auto [b4, t4] = entry(i, 4);
+                auto [b2, t2] = entry(i, 2);
+                auto [b1, t1] = entry(i, 1);
+                for (int k = count(m.services[i].req, t4 + t2 + t1); k > 0; --k)
+                    plan.push_back(one({{4, 0, i, b4}, {2, 4, i, b2}, {1, 6, i, b1}}));
+            }
+        }
+        rc = emit(plan, out, cap, n_out);
+    });
+    return g != MIG_OK ? g : rc;
+}
+
 int mig_brute_force_optimum(mig_ctx* ctx, int32_t cap, int64_t node_budget, mig_config* out, int32_t out_cap,
                             int32_t* n_out, int32_t* found) {
     int rc = MIG_OK;

@@ -35,6 +35,8 @@ const void* bf_warp_kernel_ptr();
 int bf_threads();
 const void* mcts_kernel_ptr();
 void mcts_read_topk_timers(unsigned long long* h);
+cudaError_t build_keyrank(const DevModel& M, const uint64_t* rows, long long P, unsigned* rank, cudaStream_t stream,
+                          int* launches);
 int mcts_threads();
 const void* rollout_kernel_ptr();
 int rollout_threads();
@@ -331,16 +333,13 @@ Engine::Engine(const Rules& rules, std::map<std::string, ModelProfile> profiles,
 
 const unsigned* Engine::keyrank() {
     std::call_once(keyrank_once_, [&] {
-        const size_t P = base_rows_.size();
-        std::vector<std::pair<std::array<uint64_t, 2>, unsigned>> k(P);
-        for (size_t i = 0; i < P; ++i) k[i] = {m_.key(base_rows_[i]), static_cast<unsigned>(i)};
-        std::sort(k.begin(), k.end());
-        std::vector<unsigned> rank(P);
-        for (size_t r = 0; r < P; ++r) rank[k[r].second] = static_cast<unsigned>(r);
+        const long long P = static_cast<long long>(base_rows_.size());
         CK(cudaSetDevice(device_));
-        CK(cudaMalloc(&d_keyrank_, sizeof(unsigned) * std::max<size_t>(P, 1)));
+        CK(cudaMalloc(&d_keyrank_, sizeof(unsigned) * std::max<long long>(P, 1)));
         dev_allocs_.push_back(d_keyrank_);
-        if (P) CK(cudaMemcpy(d_keyrank_, rank.data(), sizeof(unsigned) * P, cudaMemcpyHostToDevice));
+        int l = 0;
+        CK(build_keyrank(dm_, d_base_, P, d_keyrank_, nullptr, &l));
+        stats.launches += l;
     });
     return d_keyrank_;
 }
@@ -976,7 +975,8 @@ void Engine::greedy_batch(const double* d_comps, int count, long long cap_steps,
             }
         } rel{calls};
         // the SMs are split between the instances (each a complete fast_algo on its CTAs)
-        const int gpc = std::max(1, num_sms_ * greedy_blocks_per_sm_ / nb);
+        int gpc = std::max(1, num_sms_ * greedy_blocks_per_sm_ / nb);
+        if (const char* v = std::getenv("MIGPLAN_GREEDY_CTAS")) gpc = std::max(1, std::min(gpc, std::atoi(v)));
         std::unique_ptr<GreedyLaunch> L(new GreedyLaunch{});
         L->n_groups = nb;
         L->ctas_per_group = gpc;

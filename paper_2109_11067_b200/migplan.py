@@ -1046,6 +1046,22 @@ def lower_bound(services, profiles) -> int:  # bench.hpp:93-108 (host arithmetic
     return int(math.ceil(total / 7.0 - 1e-9))
 
 
+BASELINE_KINDS = {"7of7": 0, "7x1": 1, "mix": 2}  # A100-7/7, A100-7x1/7, A100-MIX (bench.hpp:13-22)
+BASELINE_NAMES = {0: "A100-7/7", 1: "A100-7x1/7", 2: "A100-MIX"}
+
+
+def baseline(kind, services, profiles, backend=None) -> Deployment:
+    """baseline(kind, services, profiles), bench.hpp:42-90 — static-partition deployments.
+    kind: 0/"7of7" whole GPUs, 1/"7x1" 1/7 instances packed seven per GPU, 2/"mix" 4+2+1."""
+    k = BASELINE_KINDS[kind] if isinstance(kind, str) else int(kind)
+    services = list(services)
+    if not services:
+        return make_deployment([])
+    ctx = PlanContext(services, profiles, PartitionRuleSet.defaults(), 1, backend)
+    plan = _run_plan(ctx, lambda out, cp, nout: ctx.backend.lib.mig_baseline(ctx._p, k, out, cp, C.byref(nout)))
+    return make_deployment(plan)
+
+
 def brute_force_optimum(services, profiles, rules, cap: int, node_budget: int = 20_000_000,
                         backend=None, device: int = 0) -> Deployment | None:
     """brute_force_optimum, bench.hpp:160-219 — the exhaustive minimum-GPU oracle for small

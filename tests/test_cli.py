@@ -120,3 +120,36 @@ def test_oracle_subcommand(impl, tmp_path, capsys):  # migplan.cpp:244-251, 382-
     assert json.load(open(out + ".manifest.json"))["command"] == "oracle"
     assert cli.main(base + ["--cap", "2"]) == 1  # "no deployment within 2 GPUs"
     assert "no deployment within 2 GPUs" in capsys.readouterr().err
+
+
+@pytest.mark.skipif(S.ref_backend() is None, reason="reference shim not built")
+def test_baseline_subcommand(impl, tmp_path, capsys):  # migplan.cpp:184-190, 294-309
+    ps = S.profiles()
+    out = str(tmp_path / "b.json")
+    base = ["baseline", "--slos", os.path.join(FIX, "slos_day.json"), "--profiles", os.path.join(FIX, "profiles.json"),
+            "-o", out, *backend_args(impl)]
+    assert cli.main(base[:1] + ["--kind", "7of7"] + base[1:]) == 0
+    sv = S.fixture_services("slos_day", ps)
+    gold = S.load_golden("baseline.json")["slos_day/0"]["outcome"]
+    plan = plan_of(out)
+    assert S.plan_key(plan) == gold
+    with open(out, "rb") as f:
+        assert f.read() == ref_json(plan, sv, ps)
+    assert cli.main(base[:1] + ["--kind", "7x1"] + base[1:]) == 1  # gpt2-medium infeasible on 1/7
+    assert "infeasible on a 1/7 instance" in capsys.readouterr().err
+    assert cli.main(base[:1] + ["--kind", "nope"] + base[1:]) == 2
+
+
+def test_gen_workload_subcommand(impl, tmp_path):  # migplan.cpp:200-213, 324-345
+    out = str(tmp_path / "w.json")
+    args = ["gen-workload", "--n", "12", "--seed", "77", "--mu", "6.5", "--profiles", os.path.join(FIX, "profiles.json"),
+            "-o", out, *backend_args(impl)]
+    assert cli.main(args) == 0
+    ps = S.profiles()
+    got = mp.load_services(out, ps)
+    want = mp.gen_workload(12, True, 6.5, 0.6, 100.0, 77, ps, backend=S.host_backend())
+    assert [(s.service_id, s.model_name, s.required_rps, s.max_p90_ms) for s in got] == \
+        [(s.service_id, s.model_name, cli.out_num(s.required_rps), cli.out_num(s.max_p90_ms)) for s in want]
+    j = json.load(open(out))
+    assert list(j) == ["services"] and list(j["services"][0]) == ["id", "max_p90_ms", "model", "required_rps"]
+    assert cli.main(args[:3] + args[5:]) == 2  # --seed is required
