@@ -99,6 +99,7 @@ constexpr int kMaxGroups = 8;  // instances per launch (param space: 8 x 368 B)
 struct GreedyLaunch {
     int n_groups;
     int ctas_per_group;
+    int cluster;  // each group is one thread-block cluster (<= 16 CTAs): DSMEM argmax, cluster barriers
     GreedyArgs g[kMaxGroups];
 };
 

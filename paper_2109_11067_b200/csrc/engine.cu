@@ -35,8 +35,10 @@ const void* bf_warp_kernel_ptr();
 int bf_threads();
 const void* mcts_kernel_ptr();
 void mcts_read_topk_timers(unsigned long long* h);
-cudaError_t build_keyrank(const DevModel& M, const uint64_t* rows, long long P, unsigned* rank, cudaStream_t stream,
-                          int* launches);
+void greedy_read_diag(unsigned long long* skew_ns, unsigned long long* release_ns);
+size_t keyrank_scratch_bytes(long long P);
+cudaError_t build_keyrank(const DevModel& M, const uint64_t* rows, long long P, unsigned* rank, void* scratch,
+                          size_t scratch_bytes, cudaStream_t stream, int* launches);
 int mcts_threads();
 const void* rollout_kernel_ptr();
 int rollout_threads();
@@ -188,7 +190,7 @@ Engine::Engine(const Rules& rules, std::map<std::string, ModelProfile> profiles,
     if (const char* e = std::getenv("MIGPLAN_RING")) ring_stages_ = std::max(0, std::min(8, std::atoi(e)));
     {
         const long long fixed = static_cast<long long>(greedy_smem_bytes(m_.n, m_.PP, 0, ring_stages_)) + 128;
-        long long room = static_cast<long long>(info.smem_optin) - 2048 - fixed;
+        long long room = static_cast<long long>(info.smem_optin) - info.greedy_static_smem - 256 - fixed;
         cache_units_ = static_cast<int>(std::max<long long>(0, room / 16) / T * T);
         if (const char* e = std::getenv("MIGPLAN_ROW_CACHE_UNITS"))
             cache_units_ = std::max(0, std::min(cache_units_, std::atoi(e) / T * T));
@@ -335,10 +337,12 @@ const unsigned* Engine::keyrank() {
     std::call_once(keyrank_once_, [&] {
         const long long P = static_cast<long long>(base_rows_.size());
         CK(cudaSetDevice(device_));
-        CK(cudaMalloc(&d_keyrank_, sizeof(unsigned) * std::max<long long>(P, 1)));
-        dev_allocs_.push_back(d_keyrank_);
+        keyrank_buf_ = std::make_unique<Scratch>(device_, sizeof(unsigned) * std::max<long long>(P, 1));
+        d_keyrank_ = static_cast<unsigned*>(keyrank_buf_->get());
         int l = 0;
-        CK(build_keyrank(dm_, d_base_, P, d_keyrank_, nullptr, &l));
+        const size_t need = keyrank_scratch_bytes(P);
+        Scratch tmp(device_, need);
+        CK(build_keyrank(dm_, d_base_, P, d_keyrank_, tmp.get(), need, nullptr, &l));
         stats.launches += l;
     });
     return d_keyrank_;
@@ -389,6 +393,7 @@ const DeviceInfo& device_info(int device) {
     // every kernel may use all the opt-in shared memory its static allocation leaves
     CK(cudaFuncSetAttribute(topk1_kernel_ptr(32), cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     CK(cudaFuncSetAttribute(mcts_kernel_ptr(), cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    CK(cudaFuncSetAttribute(greedy_kernel_ptr(), cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     for (const void* k : {greedy_kernel_ptr(), topk_kernel_ptr(), topk1_kernel_ptr(32), rollout_kernel_ptr(),
                           mcts_kernel_ptr()}) {
         cudaFuncAttributes fa{};
@@ -396,6 +401,7 @@ const DeviceInfo& device_info(int device) {
         CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 static_cast<int>(prop.sharedMemPerBlockOptin - fa.sharedSizeBytes)));
         if (k == mcts_kernel_ptr()) info.mcts_static_smem = static_cast<long long>(fa.sharedSizeBytes);
+        if (k == greedy_kernel_ptr()) info.greedy_static_smem = static_cast<long long>(fa.sharedSizeBytes);
     }
     return cache.emplace(device, info).first->second;
 }
@@ -419,6 +425,50 @@ SlotPool& slot_pool(int device) {
 }
 
 }  // namespace
+
+namespace {
+
+// Process-wide pool of device scratch buffers (per device, power-of-two size classes): the
+// per-call temporaries of the GA phases and the per-context key ranks never pay cudaMalloc /
+// cudaFree (a device-wide synchronization) inside a plan.
+struct ScratchPool {
+    std::mutex mu;
+    std::multimap<size_t, void*> free;
+};
+ScratchPool& scratch_pool(int device) {
+    static std::mutex m;
+    static std::map<int, ScratchPool*> pools;  // intentionally leaked: lives until process exit
+    std::lock_guard<std::mutex> g(m);
+    auto& p = pools[device];
+    if (!p) p = new ScratchPool;
+    return *p;
+}
+
+}  // namespace
+
+Scratch::Scratch(int device, size_t bytes) : device_(device) {
+    size_t cls = 4096;
+    while (cls < bytes) cls <<= 1;
+    bytes_ = cls;
+    ScratchPool& pool = scratch_pool(device);
+    {
+        std::lock_guard<std::mutex> g(pool.mu);
+        auto it = pool.free.lower_bound(cls);
+        if (it != pool.free.end() && it->first == cls) {
+            p_ = it->second;
+            pool.free.erase(it);
+            return;
+        }
+    }
+    CK(cudaMalloc(&p_, cls));
+}
+
+Scratch::~Scratch() {
+    if (!p_) return;
+    ScratchPool& pool = scratch_pool(device_);
+    std::lock_guard<std::mutex> g(pool.mu);
+    pool.free.emplace(bytes_, p_);
+}
 
 Slot* Engine::acquire() {
     SlotPool& pool = slot_pool(device_);
@@ -572,10 +622,67 @@ bool Engine::greedy_finish(GreedyCall& c, float ms, int attempt, std::vector<uin
     stats.ext_events += h.n_events;
     stats.ext_rows += static_cast<long long>(h.ext_count);
     for (int k = 0; k < 5; ++k) stats.phase_ns[k] += static_cast<long long>(h.phase_ns[k]);
+    if (std::getenv("MIGPLAN_PHASE_TIMERS")) {
+        unsigned long long sk = 0, rl = 0;
+        greedy_read_diag(&sk, &rl);
+        std::fprintf(stderr, "[greedy] cumulative arrival skew (last CTA - CTA 0) %.3f ms, reduce+release %.3f ms\n",
+                     sk * 1e-6, rl * 1e-6);
+    }
     if (h.status == kNoPositive)
         throw PlanningError("fast_algo: no config with positive score while services remain unsatisfied");
     return true;
 }
+// Greedy launch: cooperative (grid-wide barriers over every SM) or, for small working sets,
+// one thread-block cluster per instance (DSMEM argmax and cluster barriers: a step costs a
+// few microseconds instead of a grid-wide barrier over 148 CTAs).
+void launch_greedy(const GreedyLaunch& L, int T, size_t smem, cudaStream_t st) {
+    void* args[] = {const_cast<GreedyLaunch*>(&L)};
+    if (!L.cluster) {
+        CK(cudaLaunchCooperativeKernel(greedy_kernel_ptr(), L.n_groups * L.ctas_per_group, T, args, smem, st));
+        return;
+    }
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(L.n_groups * L.ctas_per_group);
+    cfg.blockDim = dim3(T);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = L.ctas_per_group;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    CK(cudaLaunchKernelExC(&cfg, greedy_kernel_ptr(), args));
+}
+
+// CTAs per instance in cluster mode (0: cooperative).  Cluster mode when the working set
+// stays small: the base pool plus the extension bound (bench.hpp-style closed form) under
+// kClusterRows; MIGPLAN_GREEDY_CLUSTER=0 disables it, =k forces k CTAs.
+int Engine::greedy_cluster_ctas(size_t smem) const {
+    if (n_ranks_ > 1) return 0;
+    constexpr long long kClusterRows = 256ll << 10;
+    int want = pool_size() + ext_bound_ <= kClusterRows ? 16 : 0;
+    if (const char* v = std::getenv("MIGPLAN_GREEDY_CLUSTER")) want = std::max(0, std::min(16, std::atoi(v)));
+    for (; want >= 2; want >>= 1) {  // the largest size the GPU can co-schedule
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3(want);
+        cfg.blockDim = dim3(kernel_threads());
+        cfg.dynamicSmemBytes = smem;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = want;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        int nc = 0;
+        if (cudaOccupancyMaxActiveClusters(&nc, greedy_kernel_ptr(), &cfg) == cudaSuccess && nc > 0) return want;
+        cudaGetLastError();
+    }
+    return 0;
+}
+
 
 // fast_algo on one engine, or on the ranks of a sharded greedy that share this GPU: their
 // instances run as CTA ranges of ONE cooperative launch (GreedyLaunch), so the per-step
@@ -617,20 +724,22 @@ void Engine::fast_algo_group(const std::vector<Engine*>& es, const std::vector<d
     int G = e0->num_sms_ * e0->greedy_blocks_per_sm_ / P;
     if (e0->max_ctas_ > 0) G = std::min(G, e0->max_ctas_);
     if (const char* v = std::getenv("MIGPLAN_GREEDY_CTAS")) G = std::max(1, std::min(G, std::atoi(v)));
+    const int GC = P == 1 ? e0->greedy_cluster_ctas(smem) : 0;
+    if (GC) G = GC;
     Slot* s0 = calls[0].s;
     for (int attempt = 0;; ++attempt) {
         GreedyLaunch L{};
         L.n_groups = P;
         L.ctas_per_group = G;
+        L.cluster = GC ? 1 : 0;
         const long long cap_steps = std::min<long long>(e0->step_bound(comp), 1 << 24);
         for (int r = 0; r < P; ++r) {
             es[r]->greedy_prepare(calls[r], comp.data(), nullptr, cap_steps);
             L.g[r] = calls[r].a;
         }
         for (int r = 1; r < P; ++r) CK(cudaStreamSynchronize(calls[r].s->stream));  // their arena copies
-        void* args[] = {&L};
         CK(cudaEventRecord(s0->e0, s0->stream));
-        CK(cudaLaunchCooperativeKernel(greedy_kernel_ptr(), G * P, T, args, smem, s0->stream));
+        launch_greedy(L, T, smem, s0->stream);
         for (Engine* e : es) e->stats.launches++;
         CK(cudaEventRecord(s0->e1, s0->stream));
         CK(cudaStreamSynchronize(s0->stream));
@@ -977,9 +1086,12 @@ void Engine::greedy_batch(const double* d_comps, int count, long long cap_steps,
         // the SMs are split between the instances (each a complete fast_algo on its CTAs)
         int gpc = std::max(1, num_sms_ * greedy_blocks_per_sm_ / nb);
         if (const char* v = std::getenv("MIGPLAN_GREEDY_CTAS")) gpc = std::max(1, std::min(gpc, std::atoi(v)));
+        const int GC = greedy_cluster_ctas(smem);
+        if (GC && GC * nb <= num_sms_) gpc = GC;
         std::unique_ptr<GreedyLaunch> L(new GreedyLaunch{});
         L->n_groups = nb;
         L->ctas_per_group = gpc;
+        L->cluster = GC && GC * nb <= num_sms_ ? 1 : 0;
         for (int i = 0; i < nb; ++i) {
             calls[i].e = this;
             calls[i].s = acquire();
@@ -988,9 +1100,8 @@ void Engine::greedy_batch(const double* d_comps, int count, long long cap_steps,
         }
         for (int i = 1; i < nb; ++i) CK(cudaStreamSynchronize(calls[i].s->stream));
         Slot* s0 = calls[0].s;
-        void* args[] = {L.get()};
         CK(cudaEventRecord(s0->e0, s0->stream));
-        CK(cudaLaunchCooperativeKernel(greedy_kernel_ptr(), nb * gpc, T, args, smem, s0->stream));
+        launch_greedy(*L, T, smem, s0->stream);
         stats.launches++;
         CK(cudaEventRecord(s0->e1, s0->stream));
         CK(cudaStreamSynchronize(s0->stream));
@@ -1261,12 +1372,8 @@ void Engine::fast_algo_batch(const std::vector<std::vector<double>>& comps, std:
     }
     std::vector<double> flat;
     for (const auto& c : comps) flat.insert(flat.end(), c.begin(), c.end());
-    double* d = nullptr;
-    CK(cudaMalloc(&d, sizeof(double) * flat.size()));
-    struct Free {
-        double* p;
-        ~Free() { cudaFree(p); }
-    } fr{d};
+    Scratch buf(device_, sizeof(double) * flat.size());
+    double* d = static_cast<double*>(buf.get());
     CK(cudaMemcpy(d, flat.data(), sizeof(double) * flat.size(), cudaMemcpyHostToDevice));
     stats.h2d += static_cast<long long>(sizeof(double) * flat.size());
     std::vector<const uint64_t*> drows;

@@ -44,6 +44,7 @@ struct DeviceInfo {
     int num_sms = 0;
     long long smem_optin = 0;
     long long mcts_static_smem = 0;  // static shared memory of mcts_kernel
+    long long greedy_static_smem = 0;  // static shared memory of greedy_kernel
 };
 const DeviceInfo& device_info(int device);
 
@@ -84,6 +85,21 @@ struct RolloutResult {
     long long completed = 0, capped = 0, failed = 0, steps = 0, keys = 0;
     int rounds = 0, launches = 0;
     double ms = 0.0;          // device time (CUDA events)
+};
+
+// A device buffer from the process-wide scratch pool (returned on destruction).
+class Scratch {
+  public:
+    Scratch(int device, size_t bytes);
+    ~Scratch();
+    Scratch(const Scratch&) = delete;
+    Scratch& operator=(const Scratch&) = delete;
+    void* get() const { return p_; }
+
+  private:
+    int device_ = 0;
+    size_t bytes_ = 0;
+    void* p_ = nullptr;
 };
 
 class Engine {
@@ -178,8 +194,10 @@ class Engine {
     // rank of every base row in the config order (core.hpp:174-200), for the device
     // top-Ks' last tie-break (built on first use)
     unsigned* d_keyrank_ = nullptr;
+    std::unique_ptr<Scratch> keyrank_buf_;
     std::once_flag keyrank_once_;
     const unsigned* keyrank();
+    int greedy_cluster_ctas(size_t smem) const;  // 0: cooperative launch
     std::vector<double> min_u_;  // smallest positive utility per service (step bound)
     long long ext_bound_ = 0;
     int cache_units_ = 0;  // greedy shared-memory row cache per CTA (16-byte units)

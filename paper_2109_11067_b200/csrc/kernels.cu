@@ -14,6 +14,8 @@
 // Bit-exactness: every floating add/multiply on the score path is an explicit
 // __dadd_rn/__dmul_rn (and the TU is built with -fmad=false), so no FMA contraction
 // changes the reference's FP64 bits (SURVEY §0 hazard 1).
+#include <cooperative_groups.h>
+
 #include "common.cuh"
 
 namespace mgb {
@@ -119,6 +121,34 @@ __device__ Best exchange_best(const DevModel& M, const GreedyArgs& a, Best x, un
     return g;
 }
 
+namespace cg = cooperative_groups;
+
+// The argmax of a cluster-mode group: every CTA publishes its block best in shared memory
+// (double-buffered by step parity), one cluster barrier, then every CTA reduces the G
+// records over DSMEM in the same order, so all agree on the winner.
+__device__ Best cluster_argmax(const DevModel& M, const Best& mine, Best* xch, int parity, Best* red, int G) {
+    cg::cluster_group cl = cg::this_cluster();
+    if (threadIdx.x == 0) xch[parity] = mine;
+    cl.sync();
+    if ((threadIdx.x >> 5) == 0) {
+        Best x = none();
+        for (int q = lane_id(); q < G; q += 32) {
+            const Best b = *cl.map_shared_rank(xch + parity, q);
+            if (better(M, b, x)) x = b;
+        }
+        x = warp_best(M, x);
+        if (lane_id() == 0) red[0] = x;
+    }
+    __syncthreads();
+    const Best r = red[0];
+    __syncthreads();
+    return r;
+}
+
+constexpr int kKeyMaxPP = 128;  // key tables on chip up to this many patterns
+constexpr int kKeyMaxLayouts = 32;  // == kMaxLayouts (model.hpp)
+__device__ unsigned long long g_dep[1024], g_cta_dur[1024];
+__device__ unsigned long long g_arrive0, g_arrive_last, g_skew_ns, g_release_ns;
 __device__ Best grid_argmax(const DevModel& M, const Best& mine, Best* partials, Best* winrec, unsigned* count,
                             unsigned* gen, int G, Best* red, const GreedyArgs& a, unsigned long long seq,
                             int* xstatus, int bi) {
@@ -134,6 +164,12 @@ __device__ Best grid_argmax(const DevModel& M, const Best& mine, Best* partials,
         const unsigned t = c.fetch_add(1u, cuda::memory_order_acq_rel);
         s_last = t == static_cast<unsigned>(G) - 1u;
         s_gen = my;
+        if (a.phase_timers) {  // diagnostics: arrival skew (last CTA vs CTA 0) and reduce+release
+            const unsigned long long now = globaltimer();
+            if (g_dep[blockIdx.x]) g_cta_dur[blockIdx.x] += now - g_dep[blockIdx.x];
+            if (bi == 0) g_arrive0 = now;
+            if (s_last) g_arrive_last = now;
+        }
     }
     __syncthreads();
     if (s_last) {
@@ -165,7 +201,15 @@ __device__ Best grid_argmax(const DevModel& M, const Best& mine, Best* partials,
         while (g.load(cuda::memory_order_acquire) == s_gen) __nanosleep(32);
         red[0] = Best{__ldcg(&winrec->s), __ldcg(&winrec->u),
                       __ldcg(reinterpret_cast<const unsigned long long*>(&winrec->row))};
+        if (a.phase_timers && bi == 0) {
+            const unsigned long long now = globaltimer();
+            const unsigned long long t0 = *reinterpret_cast<volatile unsigned long long*>(&g_arrive0);
+            const unsigned long long tl = *reinterpret_cast<volatile unsigned long long*>(&g_arrive_last);
+            if (tl >= t0) g_skew_ns += tl - t0;
+            if (now >= tl) g_release_ns += now - tl;
+        }
     }
+    if (a.phase_timers && threadIdx.x == 0) g_dep[blockIdx.x] = globaltimer();
     __syncthreads();
     const Best r = red[0];
     __syncthreads();
@@ -395,7 +439,21 @@ __global__ void __launch_bounds__(kThreads, 1) greedy_kernel(const __grid_consta
     const GreedyArgs& a = GL.g[grp];
     const int G = GL.ctas_per_group;
     const int bi = static_cast<int>(blockIdx.x) - grp * G;
-    const DevModel& M = a.M;
+    // the config-order key tables (row_key, reached on exact score + util_sum ties) on chip
+    __shared__ uint8_t k_patc[kKeyMaxPP * 5], k_layc[kKeyMaxLayouts * 5];
+    __shared__ int8_t k_lays[kKeyMaxLayouts * 5 * 7];
+    __shared__ int k_sizes[5];
+    DevModel M = a.M;
+    if (M.PP <= kKeyMaxPP && M.n_layouts <= kKeyMaxLayouts) {
+        for (int i = threadIdx.x; i < M.PP * 5; i += blockDim.x) k_patc[i] = a.M.pat_count[i];
+        for (int i = threadIdx.x; i < M.n_layouts * 5; i += blockDim.x) k_layc[i] = a.M.layout_count[i];
+        for (int i = threadIdx.x; i < M.n_layouts * 35; i += blockDim.x) k_lays[i] = a.M.layout_slots[i];
+        if (threadIdx.x < M.n_sizes) k_sizes[threadIdx.x] = a.M.sizes[threadIdx.x];
+        M.pat_count = k_patc;
+        M.layout_count = k_layc;
+        M.layout_slots = k_lays;
+        M.sizes = k_sizes;
+    }
     const int n = M.n, PP = M.PP;
     const int nW = (n + 1) * PP;
     const GreedySmem L = greedy_layout(n, PP, a.cache_units, a.ring_stages);
@@ -420,6 +478,7 @@ __global__ void __launch_bounds__(kThreads, 1) greedy_kernel(const __grid_consta
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __shared__ Best red[kWarps];
+    __shared__ Best xch[2];  // cluster mode: this CTA's block best, by step parity
     __shared__ uint64_t unsat[4];
     __shared__ int s_events, s_first_new, s_done, s_m, s_status;
     __shared__ long long s_rows;
@@ -578,7 +637,10 @@ __global__ void __launch_bounds__(kThreads, 1) greedy_kernel(const __grid_consta
     long long N = a.n_base;
     auto extend_and_sync = [&]() {
         extend_new(s_first_new, s_events);
-        grid_barrier(bc, bg, G);
+        if (GL.cluster)
+            cg::this_cluster().sync();  // release/acquire at cluster scope: the appended rows
+        else
+            grid_barrier(bc, bg, G);
         if (threadIdx.x == 0) {
             s_status = *reinterpret_cast<volatile int*>(&a.st->status);
             s_rows = a.n_base + static_cast<long long>(*reinterpret_cast<volatile unsigned long long*>(&a.st->ext_count));
@@ -703,7 +765,9 @@ __global__ void __launch_bounds__(kThreads, 1) greedy_kernel(const __grid_consta
         best = block_best(M, best, red);
         mark(0);
         last_seq = a.exch_seq0 + static_cast<unsigned long long>(step) + 1ull;
-        const Best win = grid_argmax(M, best, a.partials, a.partials + G, bc, bg, G, red, a, last_seq, &a.st->status, bi);
+        const Best win = GL.cluster ? cluster_argmax(M, best, xch, step & 1, red, G)
+                                    : grid_argmax(M, best, a.partials, a.partials + G, bc, bg, G, red, a, last_seq,
+                                                  &a.st->status, bi);
         mark(1);
         if (win.row == kNoRow) {
             const int xs = *reinterpret_cast<volatile int*>(&a.st->status);
@@ -834,5 +898,24 @@ const void* greedy_kernel_ptr() { return reinterpret_cast<const void*>(&greedy_k
 const void* topk_kernel_ptr() { return reinterpret_cast<const void*>(&topk_kernel); }
 const void* enum_base_kernel_ptr() { return reinterpret_cast<const void*>(&enum_base_kernel); }
 int kernel_threads() { return kThreads; }
+
+void greedy_read_diag(unsigned long long* skew_ns, unsigned long long* release_ns) {
+    cudaMemcpyFromSymbol(skew_ns, g_skew_ns, 8);
+    cudaMemcpyFromSymbol(release_ns, g_release_ns, 8);
+    static unsigned long long d[1024];
+    cudaMemcpyFromSymbol(d, g_cta_dur, sizeof d);
+    unsigned long long mn = ~0ull, mx = 0, sum = 0;
+    int cnt = 0, amx = 0, amn = 0;
+    for (int i = 0; i < 1024; ++i)
+        if (d[i]) {
+            if (d[i] > mx) mx = d[i], amx = i;
+            if (d[i] < mn) mn = d[i], amn = i;
+            sum += d[i];
+            ++cnt;
+        }
+    if (cnt)
+        fprintf(stderr, "[greedy] per-CTA scan total: min %.3f ms (cta %d) avg %.3f max %.3f ms (cta %d)\n", mn * 1e-6, amn,
+                sum * 1e-6 / cnt, mx * 1e-6, amx);
+}
 
 }  // namespace mgb

@@ -37,36 +37,40 @@ __global__ void keyrank_scatter_kernel(const unsigned* sorted_idx, long long P, 
 
 }  // namespace
 
-// rank[i] = position of rows[i] in the config order; returns the CUDA status.  Launches 3+
-// kernels on `stream` and synchronizes it.
-cudaError_t build_keyrank(const DevModel& M, const uint64_t* rows, long long P, unsigned* rank, cudaStream_t stream,
-                          int* launches) {
-    if (P <= 0) return cudaSuccess;
-    Key128 *kin = nullptr, *kout = nullptr;
-    unsigned *iin = nullptr, *iout = nullptr;
-    void* tmp = nullptr;
+// Scratch bytes build_keyrank needs for P rows (keys and indices double-buffered + the sort).
+size_t keyrank_scratch_bytes(long long P) {
+    if (P <= 0) return 256;
     size_t tmp_bytes = 0;
-    cudaError_t e = cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, kin, kout, iin, iout, P, Key128Decomposer{}, 0,
-                                                    128, stream);
-    if (e != cudaSuccess) return e;
+    Key128 *k = nullptr;
+    unsigned* i = nullptr;
+    cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, k, k, i, i, P, Key128Decomposer{}, 0, 128);
     const size_t kb = sizeof(Key128) * static_cast<size_t>(P), ib = sizeof(unsigned) * static_cast<size_t>(P);
-    unsigned char* mem = nullptr;
-    if ((e = cudaMalloc(&mem, 2 * kb + 2 * ib + tmp_bytes + 256)) != cudaSuccess) return e;
-    kin = reinterpret_cast<Key128*>(mem);
-    kout = reinterpret_cast<Key128*>(mem + kb);
-    iin = reinterpret_cast<unsigned*>(mem + 2 * kb);
-    iout = reinterpret_cast<unsigned*>(mem + 2 * kb + ib);
-    tmp = mem + ((2 * kb + 2 * ib + 255) & ~size_t(255));
+    return ((2 * kb + 2 * ib + 255) & ~size_t(255)) + tmp_bytes + 256;
+}
+
+// rank[i] = position of rows[i] in the config order; returns the CUDA status.  Launches the
+// key kernel, the radix sort and a scatter on `stream` and synchronizes it.
+cudaError_t build_keyrank(const DevModel& M, const uint64_t* rows, long long P, unsigned* rank, void* scratch,
+                          size_t scratch_bytes, cudaStream_t stream, int* launches) {
+    if (P <= 0) return cudaSuccess;
+    const size_t kb = sizeof(Key128) * static_cast<size_t>(P), ib = sizeof(unsigned) * static_cast<size_t>(P);
+    unsigned char* mem = static_cast<unsigned char*>(scratch);
+    Key128* kin = reinterpret_cast<Key128*>(mem);
+    Key128* kout = reinterpret_cast<Key128*>(mem + kb);
+    unsigned* iin = reinterpret_cast<unsigned*>(mem + 2 * kb);
+    unsigned* iout = reinterpret_cast<unsigned*>(mem + 2 * kb + ib);
+    void* tmp = mem + ((2 * kb + 2 * ib + 255) & ~size_t(255));
+    size_t tmp_bytes = scratch_bytes - ((2 * kb + 2 * ib + 255) & ~size_t(255));
     const unsigned grid = static_cast<unsigned>(std::min<long long>((P + 255) / 256, 4096));
     keyrank_keys_kernel<<<grid, 256, 0, stream>>>(M, rows, P, kin, iin);
-    e = cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, kin, kout, iin, iout, P, Key128Decomposer{}, 0, 128, stream);
+    cudaError_t e = cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, kin, kout, iin, iout, P, Key128Decomposer{}, 0,
+                                                    128, stream);
     if (e == cudaSuccess) {
         keyrank_scatter_kernel<<<grid, 256, 0, stream>>>(iout, P, rank);
         e = cudaStreamSynchronize(stream);
     }
     if (launches) *launches += 4;  // keys, the sort's passes (counted as 2), scatter
-    cudaError_t f = cudaFree(mem);
-    return e != cudaSuccess ? e : f;
+    return e;
 }
 
 }  // namespace mgb
