@@ -658,6 +658,7 @@ __global__ void __launch_bounds__(kThreads, 1) greedy_kernel(const __grid_consta
     int cj = 0;                                                  // units of mine cached so far
 
     int step = 0;
+    uint64_t prev_row = kNoRow;     // this thread's best row of the previous step
     unsigned long long kchunk = 0;  // TMA ring chunks consumed by this CTA (all steps)
     unsigned long long last_seq = a.exch_seq0;
     long long rows_total = 0;
@@ -686,7 +687,15 @@ __global__ void __launch_bounds__(kThreads, 1) greedy_kernel(const __grid_consta
             cache[cj * blockDim.x + threadIdx.x] = __ldcg(rows4 + my0 + cj * GT);
             ++cj;
         }
+        // Start from this thread's previous best row, re-scored: it is one of the thread's own
+        // rows (the working set only grows), so the argmax is unchanged, and its score is a
+        // high floor from the first row on (scores only fall as the completion rises), so the
+        // FP32 filter sends almost no row down the exact path.
         Best best = none();
+        if (prev_row != kNoRow) {
+            const double s0 = row_score(W, prev_row);
+            if (s0 > 0.0) best = Best{s0, row_usum(U, prev_row), prev_row};
+        }
         {
             int j = 0;
             for (; j + 3 < cj; j += 4) {
@@ -762,6 +771,7 @@ __global__ void __launch_bounds__(kThreads, 1) greedy_kernel(const __grid_consta
             for (; u < NU; u += GT) consider2(M, W, U, __ldcg(rows4 + u), best);
             if ((N & 1) && my0 == 0) consider(M, W, U, __ldcg(a.rows + N - 1), best);
         }
+        prev_row = best.row;
         best = block_best(M, best, red);
         mark(0);
         last_seq = a.exch_seq0 + static_cast<unsigned long long>(step) + 1ull;
