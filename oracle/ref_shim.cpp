@@ -26,6 +26,7 @@
 #include "migplan_b200.h"
 #ifdef MIGREF_WITH_IO
 #include "migplan/io.hpp"
+#include "migplan/transition_planner.hpp"
 #endif
 
 using namespace migplan;
@@ -842,6 +843,30 @@ int mig_ref_deployment_json(mig_ctx* ctx, const mig_config* cfgs, int32_t n, cha
         std::memcpy(buf, out.c_str(), out.size() + 1);
 #else
         (void)ctx, (void)cfgs, (void)n, (void)buf, (void)cap, (void)len;
+        throw std::invalid_argument("built without nlohmann/json (io.hpp)");
+#endif
+    });
+}
+
+/* The reference's transition planner (transition_planner.hpp:658-697) on deployment / SLO /
+ * profile FILES read by its own loaders (io.hpp:85-190): plan_to_json(plan).dump(2) + "\n".
+ * the planner must consume the product's plan output unchanged. */
+int mig_ref_plan_transition(const char* old_dep, const char* new_dep, const char* old_slos, const char* new_slos,
+                            const char* profiles, int32_t extra_budget, char* buf, int32_t cap, int32_t* len) {
+    return guarded([&] {
+#ifdef MIGREF_WITH_IO
+        ProfileStore ps = load_profiles(profiles);
+        auto os = load_services(old_slos, ps);
+        auto ns = load_services(new_slos, ps);
+        TransitionPlan plan = plan_transition(load_deployment(old_dep), load_deployment(new_dep), os, ns, ps,
+                                              PartitionRuleSet::defaults(), extra_budget);
+        std::string out = plan_to_json(plan).dump(2) + "\n";
+        *len = static_cast<int32_t>(out.size());
+        if (static_cast<int32_t>(out.size()) + 1 > cap) throw std::invalid_argument("output capacity too small");
+        std::memcpy(buf, out.c_str(), out.size() + 1);
+#else
+        (void)old_dep, (void)new_dep, (void)old_slos, (void)new_slos, (void)profiles, (void)extra_budget;
+        (void)buf, (void)cap, (void)len;
         throw std::invalid_argument("built without nlohmann/json (io.hpp)");
 #endif
     });

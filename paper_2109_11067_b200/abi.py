@@ -157,6 +157,8 @@ SIGNATURES = {
 # Exported by the reference shim only (bench.py reference arm, golden generation).
 REF_EXTRAS = {
     "mig_ref_count_rows": (_I, [_P, _DP, C.c_int32, _I64P]),
+    "mig_ref_plan_transition": (_I, [C.c_char_p, C.c_char_p, C.c_char_p, C.c_char_p, C.c_char_p, C.c_int32,
+                                     C.c_char_p, C.c_int32, _I32P]),
     "mig_ref_deployment_json": (_I, [_P, C.POINTER(ConfigC), C.c_int32, C.c_char_p, C.c_int32, _I32P]),
     "mig_ref_gen_workload": (_I, [C.POINTER(ModelProfileC), C.c_int32, C.c_int32, C.c_int32, C.c_double,
                                   C.c_double, C.c_double, C.c_uint64, _I32P, _DP]),

@@ -63,12 +63,64 @@ __device__ uint64_t mt_next(Mt64& g) {
 
 __device__ uint64_t mt_pick(Mt64& g, uint64_t n) {  // pick_index, util.hpp:39-47
     if (n <= 1) return 0;
+    if (n < (1ull << 16)) {  // the same arithmetic with 32-bit remainders (the search's n are small)
+        const unsigned m = static_cast<unsigned>(n);
+        const unsigned p32 = static_cast<unsigned>((1ull << 32) % m);            // 2^32 mod m
+        const unsigned rmax = ((0xFFFFFFFFu % m) * p32 + 0xFFFFFFFFu % m) % m;  // UINT64_MAX mod m
+        const uint64_t limit = ~0ull - rmax;
+        uint64_t r;
+        do {
+            r = mt_next(g);
+        } while (r >= limit);
+        const unsigned hi = static_cast<unsigned>(r >> 32), lo = static_cast<unsigned>(r);
+        return ((hi % m) * p32 + lo % m) % m;
+    }
     const uint64_t limit = ~0ull - (~0ull % n);
     uint64_t r;
     do {
         r = mt_next(g);
     } while (r >= limit);
     return r % n;
+}
+
+// The mt19937_64 twist of all 312 words by one warp (a generator that is exhausted, idx = 312):
+// the first 156 words read only old words, the rest read the first half's new words and, for
+// the last one, the new word 0 — the sequential loop's dependences, two read-then-write phases.
+__device__ void mt_twist_warp(Mt64& g) {
+    const int lane = static_cast<int>(threadIdx.x & 31u);
+    auto f = [&](int i) {
+        const uint64_t x = (g.mt[i] & 0xFFFFFFFF80000000ull) | (g.mt[(i + 1) % 312] & 0x7FFFFFFFull);
+        uint64_t xa = x >> 1;
+        if (x & 1ull) xa ^= 0xB5026F5AA96619E9ull;
+        return g.mt[(i + 156) % 312] ^ xa;
+    };
+    uint64_t v[5];
+#pragma unroll
+    for (int k = 0; k < 5; ++k) {
+        const int i = lane + 32 * k;
+        if (i < 156) v[k] = f(i);
+    }
+    __syncwarp();
+#pragma unroll
+    for (int k = 0; k < 5; ++k) {
+        const int i = lane + 32 * k;
+        if (i < 156) g.mt[i] = v[k];
+    }
+    __syncwarp();
+#pragma unroll
+    for (int k = 0; k < 5; ++k) {
+        const int i = 156 + lane + 32 * k;
+        if (i < 312) v[k] = f(i);
+    }
+    __syncwarp();
+#pragma unroll
+    for (int k = 0; k < 5; ++k) {
+        const int i = 156 + lane + 32 * k;
+        if (i < 312) g.mt[i] = v[k];
+    }
+    __syncwarp();
+    if (lane == 0) g.idx = 0;
+    __syncwarp();
 }
 
 // row touches a masked service: per-code flags built with the W table (4 byte lookups)
@@ -630,6 +682,7 @@ __global__ void __launch_bounds__(kMThreads, 1) mcts_kernel(const __grid_constan
     Cand* win = reinterpret_cast<Cand*>(carve(sizeof(Cand) * 2 * kMMaxK));  // [0,K) local, [K,2K) merged
     float* Wf = reinterpret_cast<float*>(carve(sizeof(float) * nW));
     unsigned char* hitc = carve(nW);
+    unsigned char* csvc = carve(nW);
     const int MN = a.max_nodes;
     double* nval = a.node_value;
     int *nvis = a.node_visits, *nfirst = a.node_first, *nnch = a.node_nch, *ncand = a.node_cand;
@@ -657,7 +710,10 @@ __global__ void __launch_bounds__(kMThreads, 1) mcts_kernel(const __grid_constan
     }
     const unsigned sent16 = static_cast<unsigned>(n * M.PP);
     const uint64_t hiS = static_cast<uint64_t>(sent16 | (sent16 << 16)) << 32;
-    for (int e = threadIdx.x; e < nW; e += blockDim.x) Us[e] = __ldg(&M.U[e]);
+    for (int e = threadIdx.x; e < nW; e += blockDim.x) {
+        Us[e] = __ldg(&M.U[e]);
+        csvc[e] = static_cast<unsigned char>(e / M.PP);  // service of a code (n for the sentinel row)
+    }
     __shared__ int s_exit, s_usemask, n_got, s_hits;
     __shared__ uint64_t s_mask[4];
     if (threadIdx.x == 0) {
@@ -905,7 +961,7 @@ __global__ void __launch_bounds__(kMThreads, 1) mcts_kernel(const __grid_constan
                         __syncwarp();
                         if (lane < 4) {  // members have distinct services: the adds commute
                             const int code = static_cast<int>((rowat(s_out[q]) >> (16 * lane)) & 0xFFFFull);
-                            const int svc = code / M.PP;
+                            const int svc = csvc[code];
                             if (svc < n) cc[svc] = __dadd_rn(cc[svc], Us[code]);
                         }
                         __syncwarp();
@@ -957,6 +1013,7 @@ __global__ void __launch_bounds__(kMThreads, 1) mcts_kernel(const __grid_constan
             for (;;) {
                 if (warp == 0) {
                     for (;;) {
+                        if (g.idx >= 312) mt_twist_warp(g);  // the serial twist in mt_next stays the fallback
                         uint64_t kw[4] = {0, 0, 0, 0};
                         for (int i0 = 0; i0 < n; i0 += 32) {
                             const int i = i0 + lane;
@@ -1043,7 +1100,7 @@ __global__ void __launch_bounds__(kMThreads, 1) mcts_kernel(const __grid_constan
                         idx = __shfl_sync(0xffffffffu, idx, 0);
                         if (lane < 4) {  // rollout add (mcts.hpp:139): distinct services, the adds commute
                             const int code = static_cast<int>((rowat(idx) >> (16 * lane)) & 0xFFFFull);
-                            const int svc = code / M.PP;
+                            const int svc = csvc[code];
                             if (svc < n) cur[svc] = __dadd_rn(cur[svc], Us[code]);
                         }
                         __syncwarp();
@@ -1143,6 +1200,7 @@ size_t mcts_smem_bytes(int n, int PP, int max_nodes, long long n_base, bool node
     carve(sizeof(Cand) * kMCandCap);
     carve(sizeof(Cand) * 2 * kMMaxK);
     carve(4 * nW);
+    carve(nW);
     carve(nW);
     if (node_smem) {
         carve(8 * static_cast<size_t>(max_nodes));
