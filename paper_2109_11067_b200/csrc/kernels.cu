@@ -175,10 +175,18 @@ __device__ Best grid_argmax(const DevModel& M, const Best& mine, Best* partials,
     if (s_last) {
         if ((threadIdx.x >> 5) == 0) {
             Best x = none();
-            for (int i = lane_id(); i < G; i += 32) {
-                Best p{__ldcg(&partials[i].s), __ldcg(&partials[i].u),
-                       __ldcg(reinterpret_cast<const unsigned long long*>(&partials[i].row))};
-                if (better(M, p, x)) x = p;
+            for (int i0 = 0; i0 < G; i0 += 128) {  // four independent partial loads in flight per lane
+                Best p[4];
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    const int i = i0 + 32 * k + static_cast<int>(lane_id());
+                    p[k] = i < G ? Best{__ldcg(&partials[i].s), __ldcg(&partials[i].u),
+                                        __ldcg(reinterpret_cast<const unsigned long long*>(&partials[i].row))}
+                                 : none();
+                }
+#pragma unroll
+                for (int k = 0; k < 4; ++k)
+                    if (better(M, p[k], x)) x = p[k];
             }
             x = warp_best(M, x);
             if (lane_id() == 0) {
