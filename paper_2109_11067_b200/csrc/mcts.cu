@@ -458,28 +458,46 @@ __device__ __noinline__ int block_topk_pair(const DevModel& M, const unsigned* k
     const uint4* base4 = reinterpret_cast<const uint4*>(base);  // 4 rows per 16 bytes
     const long long nq = nb >> 2;
     const long long B = blockDim.x;
-    float umax = 0.0f;
+    // the thread's two largest bounds with their rows, and its third largest bound: a thread
+    // whose third bound is below the threshold has at most these two candidate rows
+    float umax = 0.0f, u2 = 0.0f, u3 = 0.0f;
+    unsigned x1 = 0u, x2 = 0u;
+    long long p1 = -1, p2 = -1;
     int hits = 0;
-    auto bound1 = [&](unsigned x) {
+    auto bound1 = [&](unsigned x, long long pos) {
         float u = ub_pair(Wf, x);
         if (mask) {
             const bool h = hit_pair(hitc, x);
             hits += h;
             if (!h) u = 0.0f;
         }
-        umax = fmaxf(umax, u);
+        if (u > u3) {
+            if (u > u2) {
+                u3 = u2;
+                if (u > umax) {
+                    u2 = umax, x2 = x1, p2 = p1;
+                    umax = u, x1 = x, p1 = pos;
+                } else {
+                    u2 = u, x2 = x, p2 = pos;
+                }
+            } else {
+                u3 = u;
+            }
+        }
     };
     long long p = threadIdx.x;
     for (; p + B < nq; p += 2 * B) {
         const uint4 v0 = base4[p], v1 = base4[p + B];
-        bound1(v0.x), bound1(v0.y), bound1(v0.z), bound1(v0.w);
-        bound1(v1.x), bound1(v1.y), bound1(v1.z), bound1(v1.w);
+        const long long r0 = pos0 + 4 * p, r1 = pos0 + 4 * (p + B);
+        bound1(v0.x, r0), bound1(v0.y, r0 + 1), bound1(v0.z, r0 + 2), bound1(v0.w, r0 + 3);
+        bound1(v1.x, r1), bound1(v1.y, r1 + 1), bound1(v1.z, r1 + 2), bound1(v1.w, r1 + 3);
     }
     for (; p < nq; p += B) {
         const uint4 v = base4[p];
-        bound1(v.x), bound1(v.y), bound1(v.z), bound1(v.w);
+        const long long r0 = pos0 + 4 * p;
+        bound1(v.x, r0), bound1(v.y, r0 + 1), bound1(v.z, r0 + 2), bound1(v.w, r0 + 3);
     }
-    if (threadIdx.x < (nb & 3)) bound1(base[4 * nq + threadIdx.x]);
+    if (threadIdx.x < (nb & 3)) bound1(base[4 * nq + threadIdx.x], pos0 + 4 * nq + threadIdx.x);
     if (mask) {
         for (int off = 16; off > 0; off >>= 1) hits += __shfl_xor_sync(0xffffffffu, hits, off);
         if ((threadIdx.x & 31u) == 0) atomicAdd(&n_hit, hits);
@@ -539,44 +557,70 @@ __device__ __noinline__ int block_topk_pair(const DevModel& M, const unsigned* k
     };
     const unsigned sp = sent | (sent << 16);
     const uint4 padv = make_uint4(sp, sp, sp, sp);
-    const long long nq2 = (nq + 2 * B - 1) / (2 * B) * (2 * B);
-    for (long long p0 = threadIdx.x; p0 < nq2; p0 += 2 * B) {
-        const uint4 v0 = p0 < nq ? base4[p0] : padv;
-        const uint4 v1 = p0 + B < nq ? base4[p0 + B] : padv;
-        const unsigned x[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
-        float ub[8];
-        float mx = 0.0f;
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-            ub[j] = ub_pair(Wf, x[j]);
-            if (mask && !hit_pair(hitc, x[j])) ub[j] = 0.0f;
-            mx = fmaxf(mx, ub[j]);
-        }
-        if (!__any_sync(0xffffffffu, mx > 0.0f && mx >= LB_f)) continue;
-        double sc[8];
+    // lanes with a third bound reaching LB rescan all their rows; the others offer their two
+    // listed rows (exact scores only where a bound reaches LB)
+    const bool rescan = u3 > 0.0f && u3 >= LB_f;
+    {
+        unsigned xs[8] = {x1, x2, sp, sp, sp, sp, sp, sp};
+        double sc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
         unsigned tk = 0;
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-            sc[j] = 0.0;
-            if (ub[j] > 0.0f && ub[j] >= LB_f) {
-                sc[j] = __dadd_rn(W[x[j] & 0xFFFFu], W[x[j] >> 16]);
-                if (sc[j] > 0.0 && sc[j] >= LB) tk |= 1u << j;
+        if (!rescan) {
+            if (umax > 0.0f && umax >= LB_f) {
+                sc[0] = __dadd_rn(W[x1 & 0xFFFFu], W[x1 >> 16]);
+                if (sc[0] > 0.0 && sc[0] >= LB) tk |= 1u;
+            }
+            if (u2 > 0.0f && u2 >= LB_f) {
+                sc[1] = __dadd_rn(W[x2 & 0xFFFFu], W[x2 >> 16]);
+                if (sc[1] > 0.0 && sc[1] >= LB) tk |= 2u;
             }
         }
-        emit(x, sc, tk, pos0 + 4 * p0, pos0 + 4 * (p0 + B));
+        if (__any_sync(0xffffffffu, tk != 0)) {  // emit() numbers row j as r0 + j: one listed row per call
+            emit(xs, sc, tk & 1u, p1, 0);
+            unsigned xs2[8] = {x2, sp, sp, sp, sp, sp, sp, sp};
+            double sc2[8] = {sc[1], 0, 0, 0, 0, 0, 0, 0};
+            emit(xs2, sc2, (tk >> 1) & 1u, p2, 0);
+        }
     }
-    if (nb & 3) {  // the last rows, warp 0 (the scan needs the whole warp)
-        if ((threadIdx.x >> 5) == 0) {
-            const int t = static_cast<int>(threadIdx.x);
-            unsigned x[8] = {t < (nb & 3) ? base[4 * nq + t] : sp, sp, sp, sp, sp, sp, sp, sp};
-            double sc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-            unsigned tk = 0;
-            const float ub = ub_pair(Wf, x[0]);
-            if (ub > 0.0f && ub >= LB_f && (!mask || hit_pair(hitc, x[0]))) {
-                sc[0] = __dadd_rn(W[x[0] & 0xFFFFu], W[x[0] >> 16]);
-                if (sc[0] > 0.0 && sc[0] >= LB) tk = 1u;
+    if (__any_sync(0xffffffffu, rescan)) {
+        const long long nq2 = (nq + 2 * B - 1) / (2 * B) * (2 * B);
+        for (long long p0 = threadIdx.x; p0 < nq2; p0 += 2 * B) {
+            const uint4 v0 = rescan && p0 < nq ? base4[p0] : padv;
+            const uint4 v1 = rescan && p0 + B < nq ? base4[p0 + B] : padv;
+            const unsigned x[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
+            float ub[8];
+            float mx = 0.0f;
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                ub[j] = ub_pair(Wf, x[j]);
+                if (mask && !hit_pair(hitc, x[j])) ub[j] = 0.0f;
+                mx = fmaxf(mx, ub[j]);
             }
-            emit(x, sc, tk, pos0 + 4 * nq + t, 0);
+            if (!__any_sync(0xffffffffu, mx > 0.0f && mx >= LB_f)) continue;
+            double sc[8];
+            unsigned tk = 0;
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                sc[j] = 0.0;
+                if (ub[j] > 0.0f && ub[j] >= LB_f) {
+                    sc[j] = __dadd_rn(W[x[j] & 0xFFFFu], W[x[j] >> 16]);
+                    if (sc[j] > 0.0 && sc[j] >= LB) tk |= 1u << j;
+                }
+            }
+            emit(x, sc, tk, pos0 + 4 * p0, pos0 + 4 * (p0 + B));
+        }
+        if (nb & 3) {  // the last rows, warp 0 (the scan needs the whole warp)
+            if ((threadIdx.x >> 5) == 0) {
+                const int t = static_cast<int>(threadIdx.x);
+                unsigned x[8] = {rescan && t < (nb & 3) ? base[4 * nq + t] : sp, sp, sp, sp, sp, sp, sp, sp};
+                double sc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+                unsigned tk = 0;
+                const float ub = ub_pair(Wf, x[0]);
+                if (ub > 0.0f && ub >= LB_f && (!mask || hit_pair(hitc, x[0]))) {
+                    sc[0] = __dadd_rn(W[x[0] & 0xFFFFu], W[x[0] >> 16]);
+                    if (sc[0] > 0.0 && sc[0] >= LB) tk = 1u;
+                }
+                emit(x, sc, tk, pos0 + 4 * nq + t, 0);
+            }
         }
     }
     __syncthreads();
