@@ -43,7 +43,7 @@ struct GreedyState {
     int n_steps;
     unsigned long long ext_count;
     int n_events;
-    int pad;
+    unsigned int arrive;  // all-reduce argmax: arrivals so far (step s completes at (s + 1) * G)
     long long rows_scored;
     // CTA-0 %globaltimer phase totals (ns): 0 build W + scan + block reduce, 1 grid barrier,
     // 2 grid reduce + completion update, 3 maybe_extend, 4 extension enumeration + barrier

@@ -145,6 +145,47 @@ __device__ Best cluster_argmax(const DevModel& M, const Best& mine, Best* xch, i
     return r;
 }
 
+// Argmax of a single-rank cooperative group without a reducing CTA: every CTA posts its
+// block best (double-buffered by step parity), counts itself in, waits until all G CTAs of
+// this step have arrived, then reduces the G records itself in the same order — one L2
+// round trip less than "last CTA reduces, everyone reads its record".
+__device__ Best grid_allreduce_argmax(const DevModel& M, const Best& mine, Best* partials, unsigned* arrive, int G,
+                                      int step, Best* red, int bi) {
+    Best* part = partials + (step & 1) * G;
+    if (threadIdx.x == 0) {
+        __stcg(&part[bi].s, mine.s);
+        __stcg(&part[bi].u, mine.u);
+        __stcg(reinterpret_cast<unsigned long long*>(&part[bi].row), static_cast<unsigned long long>(mine.row));
+        cuda::atomic_ref<unsigned, cuda::thread_scope_device> c(*arrive);
+        c.fetch_add(1u, cuda::memory_order_release);
+        const unsigned target = static_cast<unsigned>(step + 1) * static_cast<unsigned>(G);
+        while (c.load(cuda::memory_order_acquire) < target) __nanosleep(16);
+    }
+    __syncthreads();
+    if ((threadIdx.x >> 5) == 0) {
+        Best x = none();
+        for (int i0 = 0; i0 < G; i0 += 128) {
+            Best p[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const int i = i0 + 32 * k + static_cast<int>(lane_id());
+                p[k] = i < G ? Best{__ldcg(&part[i].s), __ldcg(&part[i].u),
+                                    __ldcg(reinterpret_cast<const unsigned long long*>(&part[i].row))}
+                             : none();
+            }
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+                if (better(M, p[k], x)) x = p[k];
+        }
+        x = warp_best(M, x);
+        if (lane_id() == 0) red[0] = x;
+    }
+    __syncthreads();
+    const Best r = red[0];
+    __syncthreads();
+    return r;
+}
+
 constexpr int kKeyMaxPP = 128;  // key tables on chip up to this many patterns
 constexpr int kKeyMaxLayouts = 32;  // == kMaxLayouts (model.hpp)
 __device__ unsigned long long g_dep[1024], g_cta_dur[1024];
@@ -447,21 +488,7 @@ __global__ void __launch_bounds__(kThreads, 1) greedy_kernel(const __grid_consta
     const GreedyArgs& a = GL.g[grp];
     const int G = GL.ctas_per_group;
     const int bi = static_cast<int>(blockIdx.x) - grp * G;
-    // the config-order key tables (row_key, reached on exact score + util_sum ties) on chip
-    __shared__ uint8_t k_patc[kKeyMaxPP * 5], k_layc[kKeyMaxLayouts * 5];
-    __shared__ int8_t k_lays[kKeyMaxLayouts * 5 * 7];
-    __shared__ int k_sizes[5];
-    DevModel M = a.M;
-    if (M.PP <= kKeyMaxPP && M.n_layouts <= kKeyMaxLayouts) {
-        for (int i = threadIdx.x; i < M.PP * 5; i += blockDim.x) k_patc[i] = a.M.pat_count[i];
-        for (int i = threadIdx.x; i < M.n_layouts * 5; i += blockDim.x) k_layc[i] = a.M.layout_count[i];
-        for (int i = threadIdx.x; i < M.n_layouts * 35; i += blockDim.x) k_lays[i] = a.M.layout_slots[i];
-        if (threadIdx.x < M.n_sizes) k_sizes[threadIdx.x] = a.M.sizes[threadIdx.x];
-        M.pat_count = k_patc;
-        M.layout_count = k_layc;
-        M.layout_slots = k_lays;
-        M.sizes = k_sizes;
-    }
+    const DevModel& M = a.M;
     const int n = M.n, PP = M.PP;
     const int nW = (n + 1) * PP;
     const GreedySmem L = greedy_layout(n, PP, a.cache_units, a.ring_stages);
@@ -780,12 +807,14 @@ __global__ void __launch_bounds__(kThreads, 1) greedy_kernel(const __grid_consta
             if ((N & 1) && my0 == 0) consider(M, W, U, __ldcg(a.rows + N - 1), best);
         }
         prev_row = best.row;
-        best = block_best(M, best, red);
+        const Best bb = block_best(M, best, red);
         mark(0);
         last_seq = a.exch_seq0 + static_cast<unsigned long long>(step) + 1ull;
-        const Best win = GL.cluster ? cluster_argmax(M, best, xch, step & 1, red, G)
-                                    : grid_argmax(M, best, a.partials, a.partials + G, bc, bg, G, red, a, last_seq,
-                                                  &a.st->status, bi);
+        const Best win = GL.cluster               ? cluster_argmax(M, bb, xch, step & 1, red, G)
+                         : a.n_ranks == 1
+                             ? grid_allreduce_argmax(M, bb, a.partials, &a.st->arrive, G, step, red, bi)
+                             : grid_argmax(M, bb, a.partials, a.partials + G, bc, bg, G, red, a, last_seq,
+                                           &a.st->status, bi);
         mark(1);
         if (win.row == kNoRow) {
             const int xs = *reinterpret_cast<volatile int*>(&a.st->status);

@@ -423,8 +423,21 @@ namespace {
 //   device  the mcts_solve search loops                            (grouped mcts_kernel)
 //   device  fast_algo completions of the visit-count descents      (grouped greedy)
 //   host    answer precedence (mcts.hpp:245-251), evaluate_chromosome; PlanningError -> parent
+// MIGPLAN_GA_TIMERS=1: host-side timeline of the parity GA (phase durations to stderr).
+struct Timeline {
+    bool on = std::getenv("MIGPLAN_GA_TIMERS") != nullptr;
+    std::chrono::steady_clock::time_point t = std::chrono::steady_clock::now();
+    void mark(const char* what) {
+        if (!on) return;
+        const auto now = std::chrono::steady_clock::now();
+        std::fprintf(stderr, "[ga] %-28s %8.3f ms\n", what, std::chrono::duration<double, std::milli>(now - t).count());
+        t = now;
+    }
+};
+
 std::vector<Chromosome> breed_round(Engine& e, const std::vector<Chromosome>& pop, size_t n_parents, int round,
                                     const GaParams& p) {
+    Timeline tl;
     struct Child {
         Chromosome c;  // the mutated parent (crossover's fallback)
         std::vector<Config> survivors, fast_ref, refill;
@@ -466,6 +479,7 @@ std::vector<Chromosome> breed_round(Engine& e, const std::vector<Chromosome>& po
         x.seed = rng();  // MctsProcedure::solve: mcts_solve(comp, ctx, params, rng()) (mcts.hpp:258)
         if (satisfied(x.residual)) x.no_refill = true;  // mcts_solve returns {} (mcts.hpp:151)
     }
+    tl.mark("mutate+erase (host)");
     // fast_ref for every child still searching
     std::vector<size_t> live;
     std::vector<std::vector<double>> comps;
@@ -477,6 +491,7 @@ std::vector<Chromosome> breed_round(Engine& e, const std::vector<Chromosome>& po
     std::vector<std::vector<uint64_t>> rows;
     std::vector<int> st;
     e.fast_algo_batch(comps, rows, st);
+    tl.mark("fast_ref batch");
     std::vector<size_t> search;
     for (size_t q = 0; q < live.size(); ++q) {
         Child& x = ch[live[q]];
@@ -498,8 +513,10 @@ std::vector<Chromosome> breed_round(Engine& e, const std::vector<Chromosome>& po
             seeds.push_back(ch[i].seed);
             lrefs.push_back(static_cast<int>(ch[i].fast_ref.size()));
         }
+        tl.mark("configs (host)");
         auto res = e.mcts_device_group(sc, p.slow.budget_iters, p.slow.topk, p.slow.pick_services, p.slow.ucb_c, seeds,
                                        lrefs);
+        tl.mark("mcts group");
         for (size_t q = 0; q < search.size(); ++q) {
             if (res[q].status == 1) {
                 fail(ch[search[q]]);  // rollout: empty pool -> PlanningError
@@ -520,6 +537,7 @@ std::vector<Chromosome> breed_round(Engine& e, const std::vector<Chromosome>& po
     std::vector<std::vector<uint64_t>> drows;
     std::vector<int> dst;
     e.fast_algo_batch(dc, drows, dst);
+    tl.mark("descent batch");
     std::vector<std::vector<Config>> tail(n_parents);
     for (size_t q = 0; q < desc.size(); ++q) {
         if (dst[q]) {
@@ -542,6 +560,7 @@ std::vector<Chromosome> breed_round(Engine& e, const std::vector<Chromosome>& po
         }
         x.refill = std::move(answer);
     }
+    tl.mark("answers (host)");
     std::vector<Chromosome> out(n_parents);
     for (size_t i = 0; i < n_parents; ++i) {
         Child& x = ch[i];
@@ -557,6 +576,7 @@ std::vector<Chromosome> breed_round(Engine& e, const std::vector<Chromosome>& po
             out[i] = x.c;
         }
     }
+    tl.mark("evaluate (host)");
     return out;
 }
 
@@ -567,11 +587,14 @@ std::vector<Config> two_phase(Engine& e, const GaParams& p,
                               const std::function<void(int, int, double, bool, double)>& log) {
     auto t0 = std::chrono::steady_clock::now();
     auto elapsed = [&] { return std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count(); };
+    Timeline tl;
     std::vector<Config> seed_cfg = fast_plan(e, std::vector<double>(e.n(), 0.0));
+    tl.mark("seed fast_algo");
     if (p.time_budget_s <= 0.0 || p.max_rounds <= 0) return sorted_deployment(std::move(seed_cfg));
 
     std::vector<Chromosome> pop;
     pop.push_back(evaluate_chromosome(std::move(seed_cfg), e));
+    tl.mark("seed evaluate");
     Chromosome best = pop[0];
     MctsProc slow(p.slow);
     int stall = 0;
