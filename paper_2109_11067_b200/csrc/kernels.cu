@@ -559,6 +559,7 @@ __global__ void __launch_bounds__(kThreads, 1) greedy_kernel(const __grid_consta
                 }
                 ev += __popc(b);
             }
+            __syncwarp();  // every lane has read s_events / unsat before lane 0 rewrites them
             if (lane_id() == 0) {
                 for (int w = 0; w < 4; ++w) unsat[w] = um[w];
                 s_first_new = first;
@@ -851,6 +852,7 @@ __global__ void __launch_bounds__(kThreads, 1) greedy_kernel(const __grid_consta
         if (s_events > s_first_new) extend_and_sync();
     }
     mark(4);
+    if (GL.cluster) cg::this_cluster().sync();  // peers may still read this CTA's xch over DSMEM
     if (bi == 0) {  // one coalesced copy of the plan to host-mapped memory
         for (int i = threadIdx.x; i < step; i += blockDim.x) {
             a.host_pick_row[i] = a.pick_row[i];
