@@ -656,6 +656,16 @@ void launch_greedy(const GreedyLaunch& L, int T, size_t smem, cudaStream_t st) {
     CK(cudaLaunchKernelExC(&cfg, greedy_kernel_ptr(), args));
 }
 
+// Deal 32-unit blocks round-robin over the G CTAs instead of 512 contiguous units per CTA
+// (MIGPLAN_INTERLEAVE=1, only when the working-set bound fits the G row caches).  Measured
+// neutral at n = 24 (the per-step CTA skew is not a row-distribution effect), so off.
+int Engine::greedy_interleave(int G) const {
+    const char* v = std::getenv("MIGPLAN_INTERLEAVE");
+    if (!v || std::atoi(v) == 0) return 0;
+    const long long cap_rows = 2ll * cache_units_ * G;
+    return n_ranks_ == 1 && ring_stages_ == 0 && pool_size() + ext_bound_ <= cap_rows ? 1 : 0;
+}
+
 // CTAs per instance in cluster mode (0: cooperative).  Cluster mode when the working set
 // stays small: the base pool plus the extension bound (bench.hpp-style closed form) under
 // kClusterRows; MIGPLAN_GREEDY_CLUSTER=0 disables it, =k forces k CTAs.
@@ -735,6 +745,7 @@ void Engine::fast_algo_group(const std::vector<Engine*>& es, const std::vector<d
         const long long cap_steps = std::min<long long>(e0->step_bound(comp), 1 << 24);
         for (int r = 0; r < P; ++r) {
             es[r]->greedy_prepare(calls[r], comp.data(), nullptr, cap_steps);
+            calls[r].a.interleave = es[r]->greedy_interleave(G);
             L.g[r] = calls[r].a;
         }
         for (int r = 1; r < P; ++r) CK(cudaStreamSynchronize(calls[r].s->stream));  // their arena copies
@@ -1096,6 +1107,7 @@ void Engine::greedy_batch(const double* d_comps, int count, long long cap_steps,
             calls[i].e = this;
             calls[i].s = acquire();
             greedy_prepare(calls[i], nullptr, d_comps + static_cast<size_t>(b0 + i) * m_.n, cap_steps);
+            calls[i].a.interleave = greedy_interleave(gpc);
             L->g[i] = calls[i].a;
         }
         for (int i = 1; i < nb; ++i) CK(cudaStreamSynchronize(calls[i].s->stream));

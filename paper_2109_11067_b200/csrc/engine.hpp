@@ -198,6 +198,7 @@ class Engine {
     std::once_flag keyrank_once_;
     const unsigned* keyrank();
     int greedy_cluster_ctas(size_t smem) const;  // 0: cooperative launch
+    int greedy_interleave(int G) const;
     std::vector<double> min_u_;  // smallest positive utility per service (step bound)
     long long ext_bound_ = 0;
     int cache_units_ = 0;  // greedy shared-memory row cache per CTA (16-byte units)

@@ -188,7 +188,7 @@ __device__ Best grid_allreduce_argmax(const DevModel& M, const Best& mine, Best*
 
 constexpr int kKeyMaxPP = 128;  // key tables on chip up to this many patterns
 constexpr int kKeyMaxLayouts = 32;  // == kMaxLayouts (model.hpp)
-__device__ unsigned long long g_dep[1024], g_cta_dur[1024];
+__device__ unsigned long long g_dep[1024], g_cta_dur[1024], g_scan[1024], g_post[1024];
 __device__ unsigned long long g_arrive0, g_arrive_last, g_skew_ns, g_release_ns;
 __device__ Best grid_argmax(const DevModel& M, const Best& mine, Best* partials, Best* winrec, unsigned* count,
                             unsigned* gen, int G, Best* red, const GreedyArgs& a, unsigned long long seq,
@@ -689,11 +689,18 @@ __global__ void __launch_bounds__(kThreads, 1) greedy_kernel(const __grid_consta
 
     const uint4* rows4 = reinterpret_cast<const uint4*>(a.rows);
     const long long GT = static_cast<long long>(G) * blockDim.x;
-    const long long my0 = static_cast<long long>(bi) * blockDim.x + threadIdx.x;
+    // The thread's first unit; its units are my0 + k * GT.  Streaming scans give each CTA 512
+    // contiguous units per stride (the bulk L2 prefetch fetches them); when the whole working
+    // set lives in the row caches, 32-unit blocks are dealt round-robin over the CTAs instead,
+    // so every CTA holds a slice of each pool region (base rows, each extension event) and the
+    // per-step scan work is balanced.
+    const long long my0 = a.interleave ? (static_cast<long long>(threadIdx.x >> 5) * G + bi) * 32 + (threadIdx.x & 31)
+                                       : static_cast<long long>(bi) * blockDim.x + threadIdx.x;
     const int J = a.cache_units / static_cast<int>(blockDim.x);  // cached units per thread
     int cj = 0;                                                  // units of mine cached so far
 
     int step = 0;
+    unsigned long long t_win = 0;   // diagnostics (phase timers)
     uint64_t prev_row = kNoRow;     // this thread's best row of the previous step
     unsigned long long kchunk = 0;  // TMA ring chunks consumed by this CTA (all steps)
     unsigned long long last_seq = a.exch_seq0;
@@ -718,6 +725,11 @@ __global__ void __launch_bounds__(kThreads, 1) greedy_kernel(const __grid_consta
             break;
         }
         mark(4);
+        unsigned long long t_scan0 = 0;
+        if (a.phase_timers && threadIdx.x == 0) {  // diagnostics: per-CTA scan and post-argmax time
+            t_scan0 = globaltimer();
+            if (t_win) g_post[blockIdx.x] += t_scan0 - t_win;
+        }
         const long long NU = N >> 1;  // complete 16-byte units
         while (cj < J && my0 + cj * GT < NU) {  // pull newly complete units of mine on-chip
             cache[cj * blockDim.x + threadIdx.x] = __ldcg(rows4 + my0 + cj * GT);
@@ -809,6 +821,7 @@ __global__ void __launch_bounds__(kThreads, 1) greedy_kernel(const __grid_consta
         }
         prev_row = best.row;
         const Best bb = block_best(M, best, red);
+        if (a.phase_timers && threadIdx.x == 0) g_scan[blockIdx.x] += globaltimer() - t_scan0;
         mark(0);
         last_seq = a.exch_seq0 + static_cast<unsigned long long>(step) + 1ull;
         const Best win = GL.cluster               ? cluster_argmax(M, bb, xch, step & 1, red, G)
@@ -817,6 +830,7 @@ __global__ void __launch_bounds__(kThreads, 1) greedy_kernel(const __grid_consta
                              : grid_argmax(M, bb, a.partials, a.partials + G, bc, bg, G, red, a, last_seq,
                                            &a.st->status, bi);
         mark(1);
+        if (a.phase_timers && threadIdx.x == 0) t_win = globaltimer();
         if (win.row == kNoRow) {
             const int xs = *reinterpret_cast<volatile int*>(&a.st->status);
             status = xs != kOk ? xs : kNoPositive;
@@ -952,6 +966,21 @@ void greedy_read_diag(unsigned long long* skew_ns, unsigned long long* release_n
     cudaMemcpyFromSymbol(skew_ns, g_skew_ns, 8);
     cudaMemcpyFromSymbol(release_ns, g_release_ns, 8);
     static unsigned long long d[1024];
+    for (int which = 0; which < 2; ++which) {
+        cudaMemcpyFromSymbol(d, which ? g_post : g_scan, sizeof d);
+        unsigned long long mn = ~0ull, mx = 0, sum = 0;
+        int cnt = 0, amx = 0, amn = 0;
+        for (int i = 0; i < 1024; ++i)
+            if (d[i]) {
+                if (d[i] > mx) mx = d[i], amx = i;
+                if (d[i] < mn) mn = d[i], amn = i;
+                sum += d[i];
+                ++cnt;
+            }
+        if (cnt)
+            fprintf(stderr, "[greedy] per-CTA %s total: min %.3f ms (cta %d) avg %.3f max %.3f ms (cta %d)\n",
+                    which ? "post-argmax" : "scan", mn * 1e-6, amn, sum * 1e-6 / cnt, mx * 1e-6, amx);
+    }
     cudaMemcpyFromSymbol(d, g_cta_dur, sizeof d);
     unsigned long long mn = ~0ull, mx = 0, sum = 0;
     int cnt = 0, amx = 0, amn = 0;
