@@ -40,7 +40,7 @@ size_t keyrank_scratch_bytes(long long P);
 cudaError_t build_keyrank(const DevModel& M, const uint64_t* rows, long long P, unsigned* rank, void* scratch,
                           size_t scratch_bytes, cudaStream_t stream, int* launches);
 int mcts_threads();
-const void* rollout_kernel_ptr();
+const void* rollout_kernel_ptr(int n);
 int rollout_threads();
 
 namespace {
@@ -198,7 +198,7 @@ Engine::Engine(const Rules& rules, std::map<std::string, ModelProfile> profiles,
     const size_t gsm = greedy_smem_bytes(m_.n, m_.PP, cache_units_, ring_stages_), tsm = topk_smem_bytes(m_.n, m_.PP);
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&greedy_blocks_per_sm_, greedy_kernel_ptr(), T, gsm));
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&topk_blocks_per_sm_, topk_kernel_ptr(), T, tsm));
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&rollout_blocks_per_sm_, rollout_kernel_ptr(), rollout_threads(),
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&rollout_blocks_per_sm_, rollout_kernel_ptr(m_.n), rollout_threads(),
                                                      rollout_smem_bytes(m_.n, m_.PP)));
     if (greedy_blocks_per_sm_ < 1 || topk_blocks_per_sm_ < 1 || rollout_blocks_per_sm_ < 1)
         throw DeviceError("kernel does not fit on an SM");
@@ -394,7 +394,7 @@ const DeviceInfo& device_info(int device) {
     CK(cudaFuncSetAttribute(topk1_kernel_ptr(32), cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     CK(cudaFuncSetAttribute(mcts_kernel_ptr(), cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     CK(cudaFuncSetAttribute(greedy_kernel_ptr(), cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-    for (const void* k : {greedy_kernel_ptr(), topk_kernel_ptr(), topk1_kernel_ptr(32), rollout_kernel_ptr(),
+    for (const void* k : {greedy_kernel_ptr(), topk_kernel_ptr(), topk1_kernel_ptr(32), rollout_kernel_ptr(1), rollout_kernel_ptr(256),
                           mcts_kernel_ptr()}) {
         cudaFuncAttributes fa{};
         CK(cudaFuncGetAttributes(&fa, k));
@@ -1018,7 +1018,7 @@ RolloutResult Engine::rollouts(const std::vector<double>& comp, long long n_roll
             CK(cudaMemsetAsync(&a.cnt->best, 0xFF, sizeof(unsigned long long), st));
             void* args[] = {&a};
             CK(cudaEventRecord(e0, st));
-            CK(cudaLaunchCooperativeKernel(rollout_kernel_ptr(), G, rollout_threads(), args, smem, st));
+            CK(cudaLaunchCooperativeKernel(rollout_kernel_ptr(m_.n), G, rollout_threads(), args, smem, st));
             CK(cudaEventRecord(e1, st));
             stats.launches++;
             r.launches++;

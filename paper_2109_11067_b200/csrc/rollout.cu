@@ -34,7 +34,7 @@ constexpr int kRThreads = 512;
 constexpr int kRWarps = kRThreads / 32;
 constexpr int kRCandCap = 2048;
 constexpr int kRMaxK = 32;
-constexpr int kMaxJ = 8;  // comp registers per lane: n <= 256
+constexpr int kMaxJ = 8;  // comp registers per lane: n <= 256 (J = 2 instantiation for n <= 64)
 
 __device__ __forceinline__ uint64_t mix64(uint64_t z) {
     z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
@@ -76,12 +76,13 @@ __device__ long long probe(const RolloutArgs& a, const uint64_t* kw, int nk, boo
 
 // Unsatisfied-service bitmap (completion_type_key, mcts.hpp:38-43): bit i set when
 // comp[i] < 1 - 1e-9 (core.hpp:18,217-221).  Warp-uniform result.
-__device__ __forceinline__ bool type_key(const double (&c)[kMaxJ], int n, uint64_t (&kw)[4]) {
+template <int J>
+__device__ __forceinline__ bool type_key(const double (&c)[J], int n, uint64_t (&kw)[4]) {
     const int lane = static_cast<int>(threadIdx.x & 31u);
     bool any = false;
     for (int w = 0; w < 4; ++w) kw[w] = 0;
 #pragma unroll
-    for (int j = 0; j < kMaxJ; ++j) {
+    for (int j = 0; j < J; ++j) {
         if (32 * j >= n) break;
         const bool un = lane + 32 * j < n && c[j] < 1.0 - 1e-9;
         const unsigned b = __ballot_sync(0xffffffffu, un);
@@ -92,7 +93,8 @@ __device__ __forceinline__ bool type_key(const double (&c)[kMaxJ], int n, uint64
 }
 
 // Add the chosen candidate's utilities (add_util; mcts.hpp:139) in the owning lanes.
-__device__ __forceinline__ void add_row(const DevModel& M, uint64_t row, double (&c)[kMaxJ]) {
+template <int J>
+__device__ __forceinline__ void add_row(const DevModel& M, uint64_t row, double (&c)[J]) {
     const int lane = static_cast<int>(threadIdx.x & 31u);
 #pragma unroll
     for (int m = 0; m < 4; ++m) {
@@ -101,7 +103,7 @@ __device__ __forceinline__ void add_row(const DevModel& M, uint64_t row, double 
         if (svc < M.n && (svc & 31) == lane) {
             const double u = __ldg(&M.U[code]);
 #pragma unroll
-            for (int j = 0; j < kMaxJ; ++j)
+            for (int j = 0; j < J; ++j)
                 if ((svc >> 5) == j) c[j] = __dadd_rn(c[j], u);
         }
     }
@@ -198,7 +200,8 @@ __device__ int block_topk(const RolloutArgs& a, const double* comp, double* W, C
 
 }  // namespace
 
-__global__ void __launch_bounds__(kRThreads, 1) rollout_kernel(const __grid_constant__ RolloutArgs a) {
+template <int J>
+__global__ void __launch_bounds__(kRThreads, 2) rollout_kernel(const __grid_constant__ RolloutArgs a) {
     extern __shared__ __align__(16) unsigned char smem[];
     const DevModel& M = a.M;
     const int n = M.n;
@@ -221,10 +224,10 @@ __global__ void __launch_bounds__(kRThreads, 1) rollout_kernel(const __grid_cons
 
     // One warp-step of rollout r (see the file comment).  first: the start state (no pick).
     auto advance = [&](long long r, bool first, int nxt, int& nbuf) {
-        double c[kMaxJ];
+        double c[J];
         const double* src = first ? a.comp0 : a.comp + r * n;
 #pragma unroll
-        for (int j = 0; j < kMaxJ; ++j) c[j] = (lane + 32 * j < n) ? src[lane + 32 * j] : 2.0;
+        for (int j = 0; j < J; ++j) c[j] = (lane + 32 * j < n) ? src[lane + 32 * j] : 2.0;
         int L = first ? 0 : a.len[r];
         if (first && lane == 0) a.len[r] = 0;
         if (!first) {
@@ -266,7 +269,7 @@ __global__ void __launch_bounds__(kRThreads, 1) rollout_kernel(const __grid_cons
             return;
         }
 #pragma unroll
-        for (int j = 0; j < kMaxJ; ++j)
+        for (int j = 0; j < J; ++j)
             if (lane + 32 * j < n) a.comp[r * n + lane + 32 * j] = c[j];
         long long slot = 0;
         if (lane == 0) {
@@ -351,9 +354,9 @@ __global__ void __launch_bounds__(kRThreads, 1) rollout_kernel(const __grid_cons
         if (best != ~0ull && __ldcg(&C->status) == 0) {
             const long long r = static_cast<long long>(best & 0xFFFFFFFFull);
             const int L = static_cast<int>(best >> 32);
-            double c[kMaxJ];
+            double c[J];
 #pragma unroll
-            for (int j = 0; j < kMaxJ; ++j) c[j] = (lane + 32 * j < n) ? a.comp0[lane + 32 * j] : 2.0;
+            for (int j = 0; j < J; ++j) c[j] = (lane + 32 * j < n) ? a.comp0[lane + 32 * j] : 2.0;
             for (int t = 0; t < L; ++t) {
                 uint64_t kw[4];
                 type_key(c, n, kw);
@@ -381,7 +384,9 @@ __global__ void __launch_bounds__(kRThreads, 1) rollout_kernel(const __grid_cons
 size_t rollout_smem_bytes(int n, int PP) {
     return static_cast<size_t>((n + 1) * PP + n + 1) * 8 + static_cast<size_t>(kRCandCap + kRMaxK) * sizeof(Cand);
 }
-const void* rollout_kernel_ptr() { return reinterpret_cast<const void*>(&rollout_kernel); }
+const void* rollout_kernel_ptr(int n) {
+    return n <= 64 ? reinterpret_cast<const void*>(&rollout_kernel<2>) : reinterpret_cast<const void*>(&rollout_kernel<kMaxJ>);
+}
 int rollout_threads() { return kRThreads; }
 
 }  // namespace mgb
