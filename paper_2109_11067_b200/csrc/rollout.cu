@@ -93,9 +93,11 @@ __device__ __forceinline__ bool type_key(const double (&c)[J], int n, uint64_t (
 }
 
 // Add the chosen candidate's utilities (add_util; mcts.hpp:139) in the owning lanes.
+// Returns the lane's bitmask of modified slots (so only those are written back).
 template <int J>
-__device__ __forceinline__ void add_row(const DevModel& M, uint64_t row, double (&c)[J]) {
+__device__ __forceinline__ unsigned add_row(const DevModel& M, uint64_t row, double (&c)[J]) {
     const int lane = static_cast<int>(threadIdx.x & 31u);
+    unsigned dirty = 0;
 #pragma unroll
     for (int m = 0; m < 4; ++m) {
         const int code = static_cast<int>((row >> (16 * m)) & 0xFFFFull);
@@ -104,9 +106,10 @@ __device__ __forceinline__ void add_row(const DevModel& M, uint64_t row, double 
             const double u = __ldg(&M.U[code]);
 #pragma unroll
             for (int j = 0; j < J; ++j)
-                if ((svc >> 5) == j) c[j] = __dadd_rn(c[j], u);
+                if ((svc >> 5) == j) c[j] = __dadd_rn(c[j], u), dirty |= 1u << j;
         }
     }
+    return dirty;
 }
 
 // Top-K of the base pool under `comp` (smem) by one CTA: W = need*U, threshold from the
@@ -229,6 +232,7 @@ __global__ void __launch_bounds__(kRThreads, 2) rollout_kernel(const __grid_cons
 #pragma unroll
         for (int j = 0; j < J; ++j) c[j] = (lane + 32 * j < n) ? src[lane + 32 * j] : 2.0;
         int L = first ? 0 : a.len[r];
+        unsigned dirty = first ? ~0u : 0u;  // slots to write back (all of them for a new rollout)
         if (first && lane == 0) a.len[r] = 0;
         if (!first) {
             const unsigned slot = a.rslot[r];
@@ -243,7 +247,7 @@ __global__ void __launch_bounds__(kRThreads, 2) rollout_kernel(const __grid_cons
             }
             const uint64_t x = philox_u64(a.seed, static_cast<uint64_t>(a.id0 + r), static_cast<uint64_t>(L));
             const unsigned pick = __ldcg(&a.pool[static_cast<size_t>(slot) * a.k + philox_below(x, pn)]);
-            add_row(M, __ldg(a.base + pick), c);
+            dirty |= add_row(M, __ldg(a.base + pick), c);
             ++L;
             if (lane == 0) {
                 a.len[r] = L;
@@ -270,7 +274,7 @@ __global__ void __launch_bounds__(kRThreads, 2) rollout_kernel(const __grid_cons
         }
 #pragma unroll
         for (int j = 0; j < J; ++j)
-            if (lane + 32 * j < n) a.comp[r * n + lane + 32 * j] = c[j];
+            if (lane + 32 * j < n && ((dirty >> j) & 1u)) a.comp[r * n + lane + 32 * j] = c[j];
         long long slot = 0;
         if (lane == 0) {
             bool created = false;
