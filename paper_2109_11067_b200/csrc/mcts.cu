@@ -1056,13 +1056,21 @@ __global__ void __launch_bounds__(kMThreads, 1) mcts_kernel(const __grid_constan
             // warp 0 steps alone through cache hits; the block joins for a miss's top-K
             for (;;) {
                 if (warp == 0) {
+                    // n <= 32: lane i keeps cur[i] in a register for the whole walk (written back
+                    // when the block needs it: a miss's top-K, or the end of the rollout)
+                    const bool regc = n <= 32;
+                    double creg = regc && lane < n ? cur[lane] : 2.0;
                     for (;;) {
                         if (g.idx >= 312) mt_twist_warp(g);  // the serial twist in mt_next stays the fallback
                         uint64_t kw[4] = {0, 0, 0, 0};
-                        for (int i0 = 0; i0 < n; i0 += 32) {
-                            const int i = i0 + lane;
-                            const unsigned bm = __ballot_sync(0xffffffffu, i < n && cur[i] < 1.0 - 1e-9);
-                            kw[i0 >> 6] |= static_cast<uint64_t>(bm) << (i0 & 63);
+                        if (regc) {
+                            kw[0] = __ballot_sync(0xffffffffu, lane < n && creg < 1.0 - 1e-9);
+                        } else {
+                            for (int i0 = 0; i0 < n; i0 += 32) {
+                                const int i = i0 + lane;
+                                const unsigned bm = __ballot_sync(0xffffffffu, i < n && cur[i] < 1.0 - 1e-9);
+                                kw[i0 >> 6] |= static_cast<uint64_t>(bm) << (i0 & 63);
+                            }
                         }
                         int st = 0, idx = 0;  // st: 1 done, 2 miss, 3 abort
                         if (lane == 0) {
@@ -1140,9 +1148,19 @@ __global__ void __launch_bounds__(kMThreads, 1) mcts_kernel(const __grid_constan
                             }
                         }
                         st = __shfl_sync(0xffffffffu, st, 0);
-                        if (st) break;
+                        if (st) {
+                            if (regc && lane < n) cur[lane] = creg;
+                            break;
+                        }
                         idx = __shfl_sync(0xffffffffu, idx, 0);
-                        if (lane < 4) {  // rollout add (mcts.hpp:139): distinct services, the adds commute
+                        if (regc) {  // rollout add (mcts.hpp:139) in the owning lanes
+                            const uint64_t row = rowat(idx);
+#pragma unroll
+                            for (int m = 0; m < 4; ++m) {
+                                const int code = static_cast<int>((row >> (16 * m)) & 0xFFFFull);
+                                if (csvc[code] == lane) creg = __dadd_rn(creg, Us[code]);
+                            }
+                        } else if (lane < 4) {  // distinct services: the adds commute
                             const int code = static_cast<int>((rowat(idx) >> (16 * lane)) & 0xFFFFull);
                             const int svc = csvc[code];
                             if (svc < n) cur[svc] = __dadd_rn(cur[svc], Us[code]);
