@@ -154,13 +154,25 @@ def measured_peak():
         return 6650.0, "fallback"
 
 
-def profile_traffic():
-    """dram bytes per greedy-kernel launch from the committed ncu capture, if any."""
-    p = os.path.join(ROOT, "profiles", "greedy_kernel_ncu.json")
+# committed `ncu --set full` captures (tools/ncu_summary.py) per kernel and workload
+TRAFFIC_PROFILES = {
+    ("mcts_kernel", "slos24_ga"): ("r01c_mcts_slos24_ncu.json", "slos_24 GA round (probe_ga slos_24 1), one launch"),
+    ("greedy_kernel", "slos24_ga"): ("r01c_greedy_slos24_ncu.json", "slos_24 fast_algo (probe_greedy slos_24)"),
+    ("greedy_kernel", "gen128_8.0_greedy"): ("r01b_greedy_gen128_ncu.json", "gen(128, 8.0) fast_algo"),
+}
+
+
+def profile_traffic(kernel="mcts_kernel", workload="slos24_ga"):
+    """dram__bytes_read + dram__bytes_write per launch of `kernel` from the committed ncu
+    capture of the same workload, if any (cold-cache, serialised: context, not timing)."""
+    ent = TRAFFIC_PROFILES.get((kernel, workload))
+    if not ent:
+        return None, None
     try:
-        with open(p) as f:
+        with open(os.path.join(ROOT, "profiles", ent[0])) as f:
             d = json.load(f)
-        return d.get("dram_bytes_per_launch"), d.get("workload")
+        k = next(x for x in d["kernels"] if x["kernel"].startswith(kernel))
+        return k.get("dram_bytes_per_launch"), ent[1]
     except Exception:
         return None, None
 
@@ -188,7 +200,10 @@ def extra_measurements(mp, local, peak):
             "gpus_used": len(plan), "rows_scored": st["greedy_rows"], "steps": st["greedy_steps"],
             "ext_rows": st["ext_rows"], "kernel_ms": st["greedy_ms"], "configs_per_s": st["greedy_rows"] / sec,
             "roofline": {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
-                         "bytes_per_unit": 8, "kernel": "greedy_kernel"}}
+                         "bytes_per_unit": 8, "kernel": "greedy_kernel",
+                         "bytes_per_launch": 8.0 * st["greedy_rows"] / max(st["greedy_calls"], 1),
+                         "traffic": profile_traffic("greedy_kernel", "gen128_8.0_greedy")[0],
+                         "traffic_workload": profile_traffic("greedy_kernel", "gen128_8.0_greedy")[1]}}
         ctx.close()
     except Exception as e:  # pragma: no cover - reported, not fatal
         out["stress_greedy"] = {"error": repr(e)}
@@ -398,7 +413,7 @@ def main():
         launch_s = k_ms / 1e3 / max(k_calls, 1)
         k_bytes = 8.0 * k_rows / max(k_calls, 1)  # algorithmic bytes per launch
         achieved = k_bytes / launch_s / 1e9 if launch_s > 0 else 0.0
-        traffic, traffic_wl = profile_traffic()
+        traffic, traffic_wl = profile_traffic(dom, args.workload)
         line = {
             "metric": "candidate configs scored/sec", "value": rows_all / (dev_ms_max / 1e3), "unit": "configs/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": dev_ms_max / args.steps,
