@@ -306,12 +306,15 @@ __device__ __forceinline__ float ub2(const float* __restrict__ Wf, unsigned lo, 
 
 __device__ __forceinline__ void consider8(const DevModel& M, const double* __restrict__ W, const float* __restrict__ Wf,
                                           const double* U, const uint4& v0, const uint4& v1, const uint4& v2,
-                                          const uint4& v3, Best& best) {
+                                          const uint4& v3, Best& best, double floor = 0.0) {
     const float ub[8] = {ub2(Wf, v0.x, v0.y), ub2(Wf, v0.z, v0.w), ub2(Wf, v1.x, v1.y), ub2(Wf, v1.z, v1.w),
                          ub2(Wf, v2.x, v2.y), ub2(Wf, v2.z, v2.w), ub2(Wf, v3.x, v3.y), ub2(Wf, v3.z, v3.w)};
     // FP32 floor rounded DOWN: ub >= best.s implies ub >= ff, so no row that can win or tie
-    // is skipped; with no best yet, ff = the smallest positive float (rows must score > 0)
-    const float ff = best.s > 0.0 ? __double2float_rd(best.s) : 1.40129846e-45f;
+    // is skipped; with no best yet, ff = the smallest positive float (rows must score > 0).
+    // `floor` is a score some row of the warp already has: a row below it cannot be the argmax
+    // (it may still tie it, so the compare stays >=).
+    const double fl = fmax(best.s, floor);
+    const float ff = fl > 0.0 ? __double2float_rd(fl) : 1.40129846e-45f;
     bool hit = false;
 #pragma unroll
     for (int j = 0; j < 8; ++j) hit |= ub[j] >= ff;
@@ -322,7 +325,7 @@ __device__ __forceinline__ void consider8(const DevModel& M, const double* __res
                                (static_cast<uint64_t>(v3.y) << 32) | v3.x, (static_cast<uint64_t>(v3.w) << 32) | v3.z};
 #pragma unroll
         for (int j = 0; j < 8; ++j)
-            if (static_cast<double>(ub[j]) >= (best.s > 0.0 ? best.s : 4.9406564584124654e-324))
+            if (static_cast<double>(ub[j]) >= (fl > 0.0 ? fl : 4.9406564584124654e-324))
                 take(M, U, r[j], row_score(W, r[j]), best);
     }
 }
@@ -744,6 +747,9 @@ __global__ void __launch_bounds__(kThreads, 1) greedy_kernel(const __grid_consta
             const double s0 = row_score(W, prev_row);
             if (s0 > 0.0) best = Best{s0, row_usum(U, prev_row), prev_row};
         }
+        double wfloor = best.s;  // the warp's best re-scored row: a common floor for its lanes
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) wfloor = fmax(wfloor, __shfl_xor_sync(0xffffffffu, wfloor, off));
         {
             int j = 0;
             for (; j + 3 < cj; j += 4) {
@@ -751,7 +757,7 @@ __global__ void __launch_bounds__(kThreads, 1) greedy_kernel(const __grid_consta
                 const uint4 v1 = cache[(j + 1) * blockDim.x + threadIdx.x];
                 const uint4 v2 = cache[(j + 2) * blockDim.x + threadIdx.x];
                 const uint4 v3 = cache[(j + 3) * blockDim.x + threadIdx.x];
-                consider8(M, W, Wf, U, v0, v1, v2, v3, best);
+                consider8(M, W, Wf, U, v0, v1, v2, v3, best, wfloor);
             }
             for (; j < cj; ++j) consider2(M, W, U, cache[j * blockDim.x + threadIdx.x], best);
             long long u = my0 + static_cast<long long>(cj) * GT;
@@ -794,7 +800,7 @@ __global__ void __launch_bounds__(kThreads, 1) greedy_kernel(const __grid_consta
                     const uint4 v3 = t + 1536 < cnt ? st[t + 1536] : padv;
                     __syncwarp();
                     if (lane_id() == 0) mbar_arrive(&empty_bar[slot]);
-                    consider8(M, W, Wf, U, v0, v1, v2, v3, best);
+                    consider8(M, W, Wf, U, v0, v1, v2, v3, best, wfloor);
                     if (threadIdx.x == 0 && i + S < my_n) issue(i + S);
                 }
                 kchunk += static_cast<unsigned long long>(my_n);
@@ -814,7 +820,7 @@ __global__ void __launch_bounds__(kThreads, 1) greedy_kernel(const __grid_consta
                 // rows appended during this launch: L2-coherent loads (never the non-coherent path)
                 const uint4 v0 = ld_row4(rows4 + u, LOADM), v1 = ld_row4(rows4 + u + GT, LOADM),
                             v2 = ld_row4(rows4 + u + 2 * GT, LOADM), v3 = ld_row4(rows4 + u + 3 * GT, LOADM);
-                consider8(M, W, Wf, U, v0, v1, v2, v3, best);
+                consider8(M, W, Wf, U, v0, v1, v2, v3, best, wfloor);
             }
             for (; u < NU; u += GT) consider2(M, W, U, __ldcg(rows4 + u), best);
             if ((N & 1) && my0 == 0) consider(M, W, U, __ldcg(a.rows + N - 1), best);
