@@ -1321,8 +1321,12 @@ std::vector<MctsDeviceResult> Engine::mcts_device_group(const std::vector<std::v
         for (int q = 0; q < nb; ++q) {
             const Off& o = offs[q];
             unsigned char* b = static_cast<unsigned char*>(slots[q]->mcts_mem);
+            // the outputs are carved contiguously (trace, best, desc, dcomp, out): one copy
+            std::vector<unsigned char> hb(o.out + sizeof(int) * 24 - o.trace);
+            CK(cudaMemcpy(hb.data(), b + o.trace, hb.size(), cudaMemcpyDeviceToHost));
+            auto at = [&](size_t off) { return hb.data() + (off - o.trace); };
             int out[24];
-            CK(cudaMemcpy(out, b + o.out, sizeof(out), cudaMemcpyDeviceToHost));
+            std::memcpy(out, at(o.out), sizeof(out));
             MctsDeviceResult& r = results[b0 + q];
             r.status = out[0];
             r.best_len = out[1];
@@ -1346,12 +1350,11 @@ std::vector<MctsDeviceResult> Engine::mcts_device_group(const std::vector<std::v
             }
             r.trace.resize(4 * static_cast<size_t>(r.iterations));
             std::vector<int> best(std::max(r.best_len, 0)), desc(out[2]);
-            if (!r.trace.empty())
-                CK(cudaMemcpy(r.trace.data(), b + o.trace, sizeof(int) * r.trace.size(), cudaMemcpyDeviceToHost));
-            if (!best.empty()) CK(cudaMemcpy(best.data(), b + o.best, sizeof(int) * best.size(), cudaMemcpyDeviceToHost));
-            if (!desc.empty()) CK(cudaMemcpy(desc.data(), b + o.desc, sizeof(int) * desc.size(), cudaMemcpyDeviceToHost));
+            if (!r.trace.empty()) std::memcpy(r.trace.data(), at(o.trace), sizeof(int) * r.trace.size());
+            if (!best.empty()) std::memcpy(best.data(), at(o.best), sizeof(int) * best.size());
+            if (!desc.empty()) std::memcpy(desc.data(), at(o.desc), sizeof(int) * desc.size());
             r.descent_comp.resize(n);
-            CK(cudaMemcpy(r.descent_comp.data(), b + o.dcomp, sizeof(double) * n, cudaMemcpyDeviceToHost));
+            std::memcpy(r.descent_comp.data(), at(o.dcomp), sizeof(double) * n);
             r.best.assign(best.begin(), best.end());
             r.descent.assign(desc.begin(), desc.end());
             // work counters with the reference's definitions (mcts.hpp:59-67): every expansion
@@ -1361,8 +1364,7 @@ std::vector<MctsDeviceResult> Engine::mcts_device_group(const std::vector<std::v
             stats.mcts_topk_calls += r.expands + r.builds;
             stats.mcts_rows += r.expand_rows + static_cast<long long>(r.builds) * pool_size();
             stats.h2d += static_cast<long long>(sizeof(double) * n);
-            stats.d2h += static_cast<long long>(sizeof(out) + sizeof(int) * (r.trace.size() + best.size() + desc.size()) +
-                                                sizeof(double) * n);
+            stats.d2h += static_cast<long long>(hb.size());
         }
     }
     return results;
