@@ -1060,6 +1060,8 @@ __global__ void __launch_bounds__(kMThreads, 1) mcts_kernel(const __grid_constan
                     // when the block needs it: a miss's top-K, or the end of the rollout)
                     const bool regc = n <= 32;
                     double creg = regc && lane < n ? cur[lane] : 2.0;
+                    int r_steps = s_steps;  // lane 0's step count (written back when the walk pauses)
+                    if (lane == 0) s_miss = 0;
                     for (;;) {
                         if (g.idx >= 312) mt_twist_warp(g);  // the serial twist in mt_next stays the fallback
                         uint64_t kw[4] = {0, 0, 0, 0};
@@ -1073,13 +1075,12 @@ __global__ void __launch_bounds__(kMThreads, 1) mcts_kernel(const __grid_constan
                             }
                         }
                         int st = 0, idx = 0;  // st: 1 done, 2 miss, 3 abort
-                        if (lane == 0) {
-                            s_miss = 0;
+                        if (lane == 0) {  // lane 0's state lives in registers; the block reads it after the walk
                             if (!(kw[0] | kw[1] | kw[2] | kw[3])) {  // satisfied
                                 s_done = 1;
-                                s_est = s_steps;
+                                s_est = r_steps;
                                 st = 1;
-                            } else if (s_steps >= max_depth) {
+                            } else if (r_steps >= max_depth) {
                                 s_done = 1;
                                 s_est = max_depth;
                                 st = 1;
@@ -1091,20 +1092,20 @@ __global__ void __launch_bounds__(kMThreads, 1) mcts_kernel(const __grid_constan
                                     h ^= h >> 31;
                                 }
                                 // level 1: the on-chip copy of the cache (keys + pools in shared memory)
-                                s_l1 = -1;
-                                s_l1new = -1;
+                                int l1 = -1, l1new = -1, slot = 0;
+                                bool miss = false;
                                 if (use_l1) {
                                     unsigned q = static_cast<unsigned>(h >> 32) & (kL1Slots - 1);
                                     for (int t = 0; t < kL1Slots; ++t, q = (q + 1) & (kL1Slots - 1)) {
                                         if (l1_n[q] == kL1Empty) break;
                                         if (l1_key[q][0] == kw[0] && l1_key[q][1] == kw[1] && l1_key[q][2] == kw[2] &&
                                             l1_key[q][3] == kw[3]) {
-                                            s_l1 = static_cast<int>(q);
+                                            l1 = static_cast<int>(q);
                                             break;
                                         }
                                     }
                                 }
-                                if (s_l1 < 0) {  // level 2: the global table (source of truth)
+                                if (l1 < 0) {  // level 2: the global table (source of truth)
                                     unsigned sl = static_cast<unsigned>(h) & a.tab_mask;
                                     for (unsigned t = 0;; ++t, sl = (sl + 1) & a.tab_mask) {
                                         if (t > a.tab_mask) {
@@ -1115,7 +1116,7 @@ __global__ void __launch_bounds__(kMThreads, 1) mcts_kernel(const __grid_constan
                                         if (!a.tag[sl]) {  // miss: insert, pool built by the block
                                             a.tag[sl] = 1;
                                             for (int w = 0; w < 4; ++w) a.key[4ull * sl + w] = kw[w];
-                                            s_miss = 1;
+                                            miss = true;
                                             st = 2;
                                             break;
                                         }
@@ -1123,29 +1124,35 @@ __global__ void __launch_bounds__(kMThreads, 1) mcts_kernel(const __grid_constan
                                             a.key[4ull * sl + 2] == kw[2] && a.key[4ull * sl + 3] == kw[3])
                                             break;
                                     }
-                                    s_slot = static_cast<int>(sl);
-                                    if (s_miss && use_l1 && l1_used < kL1Slots * 3 / 4) {  // mirror the new key on chip
+                                    slot = static_cast<int>(sl);
+                                    if (miss && use_l1 && l1_used < kL1Slots * 3 / 4) {  // mirror the new key on chip
                                         unsigned q = static_cast<unsigned>(h >> 32) & (kL1Slots - 1);
                                         while (l1_n[q] != kL1Empty) q = (q + 1) & (kL1Slots - 1);
                                         for (int w = 0; w < 4; ++w) l1_key[q][w] = kw[w];
                                         l1_n[q] = kL1Pending;
                                         ++l1_used;
-                                        s_l1new = static_cast<int>(q);
+                                        l1new = static_cast<int>(q);
                                     }
                                 }
                                 if (st == 0) {  // hit: a uniform pick from the cached pool
-                                    const int pn = s_l1 >= 0 ? l1_n[s_l1] : a.pool_n[s_slot];
+                                    const int pn = l1 >= 0 ? l1_n[l1] : a.pool_n[slot];
                                     if (pn <= 0) {
                                         s_abort = 1;  // "rollout: no candidate config serves the remaining demand"
                                         st = 3;
                                     } else {
                                         const unsigned pk = static_cast<unsigned>(mt_pick(g, static_cast<uint64_t>(pn)));
-                                        idx = static_cast<int>(s_l1 >= 0 ? l1_pool[s_l1][pk]
-                                                                         : a.pool[static_cast<long long>(s_slot) * K + pk]);
-                                        a.picked[s_steps++] = idx;
+                                        idx = static_cast<int>(l1 >= 0 ? l1_pool[l1][pk]
+                                                                       : a.pool[static_cast<long long>(slot) * K + pk]);
+                                        a.picked[r_steps++] = idx;
                                     }
                                 }
+                                if (st == 2) {  // the block builds this key's pool
+                                    s_miss = 1;
+                                    s_slot = slot;
+                                    s_l1new = l1new;
+                                }
                             }
+                            if (st) s_steps = r_steps;
                         }
                         st = __shfl_sync(0xffffffffu, st, 0);
                         if (st) {
