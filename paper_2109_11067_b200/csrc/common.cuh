@@ -21,41 +21,33 @@ __device__ __forceinline__ unsigned long long globaltimer() {
 // The row's layout is the sum of its members' count patterns; within a size group the
 // lower service index holds the lower slots (config_enum.hpp:140,159-163).
 static __device__ __noinline__ void row_key(const DevModel& M, uint64_t row, uint64_t& hi, uint64_t& lo) {
-    int svc[4], pat[4], k = 0;
+    // members (ascending services): (service, pattern) and the pattern's packed size counts
+    int svc[4], k = 0;
+    uint32_t pk[4], tot = 0;
     const int sentinel = M.n * M.PP;
+#pragma unroll
     for (int j = 0; j < 4; ++j) {
-        int code = static_cast<int>((row >> (16 * j)) & 0xFFFFull);
+        const int code = static_cast<int>((row >> (16 * j)) & 0xFFFFull);
         if (code == sentinel) break;
-        svc[k] = code / M.PP;
-        pat[k] = code % M.PP;
+        const unsigned e = M.key_code[code];
+        svc[k] = static_cast<int>(e >> 8);
+        pk[k] = M.pat_packed[e & 0xFFu];
+        tot += pk[k];  // <= 7 instances per size: no carries between the 3-bit fields
         ++k;
     }
-    int tot[5] = {0, 0, 0, 0, 0};
-    for (int j = 0; j < k; ++j)
-        for (int s = 0; s < 5; ++s) tot[s] += M.pat_count[pat[j] * 5 + s];
-    int L = 0;
-    for (int l = 0; l < M.n_layouts; ++l) {
-        bool eq = true;
-        for (int s = 0; s < 5; ++s) eq &= M.layout_count[l * 5 + s] == tot[s];
-        if (eq) {
-            L = l;
-            break;
-        }
-    }
+    const int L = M.layout_of[tot & 0x7FFFu];  // the row's layout is the sum of its members' patterns
     unsigned __int128 key = 0;
     int ninst = 0;
     for (int si = 0; si < M.n_sizes; ++si) {
-        int j = 0, used = 0;
-        for (int t = 0; t < tot[si]; ++t) {
-            while (used >= M.pat_count[pat[j] * 5 + si]) {
-                ++j;
-                used = 0;
+        int t = 0;
+        for (int j = 0; j < k; ++j) {  // within a size group the lower service holds the lower slots
+            const int c = static_cast<int>((pk[j] >> (3 * si)) & 7u);
+            for (int q = 0; q < c; ++q, ++t) {
+                const unsigned slot = static_cast<unsigned>(M.layout_slots[(L * 5 + si) * 7 + t]);
+                key = (key << 15) | ((1u << 14) | (static_cast<unsigned>(M.sizes[si]) << 11) | (slot << 8) |
+                                     static_cast<unsigned>(svc[j]));
+                ++ninst;
             }
-            unsigned slot = static_cast<unsigned>(M.layout_slots[(L * 5 + si) * 7 + t]);
-            key = (key << 15) | ((1u << 14) | (static_cast<unsigned>(M.sizes[si]) << 11) | (slot << 8) |
-                                 static_cast<unsigned>(svc[j]));
-            ++used;
-            ++ninst;
         }
     }
     for (; ninst < 7; ++ninst) key <<= 15;

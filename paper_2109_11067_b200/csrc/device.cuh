@@ -26,6 +26,11 @@ struct DevModel {
     const int* sizes;             // n_sizes (ascending)
     const double* thr;            // n * 5: selected throughput per (service, size index), 0 if infeasible
     const double* req;            // n: required rps
+    // row_key tables (common.cuh): per code (svc << 8 | pattern), per pattern its size counts
+    // packed 3 bits per size index, and the layout of every packed count vector (0xFF: none)
+    const uint16_t* key_code;     // (n + 1) * PP
+    const uint32_t* pat_packed;   // PP
+    const uint8_t* layout_of;     // 1 << 15
 };
 
 // One argmax candidate: score, util_sum, packed row.

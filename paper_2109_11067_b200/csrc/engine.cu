@@ -278,6 +278,22 @@ Engine::Engine(const Rules& rules, std::map<std::string, ModelProfile> profiles,
             if (m_.feas[i][si].ok) thr[static_cast<size_t>(i) * kMaxSizes + si] = m_.feas[i][si].thr;
     }
     const size_t o_thr = put(thr.data(), thr.size() * 8), o_req = put(req.data(), req.size() * 8);
+    // row_key tables: code -> (service, pattern), pattern -> packed size counts, packed -> layout
+    if (m_.PP > 255) throw ArgumentError("partition rules with more than 255 member patterns are not supported");
+    std::vector<uint16_t> kcode(static_cast<size_t>(m_.n + 1) * m_.PP, 0);
+    for (int c = 0; c < (m_.n + 1) * m_.PP; ++c)
+        kcode[c] = static_cast<uint16_t>(((c / m_.PP) << 8) | (c % m_.PP));
+    std::vector<uint32_t> ppk(m_.PP, 0u);
+    for (int p = 0; p < m_.PP; ++p)
+        for (int q = 0; q < kMaxSizes; ++q) ppk[p] |= static_cast<uint32_t>(m_.patterns[p][q] & 7) << (3 * q);
+    std::vector<uint8_t> lof(1u << 15, 0xFF);
+    for (size_t l = 0; l < m_.layouts.size(); ++l) {
+        uint32_t v = 0;
+        for (int q = 0; q < kMaxSizes; ++q) v |= static_cast<uint32_t>(m_.layouts[l].count[q] & 7) << (3 * q);
+        if (lof[v] == 0xFF) lof[v] = static_cast<uint8_t>(l);
+    }
+    const size_t o_kc = put(kcode.data(), kcode.size() * 2), o_ppk = put(ppk.data(), ppk.size() * 4),
+                 o_lof = put(lof.data(), lof.size());
     const size_t o_base = (blob.size() + 15) & ~size_t{15};
     unsigned char* d = dalloc<unsigned char>(dev_allocs_, o_base + (static_cast<size_t>(total) + 2) * 8);
     CK(cudaMemcpy(d, blob.data(), blob.size(), cudaMemcpyHostToDevice));
@@ -293,6 +309,9 @@ Engine::Engine(const Rules& rules, std::map<std::string, ModelProfile> profiles,
     dm_.sizes = reinterpret_cast<const int*>(d + o_sz);
     dm_.thr = reinterpret_cast<const double*>(d + o_thr);
     dm_.req = reinterpret_cast<const double*>(d + o_req);
+    dm_.key_code = reinterpret_cast<const uint16_t*>(d + o_kc);
+    dm_.pat_packed = reinterpret_cast<const uint32_t*>(d + o_ppk);
+    dm_.layout_of = d + o_lof;
     d_base_ = reinterpret_cast<uint64_t*>(d + o_base);
     const auto t2 = clk::now();
 
