@@ -324,8 +324,8 @@ __device__ __forceinline__ void consider8(const DevModel& M, const double* __res
                                (static_cast<uint64_t>(v2.y) << 32) | v2.x, (static_cast<uint64_t>(v2.w) << 32) | v2.z,
                                (static_cast<uint64_t>(v3.y) << 32) | v3.x, (static_cast<uint64_t>(v3.w) << 32) | v3.z};
 #pragma unroll
-        for (int j = 0; j < 8; ++j)
-            if (static_cast<double>(ub[j]) >= (fl > 0.0 ? fl : 4.9406564584124654e-324))
+        for (int j = 0; j < 8; ++j)  // (the thread's current best row needs no second look)
+            if (static_cast<double>(ub[j]) >= (fl > 0.0 ? fl : 4.9406564584124654e-324) && r[j] != best.row)
                 take(M, U, r[j], row_score(W, r[j]), best);
     }
 }
