@@ -692,7 +692,14 @@ int Engine::greedy_cluster_ctas(size_t smem) const {
     if (n_ranks_ > 1) return 0;
     constexpr long long kClusterRows = 256ll << 10;
     int want = pool_size() + ext_bound_ <= kClusterRows ? 16 : 0;
-    if (const char* v = std::getenv("MIGPLAN_GREEDY_CLUSTER")) want = std::max(0, std::min(16, std::atoi(v)));
+    const char* v = std::getenv("MIGPLAN_GREEDY_CLUSTER");
+    if (v) want = std::max(0, std::min(16, std::atoi(v)));
+    const bool cacheable = !v;
+    if (cacheable && cluster_ctas_ >= 0) return cluster_ctas_;  // the occupancy query is per context
+    auto done = [&](int r) {
+        if (cacheable) cluster_ctas_ = r;
+        return r;
+    };
     for (; want >= 2; want >>= 1) {  // the largest size the GPU can co-schedule
         cudaLaunchConfig_t cfg{};
         cfg.gridDim = dim3(want);
@@ -706,10 +713,10 @@ int Engine::greedy_cluster_ctas(size_t smem) const {
         cfg.attrs = at;
         cfg.numAttrs = 1;
         int nc = 0;
-        if (cudaOccupancyMaxActiveClusters(&nc, greedy_kernel_ptr(), &cfg) == cudaSuccess && nc > 0) return want;
+        if (cudaOccupancyMaxActiveClusters(&nc, greedy_kernel_ptr(), &cfg) == cudaSuccess && nc > 0) return done(want);
         cudaGetLastError();
     }
-    return 0;
+    return done(0);
 }
 
 

@@ -198,6 +198,7 @@ class Engine {
     std::once_flag keyrank_once_;
     const unsigned* keyrank();
     int greedy_cluster_ctas(size_t smem) const;  // 0: cooperative launch
+    mutable int cluster_ctas_ = -1;              // its cached answer (no env override)
     int greedy_interleave(int G) const;
     std::vector<double> min_u_;  // smallest positive utility per service (step bound)
     long long ext_bound_ = 0;
