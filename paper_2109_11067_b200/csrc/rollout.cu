@@ -165,7 +165,7 @@ __device__ int block_topk(const RolloutArgs& a, const double* comp, double* W, C
     int got;
     if (nc <= kRCandCap) {
         got = min(nc, k);
-        rank_select(M, cand, nc, k, win);
+        rank_select_warp(M, cand, nc, k, win);
     } else {  // exact: k rounds of "best row strictly after the previous pick"
         got = 0;
         Cand last{0.0, 0.0, kNoRow, -1};

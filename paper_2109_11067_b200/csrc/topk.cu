@@ -131,7 +131,7 @@ __global__ void __launch_bounds__(kTopkThreads, 1) topk1_kernel(const __grid_con
     for (int i = threadIdx.x; i < nc; i += blockDim.x) cand[i].u = dev::row_usum(M.U, cand[i].row);
     __syncthreads();
     const int got = nc_raw > kCandCap ? 0 : min(nc, k);
-    if (nc_raw <= kCandCap) rank_select(M, cand, nc, k, win);
+    if (nc_raw <= kCandCap) rank_select_warp(M, cand, nc, k, win);
     __syncthreads();
     if (gridDim.x == 1) {
         if (threadIdx.x < got) a.out_row[threadIdx.x] = win[threadIdx.x].row;
@@ -180,7 +180,7 @@ __global__ void __launch_bounds__(kTopkThreads, 1) topk1_kernel(const __grid_con
         __syncthreads();
         const int mc = min(n_cand, kCandCap);
         Cand* out = win + kTopkMaxK;  // spare list after this CTA's own winners
-        rank_select(M, mc_list, mc, k, out);
+        rank_select_warp(M, mc_list, mc, k, out);
         __syncthreads();
         const int mgot = min(mc, k);
         if (threadIdx.x < mgot) a.out_row[threadIdx.x] = out[threadIdx.x].row;
