@@ -217,6 +217,11 @@ struct MctsLaunch {
     int rows_smem;           // the base pool copied into shared memory
     int timers;              // accumulate top-K phase cycles (MIGPLAN_MCTS_TIMERS)
     int pair;                // every base row has <= 2 members: on-chip copy as 32-bit rows
+    // the base pool's supports (K1 order: each a contiguous row range): a top-K scans only the
+    // supports that can hold a candidate (a service with need > 0, or a sampled service)
+    int n_sup;               // 0: scan every row
+    const int* sup_begin;    // n_sup + 1 row offsets
+    const unsigned short* sup_svc;  // service a | b << 8 (b = 0xFF: single-service support)
     MctsSolveArgs s[kMaxGroups];
 };
 

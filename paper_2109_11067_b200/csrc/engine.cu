@@ -28,7 +28,8 @@ int topk1_max_ctas();
 constexpr int kTopkMaxCtas = 4096;  // partial-list capacity (Best x 32 per CTA)
 const void* topk1_kernel_ptr(int km);
 size_t rollout_smem_bytes(int n, int PP);
-size_t mcts_smem_bytes(int n, int PP, int max_nodes, long long n_base, bool node_smem, bool rows_smem, bool pair);
+size_t mcts_smem_bytes(int n, int PP, int max_nodes, long long n_base, bool node_smem, bool rows_smem, bool pair,
+                       int n_sup);
 const void* bf_kernel_ptr();
 const void* bf_sum_kernel_ptr();
 const void* bf_warp_kernel_ptr();
@@ -365,6 +366,31 @@ const unsigned* Engine::keyrank() {
         stats.launches += l;
     });
     return d_keyrank_;
+}
+
+void Engine::support_tables() {
+    std::call_once(sup_once_, [&] {
+        const int ns = static_cast<int>(support_off_.size()) - 1;
+        if (ns <= 0 || m_.max_mix > 2) return;
+        std::vector<int> begin(ns + 1);
+        std::vector<unsigned short> svc(ns);
+        for (int i = 0; i <= ns; ++i) begin[i] = static_cast<int>(support_off_[i]);
+        for (int i = 0; i < ns; ++i) {
+            int sv[kRowK], pt[kRowK];
+            const int k = support_off_[i] < support_off_[i + 1] ? m_.members(base_rows_[support_off_[i]], sv, pt) : 0;
+            if (k < 1 || k > 2) return;  // not a pair pool: scan every row
+            svc[i] = static_cast<unsigned short>(sv[0] | ((k == 2 ? sv[1] : 0xFF) << 8));
+        }
+        const size_t bb = sizeof(int) * (ns + 1), sb = sizeof(unsigned short) * ns;
+        sup_buf_ = std::make_unique<Scratch>(device_, bb + sb + 16);
+        unsigned char* d = static_cast<unsigned char*>(sup_buf_->get());
+        CK(cudaSetDevice(device_));
+        CK(cudaMemcpy(d, begin.data(), bb, cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(d + bb, svc.data(), sb, cudaMemcpyHostToDevice));
+        d_sup_begin_ = reinterpret_cast<const int*>(d);
+        d_sup_svc_ = reinterpret_cast<const unsigned short*>(d + bb);
+        n_sup_ = ns;
+    });
 }
 
 Engine::~Engine() {
@@ -1312,12 +1338,24 @@ std::vector<MctsDeviceResult> Engine::mcts_device_group(const std::vector<std::v
             const DeviceInfo& di = device_info(device_);
             const long long room = di.smem_optin - di.mcts_static_smem - 1024;
             const int mn = static_cast<int>(offs[0].max_nodes);
-            L->rows_smem = static_cast<long long>(mcts_smem_bytes(n, m_.PP, mn, slice, false, true, pair)) <= room;
+            // supports (skip the ones that cannot hold a candidate): one CTA over the whole pool
+            int ns = 0;
+            const char* sv_env = std::getenv("MIGPLAN_MCTS_SUPPORTS");
+            if (pair && C == 1 && !(sv_env && std::atoi(sv_env) == 0)) {
+                support_tables();
+                ns = n_sup_;
+            }
+            L->rows_smem = static_cast<long long>(mcts_smem_bytes(n, m_.PP, mn, slice, false, true, pair, ns)) <= room;
+            if (!(L->rows_smem && pair)) ns = 0;
             L->timers = std::getenv("MIGPLAN_MCTS_TIMERS") ? 1 : 0;
-            L->node_smem = static_cast<long long>(mcts_smem_bytes(n, m_.PP, mn, slice, true, L->rows_smem != 0, pair)) <= room;
+            L->node_smem =
+                static_cast<long long>(mcts_smem_bytes(n, m_.PP, mn, slice, true, L->rows_smem != 0, pair, ns)) <= room;
+            L->n_sup = ns;
+            L->sup_begin = ns ? d_sup_begin_ : nullptr;
+            L->sup_svc = ns ? d_sup_svc_ : nullptr;
         }
         const size_t msm = mcts_smem_bytes(n, m_.PP, static_cast<int>(offs[0].max_nodes), slice, L->node_smem != 0,
-                                           L->rows_smem != 0, pair);
+                                           L->rows_smem != 0, pair, L->n_sup);
         for (int q = 1; q < nb; ++q) CK(cudaStreamSynchronize(slots[q]->stream));
         Slot* s0 = slots[0];
         void* args[] = {L.get()};

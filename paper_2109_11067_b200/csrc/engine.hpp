@@ -199,6 +199,13 @@ class Engine {
     const unsigned* keyrank();
     int greedy_cluster_ctas(size_t smem) const;  // 0: cooperative launch
     mutable int cluster_ctas_ = -1;              // its cached answer (no env override)
+    // base-pool supports for the MCTS top-K (built on first use; pair pools only)
+    std::once_flag sup_once_;
+    std::unique_ptr<Scratch> sup_buf_;
+    int n_sup_ = 0;
+    const int* d_sup_begin_ = nullptr;
+    const unsigned short* d_sup_svc_ = nullptr;
+    void support_tables();
     int greedy_interleave(int G) const;
     std::vector<double> min_u_;  // smallest positive utility per service (step bound)
     long long ext_bound_ = 0;

@@ -418,10 +418,19 @@ __device__ __forceinline__ float ub_pair(const float* Wf, unsigned x) { return _
 __device__ __forceinline__ bool hit_pair(const unsigned char* hitc, unsigned x) {
     return (hitc[x & 0xFFFFu] | hitc[x >> 16]) != 0;
 }
+// The base pool's supports (contiguous row ranges in K1 order) and an active-list buffer; n = 0
+// scans every row.
+struct SupTab {
+    int n;
+    const int* begin;
+    const unsigned short* svc;
+    int* act;
+};
+
 __device__ __noinline__ int block_topk_pair(const DevModel& M, const unsigned* keyrank, const unsigned* base, long long nb,
                                long long pos0, const double* comp, const uint64_t* mask, int k, const double* U,
                                double* W, float* Wf, unsigned char* hitc, Cand* cand, Cand* win, int* out, int* scored,
-                               bool tm) {
+                               bool tm, SupTab sup) {
     __shared__ unsigned t_fbits;
     __shared__ int n_cand, n_hit;
     __shared__ Cand red[kMWarps];
@@ -454,6 +463,43 @@ __device__ __noinline__ int block_topk_pair(const DevModel& M, const unsigned* k
         n_hit = 0;
     }
     __syncthreads();
+    // Supports that can hold a candidate: a member with need > 0 (rows of the others all score
+    // 0), or, with a mask, a sampled member (every row of such a support touches it).
+    __shared__ int s_nact;
+    const bool bysup = sup.n > 0;
+    const int wid = static_cast<int>(threadIdx.x >> 5), nwarps = static_cast<int>(blockDim.x >> 5);
+    if (bysup) {
+        if (threadIdx.x == 0) s_nact = 0;
+        __syncthreads();
+        int hitrows = 0;
+        for (int s0 = 0; s0 < sup.n; s0 += blockDim.x) {
+            const int si = s0 + static_cast<int>(threadIdx.x);
+            bool live = false;
+            if (si < sup.n) {
+                const unsigned e = sup.svc[si];
+                const int sa = static_cast<int>(e & 0xFFu), sb2 = static_cast<int>(e >> 8);
+                if (mask)
+                    live = ((mask[sa >> 6] >> (sa & 63)) & 1ull) ||
+                           (sb2 != 0xFF && ((mask[sb2 >> 6] >> (sb2 & 63)) & 1ull));
+                else
+                    live = comp[sa] < 1.0 || (sb2 != 0xFF && comp[sb2] < 1.0);
+            }
+            const unsigned bm = __ballot_sync(0xffffffffu, live);
+            int at = 0;
+            if ((threadIdx.x & 31u) == 0 && bm) at = atomicAdd(&s_nact, __popc(bm));
+            at = __shfl_sync(0xffffffffu, at, 0) + __popc(bm & lanemask_lt());
+            if (live) {
+                sup.act[at] = si;
+                hitrows += sup.begin[si + 1] - sup.begin[si];
+            }
+        }
+        if (mask) {
+            for (int off = 16; off > 0; off >>= 1) hitrows += __shfl_xor_sync(0xffffffffu, hitrows, off);
+            if ((threadIdx.x & 31u) == 0) atomicAdd(&n_hit, hitrows);
+        }
+        __syncthreads();
+    }
+    const int nact = bysup ? s_nact : 0;
     mark(0);
     const uint4* base4 = reinterpret_cast<const uint4*>(base);  // 4 rows per 16 bytes
     const long long nq = nb >> 2;
@@ -466,7 +512,7 @@ __device__ __noinline__ int block_topk_pair(const DevModel& M, const unsigned* k
     int hits = 0;
     auto bound1 = [&](unsigned x, long long pos) {
         float u = ub_pair(Wf, x);
-        if (mask) {
+        if (mask && !bysup) {
             const bool h = hit_pair(hitc, x);
             hits += h;
             if (!h) u = 0.0f;
@@ -485,20 +531,29 @@ __device__ __noinline__ int block_topk_pair(const DevModel& M, const unsigned* k
             }
         }
     };
-    long long p = threadIdx.x;
-    for (; p + B < nq; p += 2 * B) {
-        const uint4 v0 = base4[p], v1 = base4[p + B];
-        const long long r0 = pos0 + 4 * p, r1 = pos0 + 4 * (p + B);
-        bound1(v0.x, r0), bound1(v0.y, r0 + 1), bound1(v0.z, r0 + 2), bound1(v0.w, r0 + 3);
-        bound1(v1.x, r1), bound1(v1.y, r1 + 1), bound1(v1.z, r1 + 2), bound1(v1.w, r1 + 3);
+    if (bysup) {  // a warp per active support, lanes over its rows
+        const int lane = static_cast<int>(threadIdx.x & 31u);
+        for (int i = wid; i < nact; i += nwarps) {
+            const int si = sup.act[i];
+            const int b = sup.begin[si], e = sup.begin[si + 1];
+            for (int r = b + lane; r < e; r += 32) bound1(base[r], pos0 + r);
+        }
+    } else {
+        long long p = threadIdx.x;
+        for (; p + B < nq; p += 2 * B) {
+            const uint4 v0 = base4[p], v1 = base4[p + B];
+            const long long r0 = pos0 + 4 * p, r1 = pos0 + 4 * (p + B);
+            bound1(v0.x, r0), bound1(v0.y, r0 + 1), bound1(v0.z, r0 + 2), bound1(v0.w, r0 + 3);
+            bound1(v1.x, r1), bound1(v1.y, r1 + 1), bound1(v1.z, r1 + 2), bound1(v1.w, r1 + 3);
+        }
+        for (; p < nq; p += B) {
+            const uint4 v = base4[p];
+            const long long r0 = pos0 + 4 * p;
+            bound1(v.x, r0), bound1(v.y, r0 + 1), bound1(v.z, r0 + 2), bound1(v.w, r0 + 3);
+        }
+        if (threadIdx.x < (nb & 3)) bound1(base[4 * nq + threadIdx.x], pos0 + 4 * nq + threadIdx.x);
     }
-    for (; p < nq; p += B) {
-        const uint4 v = base4[p];
-        const long long r0 = pos0 + 4 * p;
-        bound1(v.x, r0), bound1(v.y, r0 + 1), bound1(v.z, r0 + 2), bound1(v.w, r0 + 3);
-    }
-    if (threadIdx.x < (nb & 3)) bound1(base[4 * nq + threadIdx.x], pos0 + 4 * nq + threadIdx.x);
-    if (mask) {
+    if (mask && !bysup) {
         for (int off = 16; off > 0; off >>= 1) hits += __shfl_xor_sync(0xffffffffu, hits, off);
         if ((threadIdx.x & 31u) == 0) atomicAdd(&n_hit, hits);
     }
@@ -581,7 +636,25 @@ __device__ __noinline__ int block_topk_pair(const DevModel& M, const unsigned* k
             emit(xs2, sc2, (tk >> 1) & 1u, p2, 0);
         }
     }
-    if (__any_sync(0xffffffffu, rescan)) {
+    if (bysup && __any_sync(0xffffffffu, rescan)) {  // the same rows as pass 1, one per lane per call
+        const int lane = static_cast<int>(threadIdx.x & 31u);
+        for (int i = wid; i < nact; i += nwarps) {
+            const int si = sup.act[i];
+            const int b = sup.begin[si], e = sup.begin[si + 1];
+            for (int r0 = b; r0 < e; r0 += 32) {
+                const int r = r0 + lane;
+                unsigned xs[8] = {rescan && r < e ? base[r] : sp, sp, sp, sp, sp, sp, sp, sp};
+                double sc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+                unsigned tk = 0;
+                const float ub = ub_pair(Wf, xs[0]);
+                if (ub > 0.0f && ub >= LB_f) {
+                    sc[0] = __dadd_rn(W[xs[0] & 0xFFFFu], W[xs[0] >> 16]);
+                    if (sc[0] > 0.0 && sc[0] >= LB) tk = 1u;
+                }
+                emit(xs, sc, tk, pos0 + r, 0);
+            }
+        }
+    } else if (__any_sync(0xffffffffu, rescan)) {
         const long long nq2 = (nq + 2 * B - 1) / (2 * B) * (2 * B);
         for (long long p0 = threadIdx.x; p0 < nq2; p0 += 2 * B) {
             const uint4 v0 = rescan && p0 < nq ? base4[p0] : padv;
@@ -754,6 +827,18 @@ __global__ void __launch_bounds__(kMThreads, 1) mcts_kernel(const __grid_constan
     }
     const unsigned sent16 = static_cast<unsigned>(n * M.PP);
     const uint64_t hiS = static_cast<uint64_t>(sent16 | (sent16 << 16)) << 32;
+    int* sbeg = nullptr;
+    unsigned short* ssvc = nullptr;
+    int* sact = nullptr;
+    const int nsup = L.n_sup;
+    if (nsup) {  // supports of the base pool (C == 1: the slice is the whole pool)
+        sbeg = reinterpret_cast<int*>(carve(sizeof(int) * (nsup + 1)));
+        ssvc = reinterpret_cast<unsigned short*>(carve(sizeof(unsigned short) * nsup));
+        sact = reinterpret_cast<int*>(carve(sizeof(int) * nsup));
+        for (int i = threadIdx.x; i <= nsup; i += blockDim.x) sbeg[i] = L.sup_begin[i];
+        for (int i = threadIdx.x; i < nsup; i += blockDim.x) ssvc[i] = L.sup_svc[i];
+    }
+    const SupTab sup{nsup, sbeg, ssvc, sact};
     for (int e = threadIdx.x; e < nW; e += blockDim.x) {
         Us[e] = __ldg(&M.U[e]);
         csvc[e] = static_cast<unsigned char>(e / M.PP);  // service of a code (n for the sentinel row)
@@ -779,7 +864,7 @@ __global__ void __launch_bounds__(kMThreads, 1) mcts_kernel(const __grid_constan
             __syncthreads();
             int sc = 0;
             const int got = pair ? block_topk_pair(M, L.keyrank, slice32, hi - lo, lo, cur, s_usemask ? s_mask : nullptr, K, Us, W, Wf,
-                                                   hitc, cand, win, nullptr, &sc, L.timers != 0)
+                                                   hitc, cand, win, nullptr, &sc, L.timers != 0, SupTab{})
                                  : block_topk_bound(M, L.keyrank, slice, hi - lo, lo, cur, s_usemask ? s_mask : nullptr, K, Us, W, Wf,
                                              hitc, cand, win, nullptr, &sc, L.timers != 0);
             if (threadIdx.x == 0) {
@@ -795,7 +880,7 @@ __global__ void __launch_bounds__(kMThreads, 1) mcts_kernel(const __grid_constan
         if (C == 1) {  // one CTA: its own top-K is the answer (no merge, no cluster barriers)
             __syncthreads();
             return pair ? block_topk_pair(M, L.keyrank, slice32, hi - lo, lo, cur, usemask ? s_mask : nullptr, K, Us, W,
-                                          Wf, hitc, cand, win, out, scored, L.timers != 0)
+                                          Wf, hitc, cand, win, out, scored, L.timers != 0, sup)
                         : block_topk_bound(M, L.keyrank, slice, hi - lo, lo, cur, usemask ? s_mask : nullptr, K, Us,
                                         W, Wf, hitc, cand, win, out, scored, L.timers != 0);
         }
@@ -804,7 +889,7 @@ __global__ void __launch_bounds__(kMThreads, 1) mcts_kernel(const __grid_constan
         cl.sync();
         int sc = 0;
         const int got0 = pair ? block_topk_pair(M, L.keyrank, slice32, hi - lo, lo, cur, usemask ? s_mask : nullptr, K, Us, W, Wf,
-                                                hitc, cand, win, nullptr, &sc, L.timers != 0)
+                                                hitc, cand, win, nullptr, &sc, L.timers != 0, SupTab{})
                                : block_topk_bound(M, L.keyrank, slice, hi - lo, lo, cur, usemask ? s_mask : nullptr, K, Us, W, Wf, hitc,
                                           cand, win, nullptr, &sc, L.timers != 0);
         if (threadIdx.x == 0) {
@@ -1258,7 +1343,8 @@ __global__ void __launch_bounds__(kMThreads, 1) mcts_kernel(const __grid_constan
 }
 
 // Dynamic shared memory of mcts_kernel (must mirror its carve order).
-size_t mcts_smem_bytes(int n, int PP, int max_nodes, long long n_base, bool node_smem, bool rows_smem, bool pair) {
+size_t mcts_smem_bytes(int n, int PP, int max_nodes, long long n_base, bool node_smem, bool rows_smem, bool pair,
+                       int n_sup) {
     // n_base: rows of ONE rank's slice
     const size_t nW = static_cast<size_t>(n + 1) * PP;
     size_t off = 0;
@@ -1277,6 +1363,11 @@ size_t mcts_smem_bytes(int n, int PP, int max_nodes, long long n_base, bool node
         carve(static_cast<size_t>(max_nodes));
     }
     if (rows_smem) carve((pair ? 4 : 8) * static_cast<size_t>(n_base));
+    if (n_sup) {  // support offsets, services, the active list
+        carve(4 * static_cast<size_t>(n_sup + 1));
+        carve(2 * static_cast<size_t>(n_sup));
+        carve(4 * static_cast<size_t>(n_sup));
+    }
     return off;
 }
 void mcts_read_topk_timers(unsigned long long* h) { cudaMemcpyFromSymbol(h, g_tk, sizeof g_tk); }
