@@ -457,20 +457,19 @@ __device__ __noinline__ int block_topk_pair(const DevModel& M, const unsigned* k
         Wf[e] = __double2float_ru(w);
         if (mask) hitc[e] = svc < M.n && ((mask[svc >> 6] >> (svc & 63)) & 1ull) != 0;
     }
+    __shared__ int s_nact;
     if (threadIdx.x == 0) {
         t_fbits = 0u;
         n_cand = 0;
         n_hit = 0;
+        s_nact = 0;
     }
     __syncthreads();
     // Supports that can hold a candidate: a member with need > 0 (rows of the others all score
     // 0), or, with a mask, a sampled member (every row of such a support touches it).
-    __shared__ int s_nact;
     const bool bysup = sup.n > 0;
     const int wid = static_cast<int>(threadIdx.x >> 5), nwarps = static_cast<int>(blockDim.x >> 5);
     if (bysup) {
-        if (threadIdx.x == 0) s_nact = 0;
-        __syncthreads();
         int hitrows = 0;
         for (int s0 = 0; s0 < sup.n; s0 += blockDim.x) {
             const int si = s0 + static_cast<int>(threadIdx.x);
