@@ -283,6 +283,11 @@ struct RolloutArgs {
     long long* path;        // host-mapped: winner replay (base-pool indices), max_depth
     int* path_len;          // host-mapped
     int* lengths;           // optional, n_roll: steps (capped: max_depth, empty pool: -1)
+    // the base pool's supports (pair pools): a pool build scans only supports with a member
+    // whose need is > 0 (0: scan every row)
+    int n_sup;
+    const int* sup_begin;
+    const unsigned short* sup_svc;
     double comp0[256];      // start completion (travels with the launch)
 };
 

@@ -27,7 +27,7 @@ int topk1_rows_per_cta();
 int topk1_max_ctas();
 constexpr int kTopkMaxCtas = 4096;  // partial-list capacity (Best x 32 per CTA)
 const void* topk1_kernel_ptr(int km);
-size_t rollout_smem_bytes(int n, int PP);
+size_t rollout_smem_bytes(int n, int PP, int n_sup);
 size_t mcts_smem_bytes(int n, int PP, int max_nodes, long long n_base, bool node_smem, bool rows_smem, bool pair,
                        int n_sup);
 const void* bf_kernel_ptr();
@@ -200,7 +200,7 @@ Engine::Engine(const Rules& rules, std::map<std::string, ModelProfile> profiles,
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&greedy_blocks_per_sm_, greedy_kernel_ptr(), T, gsm));
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&topk_blocks_per_sm_, topk_kernel_ptr(), T, tsm));
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&rollout_blocks_per_sm_, rollout_kernel_ptr(m_.n), rollout_threads(),
-                                                     rollout_smem_bytes(m_.n, m_.PP)));
+                                                     rollout_smem_bytes(m_.n, m_.PP, max_sup())));
     if (greedy_blocks_per_sm_ < 1 || topk_blocks_per_sm_ < 1 || rollout_blocks_per_sm_ < 1)
         throw DeviceError("kernel does not fit on an SM");
 
@@ -1024,6 +1024,10 @@ RolloutResult Engine::rollouts(const std::vector<double>& comp, long long n_roll
     a.path_len = &ho->path_len;
     int* d_len = lengths ? static_cast<int*>(alloc(sizeof(int) * batch)) : nullptr;
     a.lengths = d_len;
+    if (max_sup() > 0) support_tables();
+    a.n_sup = n_sup_ > 0 && n_sup_ <= max_sup() ? n_sup_ : 0;
+    a.sup_begin = a.n_sup ? d_sup_begin_ : nullptr;
+    a.sup_svc = a.n_sup ? d_sup_svc_ : nullptr;
     cudaStream_t st = nullptr;
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
@@ -1039,7 +1043,7 @@ RolloutResult Engine::rollouts(const std::vector<double>& comp, long long n_roll
         }
     } fs{st, e0, e1};
     const int G = num_sms_ * rollout_blocks_per_sm_;
-    const size_t smem = rollout_smem_bytes(n, m_.PP);
+    const size_t smem = rollout_smem_bytes(n, m_.PP, max_sup());
 
     for (int attempt = 0;; ++attempt) {
         const size_t cap = size_t{1} << L2;

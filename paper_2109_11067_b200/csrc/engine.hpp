@@ -206,6 +206,11 @@ class Engine {
     const int* d_sup_begin_ = nullptr;
     const unsigned short* d_sup_svc_ = nullptr;
     void support_tables();
+    // supports the pool-build scans may list (pair pools), for shared-memory sizing
+    int max_sup() const {
+        const long long ns = m_.n + static_cast<long long>(m_.n) * (m_.n - 1) / 2;  // <= 2-member supports
+        return m_.max_mix <= 2 && ns <= 4096 ? static_cast<int>(ns) : 0;
+    }
     int greedy_interleave(int G) const;
     std::vector<double> min_u_;  // smallest positive utility per service (step bound)
     long long ext_bound_ = 0;

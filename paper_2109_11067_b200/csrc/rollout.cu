@@ -116,7 +116,7 @@ __device__ __forceinline__ unsigned add_row(const DevModel& M, uint64_t row, dou
 // per-warp K-th lane maxima, parallel rank of the rows >= T (topk.cu), exact k-round
 // fallback when ties at T overflow the candidate buffer.  Writes pool[0..got), returns got.
 __device__ int block_topk(const RolloutArgs& a, const double* comp, double* W, Cand* cand, Cand* win,
-                          unsigned* pool_out) {
+                          unsigned* pool_out, int* sact) {
     const DevModel& M = a.M;
     __shared__ unsigned long long t_bits;
     __shared__ int n_cand;
@@ -132,33 +132,73 @@ __device__ int block_topk(const RolloutArgs& a, const double* comp, double* W, C
         }
         W[e] = w;
     }
+    __shared__ int s_nact;
     if (threadIdx.x == 0) {
         t_bits = 0ull;
         n_cand = 0;
+        s_nact = 0;
     }
     __syncthreads();
+    // pair pools: only supports with a member whose need is > 0 can hold a row scoring > 0
+    const bool bysup = a.n_sup > 0;
+    const int lane = static_cast<int>(threadIdx.x & 31u), wid = static_cast<int>(threadIdx.x >> 5);
+    const int nwarps = static_cast<int>(blockDim.x >> 5);
+    if (bysup) {
+        for (int s0 = 0; s0 < a.n_sup; s0 += blockDim.x) {
+            const int si = s0 + static_cast<int>(threadIdx.x);
+            bool live = false;
+            if (si < a.n_sup) {
+                const unsigned e = __ldg(&a.sup_svc[si]);
+                const int sa = static_cast<int>(e & 0xFFu), sb = static_cast<int>(e >> 8);
+                live = comp[sa] < 1.0 || (sb != 0xFF && comp[sb] < 1.0);
+            }
+            const unsigned bm = __ballot_sync(0xffffffffu, live);
+            int at = 0;
+            if (lane == 0 && bm) at = atomicAdd(&s_nact, __popc(bm));
+            at = __shfl_sync(0xffffffffu, at, 0) + __popc(bm & lanemask_lt());
+            if (live) sact[at] = si;
+        }
+        __syncthreads();
+    }
+    const int nact = bysup ? s_nact : 0;
     double tmax = 0.0;
-    for (long long i = threadIdx.x; i < a.n_base; i += blockDim.x) tmax = fmax(tmax, row_score(W, __ldg(a.base + i)));
+    if (bysup) {  // a warp per active support, lanes over its rows
+        for (int i = wid; i < nact; i += nwarps) {
+            const int si = sact[i];
+            const int b = __ldg(&a.sup_begin[si]), e = __ldg(&a.sup_begin[si + 1]);
+            for (int r = b + lane; r < e; r += 32) tmax = fmax(tmax, row_score(W, __ldg(a.base + r)));
+        }
+    } else {
+        for (long long i = threadIdx.x; i < a.n_base; i += blockDim.x) tmax = fmax(tmax, row_score(W, __ldg(a.base + i)));
+    }
     const double tw = warp_kth(tmax, k);
     if ((threadIdx.x & 31u) == 0) atomicMax(&t_bits, static_cast<unsigned long long>(__double_as_longlong(tw)));
     __syncthreads();
     const double T = __longlong_as_double(static_cast<long long>(t_bits));
-    for (long long i0 = 0; i0 < a.n_base; i0 += blockDim.x) {
-        const long long i = i0 + threadIdx.x;
+    auto push = [&](bool valid, long long i) {  // warp-collective: the rows reaching T
         uint64_t row = 0;
         double s = 0.0;
-        if (i < a.n_base) {
+        if (valid) {
             row = __ldg(a.base + i);
             s = row_score(W, row);
         }
-        const bool take = i < a.n_base && s > 0.0 && s >= T;
+        const bool take = valid && s > 0.0 && s >= T;
         const unsigned b = __ballot_sync(0xffffffffu, take);
         if (b) {
             int at = 0;
-            if ((threadIdx.x & 31u) == 0) at = atomicAdd(&n_cand, __popc(b));
+            if (lane == 0) at = atomicAdd(&n_cand, __popc(b));
             at = __shfl_sync(0xffffffffu, at, 0) + __popc(b & lanemask_lt());
             if (take && at < kRCandCap) cand[at] = Cand{s, row_usum(M.U, row), row, i};
         }
+    };
+    if (bysup) {
+        for (int i = wid; i < nact; i += nwarps) {
+            const int si = sact[i];
+            const int b = __ldg(&a.sup_begin[si]), e = __ldg(&a.sup_begin[si + 1]);
+            for (int r0 = b; r0 < e; r0 += 32) push(r0 + lane < e, r0 + lane);
+        }
+    } else {
+        for (long long i0 = 0; i0 < a.n_base; i0 += blockDim.x) push(i0 + threadIdx.x < a.n_base, i0 + threadIdx.x);
     }
     __syncthreads();
     const int nc = n_cand;
@@ -213,6 +253,7 @@ __global__ void __launch_bounds__(kRThreads, 2) rollout_kernel(const __grid_cons
     double* comp_s = W + (n + 1) * M.PP;
     Cand* cand = reinterpret_cast<Cand*>(comp_s + n + 1);
     Cand* win = cand + kRCandCap;
+    int* sact = reinterpret_cast<int*>(win + kRMaxK);  // active supports of a pool build (a.n_sup)
     __shared__ long long wbuf[kRWarps][32];  // per-warp survivor buffer (one atomic per 32 pushes)
     __shared__ unsigned long long c_steps, c_done, c_cap, c_fail;
     const int lane = static_cast<int>(threadIdx.x & 31u);
@@ -334,7 +375,7 @@ __global__ void __launch_bounds__(kRThreads, 2) rollout_kernel(const __grid_cons
             const long long r = static_cast<long long>(__ldcg(&a.claimer[slot]));
             for (int i = threadIdx.x; i < n; i += blockDim.x) comp_s[i] = __ldcg(&a.comp[r * n + i]);
             __syncthreads();
-            const int got = block_topk(a, comp_s, W, cand, win, a.pool + static_cast<size_t>(slot) * a.k);
+            const int got = block_topk(a, comp_s, W, cand, win, a.pool + static_cast<size_t>(slot) * a.k, sact);
             if (threadIdx.x == 0) a.pool_n[slot] = got;
             __syncthreads();
         }
@@ -385,8 +426,9 @@ __global__ void __launch_bounds__(kRThreads, 2) rollout_kernel(const __grid_cons
     }
 }
 
-size_t rollout_smem_bytes(int n, int PP) {
-    return static_cast<size_t>((n + 1) * PP + n + 1) * 8 + static_cast<size_t>(kRCandCap + kRMaxK) * sizeof(Cand);
+size_t rollout_smem_bytes(int n, int PP, int n_sup) {
+    return static_cast<size_t>((n + 1) * PP + n + 1) * 8 + static_cast<size_t>(kRCandCap + kRMaxK) * sizeof(Cand) +
+           sizeof(int) * static_cast<size_t>(n_sup);
 }
 const void* rollout_kernel_ptr(int n) {
     return n <= 64 ? reinterpret_cast<const void*>(&rollout_kernel<2>) : reinterpret_cast<const void*>(&rollout_kernel<kMaxJ>);
