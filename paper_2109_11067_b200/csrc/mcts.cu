@@ -457,17 +457,18 @@ __device__ __noinline__ int block_topk_pair(const DevModel& M, const unsigned* k
         Wf[e] = __double2float_ru(w);
         if (mask) hitc[e] = svc < M.n && ((mask[svc >> 6] >> (svc & 63)) & 1ull) != 0;
     }
-    __shared__ int s_nact;
+    __shared__ int s_nact, s_actrows;
     if (threadIdx.x == 0) {
         t_fbits = 0u;
         n_cand = 0;
         n_hit = 0;
         s_nact = 0;
+        s_actrows = 0;
     }
     __syncthreads();
     // Supports that can hold a candidate: a member with need > 0 (rows of the others all score
     // 0), or, with a mask, a sampled member (every row of such a support touches it).
-    const bool bysup = sup.n > 0;
+    bool bysup = sup.n > 0;
     const int wid = static_cast<int>(threadIdx.x >> 5), nwarps = static_cast<int>(blockDim.x >> 5);
     if (bysup) {
         int hitrows = 0;
@@ -492,11 +493,12 @@ __device__ __noinline__ int block_topk_pair(const DevModel& M, const unsigned* k
                 hitrows += sup.begin[si + 1] - sup.begin[si];
             }
         }
-        if (mask) {
-            for (int off = 16; off > 0; off >>= 1) hitrows += __shfl_xor_sync(0xffffffffu, hitrows, off);
-            if ((threadIdx.x & 31u) == 0) atomicAdd(&n_hit, hitrows);
-        }
+        for (int off = 16; off > 0; off >>= 1) hitrows += __shfl_xor_sync(0xffffffffu, hitrows, off);
+        if ((threadIdx.x & 31u) == 0) atomicAdd(&s_actrows, hitrows);
         __syncthreads();
+        // most rows live: the dense 4-rows-per-load scan is cheaper than a warp per support
+        if (10ll * s_actrows > 6ll * nb) bysup = false;
+        if (bysup && mask && threadIdx.x == 0) n_hit = s_actrows;  // (the dense scan counts its hits)
     }
     const int nact = bysup ? s_nact : 0;
     mark(0);
