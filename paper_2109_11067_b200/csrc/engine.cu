@@ -353,6 +353,17 @@ Engine::Engine(const Rules& rules, std::map<std::string, ModelProfile> profiles,
     ext_bound_ = static_cast<long long>(std::min<long double>(eb, 1ll << 31)) + 64;
 }
 
+// Working-set bound of a plan started from `comp`: the base pool plus every extension support
+// over the services still unsatisfied there (an extension only ever adds supports inside the
+// unsatisfied set, greedy.hpp:107-119).
+long long Engine::working_set_bound(const double* comp) const {
+    int u = 0;
+    for (int i = 0; i < m_.n; ++i) u += comp[i] < 1.0 - kSatisfyEps ? 1 : 0;
+    long double eb = 0;
+    for (int k = m_.max_mix + 1; k <= kRowK; ++k) eb += static_cast<long double>(binom(u, k)) * m_.templates[k].size();
+    return pool_size() + static_cast<long long>(std::min<long double>(eb, 1ll << 40));
+}
+
 const unsigned* Engine::keyrank() {
     std::call_once(keyrank_once_, [&] {
         const long long P = static_cast<long long>(base_rows_.size());
@@ -714,12 +725,14 @@ int Engine::greedy_interleave(int G) const {
 // CTAs per instance in cluster mode (0: cooperative).  Cluster mode when the working set
 // stays small: the base pool plus the extension bound (bench.hpp-style closed form) under
 // kClusterRows; MIGPLAN_GREEDY_CLUSTER=0 disables it, =k forces k CTAs.
-int Engine::greedy_cluster_ctas(size_t smem) const {
+int Engine::greedy_cluster_ctas(size_t smem, long long rows_bound) const {
     if (n_ranks_ > 1) return 0;
     constexpr long long kClusterRows = 256ll << 10;
-    int want = pool_size() + ext_bound_ <= kClusterRows ? 16 : 0;
+    if (rows_bound < 0) rows_bound = pool_size() + ext_bound_;
+    int want = rows_bound <= kClusterRows ? 16 : 0;
     const char* v = std::getenv("MIGPLAN_GREEDY_CLUSTER");
     if (v) want = std::max(0, std::min(16, std::atoi(v)));
+    if (want == 0) return 0;
     const bool cacheable = !v;
     if (cacheable && cluster_ctas_ >= 0) return cluster_ctas_;  // the occupancy query is per context
     auto done = [&](int r) {
@@ -786,7 +799,7 @@ void Engine::fast_algo_group(const std::vector<Engine*>& es, const std::vector<d
     int G = e0->num_sms_ * e0->greedy_blocks_per_sm_ / P;
     if (e0->max_ctas_ > 0) G = std::min(G, e0->max_ctas_);
     if (const char* v = std::getenv("MIGPLAN_GREEDY_CTAS")) G = std::max(1, std::min(G, std::atoi(v)));
-    const int GC = P == 1 ? e0->greedy_cluster_ctas(smem) : 0;
+    const int GC = P == 1 ? e0->greedy_cluster_ctas(smem, e0->working_set_bound(comp.data())) : 0;
     if (GC) G = GC;
     Slot* s0 = calls[0].s;
     for (int attempt = 0;; ++attempt) {
@@ -1132,7 +1145,8 @@ RolloutResult Engine::rollouts(const std::vector<double>& comp, long long n_roll
 // (FastProcedure, greedy.hpp:160-164) from `count` device-resident completion vectors.
 // n_steps[i] = plan length, or -1 when fast_algo raised PlanningError (no positive score)
 // or the plan would exceed cap_steps.  rows[i] = device pointer to the picked rows.
-void Engine::greedy_batch(const double* d_comps, int count, long long cap_steps, std::vector<const uint64_t*>& rows,
+void Engine::greedy_batch(const double* d_comps, int count, long long cap_steps, long long rows_bound,
+                          std::vector<const uint64_t*>& rows,
                           std::vector<int>& n_steps, std::vector<std::vector<uint64_t>>* host_rows) {
     rows.assign(count, nullptr);
     n_steps.assign(count, -1);
@@ -1153,7 +1167,7 @@ void Engine::greedy_batch(const double* d_comps, int count, long long cap_steps,
         // the SMs are split between the instances (each a complete fast_algo on its CTAs)
         int gpc = std::max(1, num_sms_ * greedy_blocks_per_sm_ / nb);
         if (const char* v = std::getenv("MIGPLAN_GREEDY_CTAS")) gpc = std::max(1, std::min(gpc, std::atoi(v)));
-        const int GC = greedy_cluster_ctas(smem);
+        const int GC = greedy_cluster_ctas(smem, rows_bound);
         if (GC && GC * nb <= num_sms_) gpc = GC;
         std::unique_ptr<GreedyLaunch> L(new GreedyLaunch{});
         L->n_groups = nb;
@@ -1460,7 +1474,9 @@ void Engine::fast_algo_batch(const std::vector<std::vector<double>>& comps, std:
     stats.h2d += static_cast<long long>(sizeof(double) * flat.size());
     std::vector<const uint64_t*> drows;
     std::vector<int> steps;
-    greedy_batch(d, count, cap_steps, drows, steps, &rows);
+    long long wsb = 0;
+    for (const auto& c : comps) wsb = std::max(wsb, working_set_bound(c.data()));
+    greedy_batch(d, count, cap_steps, wsb, drows, steps, &rows);
     for (int i = 0; i < count; ++i)
         if (steps[i] < 0) status[i] = 1;
 }
@@ -1700,7 +1716,7 @@ void Engine::ga_generation(GaRun* r, int buf, const std::vector<int>& parent_len
     // refill every child's residual with the device greedy, all children in one launch
     std::vector<const uint64_t*> rows;
     std::vector<int> steps;
-    greedy_batch(r->residual, npar, r->L_cap, rows, steps);
+    greedy_batch(r->residual, npar, r->L_cap, -1, rows, steps);
     std::vector<int> ns(npar);
     CK(cudaMemcpy(ns.data(), r->n_surv, sizeof(int) * npar, cudaMemcpyDeviceToHost));
     for (int i = 0; i < npar; ++i)

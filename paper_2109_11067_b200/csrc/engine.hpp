@@ -147,7 +147,8 @@ class Engine {
     std::vector<Config> brute_force(int cap, long long node_budget, bool& found);
 
     // Independent single-CTA greedy instances in one launch (the GA's refills).
-    void greedy_batch(const double* d_comps, int count, long long cap_steps, std::vector<const uint64_t*>& rows,
+    void greedy_batch(const double* d_comps, int count, long long cap_steps, long long rows_bound,
+                      std::vector<const uint64_t*>& rows,
                       std::vector<int>& n_steps, std::vector<std::vector<uint64_t>>* host_rows = nullptr);
     void fast_algo_batch(const std::vector<std::vector<double>>& comps, std::vector<std::vector<uint64_t>>& rows,
                          std::vector<int>& status);
@@ -197,7 +198,8 @@ class Engine {
     std::unique_ptr<Scratch> keyrank_buf_;
     std::once_flag keyrank_once_;
     const unsigned* keyrank();
-    int greedy_cluster_ctas(size_t smem) const;  // 0: cooperative launch
+    int greedy_cluster_ctas(size_t smem, long long rows_bound = -1) const;  // 0: cooperative launch
+    long long working_set_bound(const double* comp) const;
     mutable int cluster_ctas_ = -1;              // its cached answer (no env override)
     // base-pool supports for the MCTS top-K (built on first use; pair pools only)
     std::once_flag sup_once_;
