@@ -200,7 +200,7 @@ class Engine {
     const unsigned* keyrank();
     int greedy_cluster_ctas(size_t smem, long long rows_bound = -1) const;  // 0: cooperative launch
     long long working_set_bound(const double* comp) const;
-    mutable int cluster_ctas_ = -1;              // its cached answer (no env override)
+    mutable std::atomic<int> cluster_ctas_{-1};  // its cached answer (no env override)
     // base-pool supports for the MCTS top-K (built on first use; pair pools only)
     std::once_flag sup_once_;
     std::unique_ptr<Scratch> sup_buf_;
