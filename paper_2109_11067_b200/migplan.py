@@ -188,8 +188,14 @@ def slack_of(comp: Sequence[float]) -> float:  # core.hpp:232-236
     return s
 
 
+def _config_sort_key(c: GpuConfig) -> tuple:
+    """The GpuConfig order (core.hpp:174-200) as plain tuples: the same lexicographic order as
+    the dataclass comparison (instances by placement, service id, batch), without its cost."""
+    return tuple((i.placement.slices, i.placement.start_slot, i.service_id, i.batch) for i in c.instances)
+
+
 def make_deployment(configs: Iterable[GpuConfig], prefix: str = "gpu-") -> Deployment:  # core.hpp:305-312
-    cfgs = sorted(configs)
+    cfgs = sorted(configs, key=_config_sort_key)
     return Deployment([DeployedGpu(f"{prefix}{i}", c) for i, c in enumerate(cfgs)])
 
 
@@ -611,6 +617,34 @@ class PlanContext:
                                                 self.services[c.inst[k].service].service_id, c.inst[k].batch)
                                for k in range(c.n_instances)))
 
+    def _configs_from_buf(self, buf, n: int) -> list[GpuConfig]:
+        """n ConfigC records at once: one unpack of the raw ints; within the call, repeated
+        instances and configurations share one immutable object (plans repeat configurations)."""
+        if n <= 0:
+            return []
+        w = C.sizeof(abi.ConfigC) // 4
+        ints = memoryview(buf).cast("B")[: n * w * 4].cast("i").tolist()
+        icache, ccache = {}, {}
+        ids = [sv.service_id for sv in self.services]
+        out = []
+        for i in range(n):
+            b = i * w
+            k = ints[b]
+            key = tuple(ints[b + 1: b + 1 + 4 * k])
+            g = ccache.get(key)
+            if g is None:
+                insts = []
+                for j in range(k):
+                    o = b + 1 + 4 * j
+                    ik = (ints[o], ints[o + 1], ints[o + 2], ints[o + 3])
+                    inst = icache.get(ik)
+                    if inst is None:
+                        inst = icache[ik] = AssignedInstance(Placement(ik[0], ik[1]), ids[ik[2]], ik[3])
+                    insts.append(inst)
+                g = ccache[key] = GpuConfig(tuple(insts))
+            out.append(g)
+        return out
+
     def _config_to_c(self, g: GpuConfig, out: abi.ConfigC) -> None:
         if len(g.instances) > abi.MAX_INST:
             raise PlanningError("config has more than 7 instances")
@@ -658,7 +692,7 @@ def _run_plan(ctx: PlanContext, call) -> list[GpuConfig]:
             cap = n.value
             continue
         ctx.backend.check(rc)
-        return [ctx._config_from_c(buf[i]) for i in range(n.value)]
+        return ctx._configs_from_buf(buf, n.value)
 
 
 # ---------------------------------------------------------------- greedy (greedy.hpp)
