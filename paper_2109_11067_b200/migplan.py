@@ -683,7 +683,7 @@ def make_plan_context(services, profiles, rules, max_mix: int = 2, backend=None,
 
 
 def _run_plan(ctx: PlanContext, call) -> list[GpuConfig]:
-    cap = 1024  # grown to the exact size when a plan is longer (MIG_ERR_ARGUMENT + n_out)
+    cap = 4096  # a longer plan is re-run with the exact size (MIG_ERR_ARGUMENT + n_out)
     while True:
         buf = (abi.ConfigC * cap)()
         n = C.c_int32()
