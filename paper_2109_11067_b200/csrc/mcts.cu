@@ -1146,7 +1146,8 @@ __global__ void __launch_bounds__(kMThreads, 1) mcts_kernel(const __grid_constan
                     // when the block needs it: a miss's top-K, or the end of the rollout)
                     const bool regc = n <= 32;
                     double creg = regc && lane < n ? cur[lane] : 2.0;
-                    int r_steps = s_steps;  // lane 0's step count (written back when the walk pauses)
+                    int r_steps = 0;  // lane 0's step count (written back when the walk pauses)
+                    if (lane == 0) r_steps = *reinterpret_cast<volatile int*>(&s_steps);
                     if (lane == 0) s_miss = 0;
                     for (;;) {
                         if (g.idx >= 312) mt_twist_warp(g);  // the serial twist in mt_next stays the fallback
