@@ -26,6 +26,7 @@ using namespace dev;
 namespace {
 
 constexpr int kMThreads = 512;
+constexpr int kMaxServicesDev = 256;  // >= kMaxServices (model.hpp)
 constexpr int kMWarps = kMThreads / 32;
 constexpr int kMCandCap = 512;  // above-threshold rows per top-K (ties beyond: exact k-round path)
 constexpr int kMMaxK = 32;
@@ -935,6 +936,7 @@ __global__ void __launch_bounds__(kMThreads, 1) mcts_kernel(const __grid_constan
     __shared__ int s_edges, s_path, s_best, s_have, s_nodes, s_builds, s_iters, s_scored, s_expands;
     __shared__ long long s_expand_rows;
     __shared__ int s_out[kMMaxK];
+    __shared__ int s_unsat[kMaxServicesDev];  // expand: the node's unsatisfied services
     // on-chip level of the rollout cache: kL1Slots keys (filled to 3/4) with their pools
     __shared__ uint64_t l1_key[kL1Slots][4];
     __shared__ int l1_n[kL1Slots];
@@ -1047,14 +1049,17 @@ __global__ void __launch_bounds__(kMThreads, 1) mcts_kernel(const __grid_constan
             }
         } else {
             if (s_expand) {  // expand (mcts.hpp:89-116)
-                if (warp == 0) {  // unsatisfied services in order (ballot compaction), then lane 0's shuffle
+                if (warp == 0) {  // the node's completion into `cur`, its unsatisfied services in order
+                    // (ballot compaction, on chip), then lane 0's partial Fisher-Yates
                     const double* nc = a.node_comp + static_cast<long long>(s_node) * n;
                     int m = 0;
                     for (int i0 = 0; i0 < n; i0 += 32) {
                         const int i = i0 + lane;
-                        const bool u = i < n && nc[i] < 1.0 - 1e-9;
+                        const double v = i < n ? nc[i] : 2.0;
+                        if (i < n) cur[i] = v;
+                        const bool u = i < n && v < 1.0 - 1e-9;
                         const unsigned bm = __ballot_sync(0xffffffffu, u);
-                        if (u) a.unsat[m + __popc(bm & lanemask_lt())] = i;
+                        if (u) s_unsat[m + __popc(bm & lanemask_lt())] = i;
                         m += __popc(bm);
                     }
                     __syncwarp();
@@ -1062,16 +1067,15 @@ __global__ void __launch_bounds__(kMThreads, 1) mcts_kernel(const __grid_constan
                         const int take = min(L.pick_services, m);
                         for (int i = 0; i < take; ++i) {
                             const int j = i + static_cast<int>(mt_pick(g, static_cast<uint64_t>(m - i)));
-                            const int t = a.unsat[i];
-                            a.unsat[i] = a.unsat[j];
-                            a.unsat[j] = t;
+                            const int t = s_unsat[i];
+                            s_unsat[i] = s_unsat[j];
+                            s_unsat[j] = t;
                         }
                         for (int w = 0; w < 4; ++w) s_mask[w] = 0;
-                        for (int i = 0; i < take; ++i) s_mask[a.unsat[i] >> 6] |= 1ull << (a.unsat[i] & 63);
+                        for (int i = 0; i < take; ++i) s_mask[s_unsat[i] >> 6] |= 1ull << (s_unsat[i] & 63);
                         s_take = take;
                     }
                 }
-                for (int i = tid; i < n; i += blockDim.x) cur[i] = a.node_comp[static_cast<long long>(s_node) * n + i];
                 __syncthreads();
                 tick(t_exp);
                 const int got = s_take > 0 ? cluster_topk(true, s_out, &s_scored) : 0;
@@ -1087,16 +1091,18 @@ __global__ void __launch_bounds__(kMThreads, 1) mcts_kernel(const __grid_constan
                     for (int q = warp; q < got; q += kMWarps) {
                         const int c = first + q;
                         double* cc = a.node_comp + static_cast<long long>(c) * n;
-                        for (int i = lane; i < n; i += 32) cc[i] = cur[i];
-                        __syncwarp();
-                        if (lane < 4) {  // members have distinct services: the adds commute
-                            const int code = static_cast<int>((rowat(s_out[q]) >> (16 * lane)) & 0xFFFFull);
-                            const int svc = csvc[code];
-                            if (svc < n) cc[svc] = __dadd_rn(cc[svc], Us[code]);
-                        }
-                        __syncwarp();
+                        const uint64_t row = rowat(s_out[q]);
                         bool uns = false;
-                        for (int i = lane; i < n; i += 32) uns |= cc[i] < 1.0 - 1e-9;
+                        for (int i = lane; i < n; i += 32) {  // parent + the config's utility (expand, mcts.hpp:109-113)
+                            double v = cur[i];
+#pragma unroll
+                            for (int m = 0; m < 4; ++m) {
+                                const int code = static_cast<int>((row >> (16 * m)) & 0xFFFFull);
+                                if (csvc[code] == i) v = __dadd_rn(v, Us[code]);
+                            }
+                            cc[i] = v;
+                            uns |= v < 1.0 - 1e-9;
+                        }
                         const bool sat = !__any_sync(0xffffffffu, uns);
                         if (lane == 0) {
                             ncand[c] = s_out[q];
