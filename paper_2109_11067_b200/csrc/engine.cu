@@ -592,8 +592,10 @@ struct GreedyCall {
     GreedyArgs a{};
 };
 
-void Engine::greedy_prepare(GreedyCall& c, const double* comp_host, const double* comp_dev, long long cap_steps) {
+void Engine::greedy_prepare(GreedyCall& c, const double* comp_host, const double* comp_dev, long long cap_steps,
+                            cudaStream_t st) {
     Slot* s = c.s;
+    if (!st) st = s->stream;
     CK(cudaSetDevice(device_));
     if (s->cap_steps < cap_steps) {
         s->free_picks();
@@ -611,9 +613,9 @@ void Engine::greedy_prepare(GreedyCall& c, const double* comp_host, const double
     // capped at 3G rows (24 GB); the kernel reports overflow and the call is retried larger.
     ensure_ext(s, c.n_base + std::min<long long>(ext_bound_, 3ll << 30));
     if (comp_host) std::memcpy(s->io->comp, comp_host, sizeof(double) * m_.n);
-    CK(cudaMemsetAsync(s->st, 0, sizeof(GreedyState), s->stream));
+    CK(cudaMemsetAsync(s->st, 0, sizeof(GreedyState), st));
     // the working-set arena starts as a copy of the resident base pool (device to device)
-    if (c.n_base) CK(cudaMemcpyAsync(s->ext, c.base_src, c.n_base * 8, cudaMemcpyDeviceToDevice, s->stream));
+    if (c.n_base) CK(cudaMemcpyAsync(s->ext, c.base_src, c.n_base * 8, cudaMemcpyDeviceToDevice, st));
     GreedyArgs& a = c.a;
     a = GreedyArgs{};
     a.M = dm_;
@@ -1173,14 +1175,14 @@ void Engine::greedy_batch(const double* d_comps, int count, long long cap_steps,
         L->n_groups = nb;
         L->ctas_per_group = gpc;
         L->cluster = GC && GC * nb <= num_sms_ ? 1 : 0;
-        for (int i = 0; i < nb; ++i) {
+        for (int i = 0; i < nb; ++i) {  // every instance's set-up on the launch stream: no cross-stream waits
             calls[i].e = this;
             calls[i].s = acquire();
-            greedy_prepare(calls[i], nullptr, d_comps + static_cast<size_t>(b0 + i) * m_.n, cap_steps);
+            greedy_prepare(calls[i], nullptr, d_comps + static_cast<size_t>(b0 + i) * m_.n, cap_steps,
+                           calls[0].s->stream);
             calls[i].a.interleave = greedy_interleave(gpc);
             L->g[i] = calls[i].a;
         }
-        for (int i = 1; i < nb; ++i) CK(cudaStreamSynchronize(calls[i].s->stream));
         Slot* s0 = calls[0].s;
         CK(cudaEventRecord(s0->e0, s0->stream));
         launch_greedy(*L, T, smem, s0->stream);

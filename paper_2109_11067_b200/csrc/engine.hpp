@@ -176,7 +176,8 @@ class Engine {
     void release(Slot*);
     void ensure_ext(Slot* s, long long rows);
     long long step_bound(const std::vector<double>& comp) const;
-    void greedy_prepare(GreedyCall& c, const double* comp_host, const double* comp_dev, long long cap_steps);
+    void greedy_prepare(GreedyCall& c, const double* comp_host, const double* comp_dev, long long cap_steps,
+                        cudaStream_t st = nullptr);
     bool greedy_finish(GreedyCall& c, float ms, int attempt, std::vector<uint64_t>& rows, std::vector<double>& scores);
 
     Model m_;
