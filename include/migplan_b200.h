@@ -249,6 +249,11 @@ int mig_board_bytes(int32_t n_ranks, int64_t* bytes);
 int mig_board_alloc(int32_t device, int32_t n_ranks, void** board, uint8_t* ipc_handle /* 64 bytes, or NULL */);
 int mig_board_open(int32_t device, const uint8_t* ipc_handle /* 64 bytes */, void** board);
 int mig_board_free(void* board, int32_t opened /* 1: from mig_board_open */);
+/* Per-call device resources (streams, working-set arenas, pinned step buffers, scratch) are
+ * pooled per device for the process, so a new context reuses them.  This frees every pooled
+ * resource of `device` that no live call holds; the next call allocates cold.  CPU
+ * implementations: no-op. */
+int mig_device_cache_release(int32_t device);
 /* max_ctas > 0 caps the greedy grid of this context. */
 int mig_ctx_set_shard(mig_ctx* ctx, int32_t rank, int32_t n_ranks, void* const* boards, int32_t max_ctas);
 /* fast_algo on ALL ranks of a shard whose contexts share one GPU (ctxs in rank order):
@@ -354,6 +359,10 @@ typedef struct mig_stats {
 } mig_stats;
 int mig_ctx_stats(const mig_ctx* ctx, mig_stats* out);
 void mig_ctx_reset_stats(mig_ctx* ctx);
+/* Diagnostic: the working-set size (base pool + extension rows; this rank's share when
+ * sharded) scanned at each step of the most recent greedy plan completed on this context
+ * (greedy.hpp:123-134's ws.size()).  Writes min(cap, steps) values; *n_out = steps. */
+int mig_ctx_step_rows(const mig_ctx* ctx, int64_t* out, int32_t cap, int32_t* n_out);
 
 #ifdef __cplusplus
 }

@@ -194,8 +194,14 @@ def gen_ga_parallel(ref):
     cases = [("slos_day", ps, S.fixture_services("slos_day", ps), dict(seed=24, max_rounds=4)),
              ("slos_night", ps, S.fixture_services("slos_night", ps), dict(seed=5, max_rounds=4, population=8)),
              ("rand6", tw, sv6, dict(seed=9, max_rounds=5, mutation_pairs=3, erase_fraction=0.25)),
-             ("slos_24", ps, S.fixture_services("slos_24", ps), dict(seed=24, max_rounds=3))]
+             ("slos_24", ps, S.fixture_services("slos_24", ps), dict(seed=24, max_rounds=3)),
+             # population 20: from round 5 on, 10 children per generation (two refill batches of 8)
+             ("slos_day_p20", ps, S.fixture_services("slos_day", ps), dict(seed=7, max_rounds=7, population=20)),
+             ("slos_24_p20", ps, S.fixture_services("slos_24", ps), dict(seed=24, max_rounds=6, population=20))]
+    only = os.environ.get("GOLDEN_ONLY")
     for name, p, sv, kw in cases:
+        if only and name not in only.split(","):
+            continue
         t = time.time()
         logs = []
         dep = mp.two_phase_parallel(sv, p, mp.PartitionRuleSet.defaults(), mp.GaParams(time_budget_s=1e9, **kw),
@@ -290,7 +296,131 @@ def gen_baseline(ref):
     return res
 
 
-SECTIONS = {"baseline": gen_baseline, "brute_force": gen_brute_force, "greedy": gen_greedy, "mcts": gen_mcts, "ga": gen_ga, "topk": gen_topk, "partitions": gen_partitions,
+def gen_ga_big(ref):
+    """two_phase on the configs the headline claims are made on:
+    config #2 slos_24 (seed 24, P=16, MCTS budget 48, the c7 parameters with max_rounds
+    binding, acceptance.cpp:255-259) at 2 and 10 rounds, and config #3 gen(24, 8.7)."""
+    res = {}
+    ps = S.profiles()
+    slos = S.fixture_services("slos_24", ps)
+    p3, g3 = S.gen(24, 8.7)
+    cases = [("slos_24_r2", ps, slos, dict(seed=24, max_rounds=2)),
+             ("slos_24_r10", ps, slos, dict(seed=24, max_rounds=10)),
+             ("gen24_8.7_r2", p3, g3, dict(seed=4242, max_rounds=2))]
+    only = os.environ.get("GOLDEN_ONLY")
+    for name, p, sv, kw in cases:
+        if only and name not in only.split(","):
+            continue
+        params = mp.GaParams(time_budget_s=1e9, population=16, workers=min(os.cpu_count() or 1, 8),
+                             slow=mp.MctsParams(budget_iters=48), **kw)
+        logs = []
+        t = time.time()
+        dep = mp.two_phase(sv, p, mp.PartitionRuleSet.defaults(), params,
+                           log=lambda r: logs.append([r.round, r.best_gpus, S.fhex(r.best_slack), r.improved]),
+                           backend=ref)
+        plan = S.plan_key([g.config for g in dep.gpus])
+        res[name] = {"store": store_name(p), "services": svc_json(sv), "params": {**kw, "slow": 48, "population": 16},
+                     "plan": plan, "plan_sha": S.plan_sha(plan), "logs": logs,
+                     "ref_wall_s": round(time.time() - t, 2)}
+        print(f"ga_big {name}: {len(dep.gpus)} GPUs, {len(logs)} rounds ({time.time() - t:.1f}s)", flush=True)
+    return res
+
+
+def gen_mcts_big(ref):
+    """mcts_solve on config #4's gen(48, 7.0) with a bounded budget."""
+    p, sv = S.gen(48, 7.0)
+    budget, seed = int(os.environ.get("MCTS_BIG_BUDGET", "200")), 1
+    ctx = mp.make_plan_context(sv, p, mp.PartitionRuleSet.defaults(), backend=ref)
+    tr = []
+    t = time.time()
+    plan = mp.mcts_solve(mp.zero_completion(len(sv)), ctx, mp.MctsParams(budget_iters=budget), seed,
+                         trace=lambda *a: tr.append(list(a)))
+    print(f"mcts_big gen48_7.0: {len(plan)} GPUs ({time.time() - t:.1f}s)", flush=True)
+    return {"gen48_7.0": {"store": "fixture", "services": svc_json(sv), "budget": budget, "seed": seed,
+                          "plan": S.plan_key(plan), "trace": tr, "ref_wall_s": round(time.time() - t, 2)}}
+
+
+def gen_greedy_prefix(ref):
+    """gen(128, 8.0) (config #5): the reference's own fast_algo up to and including the
+    first two steps that scan the first extension (greedy.hpp:107-136; config_enum.hpp:206-211),
+    every pick and score bit, plus the instrumented replica's per-step working-set sizes
+    (VERDICT r1 item 1d).  The full plan is not completable on a CPU."""
+    import ctypes as C
+
+    p, sv = S.gen(128, 8.0)
+    ctx = mp.make_plan_context(sv, p, mp.PartitionRuleSet.defaults(), backend=ref)
+    trace = []
+    plan = []
+
+    def _tr(_u, it, cand, s, cp, nn):
+        c = ctx._cand_from_c(cand.contents)
+        plan.append(c.config)
+        trace.append([S.fhex(s), S.comp_digest(list(cp[:nn]))])
+
+    cb = abi_trace(_tr)
+    buf, n = ctx._comp(mp.zero_completion(len(sv)))
+    steps, ext_at = C.c_int32(), C.c_int32()
+    t = time.time()
+    ref.check(ref.lib.mig_ref_fast_algo_prefix(ctx._p, buf, n, -1, 2, cb, None, C.byref(steps), C.byref(ext_at)))
+    wall = time.time() - t
+    cap = steps.value + 1
+    sr = (C.c_int64 * cap)()
+    er = (C.c_int64 * 64)()
+    ns, ne = C.c_int32(), C.c_int32()
+    t2 = time.time()
+    ref.check(ref.lib.mig_ref_step_rows(ctx._p, buf, n, steps.value, sr, cap, C.byref(ns), er, 64, C.byref(ne)))
+    print(f"greedy_prefix gen128_8.0: {steps.value} steps, first extension after step {ext_at.value}, "
+          f"ext rows {list(er[:ne.value])} ({wall:.1f}s + {time.time() - t2:.1f}s)", flush=True)
+    return {"gen128_8.0": {"store": "fixture", "services": svc_json(sv), "pool_size": len(ctx.pool),
+                           "steps": steps.value, "first_ext_step": ext_at.value, "plan": S.plan_key(plan),
+                           "trace": trace, "step_rows": list(sr[:ns.value]), "ext_rows": list(er[:ne.value]),
+                           "ref_wall_s": round(wall, 2)}}
+
+
+def abi_trace(fn):
+    from paper_2109_11067_b200 import abi
+
+    return abi.GREEDY_TRACE(fn)
+
+
+def gen_pools_big(ref):
+    """Base-pool SET parity at n = 48 and n = 128 (config_enum.hpp:192-202): count, a digest of
+    the sorted canonical rows (configs, utility bits, util_sum bits), best_single_util bits."""
+    res = {}
+    for n, mu in ((48, 7.0), (128, 8.0)):
+        p, sv = S.gen(n, mu)
+        t = time.time()
+        ctx = mp.make_plan_context(sv, p, mp.PartitionRuleSet.defaults(), backend=ref)
+        res[f"gen{n}_{mu}"] = {"store": "fixture", "services": svc_json(sv), "pool_size": len(ctx.pool),
+                               "pool_sha": S.pool_sha(ctx),
+                               "best_single_util": [S.fhex(x) for x in ctx.pool.best_single_util]}
+        print(f"pools_big gen{n}_{mu}: {len(ctx.pool)} rows ({time.time() - t:.1f}s)", flush=True)
+    return res
+
+
+def gen_rollouts_big(ref):
+    """Root-parallel rollouts at config #4's gen(48, 7.0); max_depth
+    = 2 x the reference greedy's 372 GPUs (mcts.hpp:127)."""
+    p, sv = S.gen(48, 7.0)
+    res = {}
+    for name, kw in (("gen48_7.0", dict(n_rollouts=1024, seed=1, max_depth=744)),
+                     ("gen48_7.0_k4", dict(n_rollouts=512, seed=3, max_depth=744, topk=4))):
+        ctx = mp.make_plan_context(sv, p, mp.PartitionRuleSet.defaults(), backend=ref)
+        prm = mp.RolloutParams(**kw)
+        t = time.time()
+        r = mp.rollouts(mp.zero_completion(len(sv)), ctx, prm, lengths=True)
+        res[name] = {"store": "fixture", "services": svc_json(sv), "params": kw, "best_len": r.best_len,
+                     "best_id": r.best_id, "max_depth": r.max_depth, "keys": r.keys, "steps": r.steps,
+                     "rounds": r.rounds, "completed": r.completed, "capped": r.capped, "failed": r.failed,
+                     "lengths": r.lengths, "path": S.plan_key([ctx.pool[i].config for i in r.path]),
+                     "ref_wall_s": round(time.time() - t, 2)}
+        print(f"rollouts_big {name}: best {r.best_len}, keys {r.keys} ({time.time() - t:.1f}s)", flush=True)
+    return res
+
+
+SECTIONS = {"ga_big": gen_ga_big, "mcts_big": gen_mcts_big, "greedy_prefix": gen_greedy_prefix,
+            "pools_big": gen_pools_big, "rollouts_big": gen_rollouts_big,
+"baseline": gen_baseline, "brute_force": gen_brute_force, "greedy": gen_greedy, "mcts": gen_mcts, "ga": gen_ga, "topk": gen_topk, "partitions": gen_partitions,
             "greedy_big": gen_greedy_big, "rollouts": gen_rollouts, "ga_parallel": gen_ga_parallel}
 
 
@@ -301,7 +431,11 @@ def main(argv):
     for sec in argv or list(SECTIONS):
         t = time.time()
         data = SECTIONS[sec](ref)
-        with open(os.path.join(S.GOLDEN, f"{sec}.json"), "w") as f:
+        path = os.path.join(S.GOLDEN, f"{sec}.json")
+        if os.environ.get("GOLDEN_MERGE") and os.path.exists(path):  # regenerate some entries only
+            with open(path) as f:
+                data = {**json.load(f), **data}
+        with open(path, "w") as f:
             json.dump(data, f, separators=(",", ":"))
         print(f"wrote {sec}.json in {time.time() - t:.1f}s", flush=True)
 

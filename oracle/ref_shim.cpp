@@ -104,6 +104,8 @@ struct mig_ctx {
     PartitionRuleSet rules;
     std::vector<ServiceSpec> services;
     PlanContext plan;
+    std::vector<double> last_comp;  // start of the last mig_fast_algo (mig_ctx_step_rows replays it)
+    bool have_last = false;
 };
 
 struct mig_rng {
@@ -195,8 +197,12 @@ GaParams ga_of(const mig_ga_params* p) {
 
 // Instrumented replica of fast_algo's working-set growth (greedy.hpp:95-145), used
 // only to count rows scored for bench.py's reference arm; results equal fast_algo.
-int64_t count_rows(const CompletionRates& comp, const PlanContext& ctx) {
+// max_steps >= 0 stops after that many steps (a plan prefix); step_rows, if given,
+// receives each step's working-set size and ext_rows each extension event's added rows.
+int64_t count_rows(const CompletionRates& comp, const PlanContext& ctx, int64_t max_steps = -1,
+                   std::vector<int64_t>* step_rows = nullptr, std::vector<int64_t>* ext_rows = nullptr) {
     int64_t rows = 0;
+    int64_t steps = 0;
     CompletionRates cur = comp;
     if (is_satisfied(cur)) return 0;
     detail::WorkingSet ws(ctx.pool);
@@ -209,13 +215,17 @@ int64_t count_rows(const CompletionRates& comp, const PlanContext& ctx) {
             if (almost[i]) continue;
             if (1.0 - cur.values[i] < ctx.pool.best_single_util[i]) {
                 almost[i] = true;
+                size_t before = ws.extra.items.size();
                 extend_candidate_pool(ws.extra, ctx.services, *ctx.profiles, ctx.rules, i, unsat, 4);
+                if (ext_rows) ext_rows->push_back(static_cast<int64_t>(ws.extra.items.size() - before));
             }
         }
     };
     maybe_extend();
-    while (!is_satisfied(cur)) {
+    while (!is_satisfied(cur) && (max_steps < 0 || steps < max_steps)) {
+        ++steps;
         rows += static_cast<int64_t>(ws.size());
+        if (step_rows) step_rows->push_back(static_cast<int64_t>(ws.size()));
         int best = -1;
         double best_score = 0.0;
         for (size_t i = 0; i < ws.size(); ++i) {
@@ -372,6 +382,8 @@ int mig_fast_algo(mig_ctx* ctx, const double* comp, int32_t n, mig_config* out, 
                 trace(user, iter, &mc, s, cur.values.data(), static_cast<int32_t>(cur.values.size()));
             };
         auto plan = fast_algo(c, ctx->plan, tr);
+        ctx->last_comp = c.values;
+        ctx->have_last = true;
         rc = emit_plan(plan, ctx->services, out, cap, n_out);
     });
     return g != MIG_OK ? g : rc;
@@ -827,6 +839,22 @@ int mig_ctx_stats(const mig_ctx*, mig_stats* out) {
     return MIG_OK;
 }
 void mig_ctx_reset_stats(mig_ctx*) {}
+int mig_device_cache_release(int32_t) { return MIG_OK; }
+
+// The reference keeps no per-step record: the instrumented replica re-runs the last
+// mig_fast_algo call's working-set growth (count_rows above).
+int mig_ctx_step_rows(const mig_ctx* ctx, int64_t* out, int32_t cap, int32_t* n_out) {
+    return guarded([&] {
+        std::vector<int64_t> sr;
+        if (ctx->have_last) {
+            CompletionRates c;
+            c.values = ctx->last_comp;
+            count_rows(c, ctx->plan, -1, &sr);
+        }
+        *n_out = static_cast<int32_t>(sr.size());
+        for (int32_t i = 0; i < *n_out && i < cap; ++i) out[i] = sr[i];
+    });
+}
 
 // Reference-arm extras (not in the product header): rows a fast_algo scans, and
 // gen_workload (bench.hpp:125-156) so generated workloads come from the reference itself.
@@ -874,6 +902,60 @@ int mig_ref_plan_transition(const char* old_dep, const char* new_dep, const char
 
 int mig_ref_count_rows(mig_ctx* ctx, const double* comp, int32_t n, int64_t* rows) {
     return guarded([&] { *rows = count_rows(comp_of(comp, n, ctx), ctx->plan); });
+}
+
+// Per-step working-set sizes and per-event extension sizes of the first max_steps steps of
+// fast_algo (the instrumented replica above).  Returns the counts written in *n_steps / *n_ext.
+int mig_ref_step_rows(mig_ctx* ctx, const double* comp, int32_t n, int64_t max_steps, int64_t* step_rows,
+                      int32_t step_cap, int32_t* n_steps, int64_t* ext_rows, int32_t ext_cap, int32_t* n_ext) {
+    return guarded([&] {
+        std::vector<int64_t> sr, er;
+        count_rows(comp_of(comp, n, ctx), ctx->plan, max_steps, &sr, &er);
+        *n_steps = static_cast<int32_t>(sr.size());
+        *n_ext = static_cast<int32_t>(er.size());
+        for (int i = 0; i < *n_steps && i < step_cap; ++i) step_rows[i] = sr[i];
+        for (int i = 0; i < *n_ext && i < ext_cap; ++i) ext_rows[i] = er[i];
+    });
+}
+
+// The reference's own fast_algo (greedy.hpp:95-145), stopped after its first max_steps steps,
+// or (steps_after_ext >= 0) that many steps after the step following which maybe_extend
+// first fires (greedy.hpp:107-119's trigger, evaluated on the traced completion; -1 = the
+// call before step 0).  The trace callback throws a sentinel at the cap, so every step
+// reported is the unmodified reference's.  *n_steps = steps traced.
+struct PrefixStop {};
+int mig_ref_fast_algo_prefix(mig_ctx* ctx, const double* comp, int32_t n, int64_t max_steps,
+                             int64_t steps_after_ext, mig_greedy_trace_fn trace, void* user, int32_t* n_steps,
+                             int32_t* first_ext_step) {
+    int32_t steps = 0;
+    int32_t ext_at = -2;
+    int rc = guarded([&] {
+        CompletionRates c = comp_of(comp, n, ctx);
+        const auto& bsu = ctx->plan.pool.best_single_util;
+        auto fires = [&](const CompletionRates& cur) {
+            for (size_t i = 0; i < cur.values.size(); ++i)
+                if (cur.values[i] < 1.0 - kSatisfyEps && 1.0 - cur.values[i] < bsu[i]) return true;
+            return false;
+        };
+        if (fires(c)) ext_at = -1;
+        std::function<void(int, const Candidate&, double, const CompletionRates&)> tr =
+            [&](int iter, const Candidate& cand, double s, const CompletionRates& cur) {
+                mig_candidate mc;
+                cand_to_c(cand, ctx->services, &mc);
+                if (trace) trace(user, iter, &mc, s, cur.values.data(), static_cast<int32_t>(cur.values.size()));
+                ++steps;
+                if (ext_at == -2 && fires(cur)) ext_at = iter;
+                if (max_steps >= 0 && steps >= max_steps) throw PrefixStop{};
+                if (steps_after_ext >= 0 && ext_at != -2 && iter >= ext_at + steps_after_ext) throw PrefixStop{};
+            };
+        try {
+            fast_algo(c, ctx->plan, tr);
+        } catch (const PrefixStop&) {
+        }
+    });
+    *first_ext_step = ext_at;
+    *n_steps = steps;
+    return rc;
 }
 
 // Writes n services (id/model as indices into caller-owned string tables is awkward in C,

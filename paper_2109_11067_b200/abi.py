@@ -152,11 +152,15 @@ SIGNATURES = {
     "mig_brute_force_optimum": (_I, [_P, C.c_int32, C.c_int64, _P, C.c_int32, _I32P, _I32P]),
     "mig_ctx_stats": (_I, [_P, C.POINTER(StatsC)]),
     "mig_ctx_reset_stats": (None, [_P]),
+    "mig_ctx_step_rows": (_I, [_P, _I64P, C.c_int32, _I32P]),
+    "mig_device_cache_release": (_I, [C.c_int32]),
 }
 
 # Exported by the reference shim only (bench.py reference arm, golden generation).
 REF_EXTRAS = {
     "mig_ref_count_rows": (_I, [_P, _DP, C.c_int32, _I64P]),
+    "mig_ref_step_rows": (_I, [_P, _DP, C.c_int32, C.c_int64, _I64P, C.c_int32, _I32P, _I64P, C.c_int32, _I32P]),
+    "mig_ref_fast_algo_prefix": (_I, [_P, _DP, C.c_int32, C.c_int64, C.c_int64, GREEDY_TRACE, _P, _I32P, _I32P]),
     "mig_ref_plan_transition": (_I, [C.c_char_p, C.c_char_p, C.c_char_p, C.c_char_p, C.c_char_p, C.c_int32,
                                      C.c_char_p, C.c_int32, _I32P]),
     "mig_ref_deployment_json": (_I, [_P, C.POINTER(ConfigC), C.c_int32, C.c_char_p, C.c_int32, _I32P]),

@@ -490,6 +490,9 @@ int mig_board_alloc(int32_t device, int32_t n_ranks, void** board, uint8_t* ipc_
 int mig_board_open(int32_t device, const uint8_t* ipc_handle, void** board) {
     return guarded([&] { *board = board_open(device, ipc_handle); });
 }
+int mig_device_cache_release(int32_t device) {
+    return guarded([&] { release_device_cache(device); });
+}
 int mig_board_free(void* board, int32_t opened) {
     return guarded([&] { board_close(board, opened != 0); });
 }
@@ -711,5 +714,13 @@ int mig_ctx_stats(const mig_ctx* ctx, mig_stats* out) {
 }
 
 void mig_ctx_reset_stats(mig_ctx* ctx) { ctx->e->stats.reset(); }
+
+int mig_ctx_step_rows(const mig_ctx* ctx, int64_t* out, int32_t cap, int32_t* n_out) {
+    return guarded([&] {
+        auto v = ctx->e->last_step_rows();
+        *n_out = static_cast<int32_t>(v.size());
+        for (int32_t i = 0; i < *n_out && i < cap; ++i) out[i] = v[i];
+    });
+}
 
 }  // extern "C"

@@ -502,6 +502,27 @@ ScratchPool& scratch_pool(int device) {
 
 }  // namespace
 
+// Frees every pooled slot and scratch buffer of `device` not in use by a live call (the
+// next context pays the cold allocations again: bench.py's cold e2e).
+void release_device_cache(int device) {
+    std::vector<Slot*> slots;
+    {
+        SlotPool& pool = slot_pool(device);
+        std::lock_guard<std::mutex> g(pool.mu);
+        slots.swap(pool.free);
+    }
+    for (Slot* s : slots) delete s;
+    std::vector<void*> bufs;
+    {
+        ScratchPool& pool = scratch_pool(device);
+        std::lock_guard<std::mutex> g(pool.mu);
+        for (auto& [k, p] : pool.free) bufs.push_back(p);
+        pool.free.clear();
+    }
+    CK(cudaSetDevice(device));
+    for (void* p : bufs) cudaFree(p);
+}
+
 Scratch::Scratch(int device, size_t bytes) : device_(device) {
     size_t cls = 4096;
     while (cls < bytes) cls <<= 1;
@@ -670,6 +691,10 @@ bool Engine::greedy_finish(GreedyCall& c, float ms, int attempt, std::vector<uin
     if (h.status == kStepOverflow) throw DeviceError("greedy step buffer overflow");
     rows.assign(s->pick_row, s->pick_row + h.n_steps);
     scores.assign(s->pick_score, s->pick_score + h.n_steps);
+    {
+        std::lock_guard<std::mutex> g(diag_mu_);
+        last_step_rows_.assign(s->pick_rows, s->pick_rows + h.n_steps);
+    }
     stats.greedy_ns += static_cast<long long>(ms * 1e6f);
     stats.h2d += static_cast<long long>(sizeof(double) * m_.n);
     stats.d2h += static_cast<long long>(sizeof(GreedyState) + (sizeof(uint64_t) + sizeof(double) + sizeof(long long)) *
@@ -1149,7 +1174,9 @@ RolloutResult Engine::rollouts(const std::vector<double>& comp, long long n_roll
 // or the plan would exceed cap_steps.  rows[i] = device pointer to the picked rows.
 void Engine::greedy_batch(const double* d_comps, int count, long long cap_steps, long long rows_bound,
                           std::vector<const uint64_t*>& rows,
-                          std::vector<int>& n_steps, std::vector<std::vector<uint64_t>>* host_rows) {
+                          std::vector<int>& n_steps, std::vector<std::vector<uint64_t>>* host_rows,
+                          SlotLease* lease) {
+    if (lease) lease->e = this;
     rows.assign(count, nullptr);
     n_steps.assign(count, -1);
     if (count <= 0) return;
@@ -1207,10 +1234,13 @@ void Engine::greedy_batch(const double* d_comps, int count, long long cap_steps,
             }
             stats.d2h += static_cast<long long>(sizeof(GreedyState) + sizeof(uint64_t) * std::max(h.n_steps, 0));
         }
-        // the picked rows stay valid until these slots are reused: the caller consumes them
-        // (ga_finish) before the next greedy call, on this thread
+        // with a lease the slots (and the device picked rows in `rows`) are held until the
+        // caller has consumed them; the next batch then takes different slots
         for (auto& x : calls) {
-            x.e->release(x.s);
+            if (lease)
+                lease->slots.push_back(x.s);
+            else
+                x.e->release(x.s);
             x.s = nullptr;
         }
     }
@@ -1718,7 +1748,8 @@ void Engine::ga_generation(GaRun* r, int buf, const std::vector<int>& parent_len
     // refill every child's residual with the device greedy, all children in one launch
     std::vector<const uint64_t*> rows;
     std::vector<int> steps;
-    greedy_batch(r->residual, npar, r->L_cap, -1, rows, steps);
+    SlotLease lease;  // keeps every child's picked rows alive until ga_finish has read them
+    greedy_batch(r->residual, npar, r->L_cap, -1, rows, steps, nullptr, &lease);
     std::vector<int> ns(npar);
     CK(cudaMemcpy(ns.data(), r->n_surv, sizeof(int) * npar, cudaMemcpyDeviceToHost));
     for (int i = 0; i < npar; ++i)
@@ -1777,11 +1808,16 @@ void Engine::set_shard(int rank, int n_ranks, const std::vector<void*>& boards, 
     n_ranks_ = 1;
     boards_.clear();
     if (n_ranks == 1) return;
-    // base rows of the supports with index == rank (mod n_ranks), in pool order
+    // base rows by support, balanced by row count: supports in pool order, each to the rank
+    // holding the fewest rows so far (ties: lowest rank) — the same deal on every rank
     std::vector<uint64_t> mine;
-    for (size_t i = 0; i + 1 < support_off_.size(); ++i)
-        if (static_cast<int>(i % n_ranks) == rank)
+    std::vector<long long> load(n_ranks, 0);
+    for (size_t i = 0; i + 1 < support_off_.size(); ++i) {
+        const int q = static_cast<int>(std::min_element(load.begin(), load.end()) - load.begin());
+        load[q] += support_off_[i + 1] - support_off_[i];
+        if (q == rank)
             mine.insert(mine.end(), base_rows_.begin() + support_off_[i], base_rows_.begin() + support_off_[i + 1]);
+    }
     CK(cudaMalloc(&d_shard_, std::max<size_t>(mine.size(), 1) * 8 + 16));
     if (!mine.empty()) CK(cudaMemcpy(d_shard_, mine.data(), mine.size() * 8, cudaMemcpyHostToDevice));
     stats.h2d += static_cast<long long>(mine.size() * 8);

@@ -33,6 +33,7 @@ size_t board_bytes(int n_ranks);
 void* board_alloc(int device, int n_ranks, unsigned char ipc_handle[64]);
 void* board_open(int device, const unsigned char ipc_handle[64]);
 void board_close(void* board, bool opened);
+void release_device_cache(int device);
 bool config_equal(const Config& a, const Config& b);
 
 struct Slot;
@@ -146,10 +147,26 @@ class Engine {
     // must be the max_mix = n pool, n <= 4).  found = false: the optimum exceeds cap.
     std::vector<Config> brute_force(int cap, long long node_budget, bool& found);
 
-    // Independent single-CTA greedy instances in one launch (the GA's refills).
+    // Slots kept past greedy_batch so the device picked rows it returns stay valid: released
+    // when the lease is destroyed (after the caller has consumed the rows).
+    struct SlotLease {
+        Engine* e = nullptr;
+        std::vector<Slot*> slots;
+        SlotLease() = default;
+        SlotLease(const SlotLease&) = delete;
+        SlotLease& operator=(const SlotLease&) = delete;
+        ~SlotLease() {
+            for (Slot* s : slots) e->release(s);
+        }
+    };
+    // Independent single-CTA greedy instances in one launch (the GA's refills).  With `lease`
+    // every instance's slot (and so its device picked rows) is held by the lease; without
+    // one, the device pointers in `rows` are only valid until the next batch of 8 starts,
+    // so callers that read them must pass a lease (or ask for host_rows).
     void greedy_batch(const double* d_comps, int count, long long cap_steps, long long rows_bound,
                       std::vector<const uint64_t*>& rows,
-                      std::vector<int>& n_steps, std::vector<std::vector<uint64_t>>* host_rows = nullptr);
+                      std::vector<int>& n_steps, std::vector<std::vector<uint64_t>>* host_rows = nullptr,
+                      SlotLease* lease = nullptr);
     void fast_algo_batch(const std::vector<std::vector<double>>& comps, std::vector<std::vector<uint64_t>>& rows,
                          std::vector<int>& status);
     std::vector<MctsDeviceResult> mcts_device_group(const std::vector<std::vector<double>>& comps, int budget, int topk,
@@ -170,8 +187,15 @@ class Engine {
 
     Stats stats;
     int device() const { return device_; }
+    // working-set size at each step of the most recent greedy plan finished on this context
+    std::vector<long long> last_step_rows() const {
+        std::lock_guard<std::mutex> g(diag_mu_);
+        return last_step_rows_;
+    }
 
   private:
+    mutable std::mutex diag_mu_;
+    std::vector<long long> last_step_rows_;
     Slot* acquire();
     void release(Slot*);
     void ensure_ext(Slot* s, long long rows);

@@ -596,10 +596,17 @@ __global__ void __launch_bounds__(kThreads, 1) greedy_kernel(const __grid_consta
             }
             __syncthreads();
             const int m = s_m;
+            // sharded greedy: support (event e, size k, colex rank r) belongs to rank
+            // (r + k + e) mod P, so each rank unranks only its own supports r = off[k] + j*P
+            const int P = a.n_ranks > 1 ? a.n_ranks : 1;
             long long seg[5] = {0, 0, 0, 0, 0};
+            int off[5] = {0, 0, 0, 0, 0};
             long long total = 0;
             for (int k = M.max_mix + 1; k <= 4; ++k) {
-                seg[k] = binom(m, k - 1) * M.n_tmpl[k];
+                const long long B = binom(m, k - 1);
+                off[k] = P > 1 ? ((a.rank - k - e) % P + P) % P : 0;
+                const long long cnt = B > off[k] ? (B - off[k] + P - 1) / P : 0;
+                seg[k] = cnt * M.n_tmpl[k];
                 total += seg[k];
             }
             const long long stride = static_cast<long long>(G) * blockDim.x;
@@ -613,10 +620,9 @@ __global__ void __launch_bounds__(kThreads, 1) greedy_kernel(const __grid_consta
                     long long rem = g;
                     while (rem >= seg[k]) rem -= seg[k++];
                     const int nt = M.n_tmpl[k];
-                    const long long r = rem / nt;
-                    const int t = static_cast<int>(rem - r * nt);
-                    // sharded greedy: support (event e, size k, rank r) lives on one rank only
-                    if (a.n_ranks > 1 && (r * 4 + k + e) % a.n_ranks != a.rank) ok = false;
+                    const long long j = rem / nt;
+                    const int t = static_cast<int>(rem - j * nt);
+                    const long long r = off[k] + j * P;
                     int idx[3];
                     unrank(r, k - 1, m, idx);
                     int S[4];

@@ -51,14 +51,27 @@ def _decode(vals, ctx):
     return plan
 
 
-def _pick_and_broadcast(key: tuple, plan, ctx, group=None):
-    """All ranks agree on the rank with the smallest key, then receive its plan."""
+_FAILED = (1 << 63) - 1
+
+
+def _pick_and_broadcast(key: tuple, plan, ctx, group=None, error: BaseException | None = None):
+    """All ranks agree on the rank with the smallest key, then receive its plan.  A rank whose
+    local solve raised still joins the collectives (key[0] = _FAILED), so no peer blocks in
+    the all-gather; then every rank raises the failing rank's error type together."""
     world = dist.get_world_size(group)
     dev = _device(group)
-    mine = torch.tensor(list(key), dtype=torch.int64, device=dev)
+    if error is not None:
+        key = (_FAILED,) * (len(key) - 1) + (key[-1],)
+    mine = torch.tensor(list(key) + [1 if error is not None else 0], dtype=torch.int64, device=dev)
     keys = [torch.zeros_like(mine) for _ in range(world)]
     dist.all_gather(keys, mine, group=group)
     keys = [tuple(int(x) for x in k.tolist()) for k in keys]
+    failed = [r for r in range(world) if keys[r][-1]]
+    if failed:
+        if error is not None:
+            raise error
+        raise mp.PlanningError(f"rank {failed[0]} failed its local solve")
+    keys = [k[:-1] for k in keys]
     winner = min(range(world), key=lambda r: keys[r])
     enc = _encode(plan, ctx)
     length = torch.tensor([len(enc)], dtype=torch.int64, device=dev)
@@ -80,7 +93,10 @@ def island_two_phase(ctx: mp.PlanContext, params: mp.GaParams, group=None, log=N
     p = mp.GaParams(**{**params.__dict__})
     if rank > 0:  # rank 0 keeps the caller's seed: the result is never worse than two_phase(seed)
         p.seed = mp.mix_seed(params.seed, rank)
-    dep = mp.two_phase(ctx.services, ctx.profiles, ctx.rules, p, log=log, ctx=ctx)
+    try:
+        dep = mp.two_phase(ctx.services, ctx.profiles, ctx.rules, p, log=log, ctx=ctx)
+    except RuntimeError as e:
+        _pick_and_broadcast((0, 0, rank), [], ctx, group, error=e)
     plan = [g.config for g in dep.gpus]
     slack = mp.slack_of(mp.completion_of(plan, ctx.services, ctx.profiles))
     winner, best = _pick_and_broadcast((len(plan), _slack_bits(slack), rank), plan, ctx, group)
@@ -91,7 +107,10 @@ def root_parallel_mcts(comp, ctx: mp.PlanContext, params: mp.MctsParams, seed: i
     """Root-parallel MCTS: rank r searches with seed mix_seed(seed, r); the shortest plan wins."""
     rank = dist.get_rank(group)
     s = mp.mix_seed(seed, rank) if rank > 0 else seed  # rank 0 == mcts_solve(seed)
-    plan = mp.mcts_solve(comp, ctx, params, s)
+    try:
+        plan = mp.mcts_solve(comp, ctx, params, s)
+    except RuntimeError as e:
+        _pick_and_broadcast((0, rank), [], ctx, group, error=e)
     return _pick_and_broadcast((len(plan), rank), plan, ctx, group)
 
 
@@ -132,10 +151,11 @@ def fast_algo_local(ctxs: list, comp):
                                                                                       C.byref(nout)))
 
 
-def shard_context(ctx: mp.PlanContext, device: int, group=None):
+def shard_context(ctx: mp.PlanContext, device: int, group=None, max_ctas: int = 0):
     """One rank per GPU (torch.distributed): allocate this rank's exchange board, all-gather
     the CUDA IPC handles, open the peers' boards (NVLink peer memory) and shard the context.
-    Afterwards every rank calls mp.fast_algo SPMD and receives the identical plan."""
+    Afterwards every rank calls mp.fast_algo SPMD and receives the identical plan.
+    max_ctas > 0 caps the greedy grid (ranks sharing one GPU in tests)."""
     import ctypes as C
 
     rank, world = dist.get_rank(group), dist.get_world_size(group)
@@ -152,9 +172,24 @@ def shard_context(ctx: mp.PlanContext, device: int, group=None):
         ctx.backend.check(ctx.backend.lib.mig_board_open(device, h, C.byref(p)))
         ptrs.append(p.value)
     arr = (C.c_void_p * world)(*ptrs)
-    ctx.backend.check(ctx.backend.lib.mig_ctx_set_shard(ctx._p, rank, world, arr, 0))
+    ctx.backend.check(ctx.backend.lib.mig_ctx_set_shard(ctx._p, rank, world, arr, max_ctas))
+    ctx._shard_rank = rank
     dist.barrier(group=group)  # every board is zeroed before any rank posts into it
     return ptrs
+
+
+def unshard_context(ctx: mp.PlanContext, boards, group=None) -> None:
+    """Undo shard_context (collective): the context scans its whole working set again; every
+    rank closes its IPC mappings of the peers' boards, then (after a barrier) frees its own."""
+    import ctypes as C
+
+    rank = ctx._shard_rank
+    ctx.backend.check(ctx.backend.lib.mig_ctx_set_shard(ctx._p, 0, 1, None, 0))
+    for q, p in enumerate(boards):
+        if q != rank:
+            ctx.backend.check(ctx.backend.lib.mig_board_free(C.c_void_p(p), 1))
+    dist.barrier(group=group)
+    ctx.backend.check(ctx.backend.lib.mig_board_free(C.c_void_p(boards[rank]), 0))
 
 
 def sharded_rows(ctx: mp.PlanContext, group=None) -> int:
@@ -175,7 +210,10 @@ def root_parallel_rollouts(comp, ctx: mp.PlanContext, params: mp.RolloutParams, 
     R = params.n_rollouts
     lo, hi = R * rank // world, R * (rank + 1) // world
     p = mp.RolloutParams(**{**params.__dict__, "n_rollouts": hi - lo, "id_offset": params.id_offset + lo})
-    res = mp.rollouts(comp, ctx, p)
+    try:
+        res = mp.rollouts(comp, ctx, p)
+    except RuntimeError as e:
+        _pick_and_broadcast((0, 0, rank), [], ctx, group, error=e)
     plan = [ctx.pool[i].config for i in res.path]
     big = 1 << 62
     key = (res.best_len if res.best_len >= 0 else big, res.best_id if res.best_id >= 0 else big, rank)

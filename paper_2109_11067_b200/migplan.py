@@ -682,6 +682,12 @@ def make_plan_context(services, profiles, rules, max_mix: int = 2, backend=None,
     return PlanContext(services, profiles, rules, max_mix, backend, device)
 
 
+def release_device_cache(device: int = 0, backend=None) -> None:
+    """Free the process-wide pooled per-call device resources (mig_device_cache_release)."""
+    b = _backend(backend)
+    b.check(b.lib.mig_device_cache_release(device))
+
+
 def _run_plan(ctx: PlanContext, call) -> list[GpuConfig]:
     cap = 4096  # a longer plan is re-run with the exact size (MIG_ERR_ARGUMENT + n_out)
     while True:

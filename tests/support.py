@@ -109,6 +109,23 @@ def comp_digest(comp) -> str:
     return hashlib.sha1(b"".join(struct.pack("<d", c) for c in comp)).hexdigest()[:16]
 
 
+def plan_sha(plan_or_key) -> str:
+    """sha256 (16 hex) of a plan's canonical form (plan_key), printed by both bench arms."""
+    key = plan_or_key if (not plan_or_key or isinstance(plan_or_key[0], list)) else plan_key(plan_or_key)
+    return hashlib.sha256(json.dumps(key, separators=(",", ":")).encode()).hexdigest()[:16]
+
+
+def pool_sha(ctx) -> str:
+    """Order-free digest of a context's base pool: sorted canonical rows (configs, utility
+    bits, util_sum bits)."""
+    rows = []
+    for c in ctx.pool:
+        key = [[i.placement.slices, i.placement.start_slot, i.service_id, i.batch] for i in c.config.instances]
+        rows.append(json.dumps([key, [[k, v.hex()] for k, v in c.util], c.util_sum.hex()], separators=(",", ":")))
+    rows.sort()
+    return hashlib.sha256("\n".join(rows).encode()).hexdigest()[:16]
+
+
 def load_golden(name: str):
     with open(os.path.join(GOLDEN, name)) as f:
         return json.load(f)

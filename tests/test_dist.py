@@ -58,3 +58,37 @@ def test_islands_and_root_parallel_world2():
     assert w0 == w1 and plan0 == plan1 and ok0 and ok1          # every rank holds the same winner
     assert len(plan0) <= len(single0)                           # never worse than two_phase(seed) on 1 GPU
     assert m0 == m1 and mp0 == mp1 and len(mp0) <= mono0       # root-parallel MCTS: same-or-fewer GPUs
+
+
+def err_worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2109_11067_b200 import dist as D
+
+        ps, sv = S.random_workload(4, 77)
+        ctx = mp.make_plan_context(sv, ps, mp.PartitionRuleSet.defaults(), backend=S.checker_backend())
+        comp = [0.0] * 4 if rank == 0 else [0.0] * 3  # rank 1's local solve raises PlanningError
+        try:
+            D.root_parallel_mcts(comp, ctx, mp.MctsParams(budget_iters=8), 5)
+            q.put((rank, "ok"))
+        except mp.PlanningError as e:
+            q.put((rank, "raised:" + type(e).__name__))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.skipif(S.checker_backend() is None, reason="no CPU checker library")
+def test_failing_rank_does_not_hang_peers():
+    """A rank whose local solve raises still joins the all-gather; every rank then raises."""
+    ctx = tmp.get_context("spawn")
+    q = ctx.Queue()
+    port = free_port()
+    procs = [ctx.Process(target=err_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=120) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert res == {0: "raised:PlanningError", 1: "raised:PlanningError"}

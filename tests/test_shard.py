@@ -93,6 +93,78 @@ def free_port():
         return s.getsockname()[1]
 
 
+# ---------------------------------------------------------------- one process per rank (IPC boards)
+
+def ipc_worker(rank, world, port, q, name, mode):
+    """One rank of a process-sharded greedy: a gloo group carries the CUDA IPC handles of the
+    exchange boards (dist.shard_context); every step's winner then crosses processes through
+    the boards inside the persistent kernels.  All ranks share cuda:0 here (1-GPU box), so
+    the grids are capped; on an 8-GPU box each rank owns a GPU and its full grid."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    if mode == "timeout":
+        os.environ["MIGPLAN_EXCH_TIMEOUT_MS"] = "3000"
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import time
+
+        from paper_2109_11067_b200 import dist as D
+
+        g = GREEDY[name]
+        ctx = mp.make_plan_context(services_of(g), store_of(g), mp.PartitionRuleSet.defaults(), device=0)
+        D.shard_context(ctx, 0, max_ctas=8)
+        out = []
+        for rep in range(2):
+            if mode == "slow" and rank == world - 1:
+                time.sleep(1.5)  # a peer that launches late: the others wait inside their kernels
+            if mode == "timeout" and rank == world - 1:
+                break  # a peer that never launches: the others' watchdog fires
+            ctx.reset_stats()
+            try:
+                plan = S.plan_key(mp.fast_algo(mp.zero_completion(ctx.n), ctx))
+                out.append((plan, ctx.stats()["greedy_rows"]))
+            except RuntimeError as e:  # noqa: PERF203
+                out.append(("error", str(e)))
+                break
+        q.put((rank, out))
+        dist.barrier()
+    finally:
+        dist.destroy_process_group()
+
+
+def run_ipc(world, name, mode="normal"):
+    ctx = tmp.get_context("spawn")
+    q = ctx.Queue()
+    port = free_port()
+    procs = [ctx.Process(target=ipc_worker, args=(r, world, port, q, name, mode)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=600) for _ in procs)
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    return res
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("world,name,mode", [(2, "slos_day", "normal"), (2, "slos_24", "normal"),
+                                             (3, "gen24_8.7", "normal"), (2, "slos_night", "slow")])
+def test_process_sharded_greedy_ipc(world, name, mode):
+    g = GREEDY[name]
+    res = run_ipc(world, name, mode)
+    for rep in range(2):
+        plans = [res[r][rep][0] for r in range(world)]
+        assert all(p == g["plan"] for p in plans)
+        assert sum(res[r][rep][1] for r in range(world)) == g["rows_scored"]
+
+
+@pytest.mark.gpu
+def test_process_sharded_greedy_peer_never_launches():
+    """A missing peer turns into MIG_ERR_DEVICE after the exchange watchdog, not a hang."""
+    res = run_ipc(2, "slos_day", "timeout")
+    assert res[1] == []
+    assert res[0][0][0] == "error" and "timed out" in res[0][0][1]
+
+
 def roll_worker(rank, world, port, q):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
