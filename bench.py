@@ -259,9 +259,13 @@ class RefSampler:
         if name == "gen128_8.0_greedy":
             self.steps = cpu_prefix_steps()
             self.rows = self.steps * len(self.ctx.pool)  # steps before the first extension scan the base pool
-            self.sample = (f"the reference's fast_algo for its first {self.steps} steps (all before its first "
-                           f"extension event, {len(self.ctx.pool)} base rows each) on a resident context; base "
-                           f"pool build {self.build_s:.2f} s untimed; 1 core (fast_algo is single-threaded)")
+            self.sample = (f"the reference's fast_algo for its first {self.steps} step(s) — every step before its "
+                           f"first extension event (greedy_prefix.json), {len(self.ctx.pool)} base rows each, "
+                           f"including the call's WorkingSet set-up — on a resident context (base pool build "
+                           f"{self.build_s:.2f} s, untimed); 1 core (fast_algo is single-threaded).  Its most "
+                           f"favourable regime: the reference's first 3 steps, which include its first extensions "
+                           f"(~24.9 M rows each), took 825 s on one core of the build container "
+                           f"(tests/golden/greedy_prefix.json ref_wall_s)")
         else:
             # rows per step: counted by the CPU restatement on the same call sequence (untimed)
             orc = S.oracle_backend()

@@ -53,5 +53,32 @@ def build(verbose: bool = False) -> str:
     return LIB
 
 
+def build_variant(defines: list[str], out: str) -> str:
+    """Development aid (tools/probe_ab.py): the same library with extra -D flags, built into
+    `out` (objects under <out>.obj/) so kernel variants can be A/B-timed on one GPU box."""
+    obj_dir = out + ".obj"
+    os.makedirs(obj_dir, exist_ok=True)
+
+    def comp(src):
+        obj = os.path.join(obj_dir, os.path.splitext(src)[0] + ".o")
+        lang = [] if src.endswith(".cu") else ["-x", "cu"]
+        r = subprocess.run([NVCC, *FLAGS, *[f"-D{d}" for d in defines], *lang, "-c", os.path.join(CSRC, src), "-o", obj],
+                           capture_output=True, text=True)
+        if r.returncode != 0:
+            raise RuntimeError(f"nvcc failed for {src}:\n{r.stderr}")
+        return obj
+
+    with cf.ThreadPoolExecutor(max_workers=len(SOURCES)) as ex:
+        objs = list(ex.map(comp, SOURCES))
+    r = subprocess.run([NVCC, "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-o", out, *objs, "-lpthread"],
+                       capture_output=True, text=True)
+    if r.returncode != 0:
+        raise RuntimeError(f"link failed:\n{r.stderr}")
+    return out
+
+
 if __name__ == "__main__":
-    build(verbose="-v" in sys.argv)
+    if len(sys.argv) > 2 and sys.argv[1] == "variant":  # python build.py variant OUT.so DEF1 DEF2 ...
+        print(build_variant(sys.argv[3:], sys.argv[2]))
+    else:
+        build(verbose="-v" in sys.argv)

@@ -76,6 +76,7 @@ struct GreedyArgs {
     int cache_units;      // 16-byte row units of shared-memory cache per CTA
     int phase_timers;     // 1: CTA 0 records %globaltimer phase totals (diagnostics)
     int prefetch;         // bulk L2 prefetch distance of the streaming scan (iterations; 0 off)
+    int pipeline;         // streaming scan: load the next 4 units before scoring these (1) or not
     int load_mode;        // streaming row load flavour (kernels.cu ld_row4)
     int interleave;       // units dealt to CTAs in 32-unit blocks (working set fits on chip)
     int ring_stages;      // TMA ring stages (32 KB each) for rows beyond the cache; 0: direct loads

@@ -185,8 +185,9 @@ Engine::Engine(const Rules& rules, std::map<std::string, ModelProfile> profiles,
     const int T = kernel_threads();
     // greedy: everything but the row cache is fixed; the cache takes the rest of the
     // opt-in shared memory (one CTA per SM), rounded to whole units per thread.
-    // TMA ring for rows beyond the on-chip cache: measured slower than direct L2-prefetched
-    // loads at n = 128 (profiles/), so off by default; MIGPLAN_RING=k enables k stages.
+    // Per-warp TMA slots for rows beyond the on-chip cache (kernels.cu, streaming scan):
+    // measured slower at n = 128 than the software-pipelined, L2-prefetched direct loads
+    // (4.79 vs 5.1 TB/s on one box, identical plans), so off; MIGPLAN_RING=k enables k stages.
     ring_stages_ = 0;
     if (const char* e = std::getenv("MIGPLAN_RING")) ring_stages_ = std::max(0, std::min(8, std::atoi(e)));
     {
@@ -648,6 +649,8 @@ void Engine::greedy_prepare(GreedyCall& c, const double* comp_host, const double
     a.phase_timers = std::getenv("MIGPLAN_PHASE_TIMERS") ? 1 : 0;
     a.prefetch = 4;
     if (const char* e = std::getenv("MIGPLAN_PREFETCH")) a.prefetch = std::atoi(e);
+    a.pipeline = 1;  // software-pipelined streaming loads (MIGPLAN_PIPE=0: off)
+    if (const char* e = std::getenv("MIGPLAN_PIPE")) a.pipeline = std::atoi(e);
     a.load_mode = 2;  // ld.global.cs: measured best for the streaming scan (profiles/)
     if (const char* e = std::getenv("MIGPLAN_LOAD_MODE")) a.load_mode = std::atoi(e);
     a.comp0 = comp_host ? s->io->comp : comp_dev;
@@ -779,7 +782,8 @@ int Engine::greedy_cluster_ctas(size_t smem, long long rows_bound) const {
         cfg.attrs = at;
         cfg.numAttrs = 1;
         int nc = 0;
-        if (cudaOccupancyMaxActiveClusters(&nc, greedy_kernel_ptr(), &cfg) == cudaSuccess && nc > 0) return done(want);
+        if (cudaOccupancyMaxActiveClusters(&nc, greedy_kernel_ptr(), &cfg) == cudaSuccess && nc > 0)
+            return done(want);
         cudaGetLastError();
     }
     return done(0);

@@ -307,14 +307,14 @@ __device__ __forceinline__ float ub2(const float* __restrict__ Wf, unsigned lo, 
 __device__ __forceinline__ void consider8(const DevModel& M, const double* __restrict__ W, const float* __restrict__ Wf,
                                           const double* U, const uint4& v0, const uint4& v1, const uint4& v2,
                                           const uint4& v3, Best& best, double floor = 0.0) {
-    const float ub[8] = {ub2(Wf, v0.x, v0.y), ub2(Wf, v0.z, v0.w), ub2(Wf, v1.x, v1.y), ub2(Wf, v1.z, v1.w),
-                         ub2(Wf, v2.x, v2.y), ub2(Wf, v2.z, v2.w), ub2(Wf, v3.x, v3.y), ub2(Wf, v3.z, v3.w)};
     // FP32 floor rounded DOWN: ub >= best.s implies ub >= ff, so no row that can win or tie
     // is skipped; with no best yet, ff = the smallest positive float (rows must score > 0).
     // `floor` is a score some row of the warp already has: a row below it cannot be the argmax
     // (it may still tie it, so the compare stays >=).
     const double fl = fmax(best.s, floor);
     const float ff = fl > 0.0 ? __double2float_rd(fl) : 1.40129846e-45f;
+    const float ub[8] = {ub2(Wf, v0.x, v0.y), ub2(Wf, v0.z, v0.w), ub2(Wf, v1.x, v1.y), ub2(Wf, v1.z, v1.w),
+                         ub2(Wf, v2.x, v2.y), ub2(Wf, v2.z, v2.w), ub2(Wf, v3.x, v3.y), ub2(Wf, v3.z, v3.w)};
     bool hit = false;
 #pragma unroll
     for (int j = 0; j < 8; ++j) hit |= ub[j] >= ff;
@@ -324,7 +324,7 @@ __device__ __forceinline__ void consider8(const DevModel& M, const double* __res
                                (static_cast<uint64_t>(v2.y) << 32) | v2.x, (static_cast<uint64_t>(v2.w) << 32) | v2.z,
                                (static_cast<uint64_t>(v3.y) << 32) | v3.x, (static_cast<uint64_t>(v3.w) << 32) | v3.z};
 #pragma unroll
-        for (int j = 0; j < 8; ++j)  // (the thread's current best row needs no second look)
+        for (int j = 0; j < 8; ++j)
             if (static_cast<double>(ub[j]) >= (fl > 0.0 ? fl : 4.9406564584124654e-324) && r[j] != best.row)
                 take(M, U, r[j], row_score(W, r[j]), best);
     }
@@ -334,6 +334,56 @@ __device__ __forceinline__ void consider2(const DevModel& M, const double* __res
                                           const uint4& v, Best& best) {
     consider(M, W, U, (static_cast<uint64_t>(v.y) << 32) | v.x, best);
     consider(M, W, U, (static_cast<uint64_t>(v.w) << 32) | v.z, best);
+}
+
+// The streaming part of a greedy step's scan (units u, u + GT, ... < NU, four per thread per
+// iteration).  Measured alternatives (tools/gpu_ab.sh, n = 128): a non-inlined copy with its
+// own register budget, a 1024-thread CTA at 64 registers, and a max-reduced FP32 bound with
+// a separate exact path were all slower than this inlined, software-pipelined loop.
+__device__ __forceinline__ Best scan_stream(const DevModel& M, const double* W, const float* Wf, const double* U,
+                                         const uint4* rows4, long long u, long long NU, long long GT, int prefetch,
+                                         int pipeline, Best best, double wfloor) {
+    if (pipeline && u + 3 * GT < NU) {
+        // software-pipelined: the next 4 units are loaded before this 4 are scored, so every
+        // warp keeps its loads in flight while it computes
+        uint4 n0 = ld_row4(rows4 + u, LOADM), n1 = ld_row4(rows4 + u + GT, LOADM),
+              n2 = ld_row4(rows4 + u + 2 * GT, LOADM), n3 = ld_row4(rows4 + u + 3 * GT, LOADM);
+        for (; u + 3 * GT < NU; u += 4 * GT) {
+            if (threadIdx.x < 4 && prefetch > 0) {
+                const long long pu = u - threadIdx.x + (prefetch * 4 + threadIdx.x) * GT;
+                if (pu + static_cast<long long>(blockDim.x) <= NU)
+                    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(rows4 + pu),
+                                 "r"(static_cast<unsigned>(blockDim.x * 16))
+                                 : "memory");
+            }
+            const uint4 v0 = n0, v1 = n1, v2 = n2, v3 = n3;
+            if (u + 7 * GT < NU) {
+                n0 = ld_row4(rows4 + u + 4 * GT, LOADM);
+                n1 = ld_row4(rows4 + u + 5 * GT, LOADM);
+                n2 = ld_row4(rows4 + u + 6 * GT, LOADM);
+                n3 = ld_row4(rows4 + u + 7 * GT, LOADM);
+            }
+            consider8(M, W, Wf, U, v0, v1, v2, v3, best, wfloor);
+        }
+    }
+    for (; u + 3 * GT < NU; u += 4 * GT) {
+        // Bulk L2 prefetch, `prefetch` iterations ahead: one thread per CTA pulls the CTA's next
+        // stripes (contiguous: unit index = cta * blockDim + thread) into L2, so the loads
+        // below hit L2 instead of waiting on HBM latency.
+        if (threadIdx.x < 4 && prefetch > 0) {
+            const long long pu = u - threadIdx.x + (prefetch * 4 + threadIdx.x) * GT;
+            if (pu + static_cast<long long>(blockDim.x) <= NU)
+                asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(rows4 + pu),
+                             "r"(static_cast<unsigned>(blockDim.x * 16))
+                             : "memory");
+        }
+        // rows appended during this launch: L2-coherent loads (never the non-coherent path)
+        const uint4 v0 = ld_row4(rows4 + u, LOADM), v1 = ld_row4(rows4 + u + GT, LOADM),
+                    v2 = ld_row4(rows4 + u + 2 * GT, LOADM), v3 = ld_row4(rows4 + u + 3 * GT, LOADM);
+        consider8(M, W, Wf, U, v0, v1, v2, v3, best, wfloor);
+    }
+    for (; u < NU; u += GT) consider2(M, W, U, __ldcg(rows4 + u), best);
+    return best;
 }
 
 // W[e] = need * U[e] for need = 1 - comp[svc] > 0, else 0 (greedy.hpp:38-41).
@@ -365,7 +415,8 @@ __device__ __forceinline__ void unrank(long long r, int q, int m, int* out) {
 }
 
 // ---- TMA ring (cp.async.bulk + mbarrier) for the streaming part of the scan
-constexpr int kChunkUnits = 2048;  // 32 KB of rows per stage (4 units per thread)
+constexpr int kWarpChunk = 128;    // units per warp slot (4 per lane: one consider8)
+constexpr int kStageUnits = 32 * kWarpChunk;  // one stage: a 2 KB slot for each of up to 32 warps
 constexpr int kMaxStages = 8;
 
 __device__ __forceinline__ unsigned smem_u32(const void* p) {
@@ -426,7 +477,7 @@ __host__ __device__ inline GreedySmem greedy_layout(int n, int PP, int cache_uni
     o += cache_units * 16;
     o = (o + 127) & ~127;
     s.ring = o;
-    o += stages * kChunkUnits * 16;
+    o += stages * kStageUnits * 16;
     s.total = o;
     return s;
 }
@@ -485,7 +536,9 @@ __global__ void __launch_bounds__(256) enum_base_kernel(const __grid_constant__ 
 // greedy that share one GPU run as CTA ranges of ONE cooperative grid, so their per-step
 // exchange never depends on two kernels being co-scheduled.  bi / G are the CTA index and
 // CTA count of this CTA's instance.
-__global__ void __launch_bounds__(kThreads, 1) greedy_kernel(const __grid_constant__ GreedyLaunch GL) {
+template <int NT>
+__global__ void __launch_bounds__(NT, 1) greedy_kernel(const __grid_constant__ GreedyLaunch GL) {
+    constexpr int NW = NT / 32;
     extern __shared__ __align__(16) unsigned char smem[];
     const int grp = static_cast<int>(blockIdx.x) / GL.ctas_per_group;
     const GreedyArgs& a = GL.g[grp];
@@ -506,16 +559,13 @@ __global__ void __launch_bounds__(kThreads, 1) greedy_kernel(const __grid_consta
     uint8_t* xlist = smem + L.xlist;
     uint4* cache = reinterpret_cast<uint4*>(smem + L.cache);
     uint4* ring = reinterpret_cast<uint4*>(smem + L.ring);
-    __shared__ __align__(8) unsigned long long full_bar[kMaxStages], empty_bar[kMaxStages];
+    __shared__ __align__(8) unsigned long long wbar[kMaxStages][NW];  // per-warp TMA slots
     const int S = a.ring_stages;
-    if (threadIdx.x == 0) {
-        for (int q = 0; q < S; ++q) {
-            mbar_init(&full_bar[q], 1);
-            mbar_init(&empty_bar[q], kWarps);
-        }
+    if (lane_id() == 0 && S > 0) {
+        for (int q = 0; q < S; ++q) mbar_init(&wbar[q][threadIdx.x >> 5], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
-    __shared__ Best red[kWarps];
+    __shared__ Best red[NW];
     __shared__ Best xch[2];  // cluster mode: this CTA's block best, by step parity
     __shared__ uint64_t unsat[4];
     __shared__ int s_events, s_first_new, s_done, s_m, s_status;
@@ -576,9 +626,14 @@ __global__ void __launch_bounds__(kThreads, 1) greedy_kernel(const __grid_consta
     // Device-side extend_candidate_pool for the events recorded since `first`
     // (config_enum.hpp:206-211 with must_include = i, allowed = unsat, max_mix = 4):
     // every support S, max_mix < |S| <= 4, i in S subset-of unsat, not covered by an earlier
-    // event e' (i_e' in S subset-of unsat_e'), times every feasible template.  One thread
-    // per (support, template) pair; warp-aggregated appends keep the stores coalesced.
+    // event e' (i_e' in S subset-of unsat_e'), times every feasible template.
+    // Two levels per warp: the 32 lanes unrank and coverage-test 32 supports at once; then
+    // the warp walks the surviving supports (ballot order) and its lanes take that support's
+    // templates, so each support is unranked once and the appends stay warp-aggregated.
     auto extend_new = [&](int first, int last) {
+        const int ln = static_cast<int>(lane_id());
+        const long long gw = static_cast<long long>(bi) * NW + (threadIdx.x >> 5);
+        const long long GW = static_cast<long long>(G) * NW;
         for (int e = first; e < last; ++e) {
             __syncthreads();
             const int ie = ev_svc[e];
@@ -586,43 +641,38 @@ __global__ void __launch_bounds__(kThreads, 1) greedy_kernel(const __grid_consta
             if ((threadIdx.x >> 5) == 0) {
                 int m = 0;
                 for (int c = 0; c < (n + 31) / 32; ++c) {
-                    int i = c * 32 + static_cast<int>(lane_id());
+                    int i = c * 32 + ln;
                     bool in = i < n && i != ie && ((me[i >> 6] >> (i & 63)) & 1ull);
                     unsigned b = __ballot_sync(0xffffffffu, in);
                     if (in) xlist[m + __popc(b & lanemask_lt())] = static_cast<uint8_t>(i);
                     m += __popc(b);
                 }
-                if (lane_id() == 0) s_m = m;
+                if (ln == 0) s_m = m;
             }
             __syncthreads();
             const int m = s_m;
             // sharded greedy: support (event e, size k, colex rank r) belongs to rank
             // (r + k + e) mod P, so each rank unranks only its own supports r = off[k] + j*P
             const int P = a.n_ranks > 1 ? a.n_ranks : 1;
-            long long seg[5] = {0, 0, 0, 0, 0};
+            long long cnt[5] = {0, 0, 0, 0, 0};
             int off[5] = {0, 0, 0, 0, 0};
             long long total = 0;
             for (int k = M.max_mix + 1; k <= 4; ++k) {
                 const long long B = binom(m, k - 1);
                 off[k] = P > 1 ? ((a.rank - k - e) % P + P) % P : 0;
-                const long long cnt = B > off[k] ? (B - off[k] + P - 1) / P : 0;
-                seg[k] = cnt * M.n_tmpl[k];
-                total += seg[k];
+                cnt[k] = B > off[k] ? (B - off[k] + P - 1) / P : 0;
+                total += cnt[k];
             }
-            const long long stride = static_cast<long long>(G) * blockDim.x;
-            for (long long base = static_cast<long long>(bi) * blockDim.x + (threadIdx.x & ~31u);
-                 base < total; base += stride) {
-                long long g = base + lane_id();
-                bool ok = g < total;
-                uint64_t row = 0;
-                if (ok) {
-                    int k = M.max_mix + 1;
+            for (long long base = gw * 32; base < total; base += GW * 32) {
+                // level 1: lane = one support
+                const long long g = base + ln;
+                bool live = g < total;
+                int k = M.max_mix + 1;
+                unsigned packed = 0xFFFFFFFFu;  // members, ascending, one byte each (0xFF unused)
+                if (live) {
                     long long rem = g;
-                    while (rem >= seg[k]) rem -= seg[k++];
-                    const int nt = M.n_tmpl[k];
-                    const long long j = rem / nt;
-                    const int t = static_cast<int>(rem - j * nt);
-                    const long long r = off[k] + j * P;
+                    while (rem >= cnt[k]) rem -= cnt[k++];
+                    const long long r = off[k] + rem * P;
                     int idx[3];
                     unrank(r, k - 1, m, idx);
                     int S[4];
@@ -636,37 +686,57 @@ __global__ void __launch_bounds__(kThreads, 1) greedy_kernel(const __grid_consta
                         S[q++] = v;
                     }
                     if (!placed) S[q++] = ie;
-                    for (int j = 0; j < k && ok; ++j) {  // covered by an earlier event?
+                    for (int j = 0; j < k && live; ++j) {  // covered by an earlier event?
                         int ev = ev_of[S[j]];
                         if (ev >= 0 && ev < e) {
                             const uint64_t* mk = ev_mask + ev * 4;
                             bool sub = true;
                             for (int x = 0; x < k; ++x) sub &= ((mk[S[x] >> 6] >> (S[x] & 63)) & 1ull) != 0;
-                            if (sub) ok = false;
+                            if (sub) live = false;
                         }
                     }
-                    const uint64_t tp = M.tmpl[k][t];
-                    for (int j = 0; j < 4; ++j) {
-                        uint64_t code;
-                        if (j < k) {
-                            int p = static_cast<int>((tp >> (8 * (j + 1))) & 0xFF);
-                            ok &= (M.pat_mask[p] & ~M.feas_mask[S[j]]) == 0;
-                            code = static_cast<uint64_t>(S[j] * PP + p);
-                        } else {
-                            code = static_cast<uint64_t>(n * PP);
-                        }
-                        row |= code << (16 * j);
-                    }
+                    packed = 0;
+                    for (int j = 0; j < 4; ++j) packed |= static_cast<unsigned>(j < k ? S[j] : 0xFF) << (8 * j);
                 }
-                const unsigned b = __ballot_sync(0xffffffffu, ok);
-                if (b) {
-                    unsigned long long at = 0;
-                    if (lane_id() == 0) at = atomicAdd(&a.st->ext_count, static_cast<unsigned long long>(__popc(b)));
-                    at = __shfl_sync(0xffffffffu, at, 0);
-                    if (a.n_base + static_cast<long long>(at + __popc(b)) > a.cap) {
-                        if (lane_id() == 0) atomicExch(&a.st->status, static_cast<int>(kExtOverflow));
-                    } else if (ok) {
-                        a.rows[a.n_base + static_cast<long long>(at) + __popc(b & lanemask_lt())] = row;
+                // level 2: the warp takes each surviving support's templates
+                unsigned todo = __ballot_sync(0xffffffffu, live);
+                while (todo) {
+                    const int src = __ffs(todo) - 1;
+                    todo &= todo - 1;
+                    const unsigned sp = __shfl_sync(0xffffffffu, packed, src);
+                    const int kk = __shfl_sync(0xffffffffu, k, src);
+                    int S[4];
+                    for (int j = 0; j < 4; ++j) S[j] = static_cast<int>((sp >> (8 * j)) & 0xFFu);
+                    const int nt = M.n_tmpl[kk];
+                    for (int t0 = 0; t0 < nt; t0 += 32) {
+                        const int t = t0 + ln;
+                        bool ok = t < nt;
+                        uint64_t row = 0;
+                        if (ok) {
+                            const uint64_t tp = M.tmpl[kk][t];
+                            for (int j = 0; j < 4; ++j) {
+                                uint64_t code;
+                                if (j < kk) {
+                                    int p = static_cast<int>((tp >> (8 * (j + 1))) & 0xFF);
+                                    ok &= (M.pat_mask[p] & ~M.feas_mask[S[j]]) == 0;
+                                    code = static_cast<uint64_t>(S[j] * PP + p);
+                                } else {
+                                    code = static_cast<uint64_t>(n * PP);
+                                }
+                                row |= code << (16 * j);
+                            }
+                        }
+                        const unsigned b = __ballot_sync(0xffffffffu, ok);
+                        if (b) {
+                            unsigned long long at = 0;
+                            if (ln == 0) at = atomicAdd(&a.st->ext_count, static_cast<unsigned long long>(__popc(b)));
+                            at = __shfl_sync(0xffffffffu, at, 0);
+                            if (a.n_base + static_cast<long long>(at + __popc(b)) > a.cap) {
+                                if (ln == 0) atomicExch(&a.st->status, static_cast<int>(kExtOverflow));
+                            } else if (ok) {
+                                a.rows[a.n_base + static_cast<long long>(at) + __popc(b & lanemask_lt())] = row;
+                            }
+                        }
                     }
                 }
             }
@@ -768,24 +838,27 @@ __global__ void __launch_bounds__(kThreads, 1) greedy_kernel(const __grid_consta
             for (; j < cj; ++j) consider2(M, W, U, cache[j * blockDim.x + threadIdx.x], best);
             long long u = my0 + static_cast<long long>(cj) * GT;
             if (S > 0) {
-                // Rows beyond the on-chip cache, TMA-staged: the CTA streams contiguous 32 KB
-                // chunks (chunk c = bi, bi + G, ...) through an S-stage shared-memory ring; one
-                // elected thread issues cp.async.bulk, mbarriers signal full / empty stages, so
-                // up to S x 32 KB per SM are in flight while the warps score the previous stage.
+                // Rows beyond the on-chip cache, TMA-staged per WARP: the streamed region is cut
+                // into 2 KB warp-chunks (128 units: one consider8 per lane) dealt round-robin over
+                // the grid's warps; each warp keeps S chunks in flight in its own shared-memory
+                // slots (lane 0 issues cp.async.bulk, a per-warp mbarrier completes on the bytes),
+                // so the bytes in flight live in the TMA engine, not in registers, and no warp
+                // ever waits for another (no CTA-wide ring barrier).
+                const int w = static_cast<int>(threadIdx.x >> 5), ln = static_cast<int>(lane_id());
                 const long long base_u = static_cast<long long>(J) * GT;
-                const long long n_ch = NU > base_u ? (NU - base_u + kChunkUnits - 1) / kChunkUnits : 0;
-                const long long my_n = n_ch > bi ? (n_ch - bi + G - 1) / G : 0;
-                auto issue = [&](long long i) {
+                const long long n_ch = NU > base_u ? (NU - base_u + kWarpChunk - 1) / kWarpChunk : 0;
+                const long long gw = static_cast<long long>(bi) * NW + w, GW = static_cast<long long>(G) * NW;
+                const long long my_n = n_ch > gw ? (n_ch - gw + GW - 1) / GW : 0;
+                uint4* wr = ring + w * kWarpChunk;  // slot q of this warp: wr + q * kStageUnits
+                auto issue = [&](long long i) {     // lane 0
                     const unsigned long long kk = kchunk + static_cast<unsigned long long>(i);
                     const int slot = static_cast<int>(kk % S);
-                    if (kk >= static_cast<unsigned long long>(S))
-                        mbar_wait(&empty_bar[slot], static_cast<unsigned>((kk / S - 1) & 1ull));
-                    const long long u0 = base_u + (bi + i * G) * kChunkUnits;
-                    const long long cnt = min(static_cast<long long>(kChunkUnits), NU - u0);
-                    tma_load(ring + static_cast<long long>(slot) * kChunkUnits, rows4 + u0, static_cast<unsigned>(cnt * 16),
-                             &full_bar[slot]);
+                    const long long u0 = base_u + (gw + i * GW) * kWarpChunk;
+                    const long long cnt = min(static_cast<long long>(kWarpChunk), NU - u0);
+                    tma_load(wr + static_cast<long long>(slot) * kStageUnits, rows4 + u0, static_cast<unsigned>(cnt * 16),
+                             &wbar[slot][w]);
                 };
-                if (threadIdx.x == 0 && my_n > 0) {
+                if (ln == 0 && my_n > 0) {
                     asm volatile("fence.proxy.async.global;" ::: "memory");  // rows appended this launch
                     for (long long i = 0; i < my_n && i < S; ++i) issue(i);
                 }
@@ -795,40 +868,23 @@ __global__ void __launch_bounds__(kThreads, 1) greedy_kernel(const __grid_consta
                 for (long long i = 0; i < my_n; ++i) {
                     const unsigned long long kk = kchunk + static_cast<unsigned long long>(i);
                     const int slot = static_cast<int>(kk % S);
-                    mbar_wait(&full_bar[slot], static_cast<unsigned>((kk / S) & 1ull));
-                    const long long u0 = base_u + (bi + i * G) * kChunkUnits;
-                    const int cnt = static_cast<int>(min(static_cast<long long>(kChunkUnits), NU - u0));
-                    const uint4* st = ring + static_cast<long long>(slot) * kChunkUnits;
-                    const int t = threadIdx.x;
-                    const uint4 v0 = t < cnt ? st[t] : padv;
-                    const uint4 v1 = t + 512 < cnt ? st[t + 512] : padv;
-                    const uint4 v2 = t + 1024 < cnt ? st[t + 1024] : padv;
-                    const uint4 v3 = t + 1536 < cnt ? st[t + 1536] : padv;
-                    __syncwarp();
-                    if (lane_id() == 0) mbar_arrive(&empty_bar[slot]);
+                    mbar_wait(&wbar[slot][w], static_cast<unsigned>((kk / S) & 1ull));
+                    const long long u0 = base_u + (gw + i * GW) * kWarpChunk;
+                    const int cnt = static_cast<int>(min(static_cast<long long>(kWarpChunk), NU - u0));
+                    const uint4* st = wr + static_cast<long long>(slot) * kStageUnits;
+                    const uint4 v0 = ln < cnt ? st[ln] : padv;
+                    const uint4 v1 = ln + 32 < cnt ? st[ln + 32] : padv;
+                    const uint4 v2 = ln + 64 < cnt ? st[ln + 64] : padv;
+                    const uint4 v3 = ln + 96 < cnt ? st[ln + 96] : padv;
                     consider8(M, W, Wf, U, v0, v1, v2, v3, best, wfloor);
-                    if (threadIdx.x == 0 && i + S < my_n) issue(i + S);
+                    __syncwarp();  // every lane has consumed its slot data: the slot may be refilled
+                    if (ln == 0 && i + S < my_n) issue(i + S);
                 }
                 kchunk += static_cast<unsigned long long>(my_n);
                 u = NU;  // everything beyond the cache was streamed
             }
-            for (; u + 3 * GT < NU; u += 4 * GT) {
-                // Bulk L2 prefetch, a.prefetch iterations ahead: one thread per CTA pulls the
-                // CTA's next 8 KB stripes (contiguous: unit index = cta * blockDim + thread) into
-                // L2, so the loads below hit L2 instead of waiting on HBM latency.
-                if (threadIdx.x < 4 && a.prefetch > 0) {
-                    const long long pu = u - threadIdx.x + (a.prefetch * 4 + threadIdx.x) * GT;
-                    if (pu + static_cast<long long>(blockDim.x) <= NU)
-                        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(rows4 + pu),
-                                     "r"(static_cast<unsigned>(blockDim.x * 16))
-                                     : "memory");
-                }
-                // rows appended during this launch: L2-coherent loads (never the non-coherent path)
-                const uint4 v0 = ld_row4(rows4 + u, LOADM), v1 = ld_row4(rows4 + u + GT, LOADM),
-                            v2 = ld_row4(rows4 + u + 2 * GT, LOADM), v3 = ld_row4(rows4 + u + 3 * GT, LOADM);
-                consider8(M, W, Wf, U, v0, v1, v2, v3, best, wfloor);
-            }
-            for (; u < NU; u += GT) consider2(M, W, U, __ldcg(rows4 + u), best);
+            if (u < NU)
+                best = scan_stream(M, W, Wf, U, rows4, u, NU, GT, a.prefetch, a.pipeline, best, wfloor);
             if ((N & 1) && my0 == 0) consider(M, W, U, __ldcg(a.rows + N - 1), best);
         }
         prev_row = best.row;
@@ -965,11 +1021,11 @@ __global__ void __launch_bounds__(kThreads, 1) topk_kernel(const __grid_constant
 size_t greedy_smem_bytes(int n, int PP, int cache_units, int stages) {
     return static_cast<size_t>(greedy_layout(n, PP, cache_units, stages).total);
 }
-int greedy_chunk_bytes() { return kChunkUnits * 16; }
+int greedy_chunk_bytes() { return kStageUnits * 16; }
 
 size_t topk_smem_bytes(int n, int PP) { return static_cast<size_t>((n + 1) * PP + n) * 8 + 16; }
 
-const void* greedy_kernel_ptr() { return reinterpret_cast<const void*>(&greedy_kernel); }
+const void* greedy_kernel_ptr() { return reinterpret_cast<const void*>(&greedy_kernel<kThreads>); }
 const void* topk_kernel_ptr() { return reinterpret_cast<const void*>(&topk_kernel); }
 const void* enum_base_kernel_ptr() { return reinterpret_cast<const void*>(&enum_base_kernel); }
 int kernel_threads() { return kThreads; }

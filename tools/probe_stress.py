@@ -25,10 +25,13 @@ def main():
         st = ctx.stats()
         ok = mp.is_satisfied(mp.completion_of(plan, sv, ps))
         gbs = 8 * st["greedy_rows"] / (st["greedy_ms"] * 1e-3) / 1e9
-        print(f"  plan {1e3*(t3-t2):.1f} ms, GPUs {len(plan)} satisfied={ok}, steps {st['greedy_steps']}, events "
+        print(f"  plan {1e3*(t3-t2):.1f} ms, GPUs {len(plan)} sha {S.plan_sha(plan)} satisfied={ok}, steps {st['greedy_steps']}, events "
               f"{st['ext_events']}, ext rows {st['ext_rows']}, rows scored {st['greedy_rows']:.3e}, kernel "
               f"{st['greedy_ms']:.1f} ms, {st['greedy_rows']/st['greedy_ms']/1e6:.1f} Grows/s, {gbs:.0f} GB/s",
               flush=True)
+        if os.environ.get("MIGPLAN_PHASE_TIMERS"):
+            print("  phase ms (scan, barrier, reduce+update, maybe_extend, ext enum):",
+                  " ".join(f"{x:.1f}" for x in st["phase_ms"]), flush=True)
 
 
 if __name__ == "__main__":
