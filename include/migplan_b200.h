@@ -254,6 +254,16 @@ int mig_board_free(void* board, int32_t opened /* 1: from mig_board_open */);
  * resource of `device` that no live call holds; the next call allocates cold.  CPU
  * implementations: no-op. */
 int mig_device_cache_release(int32_t device);
+/* Every plan-returning call that fails with MIG_ERR_ARGUMENT because `cap` is too small sets
+ * *n_out to the plan's length and keeps the plan (per thread): this copies it out, so a caller
+ * never re-runs a stateful call (mig_crossover's Rng, mig_two_phase's time budget) to fetch a
+ * long plan. */
+int mig_last_plan(mig_config* out, int32_t cap, int32_t* n_out);
+/* Draw `step` of Philox stream `stream` under `seed` (the throughput-mode RNG: Philox4x32-10
+ * with counter (step, stream) and key seed, draw = word1 << 32 | word0).  on_device = 1
+ * evaluates it in a kernel (the product's device code path), 0 on the host; CPU
+ * implementations ignore on_device.  For known-answer tests. */
+int mig_philox_u64(uint64_t seed, uint64_t stream, uint64_t step, int32_t on_device, uint64_t* out);
 /* max_ctas > 0 caps the greedy grid of this context. */
 int mig_ctx_set_shard(mig_ctx* ctx, int32_t rank, int32_t n_ranks, void* const* boards, int32_t max_ctas);
 /* fast_algo on ALL ranks of a shard whose contexts share one GPU (ctxs in rank order):

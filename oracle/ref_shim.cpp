@@ -157,11 +157,14 @@ CompletionRates comp_of(const double* comp, int n, const mig_ctx* ctx) {
     return CompletionRates{std::vector<double>(comp, comp + n)};
 }
 
+thread_local std::vector<mig_config> g_pending;  // a plan that did not fit its caller's buffer
 int emit_plan(const std::vector<GpuConfig>& plan, const std::vector<ServiceSpec>& services, mig_config* out,
               int32_t cap, int32_t* n_out) {
     *n_out = static_cast<int32_t>(plan.size());
     for (size_t i = 0; i < plan.size() && static_cast<int32_t>(i) < cap; ++i) to_c(plan[i], services, &out[i]);
     if (static_cast<int32_t>(plan.size()) > cap) {
+        g_pending.resize(plan.size());
+        for (size_t i = 0; i < plan.size(); ++i) to_c(plan[i], services, &g_pending[i]);
         g_err = "output capacity too small";
         return MIG_ERR_ARGUMENT;
     }
@@ -840,6 +843,16 @@ int mig_ctx_stats(const mig_ctx*, mig_stats* out) {
 }
 void mig_ctx_reset_stats(mig_ctx*) {}
 int mig_device_cache_release(int32_t) { return MIG_OK; }
+int mig_last_plan(mig_config* out, int32_t cap, int32_t* n_out) {
+    *n_out = static_cast<int32_t>(g_pending.size());
+    if (*n_out > cap) return MIG_ERR_ARGUMENT;
+    std::copy(g_pending.begin(), g_pending.end(), out);
+    return MIG_OK;
+}
+int mig_philox_u64(uint64_t seed, uint64_t stream, uint64_t step, int32_t, uint64_t* out) {
+    *out = philox64_ref(seed, stream, step);
+    return MIG_OK;
+}
 
 // The reference keeps no per-step record: the instrumented replica re-runs the last
 // mig_fast_algo call's working-set growth (count_rows above).

@@ -154,6 +154,8 @@ SIGNATURES = {
     "mig_ctx_reset_stats": (None, [_P]),
     "mig_ctx_step_rows": (_I, [_P, _I64P, C.c_int32, _I32P]),
     "mig_device_cache_release": (_I, [C.c_int32]),
+    "mig_last_plan": (_I, [C.POINTER(ConfigC), C.c_int32, _I32P]),
+    "mig_philox_u64": (_I, [C.c_uint64, C.c_uint64, C.c_uint64, C.c_int32, C.POINTER(C.c_uint64)]),
 }
 
 # Exported by the reference shim only (bench.py reference arm, golden generation).

@@ -5,6 +5,7 @@
 
 #include "engine.hpp"
 #include "migplan_b200.h"
+#include "philox.cuh"
 #include "search.hpp"
 
 using namespace mgb;
@@ -102,10 +103,14 @@ Config from_c(const mig_config& c, int n_services) {
     return g;
 }
 
+thread_local std::vector<mig_config> g_pending;  // a plan that did not fit its caller's buffer
+
 int emit(const std::vector<Config>& plan, mig_config* out, int32_t cap, int32_t* n_out) {
     *n_out = static_cast<int32_t>(plan.size());
     for (size_t i = 0; i < plan.size() && static_cast<int32_t>(i) < cap; ++i) to_c(plan[i], &out[i]);
     if (static_cast<int32_t>(plan.size()) > cap) {
+        g_pending.resize(plan.size());
+        for (size_t i = 0; i < plan.size(); ++i) to_c(plan[i], &g_pending[i]);
         g_err = "output capacity too small";
         return MIG_ERR_ARGUMENT;
     }
@@ -489,6 +494,22 @@ int mig_board_alloc(int32_t device, int32_t n_ranks, void** board, uint8_t* ipc_
 }
 int mig_board_open(int32_t device, const uint8_t* ipc_handle, void** board) {
     return guarded([&] { *board = board_open(device, ipc_handle); });
+}
+int mig_philox_u64(uint64_t seed, uint64_t stream, uint64_t step, int32_t on_device, uint64_t* out) {
+    return guarded([&] {
+        if (on_device) {
+            device_info(0);  // a CUDA device or MIG_ERR_DEVICE
+            *out = philox_on_device(0, seed, stream, step);
+        } else {
+            *out = philox_u64(seed, stream, step);
+        }
+    });
+}
+int mig_last_plan(mig_config* out, int32_t cap, int32_t* n_out) {
+    *n_out = static_cast<int32_t>(g_pending.size());
+    if (*n_out > cap) return MIG_ERR_ARGUMENT;
+    std::copy(g_pending.begin(), g_pending.end(), out);
+    return MIG_OK;
 }
 int mig_device_cache_release(int32_t device) {
     return guarded([&] { release_device_cache(device); });

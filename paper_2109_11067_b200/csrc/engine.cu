@@ -505,6 +505,19 @@ ScratchPool& scratch_pool(int device) {
 
 // Frees every pooled slot and scratch buffer of `device` not in use by a live call (the
 // next context pays the cold allocations again: bench.py's cold e2e).
+const void* philox_kat_kernel_ptr();
+uint64_t philox_on_device(int device, uint64_t seed, uint64_t stream, uint64_t step) {
+    CK(cudaSetDevice(device));
+    unsigned long long* d = nullptr;
+    CK(cudaMalloc(&d, sizeof *d));
+    void* args[] = {&seed, &stream, &step, &d};
+    CK(cudaLaunchKernel(philox_kat_kernel_ptr(), 1, 1, args, 0, nullptr));
+    unsigned long long h = 0;
+    CK(cudaMemcpy(&h, d, sizeof h, cudaMemcpyDeviceToHost));
+    CK(cudaFree(d));
+    return h;
+}
+
 void release_device_cache(int device) {
     std::vector<Slot*> slots;
     {

@@ -34,6 +34,7 @@ void* board_alloc(int device, int n_ranks, unsigned char ipc_handle[64]);
 void* board_open(int device, const unsigned char ipc_handle[64]);
 void board_close(void* board, bool opened);
 void release_device_cache(int device);
+uint64_t philox_on_device(int device, uint64_t seed, uint64_t stream, uint64_t step);
 bool config_equal(const Config& a, const Config& b);
 
 struct Slot;

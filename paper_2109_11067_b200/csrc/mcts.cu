@@ -35,8 +35,16 @@ constexpr int kL1Slots = 256, kL1MaxK = 16, kL1Empty = -2, kL1Pending = -3;
 
 struct Mt64 {  // std::mt19937_64 (w 64, n 312, m 156, r 31)
     uint64_t mt[312];
+    uint64_t out[312];  // the current block's outputs, tempered when the block is twisted
     int idx;
 };
+
+__device__ __forceinline__ uint64_t mt_temper(uint64_t y) {
+    y ^= (y >> 29) & 0x5555555555555555ull;
+    y ^= (y << 17) & 0x71D67FFFEDA60000ull;
+    y ^= (y << 37) & 0xFFF7EEE000000000ull;
+    return y ^ (y >> 43);
+}
 
 __device__ void mt_seed(Mt64& g, uint64_t s) {
     g.mt[0] = s;
@@ -45,25 +53,60 @@ __device__ void mt_seed(Mt64& g, uint64_t s) {
 }
 
 __device__ uint64_t mt_next(Mt64& g) {
-    if (g.idx >= 312) {
+    if (g.idx >= 312) {  // serial twist (the rollout walk twists warp-parallel ahead of time)
         for (int i = 0; i < 312; ++i) {
             const uint64_t x = (g.mt[i] & 0xFFFFFFFF80000000ull) | (g.mt[(i + 1) % 312] & 0x7FFFFFFFull);
             uint64_t xa = x >> 1;
             if (x & 1ull) xa ^= 0xB5026F5AA96619E9ull;
             g.mt[i] = g.mt[(i + 156) % 312] ^ xa;
         }
+        for (int i = 0; i < 312; ++i) g.out[i] = mt_temper(g.mt[i]);
         g.idx = 0;
     }
-    uint64_t y = g.mt[g.idx++];
-    y ^= (y >> 29) & 0x5555555555555555ull;
-    y ^= (y << 17) & 0x71D67FFFEDA60000ull;
-    y ^= (y << 37) & 0xFFF7EEE000000000ull;
-    y ^= y >> 43;
-    return y;
+    return g.out[g.idx++];
 }
 
-__device__ uint64_t mt_pick(Mt64& g, uint64_t n) {  // pick_index, util.hpp:39-47
+// pick_index (util.hpp:39-47) constants for n <= kPickTab: the rejection limit
+// UINT64_MAX - UINT64_MAX % n, 2^32 mod n and Lemire's fastmod multiplier ceil(2^64 / n), so
+// r % n = ((r >> 32) % n * (2^32 % n) + (r & 0xffffffff) % n) % n costs three multiplies.
+constexpr int kPickTab = 256;
+struct PickTab {
+    uint64_t lim[kPickTab + 1];
+    uint64_t fm[kPickTab + 1];
+    unsigned p32[kPickTab + 1];
+};
+__device__ void pick_tab_init(PickTab& t) {
+    for (int m = threadIdx.x; m <= kPickTab; m += blockDim.x) {
+        if (m < 2) {
+            t.lim[m] = ~0ull;
+            t.fm[m] = 0;
+            t.p32[m] = 0;
+            continue;
+        }
+        const unsigned mu = static_cast<unsigned>(m);
+        const unsigned p32 = static_cast<unsigned>((1ull << 32) % mu);
+        const unsigned rmax = ((0xFFFFFFFFu % mu) * p32 + 0xFFFFFFFFu % mu) % mu;  // UINT64_MAX mod m
+        t.lim[m] = ~0ull - rmax;
+        t.fm[m] = ~0ull / mu + 1;
+        t.p32[m] = p32;
+    }
+}
+__device__ __forceinline__ unsigned fastmod32(unsigned x, uint64_t fm, unsigned d) {
+    return static_cast<unsigned>(__umul64hi(fm * x, d));
+}
+
+__device__ uint64_t mt_pick(Mt64& g, uint64_t n, const PickTab* t = nullptr) {  // pick_index, util.hpp:39-47
     if (n <= 1) return 0;
+    if (t && n <= static_cast<uint64_t>(kPickTab)) {
+        const unsigned m = static_cast<unsigned>(n);
+        const uint64_t limit = t->lim[m], fm = t->fm[m];
+        uint64_t r;
+        do {
+            r = mt_next(g);
+        } while (r >= limit);
+        const unsigned a = fastmod32(static_cast<unsigned>(r >> 32), fm, m), b = fastmod32(static_cast<unsigned>(r), fm, m);
+        return fastmod32(a * t->p32[m] + b, fm, m);
+    }
     if (n < (1ull << 16)) {  // the same arithmetic with 32-bit remainders (the search's n are small)
         const unsigned m = static_cast<unsigned>(n);
         const unsigned p32 = static_cast<unsigned>((1ull << 32) % m);            // 2^32 mod m
@@ -120,6 +163,7 @@ __device__ void mt_twist_warp(Mt64& g) {
         if (i < 312) g.mt[i] = v[k];
     }
     __syncwarp();
+    for (int i = lane; i < 312; i += 32) g.out[i] = mt_temper(g.mt[i]);
     if (lane == 0) g.idx = 0;
     __syncwarp();
 }
@@ -932,6 +976,8 @@ __global__ void __launch_bounds__(kMThreads, 1) mcts_kernel(const __grid_constan
         return got;
     };
     __shared__ Mt64 g;
+    __shared__ PickTab s_pick;
+    pick_tab_init(s_pick);
     __shared__ int s_node, s_leaf, s_expand, s_take, s_nch, s_done, s_est, s_miss, s_slot, s_abort, s_steps;
     __shared__ int s_edges, s_path, s_best, s_have, s_nodes, s_builds, s_iters, s_scored, s_expands;
     __shared__ long long s_expand_rows;
@@ -1066,7 +1112,7 @@ __global__ void __launch_bounds__(kMThreads, 1) mcts_kernel(const __grid_constan
                     if (lane == 0) {
                         const int take = min(L.pick_services, m);
                         for (int i = 0; i < take; ++i) {
-                            const int j = i + static_cast<int>(mt_pick(g, static_cast<uint64_t>(m - i)));
+                            const int j = i + static_cast<int>(mt_pick(g, static_cast<uint64_t>(m - i), &s_pick));
                             const int t = s_unsat[i];
                             s_unsat[i] = s_unsat[j];
                             s_unsat[j] = t;
@@ -1133,7 +1179,7 @@ __global__ void __launch_bounds__(kMThreads, 1) mcts_kernel(const __grid_constan
             if (tid == 0) {
                 const int nch = nnch[s_node];
                 if (nch > 0) {
-                    const int c = nfirst[s_node] + static_cast<int>(mt_pick(g, static_cast<uint64_t>(nch)));
+                    const int c = nfirst[s_node] + static_cast<int>(mt_pick(g, static_cast<uint64_t>(nch), &s_pick));
                     a.edges[s_edges++] = ncand[c];
                     a.pathnodes[s_path++] = c;
                     s_node = c;
@@ -1152,8 +1198,9 @@ __global__ void __launch_bounds__(kMThreads, 1) mcts_kernel(const __grid_constan
                     // when the block needs it: a miss's top-K, or the end of the rollout)
                     const bool regc = n <= 32;
                     double creg = regc && lane < n ? cur[lane] : 2.0;
-                    int r_steps = 0;  // lane 0's step count (written back when the walk pauses)
-                    if (lane == 0) r_steps = *reinterpret_cast<volatile int*>(&s_steps);
+                    // every lane keeps the step count; lane 0 writes it back when the walk pauses
+                    int r_steps = *reinterpret_cast<volatile int*>(&s_steps);
+                    __syncwarp();
                     if (lane == 0) s_miss = 0;
                     for (;;) {
                         if (g.idx >= 312) mt_twist_warp(g);  // the serial twist in mt_next stays the fallback
@@ -1168,36 +1215,38 @@ __global__ void __launch_bounds__(kMThreads, 1) mcts_kernel(const __grid_constan
                             }
                         }
                         int st = 0, idx = 0;  // st: 1 done, 2 miss, 3 abort
-                        if (lane == 0) {  // lane 0's state lives in registers; the block reads it after the walk
-                            if (!(kw[0] | kw[1] | kw[2] | kw[3])) {  // satisfied
+                        if (!(kw[0] | kw[1] | kw[2] | kw[3]) || r_steps >= max_depth) {  // satisfied / depth cap
+                            if (lane == 0) {
                                 s_done = 1;
-                                s_est = r_steps;
-                                st = 1;
-                            } else if (r_steps >= max_depth) {
-                                s_done = 1;
-                                s_est = max_depth;
-                                st = 1;
-                            } else {
-                                uint64_t h = 0x9e3779b97f4a7c15ull;
-                                for (int w = 0; w < 4; ++w) {
-                                    h ^= kw[w];
-                                    h *= 0xbf58476d1ce4e5b9ull;
-                                    h ^= h >> 31;
-                                }
-                                // level 1: the on-chip copy of the cache (keys + pools in shared memory)
-                                int l1 = -1, l1new = -1, slot = 0;
-                                bool miss = false;
-                                if (use_l1) {
-                                    unsigned q = static_cast<unsigned>(h >> 32) & (kL1Slots - 1);
-                                    for (int t = 0; t < kL1Slots; ++t, q = (q + 1) & (kL1Slots - 1)) {
-                                        if (l1_n[q] == kL1Empty) break;
-                                        if (l1_key[q][0] == kw[0] && l1_key[q][1] == kw[1] && l1_key[q][2] == kw[2] &&
-                                            l1_key[q][3] == kw[3]) {
-                                            l1 = static_cast<int>(q);
-                                            break;
-                                        }
+                                s_est = (kw[0] | kw[1] | kw[2] | kw[3]) ? max_depth : r_steps;
+                            }
+                            st = 1;
+                        } else {
+                            // the cache's own hash (not reference-visible): one multiply
+                            uint64_t h = (kw[0] ^ (kw[1] << 16 | kw[1] >> 48) ^ (kw[2] << 32 | kw[2] >> 32) ^
+                                          (kw[3] << 48 | kw[3] >> 16)) * 0x9e3779b97f4a7c15ull;
+                            h ^= h >> 29;
+                            // level 1: the on-chip copy of the cache, probed 32 slots at a time by
+                            // the whole warp (linear probing: the key lies before the first empty slot)
+                            int l1 = -1;
+                            if (use_l1) {
+                                const unsigned q0 = static_cast<unsigned>(h >> 32) & (kL1Slots - 1);
+                                for (int b0 = 0; b0 < kL1Slots; b0 += 32) {
+                                    const unsigned q = (q0 + b0 + lane) & (kL1Slots - 1);
+                                    const bool empty = l1_n[q] == kL1Empty;
+                                    const bool match = !empty && l1_key[q][0] == kw[0] && l1_key[q][1] == kw[1] &&
+                                                       l1_key[q][2] == kw[2] && l1_key[q][3] == kw[3];
+                                    const unsigned bm = __ballot_sync(0xffffffffu, match);
+                                    if (bm) {
+                                        l1 = static_cast<int>((q0 + b0 + __ffs(bm) - 1) & (kL1Slots - 1));
+                                        break;
                                     }
+                                    if (__ballot_sync(0xffffffffu, empty)) break;
                                 }
+                            }
+                            if (lane == 0) {  // lane 0's state lives in registers; the block reads it after the walk
+                                int l1new = -1, slot = 0;
+                                bool miss = false;
                                 if (l1 < 0) {  // level 2: the global table (source of truth)
                                     unsigned sl = static_cast<unsigned>(h) & a.tab_mask;
                                     for (unsigned t = 0;; ++t, sl = (sl + 1) & a.tab_mask) {
@@ -1233,10 +1282,10 @@ __global__ void __launch_bounds__(kMThreads, 1) mcts_kernel(const __grid_constan
                                         s_abort = 1;  // "rollout: no candidate config serves the remaining demand"
                                         st = 3;
                                     } else {
-                                        const unsigned pk = static_cast<unsigned>(mt_pick(g, static_cast<uint64_t>(pn)));
+                                        const unsigned pk = static_cast<unsigned>(mt_pick(g, static_cast<uint64_t>(pn), &s_pick));
                                         idx = static_cast<int>(l1 >= 0 ? l1_pool[l1][pk]
                                                                        : a.pool[static_cast<long long>(slot) * K + pk]);
-                                        a.picked[r_steps++] = idx;
+                                        a.picked[r_steps] = idx;
                                     }
                                 }
                                 if (st == 2) {  // the block builds this key's pool
@@ -1245,13 +1294,14 @@ __global__ void __launch_bounds__(kMThreads, 1) mcts_kernel(const __grid_constan
                                     s_l1new = l1new;
                                 }
                             }
-                            if (st) s_steps = r_steps;
                         }
                         st = __shfl_sync(0xffffffffu, st, 0);
                         if (st) {
+                            if (lane == 0) s_steps = r_steps;
                             if (regc && lane < n) cur[lane] = creg;
                             break;
                         }
+                        ++r_steps;
                         idx = __shfl_sync(0xffffffffu, idx, 0);
                         if (regc) {  // rollout add (mcts.hpp:139) in the owning lanes
                             const uint64_t row = rowat(idx);

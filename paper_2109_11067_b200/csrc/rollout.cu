@@ -435,4 +435,13 @@ const void* rollout_kernel_ptr(int n) {
 }
 int rollout_threads() { return kRThreads; }
 
+namespace {
+__global__ void philox_kat_kernel(uint64_t seed, uint64_t stream, uint64_t step, unsigned long long* out) {
+    *out = philox_u64(seed, stream, step);
+}
+}  // namespace
+
+// One Philox draw on the device code path (known-answer tests of philox.cuh, engine.cu).
+const void* philox_kat_kernel_ptr() { return reinterpret_cast<const void*>(&philox_kat_kernel); }
+
 }  // namespace mgb

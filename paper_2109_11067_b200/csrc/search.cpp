@@ -112,18 +112,14 @@ int rollout(Engine& e, const std::vector<double>& comp, const MctsParams& p, Rol
 
 // mcts_solve, mcts.hpp:148-252: fast_ref and the descent completion on the greedy kernel, the
 // search loop itself device-resident (mcts.cu: one CTA, the reference's mt19937_64 stream on
-// the device).  MIGPLAN_HOST_MCTS=1 selects the host-driven loop below (every top-K a launch).
-std::vector<Config> mcts_solve_host(Engine& e, const std::vector<double>& comp, const MctsParams& p, uint64_t seed,
-                                    const std::function<void(int, int, int, int)>& trace,
-                                    std::vector<Config> fast_ref);
-
+// the device).  The device top-K holds k <= 32 candidates: larger k is rejected (ArgumentError)
+// rather than run on a host loop.
 std::vector<Config> mcts_solve(Engine& e, const std::vector<double>& comp, const MctsParams& p, uint64_t seed,
                                const std::function<void(int, int, int, int)>& trace) {
     if (satisfied(comp)) return {};
     std::vector<Config> fast_ref = fast_plan(e, comp);
     if (p.budget_iters <= 0) return fast_ref;
-    static const bool host_loop = std::getenv("MIGPLAN_HOST_MCTS") != nullptr;
-    if (host_loop || p.topk < 1 || p.topk > 32) return mcts_solve_host(e, comp, p, seed, trace, std::move(fast_ref));
+    if (p.topk < 1 || p.topk > 32) throw ArgumentError("mcts_solve: topk must be in [1, 32] (device top-K)");
     const int l_ref = static_cast<int>(fast_ref.size());
     MctsDeviceResult r = e.mcts_device(comp, p.budget_iters, p.topk, p.pick_services, p.ucb_c, seed, l_ref);
     if (trace)
@@ -140,106 +136,6 @@ std::vector<Config> mcts_solve(Engine& e, const std::vector<double>& comp, const
     if (r.best_len >= 0 && static_cast<size_t>(r.best_len) < answer.size()) {
         answer.clear();
         for (long long idx : r.best) answer.push_back(e.config_of(e.base_rows()[idx]));
-    }
-    return answer;
-}
-
-std::vector<Config> mcts_solve_host(Engine& e, const std::vector<double>& comp, const MctsParams& p, uint64_t seed,
-                                    const std::function<void(int, int, int, int)>& trace,
-                                    std::vector<Config> fast_ref) {
-
-    const int l_ref = static_cast<int>(fast_ref.size());
-    const int max_depth = 2 * l_ref;
-    Rng rng(mix_seed(seed, 0x6d637473));
-    RolloutCache cache;
-    Node root(comp);
-    std::vector<long long> best_path;
-    bool have_best = false;
-
-    auto ucb_pick = [&](Node& node) -> Node::Edge& {
-        double log_n = std::log(std::max(1, node.visits));
-        int pick = -1;
-        double best = -1.0;
-        for (size_t i = 0; i < node.children.size(); ++i) {
-            const Node* c = node.children[i].node.get();
-            if (c->visits == 0) return node.children[i];
-            double mean = c->value_sum / c->visits;
-            double bonus = p.ucb_c * std::sqrt(log_n / c->visits);
-            double v = mean + bonus;
-            if (v > best) {
-                best = v;
-                pick = static_cast<int>(i);
-            }
-        }
-        return node.children[pick];
-    };
-
-    for (int iter = 0; iter < p.budget_iters; ++iter) {
-        std::vector<Node*> path{&root};
-        std::vector<long long> edges;
-        Node* node = &root;
-        while (node->expanded && !node->leaf && !node->children.empty()) {
-            Node::Edge& ed = ucb_pick(*node);
-            edges.push_back(ed.cand);
-            node = ed.node.get();
-            path.push_back(node);
-        }
-        int est;
-        if (node->leaf) {
-            est = 0;
-            if (!have_best || edges.size() < best_path.size()) {
-                best_path = edges;
-                have_best = true;
-            }
-        } else {
-            if (!node->expanded) expand(e, *node, p, rng);
-            if (!node->children.empty()) {
-                size_t pick = pick_index(rng, node->children.size());
-                Node::Edge& ed = node->children[pick];
-                edges.push_back(ed.cand);
-                node = ed.node.get();
-                path.push_back(node);
-            }
-            std::vector<long long> picked;
-            est = rollout(e, node->comp, p, cache, rng, max_depth, &picked);
-            bool complete = node->leaf || static_cast<int>(picked.size()) == est;
-            if (complete && est < max_depth) {
-                std::vector<long long> full = edges;
-                full.insert(full.end(), picked.begin(), picked.end());
-                if (!have_best || full.size() < best_path.size()) {
-                    best_path = std::move(full);
-                    have_best = true;
-                }
-            }
-        }
-        int total_len = static_cast<int>(edges.size()) + est;
-        double reward = total_len > 0 ? std::min(1.0, static_cast<double>(l_ref) / total_len) : 1.0;
-        for (Node* x : path) {
-            x->visits += 1;
-            x->value_sum += reward;
-        }
-        if (trace) trace(iter, static_cast<int>(edges.size()), est, have_best ? static_cast<int>(best_path.size()) : -1);
-    }
-
-    std::vector<long long> descent;
-    Node* node = &root;
-    while (node->expanded && !node->leaf && !node->children.empty()) {
-        int pick = 0;
-        for (size_t i = 1; i < node->children.size(); ++i)
-            if (node->children[i].node->visits > node->children[pick].node->visits) pick = static_cast<int>(i);
-        descent.push_back(node->children[pick].cand);
-        node = node->children[pick].node.get();
-    }
-    std::vector<Config> via_descent;
-    for (long long idx : descent) via_descent.push_back(e.config_of(e.base_rows()[idx]));
-    if (!node->leaf)
-        for (auto& c : fast_plan(e, node->comp)) via_descent.push_back(c);
-
-    std::vector<Config> answer = std::move(fast_ref);
-    if (via_descent.size() < answer.size()) answer = std::move(via_descent);
-    if (have_best && best_path.size() < answer.size()) {
-        answer.clear();
-        for (long long idx : best_path) answer.push_back(e.config_of(e.base_rows()[idx]));
     }
     return answer;
 }
@@ -602,8 +498,7 @@ std::vector<Config> two_phase(Engine& e, const GaParams& p,
         if (elapsed() >= p.time_budget_s) break;
         if (stall >= p.stall_rounds) break;
         size_t n_parents = std::min(pop.size(), (static_cast<size_t>(p.population) + 1) / 2);
-        static const bool host_loop = std::getenv("MIGPLAN_HOST_MCTS") != nullptr;
-        if (!host_loop && p.slow.topk >= 1 && p.slow.topk <= 32) {  // phased, device-batched children
+        if (p.slow.topk >= 1 && p.slow.topk <= 32) {  // phased, device-batched children
             std::vector<Chromosome> children = breed_round(e, pop, n_parents, round, p);
             for (auto& c : children) pop.push_back(std::move(c));
             std::stable_sort(pop.begin(), pop.end(), fitter);

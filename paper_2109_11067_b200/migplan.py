@@ -689,16 +689,18 @@ def release_device_cache(device: int = 0, backend=None) -> None:
 
 
 def _run_plan(ctx: PlanContext, call) -> list[GpuConfig]:
-    cap = 4096  # a longer plan is re-run with the exact size (MIG_ERR_ARGUMENT + n_out)
-    while True:
+    cap = 4096
+    buf = (abi.ConfigC * cap)()
+    n = C.c_int32()
+    rc = call(buf, cap, n)
+    if rc == abi.MIG_ERR_ARGUMENT and n.value > cap:
+        # a longer plan: the library kept it (mig_last_plan), so the call is not re-run (a
+        # re-run would consume an Rng's draws or a time budget a second time)
+        cap = n.value
         buf = (abi.ConfigC * cap)()
-        n = C.c_int32()
-        rc = call(buf, cap, n)
-        if rc == abi.MIG_ERR_ARGUMENT and n.value > cap:
-            cap = n.value
-            continue
-        ctx.backend.check(rc)
-        return ctx._configs_from_buf(buf, n.value)
+        rc = ctx.backend.lib.mig_last_plan(buf, cap, C.byref(n))
+    ctx.backend.check(rc)
+    return ctx._configs_from_buf(buf, n.value)
 
 
 # ---------------------------------------------------------------- greedy (greedy.hpp)

@@ -80,18 +80,41 @@ def test_rollouts_zero_and_satisfied(impl):
         mp.rollouts(mp.zero_completion(len(sv)), ctx, mp.RolloutParams(n_rollouts=8, topk=33))
 
 
-def test_philox_known_answer():
+KAT = [  # Random123 kat_vectors for philox4x32_10 as (seed, stream, step) -> word1:word0
+    (0, 0, 0, 0xe169c58d6627e8d5),                                   # ctr = 0, key = 0
+    (0xFFFFFFFFFFFFFFFF, 0xFFFFFFFFFFFFFFFF, 0xFFFFFFFFFFFFFFFF,
+     0x41c83b0e408f276d),                                            # ctr = ~0, key = ~0
+    (0x299f31d0a4093822, 0x0370734413198a2e, 0x85a308d3243f6a88,
+     0x94fdccebd16cfe09),                                            # the pi-digits vector
+]
+
+
+def philox_draw(b, seed, stream, step, on_device):
+    import ctypes as C
+
+    out = C.c_uint64()
+    b.check(b.lib.mig_philox_u64(seed, stream, step, on_device, C.byref(out)))
+    return out.value
+
+
+def test_philox_known_answer_host(impl):
     """Philox4x32-10 known-answer vectors (Random123 kat_vectors: ctr=0/key=0, ctr=~0/key=~0,
-    and the pi-digits vector) checked against the product's header via a tiny host port."""
-    def philox(c, k):
-        c, k = list(c), list(k)
-        for _ in range(10):
-            a, b = 0xD2511F53 * c[0], 0xCD9E8D57 * c[2]
-            c = [((b >> 32) ^ c[1] ^ k[0]) & 0xFFFFFFFF, b & 0xFFFFFFFF, ((a >> 32) ^ c[3] ^ k[1]) & 0xFFFFFFFF,
-                 a & 0xFFFFFFFF]
-            k = [(k[0] + 0x9E3779B9) & 0xFFFFFFFF, (k[1] + 0xBB67AE85) & 0xFFFFFFFF]
-        return c
-    assert philox([0, 0, 0, 0], [0, 0]) == [0x6627e8d5, 0xe169c58d, 0xbc57ac4c, 0x9b00dbd8]
-    assert philox([0xffffffff] * 4, [0xffffffff] * 2) == [0x408f276d, 0x41c83b0e, 0xa20bc7c6, 0x6d5451fd]
-    assert philox([0x243f6a88, 0x85a308d3, 0x13198a2e, 0x03707344], [0xa4093822, 0x299f31d0]) == \
-        [0xd16cfe09, 0x94fdcceb, 0x5001e420, 0x24126ea1]
+    and the pi-digits vector) through each library's own Philox: the product's philox.cuh
+    compiled for the host (no GPU needed), the restatement's and the shim's."""
+    for seed, stream, step, want in KAT:
+        assert philox_draw(impl, seed, stream, step, 0) == want
+
+
+@pytest.mark.gpu
+def test_philox_known_answer_device():
+    """The same vectors through philox.cuh's DEVICE code path (one-thread kernel)."""
+    b = S.product_backend()
+    for seed, stream, step, want in KAT:
+        assert philox_draw(b, seed, stream, step, 1) == want
+
+
+def test_philox_product_host_without_gpu():
+    """The product library answers host-path draws even without a CUDA device."""
+    b = S.product_backend()
+    for seed, stream, step, want in KAT:
+        assert philox_draw(b, seed, stream, step, 0) == want

@@ -255,3 +255,39 @@ def test_rows_scored_counts_match_checker(kind):
         st = ctx.stats()
         counts.append((st["greedy_rows"], st["topk_rows"], st["topk_calls"], st["greedy_steps"]))
     assert counts[0] == counts[1]
+
+
+def test_long_plan_is_fetched_not_recomputed(impl):
+    """A plan longer than the caller's buffer: MIG_ERR_ARGUMENT with the length, then
+    mig_last_plan returns it — the stateful call (here crossover's Rng) is not re-run."""
+    import ctypes as C
+
+    from paper_2109_11067_b200 import abi
+
+    ps = S.profiles()
+    sv = S.fixture_services("slos_day", ps)
+    ctx = mp.make_plan_context(sv, ps, mp.PartitionRuleSet.defaults(), backend=impl)
+    parent = mp.evaluate_chromosome(mp.fast_algo(mp.zero_completion(len(sv)), ctx), ctx)
+    params = mp.GaParams(erase_fraction=0.5)
+    arr = ctx._configs_to_c(parent.gpus)
+
+    def cross(rng, cap):
+        out = (abi.ConfigC * max(cap, 1))()
+        n = C.c_int32()
+        rc = ctx.backend.lib.mig_crossover(ctx._p, arr, len(parent.gpus), 0, C.byref(params.to_c()), rng._p, out, cap,
+                                           C.byref(n))
+        return rc, n.value, out
+
+    rc, n_big, out_big = cross(mp.Rng(5, ctx.backend), 4096)
+    assert rc == 0 and n_big > 4
+    r2 = mp.Rng(5, ctx.backend)
+    rc, n, _ = cross(r2, 4)
+    assert rc == abi.MIG_ERR_ARGUMENT and n == n_big
+    after = r2()  # the Rng advanced exactly as in one full call
+    r3 = mp.Rng(5, ctx.backend)
+    cross(r3, 4096)
+    assert after == r3()
+    buf = (abi.ConfigC * n)()
+    got = C.c_int32()
+    assert ctx.backend.lib.mig_last_plan(buf, n, C.byref(got)) == 0 and got.value == n
+    assert ctx._configs_from_buf(buf, n) == ctx._configs_from_buf(out_big, n_big)
