@@ -316,6 +316,17 @@ int mig_two_phase(mig_ctx* ctx, const mig_ga_params* params, mig_config* out, in
 int mig_two_phase_parallel(mig_ctx* ctx, const mig_ga_params* params, mig_config* out, int32_t cap, int32_t* n_out,
                            mig_ga_log_fn log, void* user);
 
+/* The same throughput-mode two_phase with crossover's slow procedure = the throughput
+ * mcts_solve (mig_mcts_solve_parallel) instead of FastProcedure — BASELINE config #3's
+ * "greedy -> GA -> MCTS" pipeline with a fixed Philox seed: child i of round r refills its
+ * residual with the shorter of fast_algo(residual) and the best of slow->n_rollouts
+ * root-parallel rollouts (pool size slow->topk, depth cap 2 x |fast refill|, batches of
+ * slow->batch, ids from slow->id_offset) under Philox key mix_seed(params->seed,
+ * (r << 20) + i); the fast refill wins ties (mcts.hpp:245-251).  slow->seed, ->max_depth
+ * and ->table_log2 are ignored. */
+int mig_two_phase_parallel_mcts(mig_ctx* ctx, const mig_ga_params* params, const mig_rollout_params* slow,
+                                mig_config* out, int32_t cap, int32_t* n_out, mig_ga_log_fn log, void* user);
+
 /* ---- eval bench helpers (bench.hpp) ---- */
 /* lower_bound(services, profiles), bench.hpp:93-108 */
 int mig_lower_bound(const mig_ctx* ctx, int32_t* out);

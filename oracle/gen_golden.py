@@ -418,7 +418,38 @@ def gen_rollouts_big(ref):
     return res
 
 
-SECTIONS = {"ga_big": gen_ga_big, "mcts_big": gen_mcts_big, "greedy_prefix": gen_greedy_prefix,
+def gen_ga_parallel_mcts(ref):
+    """Throughput-mode two_phase with the throughput mcts_solve refill
+    (mig_two_phase_parallel_mcts; BASELINE config #3's greedy -> GA -> MCTS pipeline with a
+    fixed Philox seed): the reference's operators, fast_algo and rollout primitives under the
+    product's Philox draw rule."""
+    res = {}
+    ps = S.profiles()
+    tw, sv6 = S.random_workload(6, 77)
+    p3, g3 = S.gen(24, 8.7)
+    cases = [("slos_day", ps, S.fixture_services("slos_day", ps), dict(seed=24, max_rounds=4),
+              dict(n_rollouts=64, topk=10)),
+             ("rand6", tw, sv6, dict(seed=9, max_rounds=5, erase_fraction=0.25), dict(n_rollouts=128, topk=4)),
+             ("slos_24", ps, S.fixture_services("slos_24", ps), dict(seed=24, max_rounds=3),
+              dict(n_rollouts=256, topk=10, batch=128)),
+             ("gen24_8.7", p3, g3, dict(seed=4242, max_rounds=2), dict(n_rollouts=256, topk=10))]
+    only = os.environ.get("GOLDEN_ONLY")
+    for name, p, sv, kw, slow in cases:
+        if only and name not in only.split(","):
+            continue
+        t = time.time()
+        logs = []
+        dep = mp.two_phase_parallel(sv, p, mp.PartitionRuleSet.defaults(), mp.GaParams(time_budget_s=1e9, **kw),
+                                    log=lambda l: logs.append([l.round, l.best_gpus, l.best_slack.hex(), l.improved]),
+                                    backend=ref, slow=mp.RolloutParams(**slow))
+        res[name] = {"store": store_name(p), "services": svc_json(sv), "params": kw, "slow": slow,
+                     "plan": S.plan_key([g.config for g in dep.gpus]), "log": logs,
+                     "ref_wall_s": round(time.time() - t, 3)}
+        print(f"ga_parallel_mcts {name}: {len(dep.gpus)} GPUs ({time.time() - t:.1f}s)", flush=True)
+    return res
+
+
+SECTIONS = {"ga_parallel_mcts": gen_ga_parallel_mcts, "ga_big": gen_ga_big, "mcts_big": gen_mcts_big, "greedy_prefix": gen_greedy_prefix,
             "pools_big": gen_pools_big, "rollouts_big": gen_rollouts_big,
 "baseline": gen_baseline, "brute_force": gen_brute_force, "greedy": gen_greedy, "mcts": gen_mcts, "ga": gen_ga, "topk": gen_topk, "partitions": gen_partitions,
             "greedy_big": gen_greedy_big, "rollouts": gen_rollouts, "ga_parallel": gen_ga_parallel}

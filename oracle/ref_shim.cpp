@@ -572,8 +572,15 @@ Chromosome mutate_philox(const Chromosome& parent, const GaParams& params, const
     return child;
 }
 
+RefPar ref_par(const PlanContext& ctx, const CompletionRates& comp, long long R, int K, int depth, uint64_t seed,
+              long long id0, long long batch, int32_t* lengths);
+
+// slow == nullptr: FastProcedure refill.  Otherwise the throughput mcts_solve
+// (mig_mcts_solve_parallel): the shorter of fast_algo(residual) and the best of
+// slow->n_rollouts root-parallel rollouts under Philox key `rseed` (fast wins ties).
 Chromosome crossover_philox(const Chromosome& parent, const PlanContext& ctx, const GaParams& params,
-                            const std::function<size_t(size_t)>& dr, size_t lcap) {  // ga.hpp:51-77, FastProcedure
+                            const std::function<size_t(size_t)>& dr, size_t lcap,
+                            const mig_rollout_params* slow = nullptr, uint64_t rseed = 0) {  // ga.hpp:51-77
     size_t n = parent.gpus.size();
     size_t erase = n == 0 ? 0 : static_cast<size_t>(std::ceil(params.erase_fraction * static_cast<double>(n)));
     if (erase == 0) return parent;
@@ -587,7 +594,16 @@ Chromosome crossover_philox(const Chromosome& parent, const PlanContext& ctx, co
         if (!erased[i]) survivors.push_back(parent.gpus[i]);
     try {
         CompletionRates residual = completion_of(survivors, ctx.services, *ctx.profiles);
-        for (auto& cfg : fast_algo(residual, ctx)) survivors.push_back(std::move(cfg));
+        std::vector<GpuConfig> refill = fast_algo(residual, ctx);
+        if (slow && !is_satisfied(residual)) {
+            RefPar r = ref_par(ctx, residual, slow->n_rollouts, slow->topk, 2 * static_cast<int>(refill.size()), rseed,
+                               slow->id_offset, slow->batch, nullptr);
+            if (r.best_len >= 0 && static_cast<size_t>(r.best_len) < refill.size()) {
+                refill.clear();
+                for (int i : r.path) refill.push_back(ctx.pool.items[i].config);
+            }
+        }
+        for (auto& cfg : refill) survivors.push_back(std::move(cfg));
         if (survivors.size() > lcap) return parent;
         return evaluate_chromosome(std::move(survivors), ctx);
     } catch (const PlanningError&) {
@@ -596,7 +612,8 @@ Chromosome crossover_philox(const Chromosome& parent, const PlanContext& ctx, co
 }
 
 std::vector<GpuConfig> two_phase_philox(const PlanContext& ctx, const GaParams& params,
-                                        const std::function<void(const GaRoundLog&)>& log) {
+                                        const std::function<void(const GaRoundLog&)>& log,
+                                        const mig_rollout_params* slow = nullptr) {
     auto t0 = std::chrono::steady_clock::now();
     auto elapsed = [&] { return std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count(); };
     std::vector<GpuConfig> seed_cfg = fast_algo(zero_completion(ctx.services.size()), ctx);
@@ -620,7 +637,8 @@ std::vector<GpuConfig> two_phase_philox(const PlanContext& ctx, const GaParams& 
             std::function<size_t(size_t)> dr = [&](size_t m) {
                 return static_cast<size_t>(((unsigned __int128)philox64_ref(params.seed, stream, t++) * m) >> 64);
             };
-            children[i] = crossover_philox(mutate_philox(pop[i], params, dr), ctx, params, dr, lcap);
+            children[i] = crossover_philox(mutate_philox(pop[i], params, dr), ctx, params, dr, lcap, slow,
+                                           mix_seed(params.seed, stream));
         }
         for (auto& c : children) pop.push_back(std::move(c));
         std::stable_sort(pop.begin(), pop.end(), fitter);
@@ -797,6 +815,22 @@ int mig_two_phase_parallel(mig_ctx* ctx, const mig_ga_params* params, mig_config
                 log(user, r.round, r.best_gpus, r.best_slack, r.improved ? 1 : 0, r.elapsed_s);
             };
         rc = emit_plan(two_phase_philox(ctx->plan, ga_of(params), lg), ctx->services, out, cap, n_out);
+    });
+    return g != MIG_OK ? g : rc;
+}
+
+int mig_two_phase_parallel_mcts(mig_ctx* ctx, const mig_ga_params* params, const mig_rollout_params* slow,
+                                mig_config* out, int32_t cap, int32_t* n_out, mig_ga_log_fn log, void* user) {
+    int rc = MIG_OK;
+    int g = guarded([&] {
+        if (!slow) throw std::invalid_argument("null rollout params");
+        if (slow->topk < 1 || slow->topk > 32) throw std::invalid_argument("rollouts: topk must be in [1, 32]");
+        std::function<void(const GaRoundLog&)> lg = nullptr;
+        if (log)
+            lg = [&](const GaRoundLog& r) {
+                log(user, r.round, r.best_gpus, r.best_slack, r.improved ? 1 : 0, r.elapsed_s);
+            };
+        rc = emit_plan(two_phase_philox(ctx->plan, ga_of(params), lg, slow), ctx->services, out, cap, n_out);
     });
     return g != MIG_OK ? g : rc;
 }

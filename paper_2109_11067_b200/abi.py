@@ -147,6 +147,8 @@ SIGNATURES = {
                            C.POINTER(ConfigC), C.c_int32, _I32P]),
     "mig_two_phase": (_I, [_P, C.POINTER(GaParamsC), C.POINTER(ConfigC), C.c_int32, _I32P, GA_LOG, _P]),
     "mig_two_phase_parallel": (_I, [_P, C.POINTER(GaParamsC), C.POINTER(ConfigC), C.c_int32, _I32P, GA_LOG, _P]),
+    "mig_two_phase_parallel_mcts": (_I, [_P, C.POINTER(GaParamsC), C.POINTER(RolloutParamsC), C.POINTER(ConfigC),
+                                         C.c_int32, _I32P, GA_LOG, _P]),
     "mig_lower_bound": (_I, [_P, _I32P]),
     "mig_baseline": (_I, [_P, C.c_int32, _P, C.c_int32, _I32P]),
     "mig_brute_force_optimum": (_I, [_P, C.c_int32, C.c_int64, _P, C.c_int32, _I32P, _I32P]),

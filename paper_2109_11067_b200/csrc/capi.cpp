@@ -607,6 +607,26 @@ int mig_two_phase_parallel(mig_ctx* ctx, const mig_ga_params* params, mig_config
     return g != MIG_OK ? g : rc;
 }
 
+int mig_two_phase_parallel_mcts(mig_ctx* ctx, const mig_ga_params* params, const mig_rollout_params* slow,
+                                mig_config* out, int32_t cap, int32_t* n_out, mig_ga_log_fn log, void* user) {
+    int rc = MIG_OK;
+    int g = guarded([&] {
+        if (!slow) throw ArgumentError("null rollout params");
+        if (slow->topk < 1 || slow->topk > 32) throw ArgumentError("rollouts: topk must be in [1, 32]");
+        std::function<void(int, int, double, bool, double)> lg = nullptr;
+        if (log) lg = [&](int r, int b, double s, bool imp, double el) { log(user, r, b, s, imp ? 1 : 0, el); };
+        RolloutRefill rf;
+        rf.n_rollouts = slow->n_rollouts;
+        rf.topk = slow->topk;
+        rf.id_offset = slow->id_offset;
+        rf.batch = slow->batch;
+        rf.table_log2 = slow->table_log2;
+        auto plan = two_phase_parallel(*ctx->e, ga_of(params), lg, &rf);
+        rc = emit(plan, out, cap, n_out);
+    });
+    return g != MIG_OK ? g : rc;
+}
+
 int mig_lower_bound(const mig_ctx* ctx, int32_t* out) {
     return guarded([&] {  // bench.hpp:93-108 over every constructible size {1,2,3,4,7}
         const Model& m = ctx->e->model();

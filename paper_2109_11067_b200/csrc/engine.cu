@@ -1681,6 +1681,7 @@ struct GaRun {
     unsigned* scratch = nullptr;
     const uint64_t** refill = nullptr;
     int* refill_n = nullptr;
+    uint64_t* alt = nullptr;  // per-child refill rows taken from a rollout (throughput MCTS refill)
     int* child_len = nullptr;
     double* child_slack = nullptr;
     std::vector<void*> owned;
@@ -1711,6 +1712,7 @@ GaRun* Engine::ga_begin(int P, int L_cap) {
     r->scratch = static_cast<unsigned*>(al(sizeof(unsigned) * 8 * L_cap * r->nch));
     r->refill = static_cast<const uint64_t**>(al(sizeof(void*) * r->nch));
     r->refill_n = static_cast<int*>(al(sizeof(int) * r->nch));
+    r->alt = static_cast<uint64_t*>(al(rowb * r->nch));
     r->child_len = static_cast<int*>(al(sizeof(int) * r->nch));
     r->child_slack = static_cast<double*>(al(sizeof(double) * r->nch));
     static std::once_flag attrs;
@@ -1738,7 +1740,7 @@ std::vector<uint64_t> Engine::ga_get(GaRun* r, int buf, int idx, int len, bool f
 
 // One generation: children of pop[buf][0..npar) (parents in fitness order, ga.hpp:146-151).
 void Engine::ga_generation(GaRun* r, int buf, const std::vector<int>& parent_len, int round, const GaParams& p,
-                           std::vector<int>& child_len, std::vector<double>& child_slack) {
+                           std::vector<int>& child_len, std::vector<double>& child_slack, const RolloutRefill* slow) {
     const int npar = static_cast<int>(parent_len.size());
     CK(cudaSetDevice(device_));
     CK(cudaMemcpy(r->pop_len, parent_len.data(), sizeof(int) * npar, cudaMemcpyHostToDevice));
@@ -1771,6 +1773,31 @@ void Engine::ga_generation(GaRun* r, int buf, const std::vector<int>& parent_len
     CK(cudaMemcpy(ns.data(), r->n_surv, sizeof(int) * npar, cudaMemcpyDeviceToHost));
     for (int i = 0; i < npar; ++i)
         if (ns[i] < 0) steps[i] = -1;  // no crossover: the child is the mutated parent
+    if (slow) {
+        // the throughput mcts_solve refill (mig_mcts_solve_parallel): each child whose greedy
+        // refill succeeded also runs slow->n_rollouts root-parallel rollouts (K5) from its
+        // residual, depth cap 2 x |greedy refill|; a strictly shorter best rollout replaces it
+        std::vector<double> res(static_cast<size_t>(npar) * m_.n);
+        CK(cudaMemcpy(res.data(), r->residual, sizeof(double) * res.size(), cudaMemcpyDeviceToHost));
+        stats.d2h += static_cast<long long>(sizeof(double) * res.size());
+        for (int i = 0; i < npar; ++i) {
+            if (steps[i] <= 0) continue;  // failed crossover, or a satisfied residual (empty refill)
+            const std::vector<double> c(res.begin() + static_cast<size_t>(i) * m_.n,
+                                        res.begin() + static_cast<size_t>(i + 1) * m_.n);
+            const uint64_t seed = mix_seed_u64(p.seed, (static_cast<uint64_t>(round) << 20) + static_cast<uint64_t>(i));
+            RolloutResult rr = rollouts(c, slow->n_rollouts, slow->topk, 2 * steps[i], seed, slow->id_offset,
+                                        slow->batch, slow->table_log2, nullptr);
+            if (rr.best_len >= 0 && rr.best_len < steps[i]) {
+                std::vector<uint64_t> rows_h;
+                for (long long idx : rr.path) rows_h.push_back(base_rows_[static_cast<size_t>(idx)]);
+                uint64_t* dst = r->alt + static_cast<size_t>(i) * r->L_cap;
+                CK(cudaMemcpy(dst, rows_h.data(), sizeof(uint64_t) * rows_h.size(), cudaMemcpyHostToDevice));
+                stats.h2d += static_cast<long long>(sizeof(uint64_t) * rows_h.size());
+                rows[i] = dst;
+                steps[i] = rr.best_len;
+            }
+        }
+    }
     CK(cudaMemcpy(r->refill, rows.data(), sizeof(void*) * npar, cudaMemcpyHostToDevice));
     CK(cudaMemcpy(r->refill_n, steps.data(), sizeof(int) * npar, cudaMemcpyHostToDevice));
     CK(cudaMemcpy(r->child_len, parent_len.data(), sizeof(int) * npar, cudaMemcpyHostToDevice));

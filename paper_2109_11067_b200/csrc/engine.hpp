@@ -80,6 +80,15 @@ struct MctsDeviceResult {
 };
 
 // Throughput-mode root-parallel rollouts (rollout.cu): the result of one mig_rollouts call.
+// Throughput mcts_solve as the GA's crossover refill (mig_two_phase_parallel_mcts).
+struct RolloutRefill {
+    long long n_rollouts = 0;
+    int topk = 10;
+    long long id_offset = 0;
+    long long batch = 0;
+    int table_log2 = 0;
+};
+
 struct RolloutResult {
     int best_len = -1;        // shortest completed rollout (steps); -1: none completed
     long long best_id = -1;   // its global id (ties: lowest id)
@@ -179,7 +188,8 @@ class Engine {
     void ga_put(GaRun* r, int buf, int idx, const std::vector<uint64_t>& genomes);
     std::vector<uint64_t> ga_get(GaRun* r, int buf, int idx, int len, bool from_child);
     void ga_generation(GaRun* r, int buf, const std::vector<int>& parent_len, int round, const GaParams& p,
-                       std::vector<int>& child_len, std::vector<double>& child_slack);
+                       std::vector<int>& child_len, std::vector<double>& child_slack,
+                       const RolloutRefill* slow = nullptr);
     void ga_select(GaRun* r, int buf, const std::vector<std::tuple<bool, int, int>>& order);
 
     // completion_of (core.hpp:291-302), count-based, on the host (control logic, not hot).

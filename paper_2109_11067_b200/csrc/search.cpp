@@ -226,7 +226,8 @@ std::vector<Config> sorted_deployment(std::vector<Config> cfgs);
 // over the whole population, with Philox draws (child i of round r: stream (r << 20) + i).
 // Host: elitist stable selection over (gpu count, slack) as ga.hpp:165-175.
 std::vector<Config> two_phase_parallel(Engine& e, const GaParams& p,
-                                       const std::function<void(int, int, double, bool, double)>& log) {
+                                       const std::function<void(int, int, double, bool, double)>& log,
+                                       const RolloutRefill* slow) {
     auto t0 = std::chrono::steady_clock::now();
     auto elapsed = [&] { return std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count(); };
     std::vector<Config> seed_cfg = fast_plan(e, std::vector<double>(e.n(), 0.0));
@@ -263,7 +264,7 @@ std::vector<Config> two_phase_parallel(Engine& e, const GaParams& p,
         std::vector<double> cslack;
         for (size_t i = 0; i < npar; ++i) plen[i] = pop[i].len;
         const double tg0 = elapsed();
-        e.ga_generation(run, buf, plen, round, p, clen, cslack);
+        e.ga_generation(run, buf, plen, round, p, clen, cslack, slow);
         if (std::getenv("MIGPLAN_GA_TIMERS"))
             std::fprintf(stderr, "[ga] round %d: generation %.2f ms\n", round, 1e3 * (elapsed() - tg0));
         struct Cand {

@@ -110,7 +110,8 @@ Chromosome mutate(const Chromosome& parent, const GaParams& p, Rng& rng);
 Chromosome crossover(const Chromosome& parent, const Procedure& slow, Engine& e, const GaParams& p, Rng& rng);
 // Throughput mode: device population generations with Philox draws (ga.cu).
 std::vector<Config> two_phase_parallel(Engine& e, const GaParams& p,
-                                       const std::function<void(int, int, double, bool, double)>& log);
+                                       const std::function<void(int, int, double, bool, double)>& log,
+                                       const RolloutRefill* slow = nullptr);
 std::vector<Config> two_phase(Engine& e, const GaParams& p,
                               const std::function<void(int, int, double, bool, double)>& log);
 std::vector<Config> sorted_deployment(std::vector<Config> cfgs);

@@ -1052,10 +1052,13 @@ def two_phase(services, profiles, rules, params: GaParams, log: Callable | None 
 
 
 def two_phase_parallel(services, profiles, rules, params: GaParams, log: Callable | None = None, backend=None,
-                       ctx: PlanContext | None = None) -> Deployment:
+                       ctx: PlanContext | None = None, slow: RolloutParams | None = None) -> Deployment:
     """Throughput-mode two_phase (include/migplan_b200.h): device-resident population, every
-    generation's mutation / crossover (FastProcedure refill) / fitness on the B200, Philox
-    draws.  Same rounds, elitism and stop rules as two_phase."""
+    generation's mutation / crossover / fitness on the B200, Philox draws.  Same rounds,
+    elitism and stop rules as two_phase.  slow=None: FastProcedure refill
+    (mig_two_phase_parallel); slow=RolloutParams: the throughput mcts_solve refill — the
+    shorter of the greedy refill and the best of slow.n_rollouts root-parallel rollouts
+    (mig_two_phase_parallel_mcts)."""
     own = ctx is None
     if own:
         ctx = make_plan_context(services, profiles, rules, 2, backend)
@@ -1063,8 +1066,13 @@ def two_phase_parallel(services, profiles, rules, params: GaParams, log: Callabl
     cb = abi.GA_LOG()
     if log is not None:
         cb = abi.GA_LOG(lambda _u, r, g, s, imp, el: log(GaRoundLog(r, g, s, bool(imp), el)))
-    cfgs = _run_plan(ctx, lambda out, cap, nout: ctx.backend.lib.mig_two_phase_parallel(
-        ctx._p, C.byref(gp), out, cap, C.byref(nout), cb, None))
+    if slow is None:
+        cfgs = _run_plan(ctx, lambda out, cap, nout: ctx.backend.lib.mig_two_phase_parallel(
+            ctx._p, C.byref(gp), out, cap, C.byref(nout), cb, None))
+    else:
+        rp = slow.to_c()
+        cfgs = _run_plan(ctx, lambda out, cap, nout: ctx.backend.lib.mig_two_phase_parallel_mcts(
+            ctx._p, C.byref(gp), C.byref(rp), out, cap, C.byref(nout), cb, None))
     return make_deployment(cfgs)
 
 

@@ -55,3 +55,34 @@ def test_two_phase_parallel_valid_and_monotone(impl):
     assert mp.is_satisfied(mp.completion_of(plan, sv, ps))
     best = [(l.best_gpus, l.best_slack) for l in logs]
     assert best == sorted(best, reverse=True) or all(a >= b for a, b in zip(best, best[1:]))
+
+
+# ---- with the throughput mcts_solve refill (mig_two_phase_parallel_mcts, BASELINE config #3)
+
+GOLD_MCTS = S.load_golden("ga_parallel_mcts.json")
+
+
+@pytest.mark.parametrize("name", sorted(GOLD_MCTS))
+def test_two_phase_parallel_mcts_matches_golden(impl, name):
+    g = GOLD_MCTS[name]
+    if impl.name != "product" and g["ref_wall_s"] > 5:
+        pytest.skip("large workload: checked on the GPU only")
+    logs = []
+    dep = mp.two_phase_parallel(services_of(g), store_of(g), mp.PartitionRuleSet.defaults(),
+                                mp.GaParams(time_budget_s=1e9, **g["params"]),
+                                log=lambda l: logs.append([l.round, l.best_gpus, l.best_slack.hex(), l.improved]),
+                                backend=impl, slow=mp.RolloutParams(**g["slow"]))
+    assert S.plan_key([x.config for x in dep.gpus]) == g["plan"]
+    assert logs == g["log"]
+
+
+def test_two_phase_parallel_mcts_never_worse_than_fast_refill(impl):
+    """Per child, the rollout refill replaces the greedy refill only when strictly shorter, so
+    with the same Philox stream the first round's best can only improve or tie."""
+    ps = S.profiles()
+    sv = S.fixture_services("slos_day", ps)
+    a = mp.two_phase_parallel(sv, ps, mp.PartitionRuleSet.defaults(), mp.GaParams(seed=3, max_rounds=1, time_budget_s=1e9),
+                              backend=impl)
+    b = mp.two_phase_parallel(sv, ps, mp.PartitionRuleSet.defaults(), mp.GaParams(seed=3, max_rounds=1, time_budget_s=1e9),
+                              backend=impl, slow=mp.RolloutParams(n_rollouts=64))
+    assert len(b.gpus) <= len(a.gpus)
