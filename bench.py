@@ -418,6 +418,35 @@ def extra_measurements(mp, local):
         ctx.close()
     except Exception as e:  # pragma: no cover
         out["config4"] = {"error": repr(e)}
+    try:  # config #3: greedy -> GA -> MCTS, throughput mode (Philox), against the reference's GA
+        import support as S2
+
+        ps, sv = S.gen(24, 8.7)
+        ctx = mp.make_plan_context(sv, ps, mp.PartitionRuleSet.defaults(), device=local)
+        slow = mp.RolloutParams(n_rollouts=1024, topk=10)
+        res3 = {"workload": "gen24_8.7 (BASELINE config #3): two_phase_parallel_mcts — device population, Philox "
+                            "seed 4242, refill = shorter of greedy and best of 1024 root-parallel rollouts",
+                "greedy_gpus": len(mp.fast_algo(mp.zero_completion(len(sv)), ctx))}
+        for rounds in (2, 10, 50):
+            prm = mp.GaParams(seed=4242, max_rounds=rounds, time_budget_s=1e9, stall_rounds=1 << 30)
+            t0 = time.perf_counter()
+            dep = mp.two_phase_parallel(sv, ps, mp.PartitionRuleSet.defaults(), prm, ctx=ctx, slow=slow)
+            res3[f"rounds_{rounds}"] = {"gpus_in_plan": len(dep.gpus), "wall_ms": 1e3 * (time.perf_counter() - t0)}
+        t0 = time.perf_counter()  # the parity-mode two_phase (reference RNG) of the same config, 2 rounds
+        dep = mp.two_phase(sv, ps, mp.PartitionRuleSet.defaults(), ga_params("gen24_8.7_ga2", 8), ctx=ctx)
+        res3["parity_two_phase_2_rounds"] = {"gpus_in_plan": len(dep.gpus), "wall_ms": 1e3 * (time.perf_counter() - t0),
+                                             "parity": golden_check("gen24_8.7_ga2", [g.config for g in dep.gpus])}
+        try:
+            ga = S2.load_golden("ga_big.json")
+            res3["reference_two_phase"] = {
+                k: {"gpus_in_plan": len(ga[k]["plan"]), "wall_s_build_container": ga[k]["ref_wall_s"],
+                    "workers": 8} for k in ("gen24_8.7_r2", "gen24_8.7_r10") if k in ga}
+        except (OSError, KeyError):
+            pass
+        out["config3"] = res3
+        ctx.close()
+    except Exception as e:  # pragma: no cover
+        out["config3"] = {"error": repr(e)}
     try:  # throughput-mode GA on config #2
         ps = S.profiles()
         sv = S.fixture_services("slos_24", ps)
@@ -445,6 +474,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-secondary", action="store_true", help="skip the config #2 GA object")
     ap.add_argument("--no-extras", action="store_true", help="skip the config #4 / device-GA objects")
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
+                    help="process group for N > 1 (gloo: ranks may share a GPU — a code-path check, not a bench)")
     args = ap.parse_args()
     if args.impl == "reference":
         return reference_arm(args)
@@ -458,13 +489,20 @@ def main():
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
+    n_dev = torch.cuda.device_count()
+    local = int(os.environ.get("LOCAL_RANK", "0")) % max(n_dev, 1)
     torch.cuda.set_device(local)
     if world > 1:
-        os.environ.setdefault("NCCL_DEBUG", "INFO")
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if args.dist_backend == "nccl":
+            os.environ.setdefault("NCCL_DEBUG", "INFO")
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group("gloo")
     name = args.workload
     sharded = world > 1 and not is_ga(name)
+    # ranks sharing one GPU (gloo code-path check): split its SMs between their greedy grids
+    share = max(1, -(-world // max(n_dev, 1))) if world > 1 else 1
+    red_dev = "cuda" if args.dist_backend == "nccl" else "cpu"
 
     ps, sv = load_workload(name)
     workers = args.workers
@@ -478,7 +516,7 @@ def main():
 
     def make_ctx():
         c = mp.make_plan_context(sv, ps, mp.PartitionRuleSet.defaults(), device=local)
-        boards = D.shard_context(c, local) if sharded else None
+        boards = D.shard_context(c, local, max_ctas=(148 // share if share > 1 else 0)) if sharded else None
         return c, boards
 
     def close_ctx(c, boards):
@@ -541,7 +579,7 @@ def main():
 
     rows = st["rows_scored"]
     t = torch.tensor([dev_ms, e2e_ms, cold_ms, float(rows), float(e2e_rows), st["greedy_ms"]], dtype=torch.float64,
-                     device="cuda")
+                     device=red_dev if world > 1 else "cuda")
     per_rank_rows = [rows]
     shas = [plan_sha]
     if world > 1:

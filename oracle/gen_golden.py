@@ -306,7 +306,8 @@ def gen_ga_big(ref):
     p3, g3 = S.gen(24, 8.7)
     cases = [("slos_24_r2", ps, slos, dict(seed=24, max_rounds=2)),
              ("slos_24_r10", ps, slos, dict(seed=24, max_rounds=10)),
-             ("gen24_8.7_r2", p3, g3, dict(seed=4242, max_rounds=2))]
+             ("gen24_8.7_r2", p3, g3, dict(seed=4242, max_rounds=2)),
+             ("gen24_8.7_r10", p3, g3, dict(seed=4242, max_rounds=10))]
     only = os.environ.get("GOLDEN_ONLY")
     for name, p, sv, kw in cases:
         if only and name not in only.split(","):

@@ -10,6 +10,8 @@
 #include <cstdio>
 #include <functional>
 
+#include <nvtx3/nvtx3.hpp>
+
 #include "engine.hpp"
 #include "search.hpp"
 
@@ -57,6 +59,9 @@ void ck(cudaError_t e, const char* what) {
     if (e != cudaSuccess) throw DeviceError(std::string(what) + ": " + cudaGetErrorString(e));
 }
 #define CK(x) ck((x), #x)
+// NVTX ranges (header-only NVTX v3: free unless a profiler is attached) around every device
+// entry point, so nsys/ncu timelines show plans, top-Ks, searches and generations by name.
+#define MGB_RANGE(name) nvtx3::scoped_range mgb_nvtx_range_{name}
 
 template <class T>
 T* dalloc(std::vector<void*>& owned, size_t count) {
@@ -172,6 +177,7 @@ bool config_equal(const Config& a, const Config& b) { return !config_less(a, b) 
 Engine::Engine(const Rules& rules, std::map<std::string, ModelProfile> profiles, std::vector<Service> services,
                int max_mix, int device)
     : profiles_(std::move(profiles)), device_(device) {
+    MGB_RANGE("migplan: context build");
     const auto tb = std::chrono::steady_clock::now();
     for (const auto& [name, p] : profiles_) validate_profile(p);
     m_ = build_model(rules, profiles_, services, max_mix);
@@ -808,6 +814,7 @@ int Engine::greedy_cluster_ctas(size_t smem, long long rows_bound) const {
 // exchange between them never waits on a kernel that is not resident.
 void Engine::fast_algo_group(const std::vector<Engine*>& es, const std::vector<double>& comp,
                              std::vector<uint64_t>& rows, std::vector<double>& scores) {
+    MGB_RANGE("migplan: fast_algo");
     rows.clear();
     scores.clear();
     const int P = static_cast<int>(es.size());
@@ -884,6 +891,7 @@ void Engine::fast_algo_group(const std::vector<Engine*>& es, const std::vector<d
 
 std::vector<long long> Engine::topk(const std::vector<double>& comp, int k, const std::vector<long long>* index,
                                     const std::vector<uint64_t>* svc_mask) {
+    MGB_RANGE("migplan: topk_candidates");
     if (static_cast<int>(comp.size()) != m_.n) throw PlanningError("completion vector length mismatch");
     std::vector<long long> out;
     if (k <= 0) return out;
@@ -1014,6 +1022,7 @@ std::vector<long long> Engine::topk(const std::vector<double>& comp, int k, cons
 // mcts_solve call, mcts.hpp:158).  A full key cache restarts the call with 4x capacity.
 RolloutResult Engine::rollouts(const std::vector<double>& comp, long long n_roll, int k, int max_depth, uint64_t seed,
                                long long id_offset, long long batch, int table_log2, int* lengths) {
+    MGB_RANGE("migplan: rollouts");
     if (static_cast<int>(comp.size()) != m_.n) throw PlanningError("completion vector length mismatch");
     if (k < 1 || k > 32) throw ArgumentError("rollouts: topk must be in [1, 32]");
     if (n_roll < 0 || max_depth < 0) throw ArgumentError("rollouts: negative count or depth");
@@ -1193,6 +1202,7 @@ void Engine::greedy_batch(const double* d_comps, int count, long long cap_steps,
                           std::vector<const uint64_t*>& rows,
                           std::vector<int>& n_steps, std::vector<std::vector<uint64_t>>* host_rows,
                           SlotLease* lease) {
+    MGB_RANGE("migplan: greedy batch (GA refills)");
     if (lease) lease->e = this;
     rows.assign(count, nullptr);
     n_steps.assign(count, -1);
@@ -1275,6 +1285,7 @@ std::vector<MctsDeviceResult> Engine::mcts_device_group(const std::vector<std::v
                                                         int topk, int pick_services, double ucb_c,
                                                         const std::vector<uint64_t>& seeds,
                                                         const std::vector<int>& l_refs) {
+    MGB_RANGE("migplan: mcts search");
     if (topk < 1 || topk > 32) throw ArgumentError("mcts: topk must be in [1, 32] on the device path");
     if (n_ranks_ > 1) throw ArgumentError("mcts on a sharded context");
     const int n = m_.n;
@@ -1532,6 +1543,7 @@ void Engine::fast_algo_batch(const std::vector<std::vector<double>>& comps, std:
 
 // ---- brute_force_optimum (bf.cu)
 std::vector<Config> Engine::brute_force(int cap, long long node_budget, bool& found) {
+    MGB_RANGE("migplan: brute_force_optimum");
     found = false;
     const int n = m_.n;
     if (n == 0) {
@@ -1741,6 +1753,7 @@ std::vector<uint64_t> Engine::ga_get(GaRun* r, int buf, int idx, int len, bool f
 // One generation: children of pop[buf][0..npar) (parents in fitness order, ga.hpp:146-151).
 void Engine::ga_generation(GaRun* r, int buf, const std::vector<int>& parent_len, int round, const GaParams& p,
                            std::vector<int>& child_len, std::vector<double>& child_slack, const RolloutRefill* slow) {
+    MGB_RANGE("migplan: GA generation");
     const int npar = static_cast<int>(parent_len.size());
     CK(cudaSetDevice(device_));
     CK(cudaMemcpy(r->pop_len, parent_len.data(), sizeof(int) * npar, cudaMemcpyHostToDevice));
@@ -1838,6 +1851,7 @@ void Engine::ga_select(GaRun* r, int buf, const std::vector<std::tuple<bool, int
 }
 
 void Engine::set_shard(int rank, int n_ranks, const std::vector<void*>& boards, int max_ctas) {
+    MGB_RANGE("migplan: set_shard");
     if (n_ranks < 1 || n_ranks > kMaxRanks || rank < 0 || rank >= n_ranks)
         throw ArgumentError("set_shard: rank/n_ranks out of range (1..8 ranks)");
     if (n_ranks > 1 && static_cast<int>(boards.size()) != n_ranks) throw ArgumentError("set_shard: one board per rank");

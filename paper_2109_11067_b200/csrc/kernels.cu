@@ -698,7 +698,11 @@ __global__ void __launch_bounds__(NT, 1) greedy_kernel(const __grid_constant__ G
                     packed = 0;
                     for (int j = 0; j < 4; ++j) packed |= static_cast<unsigned>(j < k ? S[j] : 0xFF) << (8 * j);
                 }
-                // level 2: the warp takes each surviving support's templates
+                // level 2: the warp takes each surviving support's templates.  A support's rows
+                // are appended as ONE contiguous run (one atomic for all its feasible templates,
+                // in template order): the scan's lanes then gather the Wf codes of one support's
+                // consecutive templates — few distinct shared-memory banks per gather — instead of
+                // interleaved 32-row pieces of several supports (bank conflicts, ncu r02).
                 unsigned todo = __ballot_sync(0xffffffffu, live);
                 while (todo) {
                     const int src = __ffs(todo) - 1;
@@ -708,10 +712,9 @@ __global__ void __launch_bounds__(NT, 1) greedy_kernel(const __grid_constant__ G
                     int S[4];
                     for (int j = 0; j < 4; ++j) S[j] = static_cast<int>((sp >> (8 * j)) & 0xFFu);
                     const int nt = M.n_tmpl[kk];
-                    for (int t0 = 0; t0 < nt; t0 += 32) {
-                        const int t = t0 + ln;
+                    auto make = [&](int t, uint64_t& row) {
                         bool ok = t < nt;
-                        uint64_t row = 0;
+                        row = 0;
                         if (ok) {
                             const uint64_t tp = M.tmpl[kk][t];
                             for (int j = 0; j < 4; ++j) {
@@ -726,6 +729,12 @@ __global__ void __launch_bounds__(NT, 1) greedy_kernel(const __grid_constant__ G
                                 row |= code << (16 * j);
                             }
                         }
+                        return ok;
+                    };
+#ifdef MIGPLAN_EXT_PIECES
+                    for (int t0 = 0; t0 < nt; t0 += 32) {
+                        uint64_t row;
+                        const bool ok = make(t0 + ln, row);
                         const unsigned b = __ballot_sync(0xffffffffu, ok);
                         if (b) {
                             unsigned long long at = 0;
@@ -738,6 +747,28 @@ __global__ void __launch_bounds__(NT, 1) greedy_kernel(const __grid_constant__ G
                             }
                         }
                     }
+#else
+                    int cnt = 0;
+                    for (int t0 = 0; t0 < nt; t0 += 32) {
+                        uint64_t row;
+                        cnt += __popc(__ballot_sync(0xffffffffu, make(t0 + ln, row)));
+                    }
+                    if (cnt == 0) continue;
+                    unsigned long long at = 0;
+                    if (ln == 0) at = atomicAdd(&a.st->ext_count, static_cast<unsigned long long>(cnt));
+                    at = __shfl_sync(0xffffffffu, at, 0);
+                    if (a.n_base + static_cast<long long>(at + cnt) > a.cap) {
+                        if (ln == 0) atomicExch(&a.st->status, static_cast<int>(kExtOverflow));
+                        continue;
+                    }
+                    for (int t0 = 0; t0 < nt; t0 += 32) {
+                        uint64_t row;
+                        const bool ok = make(t0 + ln, row);
+                        const unsigned b = __ballot_sync(0xffffffffu, ok);
+                        if (ok) a.rows[a.n_base + static_cast<long long>(at) + __popc(b & lanemask_lt())] = row;
+                        at += __popc(b);
+                    }
+#endif
                 }
             }
         }
