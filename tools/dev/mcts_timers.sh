@@ -1,0 +1,11 @@
+MIGPLAN_MCTS_TIMERS=1 python - <<'PY' 2> gpurun_out/mcts_timers.txt
+import sys, os
+sys.path.insert(0, 'tests')
+import support as S
+from support import mp
+ps = S.profiles(); sv = S.fixture_services("slos_24", ps)
+ctx = mp.make_plan_context(sv, ps, mp.PartitionRuleSet.defaults())
+prm = mp.GaParams(seed=24, max_rounds=10, time_budget_s=1e9, population=16, workers=8, slow=mp.MctsParams(budget_iters=48))
+mp.two_phase(sv, ps, mp.PartitionRuleSet.defaults(), prm, ctx=ctx)
+PY
+tail -30 gpurun_out/mcts_timers.txt
