@@ -199,7 +199,7 @@ def profile_traffic(kernel, workload):
     try:
         with open(os.path.join(ROOT, "profiles", name)) as f:
             d = json.load(f)
-        k = next(x for x in d["kernels"] if x["kernel"].startswith(kernel))
+        k = next(x for x in d["kernels"] if kernel in x["kernel"])
         return k.get("dram_bytes_per_launch"), name
     except Exception:
         return None, None
@@ -568,9 +568,11 @@ def main():
                                               "pinned step buffers allocated inside the timed step"}
     e2e_ms = 0.0
     e2e_rows = h2d = d2h = 0
+    e2e_list = []
     barrier()
     for _ in range(e2e_steps):
         (p2, s2), t = timed(e2e_step, flush, torch)
+        e2e_list.append(round(t, 3))
         e2e_ms += t
         e2e_rows += s2["rows_scored"]
         h2d += s2["h2d_bytes"]
@@ -627,7 +629,7 @@ def main():
                        "ext_rows_per_plan": st["ext_rows"] / max(st["greedy_calls"], 1)},
             "e2e": {"value": e2e_rows_all / (e2e_ms_max / 1e3), "unit": "configs/s",
                     "h2d_bytes_per_step": h2d // e2e_steps, "d2h_bytes_per_step": d2h // e2e_steps,
-                    "ms_per_step": e2e_ms_max / e2e_steps, "steps": e2e_steps, **cold},
+                    "ms_per_step": e2e_ms_max / e2e_steps, "steps": e2e_steps, "step_ms_rank0": e2e_list, **cold},
             "gpu_launches": st["kernel_launches"],
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                          "traffic": traffic, "traffic_source": traffic_src, "kernel": dom,
