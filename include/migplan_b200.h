@@ -340,12 +340,14 @@ int mig_baseline(const mig_ctx* ctx, int32_t kind, mig_config* out, int32_t cap,
 
 /* brute_force_optimum(services, profiles, rules, cap, node_budget), bench.hpp:160-219: the
  * exhaustive minimum-GPU search over config multisets (iterative deepening, admissible bound).
- * The context's pool must be the max_mix >= min(n, 7) pool (the product holds <= 4-member
- * configs: n <= 4).  *found = 0 (and *n_out = 0) when the optimum exceeds cap; PlanningError
- * "oracle: node budget exceeded; ..." when more than node_budget DFS nodes are visited and
- * "oracle: service cannot be served by any config" when a service has no utility anywhere.
- * Among several optima the product returns the smallest pool-index tuple; the GPU count is
- * the reference's (test_bench.cpp:120-160 compares counts). */
+ * Like the reference (bench.hpp:164-165) it builds the pool it searches — every config with
+ * at most min(n, 7) distinct services, in the reference's emission order — independently of
+ * the context's max_mix; the product's device search takes n <= 16 services and cap <= 8
+ * (MIG_ERR_ARGUMENT beyond).  *found = 0 (and *n_out = 0) when the optimum exceeds cap;
+ * PlanningError "oracle: node budget exceeded; ..." when more than node_budget DFS nodes are
+ * visited and "oracle: service cannot be served by any config" when a service has no utility
+ * anywhere.  The plan is the reference's first solution in its DFS order, and the budget
+ * guard trips at exactly the reference's node count. */
 int mig_brute_force_optimum(mig_ctx* ctx, int32_t cap, int64_t node_budget, mig_config* out, int32_t out_cap,
                             int32_t* n_out, int32_t* found);
 

@@ -243,16 +243,35 @@ def gen_brute_force(ref):
     for s in range(1, 9):  # 4 services, lighter demand: depth-4 searches over the n=4 pool
         sv = mp.gen_workload(4, True, 4.0 + 0.1 * s, 0.6, 100.0, 500 + s, fx, backend=S.host_backend())
         cases.append((f"gen4_{s}", fx, list(sv), 4))
+    # n >= 5: the max_mix = min(n, 7) pool holds 5..7-service configs (the reference's own
+    # budget-guard case has 6 services, test_bench.cpp:154-159)
+    guard = [mp.ServiceSpec(f"s{i}", "cnn-a", 900.0, 100.0) for i in range(6)]
+    cases.append(("budget_guard_6", tm, guard, 4, 2000))
+    for n, mu in ((5, 2.5), (6, 2.5), (7, 2.0), (8, 2.0)):
+        for s in range(1, 4):
+            sv = mp.gen_workload(n, True, mu, 0.6, 100.0, 900 + 10 * n + s, fx, backend=S.host_backend())
+            cases.append((f"wide{n}_{s}", fx, list(sv), 3))
+    for n in (5, 6, 7):
+        for s in range(1, 5):
+            sv = mp.gen_workload(n, True, 3.0 + 0.3 * s, 0.6, 100.0, 700 + 10 * n + s, fx, backend=S.host_backend())
+            cases.append((f"widegen{n}_{s}", fx, list(sv), 3))
+    for n, mu, s in ((10, 1.5, 1), (16, 2.0, 2)):
+        sv = mp.gen_workload(n, True, mu, 0.6, 100.0, 900 + 10 * n + s, fx, backend=S.host_backend())
+        cases.append((f"wide{n}_{s}", fx, list(sv), 3))
     res = {}
-    for name, ps, sv, cap in cases:
+    for case in cases:
+        name, ps, sv, cap = case[:4]
+        budget = case[4] if len(case) > 4 else 20_000_000
         t = time.time()
         try:
-            dep = mp.brute_force_optimum(sv, ps, rules, cap, backend=ref)
+            dep = mp.brute_force_optimum(sv, ps, rules, cap, node_budget=budget, backend=ref)
             out = "none" if dep is None else S.plan_key([g.config for g in dep.gpus])
         except mp.PlanningError as e:
             out = "error:" + str(e)
         res[name] = {"store": store_name(ps), "services": svc_json(sv), "cap": cap, "outcome": out,
                      "ref_wall_s": round(time.time() - t, 3)}
+        if budget != 20_000_000:
+            res[name]["node_budget"] = budget
         if not (isinstance(out, str) and out.startswith("error")) and res[name]["ref_wall_s"] < 0.3:
             lo, hi = 0, 20_000_000  # the reference's exact node count: the smallest budget that passes
             while lo < hi:

@@ -25,20 +25,27 @@ namespace {
 
 constexpr int kBfThreads = 256;
 
-__device__ __forceinline__ bool bf_positive(const DevModel& M, uint64_t row, const double* c) {
-    for (int j = 0; j < 4; ++j) {  // score > 0 <=> a member with need > 0 and utility > 0 (greedy.hpp:36-43)
-        const int code = static_cast<int>((row >> (16 * j)) & 0xFFFFull);
+__device__ __forceinline__ int bf_code(const uint4& row, int j) {  // member j's u16 code
+    const unsigned w = j < 4 ? (j < 2 ? row.x : row.y) : (j < 6 ? row.z : row.w);
+    return static_cast<int>((w >> (16 * (j & 1))) & 0xFFFFu);
+}
+
+__device__ __forceinline__ bool bf_positive(const DevModel& M, const uint4& row, const double* c) {
+    for (int j = 0; j < kBfCodes; ++j) {  // score > 0 <=> a member with need > 0 and utility > 0 (greedy.hpp:36-43)
+        const int code = bf_code(row, j);
         const int svc = code / M.PP;
-        if (svc < M.n && __dadd_rn(1.0, -c[svc]) > 0.0 && M.U[code] > 0.0) return true;
+        if (svc >= M.n) break;  // members are packed in front of the sentinels
+        if (__dadd_rn(1.0, -c[svc]) > 0.0 && M.U[code] > 0.0) return true;
     }
     return false;
 }
 
-__device__ __forceinline__ void bf_add(const DevModel& M, uint64_t row, double* c) {
-    for (int j = 0; j < 4; ++j) {
-        const int code = static_cast<int>((row >> (16 * j)) & 0xFFFFull);
+__device__ __forceinline__ void bf_add(const DevModel& M, const uint4& row, double* c) {
+    for (int j = 0; j < kBfCodes; ++j) {
+        const int code = bf_code(row, j);
         const int svc = code / M.PP;
-        if (svc < M.n) c[svc] = __dadd_rn(c[svc], M.U[code]);
+        if (svc >= M.n) break;
+        c[svc] = __dadd_rn(c[svc], M.U[code]);
     }
 }
 
@@ -86,7 +93,7 @@ __device__ __forceinline__ int bf_dfs(const BfArgs& a, double (*st)[kBfMaxN], lo
             --depth;
             continue;
         }
-        const uint64_t row = a.rows[i];
+        const uint4 row = a.rows[i];
         if (!bf_positive(M, row, st[depth])) continue;
         ++nodes;
         for (int k = 0; k < n; ++k) st[depth + 1][k] = st[depth][k];
@@ -121,7 +128,7 @@ __device__ __forceinline__ bool bf_prefix(const BfArgs& a, long long t, double (
     }
     for (int i = 0; i < n; ++i) st[0][i] = 0.0;
     for (int q = 0; q < pl; ++q) {
-        const uint64_t row = a.rows[idx[q]];
+        const uint4 row = a.rows[idx[q]];
         if (!bf_positive(M, row, st[q])) return false;
         if (q > 0 || pl == 1 || idx[1] == idx[0]) ++nodes;  // a level-1 node is charged once
         for (int i = 0; i < n; ++i) st[q + 1][i] = st[q][i];
@@ -189,7 +196,7 @@ __global__ void __launch_bounds__(kBfThreads) bf_warp_kernel(const __grid_consta
             int f = 0;
             bool lstop = false, lover = false;
             if (i < P) {
-                const uint64_t row = a.rows[i];
+                const uint4 row = a.rows[i];
                 if (bf_positive(M, row, st[2])) {
                     nodes = 1;
                     for (int k = 0; k < n; ++k) st[3][k] = st[2][k];
@@ -262,9 +269,145 @@ __global__ void __launch_bounds__(kBfThreads) bf_sum_kernel(const __grid_constan
     if ((threadIdx.x & 31) == 0 && s) atomicAdd(a.sum, s);
 }
 
+// ---- the pool (build_candidate_pool(services, profiles, rules, min(n, 7)), bench.hpp:164-165)
+namespace {
+
+__device__ __forceinline__ long long bf_multichoose(int m, int r) {  // C(m + r - 1, r): r-sequences over m symbols
+    long long c = 1;
+    for (int i = 1; i <= r; ++i) c = c * (m + i - 1) / i;  // exact: c * (m+i-1) is divisible by i
+    return c;
+}
+
+// Decode flat index t into its config (fill_group / materialize, config_enum.hpp:131-183);
+// false when a service is infeasible at its size or the support exceeds max_mix.
+__device__ bool bf_enum_row(const BfEnumArgs& e, long long t, uint4& out) {
+    int li = 0;
+    while (t >= e.lay_off[li + 1]) ++li;
+    long long r = t - e.lay_off[li];
+    const int G = e.n_groups[li];
+    long long dig[5];
+    for (int g = G - 1; g >= 0; --g) {
+        dig[g] = r % e.g_cnt[li][g];
+        r /= e.g_cnt[li][g];
+    }
+    unsigned mask = 0;
+    unsigned cnt[kBfMaxN];  // per service: instance counts, 3 bits per size index
+    for (int g = 0; g < G; ++g) {
+        const int len = e.g_len[li][g], z = e.g_size[li][g];
+        long long q = dig[g];
+        int v = 0;
+        for (int p = 0; p < len; ++p) {  // lexicographic unrank of a nondecreasing sequence
+            const int rem = len - p - 1;
+            for (;; ++v) {
+                const long long c = bf_multichoose(e.n - v, rem);
+                if (q < c) break;
+                q -= c;
+            }
+            if (!((e.feas_mask[v] >> z) & 1u)) return false;  // config_enum.hpp:142
+            if (!((mask >> v) & 1u)) cnt[v] = 0;
+            mask |= 1u << v;
+            cnt[v] += 1u << (3 * z);
+        }
+    }
+    if (__popc(mask) > e.max_mix) return false;  // config_enum.hpp:145
+    unsigned short code[kBfCodes];
+    int k = 0;
+    for (unsigned m = mask; m; m &= m - 1) {  // members in ascending service order
+        const int v = __ffs(m) - 1;
+        const int pat = e.pat_of[cnt[v]];
+        if (pat == 0xFF) *e.error = 1;
+        code[k++] = static_cast<unsigned short>(v * e.PP + pat);
+    }
+    for (; k < kBfCodes; ++k) code[k] = static_cast<unsigned short>(e.n * e.PP);
+    out = make_uint4(code[0] | static_cast<unsigned>(code[1]) << 16, code[2] | static_cast<unsigned>(code[3]) << 16,
+                     code[4] | static_cast<unsigned>(code[5]) << 16, code[6] | static_cast<unsigned>(code[7]) << 16);
+    return true;
+}
+
+}  // namespace
+
+// mode 0: block_cnt[b] = valid configs among indices [256 b, 256 b + 256); mode 1: write them,
+// in index order, from block_cnt[b] (the exclusive scan) on.
+__global__ void __launch_bounds__(256) bf_enum_kernel(const __grid_constant__ BfEnumArgs e, int mode) {
+    const long long t = static_cast<long long>(blockIdx.x) * 256 + threadIdx.x;
+    uint4 row;
+    const bool ok = t < e.lay_off[e.n_layouts] && bf_enum_row(e, t, row);
+    __shared__ unsigned wcnt[8];
+    const unsigned bm = __ballot_sync(0xffffffffu, ok);
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    if (lane == 0) wcnt[w] = __popc(bm);
+    __syncthreads();
+    if (mode == 0) {
+        if (threadIdx.x == 0) {
+            unsigned c = 0;
+            for (int i = 0; i < 8; ++i) c += wcnt[i];
+            e.block_cnt[blockIdx.x] = c;
+        }
+        return;
+    }
+    if (!ok) return;
+    unsigned pos = e.block_cnt[blockIdx.x] + __popc(bm & ((1u << lane) - 1u));
+    for (int i = 0; i < w; ++i) pos += wcnt[i];
+    e.rows[pos] = row;
+}
+
+// In-place exclusive scan of block_cnt[0..nb) by one CTA; block_cnt[nb] = total.
+__global__ void __launch_bounds__(1024) bf_scan_kernel(unsigned* c, int nb) {
+    __shared__ unsigned wsum[32];
+    __shared__ unsigned carry;
+    if (threadIdx.x == 0) carry = 0;
+    __syncthreads();
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    for (int b0 = 0; b0 < nb; b0 += 1024) {
+        const int i = b0 + threadIdx.x;
+        const unsigned v = i < nb ? c[i] : 0u;
+        unsigned x = v;
+        for (int o = 1; o < 32; o <<= 1) {
+            const unsigned y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x += y;
+        }
+        if (lane == 31) wsum[w] = x;
+        __syncthreads();
+        if (w == 0) {
+            unsigned s = wsum[lane];
+            for (int o = 1; o < 32; o <<= 1) {
+                const unsigned y = __shfl_up_sync(0xffffffffu, s, o);
+                if (lane >= o) s += y;
+            }
+            wsum[lane] = s;
+        }
+        __syncthreads();
+        const unsigned incl = x + (w ? wsum[w - 1] : 0u) + carry;
+        if (i < nb) c[i] = incl - v;
+        __syncthreads();
+        if (threadIdx.x == 1023) carry = incl;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) c[nb] = carry;
+}
+
+// best_any[i] = max over the pool of the utility configs give service i (bench.hpp:167-171);
+// utilities are >= 0, so their bit patterns order like the values.
+__global__ void __launch_bounds__(256) bf_best_any_kernel(const DevModel M, const uint4* rows, long long P,
+                                                          unsigned long long* best_bits) {
+    for (long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; i < P;
+         i += static_cast<long long>(gridDim.x) * blockDim.x) {
+        const uint4 row = rows[i];
+        for (int j = 0; j < kBfCodes; ++j) {
+            const int code = bf_code(row, j);
+            const int svc = code / M.PP;
+            if (svc >= M.n) break;
+            atomicMax(best_bits + svc, static_cast<unsigned long long>(__double_as_longlong(M.U[code])));
+        }
+    }
+}
+
 const void* bf_kernel_ptr() { return reinterpret_cast<const void*>(&bf_kernel); }
 const void* bf_warp_kernel_ptr() { return reinterpret_cast<const void*>(&bf_warp_kernel); }
 const void* bf_sum_kernel_ptr() { return reinterpret_cast<const void*>(&bf_sum_kernel); }
 int bf_threads() { return kBfThreads; }
+const void* bf_enum_kernel_ptr() { return reinterpret_cast<const void*>(&bf_enum_kernel); }
+const void* bf_scan_kernel_ptr() { return reinterpret_cast<const void*>(&bf_scan_kernel); }
+const void* bf_best_any_kernel_ptr() { return reinterpret_cast<const void*>(&bf_best_any_kernel); }
 
 }  // namespace mgb

@@ -226,12 +226,14 @@ struct MctsLaunch {
     MctsSolveArgs s[kMaxGroups];
 };
 
-// Device brute_force_optimum (bf.cu): one launch per iterative-deepening depth.
-constexpr int kBfMaxDepth = 8;  // cap
-constexpr int kBfMaxN = 8;      // services (the device pool holds <= 4-member configs: n <= 4)
+// Device brute_force_optimum (bf.cu): one launch per iterative-deepening depth, over the
+// max_mix = min(n, 7) pool that bf_enum_kernel builds in the reference's emission order.
+constexpr int kBfMaxDepth = 8;   // cap
+constexpr int kBfMaxN = 16;      // services (the max_mix = 7 pool of 16 services is ~1 M rows)
+constexpr int kBfCodes = 8;      // member codes per wide row (<= 7 distinct services)
 struct BfArgs {
     DevModel M;
-    const uint64_t* rows;        // the pool with max_mix = min(n, 4)
+    const uint4* rows;           // the pool: 8 u16 member codes per row (svc ascending, sentinel n*PP)
     long long n_rows;
     const double* best_any;      // n: best utility any config gives each service
     int depth;
@@ -243,6 +245,23 @@ struct BfArgs {
     unsigned long long* overrun;   // smallest rank whose own subtree exceeded `remaining`
     unsigned long long* sum;       // bf_sum_kernel: Σ cnt[rank0 .. min(best_key, rank_end-1)]
     long long* tuple;            // replay: picks (pool indices), tuple[kBfMaxDepth] = length
+};
+
+// The pool enumerator (config_enum.hpp:108-188 with max_mix = min(n, 7)): index t of layout
+// li is a mixed-radix number over the layout's groups (group 0 most significant), each digit
+// the lexicographic rank of a nondecreasing service sequence of the group's length.
+struct BfEnumArgs {
+    int n, PP, max_mix, n_layouts;
+    int n_groups[32];
+    int8_t g_len[32][5];          // slots per group
+    int8_t g_size[32][5];         // size index per group
+    long long g_cnt[32][5];       // C(n + len - 1, len): nondecreasing sequences per group
+    long long lay_off[33];        // flat index of each layout's first combination
+    uint8_t feas_mask[kBfMaxN];   // bit z: feasible at size index z
+    const uint8_t* pat_of;        // 1 << 15: count vector (3 bits per size index) -> pattern (0xFF none)
+    unsigned* block_cnt;          // per 256-index block: valid configs (mode 0) / write offset (mode 1)
+    uint4* rows;                  // mode 1 output
+    int* error;                   // a member pattern missing from pat_of
 };
 
 // Throughput-mode root-parallel rollouts (rollout.cu).

@@ -33,6 +33,9 @@ size_t rollout_smem_bytes(int n, int PP, int n_sup);
 size_t mcts_smem_bytes(int n, int PP, int max_nodes, long long n_base, bool node_smem, bool rows_smem, bool pair,
                        int n_sup);
 const void* bf_kernel_ptr();
+const void* bf_enum_kernel_ptr();
+const void* bf_scan_kernel_ptr();
+const void* bf_best_any_kernel_ptr();
 const void* bf_sum_kernel_ptr();
 const void* bf_warp_kernel_ptr();
 int bf_threads();
@@ -430,6 +433,20 @@ long long Engine::index_of(uint64_t row) const {
 Config Engine::config_of(uint64_t row) const {
     Config c;
     c.n = m_.decode(row, c.inst);
+    return c;
+}
+
+Config Engine::config_of_wide(const uint4& row) const {  // bf.cu's 8-code rows
+    const unsigned w[4] = {row.x, row.y, row.z, row.w};
+    int svc[kBfCodes], pat[kBfCodes], k = 0;
+    for (int j = 0; j < kBfCodes; ++j) {
+        const int code = static_cast<int>((w[j >> 1] >> (16 * (j & 1))) & 0xFFFFu);
+        if (code >= m_.n * m_.PP) break;
+        svc[k] = code / m_.PP;
+        pat[k++] = code % m_.PP;
+    }
+    Config c;
+    c.n = m_.decode_members(svc, pat, k, c.inst);
     return c;
 }
 
@@ -1550,60 +1567,80 @@ std::vector<Config> Engine::brute_force(int cap, long long node_budget, bool& fo
         found = true;
         return {};
     }
-    if (n > 4 || n > kBfMaxN) throw ArgumentError("device brute_force_optimum: n <= 4 services (4-member rows)");
-    if (m_.max_mix < n) throw ArgumentError("brute_force_optimum needs the max_mix = n pool");
+    if (n > kBfMaxN)
+        throw ArgumentError("device brute_force_optimum: n <= " + std::to_string(kBfMaxN) + " services");
     if (cap > kBfMaxDepth) throw ArgumentError("brute_force_optimum: cap <= 8 on the device");
-    std::vector<double> best_any(n, 0.0);  // bench.hpp:167-171
-    for (uint64_t row : base_rows_) {
-        int svc[kRowK], pat[kRowK];
-        const int k = m_.members(row, svc, pat);
-        for (int j = 0; j < k; ++j) best_any[svc[j]] = std::max(best_any[svc[j]], m_.U[static_cast<size_t>(svc[j]) * m_.PP + pat[j]]);
-    }
-    for (int i = 0; i < n; ++i)
-        if (best_any[i] <= 0.0) throw PlanningError("oracle: service cannot be served by any config");
-    // The reference's DFS walks pool.items in emission order (config_enum.hpp:108-150): size
-    // multisets in canonical order, then the per-group nondecreasing service sequences in
-    // lexicographic order.  Search the rows in that order so the first solution and the node
-    // count are the reference's.
-    const long long P = pool_size();
-    std::vector<std::pair<std::array<int, 8>, uint64_t>> keyed;
-    keyed.reserve(static_cast<size_t>(P));
-    for (uint64_t row : base_rows_) {
-        int svc[kRowK], pat[kRowK];
-        const int k = m_.members(row, svc, pat);
-        std::array<int, kMaxSizes> cnt{};
-        for (int j = 0; j < k; ++j)
-            for (int z = 0; z < kMaxSizes; ++z) cnt[z] += m_.patterns[pat[j]][z];
-        std::array<int, 8> key;
-        key.fill(-1);
-        int li = 0;
-        while (li < static_cast<int>(m_.layouts.size())) {
-            bool same = true;
-            for (int z = 0; z < kMaxSizes; ++z) same &= m_.layouts[li].count[z] == cnt[z];
-            if (same) break;
-            ++li;
-        }
-        key[0] = li;
-        int w = 1;
-        for (const auto& g : m_.layouts.at(li).groups)
-            for (int j = 0; j < k; ++j)
-                for (int c = 0; c < m_.patterns[pat[j]][g.size_idx] && w < 8; ++c) key[w++] = svc[j];
-        keyed.emplace_back(key, row);
-    }
-    std::sort(keyed.begin(), keyed.end());
-    std::vector<uint64_t> rows(keyed.size());
-    for (size_t i = 0; i < keyed.size(); ++i) rows[i] = keyed[i].second;
     CK(cudaSetDevice(device_));
+    // The pool the reference searches: build_candidate_pool(..., max_mix = min(n, 7))
+    // (bench.hpp:164-165), enumerated on the device in its emission order (config_enum.hpp:
+    // 108-150: layouts in canonical order, then the per-group nondecreasing service sequences
+    // in lexicographic order), so the DFS's first solution and node count are the reference's.
+    BfEnumArgs ea{};
+    ea.n = n;
+    ea.PP = m_.PP;
+    ea.max_mix = std::min(n, 7);
+    ea.n_layouts = static_cast<int>(m_.layouts.size());
+    long long space = 0;
+    for (int li = 0; li < ea.n_layouts; ++li) {
+        const Layout& L = m_.layouts[li];
+        ea.lay_off[li] = space;
+        ea.n_groups[li] = static_cast<int>(L.groups.size());
+        long long c = 1;
+        for (size_t g = 0; g < L.groups.size(); ++g) {
+            const int len = static_cast<int>(L.groups[g].slots.size());
+            ea.g_len[li][g] = static_cast<int8_t>(len);
+            ea.g_size[li][g] = static_cast<int8_t>(L.groups[g].size_idx);
+            long long mc = 1;
+            for (int i = 1; i <= len; ++i) mc = mc * (n + i - 1) / i;
+            ea.g_cnt[li][g] = mc;
+            c *= mc;
+        }
+        space += c;
+    }
+    ea.lay_off[ea.n_layouts] = space;
+    if (space > (1ll << 31)) throw ArgumentError("brute_force_optimum: enumeration space too large");
+    for (int i = 0; i < n; ++i) ea.feas_mask[i] = m_.feas_mask[i];
+    std::vector<uint8_t> pat_of(1u << 15, 0xFF);
+    for (int p = 0; p < m_.PP; ++p) {
+        unsigned key = 0;
+        for (int z = 0; z < kMaxSizes; ++z) key |= static_cast<unsigned>(m_.patterns[p][z]) << (3 * z);
+        pat_of[key] = static_cast<uint8_t>(p);
+    }
+    const int nb = static_cast<int>((space + 255) / 256);
+    const size_t off_cnt0 = 256, off_lut = off_cnt0 + ((sizeof(unsigned) * (nb + 1) + 255) & ~size_t(255));
+    void* emem = nullptr;
+    CK(cudaMalloc(&emem, off_lut + pat_of.size()));
+    struct EFree {
+        void* p;
+        ~EFree() { cudaFree(p); }
+    } efr{emem};
+    unsigned char* e8 = static_cast<unsigned char*>(emem);
+    CK(cudaMemset(e8, 0, 256));
+    CK(cudaMemcpy(e8 + off_lut, pat_of.data(), pat_of.size(), cudaMemcpyHostToDevice));
+    ea.error = reinterpret_cast<int*>(e8);
+    ea.block_cnt = reinterpret_cast<unsigned*>(e8 + off_cnt0);
+    ea.pat_of = e8 + off_lut;
+    int mode = 0;
+    {
+        void* args[] = {&ea, &mode};
+        CK(cudaLaunchKernel(bf_enum_kernel_ptr(), nb, 256, args, 0, nullptr));
+        void* sargs[] = {&ea.block_cnt, const_cast<int*>(&nb)};
+        CK(cudaLaunchKernel(bf_scan_kernel_ptr(), 1, 1024, sargs, 0, nullptr));
+        stats.launches += 2;
+    }
+    unsigned total = 0;
+    CK(cudaMemcpy(&total, ea.block_cnt + nb, sizeof total, cudaMemcpyDeviceToHost));
+    const long long P = total;
     // depth 1-2: a thread per prefix; depth >= 3: a warp per two-pick prefix (bf.cu)
     const long long chunk_t = static_cast<long long>(num_sms_) * bf_threads() * 4;
     const long long chunk_w = static_cast<long long>(num_sms_) * 64 * 8;
-    const long long max_ranks = std::min(P * (P + 1) / 2, std::max(chunk_t, chunk_w));
+    const long long max_ranks = std::min(std::max(P * (P + 1) / 2, 1ll), std::max(chunk_t, chunk_w));
     struct Words {
         unsigned long long best_key, overrun, sum, pad;
     };
     const size_t off_tuple = sizeof(Words), off_any = off_tuple + sizeof(long long) * (kBfMaxDepth + 1);
     const size_t off_rows = (off_any + sizeof(double) * n + 255) & ~size_t(255);
-    const size_t off_cnt = (off_rows + sizeof(uint64_t) * static_cast<size_t>(P) + 255) & ~size_t(255);
+    const size_t off_cnt = (off_rows + sizeof(uint4) * static_cast<size_t>(std::max(P, 1ll)) + 255) & ~size_t(255);
     void* mem = nullptr;
     CK(cudaMalloc(&mem, off_cnt + sizeof(unsigned long long) * std::max<long long>(max_ranks, 1)));
     struct Free {
@@ -1612,8 +1649,28 @@ std::vector<Config> Engine::brute_force(int cap, long long node_budget, bool& fo
     } fr{mem};
     unsigned char* m8 = static_cast<unsigned char*>(mem);
     Words* w = reinterpret_cast<Words*>(m8);
-    CK(cudaMemcpy(m8 + off_any, best_any.data(), sizeof(double) * n, cudaMemcpyHostToDevice));
-    CK(cudaMemcpy(m8 + off_rows, rows.data(), sizeof(uint64_t) * rows.size(), cudaMemcpyHostToDevice));
+    const uint4* rows = reinterpret_cast<const uint4*>(m8 + off_rows);
+    std::vector<double> best_any(n, 0.0);  // bench.hpp:167-171
+    CK(cudaMemset(m8 + off_any, 0, sizeof(double) * n));
+    if (P > 0) {
+        ea.rows = reinterpret_cast<uint4*>(m8 + off_rows);
+        mode = 1;
+        void* args[] = {&ea, &mode};
+        CK(cudaLaunchKernel(bf_enum_kernel_ptr(), nb, 256, args, 0, nullptr));
+        DevModel dm = dm_;
+        long long Pv = P;
+        unsigned long long* bits = reinterpret_cast<unsigned long long*>(m8 + off_any);
+        void* bargs[] = {&dm, const_cast<uint4**>(&rows), &Pv, &bits};
+        CK(cudaLaunchKernel(bf_best_any_kernel_ptr(), static_cast<unsigned>(std::min<long long>((P + 255) / 256, num_sms_ * 8)),
+                            256, bargs, 0, nullptr));
+        stats.launches += 2;
+    }
+    int enum_err = 0;
+    CK(cudaMemcpy(&enum_err, ea.error, sizeof enum_err, cudaMemcpyDeviceToHost));
+    if (enum_err) throw DeviceError("brute_force_optimum: a member pattern is missing from the model");
+    CK(cudaMemcpy(best_any.data(), m8 + off_any, sizeof(double) * n, cudaMemcpyDeviceToHost));
+    for (int i = 0; i < n; ++i)
+        if (best_any[i] <= 0.0) throw PlanningError("oracle: service cannot be served by any config");
     const unsigned long long budget = static_cast<unsigned long long>(std::max<long long>(node_budget, 0));
     auto over = [] { throw PlanningError("oracle: node budget exceeded; shrink the instance or raise the budget"); };
     unsigned long long nodes = 0;  // the reference's ++nodes, cumulative over depths
@@ -1625,7 +1682,7 @@ std::vector<Config> Engine::brute_force(int cap, long long node_budget, bool& fo
         if (d == 0 || root_bound > d) continue;  // bench.hpp:197
         BfArgs a{};
         a.M = dm_;
-        a.rows = reinterpret_cast<const uint64_t*>(m8 + off_rows);
+        a.rows = rows;
         a.n_rows = P;
         a.best_any = reinterpret_cast<const double*>(m8 + off_any);
         a.depth = d;
@@ -1666,7 +1723,11 @@ std::vector<Config> Engine::brute_force(int cap, long long node_budget, bool& fo
                 long long tup[kBfMaxDepth + 1];
                 CK(cudaMemcpy(tup, a.tuple, sizeof tup, cudaMemcpyDeviceToHost));
                 std::vector<Config> out;
-                for (long long q = 0; q < tup[kBfMaxDepth]; ++q) out.push_back(config_of(rows[tup[q]]));
+                for (long long q = 0; q < tup[kBfMaxDepth]; ++q) {
+                    uint4 r;
+                    CK(cudaMemcpy(&r, rows + tup[q], sizeof r, cudaMemcpyDeviceToHost));
+                    out.push_back(config_of_wide(r));
+                }
                 found = true;
                 return out;
             }

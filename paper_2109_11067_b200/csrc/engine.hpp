@@ -125,6 +125,7 @@ class Engine {
     long long pool_size() const { return static_cast<long long>(base_rows_.size()); }
     long long index_of(uint64_t row) const;
     Config config_of(uint64_t row) const;
+    Config config_of_wide(const uint4& row) const;  // brute_force_optimum's 8-code rows
 
     // fast_algo (greedy.hpp:95-145) on the device.  Returns picked rows and their scores.
     void fast_algo(const std::vector<double>& comp, std::vector<uint64_t>& rows, std::vector<double>& scores);
@@ -153,8 +154,8 @@ class Engine {
     MctsDeviceResult mcts_device(const std::vector<double>& comp, int budget, int topk, int pick_services, double ucb_c,
                                  uint64_t seed, int l_ref);
 
-    // brute_force_optimum (bench.hpp:160-219) on the device over this context's pool (which
-    // must be the max_mix = n pool, n <= 4).  found = false: the optimum exceeds cap.
+    // brute_force_optimum (bench.hpp:160-219) on the device over the max_mix = min(n, 7) pool
+    // it enumerates itself (bench.hpp:164-165; n <= 16).  found = false: the optimum exceeds cap.
     std::vector<Config> brute_force(int cap, long long node_budget, bool& found);
 
     // Slots kept past greedy_batch so the device picked rows it returns stay valid: released

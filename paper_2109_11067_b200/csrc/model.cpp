@@ -305,7 +305,11 @@ int Model::members(uint64_t row, int* svc, int* pat) const {
 
 int Model::decode(uint64_t row, Inst* out) const {
     int svc[kRowK], pat[kRowK];
-    int k = members(row, svc, pat);
+    const int k = members(row, svc, pat);
+    return decode_members(svc, pat, k, out);
+}
+
+int Model::decode_members(const int* svc, const int* pat, int k, Inst* out) const {
     std::array<uint8_t, kMaxSizes> tot{};
     for (int j = 0; j < k; ++j)
         for (int s = 0; s < kMaxSizes; ++s) tot[s] = static_cast<uint8_t>(tot[s] + patterns[pat[j]][s]);

@@ -135,6 +135,9 @@ struct Model {
         int slices, slot, svc, batch;
     };
     int decode(uint64_t row, Inst* out) const;  // normalized instances, returns count
+    // the config of members (svc ascending, pattern ids; any k <= 7): canonical layout of the
+    // summed patterns, lower service index on the lower slots of each size group
+    int decode_members(const int* svc, const int* pat, int k, Inst* out) const;
     std::array<uint64_t, 2> key(uint64_t row) const;
     double util_sum(uint64_t row) const;
     double score(uint64_t row, const double* comp) const;

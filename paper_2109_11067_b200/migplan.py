@@ -1115,12 +1115,13 @@ def baseline(kind, services, profiles, backend=None) -> Deployment:
 def brute_force_optimum(services, profiles, rules, cap: int, node_budget: int = 20_000_000,
                         backend=None, device: int = 0) -> Deployment | None:
     """brute_force_optimum, bench.hpp:160-219 — the exhaustive minimum-GPU oracle for small
-    instances; None when the optimum exceeds cap.  Runs over the max_mix = min(n, 7) pool
-    (the product's device search holds <= 4-member configs, so n <= 4 there)."""
+    instances; None when the optimum exceeds cap.  The search builds its own max_mix =
+    min(n, 7) pool (bench.hpp:164-165), so the context only carries the model (max_mix 1);
+    the device search takes n <= 16 services."""
     services = list(services)
     if not services:  # bench.hpp:163
         return make_deployment([])
-    ctx = PlanContext(services, profiles, rules, min(len(services), 7), backend, device)
+    ctx = PlanContext(services, profiles, rules, 1, backend, device)
     found = C.c_int32()
     plan = _run_plan(ctx, lambda out, cp, nout: ctx.backend.lib.mig_brute_force_optimum(
         ctx._p, cap, node_budget, out, cp, C.byref(nout), C.byref(found)))

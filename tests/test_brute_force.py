@@ -27,11 +27,12 @@ def case(name):
 def test_matches_reference(impl, name):
     g, ps, sv = case(name)
     want = g["outcome"]
+    budget = g.get("node_budget", 20_000_000)
     if isinstance(want, str) and want.startswith("error:"):
         with pytest.raises(mp.PlanningError, match=want[len("error:"):][:20]):
-            mp.brute_force_optimum(sv, ps, RULES, g["cap"], backend=impl)
+            mp.brute_force_optimum(sv, ps, RULES, g["cap"], node_budget=budget, backend=impl)
         return
-    dep = mp.brute_force_optimum(sv, ps, RULES, g["cap"], backend=impl)
+    dep = mp.brute_force_optimum(sv, ps, RULES, g["cap"], node_budget=budget, backend=impl)
     if want == "none":
         assert dep is None
         return
@@ -70,11 +71,19 @@ def test_cap_zero_is_none(impl):
 
 
 @pytest.mark.gpu
-def test_product_rejects_more_than_four_services():
+def test_product_rejects_more_than_sixteen_services():
     ps = S.profiles()
-    sv = mp.gen_workload(5, True, 4.0, 0.6, 100.0, 7, ps, backend=S.host_backend())
-    with pytest.raises(ValueError):
+    sv = mp.gen_workload(17, True, 2.0, 0.6, 100.0, 7, ps, backend=S.host_backend())
+    with pytest.raises(ValueError, match="16"):
         mp.brute_force_optimum(sv, ps, RULES, 3, backend=S.product_backend())
+
+
+def test_wide_pool_cases_present():
+    """n >= 5 instances (5-7-service configs in the max_mix = min(n, 7) pool) are pinned."""
+    wide = [k for k, v in BF.items() if len(v["services"]) >= 5]
+    assert len(wide) >= 20
+    assert any(isinstance(BF[k]["outcome"], list) and "nodes" in BF[k] for k in wide)
+    assert any(str(BF[k]["outcome"]).startswith("error:") for k in wide)
 
 
 @pytest.mark.parametrize("name", sorted(k for k, v in BF.items() if "nodes" in v))
