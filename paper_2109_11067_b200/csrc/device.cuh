@@ -223,6 +223,7 @@ struct MctsLaunch {
     int n_sup;               // 0: scan every row
     const int* sup_begin;    // n_sup + 1 row offsets
     const unsigned short* sup_svc;  // service a | b << 8 (b = 0xFF: single-service support)
+    int l1_slots;            // on-chip rollout-cache slots (power of two; 0: global table only)
     MctsSolveArgs s[kMaxGroups];
 };
 

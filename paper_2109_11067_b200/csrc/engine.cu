@@ -39,7 +39,8 @@ const void* bf_best_any_kernel_ptr();
 const void* bf_sum_kernel_ptr();
 const void* bf_warp_kernel_ptr();
 int bf_threads();
-const void* mcts_kernel_ptr();
+const void* mcts_kernel_ptr(int n);  // the key-width variant for n services
+void mcts_set_dense_pct(int pct);
 void mcts_read_topk_timers(unsigned long long* h);
 void greedy_read_diag(unsigned long long* skew_ns, unsigned long long* release_ns);
 size_t keyrank_scratch_bytes(long long P);
@@ -472,15 +473,17 @@ const DeviceInfo& device_info(int device) {
     info.smem_optin = static_cast<long long>(prop.sharedMemPerBlockOptin);
     // every kernel may use all the opt-in shared memory its static allocation leaves
     CK(cudaFuncSetAttribute(topk1_kernel_ptr(32), cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-    CK(cudaFuncSetAttribute(mcts_kernel_ptr(), cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    CK(cudaFuncSetAttribute(mcts_kernel_ptr(1), cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    CK(cudaFuncSetAttribute(mcts_kernel_ptr(255), cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     CK(cudaFuncSetAttribute(greedy_kernel_ptr(), cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     for (const void* k : {greedy_kernel_ptr(), topk_kernel_ptr(), topk1_kernel_ptr(32), rollout_kernel_ptr(1), rollout_kernel_ptr(256),
-                          mcts_kernel_ptr()}) {
+                          mcts_kernel_ptr(1), mcts_kernel_ptr(255)}) {
         cudaFuncAttributes fa{};
         CK(cudaFuncGetAttributes(&fa, k));
         CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 static_cast<int>(prop.sharedMemPerBlockOptin - fa.sharedSizeBytes)));
-        if (k == mcts_kernel_ptr()) info.mcts_static_smem = static_cast<long long>(fa.sharedSizeBytes);
+        if (k == mcts_kernel_ptr(1) || k == mcts_kernel_ptr(255))  // the larger of the two variants
+            info.mcts_static_smem = std::max(info.mcts_static_smem, static_cast<long long>(fa.sharedSizeBytes));
         if (k == greedy_kernel_ptr()) info.greedy_static_smem = static_cast<long long>(fa.sharedSizeBytes);
     }
     return cache.emplace(device, info).first->second;
@@ -1373,7 +1376,7 @@ std::vector<MctsDeviceResult> Engine::mcts_device_group(const std::vector<std::v
             o.best = take(sizeof(int) * path_cap);
             o.desc = take(sizeof(int) * path_cap);
             o.dcomp = take(sizeof(double) * n);
-            o.out = take(sizeof(int) * 24);
+            o.out = take(sizeof(int) * 32);
             if (s->mcts_bytes < off) {
                 if (s->mcts_mem) CK(cudaFree(s->mcts_mem));
                 s->mcts_mem = nullptr;
@@ -1443,14 +1446,25 @@ std::vector<MctsDeviceResult> Engine::mcts_device_group(const std::vector<std::v
             L->rows_smem = static_cast<long long>(mcts_smem_bytes(n, m_.PP, mn, slice, false, true, pair, ns)) <= room;
             if (!(L->rows_smem && pair)) ns = 0;
             L->timers = std::getenv("MIGPLAN_MCTS_TIMERS") ? 1 : 0;
+            if (const char* v = std::getenv("MIGPLAN_MCTS_DENSE_PCT")) mcts_set_dense_pct(std::atoi(v));
             L->node_smem =
                 static_cast<long long>(mcts_smem_bytes(n, m_.PP, mn, slice, true, L->rows_smem != 0, pair, ns)) <= room;
             L->n_sup = ns;
             L->sup_begin = ns ? d_sup_begin_ : nullptr;
             L->sup_svc = ns ? d_sup_svc_ : nullptr;
         }
-        const size_t msm = mcts_smem_bytes(n, m_.PP, static_cast<int>(offs[0].max_nodes), slice, L->node_smem != 0,
-                                           L->rows_smem != 0, pair, L->n_sup);
+        size_t msm = mcts_smem_bytes(n, m_.PP, static_cast<int>(offs[0].max_nodes), slice, L->node_smem != 0,
+                                     L->rows_smem != 0, pair, L->n_sup);
+        {  // the on-chip rollout cache takes what is left (key words, pool size, K (index, row) pairs per slot)
+            const DeviceInfo& di = device_info(device_);
+            const long long left = di.smem_optin - di.mcts_static_smem - 1024 - static_cast<long long>(msm) - 64;
+            const long long per = 8ll * ((n + 63) / 64) + 4 + 8ll * topk;
+            int slots = 4096;
+            while (slots >= 32 && slots * per > left) slots >>= 1;
+            if (const char* v = std::getenv("MIGPLAN_MCTS_L1")) slots = std::min(slots, std::atoi(v));
+            L->l1_slots = slots >= 32 ? slots : 0;
+            msm += L->l1_slots ? static_cast<size_t>(L->l1_slots * per + 48) : 0;
+        }
         for (int q = 1; q < nb; ++q) CK(cudaStreamSynchronize(slots[q]->stream));
         Slot* s0 = slots[0];
         void* args[] = {L.get()};
@@ -1468,7 +1482,7 @@ std::vector<MctsDeviceResult> Engine::mcts_device_group(const std::vector<std::v
             attr[0].val.clusterDim.z = 1;
             cfg.attrs = attr;
             cfg.numAttrs = 1;
-            CK(cudaLaunchKernelExC(&cfg, mcts_kernel_ptr(), args));
+            CK(cudaLaunchKernelExC(&cfg, mcts_kernel_ptr(n), args));
         }
         stats.launches++;
         CK(cudaEventRecord(s0->e1, s0->stream));
@@ -1481,10 +1495,10 @@ std::vector<MctsDeviceResult> Engine::mcts_device_group(const std::vector<std::v
             const Off& o = offs[q];
             unsigned char* b = static_cast<unsigned char*>(slots[q]->mcts_mem);
             // the outputs are carved contiguously (trace, best, desc, dcomp, out): one copy
-            std::vector<unsigned char> hb(o.out + sizeof(int) * 24 - o.trace);
+            std::vector<unsigned char> hb(o.out + sizeof(int) * 32 - o.trace);
             CK(cudaMemcpy(hb.data(), b + o.trace, hb.size(), cudaMemcpyDeviceToHost));
             auto at = [&](size_t off) { return hb.data() + (off - o.trace); };
-            int out[24];
+            int out[32];
             std::memcpy(out, at(o.out), sizeof(out));
             MctsDeviceResult& r = results[b0 + q];
             r.status = out[0];
@@ -1500,12 +1514,15 @@ std::vector<MctsDeviceResult> Engine::mcts_device_group(const std::vector<std::v
                 unsigned long long tk[8];
                 mcts_read_topk_timers(tk);
                 if (tk[5])
-                    std::fprintf(stderr, "[mcts] top-K (cumulative) calls %llu, cycles/call: tables %.0f pass1 %.0f pass2 %.0f "
-                                 "keyrank %.0f rank %.0f, candidates/call %.1f\n", tk[5], double(tk[0]) / tk[5], double(tk[1]) / tk[5],
-                                 double(tk[2]) / tk[5], double(tk[7]) / tk[5], double(tk[3]) / tk[5], double(tk[4]) / tk[5]);
+                    std::fprintf(stderr, "[mcts] top-K (cumulative) calls %llu, cycles/call: tables %.0f scan %.0f tree %.0f pass2 %.0f "
+                                 "rank %.0f, candidates/call %.1f\n", tk[5], double(tk[0]) / tk[5], double(tk[7]) / tk[5],
+                                 double(tk[1]) / tk[5], double(tk[2]) / tk[5], double(tk[3]) / tk[5], double(tk[4]) / tk[5]);
                 std::fprintf(stderr, "[mcts] solve %d: %.1f ms device, cycles sel %lld expand-host %lld miss-host %lld topk %lld "
-                             "rollout-ctl %lld, builds %d expands %d iters %d, exact-path top-Ks (cumulative) %d\n",
-                             b0 + q, ms, t[0], t[1], t[2], t[3], t[4], out[4], out[7], out[6], out[20]);
+                             "rollout-ctl %lld, builds %d expands %d iters %d, exact-path top-Ks (cumulative) %d, walk steps %d "
+                             "cycles %lld, probes %d cycles %lld, entries %d\n",
+                             b0 + q, ms, t[0], t[1], t[2], t[3], t[4], out[4], out[7], out[6], out[20], out[21],
+                             *reinterpret_cast<const long long*>(&out[22]), out[24], *reinterpret_cast<const long long*>(&out[26]),
+                             out[25]);
             }
             r.trace.resize(4 * static_cast<size_t>(r.iterations));
             std::vector<int> best(std::max(r.best_len, 0)), desc(out[2]);

@@ -25,13 +25,16 @@ using namespace dev;
 
 namespace {
 
-constexpr int kMThreads = 512;
+#ifndef MGB_MCTS_THREADS
+#define MGB_MCTS_THREADS 512
+#endif
+constexpr int kMThreads = MGB_MCTS_THREADS;  // a power-of-two number of warps (the top-K merge tree)
 constexpr int kMaxServicesDev = 256;  // >= kMaxServices (model.hpp)
 constexpr int kMWarps = kMThreads / 32;
 constexpr int kMCandCap = 512;  // above-threshold rows per top-K (ties beyond: exact k-round path)
 constexpr int kMMaxK = 32;
 constexpr unsigned char kExpanded = 1, kLeaf = 2;
-constexpr int kL1Slots = 256, kL1MaxK = 16, kL1Empty = -2, kL1Pending = -3;
+constexpr int kL1Empty = -2, kL1Pending = -3;
 
 struct Mt64 {  // std::mt19937_64 (w 64, n 312, m 156, r 31)
     uint64_t mt[312];
@@ -472,12 +475,26 @@ struct SupTab {
     int* act;
 };
 
-__device__ __noinline__ int block_topk_pair(const DevModel& M, const unsigned* keyrank, const unsigned* base, long long nb,
+// block_topk_pair's block-wide counters: zero at kernel start (mcts_kernel) and re-zeroed by
+// every call before its closing barrier, so a call needs no opening barrier for them.
+__shared__ int tp_ncand, tp_nhit, tp_nact, tp_actrows;
+__device__ __forceinline__ void topk_pair_counters_init() {
+    if (threadIdx.x == 0) tp_ncand = tp_nhit = tp_nact = tp_actrows = 0;
+}
+__device__ int g_mcts_dense_pct = 60;  // dense scan when live rows exceed this % of the pool
+
+// Inlined into mcts_kernel: as a call, the ABI's register saves around each call site pushed
+// the 128-register kernel into spilling on the search's serial paths (measured: the GA
+// context's searches 17.4 vs 19.4 ms per two_phase inlined vs called).
+#ifdef MGB_TOPK_NOINLINE
+__device__ __noinline__
+#else
+__device__ __forceinline__
+#endif
+int block_topk_pair(const DevModel& M, const unsigned* keyrank, const unsigned* base, long long nb,
                                long long pos0, const double* comp, const uint64_t* mask, int k, const double* U,
                                double* W, float* Wf, unsigned char* hitc, Cand* cand, Cand* win, int* out, int* scored,
                                bool tm, SupTab sup) {
-    __shared__ unsigned t_fbits;
-    __shared__ int n_cand, n_hit;
     __shared__ Cand red[kMWarps];
     long long c0 = 0, c1 = 0;
     auto mark = [&](int slot) {
@@ -488,9 +505,12 @@ __device__ __noinline__ int block_topk_pair(const DevModel& M, const unsigned* k
         }
     };
     mark(-1);
+    const int lane = static_cast<int>(threadIdx.x & 31u);
+    const int wid = static_cast<int>(threadIdx.x >> 5), nwarps = static_cast<int>(blockDim.x >> 5);
     const int nW = (M.n + 1) * M.PP;
     const unsigned sent = static_cast<unsigned>(M.n * M.PP);
     const uint64_t hiS = static_cast<uint64_t>(sent | (sent << 16)) << 32;
+    // ---- tables (W = need * U, its FP32 round-up, mask hits) and the live supports: one barrier
     for (int e = threadIdx.x; e < nW; e += blockDim.x) {
         const int svc = e / M.PP;
         double w = 0.0;
@@ -502,20 +522,11 @@ __device__ __noinline__ int block_topk_pair(const DevModel& M, const unsigned* k
         Wf[e] = __double2float_ru(w);
         if (mask) hitc[e] = svc < M.n && ((mask[svc >> 6] >> (svc & 63)) & 1ull) != 0;
     }
-    __shared__ int s_nact, s_actrows;
-    if (threadIdx.x == 0) {
-        t_fbits = 0u;
-        n_cand = 0;
-        n_hit = 0;
-        s_nact = 0;
-        s_actrows = 0;
-    }
-    __syncthreads();
     // Supports that can hold a candidate: a member with need > 0 (rows of the others all score
     // 0), or, with a mask, a sampled member (every row of such a support touches it).
-    bool bysup = sup.n > 0;
-    const int wid = static_cast<int>(threadIdx.x >> 5), nwarps = static_cast<int>(blockDim.x >> 5);
-    if (bysup) {
+    const int dense_pct = g_mcts_dense_pct;
+    const bool sup_pass = sup.n > 0 && dense_pct < 100;
+    if (sup_pass) {
         int hitrows = 0;
         for (int s0 = 0; s0 < sup.n; s0 += blockDim.x) {
             const int si = s0 + static_cast<int>(threadIdx.x);
@@ -531,7 +542,7 @@ __device__ __noinline__ int block_topk_pair(const DevModel& M, const unsigned* k
             }
             const unsigned bm = __ballot_sync(0xffffffffu, live);
             int at = 0;
-            if ((threadIdx.x & 31u) == 0 && bm) at = atomicAdd(&s_nact, __popc(bm));
+            if (lane == 0 && bm) at = atomicAdd(&tp_nact, __popc(bm));
             at = __shfl_sync(0xffffffffu, at, 0) + __popc(bm & lanemask_lt());
             if (live) {
                 sup.act[at] = si;
@@ -539,13 +550,12 @@ __device__ __noinline__ int block_topk_pair(const DevModel& M, const unsigned* k
             }
         }
         for (int off = 16; off > 0; off >>= 1) hitrows += __shfl_xor_sync(0xffffffffu, hitrows, off);
-        if ((threadIdx.x & 31u) == 0) atomicAdd(&s_actrows, hitrows);
-        __syncthreads();
-        // most rows live: the dense 4-rows-per-load scan is cheaper than a warp per support
-        if (10ll * s_actrows > 6ll * nb) bysup = false;
-        if (bysup && mask && threadIdx.x == 0) n_hit = s_actrows;  // (the dense scan counts its hits)
+        if (lane == 0 && hitrows) atomicAdd(&tp_actrows, hitrows);
     }
-    const int nact = bysup ? s_nact : 0;
+    __syncthreads();
+    // few live rows: a warp per live support; most rows live: the dense 8-rows-per-iteration scan
+    const bool bysup = sup_pass && 100ll * tp_actrows <= static_cast<long long>(dense_pct) * nb;
+    const int nact = bysup ? tp_nact : 0;
     mark(0);
     const uint4* base4 = reinterpret_cast<const uint4*>(base);  // 4 rows per 16 bytes
     const long long nq = nb >> 2;
@@ -554,15 +564,9 @@ __device__ __noinline__ int block_topk_pair(const DevModel& M, const unsigned* k
     // whose third bound is below the threshold has at most these two candidate rows
     float umax = 0.0f, u2 = 0.0f, u3 = 0.0f;
     unsigned x1 = 0u, x2 = 0u;
-    long long p1 = -1, p2 = -1;
+    int p1 = -1, p2 = -1;
     int hits = 0;
-    auto bound1 = [&](unsigned x, long long pos) {
-        float u = ub_pair(Wf, x);
-        if (mask && !bysup) {
-            const bool h = hit_pair(hitc, x);
-            hits += h;
-            if (!h) u = 0.0f;
-        }
+    auto insert = [&](float u, unsigned x, int pos) {
         if (u > u3) {
             if (u > u2) {
                 u3 = u2;
@@ -577,62 +581,103 @@ __device__ __noinline__ int block_topk_pair(const DevModel& M, const unsigned* k
             }
         }
     };
-    if (bysup) {  // a warp per active support, lanes over its rows
-        const int lane = static_cast<int>(threadIdx.x & 31u);
+    const bool dmask = mask && !bysup;
+    // 8 rows: bounds (0 off the mask), and the insertion only when one beats the third bound
+    auto bound8 = [&](const unsigned (&x)[8], int r0, int r1) {
+        float ub[8];
+        float mx = 0.0f;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            ub[j] = ub_pair(Wf, x[j]);
+            if (dmask) {
+                const bool h = hit_pair(hitc, x[j]);
+                hits += h;
+                if (!h) ub[j] = 0.0f;
+            }
+            mx = fmaxf(mx, ub[j]);
+        }
+        if (mx > u3) {
+#pragma unroll
+            for (int j = 0; j < 8; ++j) insert(ub[j], x[j], j < 4 ? r0 + j : r1 + j - 4);
+        }
+    };
+    const unsigned sp = sent | (sent << 16);
+    if (bysup) {  // a warp per active support, lanes over its rows (two rounds per load batch)
         for (int i = wid; i < nact; i += nwarps) {
             const int si = sup.act[i];
             const int b = sup.begin[si], e = sup.begin[si + 1];
-            for (int r = b + lane; r < e; r += 32) bound1(base[r], pos0 + r);
+            for (int r0 = b; r0 < e; r0 += 64) {
+                const int ra = r0 + lane, rb = ra + 32;
+                const unsigned xa = ra < e ? base[ra] : sp, xb = rb < e ? base[rb] : sp;
+                const float ua = ub_pair(Wf, xa), ubb = ub_pair(Wf, xb);
+                if (fmaxf(ua, ubb) > u3) {
+                    insert(ua, xa, static_cast<int>(pos0) + ra);
+                    insert(ubb, xb, static_cast<int>(pos0) + rb);
+                }
+            }
         }
+        if (mask && threadIdx.x == 0) tp_nhit = tp_actrows;  // every row of a live support touches the mask
     } else {
         long long p = threadIdx.x;
         for (; p + B < nq; p += 2 * B) {
             const uint4 v0 = base4[p], v1 = base4[p + B];
-            const long long r0 = pos0 + 4 * p, r1 = pos0 + 4 * (p + B);
-            bound1(v0.x, r0), bound1(v0.y, r0 + 1), bound1(v0.z, r0 + 2), bound1(v0.w, r0 + 3);
-            bound1(v1.x, r1), bound1(v1.y, r1 + 1), bound1(v1.z, r1 + 2), bound1(v1.w, r1 + 3);
+            const unsigned x[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
+            bound8(x, static_cast<int>(pos0 + 4 * p), static_cast<int>(pos0 + 4 * (p + B)));
         }
         for (; p < nq; p += B) {
             const uint4 v = base4[p];
-            const long long r0 = pos0 + 4 * p;
-            bound1(v.x, r0), bound1(v.y, r0 + 1), bound1(v.z, r0 + 2), bound1(v.w, r0 + 3);
+            const unsigned x[8] = {v.x, v.y, v.z, v.w, sp, sp, sp, sp};
+            bound8(x, static_cast<int>(pos0 + 4 * p), 0);
         }
-        if (threadIdx.x < (nb & 3)) bound1(base[4 * nq + threadIdx.x], pos0 + 4 * nq + threadIdx.x);
+        if (threadIdx.x < (nb & 3)) {
+            const unsigned x[8] = {base[4 * nq + threadIdx.x], sp, sp, sp, sp, sp, sp, sp};
+            bound8(x, static_cast<int>(pos0 + 4 * nq + threadIdx.x), 0);
+        }
+        if (dmask) {
+            for (int off = 16; off > 0; off >>= 1) hits += __shfl_xor_sync(0xffffffffu, hits, off);
+            if (lane == 0 && hits) atomicAdd(&tp_nhit, hits);
+        }
     }
-    if (mask && !bysup) {
-        for (int off = 16; off > 0; off >>= 1) hits += __shfl_xor_sync(0xffffffffu, hits, off);
-        if ((threadIdx.x & 31u) == 0) atomicAdd(&n_hit, hits);
-    }
-    // U_K = the K-th largest of ALL lane maxima: every warp sorts its lane maxima, then a
-    // tree of bitonic merges (top 32 of two sorted lists: elementwise max against the partner
-    // reversed, then 5 merge stages) leaves the block's top 32 in warp 0.
-    __shared__ float ws[2][kMWarps / 2][32];
+    mark(7);
+    // the listed rows' config-order key ranks, in flight while the threshold is found
+    const unsigned kr1 = p1 >= 0 ? __ldg(keyrank + p1) : 0u, kr2 = p2 >= 0 ? __ldg(keyrank + p2) : 0u;
+    // U_K: the K-th largest of the warps' four largest lane maxima (bounds are >= 0, so their
+    // bits order like the values).  These are bounds of distinct rows, so K rows have a bound
+    // >= U_K; with four per warp it is within a few ranks of the K-th largest lane maximum.
+    __shared__ unsigned wtop[kMWarps * 4];
     {
-        const int w = static_cast<int>(threadIdx.x >> 5), lane = static_cast<int>(threadIdx.x & 31u);
-        float srt = warp_sort_desc_f(umax);
-        int buf = 0;
-        for (int half = static_cast<int>(blockDim.x >> 6); half >= 1; half >>= 1, buf ^= 1) {
-            if (w >= half && w < 2 * half) ws[buf][w - half][lane] = srt;
-            __syncthreads();
-            if (w < half) {
-                float v = fmaxf(srt, ws[buf][w][31 - lane]);
+        unsigned mine = __float_as_uint(umax);
 #pragma unroll
-                for (int j = 16; j > 0; j >>= 1) {
-                    const float o = __shfl_xor_sync(0xffffffffu, v, j);
-                    v = (lane & j) == 0 ? fmaxf(v, o) : fminf(v, o);
-                }
-                srt = v;
-            }
+        for (int r = 0; r < 4; ++r) {
+            const unsigned m = __reduce_max_sync(0xffffffffu, mine);
+            const unsigned eq = __ballot_sync(0xffffffffu, mine == m);
+            if (lane == 0) wtop[wid * 4 + r] = m;
+            if (lane == __ffs(eq) - 1) mine = 0u;
         }
-        if (w == 0 && lane == k - 1) t_fbits = __float_as_uint(srt);
     }
     __syncthreads();
+    unsigned tk_bits = 0u;
+    {  // every warp: K rounds of max-and-remove over the nwarps * 4 values (no second barrier)
+        const int nv = nwarps * 4;
+        unsigned v0 = lane < nv ? wtop[lane] : 0u, v1 = lane + 32 < nv ? wtop[lane + 32] : 0u;
+        for (int r = 0; r < k; ++r) {
+            const unsigned m = __reduce_max_sync(0xffffffffu, max(v0, v1));
+            tk_bits = m;
+            const unsigned e0 = __ballot_sync(0xffffffffu, v0 == m);
+            if (e0) {
+                if (lane == __ffs(e0) - 1) v0 = 0u;
+            } else {
+                const unsigned e1 = __ballot_sync(0xffffffffu, v1 == m);
+                if (lane == __ffs(e1) - 1) v1 = 0u;
+            }
+        }
+    }
     mark(1);
-    const double LB = __dmul_rd(static_cast<double>(__uint_as_float(t_fbits)), 1.0 - 0x1p-20);
+    const double LB = __dmul_rd(static_cast<double>(__uint_as_float(tk_bits)), 1.0 - 0x1p-20);
     const float LB_f = __double2float_rd(LB);
-    // one compaction per 8 rows: the lane's taken rows, a warp scan, one atomic per warp
-    auto emit = [&](const unsigned (&x)[8], const double (&sc)[8], unsigned tk, long long r0, long long r1) {
-        const int lane = static_cast<int>(threadIdx.x & 31u);
+    // one compaction per up to 8 rows: the lane's taken rows, a warp scan, one atomic per warp;
+    // each candidate's config-order key rank is fetched here (its latency overlaps the scan)
+    auto emit = [&](const unsigned (&x)[8], const double (&sc)[8], const long long (&pk)[8], unsigned tk) {
         const int cnt = __popc(tk);
         int incl = cnt;
 #pragma unroll
@@ -643,27 +688,27 @@ __device__ __noinline__ int block_topk_pair(const DevModel& M, const unsigned* k
         const int total = __shfl_sync(0xffffffffu, incl, 31);
         if (total == 0) return;
         int at = 0;
-        if (lane == 31) at = atomicAdd(&n_cand, total);
+        if (lane == 31) at = atomicAdd(&tp_ncand, total);
         at = __shfl_sync(0xffffffffu, at, 31) + incl - cnt;
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
             if ((tk >> j) & 1u) {
                 if (at < kMCandCap) {
                     const uint64_t row = x[j] | hiS;
-                    cand[at] = Cand{sc[j], row_usum(U, row), row, (j < 4 ? r0 + j : r1 + j - 4)};
+                    cand[at] = Cand{sc[j], row_usum(U, row), row, pk[j]};
                 }
                 ++at;
             }
         }
     };
-    const unsigned sp = sent | (sent << 16);
     const uint4 padv = make_uint4(sp, sp, sp, sp);
     // lanes with a third bound reaching LB rescan all their rows; the others offer their two
     // listed rows (exact scores only where a bound reaches LB)
     const bool rescan = u3 > 0.0f && u3 >= LB_f;
     {
-        unsigned xs[8] = {x1, x2, sp, sp, sp, sp, sp, sp};
+        const unsigned xs[8] = {x1, x2, sp, sp, sp, sp, sp, sp};
         double sc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        const long long ps[8] = {p1 | static_cast<long long>(kr1) << 32, p2 | static_cast<long long>(kr2) << 32, 0, 0, 0, 0, 0, 0};
         unsigned tk = 0;
         if (!rescan) {
             if (umax > 0.0f && umax >= LB_f) {
@@ -675,81 +720,66 @@ __device__ __noinline__ int block_topk_pair(const DevModel& M, const unsigned* k
                 if (sc[1] > 0.0 && sc[1] >= LB) tk |= 2u;
             }
         }
-        if (__any_sync(0xffffffffu, tk != 0)) {  // emit() numbers row j as r0 + j: one listed row per call
-            emit(xs, sc, tk & 1u, p1, 0);
-            unsigned xs2[8] = {x2, sp, sp, sp, sp, sp, sp, sp};
-            double sc2[8] = {sc[1], 0, 0, 0, 0, 0, 0, 0};
-            emit(xs2, sc2, (tk >> 1) & 1u, p2, 0);
-        }
+        if (__any_sync(0xffffffffu, tk != 0)) emit(xs, sc, ps, tk);
     }
-    if (bysup && __any_sync(0xffffffffu, rescan)) {  // the same rows as pass 1, one per lane per call
-        const int lane = static_cast<int>(threadIdx.x & 31u);
+    auto exact8 = [&](const unsigned (&x)[8], const int (&pos)[8], bool masked) {  // rescans: key ranks loaded here
+        float ub[8];
+        float mx = 0.0f;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            ub[j] = ub_pair(Wf, x[j]);
+            if (masked && !hit_pair(hitc, x[j])) ub[j] = 0.0f;
+            mx = fmaxf(mx, ub[j]);
+        }
+        if (!__any_sync(0xffffffffu, mx > 0.0f && mx >= LB_f)) return;
+        double sc[8];
+        unsigned tk = 0;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            sc[j] = 0.0;
+            if (ub[j] > 0.0f && ub[j] >= LB_f) {
+                sc[j] = __dadd_rn(W[x[j] & 0xFFFFu], W[x[j] >> 16]);
+                if (sc[j] > 0.0 && sc[j] >= LB) tk |= 1u << j;
+            }
+        }
+        long long pk[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) pk[j] = (tk >> j) & 1u ? pack_pos(keyrank, pos[j]) : 0ll;
+        emit(x, sc, pk, tk);
+    };
+    if (bysup && __any_sync(0xffffffffu, rescan)) {  // the same rows as pass 1, two per lane per call
         for (int i = wid; i < nact; i += nwarps) {
             const int si = sup.act[i];
             const int b = sup.begin[si], e = sup.begin[si + 1];
-            for (int r0 = b; r0 < e; r0 += 32) {
-                const int r = r0 + lane;
-                unsigned xs[8] = {rescan && r < e ? base[r] : sp, sp, sp, sp, sp, sp, sp, sp};
-                double sc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-                unsigned tk = 0;
-                const float ub = ub_pair(Wf, xs[0]);
-                if (ub > 0.0f && ub >= LB_f) {
-                    sc[0] = __dadd_rn(W[xs[0] & 0xFFFFu], W[xs[0] >> 16]);
-                    if (sc[0] > 0.0 && sc[0] >= LB) tk = 1u;
-                }
-                emit(xs, sc, tk, pos0 + r, 0);
+            for (int r0 = b; r0 < e; r0 += 64) {
+                const int ra = r0 + lane, rb = ra + 32;
+                const unsigned x[8] = {rescan && ra < e ? base[ra] : sp, rescan && rb < e ? base[rb] : sp, sp, sp, sp, sp, sp, sp};
+                const int ps[8] = {static_cast<int>(pos0) + ra, static_cast<int>(pos0) + rb, 0, 0, 0, 0, 0, 0};
+                exact8(x, ps, false);
             }
         }
-    } else if (__any_sync(0xffffffffu, rescan)) {
+    } else if (!bysup && __any_sync(0xffffffffu, rescan)) {
         const long long nq2 = (nq + 2 * B - 1) / (2 * B) * (2 * B);
         for (long long p0 = threadIdx.x; p0 < nq2; p0 += 2 * B) {
             const uint4 v0 = rescan && p0 < nq ? base4[p0] : padv;
             const uint4 v1 = rescan && p0 + B < nq ? base4[p0 + B] : padv;
             const unsigned x[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
-            float ub[8];
-            float mx = 0.0f;
-#pragma unroll
-            for (int j = 0; j < 8; ++j) {
-                ub[j] = ub_pair(Wf, x[j]);
-                if (mask && !hit_pair(hitc, x[j])) ub[j] = 0.0f;
-                mx = fmaxf(mx, ub[j]);
-            }
-            if (!__any_sync(0xffffffffu, mx > 0.0f && mx >= LB_f)) continue;
-            double sc[8];
-            unsigned tk = 0;
-#pragma unroll
-            for (int j = 0; j < 8; ++j) {
-                sc[j] = 0.0;
-                if (ub[j] > 0.0f && ub[j] >= LB_f) {
-                    sc[j] = __dadd_rn(W[x[j] & 0xFFFFu], W[x[j] >> 16]);
-                    if (sc[j] > 0.0 && sc[j] >= LB) tk |= 1u << j;
-                }
-            }
-            emit(x, sc, tk, pos0 + 4 * p0, pos0 + 4 * (p0 + B));
+            const int r0 = static_cast<int>(pos0 + 4 * p0), r1 = static_cast<int>(pos0 + 4 * (p0 + B));
+            const int ps[8] = {r0, r0 + 1, r0 + 2, r0 + 3, r1, r1 + 1, r1 + 2, r1 + 3};
+            exact8(x, ps, mask != nullptr);
         }
         if (nb & 3) {  // the last rows, warp 0 (the scan needs the whole warp)
-            if ((threadIdx.x >> 5) == 0) {
+            if (wid == 0) {
                 const int t = static_cast<int>(threadIdx.x);
-                unsigned x[8] = {rescan && t < (nb & 3) ? base[4 * nq + t] : sp, sp, sp, sp, sp, sp, sp, sp};
-                double sc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-                unsigned tk = 0;
-                const float ub = ub_pair(Wf, x[0]);
-                if (ub > 0.0f && ub >= LB_f && (!mask || hit_pair(hitc, x[0]))) {
-                    sc[0] = __dadd_rn(W[x[0] & 0xFFFFu], W[x[0] >> 16]);
-                    if (sc[0] > 0.0 && sc[0] >= LB) tk = 1u;
-                }
-                emit(x, sc, tk, pos0 + 4 * nq + t, 0);
+                const unsigned x[8] = {rescan && t < (nb & 3) ? base[4 * nq + t] : sp, sp, sp, sp, sp, sp, sp, sp};
+                const int ps[8] = {static_cast<int>(pos0 + 4 * nq) + t, 0, 0, 0, 0, 0, 0, 0};
+                exact8(x, ps, mask != nullptr);
             }
         }
     }
     __syncthreads();
     mark(2);
-    const int nc = n_cand;
-    if (nc <= kMCandCap) {
-        fill_keyrank(keyrank, cand, nc);
-        __syncthreads();
-    }
-    mark(7);
+    const int nc = tp_ncand;
     int got;
     if (nc <= kMCandCap) {
         got = min(nc, k);
@@ -775,7 +805,7 @@ __device__ __noinline__ int block_topk_pair(const DevModel& M, const unsigned* k
                              __shfl_xor_sync(0xffffffffu, b.row, off), __shfl_xor_sync(0xffffffffu, b.pos, off)};
                 if (o.row != kNoRow && (b.row == kNoRow || precedes_kr(o, b))) b = o;
             }
-            if ((threadIdx.x & 31u) == 0) red[threadIdx.x >> 5] = b;
+            if (lane == 0) red[wid] = b;
             __syncthreads();
             Cand x = red[0];
             for (int w = 1; w < kMWarps; ++w)
@@ -789,7 +819,10 @@ __device__ __noinline__ int block_topk_pair(const DevModel& M, const unsigned* k
     }
     __syncthreads();
     if (out && threadIdx.x < got) out[threadIdx.x] = pos_of(win[threadIdx.x]);
-    if (threadIdx.x == 0) *scored = mask ? n_hit : static_cast<int>(nb);
+    if (threadIdx.x == 0) {
+        *scored = mask ? tp_nhit : static_cast<int>(nb);
+        tp_ncand = tp_nhit = tp_nact = tp_actrows = 0;  // the next call's counters
+    }
     __syncthreads();
     mark(3);
     if (tm && threadIdx.x == 0) {
@@ -815,6 +848,9 @@ __device__ __forceinline__ void add_row_util(const DevModel& M, const double* U,
 
 }  // namespace
 
+// NK: 64-bit words of the rollout-cache key (the unsatisfied bitmap): 1 for n <= 64, else 4 —
+// the walk keeps the key in registers, so the narrow variant frees 12 of them.
+template <int NK>
 __global__ void __launch_bounds__(kMThreads, 1) mcts_kernel(const __grid_constant__ MctsLaunch L) {
     extern __shared__ __align__(16) unsigned char smem[];
     // One search per thread-block CLUSTER: rank 0 runs the search; every rank scans its slice
@@ -895,6 +931,7 @@ __global__ void __launch_bounds__(kMThreads, 1) mcts_kernel(const __grid_constan
         s_exit = 0;
         s_usemask = 0;
     }
+    topk_pair_counters_init();
     __syncthreads();
     if (rank != 0) {  // helper: serve rank 0's top-K requests until it posts exit
         for (;;) {
@@ -980,16 +1017,19 @@ __global__ void __launch_bounds__(kMThreads, 1) mcts_kernel(const __grid_constan
     pick_tab_init(s_pick);
     __shared__ int s_node, s_leaf, s_expand, s_take, s_nch, s_done, s_est, s_miss, s_slot, s_abort, s_steps;
     __shared__ int s_edges, s_path, s_best, s_have, s_nodes, s_builds, s_iters, s_scored, s_expands;
-    __shared__ long long s_expand_rows;
+    __shared__ long long s_expand_rows, s_wcyc;  // s_wcyc, s_wsteps: walk cycles and steps (timers)
+    __shared__ int s_wsteps, s_wprobes, s_wentries;
+    __shared__ long long s_wpcyc;
     __shared__ int s_out[kMMaxK];
     __shared__ int s_unsat[kMaxServicesDev];  // expand: the node's unsatisfied services
-    // on-chip level of the rollout cache: kL1Slots keys (filled to 3/4) with their pools
-    __shared__ uint64_t l1_key[kL1Slots][4];
-    __shared__ int l1_n[kL1Slots];
-    __shared__ unsigned l1_pool[kL1Slots][kL1MaxK];
-    __shared__ int l1_used, s_l1, s_l1new;
-    const bool use_l1 = K <= kL1MaxK;
-    for (int q = threadIdx.x; q < kL1Slots; q += blockDim.x) l1_n[q] = kL1Empty;
+    // on-chip level of the rollout cache (dynamic shared memory, filled to 3/4): per slot the
+    // key's nk words, the pool size and the pool as (base index, low 32 row bits)
+    __shared__ int l1_used, s_l1new;
+    const int l1_slots = rank == 0 ? L.l1_slots : 0, nk = (n + 63) >> 6;
+    uint64_t* l1k = reinterpret_cast<uint64_t*>(carve(sizeof(uint64_t) * l1_slots * nk));
+    int* l1n = reinterpret_cast<int*>(carve(sizeof(int) * l1_slots));
+    uint2* l1p = reinterpret_cast<uint2*>(carve(sizeof(uint2) * l1_slots * K));
+    for (int q = threadIdx.x; q < l1_slots; q += blockDim.x) l1n[q] = kL1Empty;
     if (threadIdx.x == 0) l1_used = 0;
     // rows by pool index for the utility adds: the on-chip copy when it holds the whole pool
     const uint64_t* prow = (C == 1 && L.rows_smem && !pair) ? slice : rows;
@@ -998,8 +1038,9 @@ __global__ void __launch_bounds__(kMThreads, 1) mcts_kernel(const __grid_constan
     const int max_depth = 2 * a.l_ref;
     const int tid = threadIdx.x;
     long long t_sel = 0, t_exp = 0, t_miss = 0, t_roll = 0, t_topk = 0, tc = 0;  // thread-0 clock64 phase split
+    const bool timers = L.timers != 0;
     auto tick = [&](long long& acc) {
-        if (tid == 0) {
+        if (timers && tid == 0) {
             const long long t = clock64();
             acc += t - tc;
             tc = t;
@@ -1018,6 +1059,11 @@ __global__ void __launch_bounds__(kMThreads, 1) mcts_kernel(const __grid_constan
         s_iters = 0;
         s_expands = 0;
         s_expand_rows = 0;
+        s_wcyc = 0;
+        s_wsteps = 0;
+        s_wprobes = 0;
+        s_wentries = 0;
+        s_wpcyc = 0;
         nvis[0] = 0;
         nval[0] = 0.0;
         nnch[0] = 0;
@@ -1194,128 +1240,212 @@ __global__ void __launch_bounds__(kMThreads, 1) mcts_kernel(const __grid_constan
             // warp 0 steps alone through cache hits; the block joins for a miss's top-K
             for (;;) {
                 if (warp == 0) {
-                    // n <= 32: lane i keeps cur[i] in a register for the whole walk (written back
-                    // when the block needs it: a miss's top-K, or the end of the rollout)
+                    // Warp 0 walks; its state is warp-uniform registers: the unsatisfied bitmap (the
+                    // type key), the cache entry it maps to (re-probed only when the key changes:
+                    // most steps satisfy no service), the pick constants of that entry's size and
+                    // the mt19937_64 position.  n <= 32: lane i keeps cur[i] in a register.
                     const bool regc = n <= 32;
                     double creg = regc && lane < n ? cur[lane] : 2.0;
-                    // every lane keeps the step count; lane 0 writes it back when the walk pauses
                     int r_steps = *reinterpret_cast<volatile int*>(&s_steps);
+                    int midx = *reinterpret_cast<volatile int*>(&g.idx);
+                    uint64_t kw[NK];
+#pragma unroll
+                    for (int w = 0; w < NK; ++w) kw[w] = ~0ull;
+                    bool have = false, inl1 = false;
+                    int pn = 0, slot = 0;  // the entry: pool size, L1 slot (inl1) or global slot
+                    const int steps0 = r_steps;
+                    const long long wc0 = timers ? clock64() : 0;
                     __syncwarp();
                     if (lane == 0) s_miss = 0;
                     for (;;) {
-                        if (g.idx >= 312) mt_twist_warp(g);  // the serial twist in mt_next stays the fallback
-                        uint64_t kw[4] = {0, 0, 0, 0};
+                        uint64_t kn[NK];
+#pragma unroll
+                        for (int w = 0; w < NK; ++w) kn[w] = 0ull;
                         if (regc) {
-                            kw[0] = __ballot_sync(0xffffffffu, lane < n && creg < 1.0 - 1e-9);
+                            kn[0] = __ballot_sync(0xffffffffu, lane < n && creg < 1.0 - 1e-9);
                         } else {
-                            for (int i0 = 0; i0 < n; i0 += 32) {
-                                const int i = i0 + lane;
-                                const unsigned bm = __ballot_sync(0xffffffffu, i < n && cur[i] < 1.0 - 1e-9);
-                                kw[i0 >> 6] |= static_cast<uint64_t>(bm) << (i0 & 63);
+#pragma unroll
+                            for (int c = 0; c < 2 * NK; ++c) {  // static indices: kn stays in registers
+                                const int i = 32 * c + lane;
+                                if (32 * c < n) {
+                                    const unsigned bm = __ballot_sync(0xffffffffu, i < n && cur[i] < 1.0 - 1e-9);
+                                    kn[c >> 1] |= static_cast<uint64_t>(bm) << (32 * (c & 1));
+                                }
                             }
                         }
-                        int st = 0, idx = 0;  // st: 1 done, 2 miss, 3 abort
-                        if (!(kw[0] | kw[1] | kw[2] | kw[3]) || r_steps >= max_depth) {  // satisfied / depth cap
+                        int st = 0;  // 1 done, 2 miss, 3 abort
+                        uint64_t any = 0ull, diff = 0ull;
+#pragma unroll
+                        for (int w = 0; w < NK; ++w) {
+                            any |= kn[w];
+                            diff |= kn[w] ^ kw[w];
+                        }
+                        if (!any || r_steps >= max_depth) {  // satisfied / depth cap
                             if (lane == 0) {
                                 s_done = 1;
-                                s_est = (kw[0] | kw[1] | kw[2] | kw[3]) ? max_depth : r_steps;
+                                s_est = any ? max_depth : r_steps;
                             }
                             st = 1;
-                        } else {
+                        } else if (!have || diff) {
+                            const long long pc0 = timers ? clock64() : 0;
+#pragma unroll
+                            for (int w = 0; w < NK; ++w) kw[w] = kn[w];
+                            have = false;
                             // the cache's own hash (not reference-visible): one multiply
-                            uint64_t h = (kw[0] ^ (kw[1] << 16 | kw[1] >> 48) ^ (kw[2] << 32 | kw[2] >> 32) ^
-                                          (kw[3] << 48 | kw[3] >> 16)) * 0x9e3779b97f4a7c15ull;
+                            uint64_t h = kw[0];
+#pragma unroll
+                            for (int w = 1; w < NK; ++w) h ^= kw[w] << (16 * w) | kw[w] >> (64 - 16 * w);
+                            h *= 0x9e3779b97f4a7c15ull;
                             h ^= h >> 29;
-                            // level 1: the on-chip copy of the cache, probed 32 slots at a time by
-                            // the whole warp (linear probing: the key lies before the first empty slot)
+                            // level 1: the on-chip copy, probed 32 slots at a time (linear probing:
+                            // the key lies before the first empty slot)
                             int l1 = -1;
-                            if (use_l1) {
-                                const unsigned q0 = static_cast<unsigned>(h >> 32) & (kL1Slots - 1);
-                                for (int b0 = 0; b0 < kL1Slots; b0 += 32) {
-                                    const unsigned q = (q0 + b0 + lane) & (kL1Slots - 1);
-                                    const bool empty = l1_n[q] == kL1Empty;
-                                    const bool match = !empty && l1_key[q][0] == kw[0] && l1_key[q][1] == kw[1] &&
-                                                       l1_key[q][2] == kw[2] && l1_key[q][3] == kw[3];
+                            if (l1_slots) {
+                                const unsigned q0 = static_cast<unsigned>(h >> 32) & (l1_slots - 1);
+                                for (int b0 = 0; b0 < l1_slots; b0 += 32) {
+                                    const unsigned q = (q0 + b0 + lane) & (l1_slots - 1);
+                                    const int qn = l1n[q];
+                                    bool match = qn != kL1Empty;
+#pragma unroll
+                                    for (int w = 0; w < NK; ++w)
+                                        if (w < nk) match = match && l1k[q * nk + w] == kw[w];
                                     const unsigned bm = __ballot_sync(0xffffffffu, match);
                                     if (bm) {
-                                        l1 = static_cast<int>((q0 + b0 + __ffs(bm) - 1) & (kL1Slots - 1));
+                                        l1 = static_cast<int>((q0 + b0 + __ffs(bm) - 1) & (l1_slots - 1));
                                         break;
                                     }
-                                    if (__ballot_sync(0xffffffffu, empty)) break;
+                                    if (__ballot_sync(0xffffffffu, qn == kL1Empty)) break;
                                 }
                             }
-                            if (lane == 0) {  // lane 0's state lives in registers; the block reads it after the walk
-                                int l1new = -1, slot = 0;
-                                bool miss = false;
-                                if (l1 < 0) {  // level 2: the global table (source of truth)
-                                    unsigned sl = static_cast<unsigned>(h) & a.tab_mask;
-                                    for (unsigned t = 0;; ++t, sl = (sl + 1) & a.tab_mask) {
-                                        if (t > a.tab_mask) {
-                                            s_abort = 2;  // cache full
-                                            st = 3;
-                                            break;
-                                        }
-                                        if (!a.tag[sl]) {  // miss: insert, pool built by the block
-                                            a.tag[sl] = 1;
-                                            for (int w = 0; w < 4; ++w) a.key[4ull * sl + w] = kw[w];
-                                            miss = true;
-                                            st = 2;
-                                            break;
-                                        }
-                                        if (a.key[4ull * sl] == kw[0] && a.key[4ull * sl + 1] == kw[1] &&
-                                            a.key[4ull * sl + 2] == kw[2] && a.key[4ull * sl + 3] == kw[3])
-                                            break;
-                                    }
-                                    slot = static_cast<int>(sl);
-                                    if (miss && use_l1 && l1_used < kL1Slots * 3 / 4) {  // mirror the new key on chip
-                                        unsigned q = static_cast<unsigned>(h >> 32) & (kL1Slots - 1);
-                                        while (l1_n[q] != kL1Empty) q = (q + 1) & (kL1Slots - 1);
-                                        for (int w = 0; w < 4; ++w) l1_key[q][w] = kw[w];
-                                        l1_n[q] = kL1Pending;
-                                        ++l1_used;
-                                        l1new = static_cast<int>(q);
-                                    }
-                                }
-                                if (st == 0) {  // hit: a uniform pick from the cached pool
-                                    const int pn = l1 >= 0 ? l1_n[l1] : a.pool_n[slot];
-                                    if (pn <= 0) {
-                                        s_abort = 1;  // "rollout: no candidate config serves the remaining demand"
+                            if (l1 >= 0) {
+                                inl1 = true;
+                                pn = l1n[l1];
+                                slot = l1;
+                            } else {  // level 2: the global table (source of truth), 32 slots a probe
+                                inl1 = false;
+                                int found = -1, empty_at = -1;
+                                for (unsigned t0 = 0;; t0 += 32) {
+                                    if (t0 > a.tab_mask) {
+                                        if (lane == 0) s_abort = 2;  // cache full
                                         st = 3;
-                                    } else {
-                                        const unsigned pk = static_cast<unsigned>(mt_pick(g, static_cast<uint64_t>(pn), &s_pick));
-                                        idx = static_cast<int>(l1 >= 0 ? l1_pool[l1][pk]
-                                                                       : a.pool[static_cast<long long>(slot) * K + pk]);
-                                        a.picked[r_steps] = idx;
+                                        break;
+                                    }
+                                    const unsigned sl = (static_cast<unsigned>(h) + t0 + lane) & a.tab_mask;
+                                    const bool used = a.tag[sl] != 0;
+                                    bool match = used;
+#pragma unroll
+                                    for (int w = 0; w < NK; ++w)
+                                        if (w < nk) match = match && a.key[4ull * sl + w] == kw[w];
+                                    const unsigned mm = __ballot_sync(0xffffffffu, match), em = __ballot_sync(0xffffffffu, !used);
+                                    const unsigned fmask = mm & (em ? ((em & (0u - em)) - 1u) : 0xffffffffu);  // before the first empty
+                                    if (fmask) {
+                                        found = static_cast<int>((static_cast<unsigned>(h) + t0 + __ffs(fmask) - 1) & a.tab_mask);
+                                        break;
+                                    }
+                                    if (em) {
+                                        empty_at = static_cast<int>((static_cast<unsigned>(h) + t0 + __ffs(em) - 1) & a.tab_mask);
+                                        break;
                                     }
                                 }
-                                if (st == 2) {  // the block builds this key's pool
-                                    s_miss = 1;
-                                    s_slot = slot;
-                                    s_l1new = l1new;
+                                if (st == 0 && found < 0) {  // miss: insert; the block builds the pool
+                                    st = 2;
+                                    if (lane == 0) {
+                                        a.tag[empty_at] = 1;
+#pragma unroll
+                                        for (int w = 0; w < 4; ++w) a.key[4ull * empty_at + w] = w < NK ? kw[w] : 0ull;
+                                        int l1new = -1;
+                                        if (l1_slots && l1_used < l1_slots * 3 / 4) {  // mirror the new key on chip
+                                            unsigned q = static_cast<unsigned>(h >> 32) & (l1_slots - 1);
+                                            while (l1n[q] != kL1Empty) q = (q + 1) & (l1_slots - 1);
+#pragma unroll
+                                            for (int w = 0; w < NK; ++w)
+                                                if (w < nk) l1k[q * nk + w] = kw[w];
+                                            l1n[q] = kL1Pending;
+                                            ++l1_used;
+                                            l1new = static_cast<int>(q);
+                                        }
+                                        s_miss = 1;
+                                        s_slot = empty_at;
+                                        s_l1new = l1new;
+                                    }
+                                } else if (st == 0) {
+                                    slot = found;
+                                    pn = a.pool_n[found];
                                 }
+                            }
+                            if (st == 0) {
+                                if (pn <= 0) {
+                                    if (lane == 0) s_abort = 1;  // "rollout: no candidate config serves the remaining demand"
+                                    st = 3;
+                                } else {
+                                    have = true;
+                                }
+                            }
+                            if (timers && lane == 0) {
+                                ++s_wprobes;
+                                s_wpcyc += clock64() - pc0;
                             }
                         }
-                        st = __shfl_sync(0xffffffffu, st, 0);
                         if (st) {
-                            if (lane == 0) s_steps = r_steps;
+                            if (midx >= 312) {  // twist here, warp-parallel, not in lane 0's next mt_next
+                                mt_twist_warp(g);
+                                midx = 0;
+                            }
+                            if (lane == 0) {
+                                s_steps = r_steps;
+                                g.idx = midx;
+                                if (timers) {
+                                    ++s_wentries;
+                                    s_wsteps += r_steps - steps0;
+                                    s_wcyc += clock64() - wc0;
+                                }
+                            }
                             if (regc && lane < n) cur[lane] = creg;
                             break;
                         }
+                        // a uniform pick from the cached pool (pick_index, util.hpp:39-47), every lane
+                        unsigned pk = 0;
+                        if (pn > 1) {  // pick_index constants (mt_pick), read beside the draw
+                            const uint64_t lim = s_pick.lim[pn], fm = s_pick.fm[pn];
+                            const unsigned p32 = s_pick.p32[pn];
+                            uint64_t r;
+                            do {
+                                if (midx >= 312) {
+                                    mt_twist_warp(g);
+                                    midx = 0;
+                                }
+                                r = g.out[midx++];
+                            } while (r >= lim);
+                            const unsigned m = static_cast<unsigned>(pn);
+                            const unsigned ra = fastmod32(static_cast<unsigned>(r >> 32), fm, m), rb = fastmod32(static_cast<unsigned>(r), fm, m);
+                            pk = fastmod32(ra * p32 + rb, fm, m);
+                        }
+                        int idx;
+                        uint64_t row;
+                        if (inl1) {
+                            const uint2 e = l1p[slot * K + pk];
+                            idx = static_cast<int>(e.x);
+                            row = pair ? (static_cast<uint64_t>(e.y) | hiS) : rowat(idx);
+                        } else {
+                            idx = static_cast<int>(a.pool[static_cast<long long>(slot) * K + pk]);
+                            row = rowat(idx);
+                        }
+                        if (lane == 0) a.picked[r_steps] = idx;
                         ++r_steps;
-                        idx = __shfl_sync(0xffffffffu, idx, 0);
                         if (regc) {  // rollout add (mcts.hpp:139) in the owning lanes
-                            const uint64_t row = rowat(idx);
 #pragma unroll
                             for (int m = 0; m < 4; ++m) {
                                 const int code = static_cast<int>((row >> (16 * m)) & 0xFFFFull);
                                 if (csvc[code] == lane) creg = __dadd_rn(creg, Us[code]);
                             }
-                        } else if (lane < 4) {  // distinct services: the adds commute
-                            const int code = static_cast<int>((rowat(idx) >> (16 * lane)) & 0xFFFFull);
-                            const int svc = csvc[code];
-                            if (svc < n) cur[svc] = __dadd_rn(cur[svc], Us[code]);
+                        } else {
+                            if (lane < 4) {  // distinct services: the adds commute
+                                const int code = static_cast<int>((row >> (16 * lane)) & 0xFFFFull);
+                                const int svc = csvc[code];
+                                if (svc < n) cur[svc] = __dadd_rn(cur[svc], Us[code]);
+                            }
+                            __syncwarp();
                         }
-                        __syncwarp();
                     }
                 }
                 __syncthreads();
@@ -1325,11 +1455,15 @@ __global__ void __launch_bounds__(kMThreads, 1) mcts_kernel(const __grid_constan
                 // finds the key again and picks from the new pool
                 const int got = cluster_topk(false, s_out, &s_scored);
                 tick(t_topk);
-                if (tid < got) a.pool[static_cast<long long>(s_slot) * K + tid] = static_cast<unsigned>(s_out[tid]);
-                if (s_l1new >= 0 && tid < got) l1_pool[s_l1new][tid] = static_cast<unsigned>(s_out[tid]);
+                if (tid < got) {
+                    a.pool[static_cast<long long>(s_slot) * K + tid] = static_cast<unsigned>(s_out[tid]);
+                    if (s_l1new >= 0)
+                        l1p[static_cast<long long>(s_l1new) * K + tid] =
+                            make_uint2(static_cast<unsigned>(s_out[tid]), static_cast<unsigned>(rowat(s_out[tid])));
+                }
                 if (tid == 0) {
                     a.pool_n[s_slot] = got;
-                    if (s_l1new >= 0) l1_n[s_l1new] = got;
+                    if (s_l1new >= 0) l1n[s_l1new] = got;
                     ++s_builds;
                 }
                 __syncthreads();
@@ -1392,6 +1526,11 @@ __global__ void __launch_bounds__(kMThreads, 1) mcts_kernel(const __grid_constan
         reinterpret_cast<long long*>(a.out)[8] = t_topk;  // out[16..17]
         reinterpret_cast<long long*>(a.out)[9] = t_roll;  // out[18..19]
         a.out[20] = static_cast<int>(g_mcts_fallbacks);
+        a.out[21] = s_wsteps;
+        reinterpret_cast<long long*>(a.out)[11] = s_wcyc;  // out[22..23]
+        a.out[24] = s_wprobes;
+        a.out[25] = s_wentries;
+        reinterpret_cast<long long*>(a.out)[13] = s_wpcyc;  // out[26..27]
         reinterpret_cast<long long*>(a.out)[4] = s_expand_rows;  // out[8..9]
     }
     if (threadIdx.x == 0) s_exit = 1;  // release the helper ranks
@@ -1429,7 +1568,10 @@ size_t mcts_smem_bytes(int n, int PP, int max_nodes, long long n_base, bool node
     return off;
 }
 void mcts_read_topk_timers(unsigned long long* h) { cudaMemcpyFromSymbol(h, g_tk, sizeof g_tk); }
-const void* mcts_kernel_ptr() { return reinterpret_cast<const void*>(&mcts_kernel); }
+void mcts_set_dense_pct(int pct) { cudaMemcpyToSymbol(g_mcts_dense_pct, &pct, sizeof pct); }
+const void* mcts_kernel_ptr(int n) {
+    return n <= 64 ? reinterpret_cast<const void*>(&mcts_kernel<1>) : reinterpret_cast<const void*>(&mcts_kernel<4>);
+}
 int mcts_threads() { return kMThreads; }
 
 }  // namespace mgb
