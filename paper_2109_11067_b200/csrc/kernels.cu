@@ -539,6 +539,9 @@ __global__ void __launch_bounds__(256) enum_base_kernel(const __grid_constant__ 
 template <int NT>
 __global__ void __launch_bounds__(NT, 1) greedy_kernel(const __grid_constant__ GreedyLaunch GL) {
     constexpr int NW = NT / 32;
+#ifdef MGB_GREEDY_PRINT_PHASES
+    const unsigned long long t_entry = globaltimer();
+#endif
     extern __shared__ __align__(16) unsigned char smem[];
     const int grp = static_cast<int>(blockIdx.x) / GL.ctas_per_group;
     const GreedyArgs& a = GL.g[grp];
@@ -663,10 +666,13 @@ __global__ void __launch_bounds__(NT, 1) greedy_kernel(const __grid_constant__ G
                 cnt[k] = B > off[k] ? (B - off[k] + P - 1) / P : 0;
                 total += cnt[k];
             }
-            for (long long base = gw * 32; base < total; base += GW * 32) {
+            // batch width: 32 supports per warp when there is work for every warp's lanes,
+            // fewer (down to 1) for small events so every warp of the grid gets a share
+            const long long bw = min(32ll, max(1ll, (total + GW - 1) / GW));
+            for (long long base = gw * bw; base < total; base += GW * bw) {
                 // level 1: lane = one support
                 const long long g = base + ln;
-                bool live = g < total;
+                bool live = ln < bw && g < total;
                 int k = M.max_mix + 1;
                 unsigned packed = 0xFFFFFFFFu;  // members, ascending, one byte each (0xFF unused)
                 if (live) {
@@ -825,6 +831,9 @@ __global__ void __launch_bounds__(NT, 1) greedy_kernel(const __grid_constant__ G
             tp = t;
         }
     };
+#ifdef MGB_GREEDY_PRINT_PHASES
+    const unsigned long long t_loop = globaltimer();
+#endif
     while (!s_done) {
         if (s_status != kOk) {
             status = s_status;
@@ -965,6 +974,9 @@ __global__ void __launch_bounds__(NT, 1) greedy_kernel(const __grid_constant__ G
         if (s_events > s_first_new) extend_and_sync();
     }
     mark(4);
+#ifdef MGB_GREEDY_PRINT_PHASES
+    const unsigned long long t_end = globaltimer();
+#endif
     if (GL.cluster) cg::this_cluster().sync();  // peers may still read this CTA's xch over DSMEM
     if (bi == 0) {  // one coalesced copy of the plan to host-mapped memory
         for (int i = threadIdx.x; i < step; i += blockDim.x) {
@@ -985,6 +997,11 @@ __global__ void __launch_bounds__(NT, 1) greedy_kernel(const __grid_constant__ G
         o->ext_count = *reinterpret_cast<volatile unsigned long long*>(&a.st->ext_count);
         o->status = *reinterpret_cast<volatile int*>(&a.st->status);
         __threadfence_system();
+#ifdef MGB_GREEDY_PRINT_PHASES
+        const unsigned long long t_exit = globaltimer();
+        printf("[greedy cta0] prologue %.1f us (events %d), loop %.1f us (%d steps), epilogue %.1f us, G %d\n",
+               (t_loop - t_entry) / 1e3, s_events, (t_end - t_loop) / 1e3, step, (t_exit - t_end) / 1e3, G);
+#endif
     }
 }
 
