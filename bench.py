@@ -184,9 +184,9 @@ def measured_peak():
 
 # committed `ncu --set full` captures (tools/ncu_summary.py) per kernel and workload
 TRAFFIC_PROFILES = {
-    ("greedy_kernel", "gen128_8.0_greedy"): "r02_greedy_gen128_ncu.json",
-    ("mcts_kernel", "slos24_ga10"): "r02_mcts_slos24_ncu.json",
-    ("greedy_kernel", "slos24_ga10"): "r01c_greedy_slos24_ncu.json",
+    ("greedy_kernel", "gen128_8.0_greedy"): "r02g_greedy_gen128_ncu.json",
+    ("mcts_kernel", "slos24_ga10"): "r02g_mcts_ga_ncu.json",
+    ("greedy_kernel", "slos24_ga10"): "r02g_greedy_slos24_ncu.json",
 }
 
 
