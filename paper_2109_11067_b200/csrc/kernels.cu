@@ -190,6 +190,13 @@ constexpr int kKeyMaxPP = 128;  // key tables on chip up to this many patterns
 constexpr int kKeyMaxLayouts = 32;  // == kMaxLayouts (model.hpp)
 __device__ unsigned long long g_dep[1024], g_cta_dur[1024], g_scan[1024], g_post[1024];
 __device__ unsigned long long g_arrive0, g_arrive_last, g_skew_ns, g_release_ns;
+#ifdef MGB_GREEDY_STEP_DIAG
+// development aid: per step, the slowest CTA's scan (ns, which CTA), the mean, and the most
+// exact-path rows one CTA evaluated; CTA 0 prints the table at the end of the launch
+constexpr int kDiagSteps = 4096;
+__device__ unsigned long long g_sd_max[kDiagSteps], g_sd_sum[kDiagSteps], g_sd_exact[kDiagSteps], g_sd_arg[kDiagSteps];
+__device__ unsigned g_sd_cnt[1024];
+#endif
 __device__ Best grid_argmax(const DevModel& M, const Best& mine, Best* partials, Best* winrec, unsigned* count,
                             unsigned* gen, int G, Best* red, const GreedyArgs& a, unsigned long long seq,
                             int* xstatus, int bi) {
@@ -325,8 +332,12 @@ __device__ __forceinline__ void consider8(const DevModel& M, const double* __res
                                (static_cast<uint64_t>(v3.y) << 32) | v3.x, (static_cast<uint64_t>(v3.w) << 32) | v3.z};
 #pragma unroll
         for (int j = 0; j < 8; ++j)
-            if (static_cast<double>(ub[j]) >= (fl > 0.0 ? fl : 4.9406564584124654e-324) && r[j] != best.row)
+            if (static_cast<double>(ub[j]) >= (fl > 0.0 ? fl : 4.9406564584124654e-324) && r[j] != best.row) {
+#ifdef MGB_GREEDY_STEP_DIAG
+                atomicAdd(&g_sd_cnt[blockIdx.x], 1u);
+#endif
                 take(M, U, r[j], row_score(W, r[j]), best);
+            }
     }
 }
 
@@ -930,6 +941,16 @@ __global__ void __launch_bounds__(NT, 1) greedy_kernel(const __grid_constant__ G
         prev_row = best.row;
         const Best bb = block_best(M, best, red);
         if (a.phase_timers && threadIdx.x == 0) g_scan[blockIdx.x] += globaltimer() - t_scan0;
+#ifdef MGB_GREEDY_STEP_DIAG
+        if (threadIdx.x == 0 && step < kDiagSteps) {
+            const unsigned long long dt = globaltimer() - t_scan0;
+            atomicMax(&g_sd_max[step], dt);
+            atomicAdd(&g_sd_sum[step], dt);
+            const unsigned c = atomicExch(&g_sd_cnt[blockIdx.x], 0u);
+            atomicMax(&g_sd_exact[step], static_cast<unsigned long long>(c));
+            atomicMax(&g_sd_arg[step], (dt << 12) | blockIdx.x);
+        }
+#endif
         mark(0);
         last_seq = a.exch_seq0 + static_cast<unsigned long long>(step) + 1ull;
         const Best win = GL.cluster               ? cluster_argmax(M, bb, xch, step & 1, red, G)
@@ -997,6 +1018,13 @@ __global__ void __launch_bounds__(NT, 1) greedy_kernel(const __grid_constant__ G
         o->ext_count = *reinterpret_cast<volatile unsigned long long*>(&a.st->ext_count);
         o->status = *reinterpret_cast<volatile int*>(&a.st->status);
         __threadfence_system();
+#ifdef MGB_GREEDY_STEP_DIAG
+        for (int q = 0; q < step && q < kDiagSteps; ++q) {
+            printf("[step %d] rows %lld scan max %.2f us (cta %llu) mean %.2f us, max exact rows/cta %llu\n", q,
+                   a.pick_rows[q], g_sd_max[q] / 1e3, g_sd_arg[q] & 4095ull, g_sd_sum[q] / 1e3 / G, g_sd_exact[q]);
+            g_sd_max[q] = g_sd_sum[q] = g_sd_exact[q] = g_sd_arg[q] = 0;
+        }
+#endif
 #ifdef MGB_GREEDY_PRINT_PHASES
         const unsigned long long t_exit = globaltimer();
         printf("[greedy cta0] prologue %.1f us (events %d), loop %.1f us (%d steps), epilogue %.1f us, G %d\n",

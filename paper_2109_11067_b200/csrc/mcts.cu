@@ -35,6 +35,7 @@ constexpr int kMCandCap = 512;  // above-threshold rows per top-K (ties beyond: 
 constexpr int kMMaxK = 32;
 constexpr unsigned char kExpanded = 1, kLeaf = 2;
 constexpr int kL1Empty = -2, kL1Pending = -3;
+constexpr int kLogSmem = 256;  // log(visits) entries kept on chip (selection reads one per level)
 
 struct Mt64 {  // std::mt19937_64 (w 64, n 312, m 156, r 31)
     uint64_t mt[312];
@@ -1015,6 +1016,8 @@ __global__ void __launch_bounds__(kMThreads, 1) mcts_kernel(const __grid_constan
     __shared__ Mt64 g;
     __shared__ PickTab s_pick;
     pick_tab_init(s_pick);
+    __shared__ double s_log[kLogSmem];
+    for (int v = threadIdx.x; v < kLogSmem && v < L.budget + 2; v += blockDim.x) s_log[v] = L.logtab[v];
     __shared__ int s_node, s_leaf, s_expand, s_take, s_nch, s_done, s_est, s_miss, s_slot, s_abort, s_steps;
     __shared__ int s_edges, s_path, s_best, s_have, s_nodes, s_builds, s_iters, s_scored, s_expands;
     __shared__ long long s_expand_rows, s_wcyc;  // s_wcyc, s_wsteps: walk cycles and steps (timers)
@@ -1084,7 +1087,8 @@ __global__ void __launch_bounds__(kMThreads, 1) mcts_kernel(const __grid_constan
             if (lane == 0) a.pathnodes[0] = 0;
             while ((nflags[node] & kExpanded) && !(nflags[node] & kLeaf) && nnch[node] > 0) {
                 const int nch = nnch[node], f0 = nfirst[node];
-                const double log_n = L.logtab[max(1, nvis[node])];
+                const int nv = max(1, nvis[node]);
+                const double log_n = nv < kLogSmem ? s_log[nv] : L.logtab[nv];
                 int pick = -1, bq = -1;
                 double bv = -1.0;
                 for (int q0 = 0; q0 < nch; q0 += 32) {
@@ -1222,19 +1226,39 @@ __global__ void __launch_bounds__(kMThreads, 1) mcts_kernel(const __grid_constan
                 if (s_abort) break;
             }
             // random child (mcts.hpp:202-207)
+            __shared__ int s_child_row;
             if (tid == 0) {
                 const int nch = nnch[s_node];
+                s_child_row = -1;
                 if (nch > 0) {
                     const int c = nfirst[s_node] + static_cast<int>(mt_pick(g, static_cast<uint64_t>(nch), &s_pick));
                     a.edges[s_edges++] = ncand[c];
                     a.pathnodes[s_path++] = c;
                     s_node = c;
+                    s_child_row = ncand[c];
                 }
                 s_steps = 0;
                 s_done = 0;
             }
             __syncthreads();
-            for (int i = tid; i < n; i += blockDim.x) cur[i] = a.node_comp[static_cast<long long>(s_node) * n + i];
+            if (s_expand) {
+                // expanded in this iteration: `cur` still holds the parent's completion, and the
+                // child's is the same adds the expansion made (bit for bit), without re-reading it
+                if (s_child_row >= 0 && warp == 0) {
+                    const uint64_t row = rowat(s_child_row);
+                    for (int i = lane; i < n; i += 32) {
+                        double v = cur[i];
+#pragma unroll
+                        for (int m = 0; m < 4; ++m) {
+                            const int code = static_cast<int>((row >> (16 * m)) & 0xFFFFull);
+                            if (csvc[code] == i) v = __dadd_rn(v, Us[code]);
+                        }
+                        cur[i] = v;
+                    }
+                }
+            } else {
+                for (int i = tid; i < n; i += blockDim.x) cur[i] = a.node_comp[static_cast<long long>(s_node) * n + i];
+            }
             __syncthreads();
             // rollout (mcts.hpp:122-143) with the RolloutCache keyed by the unsatisfied bitmap:
             // warp 0 steps alone through cache hits; the block joins for a miss's top-K
@@ -1300,6 +1324,9 @@ __global__ void __launch_bounds__(kMThreads, 1) mcts_kernel(const __grid_constan
                             // level 1: the on-chip copy, probed 32 slots at a time (linear probing:
                             // the key lies before the first empty slot)
                             int l1 = -1;
+                            // while the on-chip level has never refused a key (it is filled to 3/4)
+                            // it holds every key of this search: an L1 miss is a cache miss
+                            const bool l1_all = l1_slots && *reinterpret_cast<volatile int*>(&l1_used) < l1_slots * 3 / 4;
                             if (l1_slots) {
                                 const unsigned q0 = static_cast<unsigned>(h >> 32) & (l1_slots - 1);
                                 for (int b0 = 0; b0 < l1_slots; b0 += 32) {
@@ -1321,7 +1348,22 @@ __global__ void __launch_bounds__(kMThreads, 1) mcts_kernel(const __grid_constan
                                 inl1 = true;
                                 pn = l1n[l1];
                                 slot = l1;
-                            } else {  // level 2: the global table (source of truth), 32 slots a probe
+                            } else if (l1_all) {  // miss, inserted on chip only (no global round trips)
+                                inl1 = false;
+                                st = 2;
+                                if (lane == 0) {
+                                    unsigned q = static_cast<unsigned>(h >> 32) & (l1_slots - 1);
+                                    while (l1n[q] != kL1Empty) q = (q + 1) & (l1_slots - 1);
+#pragma unroll
+                                    for (int w = 0; w < NK; ++w)
+                                        if (w < nk) l1k[q * nk + w] = kw[w];
+                                    l1n[q] = kL1Pending;
+                                    ++l1_used;
+                                    s_miss = 1;
+                                    s_slot = -1;
+                                    s_l1new = static_cast<int>(q);
+                                }
+                            } else {  // level 2: the global table (keys the full L1 refused), 32 slots a probe
                                 inl1 = false;
                                 int found = -1, empty_at = -1;
                                 for (unsigned t0 = 0;; t0 += 32) {
@@ -1456,13 +1498,13 @@ __global__ void __launch_bounds__(kMThreads, 1) mcts_kernel(const __grid_constan
                 const int got = cluster_topk(false, s_out, &s_scored);
                 tick(t_topk);
                 if (tid < got) {
-                    a.pool[static_cast<long long>(s_slot) * K + tid] = static_cast<unsigned>(s_out[tid]);
+                    if (s_slot >= 0) a.pool[static_cast<long long>(s_slot) * K + tid] = static_cast<unsigned>(s_out[tid]);
                     if (s_l1new >= 0)
                         l1p[static_cast<long long>(s_l1new) * K + tid] =
                             make_uint2(static_cast<unsigned>(s_out[tid]), static_cast<unsigned>(rowat(s_out[tid])));
                 }
                 if (tid == 0) {
-                    a.pool_n[s_slot] = got;
+                    if (s_slot >= 0) a.pool_n[s_slot] = got;
                     if (s_l1new >= 0) l1n[s_l1new] = got;
                     ++s_builds;
                 }
