@@ -56,7 +56,13 @@ static __device__ __noinline__ void row_key(const DevModel& M, uint64_t row, uin
 }
 
 // Third key of candidate_preferred; reached only on exact (score, util_sum) ties.
+#ifdef MGB_GREEDY_STEP_DIAG
+__device__ unsigned g_sd_keys[1024];
+#endif
 static __device__ __noinline__ bool row_key_less(const DevModel& M, uint64_t a, uint64_t b) {
+#ifdef MGB_GREEDY_STEP_DIAG
+    atomicAdd(&g_sd_keys[blockIdx.x], 1u);
+#endif
     uint64_t ah, al, bh, bl;
     row_key(M, a, ah, al);
     row_key(M, b, bh, bl);
@@ -95,6 +101,30 @@ __device__ __forceinline__ Best shfl_xor_best(const Best& b, int off) {
                 __shfl_xor_sync(0xffffffffu, b.row, off)};
 }
 
+// Lane holding the smallest config key among the `tied` lanes (rows tied on score and
+// util_sum): every tied lane computes its own key once, in parallel (a call: the keys' table
+// loads stay out of the caller's register budget).
+static __device__ __noinline__ int warp_key_argmin(const DevModel& M, uint64_t row, bool tied) {
+    const int lane = static_cast<int>(lane_id());
+    uint64_t kh = ~0ull, kl = ~0ull;
+    if (tied) row_key(M, row, kh, kl);
+    int ln = tied ? lane : 32;
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+        const uint64_t oh = __shfl_xor_sync(0xffffffffu, kh, off), ol = __shfl_xor_sync(0xffffffffu, kl, off);
+        const int on = __shfl_xor_sync(0xffffffffu, ln, off);
+        if (oh < kh || (oh == kh && (ol < kl || (ol == kl && on < ln)))) kh = oh, kl = ol, ln = on;
+    }
+    return ln;
+}
+
+// The warp's best under candidate_preferred, in every lane.  The butterfly orders by
+// (score, util_sum) and, on equal pairs, by the raw row bits — cheap, but not the reference's
+// third key — so when lanes holding DISTINCT rows tie with the winner on both, the config key
+// decides among them: each tied lane computes its key once, in parallel, instead of two keys
+// per tied pair at each of the five levels (tie-heavy greedy steps of slos_24 spent up to
+// 25 us per step in serial key compares: tools/ab/diag.so, MGB_GREEDY_STEP_DIAG).
+#ifdef MGB_OLD_WARP_BEST
 __device__ __forceinline__ Best warp_best(const DevModel& M, Best b) {
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) {
@@ -103,6 +133,23 @@ __device__ __forceinline__ Best warp_best(const DevModel& M, Best b) {
     }
     return b;
 }
+#else
+__device__ __forceinline__ Best warp_best(const DevModel& M, Best b) {
+    Best w = b;
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+        const Best o = shfl_xor_best(w, off);
+        if (o.s > w.s || (o.s == w.s && (o.u > w.u || (o.u == w.u && o.row < w.row)))) w = o;
+    }
+    if (w.row == kNoRow) return none();
+    const bool tied = b.row != kNoRow && b.s == w.s && b.u == w.u;
+    if (__any_sync(0xffffffffu, tied && b.row != w.row)) {
+        const int src = warp_key_argmin(M, b.row, tied);
+        w = Best{__shfl_sync(0xffffffffu, b.s, src), __shfl_sync(0xffffffffu, b.u, src), __shfl_sync(0xffffffffu, b.row, src)};
+    }
+    return w;
+}
+#endif
 
 // Generation barrier across all co-resident (cooperatively launched) CTAs.  The CTA's
 // writes are ordered before thread 0's arrival by bar.sync + a gpu-scope acq_rel fence

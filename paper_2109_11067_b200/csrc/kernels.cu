@@ -194,7 +194,7 @@ __device__ unsigned long long g_arrive0, g_arrive_last, g_skew_ns, g_release_ns;
 // development aid: per step, the slowest CTA's scan (ns, which CTA), the mean, and the most
 // exact-path rows one CTA evaluated; CTA 0 prints the table at the end of the launch
 constexpr int kDiagSteps = 4096;
-__device__ unsigned long long g_sd_max[kDiagSteps], g_sd_sum[kDiagSteps], g_sd_exact[kDiagSteps], g_sd_arg[kDiagSteps];
+__device__ unsigned long long g_sd_max[kDiagSteps], g_sd_sum[kDiagSteps], g_sd_exact[kDiagSteps], g_sd_arg[kDiagSteps], g_sd_key[kDiagSteps];
 __device__ unsigned g_sd_cnt[1024];
 #endif
 __device__ Best grid_argmax(const DevModel& M, const Best& mine, Best* partials, Best* winrec, unsigned* count,
@@ -949,6 +949,8 @@ __global__ void __launch_bounds__(NT, 1) greedy_kernel(const __grid_constant__ G
             const unsigned c = atomicExch(&g_sd_cnt[blockIdx.x], 0u);
             atomicMax(&g_sd_exact[step], static_cast<unsigned long long>(c));
             atomicMax(&g_sd_arg[step], (dt << 12) | blockIdx.x);
+            const unsigned kc = atomicExch(&g_sd_keys[blockIdx.x], 0u);
+            atomicMax(&g_sd_key[step], static_cast<unsigned long long>(kc));
         }
 #endif
         mark(0);
@@ -1020,9 +1022,9 @@ __global__ void __launch_bounds__(NT, 1) greedy_kernel(const __grid_constant__ G
         __threadfence_system();
 #ifdef MGB_GREEDY_STEP_DIAG
         for (int q = 0; q < step && q < kDiagSteps; ++q) {
-            printf("[step %d] rows %lld scan max %.2f us (cta %llu) mean %.2f us, max exact rows/cta %llu\n", q,
-                   a.pick_rows[q], g_sd_max[q] / 1e3, g_sd_arg[q] & 4095ull, g_sd_sum[q] / 1e3 / G, g_sd_exact[q]);
-            g_sd_max[q] = g_sd_sum[q] = g_sd_exact[q] = g_sd_arg[q] = 0;
+            printf("[step %d] rows %lld scan max %.2f us (cta %llu) mean %.2f us, max exact rows/cta %llu, max key compares/cta %llu\n", q,
+                   a.pick_rows[q], g_sd_max[q] / 1e3, g_sd_arg[q] & 4095ull, g_sd_sum[q] / 1e3 / G, g_sd_exact[q], g_sd_key[q]);
+            g_sd_max[q] = g_sd_sum[q] = g_sd_exact[q] = g_sd_arg[q] = g_sd_key[q] = 0;
         }
 #endif
 #ifdef MGB_GREEDY_PRINT_PHASES

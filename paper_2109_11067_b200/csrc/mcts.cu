@@ -190,7 +190,7 @@ __device__ __forceinline__ float ub_row(const float* Wf, uint64_t row) {
 __device__ unsigned g_mcts_fallbacks = 0;  // diagnostics: exact-path top-Ks (MIGPLAN_MCTS_TIMERS)
 // diagnostics (MctsLaunch::timers): top-K phase cycles seen by thread 0 — tables, pass 1 +
 // threshold, pass 2, rank + output — then Σ candidates and calls
-__device__ unsigned long long g_tk[8];  // [6]: pass-2 rescans
+__device__ unsigned long long g_tk[12];  // [6]: pass-2 rescans; [8..10]: pair top-K warps' scan end, max/mean/min
 
 __device__ __forceinline__ float ub_half(const float* Wf, unsigned lo, unsigned hi) {
     float s = __fadd_ru(Wf[lo & 0xFFFFu], Wf[lo >> 16]);
@@ -479,6 +479,9 @@ struct SupTab {
 // block_topk_pair's block-wide counters: zero at kernel start (mcts_kernel) and re-zeroed by
 // every call before its closing barrier, so a call needs no opening barrier for them.
 __shared__ int tp_ncand, tp_nhit, tp_nact, tp_actrows;
+#ifdef MGB_MCTS_SKEW
+__shared__ long long tp_c0, tp_dmax, tp_dmin, tp_dsum;  // development aid: warps' scan-end skew
+#endif
 __device__ __forceinline__ void topk_pair_counters_init() {
     if (threadIdx.x == 0) tp_ncand = tp_nhit = tp_nact = tp_actrows = 0;
 }
@@ -511,6 +514,13 @@ int block_topk_pair(const DevModel& M, const unsigned* keyrank, const unsigned* 
     const int nW = (M.n + 1) * M.PP;
     const unsigned sent = static_cast<unsigned>(M.n * M.PP);
     const uint64_t hiS = static_cast<uint64_t>(sent | (sent << 16)) << 32;
+#ifdef MGB_MCTS_SKEW
+    if (tm && threadIdx.x == 0) {
+        tp_c0 = c0;
+        tp_dmax = tp_dsum = 0;
+        tp_dmin = 1ll << 62;
+    }
+#endif
     // ---- tables (W = need * U, its FP32 round-up, mask hits) and the live supports: one barrier
     for (int e = threadIdx.x; e < nW; e += blockDim.x) {
         const int svc = e / M.PP;
@@ -639,6 +649,14 @@ int block_topk_pair(const DevModel& M, const unsigned* keyrank, const unsigned* 
             if (lane == 0 && hits) atomicAdd(&tp_nhit, hits);
         }
     }
+#ifdef MGB_MCTS_SKEW
+    if (tm && lane == 0) {
+        const long long d = clock64() - tp_c0;
+        atomicMax(reinterpret_cast<unsigned long long*>(&tp_dmax), static_cast<unsigned long long>(d));
+        atomicMin(reinterpret_cast<unsigned long long*>(&tp_dmin), static_cast<unsigned long long>(d));
+        atomicAdd(reinterpret_cast<unsigned long long*>(&tp_dsum), static_cast<unsigned long long>(d));
+    }
+#endif
     mark(7);
     // the listed rows' config-order key ranks, in flight while the threshold is found
     const unsigned kr1 = p1 >= 0 ? __ldg(keyrank + p1) : 0u, kr2 = p2 >= 0 ? __ldg(keyrank + p2) : 0u;
@@ -829,6 +847,12 @@ int block_topk_pair(const DevModel& M, const unsigned* keyrank, const unsigned* 
     if (tm && threadIdx.x == 0) {
         atomicAdd(&g_tk[4], static_cast<unsigned long long>(nc));
         atomicAdd(&g_tk[5], 1ull);
+#ifdef MGB_MCTS_SKEW
+        atomicAdd(&g_tk[8], static_cast<unsigned long long>(tp_dmax));
+        atomicAdd(&g_tk[9], static_cast<unsigned long long>(tp_dsum / nwarps));
+        atomicAdd(&g_tk[10], static_cast<unsigned long long>(tp_dmin));
+#endif
+        atomicAdd(&g_tk[11], static_cast<unsigned long long>(bysup));
     }
     return got;
 }
