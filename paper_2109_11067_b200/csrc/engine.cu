@@ -127,9 +127,12 @@ struct Slot {
     long long index_cap = 0;
     HostIO* io = nullptr;  // host-mapped
 
-    // device MCTS scratch (mcts.cu), grown on demand
+    // device MCTS scratch (mcts.cu), grown on demand, and its pinned host staging (inputs in,
+    // the search's outputs back, all on the launch stream: one synchronisation per launch)
     void* mcts_mem = nullptr;
     size_t mcts_bytes = 0;
+    unsigned char* mcts_host = nullptr;
+    size_t mcts_host_bytes = 0;
     double* logtab = nullptr;
     int logtab_n = 0;
 
@@ -157,6 +160,7 @@ struct Slot {
             if (p) cudaFree(p);
         free_picks();
         if (io) cudaFreeHost(io);
+        if (mcts_host) cudaFreeHost(mcts_host);
         if (e0) cudaEventDestroy(e0);
         if (e1) cudaEventDestroy(e1);
         if (stream) cudaStreamDestroy(stream);
@@ -1392,9 +1396,18 @@ std::vector<MctsDeviceResult> Engine::mcts_device_group(const std::vector<std::v
                 s->logtab_n = static_cast<int>(lt.size());
             }
             unsigned char* b = static_cast<unsigned char*>(s->mcts_mem);
-            CK(cudaMemcpyAsync(b + o.comp0, comps[b0 + q].data(), sizeof(double) * n, cudaMemcpyHostToDevice,
-                               s->stream));
-            CK(cudaMemsetAsync(b + o.tag, 0, sizeof(unsigned) * cap, s->stream));
+            // pinned staging: the completion in, the outputs (trace .. out, carved contiguously) back
+            const size_t hb_bytes = std::max(sizeof(double) * n, o.out + sizeof(int) * 32 - o.trace);
+            if (s->mcts_host_bytes < hb_bytes) {
+                if (s->mcts_host) CK(cudaFreeHost(s->mcts_host));
+                s->mcts_host = nullptr;
+                CK(cudaMallocHost(&s->mcts_host, hb_bytes));
+                s->mcts_host_bytes = hb_bytes;
+            }
+            cudaStream_t ls = slots[0]->stream;  // every search's set-up on the launch stream
+            std::memcpy(s->mcts_host, comps[b0 + q].data(), sizeof(double) * n);
+            CK(cudaMemcpyAsync(b + o.comp0, s->mcts_host, sizeof(double) * n, cudaMemcpyHostToDevice, ls));
+            CK(cudaMemsetAsync(b + o.tag, 0, sizeof(unsigned) * cap, ls));
             MctsSolveArgs& a = L->s[q];
             a.comp0 = reinterpret_cast<const double*>(b + o.comp0);
             a.seed = mix_seed_u64(seeds[b0 + q], 0x6d637473);
@@ -1465,7 +1478,6 @@ std::vector<MctsDeviceResult> Engine::mcts_device_group(const std::vector<std::v
             L->l1_slots = slots >= 32 ? slots : 0;
             msm += L->l1_slots ? static_cast<size_t>(L->l1_slots * per + 48) : 0;
         }
-        for (int q = 1; q < nb; ++q) CK(cudaStreamSynchronize(slots[q]->stream));
         Slot* s0 = slots[0];
         void* args[] = {L.get()};
         CK(cudaEventRecord(s0->e0, s0->stream));
@@ -1486,6 +1498,11 @@ std::vector<MctsDeviceResult> Engine::mcts_device_group(const std::vector<std::v
         }
         stats.launches++;
         CK(cudaEventRecord(s0->e1, s0->stream));
+        for (int q = 0; q < nb; ++q) {  // the outputs are carved contiguously (trace, best, desc, dcomp, out)
+            const Off& o = offs[q];
+            CK(cudaMemcpyAsync(slots[q]->mcts_host, static_cast<unsigned char*>(slots[q]->mcts_mem) + o.trace,
+                               o.out + sizeof(int) * 32 - o.trace, cudaMemcpyDeviceToHost, s0->stream));
+        }
         CK(cudaStreamSynchronize(s0->stream));
         float ms = 0.f;
         CK(cudaEventElapsedTime(&ms, s0->e0, s0->e1));
@@ -1493,11 +1510,9 @@ std::vector<MctsDeviceResult> Engine::mcts_device_group(const std::vector<std::v
         stats.mcts_launches++;
         for (int q = 0; q < nb; ++q) {
             const Off& o = offs[q];
-            unsigned char* b = static_cast<unsigned char*>(slots[q]->mcts_mem);
-            // the outputs are carved contiguously (trace, best, desc, dcomp, out): one copy
-            std::vector<unsigned char> hb(o.out + sizeof(int) * 32 - o.trace);
-            CK(cudaMemcpy(hb.data(), b + o.trace, hb.size(), cudaMemcpyDeviceToHost));
-            auto at = [&](size_t off) { return hb.data() + (off - o.trace); };
+            const unsigned char* hbd = slots[q]->mcts_host;
+            const size_t hb_size = o.out + sizeof(int) * 32 - o.trace;
+            auto at = [&](size_t off) { return hbd + (off - o.trace); };
             int out[32];
             std::memcpy(out, at(o.out), sizeof(out));
             MctsDeviceResult& r = results[b0 + q];
@@ -1511,12 +1526,14 @@ std::vector<MctsDeviceResult> Engine::mcts_device_group(const std::vector<std::v
             if (std::getenv("MIGPLAN_MCTS_TIMERS")) {
                 long long t[5];
                 std::memcpy(t, &out[10], sizeof t);
-                unsigned long long tk[8];
+                unsigned long long tk[12];
                 mcts_read_topk_timers(tk);
                 if (tk[5])
                     std::fprintf(stderr, "[mcts] top-K (cumulative) calls %llu, cycles/call: tables %.0f scan %.0f tree %.0f pass2 %.0f "
-                                 "rank %.0f, candidates/call %.1f\n", tk[5], double(tk[0]) / tk[5], double(tk[7]) / tk[5],
-                                 double(tk[1]) / tk[5], double(tk[2]) / tk[5], double(tk[3]) / tk[5], double(tk[4]) / tk[5]);
+                                 "rank %.0f, candidates/call %.1f; warps' scan end (from call start) max %.0f mean %.0f min %.0f, "
+                                 "by-support %llu\n", tk[5], double(tk[0]) / tk[5], double(tk[7]) / tk[5],
+                                 double(tk[1]) / tk[5], double(tk[2]) / tk[5], double(tk[3]) / tk[5], double(tk[4]) / tk[5],
+                                 double(tk[8]) / tk[5], double(tk[9]) / tk[5], double(tk[10]) / tk[5], tk[11]);
                 std::fprintf(stderr, "[mcts] solve %d: %.1f ms device, cycles sel %lld expand-host %lld miss-host %lld topk %lld "
                              "rollout-ctl %lld, builds %d expands %d iters %d, exact-path top-Ks (cumulative) %d, walk steps %d "
                              "cycles %lld, probes %d cycles %lld, entries %d\n",
@@ -1540,7 +1557,7 @@ std::vector<MctsDeviceResult> Engine::mcts_device_group(const std::vector<std::v
             stats.mcts_topk_calls += r.expands + r.builds;
             stats.mcts_rows += r.expand_rows + static_cast<long long>(r.builds) * pool_size();
             stats.h2d += static_cast<long long>(sizeof(double) * n);
-            stats.d2h += static_cast<long long>(hb.size());
+            stats.d2h += static_cast<long long>(hb_size);
         }
     }
     return results;
@@ -2000,6 +2017,46 @@ void board_close(void* board, bool opened) {
 // completion_of / detail::sum_rates (core.hpp:245-269): counts keyed by (svc, size, batch)
 // in key order, total += count * thr, one division per service.
 std::vector<double> Engine::completion_of(const std::vector<Config>& cfgs) const {
+    // Fast path (every configuration the optimizer itself builds): each instance runs its
+    // service's selected batch for its size, so the reference's per-(service, size, batch)
+    // sums (core.hpp:245-269) are dense counts summed in ascending size order — the same
+    // additions in the same order as the general path below, without its ordered map.
+    {
+        const int S = static_cast<int>(m_.sizes.size());
+        thread_local std::vector<long long> cnt;
+        cnt.assign(static_cast<size_t>(m_.n) * S, 0);
+        int sidx[16];
+        for (int& v : sidx) v = -1;
+        for (int i = 0; i < S; ++i)
+            if (m_.sizes[i] >= 0 && m_.sizes[i] < 16) sidx[m_.sizes[i]] = i;
+        bool fast = true;
+        for (const auto& c : cfgs) {
+            for (int k = 0; k < c.n && fast; ++k) {
+                const auto& in = c.inst[k];
+                const int si = in.slices >= 0 && in.slices < 16 ? sidx[in.slices] : -1;
+                if (in.svc < 0 || in.svc >= m_.n || si < 0 || !m_.feas[in.svc][si].ok || m_.feas[in.svc][si].batch != in.batch) {
+                    fast = false;
+                    break;
+                }
+                ++cnt[static_cast<size_t>(in.svc) * S + si];
+            }
+            if (!fast) break;
+        }
+        if (fast) {
+            std::vector<double> out(m_.n);
+            for (int i = 0; i < m_.n; ++i) {
+                double total = 0.0;
+                for (int si = 0; si < S; ++si) {
+                    const long long c = cnt[static_cast<size_t>(i) * S + si];
+                    if (c == 0) continue;
+                    volatile double prod = static_cast<double>(c) * m_.feas[i][si].thr;
+                    total = total + prod;
+                }
+                out[i] = total / m_.services[i].req;
+            }
+            return out;
+        }
+    }
     std::map<std::tuple<int, int, int>, long long> counts;
     for (const auto& c : cfgs)
         for (int k = 0; k < c.n; ++k) {

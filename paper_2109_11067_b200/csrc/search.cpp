@@ -195,12 +195,17 @@ Chromosome mutate(const Chromosome& parent, const GaParams& p, Rng& rng) {
     struct Ref {
         size_t gpu, inst;
     };
-    std::map<int, std::vector<Ref>> by_size;
+    // instances by size, sizes ascending (the reference's std::map order); sizes are small
+    // slice counts, so a flat table replaces the map
+    int max_size = 0;
+    for (const auto& g : child.gpus)
+        for (int k = 0; k < g.n; ++k) max_size = std::max(max_size, g.inst[k].slices);
+    std::vector<std::vector<Ref>> by_size(static_cast<size_t>(max_size) + 1);
     for (size_t g = 0; g < child.gpus.size(); ++g)
         for (int k = 0; k < child.gpus[g].n; ++k) by_size[child.gpus[g].inst[k].slices].push_back(Ref{g, size_t(k)});
     std::vector<int> sizes;
-    for (const auto& [size, refs] : by_size)
-        if (refs.size() >= 2) sizes.push_back(size);
+    for (int size = 0; size <= max_size; ++size)
+        if (by_size[size].size() >= 2) sizes.push_back(size);
     if (sizes.empty()) return child;
     for (int pair = 0; pair < p.mutation_pairs; ++pair) {
         for (int attempt = 0; attempt < 64; ++attempt) {
