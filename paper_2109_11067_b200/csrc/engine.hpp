@@ -177,7 +177,7 @@ class Engine {
     void greedy_batch(const double* d_comps, int count, long long cap_steps, long long rows_bound,
                       std::vector<const uint64_t*>& rows,
                       std::vector<int>& n_steps, std::vector<std::vector<uint64_t>>* host_rows = nullptr,
-                      SlotLease* lease = nullptr);
+                      SlotLease* lease = nullptr, const double* h_comps = nullptr);
     void fast_algo_batch(const std::vector<std::vector<double>>& comps, std::vector<std::vector<uint64_t>>& rows,
                          std::vector<int>& status);
     std::vector<MctsDeviceResult> mcts_device_group(const std::vector<std::vector<double>>& comps, int budget, int topk,

@@ -29,7 +29,9 @@ def main():
         st = ctx.stats()
         print(f"{os.path.basename(lib or 'product')} rep {rep}: {rounds} rounds {len(dep.gpus)} GPUs in {1e3 * dt:.2f} ms, "
               f"greedy {st['greedy_ms']:.2f} ms / {st['greedy_calls']} calls, mcts {st['mcts_ms']:.2f} ms / "
-              f"{st['mcts_launches']} launches, launches {st['kernel_launches']}", flush=True)
+              f"{st['mcts_launches']} launches, launches {st['kernel_launches']}, greedy phases [scan bar red decide ext] "
+              f"{' '.join(f'{x:.2f}' for x in st['phase_ms'])} ms, steps {st['greedy_steps']}, events {st['ext_events']}, "
+              f"ext rows {st['ext_rows']}", flush=True)
 
 
 if __name__ == "__main__":
