@@ -269,7 +269,8 @@ struct BfEnumArgs {
 struct RolloutCounters {
     unsigned long long n_act[2];  // active-list lengths (ping-pong by round parity)
     unsigned long long n_pend[2]; // key-cache slots created per round (ping-pong)
-    unsigned int bar_count, bar_gen;
+    int done;                     // a round found no active rollout (its build kernel sets it)
+    int pad;
     int status;                   // 0 ok, 1 key cache full
     int rounds;
     unsigned long long best;      // min over completed rollouts of (steps << 32 | batch index)
@@ -309,6 +310,7 @@ struct RolloutArgs {
     int n_sup;
     const int* sup_begin;
     const unsigned short* sup_svc;
+    int timers;             // diagnostics: CTA 0 prints its phase split (MIGPLAN_ROLLOUT_TIMERS)
     double comp0[256];      // start completion (travels with the launch)
 };
 

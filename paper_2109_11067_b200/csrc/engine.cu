@@ -47,8 +47,11 @@ size_t keyrank_scratch_bytes(long long P);
 cudaError_t build_keyrank(const DevModel& M, const uint64_t* rows, long long P, unsigned* rank, void* scratch,
                           size_t scratch_bytes, cudaStream_t stream, int* launches);
 int mcts_threads();
-const void* rollout_kernel_ptr(int n);
+const void* rollout_build_ptr();
+const void* rollout_advance_ptr(int n);
+const void* rollout_replay_ptr(int n);
 int rollout_threads();
+int rollout_advance_threads();
 
 namespace {
 
@@ -214,9 +217,11 @@ Engine::Engine(const Rules& rules, std::map<std::string, ModelProfile> profiles,
     const size_t gsm = greedy_smem_bytes(m_.n, m_.PP, cache_units_, ring_stages_), tsm = topk_smem_bytes(m_.n, m_.PP);
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&greedy_blocks_per_sm_, greedy_kernel_ptr(), T, gsm));
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&topk_blocks_per_sm_, topk_kernel_ptr(), T, tsm));
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&rollout_blocks_per_sm_, rollout_kernel_ptr(m_.n), rollout_threads(),
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&rollout_blocks_per_sm_, rollout_build_ptr(), rollout_threads(),
                                                      rollout_smem_bytes(m_.n, m_.PP, max_sup())));
-    if (greedy_blocks_per_sm_ < 1 || topk_blocks_per_sm_ < 1 || rollout_blocks_per_sm_ < 1)
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&rollout_adv_blocks_per_sm_, rollout_advance_ptr(m_.n),
+                                                     rollout_advance_threads(), 0));
+    if (greedy_blocks_per_sm_ < 1 || topk_blocks_per_sm_ < 1 || rollout_blocks_per_sm_ < 1 || rollout_adv_blocks_per_sm_ < 1)
         throw DeviceError("kernel does not fit on an SM");
 
     // ---- K1 input: every support with 1..max_mix members and its row offset (pool order)
@@ -480,7 +485,7 @@ const DeviceInfo& device_info(int device) {
     CK(cudaFuncSetAttribute(mcts_kernel_ptr(1), cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     CK(cudaFuncSetAttribute(mcts_kernel_ptr(255), cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     CK(cudaFuncSetAttribute(greedy_kernel_ptr(), cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-    for (const void* k : {greedy_kernel_ptr(), topk_kernel_ptr(), topk1_kernel_ptr(32), rollout_kernel_ptr(1), rollout_kernel_ptr(256),
+    for (const void* k : {greedy_kernel_ptr(), topk_kernel_ptr(), topk1_kernel_ptr(32), rollout_build_ptr(),
                           mcts_kernel_ptr(1), mcts_kernel_ptr(255)}) {
         cudaFuncAttributes fa{};
         CK(cudaFuncGetAttributes(&fa, k));
@@ -1103,6 +1108,7 @@ RolloutResult Engine::rollouts(const std::vector<double>& comp, long long n_roll
     a.seed = seed;
     a.k = k;
     a.max_depth = max_depth;
+    a.timers = std::getenv("MIGPLAN_ROLLOUT_TIMERS") ? 1 : 0;
     a.comp = static_cast<double*>(alloc(sizeof(double) * n * batch));
     a.len = static_cast<int*>(alloc(sizeof(int) * batch));
     a.status = static_cast<uint8_t*>(alloc(batch));
@@ -1162,13 +1168,41 @@ RolloutResult Engine::rollouts(const std::vector<double>& comp, long long n_roll
             a.id0 = id_offset + done;
             CK(cudaMemsetAsync(a.cnt, 0, sizeof(RolloutCounters), st));
             CK(cudaMemsetAsync(&a.cnt->best, 0xFF, sizeof(unsigned long long), st));
-            void* args[] = {&a};
+            // the start, then per round a pool-build launch and an advance launch, enqueued in
+            // growing chunks; a round with no active rollout makes every later launch a no-op
+            const int GA = num_sms_ * rollout_adv_blocks_per_sm_;
+            const void* kb = rollout_build_ptr();
+            const void* ka = rollout_advance_ptr(m_.n);
+            auto adv = [&](int round) {
+                void* args[] = {&a, &round};
+                CK(cudaLaunchKernel(ka, GA, rollout_advance_threads(), args, 0, st));
+            };
+            auto bld = [&](int round) {
+                void* args[] = {&a, &round};
+                CK(cudaLaunchKernel(kb, G, rollout_threads(), args, smem, st));
+            };
             CK(cudaEventRecord(e0, st));
-            CK(cudaLaunchCooperativeKernel(rollout_kernel_ptr(m_.n), G, rollout_threads(), args, smem, st));
-            CK(cudaEventRecord(e1, st));
-            stats.launches++;
-            r.launches++;
+            adv(-1);
+            int launches = 1;
             RolloutCounters c{};
+            for (int round = 0, chunk = 8;; chunk = std::min(2 * chunk, 128)) {
+                for (int q = 0; q < chunk && round <= max_depth + 1; ++q, ++round) {
+                    bld(round);
+                    adv(round);
+                    launches += 2;
+                }
+                CK(cudaMemcpyAsync(&c, a.cnt, sizeof c, cudaMemcpyDeviceToHost, st));
+                CK(cudaStreamSynchronize(st));
+                if (c.done || c.status != 0 || round > max_depth + 1) break;
+            }
+            {
+                void* args[] = {&a};
+                CK(cudaLaunchKernel(rollout_replay_ptr(m_.n), 1, 32, args, 0, st));
+                ++launches;
+            }
+            CK(cudaEventRecord(e1, st));
+            stats.launches += launches;
+            r.launches += launches;
             CK(cudaMemcpyAsync(&c, a.cnt, sizeof c, cudaMemcpyDeviceToHost, st));
             if (lengths)
                 CK(cudaMemcpyAsync(lengths + done, d_len, sizeof(int) * a.n_roll, cudaMemcpyDeviceToHost, st));
@@ -1280,6 +1314,7 @@ void Engine::greedy_batch(const double* d_comps, int count, long long cap_steps,
             stats.greedy_steps += h.n_steps;
             stats.ext_events += h.n_events;
             stats.ext_rows += static_cast<long long>(h.ext_count);
+            for (int k = 0; k < 5; ++k) stats.phase_ns[k] += static_cast<long long>(h.phase_ns[k]);
             if (h.status == kOk) {
                 n_steps[b0 + i] = h.n_steps;
                 rows[b0 + i] = calls[i].s->d_pick_row;

@@ -222,7 +222,8 @@ class Engine {
     int num_sms_ = 0;
     int greedy_blocks_per_sm_ = 0;
     int topk_blocks_per_sm_ = 0;
-    int rollout_blocks_per_sm_ = 0;
+    int rollout_blocks_per_sm_ = 0;      // pool-build kernel
+    int rollout_adv_blocks_per_sm_ = 0;  // advance kernel
     DevModel dm_{};
     std::vector<void*> dev_allocs_;
     uint64_t* d_base_ = nullptr;

@@ -16,8 +16,10 @@
 //     CTA after a grid barrier (the same threshold + parallel-rank top-K as topk.cu);
 //   - the shortest completed rollout (ties: lowest index) is replayed at the end from the
 //     (immutable) cache to emit its path.
-// Per round: [pick + add + satisfied check + key probe, warp per rollout] -> grid barrier ->
-// [build the round's new pools, CTA per key] -> grid barrier.
+// Per round, two launches: [build the round's new pools, CTA per key] then [pick + add +
+// satisfied check + key probe, warp per rollout].  The advance kernel is separate so its small
+// register footprint gives full occupancy (a step is a chain of dependent L2 round trips: more
+// warps in flight is what raises its rate); kernel boundaries replace the grid barriers.
 // oracle/oracle.cpp (`rollouts_restated`) restates exactly this schedule on the CPU.
 #include <cuda/atomic>
 
@@ -35,6 +37,11 @@ constexpr int kRWarps = kRThreads / 32;
 constexpr int kRCandCap = 2048;
 constexpr int kRMaxK = 32;
 constexpr int kMaxJ = 8;  // comp registers per lane: n <= 256 (J = 2 instantiation for n <= 64)
+constexpr int kAThreads = 256;  // advance kernel: small blocks, register-lean, many warps per SM
+#ifndef MGB_ROLLOUT_AOCC
+#define MGB_ROLLOUT_AOCC 6
+#endif
+constexpr int kAOcc = MGB_ROLLOUT_AOCC;
 
 __device__ __forceinline__ uint64_t mix64(uint64_t z) {
     z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
@@ -243,31 +250,28 @@ __device__ int block_topk(const RolloutArgs& a, const double* comp, double* W, C
 
 }  // namespace
 
+// One warp-step of rollout r (see the file comment).  first: the start state (no pick).
+// Pushes r to the next round's active list through the warp's buffer `wb` (32 entries).
 template <int J>
-__global__ void __launch_bounds__(kRThreads, 2) rollout_kernel(const __grid_constant__ RolloutArgs a) {
-    extern __shared__ __align__(16) unsigned char smem[];
-    const DevModel& M = a.M;
-    const int n = M.n;
-    const int nk = (n + 63) / 64;
-    double* W = reinterpret_cast<double*>(smem);
-    double* comp_s = W + (n + 1) * M.PP;
-    Cand* cand = reinterpret_cast<Cand*>(comp_s + n + 1);
-    Cand* win = cand + kRCandCap;
-    int* sact = reinterpret_cast<int*>(win + kRMaxK);  // active supports of a pool build (a.n_sup)
-    __shared__ long long wbuf[kRWarps][32];  // per-warp survivor buffer (one atomic per 32 pushes)
-    __shared__ unsigned long long c_steps, c_done, c_cap, c_fail;
-    const int lane = static_cast<int>(threadIdx.x & 31u);
-    const int warp = static_cast<int>(threadIdx.x >> 5);
-    const long long gw = static_cast<long long>(blockIdx.x) * kRWarps + warp;
-    const long long nwarps = static_cast<long long>(gridDim.x) * kRWarps;
-    RolloutCounters* C = a.cnt;
-    unsigned* bc = &C->bar_count;
-    unsigned* bg = &C->bar_gen;
-    if (threadIdx.x == 0) c_steps = c_done = c_cap = c_fail = 0;
-    __syncthreads();
+struct Advancer {
+    const RolloutArgs& a;
+    long long* wb;
+    unsigned long long *c_steps, *c_done, *c_cap, *c_fail;
+    int lane, nk, nxt, nbuf = 0;
 
-    // One warp-step of rollout r (see the file comment).  first: the start state (no pick).
-    auto advance = [&](long long r, bool first, int nxt, int& nbuf) {
+    __device__ void push_flush() {
+        if (nbuf && lane == 0) {
+            const unsigned long long at = atomicAdd(&a.cnt->n_act[nxt], static_cast<unsigned long long>(nbuf));
+            for (int i = 0; i < nbuf; ++i) (nxt ? a.act1 : a.act0)[at + i] = wb[i];
+        }
+        __syncwarp();
+        nbuf = 0;
+    }
+
+    __device__ void step(long long r, bool first) {
+        const DevModel& M = a.M;
+        const int n = M.n;
+        RolloutCounters* C = a.cnt;
         double c[J];
         const double* src = first ? a.comp0 : a.comp + r * n;
 #pragma unroll
@@ -282,7 +286,7 @@ __global__ void __launch_bounds__(kRThreads, 2) rollout_kernel(const __grid_cons
                 if (lane == 0) {
                     a.status[r] = 3;
                     if (a.lengths) a.lengths[r] = -1;
-                    atomicAdd(&c_fail, 1ull);
+                    atomicAdd(c_fail, 1ull);
                 }
                 return;
             }
@@ -292,7 +296,7 @@ __global__ void __launch_bounds__(kRThreads, 2) rollout_kernel(const __grid_cons
             ++L;
             if (lane == 0) {
                 a.len[r] = L;
-                atomicAdd(&c_steps, 1ull);
+                atomicAdd(c_steps, 1ull);
             }
         }
         uint64_t kw[4];
@@ -301,7 +305,7 @@ __global__ void __launch_bounds__(kRThreads, 2) rollout_kernel(const __grid_cons
                 a.status[r] = 1;
                 if (a.lengths) a.lengths[r] = L;
                 atomicMin(&C->best, (static_cast<unsigned long long>(L) << 32) | static_cast<unsigned long long>(r));
-                atomicAdd(&c_done, 1ull);
+                atomicAdd(c_done, 1ull);
             }
             return;
         }
@@ -309,17 +313,16 @@ __global__ void __launch_bounds__(kRThreads, 2) rollout_kernel(const __grid_cons
             if (lane == 0) {
                 a.status[r] = 2;
                 if (a.lengths) a.lengths[r] = a.max_depth;
-                atomicAdd(&c_cap, 1ull);
+                atomicAdd(c_cap, 1ull);
             }
             return;
         }
 #pragma unroll
         for (int j = 0; j < J; ++j)
             if (lane + 32 * j < n && ((dirty >> j) & 1u)) a.comp[r * n + lane + 32 * j] = c[j];
-        long long slot = 0;
         if (lane == 0) {
             bool created = false;
-            slot = probe(a, kw, nk, true, created);
+            long long slot = probe(a, kw, nk, true, created);
             if (slot < 0) {
                 atomicExch(&C->status, 1);
                 slot = 0;
@@ -332,108 +335,132 @@ __global__ void __launch_bounds__(kRThreads, 2) rollout_kernel(const __grid_cons
                     atomicMin(&a.claimer[slot], static_cast<unsigned long long>(r));
             }
             a.rslot[r] = static_cast<unsigned>(slot);
-            wbuf[warp][nbuf] = r;
+            wb[nbuf] = r;
         }
-        if (++nbuf == 32) {
-            if (lane == 0) {
-                const unsigned long long at = atomicAdd(&C->n_act[nxt], 32ull);
-                for (int i = 0; i < 32; ++i) (nxt ? a.act1 : a.act0)[at + i] = wbuf[warp][i];
-            }
-            __syncwarp();
-            nbuf = 0;
-        }
-    };
-    auto flush = [&](int nxt, int nbuf) {
-        if (nbuf && lane == 0) {
-            const unsigned long long at = atomicAdd(&C->n_act[nxt], static_cast<unsigned long long>(nbuf));
-            for (int i = 0; i < nbuf; ++i) (nxt ? a.act1 : a.act0)[at + i] = wbuf[warp][i];
-        }
-        __syncwarp();
-    };
+        if (++nbuf == 32) push_flush();
+    }
+};
 
-    // round 0: every rollout starts at the root
-    {
-        int nbuf = 0;
-        for (long long r = gw; r < a.n_roll; r += nwarps) advance(r, true, 0, nbuf);
-        flush(0, nbuf);
+// Round `round` (or the start, round < 0): every active rollout advances one step, a warp per
+// rollout.  Counters are summed per block, then once into the launch's RolloutCounters.
+template <int J>
+__global__ void __launch_bounds__(kAThreads, kAOcc) rollout_advance_kernel(const __grid_constant__ RolloutArgs a, int round) {
+    __shared__ long long wbuf[kAThreads / 32][32];
+    __shared__ unsigned long long c_steps, c_done, c_cap, c_fail;
+    RolloutCounters* C = a.cnt;
+    const bool first = round < 0;
+    const int cur = first ? 1 : (round & 1);
+    unsigned long long n_act = static_cast<unsigned long long>(a.n_roll);
+    if (!first) {  // rounds enqueued past the last one (C->done) are no-ops
+        n_act = __ldcg(&C->n_act[cur]);
+        if (n_act == 0 || __ldcg(&C->status) != 0 || *reinterpret_cast<volatile int*>(&C->done)) return;
     }
-    grid_barrier(bc, bg, gridDim.x);
-    int round = 0;
-    for (;; ++round) {
-        const int cur = round & 1, nxt = cur ^ 1;
-        const unsigned long long n_act = __ldcg(&C->n_act[cur]);
-        const unsigned long long n_pend = __ldcg(&C->n_pend[cur]);
-        if (n_act == 0 || __ldcg(&C->status) != 0) break;
-        if (blockIdx.x == 0 && threadIdx.x == 0) {  // last read in round - 1, next written after the barrier below
-            C->n_act[nxt] = 0;
-            C->n_pend[nxt] = 0;
-            C->keys += n_pend;
-        }
-        // build the pools of the keys first reached in this round (CTA per key)
-        for (unsigned long long p = blockIdx.x; p < n_pend; p += gridDim.x) {
-            const unsigned slot = __ldcg(&(cur ? a.pend1 : a.pend0)[p]);
-            const long long r = static_cast<long long>(__ldcg(&a.claimer[slot]));
-            for (int i = threadIdx.x; i < n; i += blockDim.x) comp_s[i] = __ldcg(&a.comp[r * n + i]);
-            __syncthreads();
-            const int got = block_topk(a, comp_s, W, cand, win, a.pool + static_cast<size_t>(slot) * a.k, sact);
-            if (threadIdx.x == 0) a.pool_n[slot] = got;
-            __syncthreads();
-        }
-        grid_barrier(bc, bg, gridDim.x);
-        int nbuf = 0;
-        const long long* act = cur ? a.act1 : a.act0;
-        for (long long i = gw; i < static_cast<long long>(n_act); i += nwarps) advance(__ldcg(&act[i]), false, nxt, nbuf);
-        flush(nxt, nbuf);
-        grid_barrier(bc, bg, gridDim.x);
-    }
+    if (threadIdx.x == 0) c_steps = c_done = c_cap = c_fail = 0;
+    __syncthreads();
+    const int warp = static_cast<int>(threadIdx.x >> 5);
+    Advancer<J> adv{a, wbuf[warp], &c_steps, &c_done, &c_cap, &c_fail, static_cast<int>(threadIdx.x & 31u),
+                    (a.M.n + 63) / 64, cur ^ 1};
+    const long long gw = static_cast<long long>(blockIdx.x) * (kAThreads / 32) + warp;
+    const long long nwarps = static_cast<long long>(gridDim.x) * (kAThreads / 32);
+    const long long* act = cur ? a.act1 : a.act0;
+    for (long long i = gw; i < static_cast<long long>(n_act); i += nwarps) adv.step(first ? i : __ldcg(&act[i]), first);
+    adv.push_flush();
+    __syncthreads();
     if (threadIdx.x == 0) {
-        atomicAdd(&C->steps, c_steps);
-        atomicAdd(&C->completed, c_done);
-        atomicAdd(&C->capped, c_cap);
-        atomicAdd(&C->failed, c_fail);
+        if (c_steps) atomicAdd(&C->steps, c_steps);
+        if (c_done) atomicAdd(&C->completed, c_done);
+        if (c_cap) atomicAdd(&C->capped, c_cap);
+        if (c_fail) atomicAdd(&C->failed, c_fail);
     }
-    // replay the winner from the immutable cache: its path, pick by pick
-    if (blockIdx.x == 0 && warp == 0) {
-        const unsigned long long best = __ldcg(&C->best);
-        int plen = 0;
-        if (best != ~0ull && __ldcg(&C->status) == 0) {
-            const long long r = static_cast<long long>(best & 0xFFFFFFFFull);
-            const int L = static_cast<int>(best >> 32);
-            double c[J];
+}
+
+// Round `round`: the pools of the keys first reached in the previous step (CTA per key).
+// Block 0 also opens the round: the next round's lists start empty.
+__global__ void __launch_bounds__(kRThreads, 2) rollout_build_kernel(const __grid_constant__ RolloutArgs a, int round) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const DevModel& M = a.M;
+    const int n = M.n;
+    double* W = reinterpret_cast<double*>(smem);
+    double* comp_s = W + (n + 1) * M.PP;
+    Cand* cand = reinterpret_cast<Cand*>(comp_s + n + 1);
+    Cand* win = cand + kRCandCap;
+    int* sact = reinterpret_cast<int*>(win + kRMaxK);  // active supports of a pool build (a.n_sup)
+    RolloutCounters* C = a.cnt;
+    const int cur = round & 1, nxt = cur ^ 1;
+    if (*reinterpret_cast<volatile int*>(&C->done)) return;  // enqueued past the last round
+    const unsigned long long n_act = __ldcg(&C->n_act[cur]);
+    const unsigned long long n_pend = __ldcg(&C->n_pend[cur]);
+    if (n_act == 0 || __ldcg(&C->status) != 0) {
+        if (blockIdx.x == 0 && threadIdx.x == 0) C->done = 1;
+        return;
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) {  // last read by the previous round's kernels
+        C->n_act[nxt] = 0;
+        C->n_pend[nxt] = 0;
+        C->keys += n_pend;
+        C->rounds = round + 1;
+    }
+    for (unsigned long long p = blockIdx.x; p < n_pend; p += gridDim.x) {
+        const unsigned slot = __ldcg(&(cur ? a.pend1 : a.pend0)[p]);
+        const long long r = static_cast<long long>(__ldcg(&a.claimer[slot]));
+        for (int i = threadIdx.x; i < n; i += blockDim.x) comp_s[i] = __ldcg(&a.comp[r * n + i]);
+        __syncthreads();
+        const int got = block_topk(a, comp_s, W, cand, win, a.pool + static_cast<size_t>(slot) * a.k, sact);
+        if (threadIdx.x == 0) a.pool_n[slot] = got;
+        __syncthreads();
+    }
+}
+
+// The shortest completed rollout (ties: lowest index), replayed from the immutable cache.
+template <int J>
+__global__ void rollout_replay_kernel(const __grid_constant__ RolloutArgs a) {
+    const DevModel& M = a.M;
+    const int n = M.n, nk = (n + 63) / 64;
+    const int lane = static_cast<int>(threadIdx.x & 31u);
+    RolloutCounters* C = a.cnt;
+    const unsigned long long best = __ldcg(&C->best);
+    int plen = 0;
+    if (best != ~0ull && __ldcg(&C->status) == 0) {
+        const long long r = static_cast<long long>(best & 0xFFFFFFFFull);
+        const int L = static_cast<int>(best >> 32);
+        double c[J];
 #pragma unroll
-            for (int j = 0; j < J; ++j) c[j] = (lane + 32 * j < n) ? a.comp0[lane + 32 * j] : 2.0;
-            for (int t = 0; t < L; ++t) {
-                uint64_t kw[4];
-                type_key(c, n, kw);
-                long long slot = 0;
-                if (lane == 0) {
-                    bool created;
-                    slot = probe(a, kw, nk, false, created);
-                }
-                slot = __shfl_sync(0xffffffffu, slot, 0);
-                const int pn = __ldcg(&a.pool_n[slot]);
-                const uint64_t x = philox_u64(a.seed, static_cast<uint64_t>(a.id0 + r), static_cast<uint64_t>(t));
-                const unsigned pick = __ldcg(&a.pool[static_cast<size_t>(slot) * a.k + philox_below(x, pn)]);
-                if (lane == 0) a.path[t] = pick;
-                add_row(M, __ldg(a.base + pick), c);
+        for (int j = 0; j < J; ++j) c[j] = (lane + 32 * j < n) ? a.comp0[lane + 32 * j] : 2.0;
+        for (int t = 0; t < L; ++t) {
+            uint64_t kw[4];
+            type_key(c, n, kw);
+            long long slot = 0;
+            if (lane == 0) {
+                bool created;
+                slot = probe(a, kw, nk, false, created);
             }
-            plen = L;
+            slot = __shfl_sync(0xffffffffu, slot, 0);
+            const int pn = __ldcg(&a.pool_n[slot]);
+            const uint64_t x = philox_u64(a.seed, static_cast<uint64_t>(a.id0 + r), static_cast<uint64_t>(t));
+            const unsigned pick = __ldcg(&a.pool[static_cast<size_t>(slot) * a.k + philox_below(x, pn)]);
+            if (lane == 0) a.path[t] = pick;
+            add_row(M, __ldg(a.base + pick), c);
         }
-        if (lane == 0) {
-            *a.path_len = plen;
-            C->rounds = round;
-        }
+        plen = L;
     }
+    if (lane == 0) *a.path_len = plen;
 }
 
 size_t rollout_smem_bytes(int n, int PP, int n_sup) {
     return static_cast<size_t>((n + 1) * PP + n + 1) * 8 + static_cast<size_t>(kRCandCap + kRMaxK) * sizeof(Cand) +
            sizeof(int) * static_cast<size_t>(n_sup);
 }
-const void* rollout_kernel_ptr(int n) {
-    return n <= 64 ? reinterpret_cast<const void*>(&rollout_kernel<2>) : reinterpret_cast<const void*>(&rollout_kernel<kMaxJ>);
+const void* rollout_build_ptr() { return reinterpret_cast<const void*>(&rollout_build_kernel); }
+const void* rollout_advance_ptr(int n) {
+    return n <= 64 ? reinterpret_cast<const void*>(&rollout_advance_kernel<2>)
+                   : reinterpret_cast<const void*>(&rollout_advance_kernel<kMaxJ>);
+}
+const void* rollout_replay_ptr(int n) {
+    return n <= 64 ? reinterpret_cast<const void*>(&rollout_replay_kernel<2>)
+                   : reinterpret_cast<const void*>(&rollout_replay_kernel<kMaxJ>);
 }
 int rollout_threads() { return kRThreads; }
+int rollout_advance_threads() { return kAThreads; }
 
 namespace {
 __global__ void philox_kat_kernel(uint64_t seed, uint64_t stream, uint64_t step, unsigned long long* out) {
