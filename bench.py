@@ -390,6 +390,8 @@ def secondary_ga(mp, local, flush, torch, steps, workers):
 def extra_measurements(mp, local):
     """Device-timed evidence for the other BASELINE configs: config #4 (1e6 root-parallel
     rollouts; parity-mode MCTS with 2,000 iterations, ms/iteration) and the device GA."""
+    import torch
+
     import support as S
 
     out = {}
@@ -428,11 +430,19 @@ def extra_measurements(mp, local):
         res3 = {"workload": "gen24_8.7 (BASELINE config #3): two_phase_parallel_mcts — device population, Philox "
                             "seed 4242, refill = shorter of greedy and best of 1024 root-parallel rollouts",
                 "greedy_gpus": len(mp.fast_algo(mp.zero_completion(len(sv)), ctx))}
+        warm = mp.GaParams(seed=4242, max_rounds=2, time_budget_s=1e9, stall_rounds=1 << 30)
+        mp.two_phase_parallel(sv, ps, mp.PartitionRuleSet.defaults(), warm, ctx=ctx, slow=slow)  # first-use set-up
         for rounds in (2, 10, 50):
             prm = mp.GaParams(seed=4242, max_rounds=rounds, time_budget_s=1e9, stall_rounds=1 << 30)
+            ctx.reset_stats()
+            torch.cuda.synchronize()
             t0 = time.perf_counter()
             dep = mp.two_phase_parallel(sv, ps, mp.PartitionRuleSet.defaults(), prm, ctx=ctx, slow=slow)
-            res3[f"rounds_{rounds}"] = {"gpus_in_plan": len(dep.gpus), "wall_ms": 1e3 * (time.perf_counter() - t0)}
+            st3 = ctx.stats()
+            res3[f"rounds_{rounds}"] = {"gpus_in_plan": len(dep.gpus), "wall_ms": 1e3 * (time.perf_counter() - t0),
+                                        "device_ms": {"greedy": st3["greedy_ms"], "rollouts": st3["rollout_ms"]},
+                                        "rollout_calls": st3["rollout_calls"], "rollout_steps": st3["rollout_steps"],
+                                        "launches": st3["kernel_launches"]}
         t0 = time.perf_counter()  # the parity-mode two_phase (reference RNG) of the same config, 2 rounds
         dep = mp.two_phase(sv, ps, mp.PartitionRuleSet.defaults(), ga_params("gen24_8.7_ga2", 8), ctx=ctx)
         res3["parity_two_phase_2_rounds"] = {"gpus_in_plan": len(dep.gpus), "wall_ms": 1e3 * (time.perf_counter() - t0),

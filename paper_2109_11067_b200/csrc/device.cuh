@@ -11,6 +11,7 @@ constexpr uint64_t kNoRow = ~0ull;
 struct DevModel {
     int n;         // services
     int PP;        // patterns; row code = svc * PP + pattern, sentinel n * PP
+    unsigned pp_magic;  // ceil(2^32 / PP): svc_of(code) = umulhi(code, pp_magic), exact for code < 2^16
     int n_sizes;
     int n_layouts;
     int max_mix;
@@ -32,6 +33,12 @@ struct DevModel {
     const uint32_t* pat_packed;   // PP
     const uint8_t* layout_of;     // 1 << 15
 };
+
+// code / PP by a multiply: for code < 2^16 and PP < 2^16 the error of ceil(2^32 / PP) stays
+// below 1/PP, so the quotient is exact (the scan loops called the integer-division routine).
+__device__ __forceinline__ int svc_of(const DevModel& M, unsigned code) {
+    return M.pp_magic ? static_cast<int>(__umulhi(code, M.pp_magic)) : static_cast<int>(code);  // 0: PP == 1
+}
 
 // One argmax candidate: score, util_sum, packed row.
 struct Best {

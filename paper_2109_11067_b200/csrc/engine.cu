@@ -263,6 +263,9 @@ Engine::Engine(const Rules& rules, std::map<std::string, ModelProfile> profiles,
     };
     dm_.n = m_.n;
     dm_.PP = m_.PP;
+    dm_.pp_magic = m_.PP > 1 ? static_cast<unsigned>(((1ull << 32) + static_cast<unsigned long long>(m_.PP) - 1) /
+                                                     static_cast<unsigned long long>(m_.PP))
+                             : 0u;
     dm_.n_sizes = static_cast<int>(m_.sizes.size());
     dm_.n_layouts = static_cast<int>(m_.layouts.size());
     dm_.max_mix = m_.max_mix;

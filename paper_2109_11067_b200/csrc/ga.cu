@@ -45,7 +45,7 @@ __device__ uint64_t row_genome(const DevModel& M, uint64_t row) {
     for (int j = 0; j < 4; ++j) {
         const int code = static_cast<int>((row >> (16 * j)) & 0xFFFFull);
         if (code == sentinel) break;
-        svc[k] = code / M.PP;
+        svc[k] = svc_of(M, static_cast<unsigned>(code));
         pat[k] = code % M.PP;
         ++k;
     }

@@ -296,7 +296,7 @@ __device__ __noinline__ int block_topk_bound(const DevModel& M, const unsigned* 
     mark(-1);
     const int nW = (M.n + 1) * M.PP;
     for (int e = threadIdx.x; e < nW; e += blockDim.x) {
-        const int svc = e / M.PP;
+        const int svc = svc_of(M, static_cast<unsigned>(e));
         double w = 0.0;
         if (svc < M.n) {
             const double need = __dadd_rn(1.0, -comp[svc]);
@@ -523,7 +523,7 @@ int block_topk_pair(const DevModel& M, const unsigned* keyrank, const unsigned* 
 #endif
     // ---- tables (W = need * U, its FP32 round-up, mask hits) and the live supports: one barrier
     for (int e = threadIdx.x; e < nW; e += blockDim.x) {
-        const int svc = e / M.PP;
+        const int svc = svc_of(M, static_cast<unsigned>(e));
         double w = 0.0;
         if (svc < M.n) {
             const double need = __dadd_rn(1.0, -comp[svc]);
@@ -866,7 +866,7 @@ __device__ __forceinline__ bool comp_satisfied(const double* c, int n) {  // cor
 __device__ __forceinline__ void add_row_util(const DevModel& M, const double* U, uint64_t row, double* c) {
     for (int j = 0; j < 4; ++j) {  // rollout / expand add (mcts.hpp:112,139)
         const int code = static_cast<int>((row >> (16 * j)) & 0xFFFFull);
-        const int svc = code / M.PP;
+        const int svc = svc_of(M, static_cast<unsigned>(code));
         if (svc < M.n) c[svc] = __dadd_rn(c[svc], U[code]);
     }
 }
@@ -948,7 +948,7 @@ __global__ void __launch_bounds__(kMThreads, 1) mcts_kernel(const __grid_constan
     const SupTab sup{nsup, sbeg, ssvc, sact};
     for (int e = threadIdx.x; e < nW; e += blockDim.x) {
         Us[e] = __ldg(&M.U[e]);
-        csvc[e] = static_cast<unsigned char>(e / M.PP);  // service of a code (n for the sentinel row)
+        csvc[e] = static_cast<unsigned char>(svc_of(M, static_cast<unsigned>(e)));  // service of a code (n for the sentinel row)
     }
     __shared__ int s_exit, s_usemask, n_got, s_hits;
     __shared__ uint64_t s_mask[4];

@@ -108,7 +108,7 @@ __device__ __forceinline__ unsigned add_row(const DevModel& M, uint64_t row, dou
 #pragma unroll
     for (int m = 0; m < 4; ++m) {
         const int code = static_cast<int>((row >> (16 * m)) & 0xFFFFull);
-        const int svc = code / M.PP;
+        const int svc = svc_of(M, static_cast<unsigned>(code));
         if (svc < M.n && (svc & 31) == lane) {
             const double u = __ldg(&M.U[code]);
 #pragma unroll
@@ -131,7 +131,7 @@ __device__ int block_topk(const RolloutArgs& a, const double* comp, double* W, C
     const int nW = (M.n + 1) * M.PP;
     const int k = a.k;
     for (int e = threadIdx.x; e < nW; e += blockDim.x) {
-        const int svc = e / M.PP;
+        const int svc = svc_of(M, static_cast<unsigned>(e));
         double w = 0.0;
         if (svc < M.n) {
             const double need = __dadd_rn(1.0, -comp[svc]);
@@ -341,6 +341,130 @@ struct Advancer {
     }
 };
 
+// n <= 64: a HALF-warp per rollout (16 lanes x 4 completion slots), two rollouts per warp.
+// The per-step work is mostly uniform within a rollout (Philox draw, cache-slot and pool
+// lookups, the probe), so two halves issuing it together halve the instructions per rollout
+// step and double the dependent load chains in flight (the advance kernel is issue-bound:
+// 62% of issue slots at a warp per rollout, profiles/r02l_roll_adv_ncu.json).
+struct Advancer16 {
+    const RolloutArgs& a;
+    long long* wb;
+    unsigned long long *c_steps, *c_done, *c_cap, *c_fail;
+    int lane, nxt, nbuf = 0;
+
+    __device__ void push_flush() {
+        if (nbuf && lane == 0) {
+            const unsigned long long at = atomicAdd(&a.cnt->n_act[nxt], static_cast<unsigned long long>(nbuf));
+            for (int i = 0; i < nbuf; ++i) (nxt ? a.act1 : a.act0)[at + i] = wb[i];
+        }
+        __syncwarp();
+        nbuf = 0;
+    }
+
+    // both halves call this together (warp-collective); `valid`: this half holds rollout r
+    __device__ void step(long long r, bool valid, bool first) {
+        const DevModel& M = a.M;
+        const int n = M.n;
+        RolloutCounters* C = a.cnt;
+        const int half = lane >> 4, hl = lane & 15;
+        double c[4];
+        const double* src = first ? a.comp0 : a.comp + r * n;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) c[j] = (valid && hl + 16 * j < n) ? src[hl + 16 * j] : 2.0;
+        bool active = valid;
+        int L = 0;
+        unsigned dirty = first ? 0xFu : 0u;
+        if (valid && !first) {
+            L = a.len[r];
+            const unsigned slot = a.rslot[r];
+            const int pn = __ldcg(&a.pool_n[slot]);
+            if (pn <= 0) {  // rollout: "no candidate config serves the remaining demand" (mcts.hpp:135-136)
+                if (hl == 0) {
+                    a.status[r] = 3;
+                    if (a.lengths) a.lengths[r] = -1;
+                    atomicAdd(c_fail, 1ull);
+                }
+                active = false;
+            } else {
+                const uint64_t x = philox_u64(a.seed, static_cast<uint64_t>(a.id0 + r), static_cast<uint64_t>(L));
+                const unsigned pick = __ldcg(&a.pool[static_cast<size_t>(slot) * a.k + philox_below(x, pn)]);
+                const uint64_t row = __ldg(a.base + pick);
+#pragma unroll
+                for (int m = 0; m < 4; ++m) {  // add_util (mcts.hpp:139) in the owning lanes
+                    const unsigned code = static_cast<unsigned>((row >> (16 * m)) & 0xFFFFull);
+                    const int svc = svc_of(M, code);
+                    if (svc < n && (svc & 15) == hl) {
+                        const double u = __ldg(&M.U[code]);
+#pragma unroll
+                        for (int j = 0; j < 4; ++j)
+                            if ((svc >> 4) == j) c[j] = __dadd_rn(c[j], u), dirty |= 1u << j;
+                    }
+                }
+                ++L;
+                if (hl == 0) {
+                    a.len[r] = L;
+                    atomicAdd(c_steps, 1ull);
+                }
+            }
+        }
+        if (first && valid && hl == 0) a.len[r] = 0;
+        uint64_t kw[4] = {0, 0, 0, 0};  // completion_type_key (mcts.hpp:38-43), this half's bitmap
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            if (16 * j >= n) break;
+            const unsigned b = __ballot_sync(0xffffffffu, hl + 16 * j < n && c[j] < 1.0 - 1e-9);
+            kw[0] |= static_cast<uint64_t>((b >> (16 * half)) & 0xFFFFu) << (16 * j);
+        }
+        if (active && kw[0] == 0) {  // satisfied
+            if (hl == 0) {
+                a.status[r] = 1;
+                if (a.lengths) a.lengths[r] = L;
+                atomicMin(&C->best, (static_cast<unsigned long long>(L) << 32) | static_cast<unsigned long long>(r));
+                atomicAdd(c_done, 1ull);
+            }
+            active = false;
+        }
+        if (active && L >= a.max_depth) {  // rollout returns max_depth (mcts.hpp:127)
+            if (hl == 0) {
+                a.status[r] = 2;
+                if (a.lengths) a.lengths[r] = a.max_depth;
+                atomicAdd(c_cap, 1ull);
+            }
+            active = false;
+        }
+        if (active) {
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+                if (hl + 16 * j < n && ((dirty >> j) & 1u)) a.comp[r * n + hl + 16 * j] = c[j];
+        }
+        if (active && hl == 0) {
+            bool created = false;
+            long long slot = probe(a, kw, 1, true, created);
+            if (slot < 0) {
+                atomicExch(&C->status, 1);
+                slot = 0;
+            } else {
+                if (created) {
+                    const unsigned long long at = atomicAdd(&C->n_pend[nxt], 1ull);
+                    (nxt ? a.pend1 : a.pend0)[at] = static_cast<unsigned>(slot);
+                }
+                if (__ldcg(&a.pool_n[slot]) < 0 && __ldcg(&a.claimer[slot]) > static_cast<unsigned long long>(r))
+                    atomicMin(&a.claimer[slot], static_cast<unsigned long long>(r));
+            }
+            a.rslot[r] = static_cast<unsigned>(slot);
+        }
+        // the next round's active list: the warp's buffer takes up to two entries
+        const bool plo = __shfl_sync(0xffffffffu, active, 0), phi = __shfl_sync(0xffffffffu, active, 16);
+        const long long rhi = __shfl_sync(0xffffffffu, r, 16);
+        if (lane == 0) {
+            if (plo) wb[nbuf] = r;
+            if (phi) wb[nbuf + (plo ? 1 : 0)] = rhi;
+        }
+        nbuf += (plo ? 1 : 0) + (phi ? 1 : 0);
+        if (nbuf >= 31) push_flush();
+    }
+};
+
 // Round `round` (or the start, round < 0): every active rollout advances one step, a warp per
 // rollout.  Counters are summed per block, then once into the launch's RolloutCounters.
 template <int J>
@@ -358,13 +482,24 @@ __global__ void __launch_bounds__(kAThreads, kAOcc) rollout_advance_kernel(const
     if (threadIdx.x == 0) c_steps = c_done = c_cap = c_fail = 0;
     __syncthreads();
     const int warp = static_cast<int>(threadIdx.x >> 5);
-    Advancer<J> adv{a, wbuf[warp], &c_steps, &c_done, &c_cap, &c_fail, static_cast<int>(threadIdx.x & 31u),
-                    (a.M.n + 63) / 64, cur ^ 1};
     const long long gw = static_cast<long long>(blockIdx.x) * (kAThreads / 32) + warp;
     const long long nwarps = static_cast<long long>(gridDim.x) * (kAThreads / 32);
     const long long* act = cur ? a.act1 : a.act0;
-    for (long long i = gw; i < static_cast<long long>(n_act); i += nwarps) adv.step(first ? i : __ldcg(&act[i]), first);
-    adv.push_flush();
+    if constexpr (J == 2) {  // n <= 64: two rollouts per warp
+        Advancer16 adv{a, wbuf[warp], &c_steps, &c_done, &c_cap, &c_fail, static_cast<int>(threadIdx.x & 31u), cur ^ 1};
+        const int half = static_cast<int>((threadIdx.x >> 4) & 1u);
+        for (long long i0 = 2 * gw; i0 < static_cast<long long>(n_act); i0 += 2 * nwarps) {
+            const long long i = i0 + half;
+            const bool valid = i < static_cast<long long>(n_act);
+            adv.step(valid ? (first ? i : __ldcg(&act[i])) : 0, valid, first);
+        }
+        adv.push_flush();
+    } else {
+        Advancer<J> adv{a, wbuf[warp], &c_steps, &c_done, &c_cap, &c_fail, static_cast<int>(threadIdx.x & 31u),
+                        (a.M.n + 63) / 64, cur ^ 1};
+        for (long long i = gw; i < static_cast<long long>(n_act); i += nwarps) adv.step(first ? i : __ldcg(&act[i]), first);
+        adv.push_flush();
+    }
     __syncthreads();
     if (threadIdx.x == 0) {
         if (c_steps) atomicAdd(&C->steps, c_steps);

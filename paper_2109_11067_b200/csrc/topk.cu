@@ -53,7 +53,7 @@ __global__ void __launch_bounds__(kTopkThreads, 1) topk1_kernel(const __grid_con
         cta_scored = 0;
     }
     for (int e = threadIdx.x; e < nW; e += blockDim.x) {  // W = need * U (greedy.hpp:38-41)
-        const int svc = e / M.PP;
+        const int svc = svc_of(M, static_cast<unsigned>(e));
         double w = 0.0;
         if (svc < M.n) {
             const double need = __dadd_rn(1.0, -a.comp[svc]);
