@@ -317,7 +317,9 @@ struct RolloutArgs {
     int n_sup;
     const int* sup_begin;
     const unsigned short* sup_svc;
-    int timers;             // diagnostics: CTA 0 prints its phase split (MIGPLAN_ROLLOUT_TIMERS)
+    const unsigned* base32;   // pair pools: the rows' low 32 bits (the pair top-K), else nullptr
+    const unsigned* keyrank;  // config-order key rank of every base row (pair top-K tie-break)
+    int timers;             // diagnostics (unused by the split kernels)
     double comp0[256];      // start completion (travels with the launch)
 };
 

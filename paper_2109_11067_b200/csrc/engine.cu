@@ -427,6 +427,18 @@ void Engine::support_tables() {
     });
 }
 
+const unsigned* Engine::base32() {
+    std::call_once(base32_once_, [&] {
+        const size_t P = base_rows_.size();
+        std::vector<unsigned> lo(std::max<size_t>(P, 1));
+        for (size_t i = 0; i < P; ++i) lo[i] = static_cast<unsigned>(base_rows_[i]);
+        CK(cudaSetDevice(device_));
+        base32_buf_ = std::make_unique<Scratch>(device_, sizeof(unsigned) * lo.size());
+        CK(cudaMemcpy(base32_buf_->get(), lo.data(), sizeof(unsigned) * lo.size(), cudaMemcpyHostToDevice));
+    });
+    return static_cast<const unsigned*>(base32_buf_->get());
+}
+
 Engine::~Engine() {
     cudaSetDevice(device_);
     if (d_shard_) cudaFree(d_shard_);
@@ -1127,6 +1139,9 @@ RolloutResult Engine::rollouts(const std::vector<double>& comp, long long n_roll
     a.n_sup = n_sup_ > 0 && n_sup_ <= max_sup() ? n_sup_ : 0;
     a.sup_begin = a.n_sup ? d_sup_begin_ : nullptr;
     a.sup_svc = a.n_sup ? d_sup_svc_ : nullptr;
+    // pair pools: pool builds run the FP32-bounded pair top-K (topk_pair.cuh) on 32-bit rows
+    a.base32 = a.n_sup ? base32() : nullptr;
+    a.keyrank = a.n_sup ? keyrank() : nullptr;
     cudaStream_t st = nullptr;
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));

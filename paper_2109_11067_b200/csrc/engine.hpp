@@ -246,6 +246,11 @@ class Engine {
     const int* d_sup_begin_ = nullptr;
     const unsigned short* d_sup_svc_ = nullptr;
     void support_tables();
+    // the base pool's rows as 32-bit pairs (max_mix <= 2: the two high codes are sentinels),
+    // for the pool builds' pair top-K (built on first use)
+    std::once_flag base32_once_;
+    std::unique_ptr<Scratch> base32_buf_;
+    const unsigned* base32();
     // supports the pool-build scans may list (pair pools), for shared-memory sizing
     int max_sup() const {
         const long long ns = m_.n + static_cast<long long>(m_.n) * (m_.n - 1) / 2;  // <= 2-member supports

@@ -25,6 +25,7 @@
 
 #include "common.cuh"
 #include "philox.cuh"
+#include "topk_pair.cuh"
 
 namespace mgb {
 
@@ -42,6 +43,10 @@ constexpr int kAThreads = 256;  // advance kernel: small blocks, register-lean, 
 #define MGB_ROLLOUT_AOCC 6
 #endif
 constexpr int kAOcc = MGB_ROLLOUT_AOCC;
+#ifndef MGB_ROLL_LANES
+#define MGB_ROLL_LANES 4
+#endif
+constexpr int kRollLanes = MGB_ROLL_LANES;  // lanes per rollout when n <= 64 (4: eight per warp; A/B profiles/r02l_ab_rollout_lanes.txt)
 
 __device__ __forceinline__ uint64_t mix64(uint64_t z) {
     z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
@@ -341,12 +346,15 @@ struct Advancer {
     }
 };
 
-// n <= 64: a HALF-warp per rollout (16 lanes x 4 completion slots), two rollouts per warp.
+// n <= 64: a HALF-warp per rollout (16 lanes x 4 completion slots), two rollouts per warp
+// (HL = 8: a quarter-warp, four per warp).
 // The per-step work is mostly uniform within a rollout (Philox draw, cache-slot and pool
 // lookups, the probe), so two halves issuing it together halve the instructions per rollout
 // step and double the dependent load chains in flight (the advance kernel is issue-bound:
 // 62% of issue slots at a warp per rollout, profiles/r02l_roll_adv_ncu.json).
-struct Advancer16 {
+template <int HL>
+struct AdvancerH {  // HL lanes per rollout, 64 / HL completion slots per lane (n <= 64)
+    static constexpr int S = 64 / HL, R = 32 / HL;
     const RolloutArgs& a;
     long long* wb;
     unsigned long long *c_steps, *c_done, *c_cap, *c_fail;
@@ -366,14 +374,14 @@ struct Advancer16 {
         const DevModel& M = a.M;
         const int n = M.n;
         RolloutCounters* C = a.cnt;
-        const int half = lane >> 4, hl = lane & 15;
-        double c[4];
+        const int half = lane / HL, hl = lane % HL;
+        double c[S];
         const double* src = first ? a.comp0 : a.comp + r * n;
 #pragma unroll
-        for (int j = 0; j < 4; ++j) c[j] = (valid && hl + 16 * j < n) ? src[hl + 16 * j] : 2.0;
+        for (int j = 0; j < S; ++j) c[j] = (valid && hl + HL * j < n) ? src[hl + HL * j] : 2.0;
         bool active = valid;
         int L = 0;
-        unsigned dirty = first ? 0xFu : 0u;
+        unsigned dirty = first ? ~0u : 0u;  // a new rollout writes every slot
         if (valid && !first) {
             L = a.len[r];
             const unsigned slot = a.rslot[r];
@@ -393,11 +401,11 @@ struct Advancer16 {
                 for (int m = 0; m < 4; ++m) {  // add_util (mcts.hpp:139) in the owning lanes
                     const unsigned code = static_cast<unsigned>((row >> (16 * m)) & 0xFFFFull);
                     const int svc = svc_of(M, code);
-                    if (svc < n && (svc & 15) == hl) {
+                    if (svc < n && (svc % HL) == hl) {
                         const double u = __ldg(&M.U[code]);
 #pragma unroll
-                        for (int j = 0; j < 4; ++j)
-                            if ((svc >> 4) == j) c[j] = __dadd_rn(c[j], u), dirty |= 1u << j;
+                        for (int j = 0; j < S; ++j)
+                            if ((svc / HL) == j) c[j] = __dadd_rn(c[j], u), dirty |= 1u << j;
                     }
                 }
                 ++L;
@@ -410,10 +418,10 @@ struct Advancer16 {
         if (first && valid && hl == 0) a.len[r] = 0;
         uint64_t kw[4] = {0, 0, 0, 0};  // completion_type_key (mcts.hpp:38-43), this half's bitmap
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-            if (16 * j >= n) break;
-            const unsigned b = __ballot_sync(0xffffffffu, hl + 16 * j < n && c[j] < 1.0 - 1e-9);
-            kw[0] |= static_cast<uint64_t>((b >> (16 * half)) & 0xFFFFu) << (16 * j);
+        for (int j = 0; j < S; ++j) {
+            if (HL * j >= n) break;
+            const unsigned b = __ballot_sync(0xffffffffu, hl + HL * j < n && c[j] < 1.0 - 1e-9);
+            kw[0] |= static_cast<uint64_t>((b >> (HL * half)) & ((1u << HL) - 1u)) << (HL * j);
         }
         if (active && kw[0] == 0) {  // satisfied
             if (hl == 0) {
@@ -434,8 +442,8 @@ struct Advancer16 {
         }
         if (active) {
 #pragma unroll
-            for (int j = 0; j < 4; ++j)
-                if (hl + 16 * j < n && ((dirty >> j) & 1u)) a.comp[r * n + hl + 16 * j] = c[j];
+            for (int j = 0; j < S; ++j)
+                if (hl + HL * j < n && ((dirty >> j) & 1u)) a.comp[r * n + hl + HL * j] = c[j];
         }
         if (active && hl == 0) {
             bool created = false;
@@ -453,15 +461,15 @@ struct Advancer16 {
             }
             a.rslot[r] = static_cast<unsigned>(slot);
         }
-        // the next round's active list: the warp's buffer takes up to two entries
-        const bool plo = __shfl_sync(0xffffffffu, active, 0), phi = __shfl_sync(0xffffffffu, active, 16);
-        const long long rhi = __shfl_sync(0xffffffffu, r, 16);
-        if (lane == 0) {
-            if (plo) wb[nbuf] = r;
-            if (phi) wb[nbuf + (plo ? 1 : 0)] = rhi;
+        // the next round's active list: the warp's buffer takes up to R entries
+        const unsigned pm = __ballot_sync(0xffffffffu, active && hl == 0);  // bit HL*q: rollout q continues
+#pragma unroll
+        for (int q = 0; q < R; ++q) {
+            const long long rq = __shfl_sync(0xffffffffu, r, HL * q);
+            if (lane == 0 && ((pm >> (HL * q)) & 1u)) wb[nbuf + __popc(pm & ((1u << (HL * q)) - 1u))] = rq;
         }
-        nbuf += (plo ? 1 : 0) + (phi ? 1 : 0);
-        if (nbuf >= 31) push_flush();
+        nbuf += __popc(pm);
+        if (nbuf > 32 - R) push_flush();
     }
 };
 
@@ -485,10 +493,11 @@ __global__ void __launch_bounds__(kAThreads, kAOcc) rollout_advance_kernel(const
     const long long gw = static_cast<long long>(blockIdx.x) * (kAThreads / 32) + warp;
     const long long nwarps = static_cast<long long>(gridDim.x) * (kAThreads / 32);
     const long long* act = cur ? a.act1 : a.act0;
-    if constexpr (J == 2) {  // n <= 64: two rollouts per warp
-        Advancer16 adv{a, wbuf[warp], &c_steps, &c_done, &c_cap, &c_fail, static_cast<int>(threadIdx.x & 31u), cur ^ 1};
-        const int half = static_cast<int>((threadIdx.x >> 4) & 1u);
-        for (long long i0 = 2 * gw; i0 < static_cast<long long>(n_act); i0 += 2 * nwarps) {
+    if constexpr (J == 2) {  // n <= 64: several rollouts per warp
+        using Adv = AdvancerH<kRollLanes>;
+        Adv adv{a, wbuf[warp], &c_steps, &c_done, &c_cap, &c_fail, static_cast<int>(threadIdx.x & 31u), cur ^ 1};
+        const int half = static_cast<int>((threadIdx.x & 31u) / kRollLanes);
+        for (long long i0 = Adv::R * gw; i0 < static_cast<long long>(n_act); i0 += Adv::R * nwarps) {
             const long long i = i0 + half;
             const bool valid = i < static_cast<long long>(n_act);
             adv.step(valid ? (first ? i : __ldcg(&act[i])) : 0, valid, first);
@@ -511,16 +520,21 @@ __global__ void __launch_bounds__(kAThreads, kAOcc) rollout_advance_kernel(const
 
 // Round `round`: the pools of the keys first reached in the previous step (CTA per key).
 // Block 0 also opens the round: the next round's lists start empty.
-__global__ void __launch_bounds__(kRThreads, 2) rollout_build_kernel(const __grid_constant__ RolloutArgs a, int round) {
+__global__ void __launch_bounds__(kRThreads, 1) rollout_build_kernel(const __grid_constant__ RolloutArgs a, int round) {
     extern __shared__ __align__(16) unsigned char smem[];
     const DevModel& M = a.M;
     const int n = M.n;
+    const int nW = (n + 1) * M.PP;
     double* W = reinterpret_cast<double*>(smem);
-    double* comp_s = W + (n + 1) * M.PP;
+    double* comp_s = W + nW;
     Cand* cand = reinterpret_cast<Cand*>(comp_s + n + 1);
     Cand* win = cand + kRCandCap;
     int* sact = reinterpret_cast<int*>(win + kRMaxK);  // active supports of a pool build (a.n_sup)
+    float* Wf = reinterpret_cast<float*>(sact + (a.n_sup > 0 ? a.n_sup : 0));  // pair top-K tables
+    unsigned char* hitc = reinterpret_cast<unsigned char*>(Wf + nW);
+    __shared__ int s_out[kRMaxK];
     RolloutCounters* C = a.cnt;
+    topk_pair_counters_init();
     const int cur = round & 1, nxt = cur ^ 1;
     if (*reinterpret_cast<volatile int*>(&C->done)) return;  // enqueued past the last round
     const unsigned long long n_act = __ldcg(&C->n_act[cur]);
@@ -540,7 +554,15 @@ __global__ void __launch_bounds__(kRThreads, 2) rollout_build_kernel(const __gri
         const long long r = static_cast<long long>(__ldcg(&a.claimer[slot]));
         for (int i = threadIdx.x; i < n; i += blockDim.x) comp_s[i] = __ldcg(&a.comp[r * n + i]);
         __syncthreads();
-        const int got = block_topk(a, comp_s, W, cand, win, a.pool + static_cast<size_t>(slot) * a.k, sact);
+        int got;
+        if (a.base32) {  // pair pool: FP32-bounded two-pass top-K over the live supports (K7's)
+            int scored = 0;
+            got = block_topk_pair(M, a.keyrank, a.base32, a.n_base, 0, comp_s, nullptr, a.k, M.U, W, Wf, hitc, cand, win,
+                                  s_out, &scored, false, SupTab{a.n_sup, a.sup_begin, a.sup_svc, sact});
+            if (threadIdx.x < got) a.pool[static_cast<size_t>(slot) * a.k + threadIdx.x] = static_cast<unsigned>(s_out[threadIdx.x]);
+        } else {
+            got = block_topk(a, comp_s, W, cand, win, a.pool + static_cast<size_t>(slot) * a.k, sact);
+        }
         if (threadIdx.x == 0) a.pool_n[slot] = got;
         __syncthreads();
     }
@@ -582,8 +604,9 @@ __global__ void rollout_replay_kernel(const __grid_constant__ RolloutArgs a) {
 }
 
 size_t rollout_smem_bytes(int n, int PP, int n_sup) {
-    return static_cast<size_t>((n + 1) * PP + n + 1) * 8 + static_cast<size_t>(kRCandCap + kRMaxK) * sizeof(Cand) +
-           sizeof(int) * static_cast<size_t>(n_sup);
+    const size_t nW = static_cast<size_t>(n + 1) * PP;
+    return (nW + n + 1) * 8 + static_cast<size_t>(kRCandCap + kRMaxK) * sizeof(Cand) + sizeof(int) * static_cast<size_t>(n_sup) +
+           nW * 4 + nW + 16;  // + the pair top-K's Wf and mask-hit tables
 }
 const void* rollout_build_ptr() { return reinterpret_cast<const void*>(&rollout_build_kernel); }
 const void* rollout_advance_ptr(int n) {
