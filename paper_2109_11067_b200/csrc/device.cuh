@@ -277,7 +277,7 @@ struct RolloutCounters {
     unsigned long long n_act[2];  // active-list lengths (ping-pong by round parity)
     unsigned long long n_pend[2]; // key-cache slots created per round (ping-pong)
     int done;                     // a round found no active rollout (its build kernel sets it)
-    int pad;
+    unsigned int bar_count, bar_gen;  // grid barrier of the persistent small-batch kernel
     int status;                   // 0 ok, 1 key cache full
     int rounds;
     unsigned long long best;      // min over completed rollouts of (steps << 32 | batch index)

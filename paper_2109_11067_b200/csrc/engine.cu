@@ -50,6 +50,8 @@ int mcts_threads();
 const void* rollout_build_ptr();
 const void* rollout_advance_ptr(int n);
 const void* rollout_replay_ptr(int n);
+const void* rollout_persistent_ptr(int n);
+int rollout_per_warp(int n);
 int rollout_threads();
 int rollout_advance_threads();
 
@@ -443,6 +445,12 @@ Engine::~Engine() {
     cudaSetDevice(device_);
     if (d_shard_) cudaFree(d_shard_);
     for (void* p : dev_allocs_) cudaFree(p);
+    for (auto& b : ro_blocks_) b.host ? cudaFreeHost(b.p) : cudaFree(b.p);
+    for (auto& x : ro_streams_) {
+        cudaEventDestroy(x.e0);
+        cudaEventDestroy(x.e1);
+        cudaStreamDestroy(x.s);
+    }
 }
 
 long long Engine::index_of(uint64_t row) const {
@@ -500,7 +508,7 @@ const DeviceInfo& device_info(int device) {
     CK(cudaFuncSetAttribute(mcts_kernel_ptr(1), cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     CK(cudaFuncSetAttribute(mcts_kernel_ptr(255), cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     CK(cudaFuncSetAttribute(greedy_kernel_ptr(), cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-    for (const void* k : {greedy_kernel_ptr(), topk_kernel_ptr(), topk1_kernel_ptr(32), rollout_build_ptr(),
+    for (const void* k : {greedy_kernel_ptr(), topk_kernel_ptr(), topk1_kernel_ptr(32), rollout_build_ptr(), rollout_persistent_ptr(1), rollout_persistent_ptr(256),
                           mcts_kernel_ptr(1), mcts_kernel_ptr(255)}) {
         cudaFuncAttributes fa{};
         CK(cudaFuncGetAttributes(&fa, k));
@@ -822,7 +830,11 @@ int Engine::greedy_cluster_ctas(size_t smem, long long rows_bound) const {
     if (n_ranks_ > 1) return 0;
     constexpr long long kClusterRows = 256ll << 10;
     if (rows_bound < 0) rows_bound = pool_size() + ext_bound_;
-    int want = rows_bound <= kClusterRows ? 16 : 0;
+    static const int small = [] {  // CTAs per small instance (MIGPLAN_GREEDY_CLUSTER_SMALL: A/B)
+        const char* e = std::getenv("MIGPLAN_GREEDY_CLUSTER_SMALL");
+        return e ? std::max(2, std::min(16, std::atoi(e))) : 8;  // 8: GA refills 5.5 -> 5.0 ms per GA10 (16 and 4 slower)
+    }();
+    int want = rows_bound <= kClusterRows ? small : 0;
     const char* v = std::getenv("MIGPLAN_GREEDY_CLUSTER");
     if (v) want = std::max(0, std::min(16, std::atoi(v)));
     if (want == 0) return 0;
@@ -1064,6 +1076,59 @@ std::vector<long long> Engine::topk(const std::vector<double>& comp, int k, cons
 // Root-parallel rollouts (rollout.cu).  Device buffers live for the call; the key cache
 // persists across the call's batches (the reference's RolloutCache lives for one
 // mcts_solve call, mcts.hpp:158).  A full key cache restarts the call with 4x capacity.
+void* Engine::ro_get(size_t bytes, bool host) {
+    bytes = std::max<size_t>(bytes, 16);
+    {
+        std::lock_guard<std::mutex> g(ro_mu_);
+        int best = -1;
+        for (int i = 0; i < static_cast<int>(ro_blocks_.size()); ++i) {  // best fit, at most 4x the request
+            const CacheBlk& b = ro_blocks_[i];
+            if (!b.used && b.host == host && b.n >= bytes && b.n <= 4 * bytes + (1 << 20) &&
+                (best < 0 || b.n < ro_blocks_[best].n))
+                best = i;
+        }
+        if (best >= 0) {
+            ro_blocks_[best].used = true;
+            return ro_blocks_[best].p;
+        }
+    }
+    void* p = nullptr;
+    if (host)
+        CK(cudaHostAlloc(&p, bytes, cudaHostAllocMapped));
+    else
+        CK(cudaMalloc(&p, bytes));
+    std::lock_guard<std::mutex> g(ro_mu_);
+    ro_blocks_.push_back(CacheBlk{p, bytes, host, true});
+    return p;
+}
+void Engine::ro_put(void* p) {
+    std::lock_guard<std::mutex> g(ro_mu_);
+    for (auto& b : ro_blocks_)
+        if (b.p == p) b.used = false;
+}
+int Engine::ro_stream() {
+    {
+        std::lock_guard<std::mutex> g(ro_mu_);
+        for (int i = 0; i < static_cast<int>(ro_streams_.size()); ++i)
+            if (!ro_streams_[i].used) {
+                ro_streams_[i].used = true;
+                return i;
+            }
+    }
+    CacheStream x{};
+    CK(cudaStreamCreateWithFlags(&x.s, cudaStreamNonBlocking));
+    CK(cudaEventCreate(&x.e0));
+    CK(cudaEventCreate(&x.e1));
+    x.used = true;
+    std::lock_guard<std::mutex> g(ro_mu_);
+    ro_streams_.push_back(x);
+    return static_cast<int>(ro_streams_.size()) - 1;
+}
+void Engine::ro_stream_put(int i) {
+    std::lock_guard<std::mutex> g(ro_mu_);
+    ro_streams_[i].used = false;
+}
+
 RolloutResult Engine::rollouts(const std::vector<double>& comp, long long n_roll, int k, int max_depth, uint64_t seed,
                                long long id_offset, long long batch, int table_log2, int* lengths) {
     MGB_RANGE("migplan: rollouts");
@@ -1083,16 +1148,16 @@ RolloutResult Engine::rollouts(const std::vector<double>& comp, long long n_roll
     }
     L2 = std::min(std::max(L2, 4), 30);
     const int n = m_.n;
-    std::vector<void*> owned;
+    std::vector<void*> owned;  // cached blocks (ro_get), handed back when the call ends
     struct Free {
+        Engine* e;
         std::vector<void*>& v;
         ~Free() {
-            for (void* p : v) cudaFree(p);
+            for (void* p : v) e->ro_put(p);
         }
-    } fr{owned};
+    } fr{this, owned};
     auto alloc = [&](size_t bytes) {
-        void* p = nullptr;
-        CK(cudaMalloc(&p, std::max<size_t>(bytes, 16)));
+        void* p = ro_get(bytes, false);
         owned.push_back(p);
         return p;
     };
@@ -1101,18 +1166,10 @@ RolloutResult Engine::rollouts(const std::vector<double>& comp, long long n_roll
         int pad;
         double comp[256];
     };
-    HostOut* ho = nullptr;
-    long long* hpath = nullptr;
-    CK(cudaHostAlloc(&ho, sizeof(HostOut), cudaHostAllocMapped));
-    CK(cudaHostAlloc(&hpath, sizeof(long long) * (max_depth + 1), cudaHostAllocMapped));
-    struct FreeHost {
-        void* a;
-        void* b;
-        ~FreeHost() {
-            cudaFreeHost(a);
-            cudaFreeHost(b);
-        }
-    } fh{ho, hpath};
+    HostOut* ho = static_cast<HostOut*>(ro_get(sizeof(HostOut), true));
+    owned.push_back(ho);
+    long long* hpath = static_cast<long long*>(ro_get(sizeof(long long) * (max_depth + 1), true));
+    owned.push_back(hpath);
     std::memcpy(ho->comp, comp.data(), sizeof(double) * n);
 
     RolloutArgs a{};
@@ -1142,20 +1199,24 @@ RolloutResult Engine::rollouts(const std::vector<double>& comp, long long n_roll
     // pair pools: pool builds run the FP32-bounded pair top-K (topk_pair.cuh) on 32-bit rows
     a.base32 = a.n_sup ? base32() : nullptr;
     a.keyrank = a.n_sup ? keyrank() : nullptr;
-    cudaStream_t st = nullptr;
-    cudaEvent_t e0 = nullptr, e1 = nullptr;
-    CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
-    CK(cudaEventCreate(&e0));
-    CK(cudaEventCreate(&e1));
-    struct FreeStream {
+    const int si = ro_stream();  // cached stream + events (handed back at the end of the call)
+    cudaStream_t st;
+    cudaEvent_t e0, e1;
+    {
+        std::lock_guard<std::mutex> g(ro_mu_);
+        st = ro_streams_[si].s;
+        e0 = ro_streams_[si].e0;
+        e1 = ro_streams_[si].e1;
+    }
+    struct PutStream {
+        Engine* e;
+        int i;
         cudaStream_t s;
-        cudaEvent_t a, b;
-        ~FreeStream() {
-            cudaEventDestroy(a);
-            cudaEventDestroy(b);
-            cudaStreamDestroy(s);
+        ~PutStream() {
+            cudaStreamSynchronize(s);
+            e->ro_stream_put(i);
         }
-    } fs{st, e0, e1};
+    } ps{this, si, st};
     const int G = num_sms_ * rollout_blocks_per_sm_;
     const size_t smem = rollout_smem_bytes(n, m_.PP, max_sup());
 
@@ -1199,21 +1260,32 @@ RolloutResult Engine::rollouts(const std::vector<double>& comp, long long n_roll
                 void* args[] = {&a, &round};
                 CK(cudaLaunchKernel(kb, G, rollout_threads(), args, smem, st));
             };
+            // every round a rollout can need (a rollout takes at most max_depth steps) is enqueued
+            // up front: the host never waits between rounds (a synchronisation per chunk left the
+            // GPU idle while the next chunk was enqueued), and the rounds past the last one are
+            // no-op launches (C->done)
             CK(cudaEventRecord(e0, st));
-            adv(-1);
-            int launches = 1;
+            int launches = 0;
             RolloutCounters c{};
-            for (int round = 0, chunk = 8;; chunk = std::min(2 * chunk, 128)) {
-                for (int q = 0; q < chunk && round <= max_depth + 1; ++q, ++round) {
+            // small batches (one advance pass per round fits the grid once): one cooperative
+            // launch runs every round with grid barriers (MIGPLAN_ROLLOUT_PERSIST=0/1 forces)
+            const long long per_pass = static_cast<long long>(num_sms_) * (rollout_threads() / 32) * rollout_per_warp(m_.n);
+            bool persist = a.n_roll <= per_pass;
+            if (const char* v = std::getenv("MIGPLAN_ROLLOUT_PERSIST")) persist = std::atoi(v) != 0;
+            if (persist) {
+                void* args[] = {&a};
+                CK(cudaLaunchCooperativeKernel(rollout_persistent_ptr(m_.n), num_sms_, rollout_threads(), args, smem, st));
+                launches = 1;
+            } else {
+                adv(-1);
+                launches = 1;
+                for (int round = 0; round <= max_depth + 1; ++round) {
                     bld(round);
                     adv(round);
                     launches += 2;
                 }
-                CK(cudaMemcpyAsync(&c, a.cnt, sizeof c, cudaMemcpyDeviceToHost, st));
-                CK(cudaStreamSynchronize(st));
-                if (c.done || c.status != 0 || round > max_depth + 1) break;
             }
-            {
+            if (!persist) {
                 void* args[] = {&a};
                 CK(cudaLaunchKernel(rollout_replay_ptr(m_.n), 1, 32, args, 0, st));
                 ++launches;
@@ -1251,7 +1323,7 @@ RolloutResult Engine::rollouts(const std::vector<double>& comp, long long n_roll
         }
         if (full && attempt < 3 && L2 < 30) {
             for (void* p : table) {
-                cudaFree(p);
+                ro_put(p);
                 owned.erase(std::find(owned.begin(), owned.end(), p));
             }
             L2 = std::min(L2 + 2, 30);

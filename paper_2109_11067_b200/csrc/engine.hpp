@@ -9,6 +9,7 @@
 
 #include <atomic>
 #include <map>
+#include <deque>
 #include <memory>
 #include <mutex>
 #include <string>
@@ -226,6 +227,26 @@ class Engine {
     int rollout_adv_blocks_per_sm_ = 0;  // advance kernel
     DevModel dm_{};
     std::vector<void*> dev_allocs_;
+    // per-call rollout buffers (device and host-mapped) and streams, cached across calls: a
+    // rollout call with cudaMalloc/cudaHostAlloc/cudaFree of its tables cost milliseconds of
+    // host time (config #3 runs hundreds of small rollout calls)
+    struct CacheBlk {
+        void* p;
+        size_t n;
+        bool host, used;
+    };
+    std::mutex ro_mu_;
+    std::vector<CacheBlk> ro_blocks_;
+    struct CacheStream {
+        cudaStream_t s;
+        cudaEvent_t e0, e1;
+        bool used;
+    };
+    std::deque<CacheStream> ro_streams_;  // deque: entries stay put while others are added
+    void* ro_get(size_t bytes, bool host);
+    void ro_put(void* p);
+    int ro_stream();
+    void ro_stream_put(int i);
     uint64_t* d_base_ = nullptr;
     std::vector<uint64_t> base_rows_;
     mutable std::unordered_map<uint64_t, long long> row_index_;

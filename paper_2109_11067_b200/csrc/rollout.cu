@@ -473,29 +473,22 @@ struct AdvancerH {  // HL lanes per rollout, 64 / HL completion slots per lane (
     }
 };
 
-// Round `round` (or the start, round < 0): every active rollout advances one step, a warp per
-// rollout.  Counters are summed per block, then once into the launch's RolloutCounters.
-template <int J>
-__global__ void __launch_bounds__(kAThreads, kAOcc) rollout_advance_kernel(const __grid_constant__ RolloutArgs a, int round) {
-    __shared__ long long wbuf[kAThreads / 32][32];
-    __shared__ unsigned long long c_steps, c_done, c_cap, c_fail;
+// One advance pass of a block over the active list (or, first, over every rollout): a warp
+// per rollout (n > 64) or kRollLanes lanes per rollout (n <= 64).  Block-level counters are
+// summed into the launch's RolloutCounters at the end.  Ends with a barrier.
+template <int J, int NT>
+__device__ void advance_pass(const RolloutArgs& a, bool first, int cur, unsigned long long n_act, long long (*wbuf)[32],
+                             unsigned long long* cnt4) {
     RolloutCounters* C = a.cnt;
-    const bool first = round < 0;
-    const int cur = first ? 1 : (round & 1);
-    unsigned long long n_act = static_cast<unsigned long long>(a.n_roll);
-    if (!first) {  // rounds enqueued past the last one (C->done) are no-ops
-        n_act = __ldcg(&C->n_act[cur]);
-        if (n_act == 0 || __ldcg(&C->status) != 0 || *reinterpret_cast<volatile int*>(&C->done)) return;
-    }
-    if (threadIdx.x == 0) c_steps = c_done = c_cap = c_fail = 0;
+    if (threadIdx.x == 0) cnt4[0] = cnt4[1] = cnt4[2] = cnt4[3] = 0;
     __syncthreads();
     const int warp = static_cast<int>(threadIdx.x >> 5);
-    const long long gw = static_cast<long long>(blockIdx.x) * (kAThreads / 32) + warp;
-    const long long nwarps = static_cast<long long>(gridDim.x) * (kAThreads / 32);
+    const long long gw = static_cast<long long>(blockIdx.x) * (NT / 32) + warp;
+    const long long nwarps = static_cast<long long>(gridDim.x) * (NT / 32);
     const long long* act = cur ? a.act1 : a.act0;
     if constexpr (J == 2) {  // n <= 64: several rollouts per warp
         using Adv = AdvancerH<kRollLanes>;
-        Adv adv{a, wbuf[warp], &c_steps, &c_done, &c_cap, &c_fail, static_cast<int>(threadIdx.x & 31u), cur ^ 1};
+        Adv adv{a, wbuf[warp], &cnt4[0], &cnt4[1], &cnt4[2], &cnt4[3], static_cast<int>(threadIdx.x & 31u), cur ^ 1};
         const int half = static_cast<int>((threadIdx.x & 31u) / kRollLanes);
         for (long long i0 = Adv::R * gw; i0 < static_cast<long long>(n_act); i0 += Adv::R * nwarps) {
             const long long i = i0 + half;
@@ -504,73 +497,66 @@ __global__ void __launch_bounds__(kAThreads, kAOcc) rollout_advance_kernel(const
         }
         adv.push_flush();
     } else {
-        Advancer<J> adv{a, wbuf[warp], &c_steps, &c_done, &c_cap, &c_fail, static_cast<int>(threadIdx.x & 31u),
+        Advancer<J> adv{a, wbuf[warp], &cnt4[0], &cnt4[1], &cnt4[2], &cnt4[3], static_cast<int>(threadIdx.x & 31u),
                         (a.M.n + 63) / 64, cur ^ 1};
         for (long long i = gw; i < static_cast<long long>(n_act); i += nwarps) adv.step(first ? i : __ldcg(&act[i]), first);
         adv.push_flush();
     }
     __syncthreads();
     if (threadIdx.x == 0) {
-        if (c_steps) atomicAdd(&C->steps, c_steps);
-        if (c_done) atomicAdd(&C->completed, c_done);
-        if (c_cap) atomicAdd(&C->capped, c_cap);
-        if (c_fail) atomicAdd(&C->failed, c_fail);
+        if (cnt4[0]) atomicAdd(&C->steps, cnt4[0]);
+        if (cnt4[1]) atomicAdd(&C->completed, cnt4[1]);
+        if (cnt4[2]) atomicAdd(&C->capped, cnt4[2]);
+        if (cnt4[3]) atomicAdd(&C->failed, cnt4[3]);
     }
 }
 
-// Round `round`: the pools of the keys first reached in the previous step (CTA per key).
-// Block 0 also opens the round: the next round's lists start empty.
-__global__ void __launch_bounds__(kRThreads, 1) rollout_build_kernel(const __grid_constant__ RolloutArgs a, int round) {
-    extern __shared__ __align__(16) unsigned char smem[];
+// Shared-memory tables of a pool build (same offsets in the build and persistent kernels).
+struct BuildSmem {
+    double *W, *comp;
+    Cand *cand, *win;
+    int* sact;
+    float* Wf;
+    unsigned char* hitc;
+    __device__ BuildSmem(unsigned char* smem, const RolloutArgs& a) {
+        const int n = a.M.n, nW = (n + 1) * a.M.PP;
+        W = reinterpret_cast<double*>(smem);
+        comp = W + nW;
+        cand = reinterpret_cast<Cand*>(comp + n + 1);
+        win = cand + kRCandCap;
+        sact = reinterpret_cast<int*>(win + kRMaxK);  // active supports of a pool build (a.n_sup)
+        Wf = reinterpret_cast<float*>(sact + (a.n_sup > 0 ? a.n_sup : 0));  // pair top-K tables
+        hitc = reinterpret_cast<unsigned char*>(Wf + nW);
+    }
+};
+
+// The pools of the keys created in the previous step (slots pend[0..n_pend)), CTA per key.
+__device__ void build_pass(const RolloutArgs& a, const BuildSmem& sm, int cur, unsigned long long n_pend, int* s_out) {
     const DevModel& M = a.M;
     const int n = M.n;
-    const int nW = (n + 1) * M.PP;
-    double* W = reinterpret_cast<double*>(smem);
-    double* comp_s = W + nW;
-    Cand* cand = reinterpret_cast<Cand*>(comp_s + n + 1);
-    Cand* win = cand + kRCandCap;
-    int* sact = reinterpret_cast<int*>(win + kRMaxK);  // active supports of a pool build (a.n_sup)
-    float* Wf = reinterpret_cast<float*>(sact + (a.n_sup > 0 ? a.n_sup : 0));  // pair top-K tables
-    unsigned char* hitc = reinterpret_cast<unsigned char*>(Wf + nW);
-    __shared__ int s_out[kRMaxK];
-    RolloutCounters* C = a.cnt;
-    topk_pair_counters_init();
-    const int cur = round & 1, nxt = cur ^ 1;
-    if (*reinterpret_cast<volatile int*>(&C->done)) return;  // enqueued past the last round
-    const unsigned long long n_act = __ldcg(&C->n_act[cur]);
-    const unsigned long long n_pend = __ldcg(&C->n_pend[cur]);
-    if (n_act == 0 || __ldcg(&C->status) != 0) {
-        if (blockIdx.x == 0 && threadIdx.x == 0) C->done = 1;
-        return;
-    }
-    if (blockIdx.x == 0 && threadIdx.x == 0) {  // last read by the previous round's kernels
-        C->n_act[nxt] = 0;
-        C->n_pend[nxt] = 0;
-        C->keys += n_pend;
-        C->rounds = round + 1;
-    }
     for (unsigned long long p = blockIdx.x; p < n_pend; p += gridDim.x) {
         const unsigned slot = __ldcg(&(cur ? a.pend1 : a.pend0)[p]);
         const long long r = static_cast<long long>(__ldcg(&a.claimer[slot]));
-        for (int i = threadIdx.x; i < n; i += blockDim.x) comp_s[i] = __ldcg(&a.comp[r * n + i]);
+        for (int i = threadIdx.x; i < n; i += blockDim.x) sm.comp[i] = __ldcg(&a.comp[r * n + i]);
         __syncthreads();
         int got;
         if (a.base32) {  // pair pool: FP32-bounded two-pass top-K over the live supports (K7's)
             int scored = 0;
-            got = block_topk_pair(M, a.keyrank, a.base32, a.n_base, 0, comp_s, nullptr, a.k, M.U, W, Wf, hitc, cand, win,
-                                  s_out, &scored, false, SupTab{a.n_sup, a.sup_begin, a.sup_svc, sact});
+            got = block_topk_pair(M, a.keyrank, a.base32, a.n_base, 0, sm.comp, nullptr, a.k, M.U, sm.W, sm.Wf, sm.hitc,
+                                  sm.cand, sm.win, s_out, &scored, false, SupTab{a.n_sup, a.sup_begin, a.sup_svc, sm.sact});
             if (threadIdx.x < got) a.pool[static_cast<size_t>(slot) * a.k + threadIdx.x] = static_cast<unsigned>(s_out[threadIdx.x]);
         } else {
-            got = block_topk(a, comp_s, W, cand, win, a.pool + static_cast<size_t>(slot) * a.k, sact);
+            got = block_topk(a, sm.comp, sm.W, sm.cand, sm.win, a.pool + static_cast<size_t>(slot) * a.k, sm.sact);
         }
         if (threadIdx.x == 0) a.pool_n[slot] = got;
         __syncthreads();
     }
 }
 
-// The shortest completed rollout (ties: lowest index), replayed from the immutable cache.
+// The shortest completed rollout (ties: lowest index), replayed from the immutable cache by
+// one warp: its path, pick by pick.
 template <int J>
-__global__ void rollout_replay_kernel(const __grid_constant__ RolloutArgs a) {
+__device__ void replay_winner(const RolloutArgs& a) {
     const DevModel& M = a.M;
     const int n = M.n, nk = (n + 63) / 64;
     const int lane = static_cast<int>(threadIdx.x & 31u);
@@ -603,6 +589,85 @@ __global__ void rollout_replay_kernel(const __grid_constant__ RolloutArgs a) {
     if (lane == 0) *a.path_len = plen;
 }
 
+// Round `round` (or the start, round < 0): every active rollout advances one step.
+template <int J>
+__global__ void __launch_bounds__(kAThreads, kAOcc) rollout_advance_kernel(const __grid_constant__ RolloutArgs a, int round) {
+    __shared__ long long wbuf[kAThreads / 32][32];
+    __shared__ unsigned long long cnt4[4];
+    RolloutCounters* C = a.cnt;
+    const bool first = round < 0;
+    const int cur = first ? 1 : (round & 1);
+    unsigned long long n_act = static_cast<unsigned long long>(a.n_roll);
+    if (!first) {  // rounds enqueued past the last one (C->done) are no-ops
+        n_act = __ldcg(&C->n_act[cur]);
+        if (n_act == 0 || __ldcg(&C->status) != 0 || *reinterpret_cast<volatile int*>(&C->done)) return;
+    }
+    advance_pass<J, kAThreads>(a, first, cur, n_act, wbuf, cnt4);
+}
+
+// Round `round`: the pools of the keys first reached in the previous step (CTA per key).
+// Block 0 also opens the round: the next round's lists start empty.
+__global__ void __launch_bounds__(kRThreads, 1) rollout_build_kernel(const __grid_constant__ RolloutArgs a, int round) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const BuildSmem sm(smem, a);
+    __shared__ int s_out[kRMaxK];
+    RolloutCounters* C = a.cnt;
+    topk_pair_counters_init();
+    const int cur = round & 1, nxt = cur ^ 1;
+    if (*reinterpret_cast<volatile int*>(&C->done)) return;  // enqueued past the last round
+    const unsigned long long n_act = __ldcg(&C->n_act[cur]);
+    const unsigned long long n_pend = __ldcg(&C->n_pend[cur]);
+    if (n_act == 0 || __ldcg(&C->status) != 0) {
+        if (blockIdx.x == 0 && threadIdx.x == 0) C->done = 1;
+        return;
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) {  // last read by the previous round's kernels
+        C->n_act[nxt] = 0;
+        C->n_pend[nxt] = 0;
+        C->keys += n_pend;
+        C->rounds = round + 1;
+    }
+    build_pass(a, sm, cur, n_pend, s_out);
+}
+
+template <int J>
+__global__ void rollout_replay_kernel(const __grid_constant__ RolloutArgs a) {
+    replay_winner<J>(a);
+}
+
+// Small batches (one advance pass per round fits one wave of the grid): the same rounds in
+// ONE cooperative launch with grid barriers — per-round launches cost more than the work there
+// (config #3's refills: 1,024 rollouts, ~100 rounds per call).
+template <int J>
+__global__ void __launch_bounds__(kRThreads, 1) rollout_persistent_kernel(const __grid_constant__ RolloutArgs a) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const BuildSmem sm(smem, a);
+    __shared__ int s_out[kRMaxK];
+    __shared__ long long wbuf[kRThreads / 32][32];
+    __shared__ unsigned long long cnt4[4];
+    RolloutCounters* C = a.cnt;
+    topk_pair_counters_init();
+    advance_pass<J, kRThreads>(a, true, 1, static_cast<unsigned long long>(a.n_roll), wbuf, cnt4);
+    grid_barrier(&C->bar_count, &C->bar_gen, gridDim.x);
+    for (int round = 0;; ++round) {
+        const int cur = round & 1, nxt = cur ^ 1;
+        const unsigned long long n_act = __ldcg(&C->n_act[cur]);
+        const unsigned long long n_pend = __ldcg(&C->n_pend[cur]);
+        if (n_act == 0 || __ldcg(&C->status) != 0) break;
+        if (blockIdx.x == 0 && threadIdx.x == 0) {  // last read in round - 1, next written after the barrier below
+            C->n_act[nxt] = 0;
+            C->n_pend[nxt] = 0;
+            C->keys += n_pend;
+            C->rounds = round + 1;
+        }
+        build_pass(a, sm, cur, n_pend, s_out);
+        grid_barrier(&C->bar_count, &C->bar_gen, gridDim.x);
+        advance_pass<J, kRThreads>(a, false, cur, n_act, wbuf, cnt4);
+        grid_barrier(&C->bar_count, &C->bar_gen, gridDim.x);
+    }
+    if (blockIdx.x == 0 && threadIdx.x < 32) replay_winner<J>(a);
+}
+
 size_t rollout_smem_bytes(int n, int PP, int n_sup) {
     const size_t nW = static_cast<size_t>(n + 1) * PP;
     return (nW + n + 1) * 8 + static_cast<size_t>(kRCandCap + kRMaxK) * sizeof(Cand) + sizeof(int) * static_cast<size_t>(n_sup) +
@@ -613,6 +678,11 @@ const void* rollout_advance_ptr(int n) {
     return n <= 64 ? reinterpret_cast<const void*>(&rollout_advance_kernel<2>)
                    : reinterpret_cast<const void*>(&rollout_advance_kernel<kMaxJ>);
 }
+const void* rollout_persistent_ptr(int n) {
+    return n <= 64 ? reinterpret_cast<const void*>(&rollout_persistent_kernel<2>)
+                   : reinterpret_cast<const void*>(&rollout_persistent_kernel<kMaxJ>);
+}
+int rollout_per_warp(int n) { return n <= 64 ? 32 / kRollLanes : 1; }
 const void* rollout_replay_ptr(int n) {
     return n <= 64 ? reinterpret_cast<const void*>(&rollout_replay_kernel<2>)
                    : reinterpret_cast<const void*>(&rollout_replay_kernel<kMaxJ>);
