@@ -118,3 +118,19 @@ def test_philox_product_host_without_gpu():
     b = S.product_backend()
     for seed, stream, step, want in KAT:
         assert philox_draw(b, seed, stream, step, 0) == want
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("persist", ["0", "1"])
+@pytest.mark.parametrize("name", sorted(ROLL))
+def test_rollout_launch_modes_match_golden(name, persist, monkeypatch):
+    """Both launch schedules of the device rollouts — one cooperative launch for a batch that fits
+    one advance pass, per-round build/advance launches otherwise (rollout.cu) — forced either way
+    (MIGPLAN_ROLLOUT_PERSIST), reproduce the goldens."""
+    g = ROLL[name]
+    monkeypatch.setenv("MIGPLAN_ROLLOUT_PERSIST", persist)
+    ctx = mp.make_plan_context(services_of(g), store_of(g), mp.PartitionRuleSet.defaults())
+    r = mp.rollouts(mp.zero_completion(ctx.n), ctx, mp.RolloutParams(**g["params"]), lengths=True)
+    assert r.lengths == g["lengths"]
+    assert (r.best_len, r.best_id, r.keys, r.rounds, r.steps) == (g["best_len"], g["best_id"], g["keys"], g["rounds"], g["steps"])
+    assert S.plan_key([ctx.pool[i].config for i in r.path]) == g["path"]
