@@ -299,6 +299,7 @@ struct RolloutArgs {
     unsigned* rslot;        // n_roll: key-cache slot of the current key
     long long* act0;        // active lists (ping-pong)
     long long* act1;
+    uint64_t* keys;         // n <= 64: n_roll type keys (the unsatisfied bitmap), kept per rollout
     // key cache (RolloutCache, mcts.hpp:47-50): open addressing over the unsat bitmap
     unsigned tab_mask;      // capacity - 1 (power of two)
     unsigned* tag;          // 0 empty, 1 key being written, 2 key ready

@@ -17,6 +17,25 @@
 
 namespace mgb {
 
+namespace {
+// MIGPLAN_HOST_TIMERS=1: host-side split of the grouped launches (set-up / launch to sync / after)
+struct HostTimer {
+    bool on = std::getenv("MIGPLAN_HOST_TIMERS") != nullptr;
+    std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now(), t = t0;
+    double parts[4] = {0, 0, 0, 0};
+    void mark(int k) {
+        if (!on) return;
+        const auto now = std::chrono::steady_clock::now();
+        parts[k] += std::chrono::duration<double, std::micro>(now - t).count();
+        t = now;
+    }
+    void print(const char* what) const {
+        if (on) std::fprintf(stderr, "[host] %-14s set-up %.1f us, launch->sync %.1f us, after %.1f us\n", what, parts[0], parts[1], parts[2]);
+    }
+};
+}  // namespace
+
+
 size_t greedy_smem_bytes(int n, int PP, int cache_units, int stages);
 size_t topk_smem_bytes(int n, int PP);
 const void* greedy_kernel_ptr();
@@ -1187,6 +1206,7 @@ RolloutResult Engine::rollouts(const std::vector<double>& comp, long long n_roll
     a.rslot = static_cast<unsigned*>(alloc(sizeof(unsigned) * batch));
     a.act0 = static_cast<long long*>(alloc(sizeof(long long) * batch));
     a.act1 = static_cast<long long*>(alloc(sizeof(long long) * batch));
+    a.keys = n <= 64 ? static_cast<uint64_t*>(alloc(sizeof(uint64_t) * batch)) : nullptr;
     a.cnt = static_cast<RolloutCounters*>(alloc(sizeof(RolloutCounters)));
     a.path = hpath;
     a.path_len = &ho->path_len;
@@ -1358,6 +1378,11 @@ void Engine::greedy_batch(const double* d_comps, int count, long long cap_steps,
     if (n_ranks_ > 1) throw ArgumentError("greedy_batch on a sharded context");
     const int T = kernel_threads();
     const size_t smem = greedy_smem_bytes(m_.n, m_.PP, cache_units_, ring_stages_);
+    HostTimer ht;
+    struct PrintT {
+        HostTimer& h;
+        ~PrintT() { h.print("greedy batch"); }
+    } pt{ht};
     for (int b0 = 0; b0 < count; b0 += kMaxGroups) {
         const int nb = std::min(kMaxGroups, count - b0);
         std::vector<GreedyCall> calls(nb);
@@ -1389,10 +1414,12 @@ void Engine::greedy_batch(const double* d_comps, int count, long long cap_steps,
         }
         Slot* s0 = calls[0].s;
         CK(cudaEventRecord(s0->e0, s0->stream));
+        ht.mark(0);
         launch_greedy(*L, T, smem, s0->stream);
         stats.launches++;
         CK(cudaEventRecord(s0->e1, s0->stream));
         CK(cudaStreamSynchronize(s0->stream));
+        ht.mark(1);
         float ms = 0.f;
         CK(cudaEventElapsedTime(&ms, s0->e0, s0->e1));
         stats.greedy_ns += static_cast<long long>(ms * 1e6f);
@@ -1421,6 +1448,7 @@ void Engine::greedy_batch(const double* d_comps, int count, long long cap_steps,
                 x.e->release(x.s);
             x.s = nullptr;
         }
+        ht.mark(2);
     }
 }
 
@@ -1443,6 +1471,11 @@ std::vector<MctsDeviceResult> Engine::mcts_device_group(const std::vector<std::v
     const int count = static_cast<int>(comps.size());
     std::vector<MctsDeviceResult> results(count);
     CK(cudaSetDevice(device_));
+    HostTimer ht;
+    struct PrintT {
+        HostTimer& h;
+        ~PrintT() { h.print("mcts group"); }
+    } pt{ht};
     for (int b0 = 0; b0 < count; b0 += kMaxGroups) {
         const int nb = std::min(kMaxGroups, count - b0);
         std::vector<Slot*> slots;
@@ -1607,6 +1640,7 @@ std::vector<MctsDeviceResult> Engine::mcts_device_group(const std::vector<std::v
         }
         Slot* s0 = slots[0];
         void* args[] = {L.get()};
+        ht.mark(0);
         CK(cudaEventRecord(s0->e0, s0->stream));
         {
             cudaLaunchConfig_t cfg{};
@@ -1631,6 +1665,7 @@ std::vector<MctsDeviceResult> Engine::mcts_device_group(const std::vector<std::v
                                o.out + sizeof(int) * 32 - o.trace, cudaMemcpyDeviceToHost, s0->stream));
         }
         CK(cudaStreamSynchronize(s0->stream));
+        ht.mark(1);
         float ms = 0.f;
         CK(cudaEventElapsedTime(&ms, s0->e0, s0->e1));
         stats.mcts_ns += static_cast<long long>(ms * 1e6);
@@ -1686,6 +1721,7 @@ std::vector<MctsDeviceResult> Engine::mcts_device_group(const std::vector<std::v
             stats.h2d += static_cast<long long>(sizeof(double) * n);
             stats.d2h += static_cast<long long>(hb_size);
         }
+        ht.mark(2);
     }
     return results;
 }

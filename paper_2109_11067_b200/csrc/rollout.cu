@@ -43,10 +43,6 @@ constexpr int kAThreads = 256;  // advance kernel: small blocks, register-lean, 
 #define MGB_ROLLOUT_AOCC 6
 #endif
 constexpr int kAOcc = MGB_ROLLOUT_AOCC;
-#ifndef MGB_ROLL_LANES
-#define MGB_ROLL_LANES 4
-#endif
-constexpr int kRollLanes = MGB_ROLL_LANES;  // lanes per rollout when n <= 64 (4: eight per warp; A/B profiles/r02l_ab_rollout_lanes.txt)
 
 __device__ __forceinline__ uint64_t mix64(uint64_t z) {
     z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
@@ -346,135 +342,106 @@ struct Advancer {
     }
 };
 
-// n <= 64: a HALF-warp per rollout (16 lanes x 4 completion slots), two rollouts per warp
-// (HL = 8: a quarter-warp, four per warp).
-// The per-step work is mostly uniform within a rollout (Philox draw, cache-slot and pool
-// lookups, the probe), so two halves issuing it together halve the instructions per rollout
-// step and double the dependent load chains in flight (the advance kernel is issue-bound:
-// 62% of issue slots at a warp per rollout, profiles/r02l_roll_adv_ncu.json).
-template <int HL>
-struct AdvancerH {  // HL lanes per rollout, 64 / HL completion slots per lane (n <= 64)
-    static constexpr int S = 64 / HL, R = 32 / HL;
-    const RolloutArgs& a;
-    long long* wb;
-    unsigned long long *c_steps, *c_done, *c_cap, *c_fail;
-    int lane, nxt, nbuf = 0;
-
-    __device__ void push_flush() {
-        if (nbuf && lane == 0) {
-            const unsigned long long at = atomicAdd(&a.cnt->n_act[nxt], static_cast<unsigned long long>(nbuf));
-            for (int i = 0; i < nbuf; ++i) (nxt ? a.act1 : a.act0)[at + i] = wb[i];
+// n <= 64: ONE LANE per rollout.  The rollout's type key (completion_type_key, mcts.hpp:38-43)
+// is kept beside its completion vector, and a step touches only the <= 4 services of the picked
+// config: their completions are read, the utilities added (mcts.hpp:139), their key bits
+// updated (a completion only grows, so a bit only clears) — the other n - 4 completions are
+// neither read nor written.  A warp advances 32 rollouts at once; the next round's active list
+// takes one atomic per warp.  Same draws, pools and schedule as the lane-group steppers.
+__device__ void advance_lane_step(const RolloutArgs& a, long long r, bool valid, bool first, int nxt,
+                                  unsigned long long* cnt4) {
+    const DevModel& M = a.M;
+    const int n = M.n;
+    RolloutCounters* C = a.cnt;
+    const int lane = static_cast<int>(threadIdx.x & 31u);
+    bool active = valid;
+    int L = 0;
+    uint64_t key = 0;
+    if (valid && first) {  // a new rollout: the start completion and its key
+        for (int i = 0; i < n; ++i) {
+            const double v = a.comp0[i];
+            a.comp[r * n + i] = v;
+            if (v < 1.0 - 1e-9) key |= 1ull << i;
         }
-        __syncwarp();
-        nbuf = 0;
-    }
-
-    // both halves call this together (warp-collective); `valid`: this half holds rollout r
-    __device__ void step(long long r, bool valid, bool first) {
-        const DevModel& M = a.M;
-        const int n = M.n;
-        RolloutCounters* C = a.cnt;
-        const int half = lane / HL, hl = lane % HL;
-        double c[S];
-        const double* src = first ? a.comp0 : a.comp + r * n;
-#pragma unroll
-        for (int j = 0; j < S; ++j) c[j] = (valid && hl + HL * j < n) ? src[hl + HL * j] : 2.0;
-        bool active = valid;
-        int L = 0;
-        unsigned dirty = first ? ~0u : 0u;  // a new rollout writes every slot
-        if (valid && !first) {
-            L = a.len[r];
-            const unsigned slot = a.rslot[r];
-            const int pn = __ldcg(&a.pool_n[slot]);
-            if (pn <= 0) {  // rollout: "no candidate config serves the remaining demand" (mcts.hpp:135-136)
-                if (hl == 0) {
-                    a.status[r] = 3;
-                    if (a.lengths) a.lengths[r] = -1;
-                    atomicAdd(c_fail, 1ull);
-                }
-                active = false;
-            } else {
-                const uint64_t x = philox_u64(a.seed, static_cast<uint64_t>(a.id0 + r), static_cast<uint64_t>(L));
-                const unsigned pick = __ldcg(&a.pool[static_cast<size_t>(slot) * a.k + philox_below(x, pn)]);
-                const uint64_t row = __ldg(a.base + pick);
-#pragma unroll
-                for (int m = 0; m < 4; ++m) {  // add_util (mcts.hpp:139) in the owning lanes
-                    const unsigned code = static_cast<unsigned>((row >> (16 * m)) & 0xFFFFull);
-                    const int svc = svc_of(M, code);
-                    if (svc < n && (svc % HL) == hl) {
-                        const double u = __ldg(&M.U[code]);
-#pragma unroll
-                        for (int j = 0; j < S; ++j)
-                            if ((svc / HL) == j) c[j] = __dadd_rn(c[j], u), dirty |= 1u << j;
-                    }
-                }
-                ++L;
-                if (hl == 0) {
-                    a.len[r] = L;
-                    atomicAdd(c_steps, 1ull);
-                }
-            }
-        }
-        if (first && valid && hl == 0) a.len[r] = 0;
-        uint64_t kw[4] = {0, 0, 0, 0};  // completion_type_key (mcts.hpp:38-43), this half's bitmap
-#pragma unroll
-        for (int j = 0; j < S; ++j) {
-            if (HL * j >= n) break;
-            const unsigned b = __ballot_sync(0xffffffffu, hl + HL * j < n && c[j] < 1.0 - 1e-9);
-            kw[0] |= static_cast<uint64_t>((b >> (HL * half)) & ((1u << HL) - 1u)) << (HL * j);
-        }
-        if (active && kw[0] == 0) {  // satisfied
-            if (hl == 0) {
-                a.status[r] = 1;
-                if (a.lengths) a.lengths[r] = L;
-                atomicMin(&C->best, (static_cast<unsigned long long>(L) << 32) | static_cast<unsigned long long>(r));
-                atomicAdd(c_done, 1ull);
-            }
+        a.len[r] = 0;
+    } else if (valid) {
+        L = a.len[r];
+        key = a.keys[r];
+        const unsigned slot = a.rslot[r];
+        const int pn = __ldcg(&a.pool_n[slot]);
+        if (pn <= 0) {  // rollout: "no candidate config serves the remaining demand" (mcts.hpp:135-136)
+            a.status[r] = 3;
+            if (a.lengths) a.lengths[r] = -1;
             active = false;
-        }
-        if (active && L >= a.max_depth) {  // rollout returns max_depth (mcts.hpp:127)
-            if (hl == 0) {
-                a.status[r] = 2;
-                if (a.lengths) a.lengths[r] = a.max_depth;
-                atomicAdd(c_cap, 1ull);
-            }
-            active = false;
-        }
-        if (active) {
+        } else {
+            const uint64_t x = philox_u64(a.seed, static_cast<uint64_t>(a.id0 + r), static_cast<uint64_t>(L));
+            const unsigned pick = __ldcg(&a.pool[static_cast<size_t>(slot) * a.k + philox_below(x, pn)]);
+            const uint64_t row = __ldg(a.base + pick);
+            double* cr = a.comp + r * n;
 #pragma unroll
-            for (int j = 0; j < S; ++j)
-                if (hl + HL * j < n && ((dirty >> j) & 1u)) a.comp[r * n + hl + HL * j] = c[j];
-        }
-        if (active && hl == 0) {
-            bool created = false;
-            long long slot = probe(a, kw, 1, true, created);
-            if (slot < 0) {
-                atomicExch(&C->status, 1);
-                slot = 0;
-            } else {
-                if (created) {
-                    const unsigned long long at = atomicAdd(&C->n_pend[nxt], 1ull);
-                    (nxt ? a.pend1 : a.pend0)[at] = static_cast<unsigned>(slot);
+            for (int m = 0; m < 4; ++m) {  // distinct services: the adds commute
+                const unsigned code = static_cast<unsigned>((row >> (16 * m)) & 0xFFFFull);
+                const int svc = svc_of(M, code);
+                if (svc < n) {
+                    const double v = __dadd_rn(cr[svc], __ldg(&M.U[code]));
+                    cr[svc] = v;
+                    if (!(v < 1.0 - 1e-9)) key &= ~(1ull << svc);
                 }
-                if (__ldcg(&a.pool_n[slot]) < 0 && __ldcg(&a.claimer[slot]) > static_cast<unsigned long long>(r))
-                    atomicMin(&a.claimer[slot], static_cast<unsigned long long>(r));
             }
-            a.rslot[r] = static_cast<unsigned>(slot);
+            ++L;
+            a.len[r] = L;
         }
-        // the next round's active list: the warp's buffer takes up to R entries
-        const unsigned pm = __ballot_sync(0xffffffffu, active && hl == 0);  // bit HL*q: rollout q continues
-#pragma unroll
-        for (int q = 0; q < R; ++q) {
-            const long long rq = __shfl_sync(0xffffffffu, r, HL * q);
-            if (lane == 0 && ((pm >> (HL * q)) & 1u)) wb[nbuf + __popc(pm & ((1u << (HL * q)) - 1u))] = rq;
-        }
-        nbuf += __popc(pm);
-        if (nbuf > 32 - R) push_flush();
     }
-};
+    const bool stepped = valid && !first && active;
+    bool sat = false, cap = false;
+    if (active && key == 0) {  // satisfied
+        a.status[r] = 1;
+        if (a.lengths) a.lengths[r] = L;
+        atomicMin(&C->best, (static_cast<unsigned long long>(L) << 32) | static_cast<unsigned long long>(r));
+        sat = true;
+        active = false;
+    }
+    if (active && L >= a.max_depth) {  // rollout returns max_depth (mcts.hpp:127)
+        a.status[r] = 2;
+        if (a.lengths) a.lengths[r] = a.max_depth;
+        cap = true;
+        active = false;
+    }
+    if (active) {
+        a.keys[r] = key;
+        bool created = false;
+        long long slot = probe(a, &key, 1, true, created);
+        if (slot < 0) {
+            atomicExch(&C->status, 1);
+            slot = 0;
+        } else {
+            if (created) {
+                const unsigned long long at = atomicAdd(&C->n_pend[nxt], 1ull);
+                (nxt ? a.pend1 : a.pend0)[at] = static_cast<unsigned>(slot);
+            }
+            if (__ldcg(&a.pool_n[slot]) < 0 && __ldcg(&a.claimer[slot]) > static_cast<unsigned long long>(r))
+                atomicMin(&a.claimer[slot], static_cast<unsigned long long>(r));
+        }
+        a.rslot[r] = static_cast<unsigned>(slot);
+    }
+    // counters and the next round's active list: one shared/global atomic per warp
+    const unsigned bs = __ballot_sync(0xffffffffu, stepped), bd = __ballot_sync(0xffffffffu, sat),
+                   bc = __ballot_sync(0xffffffffu, cap), bf = __ballot_sync(0xffffffffu, valid && !first && !stepped),
+                   ba = __ballot_sync(0xffffffffu, active);
+    if (lane == 0) {
+        if (bs) atomicAdd(&cnt4[0], static_cast<unsigned long long>(__popc(bs)));
+        if (bd) atomicAdd(&cnt4[1], static_cast<unsigned long long>(__popc(bd)));
+        if (bc) atomicAdd(&cnt4[2], static_cast<unsigned long long>(__popc(bc)));
+        if (bf) atomicAdd(&cnt4[3], static_cast<unsigned long long>(__popc(bf)));
+    }
+    unsigned long long at = 0;
+    if (lane == 0 && ba) at = atomicAdd(&C->n_act[nxt], static_cast<unsigned long long>(__popc(ba)));
+    at = __shfl_sync(0xffffffffu, at, 0);
+    if (active) (nxt ? a.act1 : a.act0)[at + __popc(ba & ((1u << lane) - 1u))] = r;
+}
 
 // One advance pass of a block over the active list (or, first, over every rollout): a warp
-// per rollout (n > 64) or kRollLanes lanes per rollout (n <= 64).  Block-level counters are
+// per rollout (n > 64) or one lane per rollout (n <= 64, advance_lane_step).  Block-level counters are
 // summed into the launch's RolloutCounters at the end.  Ends with a barrier.
 template <int J, int NT>
 __device__ void advance_pass(const RolloutArgs& a, bool first, int cur, unsigned long long n_act, long long (*wbuf)[32],
@@ -486,16 +453,13 @@ __device__ void advance_pass(const RolloutArgs& a, bool first, int cur, unsigned
     const long long gw = static_cast<long long>(blockIdx.x) * (NT / 32) + warp;
     const long long nwarps = static_cast<long long>(gridDim.x) * (NT / 32);
     const long long* act = cur ? a.act1 : a.act0;
-    if constexpr (J == 2) {  // n <= 64: several rollouts per warp
-        using Adv = AdvancerH<kRollLanes>;
-        Adv adv{a, wbuf[warp], &cnt4[0], &cnt4[1], &cnt4[2], &cnt4[3], static_cast<int>(threadIdx.x & 31u), cur ^ 1};
-        const int half = static_cast<int>((threadIdx.x & 31u) / kRollLanes);
-        for (long long i0 = Adv::R * gw; i0 < static_cast<long long>(n_act); i0 += Adv::R * nwarps) {
-            const long long i = i0 + half;
+    if constexpr (J == 2) {  // n <= 64: a lane per rollout
+        const int lane = static_cast<int>(threadIdx.x & 31u);
+        for (long long i0 = 32 * gw; i0 < static_cast<long long>(n_act); i0 += 32 * nwarps) {
+            const long long i = i0 + lane;
             const bool valid = i < static_cast<long long>(n_act);
-            adv.step(valid ? (first ? i : __ldcg(&act[i])) : 0, valid, first);
+            advance_lane_step(a, valid ? (first ? i : __ldcg(&act[i])) : 0, valid, first, cur ^ 1, cnt4);
         }
-        adv.push_flush();
     } else {
         Advancer<J> adv{a, wbuf[warp], &cnt4[0], &cnt4[1], &cnt4[2], &cnt4[3], static_cast<int>(threadIdx.x & 31u),
                         (a.M.n + 63) / 64, cur ^ 1};
@@ -682,7 +646,7 @@ const void* rollout_persistent_ptr(int n) {
     return n <= 64 ? reinterpret_cast<const void*>(&rollout_persistent_kernel<2>)
                    : reinterpret_cast<const void*>(&rollout_persistent_kernel<kMaxJ>);
 }
-int rollout_per_warp(int n) { return n <= 64 ? 32 / kRollLanes : 1; }
+int rollout_per_warp(int n) { return n <= 64 ? 32 : 1; }
 const void* rollout_replay_ptr(int n) {
     return n <= 64 ? reinterpret_cast<const void*>(&rollout_replay_kernel<2>)
                    : reinterpret_cast<const void*>(&rollout_replay_kernel<kMaxJ>);
