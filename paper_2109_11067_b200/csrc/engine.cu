@@ -71,6 +71,7 @@ const void* rollout_advance_ptr(int n);
 const void* rollout_replay_ptr(int n);
 const void* rollout_persistent_ptr(int n);
 int rollout_per_warp(int n);
+void rollout_set_dense_pct(int pct);
 int rollout_threads();
 int rollout_advance_threads();
 
@@ -1199,7 +1200,8 @@ RolloutResult Engine::rollouts(const std::vector<double>& comp, long long n_roll
     a.seed = seed;
     a.k = k;
     a.max_depth = max_depth;
-    a.timers = std::getenv("MIGPLAN_ROLLOUT_TIMERS") ? 1 : 0;
+    a.timers = 0;
+    if (const char* v = std::getenv("MIGPLAN_ROLLOUT_DENSE_PCT")) rollout_set_dense_pct(std::atoi(v));  // A/B
     a.comp = static_cast<double*>(alloc(sizeof(double) * n * batch));
     a.len = static_cast<int*>(alloc(sizeof(int) * batch));
     a.status = static_cast<uint8_t*>(alloc(batch));

@@ -25,6 +25,7 @@
 
 #include "common.cuh"
 #include "philox.cuh"
+#define MGB_TOPK_DENSE_PCT 100  // A/B (MIGPLAN_ROLLOUT_DENSE_PCT): by-support scans for every build
 #include "topk_pair.cuh"
 
 namespace mgb {
@@ -652,6 +653,7 @@ const void* rollout_replay_ptr(int n) {
                    : reinterpret_cast<const void*>(&rollout_replay_kernel<kMaxJ>);
 }
 int rollout_threads() { return kRThreads; }
+void rollout_set_dense_pct(int pct) { cudaMemcpyToSymbol(g_mcts_dense_pct, &pct, sizeof pct); }  // this TU's copy
 int rollout_advance_threads() { return kAThreads; }
 
 namespace {

@@ -84,7 +84,10 @@ __shared__ long long tp_c0, tp_dmax, tp_dmin, tp_dsum;  // development aid: warp
 __device__ __forceinline__ void topk_pair_counters_init() {
     if (threadIdx.x == 0) tp_ncand = tp_nhit = tp_nact = tp_actrows = 0;
 }
-__device__ int g_mcts_dense_pct = 60;  // dense scan when live rows exceed this % of the pool
+#ifndef MGB_TOPK_DENSE_PCT
+#define MGB_TOPK_DENSE_PCT 60  // K7 (rows on chip); rollout.cu's pool builds (rows in L2) use 100
+#endif
+__device__ int g_mcts_dense_pct = MGB_TOPK_DENSE_PCT;  // dense scan when live rows exceed this % of the pool
 
 // Inlined into mcts_kernel: as a call, the ABI's register saves around each call site pushed
 // the 128-register kernel into spilling on the search's serial paths (measured: the GA
