@@ -285,6 +285,11 @@ Engine::Engine(const Rules& rules, std::map<std::string, ModelProfile> profiles,
     };
     dm_.n = m_.n;
     dm_.PP = m_.PP;
+    gk_.phase_timers = std::getenv("MIGPLAN_PHASE_TIMERS") ? 1 : 0;
+    if (const char* e = std::getenv("MIGPLAN_PREFETCH")) gk_.prefetch = std::atoi(e);
+    if (const char* e = std::getenv("MIGPLAN_PIPE")) gk_.pipeline = std::atoi(e);
+    if (const char* e = std::getenv("MIGPLAN_LOAD_MODE")) gk_.load_mode = std::atoi(e);
+    if (const char* e = std::getenv("MIGPLAN_EXCH_TIMEOUT_MS")) gk_.exch_timeout_ns = std::atoll(e) * 1'000'000ll;
     dm_.pp_magic = m_.PP > 1 ? static_cast<unsigned>(((1ull << 32) + static_cast<unsigned long long>(m_.PP) - 1) /
                                                      static_cast<unsigned long long>(m_.PP))
                              : 0u;
@@ -706,7 +711,7 @@ struct GreedyCall {
 };
 
 void Engine::greedy_prepare(GreedyCall& c, const double* comp_host, const double* comp_dev, long long cap_steps,
-                            cudaStream_t st) {
+                            cudaStream_t st, bool defer_init) {
     Slot* s = c.s;
     if (!st) st = s->stream;
     CK(cudaSetDevice(device_));
@@ -726,9 +731,11 @@ void Engine::greedy_prepare(GreedyCall& c, const double* comp_host, const double
     // capped at 3G rows (24 GB); the kernel reports overflow and the call is retried larger.
     ensure_ext(s, c.n_base + std::min<long long>(ext_bound_, 3ll << 30));
     if (comp_host) std::memcpy(s->io->comp, comp_host, sizeof(double) * m_.n);
-    CK(cudaMemsetAsync(s->st, 0, sizeof(GreedyState), st));
-    // the working-set arena starts as a copy of the resident base pool (device to device)
-    if (c.n_base) CK(cudaMemcpyAsync(s->ext, c.base_src, c.n_base * 8, cudaMemcpyDeviceToDevice, st));
+    if (!defer_init) {  // (greedy_batch: one launch_greedy_batch_init for every instance instead)
+        CK(cudaMemsetAsync(s->st, 0, sizeof(GreedyState), st));
+        // the working-set arena starts as a copy of the resident base pool (device to device)
+        if (c.n_base) CK(cudaMemcpyAsync(s->ext, c.base_src, c.n_base * 8, cudaMemcpyDeviceToDevice, st));
+    }
     GreedyArgs& a = c.a;
     a = GreedyArgs{};
     a.M = dm_;
@@ -737,13 +744,10 @@ void Engine::greedy_prepare(GreedyCall& c, const double* comp_host, const double
     a.cap = s->ext_cap;
     a.cache_units = cache_units_;
     a.ring_stages = ring_stages_;
-    a.phase_timers = std::getenv("MIGPLAN_PHASE_TIMERS") ? 1 : 0;
-    a.prefetch = 4;
-    if (const char* e = std::getenv("MIGPLAN_PREFETCH")) a.prefetch = std::atoi(e);
-    a.pipeline = 1;  // software-pipelined streaming loads (MIGPLAN_PIPE=0: off)
-    if (const char* e = std::getenv("MIGPLAN_PIPE")) a.pipeline = std::atoi(e);
-    a.load_mode = 2;  // ld.global.cs: measured best for the streaming scan (profiles/)
-    if (const char* e = std::getenv("MIGPLAN_LOAD_MODE")) a.load_mode = std::atoi(e);
+    a.phase_timers = gk_.phase_timers;
+    a.prefetch = gk_.prefetch;
+    a.pipeline = gk_.pipeline;  // software-pipelined streaming loads (MIGPLAN_PIPE=0: off)
+    a.load_mode = gk_.load_mode;  // ld.global.cs: measured best for the streaming scan (profiles/)
     a.comp0 = comp_host ? s->io->comp : comp_dev;
     a.st = s->st;
     a.out = &s->io->res;
@@ -760,8 +764,7 @@ void Engine::greedy_prepare(GreedyCall& c, const double* comp_host, const double
     a.rank = rank_;
     for (int q = 0; q < n_ranks_ && n_ranks_ > 1; ++q) a.boards[q] = static_cast<ExchSlot*>(boards_[q]);
     a.exch_seq0 = exch_seq_;
-    a.exch_timeout_ns = 10'000'000'000ll;
-    if (const char* e = std::getenv("MIGPLAN_EXCH_TIMEOUT_MS")) a.exch_timeout_ns = std::atoll(e) * 1'000'000ll;
+    a.exch_timeout_ns = gk_.exch_timeout_ns;
 }
 
 // Returns false when the arena overflowed and was grown (the caller relaunches).
@@ -812,6 +815,7 @@ bool Engine::greedy_finish(GreedyCall& c, float ms, int attempt, std::vector<uin
 // Greedy launch: cooperative (grid-wide barriers over every SM) or, for small working sets,
 // one thread-block cluster per instance (DSMEM argmax and cluster barriers: a step costs a
 // few microseconds instead of a grid-wide barrier over 148 CTAs).
+void launch_greedy_batch_init(const GreedyLaunch& L, const uint64_t* base, long long n_base, cudaStream_t st);
 void launch_greedy(const GreedyLaunch& L, int T, size_t smem, cudaStream_t st) {
     void* args[] = {const_cast<GreedyLaunch*>(&L)};
     if (!L.cluster) {
@@ -1410,11 +1414,14 @@ void Engine::greedy_batch(const double* d_comps, int count, long long cap_steps,
             // host completions go through each slot's host-mapped input (no staging copy)
             greedy_prepare(calls[i], h_comps ? h_comps + static_cast<size_t>(b0 + i) * m_.n : nullptr,
                            h_comps ? nullptr : d_comps + static_cast<size_t>(b0 + i) * m_.n, cap_steps,
-                           calls[0].s->stream);
+                           calls[0].s->stream, true);
             calls[i].a.interleave = greedy_interleave(gpc);
             L->g[i] = calls[i].a;
         }
         Slot* s0 = calls[0].s;
+        launch_greedy_batch_init(*L, calls[0].base_src, calls[0].n_base, s0->stream);  // states + arenas
+        CK(cudaGetLastError());
+        stats.launches++;
         CK(cudaEventRecord(s0->e0, s0->stream));
         ht.mark(0);
         launch_greedy(*L, T, smem, s0->stream);
@@ -1566,12 +1573,11 @@ std::vector<MctsDeviceResult> Engine::mcts_device_group(const std::vector<std::v
                 CK(cudaMallocHost(&s->mcts_host, hb_bytes));
                 s->mcts_host_bytes = hb_bytes;
             }
-            cudaStream_t ls = slots[0]->stream;  // every search's set-up on the launch stream
+            // the kernel reads its start completion from the pinned staging (mapped) and zeroes its
+            // own cache tags: no per-search copy or memset enqueued
             std::memcpy(s->mcts_host, comps[b0 + q].data(), sizeof(double) * n);
-            CK(cudaMemcpyAsync(b + o.comp0, s->mcts_host, sizeof(double) * n, cudaMemcpyHostToDevice, ls));
-            CK(cudaMemsetAsync(b + o.tag, 0, sizeof(unsigned) * cap, ls));
             MctsSolveArgs& a = L->s[q];
-            a.comp0 = reinterpret_cast<const double*>(b + o.comp0);
+            a.comp0 = reinterpret_cast<const double*>(s->mcts_host);
             a.seed = mix_seed_u64(seeds[b0 + q], 0x6d637473);
             a.l_ref = l_ref;
             a.max_nodes = static_cast<int>(max_nodes);

@@ -214,7 +214,13 @@ class Engine {
     void ensure_ext(Slot* s, long long rows);
     long long step_bound(const std::vector<double>& comp) const;
     void greedy_prepare(GreedyCall& c, const double* comp_host, const double* comp_dev, long long cap_steps,
-                        cudaStream_t st = nullptr);
+                        cudaStream_t st = nullptr, bool defer_init = false);
+    // environment knobs of greedy_prepare, read once per context (greedy_prepare ran five
+    // getenv calls per instance)
+    struct GreedyKnobs {
+        int phase_timers = 0, prefetch = 4, pipeline = 1, load_mode = 2;
+        long long exch_timeout_ns = 10'000'000'000ll;
+    } gk_;
     bool greedy_finish(GreedyCall& c, float ms, int attempt, std::vector<uint64_t>& rows, std::vector<double>& scores);
 
     Model m_;

@@ -1104,6 +1104,23 @@ int greedy_chunk_bytes() { return kStageUnits * 16; }
 size_t topk_smem_bytes(int n, int PP) { return static_cast<size_t>((n + 1) * PP + n) * 8 + 16; }
 
 const void* greedy_kernel_ptr() { return reinterpret_cast<const void*>(&greedy_kernel<kThreads>); }
+
+// Set-up of a grouped greedy launch in ONE kernel (blockIdx.y = instance): each instance's
+// GreedyState zeroed and its arena seeded with the base pool — instead of a memset and a
+// device-to-device copy enqueued per instance (host API time dominated the GA refills' set-up).
+__global__ void greedy_batch_init_kernel(const __grid_constant__ GreedyLaunch GL, const uint64_t* base, long long n_base) {
+    const GreedyArgs& a = GL.g[blockIdx.y];
+    if (blockIdx.x == 0)
+        for (int i = threadIdx.x; i < static_cast<int>(sizeof(GreedyState)); i += blockDim.x)
+            reinterpret_cast<unsigned char*>(a.st)[i] = 0;
+    for (long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; i < n_base;
+         i += static_cast<long long>(gridDim.x) * blockDim.x)
+        a.rows[i] = base[i];
+}
+void launch_greedy_batch_init(const GreedyLaunch& L, const uint64_t* base, long long n_base, cudaStream_t st) {
+    const int bx = static_cast<int>(std::min<long long>(64, std::max<long long>(1, (n_base + 255) / 256)));
+    greedy_batch_init_kernel<<<dim3(bx, L.n_groups), 256, 0, st>>>(L, base, n_base);
+}
 const void* topk_kernel_ptr() { return reinterpret_cast<const void*>(&topk_kernel); }
 const void* enum_base_kernel_ptr() { return reinterpret_cast<const void*>(&enum_base_kernel); }
 int kernel_threads() { return kThreads; }

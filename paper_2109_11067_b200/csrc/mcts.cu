@@ -657,7 +657,8 @@ __global__ void __launch_bounds__(kMThreads, 1) mcts_kernel(const __grid_constan
         nfirst[0] = 0;
         ncand[0] = -1;
     }
-    for (int i = tid; i < n; i += blockDim.x) a.node_comp[i] = a.comp0[i];
+    for (int i = tid; i < n; i += blockDim.x) a.node_comp[i] = a.comp0[i];  // pinned host staging (mapped)
+    for (unsigned i = tid; i <= a.tab_mask; i += blockDim.x) a.tag[i] = 0;    // the global rollout-cache level
     __syncthreads();
     if (tid == 0) nflags[0] = comp_satisfied(a.node_comp, n) ? kLeaf : 0;
     __syncthreads();
