@@ -572,11 +572,18 @@ def main():
     mp.release_device_cache(local)
     cold = {}
 
+    e2e_host = []  # per e2e step: host wall of context build, plan call, close (ms)
+
     def e2e_step():
+        t0 = time.perf_counter()
         c2, b2 = make_ctx()
+        t1 = time.perf_counter()
         p = step(c2)
+        t2 = time.perf_counter()
         s2 = c2.stats()
         close_ctx(c2, b2)
+        t3 = time.perf_counter()
+        e2e_host.append([round(1e3 * (t1 - t0), 2), round(1e3 * (t2 - t1), 2), round(1e3 * (t3 - t2), 2)])
         return p, s2
 
     (_, s_cold), cold_ms = timed(e2e_step, flush, torch)
@@ -650,7 +657,7 @@ def main():
             "e2e": {"value": e2e_rows_all / (e2e_ms_max / 1e3), "unit": "configs/s",
                     "h2d_bytes_per_step": h2d // e2e_steps, "d2h_bytes_per_step": d2h // e2e_steps,
                     "ms_per_step": e2e_ms_max / e2e_steps, "steps": e2e_steps, "step_ms_rank0": e2e_list,
-                    "kernel_ms_rank0": e2e_kern, "clocks": e2e_clock, **cold},
+                    "kernel_ms_rank0": e2e_kern, "host_ctx_plan_close_ms_rank0": e2e_host, "clocks": e2e_clock, **cold},
             "gpu_launches": st["kernel_launches"],
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                          "traffic": traffic, "traffic_source": traffic_src, "kernel": dom,

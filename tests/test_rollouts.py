@@ -134,3 +134,28 @@ def test_rollout_launch_modes_match_golden(name, persist, monkeypatch):
     assert r.lengths == g["lengths"]
     assert (r.best_len, r.best_id, r.keys, r.rounds, r.steps) == (g["best_len"], g["best_id"], g["keys"], g["rounds"], g["steps"])
     assert S.plan_key([ctx.pool[i].config for i in r.path]) == g["path"]
+
+
+@pytest.mark.gpu
+def test_rollouts_wide_services_modes_agree():
+    """n > 64 services: the warp-per-rollout stepper (rollout.cu Advancer<8>, the type key over
+    several 64-bit words) gives the same rollouts in both launch modes, and the winner's path is
+    a plan that satisfies every service.  (The CPU restatement takes minutes at this size; the
+    n <= 64 goldens pin the schedule itself.)"""
+    import os
+    ps, sv = S.gen(72, 5.0, seed=7)
+    prm = mp.RolloutParams(n_rollouts=2048, seed=11, topk=6)
+    runs = []
+    for persist in ("1", "0"):
+        os.environ["MIGPLAN_ROLLOUT_PERSIST"] = persist
+        try:
+            ctx = mp.make_plan_context(sv, ps, mp.PartitionRuleSet.defaults())
+            runs.append((ctx, mp.rollouts(mp.zero_completion(len(sv)), ctx, prm, lengths=True)))
+        finally:
+            del os.environ["MIGPLAN_ROLLOUT_PERSIST"]
+    (c0, a), (c1, b) = runs
+    assert a.lengths == b.lengths and a.completed == b.completed == 2048
+    assert (a.best_len, a.best_id, a.keys, a.rounds, a.steps) == (b.best_len, b.best_id, b.keys, b.rounds, b.steps)
+    path = [c0.pool[i].config for i in a.path]
+    assert len(path) == a.best_len == min(a.lengths)
+    assert mp.is_satisfied(mp.completion_of(path, sv, ps))
