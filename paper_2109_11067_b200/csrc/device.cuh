@@ -225,6 +225,7 @@ struct MctsLaunch {
     int rows_smem;           // the base pool copied into shared memory
     int timers;              // accumulate top-K phase cycles (MIGPLAN_MCTS_TIMERS)
     int pair;                // every base row has <= 2 members: on-chip copy as 32-bit rows
+    const unsigned* base32;  // pair pool too large for shared memory: its 32-bit rows in global memory
     // the base pool's supports (K1 order: each a contiguous row range): a top-K scans only the
     // supports that can hold a candidate (a service with need > 0, or a sampled service)
     int n_sup;               // 0: scan every row

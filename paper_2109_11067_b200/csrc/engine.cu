@@ -1625,7 +1625,12 @@ std::vector<MctsDeviceResult> Engine::mcts_device_group(const std::vector<std::v
                 ns = n_sup_;
             }
             L->rows_smem = static_cast<long long>(mcts_smem_bytes(n, m_.PP, mn, slice, false, true, pair, ns)) <= room;
-            if (!(L->rows_smem && pair)) ns = 0;
+            // a pair pool too large for shared memory: the pair top-K reads its 32-bit rows from
+            // global memory (L2), with the support tables still on chip when they fit
+            const bool pair_global = pair && !L->rows_smem && C == 1;
+            L->base32 = pair_global ? base32() : nullptr;
+            const bool sup_fit = static_cast<long long>(mcts_smem_bytes(n, m_.PP, mn, slice, false, L->rows_smem != 0, pair, ns)) <= room;
+            if (!((L->rows_smem && pair) || pair_global) || !sup_fit) ns = 0;
             L->timers = std::getenv("MIGPLAN_MCTS_TIMERS") ? 1 : 0;
             if (const char* v = std::getenv("MIGPLAN_MCTS_DENSE_PCT")) mcts_set_dense_pct(std::atoi(v));
             L->node_smem =

@@ -482,8 +482,11 @@ __global__ void __launch_bounds__(kMThreads, 1) mcts_kernel(const __grid_constan
     const uint64_t* rows = L.base;  // whole pool (rank 0's adds); slice for the top-K scans
     const uint64_t* slice = L.base + lo;
     const unsigned* slice32 = nullptr;  // pair rows: low halves only (L.pair)
-    const bool pair = L.rows_smem && L.pair;
-    if (pair) {
+    // pair top-K over 32-bit rows: on chip when they fit, else from global memory (L.base32)
+    const bool pair = L.pair && (L.rows_smem || (L.base32 && C == 1));
+    if (pair && !L.rows_smem) {
+        slice32 = L.base32 + lo;
+    } else if (pair) {
         unsigned* r = reinterpret_cast<unsigned*>(carve(sizeof(unsigned) * chunk));
         for (long long i = threadIdx.x; i < hi - lo; i += blockDim.x) r[i] = static_cast<unsigned>(__ldg(L.base + lo + i));
         slice32 = r;
