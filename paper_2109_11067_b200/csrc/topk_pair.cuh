@@ -73,6 +73,7 @@ struct SupTab {
     const int* begin;
     const unsigned short* svc;
     int* act;
+    int dense_pct = -1;  // dense scan above this % of live rows (-1: g_mcts_dense_pct)
 };
 
 // block_topk_pair's block-wide counters: zero at kernel start (mcts_kernel) and re-zeroed by
@@ -137,7 +138,7 @@ int block_topk_pair(const DevModel& M, const unsigned* keyrank, const unsigned* 
     }
     // Supports that can hold a candidate: a member with need > 0 (rows of the others all score
     // 0), or, with a mask, a sampled member (every row of such a support touches it).
-    const int dense_pct = g_mcts_dense_pct;
+    const int dense_pct = sup.dense_pct >= 0 ? sup.dense_pct : g_mcts_dense_pct;
     const bool sup_pass = sup.n > 0 && dense_pct < 100;
     if (sup_pass) {
         int hitrows = 0;
