@@ -346,7 +346,10 @@ Engine::Engine(const Rules& rules, std::map<std::string, ModelProfile> profiles,
     const size_t o_kc = put(kcode.data(), kcode.size() * 2), o_ppk = put(ppk.data(), ppk.size() * 4),
                  o_lof = put(lof.data(), lof.size());
     const size_t o_base = (blob.size() + 15) & ~size_t{15};
-    unsigned char* d = dalloc<unsigned char>(dev_allocs_, o_base + (static_cast<size_t>(total) + 2) * 8);
+    // from the process-wide scratch pool: closing a context hands it back instead of cudaFree
+    // (measured: a cudaFree here took 1-375 ms while the process holds the large greedy arenas)
+    ctx_buf_ = std::make_unique<Scratch>(device_, o_base + (static_cast<size_t>(total) + 2) * 8);
+    unsigned char* d = static_cast<unsigned char*>(ctx_buf_->get());
     CK(cudaMemcpy(d, blob.data(), blob.size(), cudaMemcpyHostToDevice));
     stats.h2d += static_cast<long long>(blob.size());
     for (int k = 0; k <= kRowK; ++k) dm_.tmpl[k] = reinterpret_cast<const uint64_t*>(d + o_tmpl[k]);
@@ -467,9 +470,13 @@ const unsigned* Engine::base32() {
 }
 
 Engine::~Engine() {
+    const auto t0 = std::chrono::steady_clock::now();
     cudaSetDevice(device_);
     if (d_shard_) cudaFree(d_shard_);
     for (void* p : dev_allocs_) cudaFree(p);
+    if (std::getenv("MIGPLAN_HOST_TIMERS"))
+        std::fprintf(stderr, "[host] context free: %.1f us (%zu device buffers)\n",
+                     std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0).count(), dev_allocs_.size());
     for (auto& b : ro_blocks_) b.host ? cudaFreeHost(b.p) : cudaFree(b.p);
     for (auto& x : ro_streams_) {
         cudaEventDestroy(x.e0);

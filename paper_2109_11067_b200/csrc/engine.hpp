@@ -233,6 +233,7 @@ class Engine {
     int rollout_adv_blocks_per_sm_ = 0;  // advance kernel
     DevModel dm_{};
     std::vector<void*> dev_allocs_;
+    std::unique_ptr<Scratch> ctx_buf_;  // model tables + resident base pool (pooled, see engine.cu)
     // per-call rollout buffers (device and host-mapped) and streams, cached across calls: a
     // rollout call with cudaMalloc/cudaHostAlloc/cudaFree of its tables cost milliseconds of
     // host time (config #3 runs hundreds of small rollout calls)
