@@ -477,12 +477,6 @@ Engine::~Engine() {
     if (std::getenv("MIGPLAN_HOST_TIMERS"))
         std::fprintf(stderr, "[host] context free: %.1f us (%zu device buffers)\n",
                      std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0).count(), dev_allocs_.size());
-    for (auto& b : ro_blocks_) b.host ? cudaFreeHost(b.p) : cudaFree(b.p);
-    for (auto& x : ro_streams_) {
-        cudaEventDestroy(x.e0);
-        cudaEventDestroy(x.e1);
-        cudaStreamDestroy(x.s);
-    }
 }
 
 long long Engine::index_of(uint64_t row) const {
@@ -608,7 +602,45 @@ uint64_t philox_on_device(int device, uint64_t seed, uint64_t stream, uint64_t s
     return h;
 }
 
+// The rollout calls' cached buffers and streams, per device (process lifetime, like the slots).
+struct RoCache {
+    std::mutex mu;
+    struct Blk {
+        void* p;
+        size_t n;
+        bool host, used;
+    };
+    std::vector<Blk> blocks;
+    struct Strm {
+        cudaStream_t s;
+        cudaEvent_t e0, e1;
+        bool used;
+    };
+    std::deque<Strm> streams;  // deque: entries stay put while others are added
+};
+RoCache& ro_cache(int device) {
+    static std::mutex m;
+    static std::map<int, RoCache*> caches;  // intentionally leaked: lives until process exit
+    std::lock_guard<std::mutex> g(m);
+    auto& c = caches[device];
+    if (!c) c = new RoCache;
+    return *c;
+}
+
 void release_device_cache(int device) {
+    {  // unused rollout buffers
+        RoCache& rc = ro_cache(device);
+        std::lock_guard<std::mutex> g(rc.mu);
+        CK(cudaSetDevice(device));
+        std::vector<RoCache::Blk> keep;
+        for (auto& b : rc.blocks) {
+            if (b.used)
+                keep.push_back(b);
+            else
+                b.host ? cudaFreeHost(b.p) : cudaFree(b.p);
+        }
+        rc.blocks.swap(keep);
+    }
     std::vector<Slot*> slots;
     {
         SlotPool& pool = slot_pool(device);
@@ -1109,18 +1141,19 @@ std::vector<long long> Engine::topk(const std::vector<double>& comp, int k, cons
 // mcts_solve call, mcts.hpp:158).  A full key cache restarts the call with 4x capacity.
 void* Engine::ro_get(size_t bytes, bool host) {
     bytes = std::max<size_t>(bytes, 16);
+    RoCache& rc = ro_cache(device_);
     {
-        std::lock_guard<std::mutex> g(ro_mu_);
+        std::lock_guard<std::mutex> g(rc.mu);
         int best = -1;
-        for (int i = 0; i < static_cast<int>(ro_blocks_.size()); ++i) {  // best fit, at most 4x the request
-            const CacheBlk& b = ro_blocks_[i];
+        for (int i = 0; i < static_cast<int>(rc.blocks.size()); ++i) {  // best fit, at most 4x the request
+            const RoCache::Blk& b = rc.blocks[i];
             if (!b.used && b.host == host && b.n >= bytes && b.n <= 4 * bytes + (1 << 20) &&
-                (best < 0 || b.n < ro_blocks_[best].n))
+                (best < 0 || b.n < rc.blocks[best].n))
                 best = i;
         }
         if (best >= 0) {
-            ro_blocks_[best].used = true;
-            return ro_blocks_[best].p;
+            rc.blocks[best].used = true;
+            return rc.blocks[best].p;
         }
     }
     void* p = nullptr;
@@ -1128,36 +1161,39 @@ void* Engine::ro_get(size_t bytes, bool host) {
         CK(cudaHostAlloc(&p, bytes, cudaHostAllocMapped));
     else
         CK(cudaMalloc(&p, bytes));
-    std::lock_guard<std::mutex> g(ro_mu_);
-    ro_blocks_.push_back(CacheBlk{p, bytes, host, true});
+    std::lock_guard<std::mutex> g(rc.mu);
+    rc.blocks.push_back(RoCache::Blk{p, bytes, host, true});
     return p;
 }
 void Engine::ro_put(void* p) {
-    std::lock_guard<std::mutex> g(ro_mu_);
-    for (auto& b : ro_blocks_)
+    RoCache& rc = ro_cache(device_);
+    std::lock_guard<std::mutex> g(rc.mu);
+    for (auto& b : rc.blocks)
         if (b.p == p) b.used = false;
 }
 int Engine::ro_stream() {
+    RoCache& rc = ro_cache(device_);
     {
-        std::lock_guard<std::mutex> g(ro_mu_);
-        for (int i = 0; i < static_cast<int>(ro_streams_.size()); ++i)
-            if (!ro_streams_[i].used) {
-                ro_streams_[i].used = true;
+        std::lock_guard<std::mutex> g(rc.mu);
+        for (int i = 0; i < static_cast<int>(rc.streams.size()); ++i)
+            if (!rc.streams[i].used) {
+                rc.streams[i].used = true;
                 return i;
             }
     }
-    CacheStream x{};
+    RoCache::Strm x{};
     CK(cudaStreamCreateWithFlags(&x.s, cudaStreamNonBlocking));
     CK(cudaEventCreate(&x.e0));
     CK(cudaEventCreate(&x.e1));
     x.used = true;
-    std::lock_guard<std::mutex> g(ro_mu_);
-    ro_streams_.push_back(x);
-    return static_cast<int>(ro_streams_.size()) - 1;
+    std::lock_guard<std::mutex> g(rc.mu);
+    rc.streams.push_back(x);
+    return static_cast<int>(rc.streams.size()) - 1;
 }
 void Engine::ro_stream_put(int i) {
-    std::lock_guard<std::mutex> g(ro_mu_);
-    ro_streams_[i].used = false;
+    RoCache& rc = ro_cache(device_);
+    std::lock_guard<std::mutex> g(rc.mu);
+    rc.streams[i].used = false;
 }
 
 RolloutResult Engine::rollouts(const std::vector<double>& comp, long long n_roll, int k, int max_depth, uint64_t seed,
@@ -1236,10 +1272,11 @@ RolloutResult Engine::rollouts(const std::vector<double>& comp, long long n_roll
     cudaStream_t st;
     cudaEvent_t e0, e1;
     {
-        std::lock_guard<std::mutex> g(ro_mu_);
-        st = ro_streams_[si].s;
-        e0 = ro_streams_[si].e0;
-        e1 = ro_streams_[si].e1;
+        RoCache& rc = ro_cache(device_);
+        std::lock_guard<std::mutex> g(rc.mu);
+        st = rc.streams[si].s;
+        e0 = rc.streams[si].e0;
+        e1 = rc.streams[si].e1;
     }
     struct PutStream {
         Engine* e;

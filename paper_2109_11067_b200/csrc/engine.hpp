@@ -234,22 +234,9 @@ class Engine {
     DevModel dm_{};
     std::vector<void*> dev_allocs_;
     std::unique_ptr<Scratch> ctx_buf_;  // model tables + resident base pool (pooled, see engine.cu)
-    // per-call rollout buffers (device and host-mapped) and streams, cached across calls: a
-    // rollout call with cudaMalloc/cudaHostAlloc/cudaFree of its tables cost milliseconds of
-    // host time (config #3 runs hundreds of small rollout calls)
-    struct CacheBlk {
-        void* p;
-        size_t n;
-        bool host, used;
-    };
-    std::mutex ro_mu_;
-    std::vector<CacheBlk> ro_blocks_;
-    struct CacheStream {
-        cudaStream_t s;
-        cudaEvent_t e0, e1;
-        bool used;
-    };
-    std::deque<CacheStream> ro_streams_;  // deque: entries stay put while others are added
+    // per-call rollout buffers (device and host-mapped) and streams, cached per device across
+    // calls and contexts (engine.cu ro_cache): a rollout call that cudaMalloc'd / cudaHostAlloc'd
+    // / freed its tables cost milliseconds of host time (config #3 runs hundreds of small calls)
     void* ro_get(size_t bytes, bool host);
     void ro_put(void* p);
     int ro_stream();
