@@ -175,6 +175,9 @@ class ClockSampler:
                 "sm_max_mhz": max(s[1] for s in self.samples), "reasons": reasons, "samples": len(self.samples)}
 
 
+READ_STREAM_GBS = 7383.0  # profiles/r02a_readbw.txt: read-only 16-B loads, 512 x 592 CTAs, B200
+
+
 def measured_peak():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -185,7 +188,7 @@ def measured_peak():
 
 # committed `ncu --set full` captures (tools/ncu_summary.py) per kernel and workload
 TRAFFIC_PROFILES = {
-    ("greedy_kernel", "gen128_8.0_greedy"): "r02g_greedy_gen128_ncu.json",
+    ("greedy_kernel", "gen128_8.0_greedy"): "r02t_greedy_gen128_ncu.json",
     ("mcts_kernel", "slos24_ga10"): "r02g_mcts_ga_ncu.json",
     ("greedy_kernel", "slos24_ga10"): "r02g_greedy_slos24_ncu.json",
 }
@@ -663,7 +666,11 @@ def main():
                          "traffic": traffic, "traffic_source": traffic_src, "kernel": dom,
                          "launch_ms": 1e3 * launch_s, "bytes_per_launch": k_bytes, "bytes_per_unit": 8,
                          "unit_of_work": "packed candidate row scored (8 B: four u16 (service, pattern) codes)",
-                         "peak_kind": peak_kind},
+                         "peak_kind": peak_kind,
+                         # `peak` is the driver's copy (read+write) figure; the scan only READS, and a
+                         # read-only stream on this pool's B200s measured 7,383 GB/s
+                         # (profiles/r02a_readbw.txt, best shape) -- the tighter denominator
+                         "read_stream_peak": READ_STREAM_GBS, "frac_of_read_stream": achieved / READ_STREAM_GBS},
             "clocks": clock,
             "breakdown": {"greedy_ms": st["greedy_ms"], "topk_ms": st["topk_ms"], "mcts_ms": st["mcts_ms"],
                           "phase_ms": list(st["phase_ms"]),

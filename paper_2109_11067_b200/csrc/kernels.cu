@@ -304,11 +304,18 @@ __device__ __forceinline__ float row_ub(const float* __restrict__ Wf, uint64_t r
 }
 
 // Upper bound of one row from its two 32-bit halves (codes 0,1 in lo; 2,3 in hi): 32-bit
-// field extraction only, no 64-bit shifts on the hot path.
+// field extraction only, no 64-bit shifts on the hot path.  Codes are < 2^14 (model.cpp), so
+// x << 2 holds BOTH codes' byte offsets into Wf (4 * code < 2^16 in each half): one shift
+// serves two gathers, and each offset is one mask or one shift (3 ALU ops per half instead of
+// a shift and a mask per code).
+__device__ __forceinline__ float wf_at(const float* __restrict__ Wf, unsigned byte_off) {
+    return *reinterpret_cast<const float*>(reinterpret_cast<const char*>(Wf) + byte_off);
+}
 __device__ __forceinline__ float ub2(const float* __restrict__ Wf, unsigned lo, unsigned hi) {
-    float s = __fadd_ru(Wf[lo & 0xFFFFu], Wf[lo >> 16]);
-    s = __fadd_ru(s, Wf[hi & 0xFFFFu]);
-    return __fadd_ru(s, Wf[hi >> 16]);
+    const unsigned l = lo << 2, h = hi << 2;
+    float s = __fadd_ru(wf_at(Wf, l & 0xFFFFu), wf_at(Wf, l >> 16));
+    s = __fadd_ru(s, wf_at(Wf, h & 0xFFFFu));
+    return __fadd_ru(s, wf_at(Wf, h >> 16));
 }
 
 __device__ __forceinline__ void consider8(const DevModel& M, const double* __restrict__ W, const float* __restrict__ Wf,

@@ -231,7 +231,10 @@ Model build_model(const Rules& rules, const std::map<std::string, ModelProfile>&
     }
     m.PP = next;
     if (m.PP > kMaxPatterns) throw ArgumentError("too many instance-count patterns");
-    if ((m.n + 1) * m.PP > 65535) throw ArgumentError("service x pattern codes exceed 16 bits");
+    // codes < 2^14: the greedy scan gathers Wf at byte offset 4 * code, formed for two codes of
+    // a 32-bit row half with one shift (kernels.cu ub2); kMaxServices/kMaxPatterns keep it so
+    static_assert((kMaxServices + 1) * kMaxPatterns <= 16384);
+    if ((m.n + 1) * m.PP > 16384) throw ArgumentError("service x pattern codes exceed 14 bits");
     m.templates.assign(kRowK + 1, {});
     for (int k = 1; k <= kRowK; ++k)
         for (const auto& [li, pats] : raw_t[k]) {
