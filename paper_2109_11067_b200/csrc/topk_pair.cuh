@@ -282,6 +282,30 @@ int block_topk_pair(const DevModel& M, const unsigned* keyrank, const unsigned* 
     {  // every warp: K rounds of max-and-remove over the nwarps * 4 values (no second barrier)
         const int nv = nwarps * 4;
         unsigned v0 = lane < nv ? wtop[lane] : 0u, v1 = lane + 32 < nv ? wtop[lane + 32] : 0u;
+#ifndef MGB_TK_ROUNDS  // MGB_TK_ROUNDS: the K max-and-remove rounds (A/B)
+        // the 64 values sorted descending by a warp bitonic network (element lane in v0, lane + 32
+        // in v1; 21 compare-exchange stages instead of K dependent max-and-remove rounds); the K-th
+        // largest (with multiplicity, as the rounds give it) is then element K - 1 (K <= 32)
+#pragma unroll
+        for (int size = 2; size <= 64; size <<= 1) {
+#pragma unroll
+            for (int stride = size >> 1; stride > 0; stride >>= 1) {
+                if (stride == 32) {
+                    const unsigned hi = max(v0, v1), lo = min(v0, v1);
+                    v0 = hi, v1 = lo;
+                } else {
+                    const unsigned o0 = __shfl_xor_sync(0xffffffffu, v0, stride);
+                    const unsigned o1 = __shfl_xor_sync(0xffffffffu, v1, stride);
+                    const bool lower = (lane & stride) == 0;
+                    const bool desc0 = (lane & size) == 0, desc1 = ((lane + 32) & size) == 0;
+                    v0 = lower == desc0 ? max(v0, o0) : min(v0, o0);
+                    v1 = lower == desc1 ? max(v1, o1) : min(v1, o1);
+                }
+            }
+        }
+        const unsigned kv = __shfl_sync(0xffffffffu, k <= 32 ? v0 : v1, (k - 1) & 31);
+        tk_bits = k > 0 ? kv : 0u;
+#else
         for (int r = 0; r < k; ++r) {
             const unsigned m = __reduce_max_sync(0xffffffffu, max(v0, v1));
             tk_bits = m;
@@ -293,6 +317,7 @@ int block_topk_pair(const DevModel& M, const unsigned* keyrank, const unsigned* 
                 if (lane == __ffs(e1) - 1) v1 = 0u;
             }
         }
+#endif
     }
     mark(1);
     const double LB = __dmul_rd(static_cast<double>(__uint_as_float(tk_bits)), 1.0 - 0x1p-20);
