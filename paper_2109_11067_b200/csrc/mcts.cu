@@ -867,6 +867,13 @@ __global__ void __launch_bounds__(kMThreads, 1) mcts_kernel(const __grid_constan
                     for (int w = 0; w < NK; ++w) kw[w] = ~0ull;
                     bool have = false, inl1 = false;
                     int pn = 0, slot = 0;  // the entry: pool size, L1 slot (inl1) or global slot
+#ifndef MGB_PICK_SERIAL
+                    // picks of the next 32 draws for pool size sb_n, one per lane (lane j: draw
+                    // sb_i0 + j), computed off the walk's serial chain; sb_stop marks lanes whose draw
+                    // is rejected by pick_index or lies past the buffer: those steps take the serial path
+                    int sb_n = -1, sb_i0 = 0;
+                    unsigned sb_pick = 0u, sb_stop = 0u;
+#endif
                     const int steps0 = r_steps;
                     const long long wc0 = timers ? clock64() : 0;
                     __syncwarp();
@@ -1037,7 +1044,38 @@ __global__ void __launch_bounds__(kMThreads, 1) mcts_kernel(const __grid_constan
                         }
                         // a uniform pick from the cached pool (pick_index, util.hpp:39-47), every lane
                         unsigned pk = 0;
+#ifndef MGB_PICK_SERIAL
+                        bool picked = false;
+                        if (pn > 1) {
+                            int off = midx - sb_i0;
+                            if (pn != sb_n || off < 0 || off >= 32) {  // (re)fill the batch at midx
+                                if (midx >= 312) {
+                                    mt_twist_warp(g);
+                                    midx = 0;
+                                }
+                                const uint64_t lim = s_pick.lim[pn], fm = s_pick.fm[pn];
+                                const unsigned p32 = s_pick.p32[pn], m = static_cast<unsigned>(pn);
+                                const int j = midx + lane;
+                                const uint64_t r = j < 312 ? g.out[j] : ~0ull;
+                                const unsigned ra = fastmod32(static_cast<unsigned>(r >> 32), fm, m), rb = fastmod32(static_cast<unsigned>(r), fm, m);
+                                sb_pick = fastmod32(ra * p32 + rb, fm, m);
+                                sb_stop = __ballot_sync(0xffffffffu, j >= 312 || r >= lim);
+                                sb_n = pn;
+                                sb_i0 = midx;
+                                off = 0;
+                            }
+                            pk = __shfl_sync(0xffffffffu, sb_pick, off);
+                            if (!((sb_stop >> off) & 1u)) {
+                                ++midx;
+                                picked = true;
+                            } else {
+                                sb_n = -1;  // the serial path below twists or rejects: refill after it
+                            }
+                        }
+                        if (pn > 1 && !picked) {
+#else
                         if (pn > 1) {  // pick_index constants (mt_pick), read beside the draw
+#endif
                             const uint64_t lim = s_pick.lim[pn], fm = s_pick.fm[pn];
                             const unsigned p32 = s_pick.p32[pn];
                             uint64_t r;
