@@ -1103,11 +1103,23 @@ __global__ void __launch_bounds__(kMThreads, 1) mcts_kernel(const __grid_constan
                         if (lane == 0) a.picked[r_steps] = idx;
                         ++r_steps;
                         if (regc) {  // rollout add (mcts.hpp:139) in the owning lanes
+#ifndef MGB_WALK_ADD4
+                            // a row's members are distinct services: a lane owns at most one of them,
+                            // so select its term and add once (one FP64 add on the chain, not four)
+                            int own = -1;
+#pragma unroll
+                            for (int m = 0; m < 4; ++m) {
+                                const int code = static_cast<int>((row >> (16 * m)) & 0xFFFFull);
+                                if (csvc[code] == lane) own = code;
+                            }
+                            if (own >= 0) creg = __dadd_rn(creg, Us[own]);
+#else
 #pragma unroll
                             for (int m = 0; m < 4; ++m) {
                                 const int code = static_cast<int>((row >> (16 * m)) & 0xFFFFull);
                                 if (csvc[code] == lane) creg = __dadd_rn(creg, Us[code]);
                             }
+#endif
                         } else {
                             if (lane < 4) {  // distinct services: the adds commute
                                 const int code = static_cast<int>((row >> (16 * lane)) & 0xFFFFull);
